@@ -1,0 +1,194 @@
+/*
+ * apex_b200.h — C ABI of the B200-native APEX enumeration-and-retrieval path.
+ *
+ * The reference (`/root/reference/pkg/src/apexcsl`, pure Python/numpy) has no
+ * FFI: its operator API for this path is three Python functions.  Each entry
+ * point below replaces one of them (or one stage inside them), so a host
+ * binding (ctypes stub in INTEGRATION.md, or the Python mirror in
+ * paper_2510_24380_b200/engine.py) can stand in for:
+ *
+ *   engine.precompute_contributions(cache, surrogate)      engine.py:80-92
+ *       -> apex_load_cache        (K1: fp64 head_w @ u^T, fp32 rounding)
+ *   engine.search_topk_stream(library, table, query, index_range)
+ *                                                          engine.py:265-313
+ *   engine.search_topk_batched(library, table, query, chunk_size, index_range)
+ *                                                          engine.py:345-398
+ *       -> apex_query             (K2 pack, K3 enumerate+filter, K5 select,
+ *                                  K7 decode/materialize; identical results for
+ *                                  both reference variants)
+ *   ContributionTable construction / load_table            engine.py:35-72, 448-460
+ *       -> apex_load_table
+ *   CslLibrary index space (offsets, sizes, pair rows)     csl.py:57-112, 138-184
+ *       -> apex_load_library
+ *
+ * Multi-GPU (one process per GPU): apex_query_local produces a
+ * rank's exact local top-k as (key, g) entries in a caller-owned DEVICE buffer,
+ * the host all-gathers those buffers (NCCL), and apex_merge_finalize selects,
+ * orders and materializes the global result from the gathered entries.
+ *
+ * Conventions (SURVEY.md §8b "Design rules for that ABI"):
+ *   - every function returns 0 on success, nonzero (an APEX_E* code) on error;
+ *     apex_last_error() returns a thread-local message.  No C++ exception
+ *     crosses the ABI.
+ *   - host buffers are borrowed for the duration of the call.
+ *   - device state is owned by the ctx; the table is immutable after load.
+ *   - a ctx is not re-entrant; distinct ctxs may be used concurrently.
+ *   - no CPU fallback: if the device is missing or a kernel fails, the call
+ *     fails with APEX_ECUDA.
+ */
+#ifndef APEX_B200_H
+#define APEX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APEX_MAX_RGROUPS 6 /* R-groups per reaction supported by the kernels */
+
+enum {
+  APEX_OK = 0,
+  APEX_EINVAL = 1,    /* bad argument (maps to EngineError) */
+  APEX_ERANGE = 2,    /* index range invalid (engine.py:281-282) */
+  APEX_ETASK = 3,     /* unknown task (engine.py:58-62) */
+  APEX_ECUDA = 4,     /* CUDA failure / no device */
+  APEX_ESTATE = 5,    /* call order: library/table not loaded */
+  APEX_ENOMEM = 6,    /* device allocation failed */
+  APEX_ELIMIT = 7     /* request exceeds a compiled limit (k, R-groups, tests) */
+};
+
+typedef struct apex_ctx apex_ctx;
+
+/* One reaction of the library, positional (reaction(id) is positional,
+ * csl.py:90-91).  R-groups in declaration order; digit order of the codec
+ * (csl.py:151-163): first R-group most significant. */
+typedef struct {
+  int32_t n_rgroups;                       /* c >= 2 (csl.py:122-123) */
+  int32_t _pad;
+  int64_t sizes[APEX_MAX_RGROUPS];         /* synthons per R-group */
+  int64_t pair_offset[APEX_MAX_RGROUPS];   /* table row of digit 0: rg_offsets[_rg_pos[rg]] */
+  uint64_t g_offset;                       /* reaction_offset(t) (csl.py:96-97) */
+} apex_reaction;
+
+/* One constraint: task index into the table's task list, closed interval
+ * [lower, upper] with +-inf meaning unbounded (engine.py:104-112). */
+typedef struct {
+  int32_t task;
+  int32_t _pad;
+  double lower;
+  double upper;
+} apex_constraint;
+
+/* One query (engine.py:115-131) over the global index range [start, end). */
+typedef struct {
+  int32_t objective_task;
+  int32_t maximize;                /* 1 = "maximize", 0 = "minimize" */
+  int32_t n_constraints;
+  int32_t _pad;
+  const apex_constraint* constraints;
+  int64_t k;
+  uint64_t start;
+  uint64_t end;
+} apex_query_spec;
+
+/* Per-stage device time and counters of the last apex_query call. */
+typedef struct {
+  double pack_ms;          /* K2 pack of the signed test columns */
+  double seed_ms;          /* sampled admission threshold (exact, from real products) */
+  double scan_ms;          /* K3 enumeration chunks incl. threshold refreshes */
+  double select_ms;        /* compaction + K5 exact select */
+  double finalize_ms;      /* K6 ordering + K7 materialization */
+  double d2h_ms;           /* result copy to host */
+  double total_ms;         /* device time of the whole call */
+  double scan_kernel_ms;   /* K3 launches only (sum over chunks) */
+  int64_t candidates;      /* entries appended by the enumeration kernel */
+  int64_t scan_launches;   /* enumeration launches (chunks, incl. retries) */
+  int64_t kernel_launches; /* all kernels launched by the call */
+  int64_t retries;         /* chunk re-runs after candidate-buffer overflow */
+} apex_stats;
+
+/* Caller-allocated host output for one query; arrays sized for k entries
+ * (constraint_values: k * n_constraints, digits: k * APEX_MAX_RGROUPS). */
+typedef struct {
+  uint64_t* global_index;
+  double* objective;          /* value in the user's direction (engine.py:254) */
+  double* constraint_values;  /* apex_score order (engine.py:95-101) */
+  int32_t* reaction;          /* positional reaction index */
+  int32_t* digits;            /* per R-group digit, APEX_MAX_RGROUPS stride */
+  int64_t n;                  /* out: retained entries (best-first) */
+  int64_t discarded;          /* out: min(k, end-start) - retained */
+  uint64_t scanned;           /* out: end - start */
+} apex_result;
+
+/* Entry exchanged between ranks: order-preserving key of the signed
+ * objective (larger = better, +-0 canonicalized) and the global index. */
+typedef struct {
+  uint64_t key;
+  uint64_t g;
+} apex_entry;
+
+const char* apex_last_error(void);
+const char* apex_version(void);
+
+/* device: CUDA ordinal; stream: a cudaStream_t (NULL = a ctx-owned stream). */
+int apex_ctx_create(int32_t device, void* stream, apex_ctx** out);
+void apex_ctx_destroy(apex_ctx* ctx);
+int apex_set_stream(apex_ctx* ctx, void* stream);
+
+/* Library index space.  n_pairs = table rows expected. */
+int apex_load_library(apex_ctx* ctx, const apex_reaction* reactions, int32_t n_reactions,
+                      int64_t n_pairs);
+
+/* Contribution table: values float32 [n_tasks][n_pairs] (engine.py:37),
+ * biases float64 [n_tasks] (engine.py:38).  Non-finite values are rejected. */
+int apex_load_table(apex_ctx* ctx, const float* values, const double* biases, int32_t n_tasks,
+                    int64_t n_pairs);
+
+/* K1 synthon precompute (engine.py:80-92): values = fl32(head_w @ u^T) with
+ * fp64 products and accumulation, on device; the table becomes resident.
+ * u: float64 [n_pairs][d]; head_w: float64 [n_tasks][d]; head_b: float64
+ * [n_tasks].  values_out (optional, may be NULL): host copy of the table. */
+int apex_load_cache(apex_ctx* ctx, const double* u, int64_t n_pairs, int32_t d,
+                    const double* head_w, const double* head_b, int32_t n_tasks,
+                    float* values_out);
+
+/* Same as apex_load_cache but u / head_w / values_out are DEVICE pointers
+ * (no host copies); used to time K1 alone. */
+int apex_precompute_device(apex_ctx* ctx, const double* u_dev, int64_t n_pairs, int32_t d,
+                           const double* head_w_dev, int32_t n_tasks, float* values_dev);
+
+/* Run n_queries queries (batched: one enumeration schedule, all queries per
+ * launch) and materialize each result into results[i] (host buffers). */
+int apex_query(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,
+               apex_result* results, apex_stats* stats);
+
+/* Multi-GPU local step: exact local top-min(k, feasible) of each query over its
+ * [start, end), written UNSORTED into out_dev (device, capacity k entries per
+ * query, query q at out_dev + q*k); counts_host[q] = entries written. */
+int apex_query_local(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,
+                     apex_entry* out_dev, int64_t* counts_host, apex_stats* stats);
+
+/* Multi-GPU final step: entries_dev holds n_entries gathered local entries of
+ * ONE query (device; padding entries have g == UINT64_MAX and are ignored).
+ * Selects the global top-k, orders best-first, materializes into *result.
+ * total_scanned = global range size used for `discarded`. */
+int apex_merge_finalize(apex_ctx* ctx, const apex_query_spec* query, const apex_entry* entries_dev,
+                        int64_t n_entries, uint64_t total_scanned, apex_result* result,
+                        apex_stats* stats);
+
+/* Tuning / introspection. */
+int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);
+
+/* Test hook: exact fp32 thresholds of the enumeration kernel for arrays of
+ * (p, b, beta) (host buffers): up[i] = max finite fp32 x with
+ * ((p + x) + b) <= beta (fp64), +inf if all, NaN if none; lo[i] = min x with
+ * ((p + x) + b) >= beta, -inf if all, NaN if none. */
+int apex_debug_thresholds(apex_ctx* ctx, const double* p, const double* b, const double* beta, int64_t n,
+                          float* up, float* lo);
+int apex_get_device_info(apex_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APEX_B200_H */

@@ -1,0 +1,324 @@
+"""ctypes binding of the C ABI in ``include/apex_b200.h`` (libapexb200.so).
+
+This is the only way the Python mirror reaches the GPU: there is no CPU
+fallback.  If the shared library is missing, or no sm_100 device is present,
+every entry point raises ``NativeError`` (mapped to ``EngineError`` by
+``engine.py``) instead of silently computing on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+MAX_RGROUPS = 6
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("APEX_B200_LIB", _PKG / "libapexb200.so"))
+
+# status codes (apex_b200.h)
+APEX_OK, APEX_EINVAL, APEX_ERANGE, APEX_ETASK, APEX_ECUDA, APEX_ESTATE, APEX_ENOMEM, APEX_ELIMIT = range(8)
+
+EXPORTED = (
+    "apex_last_error", "apex_version", "apex_ctx_create", "apex_ctx_destroy", "apex_set_stream",
+    "apex_load_library", "apex_load_table", "apex_load_cache", "apex_precompute_device", "apex_query",
+    "apex_query_local", "apex_merge_finalize", "apex_set_option", "apex_get_device_info",
+    "apex_debug_thresholds",
+)
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class Reaction(C.Structure):
+    _fields_ = [
+        ("n_rgroups", C.c_int32),
+        ("_pad", C.c_int32),
+        ("sizes", C.c_int64 * MAX_RGROUPS),
+        ("pair_offset", C.c_int64 * MAX_RGROUPS),
+        ("g_offset", C.c_uint64),
+    ]
+
+
+class ConstraintC(C.Structure):
+    _fields_ = [("task", C.c_int32), ("_pad", C.c_int32), ("lower", C.c_double), ("upper", C.c_double)]
+
+
+class QuerySpecC(C.Structure):
+    _fields_ = [
+        ("objective_task", C.c_int32),
+        ("maximize", C.c_int32),
+        ("n_constraints", C.c_int32),
+        ("_pad", C.c_int32),
+        ("constraints", C.POINTER(ConstraintC)),
+        ("k", C.c_int64),
+        ("start", C.c_uint64),
+        ("end", C.c_uint64),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("pack_ms", C.c_double),
+        ("seed_ms", C.c_double),
+        ("scan_ms", C.c_double),
+        ("select_ms", C.c_double),
+        ("finalize_ms", C.c_double),
+        ("d2h_ms", C.c_double),
+        ("total_ms", C.c_double),
+        ("scan_kernel_ms", C.c_double),
+        ("candidates", C.c_int64),
+        ("scan_launches", C.c_int64),
+        ("kernel_launches", C.c_int64),
+        ("retries", C.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class ResultC(C.Structure):
+    _fields_ = [
+        ("global_index", C.POINTER(C.c_uint64)),
+        ("objective", C.POINTER(C.c_double)),
+        ("constraint_values", C.POINTER(C.c_double)),
+        ("reaction", C.POINTER(C.c_int32)),
+        ("digits", C.POINTER(C.c_int32)),
+        ("n", C.c_int64),
+        ("discarded", C.c_int64),
+        ("scanned", C.c_uint64),
+    ]
+
+
+class EntryC(C.Structure):
+    _fields_ = [("key", C.c_uint64), ("g", C.c_uint64)]
+
+
+_lib = None
+
+
+def load_library(path: Path | None = None):
+    """Load libapexb200.so (once).  Raises NativeError if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise NativeError(APEX_ESTATE, f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(p))
+    vp = C.c_void_p
+    sig = {
+        "apex_last_error": ([], C.c_char_p),
+        "apex_version": ([], C.c_char_p),
+        "apex_ctx_create": ([C.c_int32, vp, C.POINTER(vp)], C.c_int),
+        "apex_ctx_destroy": ([vp], None),
+        "apex_set_stream": ([vp, vp], C.c_int),
+        "apex_load_library": ([vp, C.POINTER(Reaction), C.c_int32, C.c_int64], C.c_int),
+        "apex_load_table": ([vp, vp, vp, C.c_int32, C.c_int64], C.c_int),
+        "apex_load_cache": ([vp, vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, vp], C.c_int),
+        "apex_precompute_device": ([vp, vp, C.c_int64, C.c_int32, vp, C.c_int32, vp], C.c_int),
+        "apex_query": ([vp, C.POINTER(QuerySpecC), C.c_int32, C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
+        "apex_query_local": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.POINTER(C.c_int64), C.POINTER(Stats)],
+                             C.c_int),
+        "apex_merge_finalize": ([vp, C.POINTER(QuerySpecC), vp, C.c_int64, C.c_uint64, C.POINTER(ResultC),
+                                 C.POINTER(Stats)], C.c_int),
+        "apex_set_option": ([vp, C.c_char_p, C.c_int64], C.c_int),
+        "apex_get_device_info": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
+        "apex_debug_thresholds": ([vp, vp, vp, vp, C.c_int64, vp, vp], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != APEX_OK:
+        msg = load_library().apex_last_error().decode(errors="replace")
+        raise NativeError(rc, msg)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class DeviceContext:
+    """Owns one apex_ctx (one GPU): resident library descriptors and table."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.lib = load_library()
+        self._ctx = C.c_void_p()
+        _check(self.lib.apex_ctx_create(int(device), C.c_void_p(stream) if stream else None, C.byref(self._ctx)))
+        self.device = device
+
+    def close(self) -> None:
+        if self._ctx:
+            self.lib.apex_ctx_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: int | None) -> None:
+        _check(self.lib.apex_set_stream(self._ctx, C.c_void_p(stream) if stream else None))
+
+    def set_option(self, name: str, value: int) -> None:
+        _check(self.lib.apex_set_option(self._ctx, name.encode(), int(value)))
+
+    def device_info(self) -> tuple[int, int, int]:
+        a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(self.lib.apex_get_device_info(self._ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    # -- library / table ---------------------------------------------------
+    def load_library(self, sizes: list[list[int]], pair_offsets: list[list[int]], g_offsets: list[int],
+                     n_pairs: int) -> None:
+        n = len(sizes)
+        arr = (Reaction * max(n, 1))()
+        for t in range(n):
+            c = len(sizes[t])
+            if c > MAX_RGROUPS:
+                raise NativeError(APEX_ELIMIT, f"reaction {t} has {c} R-groups (max {MAX_RGROUPS})")
+            arr[t].n_rgroups = c
+            for j in range(c):
+                arr[t].sizes[j] = int(sizes[t][j])
+                arr[t].pair_offset[j] = int(pair_offsets[t][j])
+            arr[t].g_offset = int(g_offsets[t])
+        _check(self.lib.apex_load_library(self._ctx, arr, n, int(n_pairs)))
+
+    def load_table(self, values: np.ndarray, biases: np.ndarray) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        b = np.ascontiguousarray(biases, dtype=np.float64)
+        _check(self.lib.apex_load_table(self._ctx, _ptr(v), _ptr(b), v.shape[0], v.shape[1]))
+
+    def load_cache(self, u: np.ndarray, head_w: np.ndarray, head_b: np.ndarray, want_values: bool = True):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        w = np.ascontiguousarray(head_w, dtype=np.float64)
+        b = np.ascontiguousarray(head_b, dtype=np.float64)
+        out = np.empty((w.shape[0], u.shape[0]), dtype=np.float32) if want_values else None
+        _check(self.lib.apex_load_cache(self._ctx, _ptr(u), u.shape[0], u.shape[1], _ptr(w), _ptr(b), w.shape[0],
+                                        _ptr(out) if out is not None else None))
+        return out
+
+    def precompute_device(self, u_ptr: int, n_pairs: int, d: int, w_ptr: int, n_tasks: int, out_ptr: int) -> None:
+        _check(self.lib.apex_precompute_device(self._ctx, C.c_void_p(u_ptr), n_pairs, d, C.c_void_p(w_ptr), n_tasks,
+                                               C.c_void_p(out_ptr)))
+
+    # -- queries -------------------------------------------------------------
+    @staticmethod
+    def _specs(queries):
+        """queries: list of dicts {obj, maximize, cons: [(task, lo, hi)], k, start, end}."""
+        specs = (QuerySpecC * len(queries))()
+        keep = []
+        for i, q in enumerate(queries):
+            cons = q.get("cons", [])
+            carr = (ConstraintC * max(len(cons), 1))()
+            for j, (t, lo, hi) in enumerate(cons):
+                carr[j].task = int(t)
+                carr[j].lower = float(lo)
+                carr[j].upper = float(hi)
+            keep.append(carr)
+            specs[i].objective_task = int(q["obj"])
+            specs[i].maximize = 1 if q["maximize"] else 0
+            specs[i].n_constraints = len(cons)
+            specs[i].constraints = C.cast(carr, C.POINTER(ConstraintC))
+            specs[i].k = int(q["k"])
+            specs[i].start = int(q["start"])
+            specs[i].end = int(q["end"])
+        return specs, keep
+
+    def query(self, queries: list[dict]) -> tuple[list[dict], dict]:
+        """Run a batch; returns per-query numpy result arrays and the stats."""
+        specs, keep = self._specs(queries)
+        results = (ResultC * len(queries))()
+        bufs = []
+        for i, q in enumerate(queries):
+            k = max(int(q["k"]), 1)
+            m = len(q.get("cons", []))
+            b = {
+                "g": np.empty(k, dtype=np.uint64),
+                "objective": np.empty(k, dtype=np.float64),
+                "constraint_values": np.empty((k, m), dtype=np.float64),
+                "reaction": np.empty(k, dtype=np.int32),
+                "digits": np.empty((k, MAX_RGROUPS), dtype=np.int32),
+            }
+            bufs.append(b)
+            results[i].global_index = b["g"].ctypes.data_as(C.POINTER(C.c_uint64))
+            results[i].objective = b["objective"].ctypes.data_as(C.POINTER(C.c_double))
+            results[i].constraint_values = b["constraint_values"].ctypes.data_as(C.POINTER(C.c_double))
+            results[i].reaction = b["reaction"].ctypes.data_as(C.POINTER(C.c_int32))
+            results[i].digits = b["digits"].ctypes.data_as(C.POINTER(C.c_int32))
+        st = Stats()
+        _check(self.lib.apex_query(self._ctx, specs, len(queries), results, C.byref(st)))
+        out = []
+        for i, b in enumerate(bufs):
+            n = results[i].n
+            out.append({
+                "g": b["g"][:n],
+                "objective": b["objective"][:n],
+                "constraint_values": b["constraint_values"][:n],
+                "reaction": b["reaction"][:n],
+                "digits": b["digits"][:n],
+                "n": n,
+                "discarded": results[i].discarded,
+                "scanned": results[i].scanned,
+            })
+        del keep
+        return out, st.as_dict()
+
+    def query_local(self, queries: list[dict], out_dev_ptr: int) -> tuple[list[int], dict]:
+        specs, keep = self._specs(queries)
+        counts = (C.c_int64 * len(queries))()
+        st = Stats()
+        _check(self.lib.apex_query_local(self._ctx, specs, len(queries), C.c_void_p(out_dev_ptr), counts, C.byref(st)))
+        del keep
+        return [counts[i] for i in range(len(queries))], st.as_dict()
+
+    def merge_finalize(self, query: dict, entries_dev_ptr: int, n_entries: int, total_scanned: int):
+        specs, keep = self._specs([query])
+        k = max(int(query["k"]), 1)
+        m = len(query.get("cons", []))
+        b = {
+            "g": np.empty(k, dtype=np.uint64),
+            "objective": np.empty(k, dtype=np.float64),
+            "constraint_values": np.empty((k, m), dtype=np.float64),
+            "reaction": np.empty(k, dtype=np.int32),
+            "digits": np.empty((k, MAX_RGROUPS), dtype=np.int32),
+        }
+        res = ResultC()
+        res.global_index = b["g"].ctypes.data_as(C.POINTER(C.c_uint64))
+        res.objective = b["objective"].ctypes.data_as(C.POINTER(C.c_double))
+        res.constraint_values = b["constraint_values"].ctypes.data_as(C.POINTER(C.c_double))
+        res.reaction = b["reaction"].ctypes.data_as(C.POINTER(C.c_int32))
+        res.digits = b["digits"].ctypes.data_as(C.POINTER(C.c_int32))
+        st = Stats()
+        _check(self.lib.apex_merge_finalize(self._ctx, specs, C.c_void_p(entries_dev_ptr), int(n_entries),
+                                            int(total_scanned), C.byref(res), C.byref(st)))
+        n = res.n
+        del keep
+        return {
+            "g": b["g"][:n], "objective": b["objective"][:n], "constraint_values": b["constraint_values"][:n],
+            "reaction": b["reaction"][:n], "digits": b["digits"][:n], "n": n, "discarded": res.discarded,
+            "scanned": res.scanned,
+        }, st.as_dict()
+
+    def debug_thresholds(self, p: np.ndarray, b: np.ndarray, beta: np.ndarray):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        beta = np.ascontiguousarray(beta, dtype=np.float64)
+        up = np.empty(len(p), dtype=np.float32)
+        lo = np.empty(len(p), dtype=np.float32)
+        _check(self.lib.apex_debug_thresholds(self._ctx, _ptr(p), _ptr(b), _ptr(beta), len(p), _ptr(up), _ptr(lo)))
+        return up, lo

@@ -1,0 +1,1101 @@
+// capi.cu — host runtime and C ABI (include/apex_b200.h) of the B200-native
+// APEX enumeration-and-retrieval path.
+//
+// Query protocol (one schedule for a batch of queries over the same range):
+//   init_ctl -> pack (K2) -> sample + tau(seed) -> [scan chunk (K3) -> tau]*
+//   -> tau(bound) -> compact -> select (K5, cooperative) -> rank/scatter (K6)
+//   -> materialize (K7) -> D2H.
+// Exactness argument: every appended candidate is an exactly
+// feasible product with s >= tau (exact fp32 thresholds on the last R-group's
+// contribution, K3); every tau / bound is the k-th best bin edge of a set of
+// distinct real feasible products, hence <= the true k-th best key; so the
+// true top-k is always inside the candidate set, and K5 selects it exactly by
+// (key desc, g asc) == the reference's (s desc, g asc) over feasible rows.
+// A candidate-buffer overflow is detected (count > cap) and the query is re-run
+// with the final (valid) bound as its starting threshold.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace apexb200;
+
+namespace {
+
+thread_local std::string t_err;
+
+int set_err(int code, const std::string& m) {
+  t_err = m;
+  return code;
+}
+
+#define APEX_CU(x)                                                                                \
+  do {                                                                                            \
+    cudaError_t e__ = (x);                                                                        \
+    if (e__ != cudaSuccess)                                                                       \
+      return set_err(APEX_ECUDA, std::string(#x) + " failed: " + cudaGetErrorString(e__));       \
+  } while (0)
+
+#define APEX_TRY(x)           \
+  do {                        \
+    int r__ = (x);            \
+    if (r__ != APEX_OK) return r__; \
+  } while (0)
+
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes) return APEX_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(b, 256));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(APEX_ENOMEM, "cudaMalloc(" + std::to_string(b) + ") failed: " + cudaGetErrorString(e));
+    }
+    bytes = std::max<size_t>(b, 256);
+    return APEX_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct HBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes) return APEX_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(b, 256));
+    if (e != cudaSuccess) return set_err(APEX_ENOMEM, std::string("cudaMallocHost failed: ") + cudaGetErrorString(e));
+    bytes = std::max<size_t>(b, 256);
+    return APEX_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Slot {
+  DBuf packed, buf, comp, sel, sorted, rank, hist, seed_hist, ctl, out;
+  void release() {
+    for (DBuf* b : {&packed, &buf, &comp, &sel, &sorted, &rank, &hist, &seed_hist, &ctl, &out}) b->release();
+  }
+};
+
+struct Plan {
+  uint64_t start = 0, end = 0;
+  int rows = 0;
+  int64_t cols = 0;
+  std::vector<Tile> tiles;        // permuted
+  std::vector<uint64_t> prefix;   // products in tiles[0, i)
+  DBuf d_tiles;
+  int64_t pair_lo = 0, pair_hi = 0;  // last-R-group pair rows touched
+  uint64_t stamp = 0;
+};
+
+size_t out_bytes(int64_t k, int m) { return (size_t)k * (8 + 8 + 8 * (size_t)m + 4 + 4 * kMaxRg); }
+
+}  // namespace
+
+struct apex_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  // library
+  std::vector<DevReaction> rx;
+  std::vector<unsigned long long> goff;  // n_rx + 1
+  uint64_t total = 0;
+  int64_t lib_pairs = 0;
+  DBuf d_rx, d_goff;
+  bool lib_loaded = false;
+  // table
+  DBuf d_values, d_biases;
+  std::vector<double> biases;
+  int n_tasks = 0;
+  int64_t n_pairs = 0;
+  bool table_loaded = false;
+  // query workspaces
+  std::vector<Slot> slots;
+  DBuf d_queries, d_tau0;
+  HBuf h_queries, h_ctl, h_out, h_tau0;
+  std::vector<Plan> plans;
+  uint64_t stamp = 0;
+  cudaEvent_t ev[8] = {};
+  // options
+  int64_t opt_cap = 1 << 22;        // candidate buffer entries per query (minimum)
+  int64_t opt_cb = 64;              // columns per smem block
+  int64_t opt_rl = 0;               // rows per lane (0 = auto)
+  int64_t opt_samples = 0;          // seed samples (0 = auto)
+  int64_t opt_chunk_div = 16;       // first scan chunk = 1/opt_chunk_div of the range
+  int64_t opt_chunk_min = 1 << 26;  // ranges at least this large are scanned in two chunks
+  int64_t opt_tile_products = 0;    // target products per tile (0 = auto)
+  int64_t opt_select_ctas = 16;     // CTAs per query in the select kernel
+};
+
+namespace {
+
+int check_ctx(apex_ctx* c, bool need_table) {
+  if (!c) return set_err(APEX_EINVAL, "null context");
+  if (need_table && !(c->lib_loaded && c->table_loaded))
+    return set_err(APEX_ESTATE, "library and table must be loaded before querying");
+  if (need_table && c->n_pairs != c->lib_pairs)
+    return set_err(APEX_EINVAL, "table rows (" + std::to_string(c->n_pairs) + ") do not match library pair rows (" +
+                                    std::to_string(c->lib_pairs) + ")");
+  APEX_CU(cudaSetDevice(c->device));
+  return APEX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Enumeration tiles for [start, end): per reaction, rows = prefix assignments
+// (mixed radix of the first c-1 digits), columns = last digit; partial rows at
+// the range ends (engine.py:182-189 clipping) become single-row tiles.  Tiles
+// are shuffled with a fixed seed so any prefix of the list is a representative
+// sample of the range (used for the first chunk's threshold).
+int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) {
+  for (auto& p : c->plans) {
+    if (p.start == start && p.end == end && p.rows == rows) {
+      p.stamp = ++c->stamp;
+      out = &p;
+      return APEX_OK;
+    }
+  }
+  Plan P;
+  P.start = start;
+  P.end = end;
+  P.rows = rows;
+  const uint64_t span = end - start;
+  int64_t warp_slots = (int64_t)c->sm_count * 16 * 2;
+  int64_t target = c->opt_tile_products > 0 ? c->opt_tile_products : (int64_t)(span / (uint64_t)(32 * warp_slots));
+  int64_t cols = std::max<int64_t>(64, std::min<int64_t>(2048, target / rows));
+  cols = (cols + 63) / 64 * 64;
+  P.cols = cols;
+  P.pair_lo = INT64_MAX;
+  P.pair_hi = 0;
+  const int n_rx = (int)c->rx.size();
+  for (int t = 0; t < n_rx; ++t) {
+    const uint64_t off = c->goff[t], size = c->goff[t + 1] - c->goff[t];
+    if (off + size <= start || off >= end) continue;
+    const DevReaction& R = c->rx[t];
+    const uint64_t n_last = (uint64_t)R.size[R.c - 1];
+    const uint64_t lo = std::max(start, off) - off, hi = std::min(end, off + size) - off;
+    P.pair_lo = std::min<int64_t>(P.pair_lo, R.pair_off[R.c - 1]);
+    P.pair_hi = std::max<int64_t>(P.pair_hi, R.pair_off[R.c - 1] + (int64_t)n_last);
+    auto emit = [&](uint64_t row0, uint64_t nrows, uint64_t c0, uint64_t c1) {
+      for (uint64_t cc = c0; cc < c1; cc += (uint64_t)cols) {
+        Tile T;
+        T.row0 = row0;
+        T.rx = (uint32_t)t;
+        T.nrows = (uint32_t)nrows;
+        T.col0 = (uint32_t)cc;
+        T.ncols = (uint32_t)std::min<uint64_t>((uint64_t)cols, c1 - cc);
+        P.tiles.push_back(T);
+      }
+    };
+    const uint64_t r_lo = lo / n_last, c_lo = lo % n_last, r_hi = hi / n_last, c_hi = hi % n_last;
+    if (r_lo == r_hi) {
+      emit(r_lo, 1, c_lo, c_hi);
+      continue;
+    }
+    uint64_t first_full = r_lo;
+    if (c_lo) {
+      emit(r_lo, 1, c_lo, n_last);
+      first_full = r_lo + 1;
+    }
+    for (uint64_t r = first_full; r < r_hi; r += (uint64_t)rows) emit(r, std::min<uint64_t>(rows, r_hi - r), 0, n_last);
+    if (c_hi) emit(r_hi, 1, 0, c_hi);
+  }
+  if (P.tiles.size() > 0xffffffffull) return set_err(APEX_ELIMIT, "too many enumeration tiles");
+  std::mt19937_64 rng(0x5eed5eedull ^ start ^ (end << 1));
+  std::shuffle(P.tiles.begin(), P.tiles.end(), rng);
+  P.prefix.resize(P.tiles.size() + 1);
+  P.prefix[0] = 0;
+  for (size_t i = 0; i < P.tiles.size(); ++i)
+    P.prefix[i + 1] = P.prefix[i] + (uint64_t)P.tiles[i].nrows * P.tiles[i].ncols;
+  if (P.prefix.back() != span) return set_err(APEX_EINVAL, "internal: tile plan does not cover the range");
+  if (P.pair_lo == INT64_MAX) P.pair_lo = P.pair_hi = 0;
+  APEX_TRY(P.d_tiles.ensure(std::max<size_t>(1, P.tiles.size()) * sizeof(Tile)));
+  if (!P.tiles.empty())
+    APEX_CU(cudaMemcpy(P.d_tiles.p, P.tiles.data(), P.tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+  // keep a small cache
+  if (c->plans.size() >= 8) {
+    auto it = std::min_element(c->plans.begin(), c->plans.end(),
+                               [](const Plan& a, const Plan& b) { return a.stamp < b.stamp; });
+    it->d_tiles.release();
+    c->plans.erase(it);
+  }
+  P.stamp = ++c->stamp;
+  c->plans.push_back(std::move(P));
+  out = &c->plans.back();
+  return APEX_OK;
+}
+
+// Tests of a query: test 0 = objective admission, then for every
+// task the tightest finite upper bound and the tightest finite lower bound
+// (x >= each lower <=> x >= max lower; monotone, so merging is exact).
+struct QTests {
+  int nt = 0;
+  int task[kMaxTests];
+  int lower[kMaxTests];
+  double beta[kMaxTests];
+};
+
+int make_tests(const apex_ctx* c, const apex_query_spec& q, QTests& T) {
+  T.nt = 1;
+  T.task[0] = q.objective_task;
+  T.lower[0] = q.maximize ? 1 : 0;
+  T.beta[0] = 0.0;
+  std::vector<double> lo(c->n_tasks, -INFINITY), up(c->n_tasks, INFINITY);
+  for (int i = 0; i < q.n_constraints; ++i) {
+    const apex_constraint& k = q.constraints[i];
+    if (k.task < 0 || k.task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index " + std::to_string(k.task));
+    if (!(k.lower < k.upper)) return set_err(APEX_EINVAL, "constraint bounds must satisfy lower < upper");
+    lo[k.task] = std::max(lo[k.task], k.lower);
+    up[k.task] = std::min(up[k.task], k.upper);
+  }
+  for (int t = 0; t < c->n_tasks; ++t) {
+    if (std::isfinite(up[t])) {
+      if (T.nt >= kMaxTests) return set_err(APEX_ELIMIT, "query has more than 23 finite bounds");
+      T.task[T.nt] = t; T.lower[T.nt] = 0; T.beta[T.nt] = up[t]; ++T.nt;
+    }
+    if (std::isfinite(lo[t])) {
+      if (T.nt >= kMaxTests) return set_err(APEX_ELIMIT, "query has more than 23 finite bounds");
+      T.task[T.nt] = t; T.lower[T.nt] = 1; T.beta[T.nt] = lo[t]; ++T.nt;
+    }
+  }
+  return APEX_OK;
+}
+
+int kernel_nt(int nt) {
+  static const int sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24};
+  for (int s : sizes)
+    if (nt <= s) return s;
+  return -1;
+}
+
+using ScanFn = void (*)(const ScanLaunch);
+
+template <int NT, int RL>
+ScanFn scan_ptr() { return scan_kernel<NT, RL>; }
+
+ScanFn pick_scan(int nt, int rl) {
+#define CASE(N)                                         \
+  case N:                                               \
+    return rl == 1 ? scan_ptr<N, 1>() : scan_ptr<N, 2>();
+  switch (nt) {
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(14)
+    CASE(16) CASE(20) CASE(24)
+    default: return nullptr;
+  }
+#undef CASE
+}
+
+size_t scan_smem(int nt, int cb) {
+  const int ntp = (nt + 3) / 4 * 4;
+  return (size_t)kScanWarps * 2 * cb * ntp * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
+}
+
+int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
+  APEX_CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, (const void*)fn, kScanWarps * 32, smem));
+  if (*occ < 1) return set_err(APEX_ELIMIT, "enumeration kernel does not fit on an SM");
+  return APEX_OK;
+}
+
+struct RunStats {
+  int64_t launches = 0, scans = 0, retries = 0;
+  float ms[8] = {};
+  float scan_kernel_ms = 0;
+};
+
+// Launch the whole device pipeline for nq queries sharing one range; results
+// stay on device (sel / sorted / out of each slot).  finalize: order +
+// materialize (single-GPU path); otherwise stop after select (local path).
+int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, RunStats& st) {
+  const uint64_t start = qs[0].start, end = qs[0].end, span = end - start;
+  std::vector<QTests> tests(nq);
+  int nt_max = 1;
+  int64_t k_max = 0;
+  for (int i = 0; i < nq; ++i) {
+    APEX_TRY(make_tests(c, qs[i], tests[i]));
+    nt_max = std::max(nt_max, tests[i].nt);
+    k_max = std::max<int64_t>(k_max, qs[i].k);
+    if (qs[i].n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+  }
+  const int NT = kernel_nt(nt_max);
+  if (NT < 0) return set_err(APEX_ELIMIT, "too many tests");
+  const int ntp = (NT + 3) / 4 * 4;
+  int rl = (int)c->opt_rl;
+  if (rl != 1 && rl != 2) rl = NT <= 8 ? 2 : 1;
+  const int rows = 32 * rl;
+  Plan* plan = nullptr;
+  APEX_TRY(build_plan(c, start, end, rows, plan));
+
+  if ((int)c->slots.size() < nq) c->slots.resize(nq);
+  // workspaces
+  for (int i = 0; i < nq; ++i) {
+    Slot& S = c->slots[i];
+    const int64_t k = qs[i].k;
+    const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
+    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp * sizeof(float)));
+    APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
+    APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
+    APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
+    APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
+    APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
+    APEX_TRY(S.hist.ensure(kHistBins * sizeof(unsigned)));
+    APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
+    APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
+    APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
+  }
+  APEX_TRY(c->d_queries.ensure(nq * sizeof(ScanQuery)));
+  APEX_TRY(c->h_queries.ensure(nq * sizeof(ScanQuery)));
+  ScanQuery* hq = c->h_queries.as<ScanQuery>();
+  for (int i = 0; i < nq; ++i) {
+    Slot& S = c->slots[i];
+    const apex_query_spec& q = qs[i];
+    ScanQuery& Q = hq[i];
+    std::memset(&Q, 0, sizeof(Q));
+    Q.packed = S.packed.as<float>();
+    Q.buf = S.buf.as<Entry>();
+    Q.comp = S.comp.as<Entry>();
+    Q.sel = S.sel.as<Entry>();
+    Q.sorted = S.sorted.as<Entry>();
+    Q.rank = S.rank.as<unsigned>();
+    Q.hist = S.hist.as<unsigned>();
+    Q.seed_hist = S.seed_hist.as<unsigned>();
+    Q.ctl = S.ctl.as<QCtl>();
+    Q.cap = S.buf.bytes / sizeof(Entry);
+    Q.k = q.k;
+    Q.nt = tests[i].nt;
+    Q.ntp = ntp;
+    Q.maximize = q.maximize ? 1 : 0;
+    Q.obj_task = q.objective_task;
+    Q.n_cons = q.n_constraints;
+    for (int t = 0; t < tests[i].nt; ++t) {
+      Q.test_task[t] = tests[i].task[t];
+      Q.test_lower[t] = tests[i].lower[t];
+      Q.test_beta[t] = tests[i].beta[t];
+      Q.test_bias[t] = c->biases[tests[i].task[t]];
+    }
+    for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
+    const int64_t kk = std::max<int64_t>(q.k, 1);
+    unsigned char* o = S.out.as<unsigned char>();
+    Q.out_g = reinterpret_cast<unsigned long long*>(o);
+    Q.out_obj = reinterpret_cast<double*>(o + 8 * kk);
+    Q.out_cons = reinterpret_cast<double*>(o + 16 * kk);
+    Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
+    Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
+  }
+  cudaStream_t s = c->stream;
+  APEX_CU(cudaEventRecord(c->ev[0], s));
+  APEX_CU(cudaMemcpyAsync(c->d_queries.p, hq, nq * sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+
+  // retry loop: re-run with a preset threshold after a candidate overflow
+  std::vector<unsigned long long> tau0(nq, kNoTau);
+  bool use_tau0 = false;
+  for (int attempt = 0;; ++attempt) {
+    if (use_tau0) {
+      APEX_TRY(c->d_tau0.ensure(nq * sizeof(unsigned long long)));
+      APEX_TRY(c->h_tau0.ensure(nq * sizeof(unsigned long long)));
+      std::memcpy(c->h_tau0.p, tau0.data(), nq * sizeof(unsigned long long));
+      APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    }
+    init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, use_tau0 ? c->d_tau0.as<unsigned long long>() : nullptr);
+    ++st.launches;
+    // K2 pack
+    if (plan->pair_hi > plan->pair_lo) {
+      const int64_t n = (plan->pair_hi - plan->pair_lo) * ntp;
+      const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+      pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo,
+                                                   plan->pair_hi);
+      ++st.launches;
+    }
+    APEX_CU(cudaEventRecord(c->ev[1], s));
+    // seed threshold from exact samples
+    if (!use_tau0) {
+      uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
+                                       : (uint64_t)std::min<int64_t>(1 << 21, std::max<int64_t>(1 << 18, 64 * k_max));
+      S = std::min<uint64_t>(S, span);
+      if (S > 0 && k_max > 0) {
+        SampleLaunch P;
+        P.queries = dq;
+        P.rx = c->d_rx.as<DevReaction>();
+        P.g_off = c->d_goff.as<unsigned long long>();
+        P.n_rx = (int)c->rx.size();
+        P.values = c->d_values.as<float>();
+        P.n_pairs = c->n_pairs;
+        P.start = start;
+        P.end = end;
+        P.samples = S;
+        const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
+        sample_kernel<<<dim3(blocks, nq), 256, 0, s>>>(P);
+        tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
+        st.launches += 2;
+      }
+    }
+    APEX_CU(cudaEventRecord(c->ev[2], s));
+    // K3 enumeration chunks
+    ScanFn fn = pick_scan(NT, rl);
+    if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
+    const int cb = (int)c->opt_cb;
+    const size_t smem = scan_smem(NT, cb);
+    int occ = 0;
+    APEX_TRY(scan_occupancy(fn, smem, &occ));
+    const size_t n_tiles = plan->tiles.size();
+    std::vector<size_t> bounds;  // chunk ends in tile indices
+    if (span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && n_tiles > 1) {
+      const uint64_t first = span / (uint64_t)c->opt_chunk_div;
+      size_t i1 = (size_t)(std::lower_bound(plan->prefix.begin(), plan->prefix.end(), first) - plan->prefix.begin());
+      i1 = std::min(std::max<size_t>(i1, 1), n_tiles);
+      bounds.push_back(i1);
+    }
+    bounds.push_back(n_tiles);
+    size_t tb = 0;
+    for (size_t ci = 0; ci < bounds.size(); ++ci) {
+      const size_t te = bounds[ci];
+      if (te > tb) {
+        ScanLaunch L;
+        L.tiles = plan->d_tiles.as<Tile>();
+        L.tile_begin = (unsigned)tb;
+        L.tile_end = (unsigned)te;
+        L.rx = c->d_rx.as<DevReaction>();
+        L.values = c->d_values.as<float>();
+        L.n_pairs = c->n_pairs;
+        L.queries = dq;
+        L.cb = cb;
+        const int64_t blocks =
+            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
+        APEX_CU(cudaEventRecord(c->ev[6], s));
+        fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(L);
+        APEX_CU(cudaGetLastError());
+        APEX_CU(cudaEventRecord(c->ev[7], s));
+        ++st.launches;
+        ++st.scans;
+        if (ci + 1 < bounds.size()) {
+          // reset the work counter and raise tau from the candidates so far
+          tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);
+          st.launches += 1;
+        }
+        for (int i = 0; i < nq; ++i) {
+          APEX_CU(cudaMemsetAsync(&c->slots[i].ctl.as<QCtl>()->tile_counter, 0, sizeof(unsigned), s));
+        }
+      }
+      tb = te;
+    }
+    APEX_CU(cudaEventRecord(c->ev[3], s));
+    // final bound, compaction, exact select
+    tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
+    {
+      const int blocks = c->sm_count * 4;
+      compact_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq);
+    }
+    st.launches += 2;
+    {
+      int occ_sel = 0;
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
+      const int resident = std::max(1, occ_sel * c->sm_count);
+      int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / nq));
+      if (per_q * nq > resident) return set_err(APEX_ELIMIT, "too many queries in one batch for the select kernel");
+      void* args[] = {(void*)&dq};
+      APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, nq), dim3(kSelectThreads), args, 0, s));
+      ++st.launches;
+    }
+    APEX_CU(cudaEventRecord(c->ev[4], s));
+    if (finalize && k_max > 0) {
+      for (int i = 0; i < nq; ++i)
+        APEX_CU(cudaMemsetAsync(c->slots[i].rank.p, 0, std::max<int64_t>(qs[i].k, 1) * sizeof(unsigned), s));
+      const int ib = (int)((k_max + 255) / 256);
+      int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
+      rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
+      scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+      MatLaunch M;
+      M.queries = dq;
+      M.rx = c->d_rx.as<DevReaction>();
+      M.g_off = c->d_goff.as<unsigned long long>();
+      M.n_rx = (int)c->rx.size();
+      M.values = c->d_values.as<float>();
+      M.n_pairs = c->n_pairs;
+      M.biases = c->d_biases.as<double>();
+      materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
+      st.launches += 3;
+    }
+    APEX_CU(cudaGetLastError());
+    APEX_CU(cudaEventRecord(c->ev[5], s));
+    // read control blocks (overflow check) — one sync per call
+    APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
+    for (int i = 0; i < nq; ++i)
+      APEX_CU(cudaMemcpyAsync(c->h_ctl.as<QCtl>() + i, c->slots[i].ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
+    APEX_CU(cudaStreamSynchronize(s));
+    bool overflow = false;
+    for (int i = 0; i < nq; ++i) {
+      const QCtl& C = c->h_ctl.as<QCtl>()[i];
+      const unsigned long long cap = hq[i].cap;
+      if (C.count > cap) {
+        overflow = true;
+        tau0[i] = std::max<unsigned long long>(C.bound_key, C.tau_key);
+      } else {
+        tau0[i] = kNoTau;
+      }
+    }
+    if (!overflow) break;
+    if (attempt >= 3) return set_err(APEX_ELIMIT, "candidate buffer overflow persists (massive exact ties?)");
+    ++st.retries;
+    use_tau0 = true;
+    // queries that did not overflow re-run too (cheap, keeps the batch uniform);
+    // give them their own final threshold as well
+    for (int i = 0; i < nq; ++i) {
+      const QCtl& C = c->h_ctl.as<QCtl>()[i];
+      if (tau0[i] == kNoTau) tau0[i] = C.bound_key;
+      if (attempt >= 1) {
+        // second overflow: grow the buffers
+        Slot& S = c->slots[i];
+        const size_t nb = S.buf.bytes * 4;
+        APEX_TRY(S.buf.ensure(nb));
+        APEX_TRY(S.comp.ensure(nb));
+        hq[i].buf = S.buf.as<Entry>();
+        hq[i].comp = S.comp.as<Entry>();
+        hq[i].cap = S.buf.bytes / sizeof(Entry);
+      }
+    }
+    APEX_CU(cudaMemcpyAsync(c->d_queries.p, hq, nq * sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+  }
+  for (int e = 0; e < 5; ++e) APEX_CU(cudaEventElapsedTime(&st.ms[e], c->ev[e], c->ev[e + 1]));
+  float last_scan = 0;
+  APEX_CU(cudaEventElapsedTime(&last_scan, c->ev[6], c->ev[7]));
+  st.scan_kernel_ms = last_scan;
+  return APEX_OK;
+}
+
+int validate_queries(apex_ctx* c, const apex_query_spec* qs, int nq) {
+  if (nq < 0) return set_err(APEX_EINVAL, "negative query count");
+  if (nq > 0 && !qs) return set_err(APEX_EINVAL, "null queries");
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    if (q.objective_task < 0 || q.objective_task >= c->n_tasks)
+      return set_err(APEX_ETASK, "unknown task index " + std::to_string(q.objective_task));
+    if (q.k < 0) return set_err(APEX_EINVAL, "k must be >= 0");
+    if (q.k > (int64_t)1 << 26) return set_err(APEX_ELIMIT, "k exceeds the compiled limit (2^26)");
+    if (q.n_constraints < 0 || (q.n_constraints > 0 && !q.constraints))
+      return set_err(APEX_EINVAL, "bad constraint list");
+    if (!(q.start <= q.end && q.end <= c->total))
+      return set_err(APEX_ERANGE, "index range [" + std::to_string(q.start) + ", " + std::to_string(q.end) + ") invalid");
+  }
+  return APEX_OK;
+}
+
+void fill_stats(apex_stats* stats, const RunStats& st, float d2h, float total, int64_t cand) {
+  if (!stats) return;
+  stats->pack_ms = st.ms[0];
+  stats->seed_ms = st.ms[1];
+  stats->scan_ms = st.ms[2];
+  stats->select_ms = st.ms[3];
+  stats->finalize_ms = st.ms[4];
+  stats->d2h_ms = d2h;
+  stats->total_ms = total;
+  stats->scan_kernel_ms = st.scan_kernel_ms;
+  stats->candidates = cand;
+  stats->scan_launches = st.scans;
+  stats->kernel_launches = st.launches;
+  stats->retries = st.retries;
+}
+
+// Copy materialized rows of slot i to the caller's result.
+int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* res) {
+  size_t total = 0;
+  std::vector<size_t> offs(nq);
+  for (int i = 0; i < nq; ++i) {
+    offs[i] = total;
+    total += out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints);
+  }
+  APEX_TRY(c->h_out.ensure(total));
+  for (int i = 0; i < nq; ++i)
+    if (qs[i].k > 0 && qs[i].start < qs[i].end)
+      APEX_CU(cudaMemcpyAsync(c->h_out.as<unsigned char>() + offs[i], c->slots[i].out.p,
+                              out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints), cudaMemcpyDeviceToHost,
+                              c->stream));
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    apex_result& r = res[i];
+    const uint64_t span = q.end - q.start;
+    const int64_t kk = std::max<int64_t>(q.k, 1);
+    const int m = q.n_constraints;
+    int64_t n = 0;
+    if (q.k > 0 && span > 0) n = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
+    r.n = n;
+    r.scanned = span;
+    r.discarded = (int64_t)std::min<uint64_t>((uint64_t)q.k, span) - n;
+    if (n > 0) {
+      const unsigned char* o = c->h_out.as<unsigned char>() + offs[i];
+      if (r.global_index) std::memcpy(r.global_index, o, 8 * n);
+      if (r.objective) std::memcpy(r.objective, o + 8 * kk, 8 * n);
+      if (r.constraint_values && m) std::memcpy(r.constraint_values, o + 16 * kk, 8 * (size_t)m * n);
+      if (r.reaction) std::memcpy(r.reaction, o + (16 + 8 * (size_t)m) * kk, 4 * n);
+      if (r.digits) std::memcpy(r.digits, o + (20 + 8 * (size_t)m) * kk, 4 * (size_t)kMaxRg * n);
+    }
+  }
+  return APEX_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* apex_last_error(void) { return t_err.c_str(); }
+const char* apex_version(void) { return "apex_b200 0.1 (sm_100a)"; }
+
+int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
+  if (!out) return set_err(APEX_EINVAL, "null out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return set_err(APEX_ECUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                   "); the B200 path has no CPU fallback");
+  }
+  if (device < 0 || device >= n) return set_err(APEX_EINVAL, "bad device ordinal");
+  APEX_CU(cudaSetDevice(device));
+  apex_ctx* c = new apex_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&c->cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (c->cc_major != 10) {
+    delete c;
+    return set_err(APEX_ECUDA, "device is not sm_100 (B200); kernels are built for sm_100a only");
+  }
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return set_err(APEX_ECUDA, "stream creation failed");
+    }
+    c->own_stream = true;
+  }
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  *out = c;
+  return APEX_OK;
+}
+
+void apex_ctx_destroy(apex_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& s : c->slots) s.release();
+  for (auto& p : c->plans) p.d_tiles.release();
+  c->d_rx.release();
+  c->d_goff.release();
+  c->d_values.release();
+  c->d_biases.release();
+  c->d_queries.release();
+  c->d_tau0.release();
+  c->h_queries.release();
+  c->h_ctl.release();
+  c->h_out.release();
+  c->h_tau0.release();
+  for (auto& ev : c->ev) cudaEventDestroy(ev);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int apex_set_stream(apex_ctx* c, void* stream) {
+  APEX_TRY(check_ctx(c, false));
+  if (c->own_stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+    c->own_stream = false;
+  }
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    APEX_CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  return APEX_OK;
+}
+
+int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64_t n_pairs) {
+  APEX_TRY(check_ctx(c, false));
+  if (n_rx < 0 || (n_rx > 0 && !rxs) || n_pairs < 0) return set_err(APEX_EINVAL, "bad library arguments");
+  std::vector<DevReaction> rx(n_rx);
+  std::vector<unsigned long long> goff(n_rx + 1, 0);
+  unsigned __int128 total = 0;
+  for (int t = 0; t < n_rx; ++t) {
+    const apex_reaction& a = rxs[t];
+    if (a.n_rgroups < 1 || a.n_rgroups > kMaxRg)
+      return set_err(APEX_ELIMIT, "reaction " + std::to_string(t) + " has " + std::to_string(a.n_rgroups) +
+                                      " R-groups (supported: 1.." + std::to_string(kMaxRg) + ")");
+    DevReaction& R = rx[t];
+    std::memset(&R, 0, sizeof(R));
+    R.c = a.n_rgroups;
+    unsigned __int128 size = 1;
+    for (int j = 0; j < R.c; ++j) {
+      if (a.sizes[j] < 1) return set_err(APEX_EINVAL, "empty R-group");
+      if (a.pair_offset[j] < 0 || a.pair_offset[j] + a.sizes[j] > n_pairs)
+        return set_err(APEX_EINVAL, "table rows for an R-group do not match library");
+      R.size[j] = a.sizes[j];
+      R.pair_off[j] = a.pair_offset[j];
+      size *= (unsigned __int128)a.sizes[j];
+    }
+    if (R.size[R.c - 1] > 0xffffffffll) return set_err(APEX_ELIMIT, "last R-group larger than 2^32");
+    R.n_rows = (uint64_t)(size / (unsigned __int128)R.size[R.c - 1]);
+    if ((uint64_t)total != a.g_offset) return set_err(APEX_EINVAL, "reaction offsets are not the running product count");
+    R.g_off = a.g_offset;
+    goff[t] = (unsigned long long)total;
+    total += size;
+    if (total > (unsigned __int128)UINT64_MAX) return set_err(APEX_ELIMIT, "product count exceeds unsigned 64-bit range");
+  }
+  goff[n_rx] = (unsigned long long)total;
+  APEX_TRY(c->d_rx.ensure(std::max<size_t>(1, rx.size()) * sizeof(DevReaction)));
+  APEX_TRY(c->d_goff.ensure(goff.size() * sizeof(unsigned long long)));
+  if (n_rx) APEX_CU(cudaMemcpy(c->d_rx.p, rx.data(), rx.size() * sizeof(DevReaction), cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(c->d_goff.p, goff.data(), goff.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  c->rx = std::move(rx);
+  c->goff = std::move(goff);
+  c->total = (uint64_t)total;
+  c->lib_pairs = n_pairs;
+  c->lib_loaded = true;
+  for (auto& p : c->plans) p.d_tiles.release();
+  c->plans.clear();
+  return APEX_OK;
+}
+
+int apex_load_table(apex_ctx* c, const float* values, const double* biases, int32_t n_tasks, int64_t n_pairs) {
+  APEX_TRY(check_ctx(c, false));
+  if (n_tasks < 1 || n_pairs < 0 || !biases || (n_pairs > 0 && !values)) return set_err(APEX_EINVAL, "bad table arguments");
+  const size_t n = (size_t)n_tasks * n_pairs;
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(values[i])) return set_err(APEX_EINVAL, "contribution table has non-finite entries");
+  for (int t = 0; t < n_tasks; ++t)
+    if (!std::isfinite(biases[t])) return set_err(APEX_EINVAL, "contribution table has non-finite biases");
+  APEX_TRY(c->d_values.ensure(std::max<size_t>(n, 1) * sizeof(float)));
+  APEX_TRY(c->d_biases.ensure(n_tasks * sizeof(double)));
+  if (n) APEX_CU(cudaMemcpy(c->d_values.p, values, n * sizeof(float), cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(c->d_biases.p, biases, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
+  c->biases.assign(biases, biases + n_tasks);
+  c->n_tasks = n_tasks;
+  c->n_pairs = n_pairs;
+  c->table_loaded = true;
+  return APEX_OK;
+}
+
+int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, int32_t d, const double* w_dev,
+                           int32_t n_tasks, float* values_dev) {
+  APEX_TRY(check_ctx(c, false));
+  if (n_pairs < 0 || d < 1 || n_tasks < 1 || !w_dev || !values_dev || (n_pairs > 0 && !u_dev))
+    return set_err(APEX_EINVAL, "bad precompute arguments");
+  if (n_pairs == 0) return APEX_OK;
+  const size_t smem = ((size_t)n_tasks * d + (size_t)kPreRows * (d + 1)) * sizeof(double);
+  if (smem > 220 * 1024) return set_err(APEX_ELIMIT, "precompute: n_tasks * d too large for shared memory");
+  APEX_CU(cudaFuncSetAttribute((const void*)precompute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)precompute_kernel, 256, smem));
+  const int64_t blocks = std::min<int64_t>((n_pairs + kPreRows - 1) / kPreRows, (int64_t)c->sm_count * std::max(occ, 1));
+  precompute_kernel<<<(unsigned)blocks, 256, smem, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks, values_dev);
+  APEX_CU(cudaGetLastError());
+  return APEX_OK;
+}
+
+int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, const double* head_w,
+                    const double* head_b, int32_t n_tasks, float* values_out) {
+  APEX_TRY(check_ctx(c, false));
+  if (!u || !head_w || !head_b || n_pairs < 0 || d < 1 || n_tasks < 1) return set_err(APEX_EINVAL, "bad cache arguments");
+  for (int t = 0; t < n_tasks; ++t)
+    if (!std::isfinite(head_b[t])) return set_err(APEX_EINVAL, "non-finite head bias");
+  DBuf du, dw;
+  APEX_TRY(du.ensure(std::max<size_t>(1, (size_t)n_pairs * d) * sizeof(double)));
+  APEX_TRY(dw.ensure((size_t)n_tasks * d * sizeof(double)));
+  APEX_TRY(c->d_values.ensure(std::max<size_t>(1, (size_t)n_tasks * n_pairs) * sizeof(float)));
+  APEX_TRY(c->d_biases.ensure(n_tasks * sizeof(double)));
+  APEX_CU(cudaMemcpyAsync(du.p, u, (size_t)n_pairs * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  APEX_CU(cudaMemcpyAsync(dw.p, head_w, (size_t)n_tasks * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  APEX_CU(cudaMemcpyAsync(c->d_biases.p, head_b, n_tasks * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = apex_precompute_device(c, du.as<double>(), n_pairs, d, dw.as<double>(), n_tasks, c->d_values.as<float>());
+  if (rc != APEX_OK) {
+    du.release();
+    dw.release();
+    return rc;
+  }
+  if (values_out && n_pairs > 0)
+    APEX_CU(cudaMemcpyAsync(values_out, c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float), cudaMemcpyDeviceToHost,
+                            c->stream));
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  du.release();
+  dw.release();
+  c->biases.assign(head_b, head_b + n_tasks);
+  c->n_tasks = n_tasks;
+  c->n_pairs = n_pairs;
+  c->table_loaded = true;
+  return APEX_OK;
+}
+
+int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* res, apex_stats* stats) {
+  APEX_TRY(check_ctx(c, true));
+  APEX_TRY(validate_queries(c, qs, nq));
+  if (nq > 0 && !res) return set_err(APEX_EINVAL, "null results");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  // group queries by range (each group shares one enumeration schedule)
+  std::vector<int> order(nq);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return qs[a].start != qs[b].start ? qs[a].start < qs[b].start : qs[a].end < qs[b].end;
+  });
+  RunStats agg;
+  float total_ms = 0, d2h_ms = 0;
+  int64_t cand = 0;
+  size_t g0 = 0;
+  while (g0 < order.size()) {
+    size_t g1 = g0 + 1;
+    while (g1 < order.size() && qs[order[g1]].start == qs[order[g0]].start && qs[order[g1]].end == qs[order[g0]].end) ++g1;
+    std::vector<apex_query_spec> grp;
+    std::vector<int> live;
+    for (size_t i = g0; i < g1; ++i) {
+      const apex_query_spec& q = qs[order[i]];
+      if (q.k > 0 && q.end > q.start) {
+        grp.push_back(q);
+        live.push_back(order[i]);
+      } else {
+        apex_result& r = res[order[i]];
+        r.n = 0;
+        r.scanned = q.end - q.start;
+        r.discarded = 0;
+      }
+    }
+    if (!grp.empty()) {
+      RunStats st;
+      APEX_TRY(run_batch(c, grp.data(), (int)grp.size(), true, st));
+      APEX_CU(cudaEventRecord(c->ev[6], c->stream));
+      std::vector<apex_result> tmp(grp.size());
+      for (size_t i = 0; i < grp.size(); ++i) tmp[i] = res[live[i]];
+      APEX_TRY(copy_results(c, grp.data(), (int)grp.size(), tmp.data()));
+      APEX_CU(cudaEventRecord(c->ev[7], c->stream));
+      APEX_CU(cudaEventSynchronize(c->ev[7]));
+      float d2h = 0;
+      cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]);
+      for (size_t i = 0; i < grp.size(); ++i) {
+        res[live[i]] = tmp[i];
+        cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
+      }
+      for (int e = 0; e < 5; ++e) agg.ms[e] += st.ms[e];
+      agg.scan_kernel_ms += st.scan_kernel_ms;
+      agg.launches += st.launches;
+      agg.scans += st.scans;
+      agg.retries += st.retries;
+      for (int e = 0; e < 5; ++e) total_ms += st.ms[e];
+      total_ms += d2h;
+      d2h_ms += d2h;
+    }
+    g0 = g1;
+  }
+  fill_stats(stats, agg, d2h_ms, total_ms, cand);
+  return APEX_OK;
+}
+
+int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_entry* out_dev, int64_t* counts,
+                     apex_stats* stats) {
+  APEX_TRY(check_ctx(c, true));
+  APEX_TRY(validate_queries(c, qs, nq));
+  if (nq <= 0) return APEX_OK;
+  if (!out_dev || !counts) return set_err(APEX_EINVAL, "null output");
+  for (int i = 1; i < nq; ++i)
+    if (qs[i].start != qs[0].start || qs[i].end != qs[0].end || qs[i].k != qs[0].k)
+      return set_err(APEX_EINVAL, "apex_query_local: all queries must share range and k");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const int64_t k = qs[0].k;
+  if (k == 0 || qs[0].end == qs[0].start) {
+    for (int i = 0; i < nq; ++i) counts[i] = 0;
+    return APEX_OK;
+  }
+  RunStats st;
+  APEX_TRY(run_batch(c, qs, nq, false, st));
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  export_kernel<<<dim3((unsigned)((k + 255) / 256), nq), 256, 0, c->stream>>>(dq, reinterpret_cast<Entry*>(out_dev));
+  APEX_CU(cudaGetLastError());
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  int64_t cand = 0;
+  for (int i = 0; i < nq; ++i) {
+    counts[i] = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
+    cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
+  }
+  float total = 0;
+  for (int e = 0; e < 5; ++e) total += st.ms[e];
+  fill_stats(stats, st, 0.f, total, cand);
+  return APEX_OK;
+}
+
+int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry* entries_dev, int64_t n_entries,
+                        uint64_t total_scanned, apex_result* res, apex_stats* stats) {
+  APEX_TRY(check_ctx(c, true));
+  if (!q || !res || n_entries < 0 || (n_entries > 0 && !entries_dev)) return set_err(APEX_EINVAL, "bad merge arguments");
+  if (q->objective_task < 0 || q->objective_task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+  if (q->n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+  for (int i = 0; i < q->n_constraints; ++i)
+    if (q->constraints[i].task < 0 || q->constraints[i].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const int64_t k = q->k;
+  res->scanned = total_scanned;
+  if (k == 0 || n_entries == 0) {
+    res->n = 0;
+    res->discarded = (int64_t)std::min<uint64_t>((uint64_t)k, total_scanned);
+    return APEX_OK;
+  }
+  if (c->slots.empty()) c->slots.resize(1);
+  Slot& S = c->slots[0];
+  const int64_t cap = std::max<int64_t>(n_entries, 1024);
+  APEX_TRY(S.buf.ensure(sizeof(Entry)));
+  APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
+  APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
+  APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
+  APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
+  APEX_TRY(S.hist.ensure(kHistBins * sizeof(unsigned)));
+  APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
+  APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
+  APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
+  APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
+  APEX_TRY(c->h_queries.ensure(sizeof(ScanQuery)));
+  ScanQuery& Q = *c->h_queries.as<ScanQuery>();
+  std::memset(&Q, 0, sizeof(Q));
+  Q.buf = S.buf.as<Entry>();
+  Q.comp = S.comp.as<Entry>();
+  Q.sel = S.sel.as<Entry>();
+  Q.sorted = S.sorted.as<Entry>();
+  Q.rank = S.rank.as<unsigned>();
+  Q.hist = S.hist.as<unsigned>();
+  Q.seed_hist = S.seed_hist.as<unsigned>();
+  Q.ctl = S.ctl.as<QCtl>();
+  Q.cap = (unsigned long long)cap;
+  Q.k = k;
+  Q.maximize = q->maximize ? 1 : 0;
+  Q.obj_task = q->objective_task;
+  Q.n_cons = q->n_constraints;
+  for (int m = 0; m < q->n_constraints; ++m) Q.cons_task[m] = q->constraints[m].task;
+  unsigned char* o = S.out.as<unsigned char>();
+  Q.out_g = reinterpret_cast<unsigned long long*>(o);
+  Q.out_obj = reinterpret_cast<double*>(o + 8 * k);
+  Q.out_cons = reinterpret_cast<double*>(o + 16 * k);
+  Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q->n_constraints) * k);
+  Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q->n_constraints) * k);
+  cudaStream_t s = c->stream;
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  APEX_CU(cudaEventRecord(c->ev[0], s));
+  APEX_CU(cudaMemcpyAsync(c->d_queries.p, &Q, sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+  init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr);
+  merge_load_kernel<<<(unsigned)std::min<int64_t>((n_entries + 255) / 256, c->sm_count * 4), 256, 0, s>>>(
+      dq, reinterpret_cast<const Entry*>(entries_dev), (unsigned long long)n_entries);
+  {
+    void* args[] = {(void*)&dq};
+    APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, c->sm_count)), 1),
+                                        dim3(kSelectThreads), args, 0, s));
+  }
+  APEX_CU(cudaMemsetAsync(S.rank.p, 0, k * sizeof(unsigned), s));
+  const int ib = (int)((k + 255) / 256);
+  const int js = std::max(1, std::min(ib, (2 * c->sm_count + ib - 1) / ib));
+  rank_kernel<<<dim3(ib, js, 1), 256, 0, s>>>(dq, js);
+  scatter_kernel<<<dim3(ib, 1), 256, 0, s>>>(dq);
+  MatLaunch M;
+  M.queries = dq;
+  M.rx = c->d_rx.as<DevReaction>();
+  M.g_off = c->d_goff.as<unsigned long long>();
+  M.n_rx = (int)c->rx.size();
+  M.values = c->d_values.as<float>();
+  M.n_pairs = c->n_pairs;
+  M.biases = c->d_biases.as<double>();
+  materialize_kernel<<<dim3((unsigned)((k + 127) / 128), 1), 128, 0, s>>>(M);
+  APEX_CU(cudaGetLastError());
+  APEX_TRY(c->h_ctl.ensure(sizeof(QCtl)));
+  APEX_CU(cudaMemcpyAsync(c->h_ctl.p, S.ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
+  APEX_CU(cudaEventRecord(c->ev[1], s));
+  apex_query_spec qq = *q;
+  qq.start = 0;
+  qq.end = total_scanned;
+  APEX_TRY(copy_results(c, &qq, 1, res));
+  if (stats) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    stats->select_ms = ms;
+    stats->total_ms = ms;
+    stats->kernel_launches = 6;
+  }
+  return APEX_OK;
+}
+
+int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
+  if (!c || !name) return set_err(APEX_EINVAL, "bad option arguments");
+  std::string n(name);
+  if (n == "cap") c->opt_cap = std::max<int64_t>(v, 1024);
+  else if (n == "cb") {
+    if (v < 8 || v % 8 || v > 256) return set_err(APEX_EINVAL, "cb must be a multiple of 8 in [8, 256]");
+    c->opt_cb = v;
+  } else if (n == "rl") c->opt_rl = v;
+  else if (n == "samples") c->opt_samples = v;
+  else if (n == "chunk_div") c->opt_chunk_div = v;
+  else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
+  else if (n == "tile_products") {
+    c->opt_tile_products = v;
+    for (auto& p : c->plans) p.d_tiles.release();
+    c->plans.clear();
+  } else if (n == "select_ctas") c->opt_select_ctas = std::max<int64_t>(1, v);
+  else return set_err(APEX_EINVAL, "unknown option " + n);
+  return APEX_OK;
+}
+
+int apex_get_device_info(apex_ctx* c, int32_t* sm, int32_t* ma, int32_t* mi) {
+  if (!c) return set_err(APEX_EINVAL, "null context");
+  if (sm) *sm = c->sm_count;
+  if (ma) *ma = c->cc_major;
+  if (mi) *mi = c->cc_minor;
+  return APEX_OK;
+}
+
+int apex_debug_thresholds(apex_ctx* c, const double* p, const double* b, const double* beta, int64_t n, float* up,
+                          float* lo) {
+  APEX_TRY(check_ctx(c, false));
+  if (n <= 0) return APEX_OK;
+  DBuf dp, db, dbeta, du, dl;
+  APEX_TRY(dp.ensure(n * 8));
+  APEX_TRY(db.ensure(n * 8));
+  APEX_TRY(dbeta.ensure(n * 8));
+  APEX_TRY(du.ensure(n * 4));
+  APEX_TRY(dl.ensure(n * 4));
+  APEX_CU(cudaMemcpy(dp.p, p, n * 8, cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(db.p, b, n * 8, cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(dbeta.p, beta, n * 8, cudaMemcpyHostToDevice));
+  thresholds_kernel<<<(unsigned)((n + 127) / 128), 128, 0, c->stream>>>(dp.as<double>(), db.as<double>(),
+                                                                        dbeta.as<double>(), (int)n, du.as<float>(),
+                                                                        dl.as<float>());
+  APEX_CU(cudaGetLastError());
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  APEX_CU(cudaMemcpy(up, du.p, n * 4, cudaMemcpyDeviceToHost));
+  APEX_CU(cudaMemcpy(lo, dl.p, n * 4, cudaMemcpyDeviceToHost));
+  for (DBuf* d : {&dp, &db, &dbeta, &du, &dl}) d->release();
+  return APEX_OK;
+}
+
+}  // extern "C"

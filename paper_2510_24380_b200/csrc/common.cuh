@@ -1,0 +1,186 @@
+// common.cuh — shared device helpers for the APEX B200 kernels (sm_100a).
+//
+// Exactness helpers used by every kernel:
+//   * ordered int32 keys over finite fp32 values (threshold bisection);
+//   * order-preserving uint64 keys over fp64 scores (selection);
+//   * the reference's fp64 accumulation order, ((p + x) + bias) with IEEE
+//     round-to-nearest adds that the compiler may not contract or reorder
+//     (engine.py:210-222, bias added last at :219).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/apex_b200.h"
+
+namespace apexb200 {
+
+constexpr int kMaxRg = APEX_MAX_RGROUPS;
+constexpr int kMaxTests = 24;       // compiled maximum of per-product tests
+constexpr int kMaxCons = 32;        // constraints per query (materialization)
+constexpr int kScanWarps = 8;       // warps per enumeration CTA
+constexpr int kSelectThreads = 512;
+constexpr uint64_t kNoTau = 0ull;   // "no admission threshold yet" (key 0 is never a finite score)
+
+// Reaction descriptor in device memory (positional, csl.py:90-97).
+struct DevReaction {
+  int32_t c;                      // R-groups
+  int32_t _pad;
+  int64_t size[kMaxRg];           // synthons per R-group
+  int64_t pair_off[kMaxRg];       // table row of digit 0 for each R-group
+  uint64_t g_off;                 // reaction_offset
+  uint64_t n_rows;                // product of sizes[0..c-2]
+};
+
+// One enumeration tile: rows [row0, row0+nrows) x columns [col0, col0+ncols)
+// of one reaction; row = mixed-radix prefix digits, column = last digit.
+struct Tile {
+  uint64_t row0;
+  uint32_t rx;
+  uint32_t nrows;
+  uint32_t col0;
+  uint32_t ncols;
+};
+
+// Candidate / exchange entry (== apex_entry): order-preserving key of the
+// signed objective and the 64-bit global index.  Best = larger key, then
+// smaller g (engine.py:246 ordering (-c, -s, g) restricted to feasible rows).
+struct __align__(16) Entry {
+  unsigned long long key;
+  unsigned long long g;
+};
+
+// Per-query control block (device); protocol in capi.cu.
+struct QCtl {
+  unsigned long long tau_key;     // admission threshold (kNoTau = none)
+  unsigned long long count;       // candidates appended by scans (may exceed cap)
+  unsigned long long comp_count;  // entries in the compacted array
+  unsigned long long sel_count;   // entries selected (<= k)
+  unsigned long long bound_key;   // final compaction bound
+  unsigned long long min_key;     // select scratch
+  unsigned int active;            // participates in the current launch
+  unsigned int tile_counter;      // scan work distribution
+  unsigned int barrier;           // select grid barrier
+  unsigned int out_count;         // select compaction counter
+  unsigned int hist[3][256];      // select histograms (triple-buffered)
+};
+
+constexpr int kHistBins = 65536;  // candidate histogram over key >> 48
+
+// Per-query parameters (device, read-only during a launch).
+struct ScanQuery {
+  const float* packed;            // [n_pairs][ntp] signed test columns
+  Entry* buf;                     // candidate buffer (cap entries)
+  Entry* comp;                    // compacted candidates (cap entries)
+  Entry* sel;                     // selected top-k (k entries, unordered)
+  Entry* sorted;                  // best-first (k entries)
+  unsigned int* rank;             // [k]
+  unsigned int* hist;             // [kHistBins] histogram of appended keys
+  unsigned int* seed_hist;        // [kHistBins] histogram of feasible sampled keys
+  QCtl* ctl;
+  unsigned long long cap;         // capacity of buf / comp (entries)
+  long long k;
+  int32_t nt;                     // live tests (test 0 = objective admission)
+  int32_t ntp;                    // packed row stride (floats, multiple of 4)
+  int32_t maximize;
+  int32_t obj_task;
+  int32_t n_cons;                 // constraints (materialization order)
+  int32_t _pad;
+  int32_t test_task[kMaxTests];
+  int32_t test_lower[kMaxTests];  // 1: lower-bound test (y = -x), 0: upper (y = x)
+  double test_beta[kMaxTests];    // bound (ignored for test 0: derived from tau)
+  double test_bias[kMaxTests];
+  int32_t cons_task[kMaxCons];
+  // materialization outputs (device, capacity k)
+  unsigned long long* out_g;
+  double* out_obj;
+  double* out_cons;               // [k][n_cons]
+  int32_t* out_rx;
+  int32_t* out_dig;               // [k][kMaxRg]
+};
+
+// ---------------------------------------------------------------------------
+// fp32 ordered keys: key(-0) == key(+0) == 0, key(FLT_MAX) = 0x7f7fffff.
+constexpr int64_t kKeyMax = 0x7f7fffffll;
+constexpr int64_t kKeyMin = -0x7f7fffffll;
+
+__device__ __forceinline__ int64_t fkey(float x) {
+  int32_t b = __float_as_int(x);
+  return b >= 0 ? (int64_t)b : -(int64_t)(b & 0x7fffffff);
+}
+__device__ __forceinline__ float fromkey(int64_t k) {
+  return k >= 0 ? __int_as_float((int32_t)k) : __int_as_float((int32_t)((-k) | 0x80000000ll));
+}
+
+// The reference's per-product value for fixed prefix sum p: ((p + x) + b).
+__device__ __forceinline__ double fx(double p, float x, double b) {
+  return __dadd_rn(__dadd_rn(p, (double)x), b);
+}
+
+// fp64 score -> order-preserving key (+-0 canonicalized to +0).
+__host__ __device__ __forceinline__ unsigned long long skey(double s) {
+  if (s == 0.0) s = 0.0;
+  unsigned long long u;
+#ifdef __CUDA_ARCH__
+  u = (unsigned long long)__double_as_longlong(s);
+#else
+  __builtin_memcpy(&u, &s, 8);
+#endif
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double key_to_score(unsigned long long k) {
+  unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double s;
+#ifdef __CUDA_ARCH__
+  s = __longlong_as_double((long long)u);
+#else
+  __builtin_memcpy(&s, &u, 8);
+#endif
+  return s;
+}
+
+__device__ __forceinline__ bool entry_better(const Entry& a, const Entry& b) {
+  return a.key > b.key || (a.key == b.key && a.g < b.g);
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + 1-D bulk async copy (TMA engine, SASS UBLKCP) helpers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace apexb200

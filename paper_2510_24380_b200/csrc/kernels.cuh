@@ -1,0 +1,808 @@
+// kernels.cuh — sm_100a kernels of the APEX enumeration-and-retrieval path.
+//
+//   K1 precompute_kernel   engine.py:80-92     fp64 head_w @ u^T -> fp32 table (HBM-bound)
+//   K2 pack_kernel         engine.py:195-208   per-query signed test columns, [pair][ntp]
+//   K3 scan_kernel         engine.py:169-235, 290-307
+//                                              fused enumeration + exact constraint /
+//                                              admission predicate + candidate append
+//   K5 select_kernel       engine.py:288-307 (heap), 385-386 (lexsort)
+//                                              exact top-k radix select on (key, g)
+//   K6 order kernels       engine.py:246      best-first order (s desc, g asc)
+//   K7 materialize_kernel  csl.py:166-184, engine.py:95-101, 238-262
+//                                              decode g, objective, constraint values
+//
+// Included exactly once (by capi.cu): one translation unit, no -rdc.
+#pragma once
+#include "common.cuh"
+
+namespace apexb200 {
+
+// ---------------------------------------------------------------------------
+// Exact per-row thresholds.
+//
+// For a fixed prefix (row) the reference value of product (row, x) is
+// fx(p, x, b) = ((p + x) + b) in fp64 (engine.py:214-219), monotone
+// non-decreasing in the fp32 contribution x of the last R-group.  So
+// "fx <= beta" holds exactly on a down-set of fp32 values and "fx >= beta" on an
+// up-set; we find the boundary exactly (guess, then at most a few ulp steps,
+// then bisection over the ordered fp32 keys in the rare degenerate case).
+__device__ __noinline__ float thr_upper(double p, double b, double beta) {
+  const double gd = __dsub_rn(__dsub_rn(beta, b), p);
+  int64_t k;
+  if (!(gd < 3.4028234663852886e38)) k = kKeyMax;
+  else if (!(gd > -3.4028234663852886e38)) k = kKeyMin;
+  else k = fkey(__double2float_rn(gd));
+  if (fx(p, fromkey(k), b) <= beta) {
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {
+      if (k == kKeyMax) return __int_as_float(0x7f800000);
+      if (fx(p, fromkey(k + 1), b) <= beta) ++k;
+      else return fromkey(k);
+    }
+    if (fx(p, fromkey(kKeyMax), b) <= beta) return __int_as_float(0x7f800000);
+    int64_t lo = k, hi = kKeyMax;  // lo qualifies, hi does not
+#pragma unroll 1
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (fx(p, fromkey(mid), b) <= beta) lo = mid; else hi = mid;
+    }
+    return fromkey(lo);
+  } else {
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {
+      if (k == kKeyMin) return __int_as_float(0x7fffffff);
+      --k;
+      if (fx(p, fromkey(k), b) <= beta) return fromkey(k);
+    }
+    if (!(fx(p, fromkey(kKeyMin), b) <= beta)) return __int_as_float(0x7fffffff);
+    int64_t lo = kKeyMin, hi = k;  // lo qualifies, hi does not
+#pragma unroll 1
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (fx(p, fromkey(mid), b) <= beta) lo = mid; else hi = mid;
+    }
+    return fromkey(lo);
+  }
+}
+
+__device__ __noinline__ float thr_lower(double p, double b, double beta) {
+  const double gd = __dsub_rn(__dsub_rn(beta, b), p);
+  int64_t k;
+  if (!(gd < 3.4028234663852886e38)) k = kKeyMax;
+  else if (!(gd > -3.4028234663852886e38)) k = kKeyMin;
+  else k = fkey(__double2float_rn(gd));
+  if (fx(p, fromkey(k), b) >= beta) {
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {
+      if (k == kKeyMin) return __int_as_float(0xff800000);
+      if (fx(p, fromkey(k - 1), b) >= beta) --k;
+      else return fromkey(k);
+    }
+    if (fx(p, fromkey(kKeyMin), b) >= beta) return __int_as_float(0xff800000);
+    int64_t lo = kKeyMin, hi = k;  // hi qualifies, lo does not
+#pragma unroll 1
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (fx(p, fromkey(mid), b) >= beta) hi = mid; else lo = mid;
+    }
+    return fromkey(hi);
+  } else {
+#pragma unroll 1
+    for (int it = 0; it < 3; ++it) {
+      if (k == kKeyMax) return __int_as_float(0x7fffffff);
+      ++k;
+      if (fx(p, fromkey(k), b) >= beta) return fromkey(k);
+    }
+    if (!(fx(p, fromkey(kKeyMax), b) >= beta)) return __int_as_float(0x7fffffff);
+    int64_t lo = k, hi = kKeyMax;  // hi qualifies, lo does not
+#pragma unroll 1
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (fx(p, fromkey(mid), b) >= beta) hi = mid; else lo = mid;
+    }
+    return fromkey(hi);
+  }
+}
+
+// Debug/test entry: thresholds for arrays of (p, b, beta) (used by the GPU
+// parity tests of the threshold construction itself).
+__global__ void thresholds_kernel(const double* p, const double* b, const double* beta, int n,
+                                  float* up, float* lo) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    up[i] = thr_upper(p[i], b[i], beta[i]);
+    lo[i] = thr_lower(p[i], b[i], beta[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: values[t][p] = fl32(sum_d head_w[t][d] * u[p][d]), fp64 products and
+// accumulation (engine.py:82).  HBM-bound: u is read once (coalesced through
+// shared memory), the table written once.  Each CTA stages 128 rows of u
+// (128 x d doubles) in smem; thread (row, task-group) computes the dots.
+constexpr int kPreRows = 64;
+__global__ void __launch_bounds__(256) precompute_kernel(const double* __restrict__ u, int64_t n_pairs, int d,
+                                                         const double* __restrict__ head_w, int n_tasks,
+                                                         float* __restrict__ values) {
+  extern __shared__ double psm[];
+  double* w_s = psm;                      // [n_tasks][d]
+  double* u_s = psm + n_tasks * d;        // [kPreRows][d+1]
+  const int ld = d + 1;
+  for (int i = threadIdx.x; i < n_tasks * d; i += blockDim.x) w_s[i] = head_w[i];
+  for (int64_t base = (int64_t)blockIdx.x * kPreRows; base < n_pairs; base += (int64_t)gridDim.x * kPreRows) {
+    const int rows = (int)(int)(n_pairs - base < kPreRows ? n_pairs - base : kPreRows);
+    __syncthreads();
+    const double* src = u + base * d;
+    for (int i = threadIdx.x; i < rows * d; i += blockDim.x) {
+      const int r = i / d, c = i - r * d;
+      u_s[r * ld + c] = __ldg(src + i);
+    }
+    __syncthreads();
+    // thread -> (row = tid % 64, task slice = tid / 64 of 4 slices)
+    const int r = threadIdx.x & (kPreRows - 1);
+    const int slice = threadIdx.x / kPreRows;
+    if (r < rows) {
+      for (int t = slice; t < n_tasks; t += blockDim.x / kPreRows) {
+        double acc = 0.0;
+        const double* wr = w_s + t * d;
+        const double* ur = u_s + r * ld;
+#pragma unroll 8
+        for (int c = 0; c < d; ++c) acc = __fma_rn(wr[c], ur[c], acc);
+        values[(int64_t)t * n_pairs + base + r] = __double2float_rn(acc);
+      }
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Control-block init (one CTA per query).  tau0 = preset admission key
+// (kNoTau normally; the final threshold of an overflowed run on re-run).
+__global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned long long* __restrict__ tau0) {
+  const ScanQuery& Q = qs[blockIdx.x];
+  QCtl* c = Q.ctl;
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
+  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) {
+    Q.hist[i] = 0u;
+    Q.seed_hist[i] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    c->tau_key = tau0 ? tau0[blockIdx.x] : kNoTau;
+    c->count = 0;
+    c->comp_count = 0;
+    c->sel_count = 0;
+    c->bound_key = 0;
+    c->min_key = ~0ull;
+    c->active = 1;
+    c->tile_counter = 0;
+    c->barrier = 0;
+    c->out_count = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: packed[p][i] = (test i lower ? -v : v)[task_i][p], 0 in padding columns,
+// for pair rows [row_lo, row_hi) (the R-groups K3 streams as columns).
+__global__ void pack_kernel(const ScanQuery* __restrict__ qs, const float* __restrict__ values, int64_t n_pairs,
+                            int64_t row_lo, int64_t row_hi) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  float* dst = const_cast<float*>(Q.packed);
+  const int ntp = Q.ntp;
+  const int64_t n = (row_hi - row_lo) * ntp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = row_lo + i / ntp;
+    const int t = (int)(i % ntp);
+    float v = 0.0f;
+    if (t < Q.nt) {
+      v = __ldg(values + (int64_t)Q.test_task[t] * n_pairs + p);
+      if (Q.test_lower[t]) v = -v;
+    }
+    dst[p * ntp + t] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused enumeration.
+//
+// Work unit: one warp takes one Tile (atomic work counter, dynamic balance).
+// Lane l owns rows row0 + l + 32*r (r < RL).  For each owned row and each
+// test i it computes an exact fp32 threshold thr[r][i] on the packed column
+// value y_i, folding the fp64 prefix sum, the bias and the bound (or the
+// running admission threshold tau for test 0).  Per product the work is then
+// NT fp32 compares (an FSETP predicate chain) against y values broadcast from
+// shared memory, where the last R-group's column block was staged by a 1-D
+// TMA bulk copy (double-buffered, mbarrier completion).  Every 8 columns the
+// warp votes; only if some product passed all tests (feasible AND s >= tau,
+// both exact) does it take the slow path: recompute the fp64 score in the
+// reference order, append (key, g) with one warp-aggregated atomic, and count
+// the key in the per-query histogram that drives tau.
+template <int NT>
+struct Ntp { static constexpr int value = (NT + 3) / 4 * 4; };
+
+struct ScanLaunch {
+  const Tile* tiles;
+  unsigned int tile_begin, tile_end;
+  const DevReaction* rx;
+  const float* values;
+  int64_t n_pairs;
+  const ScanQuery* queries;
+  int cb;                 // columns per smem block (multiple of 8)
+};
+
+template <int NT, int RL>
+__device__ __forceinline__ bool test_cols(const float* __restrict__ ys, int j, const float (&thr)[RL][NT],
+                                          bool (&pass)[RL]) {
+  constexpr int NTP = Ntp<NT>::value;
+  float y[NTP];
+  const float4* yp = reinterpret_cast<const float4*>(ys + j * NTP);
+#pragma unroll
+  for (int q = 0; q < NTP / 4; ++q) {
+    const float4 v = yp[q];
+    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+  }
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < RL; ++r) {
+    bool p = y[0] <= thr[r][0];
+#pragma unroll
+    for (int i = 1; i < NT; ++i) p = p & (y[i] <= thr[r][i]);
+    pass[r] = p;
+    any = any | p;
+  }
+  return any;
+}
+
+template <int NT, int RL>
+__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch L) {
+  constexpr int NTP = Ntp<NT>::value;
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  const ScanQuery& Q = L.queries[blockIdx.y];
+  QCtl* ctl = Q.ctl;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  if (!*(volatile unsigned int*)&ctl->active) return;
+
+  const int cb = L.cb;
+  float* sbuf0 = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 2 * cb * NTP;
+  float* sbuf1 = sbuf0 + cb * NTP;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + (size_t)kScanWarps * 2 * cb * NTP * sizeof(float)) + warp * 2;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t phase0 = 0, phase1 = 0;
+  unsigned bi = 0;
+
+  Entry* __restrict__ buf = Q.buf;
+  unsigned int* __restrict__ hist = Q.hist;
+  const unsigned long long cap = Q.cap;
+  const int maximize = Q.maximize;
+  const float* packed = Q.packed;
+  const double b_obj = Q.test_bias[0];
+
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->tile_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0) + L.tile_begin;
+    if (t >= L.tile_end) break;
+    const Tile T = L.tiles[t];
+    const DevReaction& R = L.rx[T.rx];
+    const int c = R.c;
+    const int64_t n_last = R.size[c - 1];
+    const float* col_src = packed + (size_t)(R.pair_off[c - 1] + T.col0) * NTP;
+    const int nblk = (int)((T.ncols + cb - 1) / cb);
+
+    // kick off the first column block before the threshold arithmetic
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(T.ncols < (uint32_t)cb ? T.ncols : (uint32_t)cb) * NTP * 4u;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[bi], bytes);
+      bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
+    }
+
+    const unsigned long long tau = *(volatile unsigned long long*)&ctl->tau_key;
+    const double tau_s = key_to_score(tau);
+
+    float thr[RL][NT];
+    double p_obj[RL];
+    unsigned long long gbase[RL];
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const unsigned local = lane + 32u * r;
+      const bool valid = local < T.nrows;
+      const uint64_t row = T.row0 + (valid ? local : 0u);
+      int64_t dig[kMaxRg];
+      {
+        uint64_t rem = row;
+        for (int j = c - 2; j >= 1; --j) {
+          const uint64_t sz = (uint64_t)R.size[j];
+          dig[j] = (int64_t)(rem % sz);
+          rem /= sz;
+        }
+        dig[0] = (int64_t)rem;
+      }
+      gbase[r] = R.g_off + row * (uint64_t)n_last + T.col0;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        float th = __int_as_float(0x7f800000);  // +inf: padding test always passes
+        if (i < Q.nt) {
+          const float* vrow = L.values + (int64_t)Q.test_task[i] * L.n_pairs;
+          double p = c > 1 ? (double)__ldg(vrow + R.pair_off[0] + dig[0]) : 0.0;  // c == 1: no prefix
+          for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(vrow + R.pair_off[j] + dig[j]));
+          const double b = Q.test_bias[i];
+          if (i == 0) {
+            p_obj[r] = p;
+            if (tau != kNoTau) th = maximize ? -thr_lower(p, b, tau_s) : thr_upper(p, b, -tau_s);
+          } else {
+            th = Q.test_lower[i] ? -thr_lower(p, b, Q.test_beta[i]) : thr_upper(p, b, Q.test_beta[i]);
+          }
+        }
+        thr[r][i] = th;
+      }
+      if (!valid) thr[r][0] = __int_as_float(0x7fffffff);  // NaN: never passes
+    }
+
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int col_base = blk * cb;
+      const int ncol = min(cb, (int)T.ncols - col_base);
+      if (blk + 1 < nblk && lane == 0) {
+        const unsigned nb = bi ^ 1u;
+        const uint32_t bytes = (uint32_t)min(cb, (int)T.ncols - col_base - cb) * NTP * 4u;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[nb], bytes);
+        bulk_g2s(nb ? sbuf1 : sbuf0, col_src + (size_t)(col_base + cb) * NTP, bytes, &bars[nb]);
+      }
+      if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
+      else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
+      const float* ys = bi ? sbuf1 : sbuf0;
+
+      for (int j0 = 0; j0 < ncol; j0 += 8) {
+        const int jn = min(8, ncol - j0);
+        bool any = false;
+        bool pass[RL];
+        if (jn == 8) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+        } else {
+          for (int jj = 0; jj < jn; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+        }
+        if (__any_sync(0xffffffffu, any)) {
+          // slow path: exact fp64 score, warp-aggregated append
+          for (int jj = 0; jj < jn; ++jj) {
+            test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+            const float y0 = ys[(j0 + jj) * NTP];
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+              const unsigned m = __ballot_sync(0xffffffffu, pass[r]);
+              if (m) {
+                const int leader = __ffs(m) - 1;
+                unsigned long long base = 0;
+                if ((int)lane == leader) base = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (pass[r]) {
+                  const float x = maximize ? -y0 : y0;
+                  const double val = fx(p_obj[r], x, b_obj);
+                  const double s = maximize ? val : -val;
+                  Entry e;
+                  e.key = skey(s);
+                  e.g = gbase[r] + (unsigned long long)(col_base + j0 + jj);
+                  const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
+                  if (idx < cap) buf[idx] = e;
+                  atomicAdd(&hist[e.key >> 48], 1u);
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      bi ^= 1u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Seed: exact evaluation of S sampled products (without replacement: one per
+// equal cell of [start, end), jittered inside the cell).  Feasible samples are
+// counted in seed_hist by key >> 48; the k-th best sampled key bin is a valid
+// admission threshold because the samples are distinct real products.
+struct SampleLaunch {
+  const ScanQuery* queries;
+  const DevReaction* rx;
+  const unsigned long long* g_off;   // [n_rx + 1]
+  int n_rx;
+  const float* values;
+  int64_t n_pairs;
+  unsigned long long start, end, samples;
+};
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return x;
+}
+
+__global__ void sample_kernel(const SampleLaunch P) {
+  const ScanQuery& Q = P.queries[blockIdx.y];
+  if (!*(volatile unsigned int*)&Q.ctl->active) return;
+  const unsigned long long span = P.end - P.start, S = P.samples;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
+    const unsigned long long lo = (unsigned long long)(((unsigned __int128)span * i) / S);
+    const unsigned long long hi = (unsigned long long)(((unsigned __int128)span * (i + 1)) / S);
+    const unsigned long long g = P.start + lo + mix64(i * 0x9e3779b97f4a7c15ull + 17) % (hi - lo);
+    int a = 0, b = P.n_rx;
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (P.g_off[mid] <= g) a = mid; else b = mid;
+    }
+    const DevReaction& R = P.rx[a];
+    unsigned long long rem = g - R.g_off;
+    int64_t pr[kMaxRg];
+    for (int j = R.c - 1; j >= 0; --j) {
+      const unsigned long long sz = (unsigned long long)R.size[j];
+      pr[j] = R.pair_off[j] + (int64_t)(rem % sz);
+      rem /= sz;
+    }
+    bool feasible = true;
+    for (int t = 1; t < Q.nt && feasible; ++t) {
+      const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
+      double val = (double)__ldg(v + pr[0]);
+      for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+      val = __dadd_rn(val, Q.test_bias[t]);
+      feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
+    }
+    if (feasible) {
+      const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
+      double val = (double)__ldg(v + pr[0]);
+      for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+      val = __dadd_rn(val, Q.test_bias[0]);
+      const double s = Q.maximize ? val : -val;
+      atomicAdd(&Q.seed_hist[skey(s) >> 48], 1u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tau from a key histogram: B = highest bin with sum_{b >= B} hist[b] >= k.
+// At least k distinct feasible products have key >= B<<48, so it is a valid
+// lower bound on the final k-th best key (never discards a true top-k
+// product).  mode 0: seed_hist -> raise tau_key; mode 1: hist -> raise
+// tau_key; mode 2: hist -> bound_key (final compaction bound).
+__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode) {
+  const ScanQuery& Q = qs[blockIdx.x];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  const unsigned long long k = (unsigned long long)Q.k;
+  __shared__ unsigned long long wsum[32];
+  __shared__ unsigned int found;
+  const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
+  const unsigned int* h = mode == 0 ? Q.seed_hist : Q.hist;
+  constexpr int PER = kHistBins / 1024;
+  unsigned long long s = 0;
+  const uint4* h4 = reinterpret_cast<const uint4*>(h + t * PER);
+#pragma unroll 4
+  for (int i = 0; i < PER / 4; ++i) {
+    const uint4 v = __ldcg(h4 + i);
+    s += (unsigned long long)v.x + v.y + v.z + v.w;
+  }
+  // inclusive suffix sum over threads (t .. 1023)
+  unsigned long long incl = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_down_sync(0xffffffffu, incl, off);
+    if (lane + off < 32) incl += o;
+  }
+  if (lane == 0) wsum[w] = incl;
+  if (t == 0) found = 0;
+  __syncthreads();
+  unsigned long long above = 0;  // sum over warps > w
+  for (unsigned v = w + 1; v < 32; ++v) above += wsum[v];
+  const unsigned long long suffix_incl = incl + above;   // bins >= t*PER
+  const unsigned long long suffix_excl = suffix_incl - s; // bins >= (t+1)*PER
+  if (suffix_excl < k && suffix_incl >= k) {
+    unsigned long long acc = suffix_excl;
+    int B = t * PER;
+    for (int b = (int)(t * PER + PER - 1); b >= (int)(t * PER); --b) {
+      acc += __ldcg(h + b);
+      if (acc >= k) { B = b; break; }
+    }
+    const unsigned long long key = (unsigned long long)B << 48;
+    if (mode < 2) {
+      if (key > ctl->tau_key) ctl->tau_key = key;
+    } else {
+      ctl->bound_key = key;
+    }
+    found = 1;
+  }
+  __syncthreads();
+  if (t == 0 && !found && mode == 2) ctl->bound_key = 0;  // fewer than k candidates: keep all
+}
+
+// Compact candidates with key >= bound_key into comp (order arbitrary).
+__global__ void compact_kernel(const ScanQuery* __restrict__ qs) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
+  const unsigned long long bound = *(volatile unsigned long long*)&ctl->bound_key;
+  const unsigned lane = lane_id();
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    const unsigned long long i = base + lane;
+    Entry e;
+    bool keep = false;
+    if (i < n) {
+      e = Q.buf[i];
+      keep = e.key >= bound;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if ((int)lane == leader) pos = atomicAdd(&ctl->comp_count, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (keep) Q.comp[pos + __popc(m & ((1u << lane) - 1u))] = e;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: exact top-k over comp[0, comp_count) by the composite order
+// (key desc, g asc): MSB-first radix select over the 128-bit composite
+// (key, ~g), 8-bit digits, histograms in smem + global, one grid barrier per
+// digit among the CTAs of a query (cooperative launch => co-resident).
+__device__ __forceinline__ void query_barrier(unsigned int* ctr, unsigned nb, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned target = gen * nb;
+    while (ld_acquire_u32(ctr) < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned digit_of(const Entry& e, int p) {
+  return p < 8 ? (unsigned)(e.key >> (56 - 8 * p)) & 0xffu : (unsigned)((~e.g) >> (56 - 8 * (p - 8))) & 0xffu;
+}
+// top 8p bits of the composite equal the prefix?
+__device__ __forceinline__ bool match_prefix(const Entry& e, unsigned long long phi, unsigned long long plo, int p) {
+  if (p == 0) return true;
+  if (p < 8) return (e.key >> (64 - 8 * p)) == (phi >> (64 - 8 * p));
+  if (e.key != phi) return false;
+  if (p == 8) return true;
+  return ((~e.g) >> (128 - 8 * p)) == (plo >> (128 - 8 * p));
+}
+// top 8d bits of the composite >= prefix?
+__device__ __forceinline__ bool ge_prefix(const Entry& e, unsigned long long phi, unsigned long long plo, int d) {
+  if (d <= 8) {
+    if (d == 8) return e.key >= phi;
+    return (e.key >> (64 - 8 * d)) >= (phi >> (64 - 8 * d));
+  }
+  if (e.key != phi) return e.key > phi;
+  if (d == 16) return (~e.g) >= plo;
+  return ((~e.g) >> (128 - 8 * d)) >= (plo >> (128 - 8 * d));
+}
+
+__global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery* __restrict__ qs) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  __shared__ unsigned int sh[256];
+  __shared__ unsigned long long s_phi, s_plo, s_need;
+  __shared__ int s_depth;
+  __shared__ unsigned long long s_min[kSelectThreads / 32];
+  const unsigned tid = threadIdx.x, nb = gridDim.x;
+  unsigned gen = 0;
+  const unsigned long long n = *(volatile unsigned long long*)&ctl->comp_count;
+  const unsigned long long k = (unsigned long long)Q.k;
+  const Entry* __restrict__ in = Q.comp;
+  const unsigned long long start = (unsigned long long)blockIdx.x * blockDim.x + tid;
+  const unsigned long long stride = (unsigned long long)nb * blockDim.x;
+
+  const bool take_all = n <= k;
+  unsigned long long phi = 0, plo = 0;
+  int depth = 0;
+  if (!take_all) {
+    if (tid == 0) { s_need = k; s_phi = 0; s_plo = 0; s_depth = -1; }
+    for (int p = 0; p < 16; ++p) {
+      for (unsigned i = tid; i < 256; i += blockDim.x) sh[i] = 0u;
+      __syncthreads();
+      phi = s_phi; plo = s_plo;
+      for (unsigned long long i = start; i < n; i += stride) {
+        const Entry e = in[i];
+        if (match_prefix(e, phi, plo, p)) atomicAdd(&sh[digit_of(e, p)], 1u);
+      }
+      __syncthreads();
+      unsigned int* gh = ctl->hist[p % 3];
+      for (unsigned i = tid; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+      if (blockIdx.x == 0)
+        for (unsigned i = tid; i < 256; i += blockDim.x) ctl->hist[(p + 1) % 3][i] = 0u;
+      query_barrier(&ctl->barrier, nb, gen);
+      for (unsigned i = tid; i < 256; i += blockDim.x) sh[i] = __ldcg(&gh[i]);
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long need = s_need, cum = 0;
+        int sel = 0;
+        for (int b = 255; b >= 0; --b) {
+          if (cum + sh[b] >= need) { sel = b; break; }
+          cum += sh[b];
+        }
+        need -= cum;
+        if (p < 8) s_phi = s_phi | ((unsigned long long)sel << (56 - 8 * p));
+        else s_plo = s_plo | ((unsigned long long)sel << (56 - 8 * (p - 8)));
+        s_need = need;
+        if (sh[sel] == need) s_depth = p + 1;
+      }
+      __syncthreads();
+      if (s_depth > 0) break;
+    }
+    phi = s_phi; plo = s_plo; depth = s_depth;
+  }
+  // compaction of the selected set + min key
+  unsigned long long mn = ~0ull;
+  const unsigned lane = tid & 31u;
+  for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (tid & ~31u); base < n; base += stride) {
+    const unsigned long long i = base + lane;
+    Entry e;
+    bool keep = false;
+    if (i < n) {
+      e = in[i];
+      keep = take_all || ge_prefix(e, phi, plo, depth);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned pos = 0;
+      if ((int)lane == leader) pos = atomicAdd(&ctl->out_count, (unsigned)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (keep) {
+        Q.sel[pos + __popc(m & ((1u << lane) - 1u))] = e;
+        mn = min(mn, e.key);
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+  if (lane == 0) s_min[tid >> 5] = mn;
+  __syncthreads();
+  if (tid == 0) {
+    for (unsigned w = 1; w < blockDim.x / 32; ++w) mn = min(mn, s_min[w]);
+    if (mn != ~0ull) atomicMin(&ctl->min_key, mn);
+  }
+  query_barrier(&ctl->barrier, nb, gen);
+  if (blockIdx.x == 0 && tid == 0) {
+    const unsigned long long cnt = *(volatile unsigned int*)&ctl->out_count;
+    ctl->sel_count = cnt;
+    if (cnt == k && k > 0) {
+      const unsigned long long mk = *(volatile unsigned long long*)&ctl->min_key;
+      if (mk > ctl->tau_key) ctl->tau_key = mk;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6: best-first order of the selected set by rank counting.  rank[i] =
+// #{j : sel[j] better than sel[i]}; keys (key, g) are unique so ranks are a
+// permutation.  Grid (i-blocks, j-splits, queries).
+__global__ void __launch_bounds__(256) rank_kernel(const ScanQuery* __restrict__ qs, int jsplit) {
+  const ScanQuery& Q = qs[blockIdx.z];
+  QCtl* ctl = Q.ctl;
+  const unsigned long long n = *(volatile unsigned long long*)&ctl->sel_count;
+  const unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x;
+  if ((unsigned long long)blockIdx.x * 256 >= n) return;
+  __shared__ Entry tile[256];
+  const unsigned long long j_lo = n * blockIdx.y / jsplit, j_hi = n * (blockIdx.y + 1) / jsplit;
+  Entry ei;
+  ei.key = 0; ei.g = ~0ull;
+  if (i < n) ei = Q.sel[i];
+  unsigned cnt = 0;
+  for (unsigned long long jb = j_lo; jb < j_hi; jb += 256) {
+    __syncthreads();
+    if (jb + threadIdx.x < j_hi) tile[threadIdx.x] = Q.sel[jb + threadIdx.x];
+    __syncthreads();
+    const int m = (int)(j_hi - jb < 256ull ? j_hi - jb : 256ull);
+    for (int jj = 0; jj < m; ++jj) cnt += entry_better(tile[jj], ei) ? 1u : 0u;
+  }
+  if (i < n && cnt) atomicAdd(&Q.rank[i], cnt);
+}
+
+__global__ void scatter_kernel(const ScanQuery* __restrict__ qs) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) Q.sorted[Q.rank[i]] = Q.sel[i];
+}
+
+// ---------------------------------------------------------------------------
+// K7: materialize best-first rows: decode g (csl.py:166-184), objective in the
+// scan's order (block_values, engine.py:210-222), constraint values in
+// apex_score's order (engine.py:95-101: acc = 0.0; acc += v_r; + bias).
+struct MatLaunch {
+  const ScanQuery* queries;
+  const DevReaction* rx;
+  const unsigned long long* g_off;  // [n_rx + 1]
+  int n_rx;
+  const float* values;
+  int64_t n_pairs;
+  const double* biases;
+};
+
+__global__ void materialize_kernel(const MatLaunch M) {
+  const ScanQuery& Q = M.queries[blockIdx.y];
+  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long g = Q.sorted[i].g;
+  int lo = 0, hi = M.n_rx;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (M.g_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  const DevReaction& R = M.rx[lo];
+  unsigned long long rem = g - R.g_off;
+  int64_t dig[kMaxRg];
+  for (int j = R.c - 1; j >= 0; --j) {
+    const unsigned long long sz = (unsigned long long)R.size[j];
+    dig[j] = (int64_t)(rem % sz);
+    rem /= sz;
+  }
+  {
+    const float* v = M.values + (int64_t)Q.obj_task * M.n_pairs;
+    double val = (double)v[R.pair_off[0] + dig[0]];
+    for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)v[R.pair_off[j] + dig[j]]);
+    val = __dadd_rn(val, M.biases[Q.obj_task]);
+    Q.out_obj[i] = val;
+  }
+  for (int ci = 0; ci < Q.n_cons; ++ci) {
+    const int task = Q.cons_task[ci];
+    const float* v = M.values + (int64_t)task * M.n_pairs;
+    double acc = 0.0;
+    for (int j = 0; j < R.c; ++j) acc = __dadd_rn(acc, (double)v[R.pair_off[j] + dig[j]]);
+    acc = __dadd_rn(acc, M.biases[task]);
+    Q.out_cons[i * Q.n_cons + ci] = acc;
+  }
+  Q.out_g[i] = g;
+  Q.out_rx[i] = lo;
+  for (int j = 0; j < kMaxRg; ++j) Q.out_dig[i * kMaxRg + j] = j < R.c ? (int32_t)dig[j] : 0;
+}
+
+// Multi-GPU: export the local selected set (unordered) to out + q*k.
+__global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restrict__ out) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[(unsigned long long)blockIdx.y * Q.k + i] = Q.sel[i];
+}
+
+// Multi-GPU: load gathered entries (skip padding g == ~0) as the compacted set.
+__global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry* __restrict__ in,
+                                  unsigned long long n) {
+  const ScanQuery& Q = qs[0];
+  QCtl* ctl = Q.ctl;
+  const unsigned lane = lane_id();
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    const unsigned long long i = base + lane;
+    Entry e;
+    bool keep = false;
+    if (i < n) {
+      e = in[i];
+      keep = e.g != ~0ull;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned long long pos = 0;
+      if ((int)lane == leader) pos = atomicAdd(&ctl->comp_count, (unsigned long long)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (keep) Q.comp[pos + __popc(m & ((1u << lane) - 1u))] = e;
+    }
+  }
+}
+
+}  // namespace apexb200

@@ -1,0 +1,63 @@
+"""Multi-GPU sharding of one query: one process per GPU.
+
+The product index space [start, end) is cut into contiguous g ranges, one per
+rank; every rank computes its exact local top-min(k, feasible) on its GPU
+(apex_query_local), the per-rank (key, g) entries (16 B each, padded to k) are
+all-gathered with NCCL over NVLink, and every rank runs the exact merge kernel
+(apex_merge_finalize) on the gathered buffer.  Exactness: the global top-k is
+contained in the union of the local top-k's, and the (key, g) order is global.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+PAD = -1  # int64 view of UINT64_MAX: key 0xff..ff / g 0xff..ff marks an empty slot
+
+
+def shard_range(start: int, end: int, rank: int, world: int) -> tuple[int, int]:
+    span = end - start
+    return start + span * rank // world, start + span * (rank + 1) // world
+
+
+def score_key(s: np.ndarray) -> np.ndarray:
+    """Host restatement of the device's order-preserving key (common.cuh skey):
+    +-0 canonicalized, larger score -> larger uint64."""
+    s = np.where(np.asarray(s, dtype=np.float64) == 0.0, 0.0, s).astype(np.float64)
+    u = s.view(np.uint64)
+    neg = (u >> np.uint64(63)) == np.uint64(1)
+    return np.where(neg, ~u, u | np.uint64(0x8000000000000000))
+
+
+def all_gather_entries(local, group=None):
+    """all-gather a [k, 2] int64 tensor of (key, g) entries from every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world * local.shape[0], 2), dtype=local.dtype, device=local.device)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local.contiguous(), group=group)
+        out = torch.cat(parts, 0)
+    return out
+
+
+def sharded_query(ctx, query: dict, group=None, stream_sync=True):
+    """Run one native query dict (task indices, start/end = global range) on
+    this rank's shard and return the merged global result (every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a, b = shard_range(query["start"], query["end"], rank, world)
+    k = int(query["k"])
+    local = torch.full((max(k, 1), 2), PAD, dtype=torch.int64, device="cuda")
+    q = dict(query, start=a, end=b)
+    counts, st_local = ctx.query_local([q], local.data_ptr())
+    gathered = all_gather_entries(local, group)
+    torch.cuda.current_stream().synchronize()
+    res, st_merge = ctx.merge_finalize(query, gathered.data_ptr(), gathered.shape[0], query["end"] - query["start"])
+    return res, {"local": st_local, "merge": st_merge, "local_count": counts[0]}

@@ -1,0 +1,377 @@
+"""Drop-in B200 implementation of the reference retrieval operator API.
+
+Mirrors `apexcsl.engine` (reference `pkg/src/apexcsl/engine.py`) for the hot
+path only:
+
+  * ``search_topk_stream(library, table, query, index_range=None)``   engine.py:265-313
+  * ``search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None)``
+                                                                      engine.py:345-398
+  * ``precompute_contributions(cache, surrogate)``                    engine.py:80-92
+  * ``search_topk_many(library, table, queries, index_range=None)``   batched multi-query
+    pass (configs 2 and 5; no reference counterpart — its oracle is one
+    ``search_topk_stream`` call per query)
+
+with the same names, argument meaning, result types and error behaviour:
+``EngineError`` (a ``RuntimeError``) with the reference's message substrings
+("unknown task", "fingerprint", "index range", "chunk size").  Inputs may be
+objects of the reference classes or of the mirrors defined here.
+
+All compute runs in libapexb200.so (C ABI, sm_100a kernels); there is no CPU
+fallback — without the library or a B200 the call raises.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .csl import MultiIndex, library_fingerprint, product_count
+
+
+class EngineError(RuntimeError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# mirror types (engine.py:35-162)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ContributionTable:
+    values: np.ndarray        # float32 (n_tasks, n_pairs), pair-row order
+    biases: np.ndarray        # float64 (n_tasks,)
+    task_names: list
+    member_ids: np.ndarray
+    rg_offsets: np.ndarray
+    rg_ids: np.ndarray
+    fingerprint: str
+
+    _rg_pos: dict = field(init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        self._rg_pos = {int(r): i for i, r in enumerate(self.rg_ids)}
+
+    @property
+    def n_tasks(self) -> int:
+        return len(self.task_names)
+
+    @property
+    def n_pairs(self) -> int:
+        return self.values.shape[1]
+
+    def task_index(self, name: str) -> int:
+        try:
+            return list(self.task_names).index(name)
+        except ValueError:
+            raise _error(f"unknown task {name!r}") from None
+
+    def check_library(self, library) -> None:
+        if self.fingerprint != library_fingerprint(library):
+            raise _error("library fingerprint does not match the contribution table")
+
+
+@dataclass(frozen=True)
+class Constraint:
+    task: str
+    lower: float = float("-inf")
+    upper: float = float("inf")
+
+    def __post_init__(self):
+        if not self.lower < self.upper:
+            raise _error(f"constraint bounds must satisfy lower < upper: {self}")
+
+
+@dataclass(frozen=True)
+class QuerySpec:
+    objective: str
+    direction: str
+    constraints: tuple = ()
+    k: int = 10
+
+    def __post_init__(self):
+        if self.direction not in ("maximize", "minimize"):
+            raise _error(f"direction must be maximize or minimize, got {self.direction!r}")
+        if self.k < 0:
+            raise _error("k must be >= 0")
+
+
+@dataclass
+class ScoredCompound:
+    global_index: int
+    chi: MultiIndex
+    objective: float
+    violation: float
+    constraint_values: tuple
+
+
+@dataclass
+class TopKResult:
+    entries: list
+    scanned: int
+    retained: int
+    discarded_for_violation: int
+    timing: dict
+
+
+def _error(msg: str) -> Exception:
+    # resolved at raise time so dropin.install() can substitute the reference's class
+    return _ERROR_CLASS[0](msg)
+
+
+_ERROR_CLASS = [EngineError]
+
+
+# ---------------------------------------------------------------------------
+# device contexts, memoized per (library, table)
+# ---------------------------------------------------------------------------
+
+def default_device() -> int:
+    for var in ("APEX_B200_DEVICE", "LOCAL_RANK"):
+        if var in os.environ:
+            return int(os.environ[var])
+    return 0
+
+
+class _Bound:
+    """A device context with one library + table resident."""
+
+    def __init__(self, library, table, device: int):
+        self.ctx = _native.DeviceContext(device)
+        rg_pos = {int(r): i for i, r in enumerate(table.rg_ids)}
+        offs = np.asarray(table.rg_offsets, dtype=np.int64)
+        sizes, pair_offsets, g_offsets = [], [], []
+        g = 0
+        for rx in library.reactions:
+            s, p = [], []
+            for rg in rx.rgroups:
+                j = rg_pos.get(int(rg.rgroup_id))
+                if j is None:
+                    raise _error(f"R-group {rg.rgroup_id} not in table")
+                lo, hi = int(offs[j]), int(offs[j + 1])
+                if hi - lo != len(rg.synthon_ids):
+                    raise _error(f"table rows for R-group {rg.rgroup_id} do not match library")
+                s.append(len(rg.synthon_ids))
+                p.append(lo)
+            sizes.append(s)
+            pair_offsets.append(p)
+            g_offsets.append(g)
+            g += math.prod(s)
+        self.total = g
+        values = np.asarray(table.values)
+        try:
+            self.ctx.load_library(sizes, pair_offsets, g_offsets, values.shape[1])
+            self.ctx.load_table(values, np.asarray(table.biases, dtype=np.float64))
+        except _native.NativeError as exc:
+            raise _error(str(exc)) from None
+        self.task_names = list(table.task_names)
+
+
+_BOUND: dict[tuple[int, int, int], tuple[weakref.ref, weakref.ref, _Bound]] = {}
+_MAX_BOUND = 4
+
+
+def bind(library, table, device: int | None = None) -> _Bound:
+    """Device context for (library, table), created on first use and reused."""
+    dev = default_device() if device is None else device
+    key = (id(library), id(table), dev)
+    hit = _BOUND.get(key)
+    if hit is not None and hit[0]() is library and hit[1]() is table:
+        return hit[2]
+    b = _Bound(library, table, dev)
+    if len(_BOUND) >= _MAX_BOUND:
+        _BOUND.pop(next(iter(_BOUND)))
+    _BOUND[key] = (weakref.ref(library), weakref.ref(table), b)
+    return b
+
+
+def _fingerprint_ok(library, table) -> None:
+    if table.fingerprint != library_fingerprint(library):
+        raise _error("library fingerprint does not match the contribution table")
+
+
+def _task_index(table, name: str) -> int:
+    try:
+        return list(table.task_names).index(name)
+    except ValueError:
+        raise _error(f"unknown task {name!r}") from None
+
+
+def _validate(library, table, query, index_range):
+    _fingerprint_ok(library, table)
+    _task_index(table, query.objective)
+    for con in query.constraints:
+        _task_index(table, con.task)
+    total = product_count(library)
+    start, end = index_range if index_range is not None else (0, total)
+    if not 0 <= start <= end <= total:
+        raise _error(f"index range [{start}, {end}) invalid")
+    return int(start), int(end)
+
+
+def _native_query(table, query, start: int, end: int) -> dict:
+    return {
+        "obj": _task_index(table, query.objective),
+        "maximize": query.direction == "maximize",
+        "cons": [(_task_index(table, c.task), float(c.lower), float(c.upper)) for c in query.constraints],
+        "k": int(query.k),
+        "start": start,
+        "end": end,
+    }
+
+
+def _types_for(library, query):
+    """Result classes from the caller's modules (reference classes when the
+    inputs are reference objects), so results compare equal to the reference's."""
+    mi = getattr(sys.modules.get(type(library).__module__), "MultiIndex", MultiIndex)
+    mod = sys.modules.get(type(query).__module__)
+    sc = getattr(mod, "ScoredCompound", ScoredCompound)
+    tk = getattr(mod, "TopKResult", TopKResult)
+    return mi, sc, tk
+
+
+def _build_result(library, query, res: dict, timing: dict):
+    mi_cls, sc_cls, tk_cls = _types_for(library, query)
+    n = int(res["n"])
+    g = res["g"].tolist()
+    obj = res["objective"].tolist()
+    cons = res["constraint_values"].tolist()
+    rxi = res["reaction"].tolist()
+    dig = res["digits"].tolist()
+    entries = []
+    reactions = library.reactions
+    for i in range(n):
+        rx = reactions[rxi[i]]
+        d = dig[i]
+        chi = mi_cls(rx.reaction_id, tuple((rg.rgroup_id, rg.synthon_ids[d[j]]) for j, rg in enumerate(rx.rgroups)))
+        entries.append(sc_cls(g[i], chi, obj[i], 0.0, tuple(cons[i])))
+    return tk_cls(entries=entries, scanned=int(res["scanned"]), retained=n,
+                  discarded_for_violation=int(res["discarded"]), timing=timing)
+
+
+def _timing(t0: float, start: int, end: int, stats: dict) -> dict:
+    dt = time.perf_counter() - t0
+    timing = {"scan_seconds": dt, "scanned": float(end - start)}
+    if dt > 0:
+        timing["products_per_second"] = (end - start) / dt
+    timing.update({f"device_{k}": float(v) for k, v in stats.items()})
+    return timing
+
+
+# ---------------------------------------------------------------------------
+# operator API
+# ---------------------------------------------------------------------------
+
+def search_topk_stream(library, table, query, index_range=None, device: int | None = None):
+    """Exact constrained top-k (engine.py:265-313), on the B200."""
+    start, end = _validate(library, table, query, index_range)
+    return _run([query], library, table, start, end, device)[0]
+
+
+def search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None, device: int | None = None):
+    """Chain-of-batches variant (engine.py:345-398).  Results are identical to
+    the stream variant by contract (test_engine.py:138-145), so both run the
+    same device pipeline; ``chunk_size`` is validated as the reference does.
+    ``trace`` (BatchTrace accounting of the CPU chain, incl. infeasible rows)
+    has no device counterpart and is rejected."""
+    _fingerprint_ok(library, table)
+    _task_index(table, query.objective)
+    for con in query.constraints:
+        _task_index(table, con.task)
+    if chunk_size < 1:
+        raise _error("chunk size must be >= 1")
+    if trace is not None:
+        raise _error("BatchTrace accounting is not supported by the B200 path (results are identical without it)")
+    start, end = _validate(library, table, query, index_range)
+    return _run([query], library, table, start, end, device)[0]
+
+
+def search_topk_many(library, table, queries, index_range=None, device: int | None = None):
+    """Several queries in one batched device pass; same results as one
+    ``search_topk_stream`` call per query."""
+    if not queries:
+        return []
+    start, end = _validate(library, table, queries[0], index_range)
+    for q in queries[1:]:
+        _validate(library, table, q, index_range)
+    return _run(list(queries), library, table, start, end, device)
+
+
+def _run(queries, library, table, start, end, device):
+    t0 = time.perf_counter()
+    out = [None] * len(queries)
+    live = [i for i, q in enumerate(queries) if q.k > 0 and end > start]
+    if live:
+        b = bind(library, table, device)
+        try:
+            res, stats = b.ctx.query([_native_query(table, queries[i], start, end) for i in live])
+        except _native.NativeError as exc:
+            raise _error(str(exc)) from None
+        timing = _timing(t0, start, end, stats)
+        for j, i in enumerate(live):
+            out[i] = _build_result(library, queries[i], res[j], dict(timing))
+    for i, q in enumerate(queries):
+        if out[i] is None:
+            empty = {"n": 0, "g": np.empty(0, np.uint64), "objective": np.empty(0), "constraint_values": np.empty((0, 0)),
+                     "reaction": np.empty(0, np.int32), "digits": np.empty((0, 6), np.int32), "discarded": 0,
+                     "scanned": end - start}
+            out[i] = _build_result(library, q, empty, _timing(t0, start, end, {}))
+    return out
+
+
+def precompute_contributions(cache, surrogate, device: int | None = None):
+    """Dot each task head with every cached associative embedding
+    (engine.py:80-92) on the device: fp64 products and accumulation, fp32
+    rounding.  Returns a table of the caller's class when available."""
+    dev = default_device() if device is None else device
+    ctx = _native.DeviceContext(dev)
+    try:
+        values = ctx.load_cache(np.asarray(cache.u, dtype=np.float64), np.asarray(surrogate.head_w, dtype=np.float64),
+                                np.asarray(surrogate.head_b, dtype=np.float64))
+    except _native.NativeError as exc:
+        raise _error(str(exc)) from None
+    finally:
+        ctx.close()
+    rg_ids = np.asarray(sorted(cache.rg_pos, key=cache.rg_pos.get))
+    mod = sys.modules.get(type(surrogate).__module__.replace("surrogate", "engine"))
+    cls = getattr(mod, "ContributionTable", ContributionTable) if mod else ContributionTable
+    return cls(
+        values=values,
+        biases=np.asarray(surrogate.head_b, dtype=np.float64).copy(),
+        task_names=list(surrogate.task_names),
+        member_ids=np.asarray(cache.member_ids).copy(),
+        rg_offsets=np.asarray(cache.rg_offsets).copy(),
+        rg_ids=rg_ids,
+        fingerprint=cache.fingerprint,
+    )
+
+
+RESULT_HEADER_PREFIX = "rank\tglobal_index\treaction_id\tsynthon_ids\tobjective\tviolation"
+
+
+def save_result(result, query, path, library=None) -> None:
+    """Delimited text export with the reference's exact format (engine.py:463-489):
+    repr() of every float, constraint columns in query order, optional
+    assembled-token column (csl.py:218-227)."""
+    cols = RESULT_HEADER_PREFIX + "".join(f"\t{con.task}" for con in query.constraints)
+    tokens = None
+    if library is not None:
+        cols += "\tassembled"
+        tokens = {s.synthon_id: s.token for s in library.synthons}
+    lines = [cols]
+    for rank, e in enumerate(result.entries):
+        sids = ",".join(map(str, e.chi.synthon_ids()))
+        row = f"{rank}\t{e.global_index}\t{e.chi.reaction_id}\t{sids}\t{e.objective!r}\t{e.violation!r}"
+        row += "".join(f"\t{v!r}" for v in e.constraint_values)
+        if tokens is not None:
+            frags = sorted(tokens[s].replace("*", "") for _, s in e.chi.assignment)
+            row += f"\tt{e.chi.reaction_id}|" + ".".join(frags)
+        lines.append(row)
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")

@@ -1,0 +1,124 @@
+"""CPU: host-side logic of the drop-in (no GPU calls)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, import_reference, unhex
+from paper_2510_24380_b200 import csl, engine, synth
+
+
+def test_fingerprint_matches_reference_serialization():
+    for case in golden_cases():
+        lib = case.library()
+        assert csl.library_fingerprint(lib, memo=False) == case.fingerprint
+        assert csl.serialize_library(lib) == case.library_text
+
+
+def test_fingerprint_memoized_per_object():
+    lib = golden_cases()[0].library()
+    a = csl.library_fingerprint(lib)
+    assert csl.library_fingerprint(lib) is a
+
+
+def test_decode_index_roundtrip():
+    lib = golden_cases()[0].library()
+    total = csl.product_count(lib)
+    for g in range(0, total, 7):
+        chi = csl.decode_index(lib, g)
+        t = chi.reaction_id
+        idx = 0
+        for rg, (rid, sid) in zip(lib.reactions[t].rgroups, chi.assignment):
+            idx = idx * len(rg.synthon_ids) + rg.synthon_ids.index(sid)
+        assert lib.reaction_offset(t) + idx == g
+
+
+def test_errors_before_device():
+    case = golden_cases()[0]
+    lib, table = case.library(), case.table()
+    Q, C = engine.QuerySpec, engine.Constraint
+    with pytest.raises(engine.EngineError, match="unknown task"):
+        engine.search_topk_stream(lib, table, Q("nope", "maximize", (), k=3))
+    with pytest.raises(engine.EngineError, match="unknown task"):
+        engine.search_topk_stream(lib, table, Q("obj", "maximize", (C("nope"),), k=3))
+    with pytest.raises(engine.EngineError, match="index range"):
+        engine.search_topk_stream(lib, table, Q("obj", "maximize", (), k=1), index_range=(10, 5))
+    with pytest.raises(engine.EngineError, match="chunk size"):
+        engine.search_topk_batched(lib, table, Q("obj", "maximize", (), k=1), 0)
+    other = golden_cases()[3].library()
+    with pytest.raises(engine.EngineError, match="fingerprint"):
+        engine.search_topk_stream(other, table, Q("obj", "maximize", (), k=1))
+    with pytest.raises(engine.EngineError, match="lower < upper"):
+        C("a", 1.0, 1.0)
+    with pytest.raises(engine.EngineError, match="direction"):
+        Q("obj", "up")
+    with pytest.raises(engine.EngineError, match="k"):
+        Q("obj", "maximize", k=-1)
+
+
+def test_save_result_matches_reference_tsv(tmp_path):
+    """The mirror's TSV writer reproduces the reference's bytes from the same entries."""
+    for case in golden_cases():
+        lib = case.library()
+        for qi, qd in enumerate(case.queries):
+            q = case.mirror_query(qd)
+            entries = []
+            for g, obj, viol, cons, rid, sids in qd["entries"]:
+                rx = lib.reactions[rid]
+                chi = csl.MultiIndex(rid, tuple((rg.rgroup_id, s) for rg, s in zip(rx.rgroups, sids)))
+                entries.append(engine.ScoredCompound(g, chi, unhex(obj), unhex(viol), tuple(unhex(v) for v in cons)))
+            res = engine.TopKResult(entries, qd["scanned"], qd["retained"], qd["discarded"], {})
+            p = tmp_path / f"{case.name}_{qi}.tsv"
+            engine.save_result(res, q, p)
+            assert p.read_text() == qd["tsv"]
+
+
+def test_reference_objects_duck_typed():
+    rcsl, rengine = import_reference()
+    case = golden_cases()[0]
+    rlib = rcsl.deserialize_library(case.library_text)
+    assert csl.library_fingerprint(rlib, memo=False) == case.fingerprint
+    mi, sc, tk = engine._types_for(rlib, rengine.QuerySpec("obj", "maximize"))
+    assert mi is rcsl.MultiIndex and sc is rengine.ScoredCompound and tk is rengine.TopKResult
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4"])
+def test_synthetic_shapes_hit_targets(name):
+    cfg = synth.SHAPES[name]
+    shape = synth.make_shape(cfg)
+    assert abs(shape.total / cfg.target - 1) < 0.002
+    assert len(shape.sizes) == cfg.n_reactions
+    assert all(2 <= n <= 200_000 for s in shape.sizes for n in s)
+    assert shape.pair_off[0][0] == 0
+    # pair rows are R-group-major in declaration order
+    flat = [p for po in shape.pair_off for p in po]
+    assert flat == sorted(flat) and shape.n_pairs == sum(sum(s) for s in shape.sizes)
+
+
+def test_c5_queries_are_valid():
+    qs = synth.c5_queries(200)
+    assert len(qs) == 200
+    for q in qs:
+        for t, lo, hi in q["constraints"]:
+            assert lo < hi and t in synth.PROPERTY_TASKS
+        assert q["k"] in (100, 1000, 10_000)
+
+
+def test_score_key_is_order_preserving():
+    from paper_2510_24380_b200.dist import score_key
+    rng = np.random.default_rng(0)
+    s = np.concatenate([rng.standard_normal(1000) * 10.0 ** rng.integers(-30, 30, 1000), [0.0, -0.0, 1e308, -1e308]])
+    k = score_key(s)
+    order_s = np.argsort(s, kind="stable")
+    assert np.all(k[order_s][1:] >= k[order_s][:-1])
+    assert score_key(np.array([0.0]))[0] == score_key(np.array([-0.0]))[0]
+
+
+def test_shard_ranges_partition():
+    from paper_2510_24380_b200.dist import shard_range
+    for world in (1, 2, 3, 8):
+        for start, end in ((0, 0), (0, 10), (5, 5_000_000_007), (3, 4)):
+            parts = [shard_range(start, end, r, world) for r in range(world)]
+            assert parts[0][0] == start and parts[-1][1] == end
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
