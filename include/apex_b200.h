@@ -105,7 +105,9 @@ typedef struct {
   int64_t candidates;      /* entries appended by the enumeration kernel */
   int64_t scan_launches;   /* enumeration launches (chunks, incl. retries) */
   int64_t kernel_launches; /* all kernels launched by the call */
-  int64_t retries;         /* chunk re-runs after candidate-buffer overflow */
+  int64_t retries;         /* re-runs after a candidate-buffer overflow */
+  int64_t h2d_bytes;       /* host->device bytes copied by the call */
+  int64_t d2h_bytes;       /* device->host bytes copied by the call */
 } apex_stats;
 
 /* Caller-allocated host output for one query; arrays sized for k entries
@@ -162,6 +164,15 @@ int apex_precompute_device(apex_ctx* ctx, const double* u_dev, int64_t n_pairs, 
  * launch) and materialize each result into results[i] (host buffers). */
 int apex_query(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,
                apex_result* results, apex_stats* stats);
+
+/* Asynchronous form of apex_query for queries sharing one range (k >= 1):
+ * enqueues the whole device pipeline on the ctx stream and returns without a
+ * host sync; results stay on the device until apex_query_fetch, which syncs,
+ * validates (re-running exactly after a candidate-buffer overflow) and copies
+ * the rows into caller-allocated host results.  A second apex_query_async
+ * before the fetch replaces the batch in flight. */
+int apex_query_async(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries, apex_stats* stats);
+int apex_query_fetch(apex_ctx* ctx, apex_result* results, apex_stats* stats);
 
 /* Multi-GPU local step: exact local top-min(k, feasible) of each query over its
  * [start, end), written UNSORTED into out_dev (device, capacity k entries per

@@ -25,7 +25,7 @@ APEX_OK, APEX_EINVAL, APEX_ERANGE, APEX_ETASK, APEX_ECUDA, APEX_ESTATE, APEX_ENO
 EXPORTED = (
     "apex_last_error", "apex_version", "apex_ctx_create", "apex_ctx_destroy", "apex_set_stream",
     "apex_load_library", "apex_load_table", "apex_load_cache", "apex_precompute_device", "apex_query",
-    "apex_query_local", "apex_merge_finalize", "apex_set_option", "apex_get_device_info",
+    "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds",
 )
 
@@ -77,6 +77,8 @@ class Stats(C.Structure):
         ("scan_launches", C.c_int64),
         ("kernel_launches", C.c_int64),
         ("retries", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -124,6 +126,8 @@ def load_library(path: Path | None = None):
         "apex_load_cache": ([vp, vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, vp], C.c_int),
         "apex_precompute_device": ([vp, vp, C.c_int64, C.c_int32, vp, C.c_int32, vp], C.c_int),
         "apex_query": ([vp, C.POINTER(QuerySpecC), C.c_int32, C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
+        "apex_query_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, C.POINTER(Stats)], C.c_int),
+        "apex_query_fetch": ([vp, C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_query_local": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.POINTER(C.c_int64), C.POINTER(Stats)],
                              C.c_int),
         "apex_merge_finalize": ([vp, C.POINTER(QuerySpecC), vp, C.c_int64, C.c_uint64, C.POINTER(ResultC),
@@ -239,9 +243,8 @@ class DeviceContext:
             specs[i].end = int(q["end"])
         return specs, keep
 
-    def query(self, queries: list[dict]) -> tuple[list[dict], dict]:
-        """Run a batch; returns per-query numpy result arrays and the stats."""
-        specs, keep = self._specs(queries)
+    @staticmethod
+    def _result_buffers(queries):
         results = (ResultC * len(queries))()
         bufs = []
         for i, q in enumerate(queries):
@@ -260,8 +263,10 @@ class DeviceContext:
             results[i].constraint_values = b["constraint_values"].ctypes.data_as(C.POINTER(C.c_double))
             results[i].reaction = b["reaction"].ctypes.data_as(C.POINTER(C.c_int32))
             results[i].digits = b["digits"].ctypes.data_as(C.POINTER(C.c_int32))
-        st = Stats()
-        _check(self.lib.apex_query(self._ctx, specs, len(queries), results, C.byref(st)))
+        return results, bufs
+
+    @staticmethod
+    def _unpack(results, bufs):
         out = []
         for i, b in enumerate(bufs):
             n = results[i].n
@@ -275,8 +280,32 @@ class DeviceContext:
                 "discarded": results[i].discarded,
                 "scanned": results[i].scanned,
             })
+        return out
+
+    def query(self, queries: list[dict]) -> tuple[list[dict], dict]:
+        """Run a batch; returns per-query numpy result arrays and the stats."""
+        specs, keep = self._specs(queries)
+        results, bufs = self._result_buffers(queries)
+        st = Stats()
+        _check(self.lib.apex_query(self._ctx, specs, len(queries), results, C.byref(st)))
         del keep
-        return out, st.as_dict()
+        return self._unpack(results, bufs), st.as_dict()
+
+    def query_async(self, queries: list[dict]) -> dict:
+        """Enqueue a batch (one shared range, k >= 1) without a host sync."""
+        specs, keep = self._specs(queries)
+        st = Stats()
+        _check(self.lib.apex_query_async(self._ctx, specs, len(queries), C.byref(st)))
+        self._inflight = queries
+        del keep
+        return st.as_dict()
+
+    def query_fetch(self) -> tuple[list[dict], dict]:
+        queries = self._inflight
+        results, bufs = self._result_buffers(queries)
+        st = Stats()
+        _check(self.lib.apex_query_fetch(self._ctx, results, C.byref(st)))
+        return self._unpack(results, bufs), st.as_dict()
 
     def query_local(self, queries: list[dict], out_dev_ptr: int) -> tuple[list[int], dict]:
         specs, keep = self._specs(queries)

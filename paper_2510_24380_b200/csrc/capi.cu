@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <random>
 #include <string>
@@ -110,9 +111,40 @@ struct Plan {
   DBuf d_tiles;
   int64_t pair_lo = 0, pair_hi = 0;  // last-R-group pair rows touched
   uint64_t stamp = 0;
+  ~Plan() { d_tiles.release(); }
 };
 
 size_t out_bytes(int64_t k, int m) { return (size_t)k * (8 + 8 + 8 * (size_t)m + 4 + 4 * kMaxRg); }
+
+// Tests of a query (DESIGN.md §3): test 0 = objective admission, then for every
+// task the tightest finite upper bound and the tightest finite lower bound
+// (x >= each lower <=> x >= max lower; monotone, so merging is exact).
+struct QTests {
+  int nt = 0;
+  int task[kMaxTests];
+  int lower[kMaxTests];
+  double beta[kMaxTests];
+};
+
+struct RunStats {
+  int64_t launches = 0, scans = 0, retries = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  float ms[8] = {};
+  float scan_kernel_ms = 0;
+};
+
+// The last enqueued batch: queries sharing one range (deep copies).
+struct Batch {
+  std::vector<apex_query_spec> qs;
+  std::vector<std::vector<apex_constraint>> cons;
+  std::vector<QTests> tests;
+  int nq = 0, NT = 0, rl = 0, ntp = 0;
+  int64_t k_max = 0;
+  bool finalize = false;
+  Plan* plan = nullptr;
+  bool pending = false;
+  RunStats st;
+};
 
 }  // namespace
 
@@ -139,9 +171,12 @@ struct apex_ctx {
   std::vector<Slot> slots;
   DBuf d_queries, d_tau0;
   HBuf h_queries, h_ctl, h_out, h_tau0;
-  std::vector<Plan> plans;
+  std::vector<std::unique_ptr<Plan>> plans;
   uint64_t stamp = 0;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t upload_ev = nullptr;
+  std::vector<ScanQuery> uploaded;   // last ScanQuery array copied to d_queries
+  Batch batch;
   // options
   int64_t opt_cap = 1 << 22;        // candidate buffer entries per query (minimum)
   int64_t opt_cb = 64;              // columns per smem block
@@ -151,6 +186,7 @@ struct apex_ctx {
   int64_t opt_chunk_min = 1 << 26;  // ranges at least this large are scanned in two chunks
   int64_t opt_tile_products = 0;    // target products per tile (0 = auto)
   int64_t opt_select_ctas = 16;     // CTAs per query in the select kernel
+  int64_t opt_force_upload = 0;     // re-upload query descriptors on every call
 };
 
 namespace {
@@ -174,13 +210,14 @@ int check_ctx(apex_ctx* c, bool need_table) {
 // sample of the range (used for the first chunk's threshold).
 int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) {
   for (auto& p : c->plans) {
-    if (p.start == start && p.end == end && p.rows == rows) {
-      p.stamp = ++c->stamp;
-      out = &p;
+    if (p->start == start && p->end == end && p->rows == rows) {
+      p->stamp = ++c->stamp;
+      out = p.get();
       return APEX_OK;
     }
   }
-  Plan P;
+  auto owned = std::make_unique<Plan>();
+  Plan& P = *owned;
   P.start = start;
   P.end = end;
   P.rows = rows;
@@ -240,25 +277,18 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) 
   // keep a small cache
   if (c->plans.size() >= 8) {
     auto it = std::min_element(c->plans.begin(), c->plans.end(),
-                               [](const Plan& a, const Plan& b) { return a.stamp < b.stamp; });
-    it->d_tiles.release();
+                               [](const std::unique_ptr<Plan>& a, const std::unique_ptr<Plan>& b) {
+                                 return a->stamp < b->stamp;
+                               });
+    if (c->batch.plan == it->get()) c->batch.plan = nullptr;
+    (*it)->d_tiles.release();
     c->plans.erase(it);
   }
   P.stamp = ++c->stamp;
-  c->plans.push_back(std::move(P));
-  out = &c->plans.back();
+  c->plans.push_back(std::move(owned));
+  out = c->plans.back().get();
   return APEX_OK;
 }
-
-// Tests of a query (DESIGN.md §3): test 0 = objective admission, then for every
-// task the tightest finite upper bound and the tightest finite lower bound
-// (x >= each lower <=> x >= max lower; monotone, so merging is exact).
-struct QTests {
-  int nt = 0;
-  int task[kMaxTests];
-  int lower[kMaxTests];
-  double beta[kMaxTests];
-};
 
 int make_tests(const apex_ctx* c, const apex_query_spec& q, QTests& T) {
   T.nt = 1;
@@ -322,42 +352,44 @@ int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
   return APEX_OK;
 }
 
-struct RunStats {
-  int64_t launches = 0, scans = 0, retries = 0;
-  float ms[8] = {};
-  float scan_kernel_ms = 0;
-};
+// ---------------------------------------------------------------------------
+// Batch lifecycle: prepare (host: tests, plan, workspaces, descriptor upload),
+// enqueue (device pipeline, no host sync), check (one sync: overflow check and
+// exact re-run with the final bound if the candidate buffer overflowed).
 
-// Launch the whole device pipeline for nq queries sharing one range; results
-// stay on device (sel / sorted / out of each slot).  finalize: order +
-// materialize (single-GPU path); otherwise stop after select (local path).
-int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, RunStats& st) {
-  const uint64_t start = qs[0].start, end = qs[0].end, span = end - start;
-  std::vector<QTests> tests(nq);
-  int nt_max = 1;
-  int64_t k_max = 0;
+int prepare_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize) {
+  Batch& B = c->batch;
+  B.qs.assign(qs, qs + nq);
+  B.cons.assign(nq, {});
   for (int i = 0; i < nq; ++i) {
-    APEX_TRY(make_tests(c, qs[i], tests[i]));
-    nt_max = std::max(nt_max, tests[i].nt);
-    k_max = std::max<int64_t>(k_max, qs[i].k);
+    B.cons[i].assign(qs[i].constraints, qs[i].constraints + qs[i].n_constraints);
+    B.qs[i].constraints = B.cons[i].data();
+  }
+  B.nq = nq;
+  B.finalize = finalize;
+  B.tests.assign(nq, QTests());
+  B.st = RunStats();
+  int nt_max = 1;
+  B.k_max = 0;
+  for (int i = 0; i < nq; ++i) {
+    APEX_TRY(make_tests(c, qs[i], B.tests[i]));
+    nt_max = std::max(nt_max, B.tests[i].nt);
+    B.k_max = std::max<int64_t>(B.k_max, qs[i].k);
     if (qs[i].n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
   }
-  const int NT = kernel_nt(nt_max);
-  if (NT < 0) return set_err(APEX_ELIMIT, "too many tests");
-  const int ntp = (NT + 3) / 4 * 4;
-  int rl = (int)c->opt_rl;
-  if (rl != 1 && rl != 2) rl = NT <= 8 ? 2 : 1;
-  const int rows = 32 * rl;
-  Plan* plan = nullptr;
-  APEX_TRY(build_plan(c, start, end, rows, plan));
+  B.NT = kernel_nt(nt_max);
+  if (B.NT < 0) return set_err(APEX_ELIMIT, "too many tests");
+  B.ntp = (B.NT + 3) / 4 * 4;
+  B.rl = (int)c->opt_rl;
+  if (B.rl != 1 && B.rl != 2) B.rl = B.NT <= 8 ? 2 : 1;
+  APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, B.plan));
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
-  // workspaces
   for (int i = 0; i < nq; ++i) {
     Slot& S = c->slots[i];
     const int64_t k = qs[i].k;
     const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
-    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp * sizeof(float)));
+    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * B.ntp * sizeof(float)));
     APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
@@ -368,12 +400,11 @@ int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, Run
     APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
     APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
   }
-  APEX_TRY(c->d_queries.ensure(nq * sizeof(ScanQuery)));
-  APEX_TRY(c->h_queries.ensure(nq * sizeof(ScanQuery)));
-  ScanQuery* hq = c->h_queries.as<ScanQuery>();
+  std::vector<ScanQuery> hq(nq);
   for (int i = 0; i < nq; ++i) {
     Slot& S = c->slots[i];
     const apex_query_spec& q = qs[i];
+    const QTests& T = B.tests[i];
     ScanQuery& Q = hq[i];
     std::memset(&Q, 0, sizeof(Q));
     Q.packed = S.packed.as<float>();
@@ -387,16 +418,16 @@ int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, Run
     Q.ctl = S.ctl.as<QCtl>();
     Q.cap = S.buf.bytes / sizeof(Entry);
     Q.k = q.k;
-    Q.nt = tests[i].nt;
-    Q.ntp = ntp;
+    Q.nt = T.nt;
+    Q.ntp = B.ntp;
     Q.maximize = q.maximize ? 1 : 0;
     Q.obj_task = q.objective_task;
     Q.n_cons = q.n_constraints;
-    for (int t = 0; t < tests[i].nt; ++t) {
-      Q.test_task[t] = tests[i].task[t];
-      Q.test_lower[t] = tests[i].lower[t];
-      Q.test_beta[t] = tests[i].beta[t];
-      Q.test_bias[t] = c->biases[tests[i].task[t]];
+    for (int t = 0; t < T.nt; ++t) {
+      Q.test_task[t] = T.task[t];
+      Q.test_lower[t] = T.lower[t];
+      Q.test_beta[t] = T.beta[t];
+      Q.test_bias[t] = c->biases[T.task[t]];
     }
     for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
     const int64_t kk = std::max<int64_t>(q.k, 1);
@@ -407,169 +438,192 @@ int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, Run
     Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
     Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
   }
-  cudaStream_t s = c->stream;
-  APEX_CU(cudaEventRecord(c->ev[0], s));
-  APEX_CU(cudaMemcpyAsync(c->d_queries.p, hq, nq * sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
-  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  // upload the descriptors only when they changed (pinned staging is reused:
+  // wait for the previous copy out of it first)
+  const size_t bytes = nq * sizeof(ScanQuery);
+  if (c->opt_force_upload || c->uploaded.size() != (size_t)nq ||
+      std::memcmp(c->uploaded.data(), hq.data(), bytes) != 0) {
+    APEX_CU(cudaEventSynchronize(c->upload_ev));
+    APEX_TRY(c->d_queries.ensure(bytes));
+    APEX_TRY(c->h_queries.ensure(bytes));
+    std::memcpy(c->h_queries.p, hq.data(), bytes);
+    APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, bytes, cudaMemcpyHostToDevice, c->stream));
+    APEX_CU(cudaEventRecord(c->upload_ev, c->stream));
+    c->uploaded = hq;
+    B.st.h2d_bytes += (int64_t)bytes;
+  }
+  return APEX_OK;
+}
 
-  // retry loop: re-run with a preset threshold after a candidate overflow
-  std::vector<unsigned long long> tau0(nq, kNoTau);
-  bool use_tau0 = false;
-  for (int attempt = 0;; ++attempt) {
-    if (use_tau0) {
-      APEX_TRY(c->d_tau0.ensure(nq * sizeof(unsigned long long)));
-      APEX_TRY(c->h_tau0.ensure(nq * sizeof(unsigned long long)));
-      std::memcpy(c->h_tau0.p, tau0.data(), nq * sizeof(unsigned long long));
-      APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    }
-    init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, use_tau0 ? c->d_tau0.as<unsigned long long>() : nullptr);
-    ++st.launches;
-    // K2 pack
-    if (plan->pair_hi > plan->pair_lo) {
-      const int64_t n = (plan->pair_hi - plan->pair_lo) * ntp;
-      const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
-      pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo,
-                                                   plan->pair_hi);
-      ++st.launches;
-    }
-    APEX_CU(cudaEventRecord(c->ev[1], s));
-    // seed threshold from exact samples
-    if (!use_tau0) {
-      uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
-                                       : (uint64_t)std::min<int64_t>(1 << 21, std::max<int64_t>(1 << 18, 64 * k_max));
-      S = std::min<uint64_t>(S, span);
-      if (S > 0 && k_max > 0) {
-        SampleLaunch P;
-        P.queries = dq;
-        P.rx = c->d_rx.as<DevReaction>();
-        P.g_off = c->d_goff.as<unsigned long long>();
-        P.n_rx = (int)c->rx.size();
-        P.values = c->d_values.as<float>();
-        P.n_pairs = c->n_pairs;
-        P.start = start;
-        P.end = end;
-        P.samples = S;
-        const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
-        sample_kernel<<<dim3(blocks, nq), 256, 0, s>>>(P);
-        tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
-        st.launches += 2;
-      }
-    }
-    APEX_CU(cudaEventRecord(c->ev[2], s));
-    // K3 enumeration chunks
-    ScanFn fn = pick_scan(NT, rl);
-    if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
-    const int cb = (int)c->opt_cb;
-    const size_t smem = scan_smem(NT, cb);
-    int occ = 0;
-    APEX_TRY(scan_occupancy(fn, smem, &occ));
-    const size_t n_tiles = plan->tiles.size();
-    std::vector<size_t> bounds;  // chunk ends in tile indices
-    if (span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && n_tiles > 1) {
-      const uint64_t first = span / (uint64_t)c->opt_chunk_div;
-      size_t i1 = (size_t)(std::lower_bound(plan->prefix.begin(), plan->prefix.end(), first) - plan->prefix.begin());
-      i1 = std::min(std::max<size_t>(i1, 1), n_tiles);
-      bounds.push_back(i1);
-    }
-    bounds.push_back(n_tiles);
-    size_t tb = 0;
-    for (size_t ci = 0; ci < bounds.size(); ++ci) {
-      const size_t te = bounds[ci];
-      if (te > tb) {
-        ScanLaunch L;
-        L.tiles = plan->d_tiles.as<Tile>();
-        L.tile_begin = (unsigned)tb;
-        L.tile_end = (unsigned)te;
-        L.rx = c->d_rx.as<DevReaction>();
-        L.values = c->d_values.as<float>();
-        L.n_pairs = c->n_pairs;
-        L.queries = dq;
-        L.cb = cb;
-        const int64_t blocks =
-            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
-        APEX_CU(cudaEventRecord(c->ev[6], s));
-        fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(L);
-        APEX_CU(cudaGetLastError());
-        APEX_CU(cudaEventRecord(c->ev[7], s));
-        ++st.launches;
-        ++st.scans;
-        if (ci + 1 < bounds.size()) {
-          // reset the work counter and raise tau from the candidates so far
-          tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);
-          st.launches += 1;
-        }
-        for (int i = 0; i < nq; ++i) {
-          APEX_CU(cudaMemsetAsync(&c->slots[i].ctl.as<QCtl>()->tile_counter, 0, sizeof(unsigned), s));
-        }
-      }
-      tb = te;
-    }
-    APEX_CU(cudaEventRecord(c->ev[3], s));
-    // final bound, compaction, exact select
-    tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
-    {
-      const int blocks = c->sm_count * 4;
-      compact_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq);
-    }
-    st.launches += 2;
-    {
-      int occ_sel = 0;
-      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
-      const int resident = std::max(1, occ_sel * c->sm_count);
-      int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / nq));
-      if (per_q * nq > resident) return set_err(APEX_ELIMIT, "too many queries in one batch for the select kernel");
-      void* args[] = {(void*)&dq};
-      APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, nq), dim3(kSelectThreads), args, 0, s));
-      ++st.launches;
-    }
-    APEX_CU(cudaEventRecord(c->ev[4], s));
-    if (finalize && k_max > 0) {
-      for (int i = 0; i < nq; ++i)
-        APEX_CU(cudaMemsetAsync(c->slots[i].rank.p, 0, std::max<int64_t>(qs[i].k, 1) * sizeof(unsigned), s));
-      const int ib = (int)((k_max + 255) / 256);
-      int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
-      rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
-      scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
-      MatLaunch M;
-      M.queries = dq;
-      M.rx = c->d_rx.as<DevReaction>();
-      M.g_off = c->d_goff.as<unsigned long long>();
-      M.n_rx = (int)c->rx.size();
-      M.values = c->d_values.as<float>();
-      M.n_pairs = c->n_pairs;
-      M.biases = c->d_biases.as<double>();
-      materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
-      st.launches += 3;
-    }
-    APEX_CU(cudaGetLastError());
-    APEX_CU(cudaEventRecord(c->ev[5], s));
-    // read control blocks (overflow check) — one sync per call
-    APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
-    for (int i = 0; i < nq; ++i)
-      APEX_CU(cudaMemcpyAsync(c->h_ctl.as<QCtl>() + i, c->slots[i].ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
+// Enqueue the device pipeline of the prepared batch.  tau0: preset admission
+// keys (re-run after an overflow), or nullptr.
+int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
+  Batch& B = c->batch;
+  RunStats& st = B.st;
+  const int nq = B.nq;
+  Plan* plan = B.plan;
+  const uint64_t start = B.qs[0].start, end = B.qs[0].end, span = end - start;
+  cudaStream_t s = c->stream;
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  APEX_CU(cudaEventRecord(c->ev[0], s));
+  if (tau0) {
+    APEX_TRY(c->d_tau0.ensure(nq * sizeof(unsigned long long)));
+    APEX_TRY(c->h_tau0.ensure(nq * sizeof(unsigned long long)));
     APEX_CU(cudaStreamSynchronize(s));
+    std::memcpy(c->h_tau0.p, tau0, nq * sizeof(unsigned long long));
+    APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    st.h2d_bytes += nq * 8;
+  }
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr);
+  ++st.launches;
+  // K2 pack
+  if (plan->pair_hi > plan->pair_lo) {
+    const int64_t n = (plan->pair_hi - plan->pair_lo) * B.ntp;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+    pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
+    ++st.launches;
+  }
+  APEX_CU(cudaEventRecord(c->ev[1], s));
+  // seed threshold from exact samples
+  if (!tau0) {
+    uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
+                                     : (uint64_t)std::min<int64_t>(1 << 21, std::max<int64_t>(1 << 18, 64 * B.k_max));
+    S = std::min<uint64_t>(S, span);
+    if (S > 0) {
+      SampleLaunch P;
+      P.queries = dq;
+      P.rx = c->d_rx.as<DevReaction>();
+      P.g_off = c->d_goff.as<unsigned long long>();
+      P.n_rx = (int)c->rx.size();
+      P.values = c->d_values.as<float>();
+      P.n_pairs = c->n_pairs;
+      P.start = start;
+      P.end = end;
+      P.samples = S;
+      const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
+      sample_kernel<<<dim3(blocks, nq), 256, 0, s>>>(P);
+      tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
+      st.launches += 2;
+    }
+  }
+  APEX_CU(cudaEventRecord(c->ev[2], s));
+  // K3 enumeration chunks
+  ScanFn fn = pick_scan(B.NT, B.rl);
+  if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
+  const int cb = (int)c->opt_cb;
+  const size_t smem = scan_smem(B.NT, cb);
+  int occ = 0;
+  APEX_TRY(scan_occupancy(fn, smem, &occ));
+  const size_t n_tiles = plan->tiles.size();
+  std::vector<size_t> bounds;  // chunk ends in tile indices
+  if (span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && n_tiles > 1) {
+    const uint64_t first = span / (uint64_t)c->opt_chunk_div;
+    size_t i1 = (size_t)(std::lower_bound(plan->prefix.begin(), plan->prefix.end(), first) - plan->prefix.begin());
+    i1 = std::min(std::max<size_t>(i1, 1), n_tiles);
+    bounds.push_back(i1);
+  }
+  bounds.push_back(n_tiles);
+  size_t tb = 0;
+  st.scan_kernel_ms = 0;
+  for (size_t ci = 0; ci < bounds.size(); ++ci) {
+    const size_t te = bounds[ci];
+    if (te > tb) {
+      ScanLaunch L;
+      L.tiles = plan->d_tiles.as<Tile>();
+      L.tile_begin = (unsigned)tb;
+      L.tile_end = (unsigned)te;
+      L.rx = c->d_rx.as<DevReaction>();
+      L.values = c->d_values.as<float>();
+      L.n_pairs = c->n_pairs;
+      L.queries = dq;
+      L.cb = cb;
+      const int64_t blocks =
+          std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
+      if (ci == 0) APEX_CU(cudaEventRecord(c->ev[6], s));
+      fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(L);
+      APEX_CU(cudaGetLastError());
+      ++st.launches;
+      ++st.scans;
+      if (ci + 1 < bounds.size()) {
+        tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);  // raise tau from the candidates so far
+        ++st.launches;
+      }
+      for (int i = 0; i < nq; ++i)
+        APEX_CU(cudaMemsetAsync(&c->slots[i].ctl.as<QCtl>()->tile_counter, 0, sizeof(unsigned), s));
+    }
+    tb = te;
+  }
+  APEX_CU(cudaEventRecord(c->ev[7], s));
+  APEX_CU(cudaEventRecord(c->ev[3], s));
+  // final bound, compaction, exact select
+  tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
+  compact_kernel<<<dim3(c->sm_count * 4, nq), 256, 0, s>>>(dq);
+  st.launches += 2;
+  {
+    int occ_sel = 0;
+    APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
+    const int resident = std::max(1, occ_sel * c->sm_count);
+    const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / nq));
+    if (per_q * nq > resident) return set_err(APEX_ELIMIT, "too many queries in one batch for the select kernel");
+    void* args[] = {(void*)&dq};
+    APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, nq), dim3(kSelectThreads), args, 0, s));
+    ++st.launches;
+  }
+  APEX_CU(cudaEventRecord(c->ev[4], s));
+  if (B.finalize) {
+    for (int i = 0; i < nq; ++i)
+      APEX_CU(cudaMemsetAsync(c->slots[i].rank.p, 0, std::max<int64_t>(B.qs[i].k, 1) * sizeof(unsigned), s));
+    const int ib = (int)((B.k_max + 255) / 256);
+    const int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
+    rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
+    scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+    MatLaunch M;
+    M.queries = dq;
+    M.rx = c->d_rx.as<DevReaction>();
+    M.g_off = c->d_goff.as<unsigned long long>();
+    M.n_rx = (int)c->rx.size();
+    M.values = c->d_values.as<float>();
+    M.n_pairs = c->n_pairs;
+    M.biases = c->d_biases.as<double>();
+    materialize_kernel<<<dim3((unsigned)((B.k_max + 127) / 128), nq), 128, 0, s>>>(M);
+    st.launches += 3;
+  }
+  APEX_CU(cudaGetLastError());
+  APEX_CU(cudaEventRecord(c->ev[5], s));
+  // control blocks to host (read by check_batch)
+  APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
+  for (int i = 0; i < nq; ++i)
+    APEX_CU(cudaMemcpyAsync(c->h_ctl.as<QCtl>() + i, c->slots[i].ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
+  st.d2h_bytes += nq * (int64_t)sizeof(QCtl);
+  B.pending = true;
+  return APEX_OK;
+}
+
+// Sync, detect candidate-buffer overflow, re-run exactly if needed.
+int check_batch(apex_ctx* c) {
+  Batch& B = c->batch;
+  if (!B.pending) return set_err(APEX_ESTATE, "no query batch in flight");
+  const int nq = B.nq;
+  std::vector<unsigned long long> tau0(nq);
+  for (int attempt = 0;; ++attempt) {
+    APEX_CU(cudaStreamSynchronize(c->stream));
     bool overflow = false;
     for (int i = 0; i < nq; ++i) {
       const QCtl& C = c->h_ctl.as<QCtl>()[i];
-      const unsigned long long cap = hq[i].cap;
-      if (C.count > cap) {
-        overflow = true;
-        tau0[i] = std::max<unsigned long long>(C.bound_key, C.tau_key);
-      } else {
-        tau0[i] = kNoTau;
-      }
+      const unsigned long long cap = c->uploaded[i].cap;
+      if (C.count > cap) overflow = true;
+      tau0[i] = std::max<unsigned long long>(C.bound_key, C.tau_key);
     }
     if (!overflow) break;
-    if (attempt >= 3) return set_err(APEX_ELIMIT, "candidate buffer overflow persists (massive exact ties?)");
-    ++st.retries;
-    use_tau0 = true;
-    // queries that did not overflow re-run too (cheap, keeps the batch uniform);
-    // give them their own final threshold as well
-    for (int i = 0; i < nq; ++i) {
-      const QCtl& C = c->h_ctl.as<QCtl>()[i];
-      if (tau0[i] == kNoTau) tau0[i] = C.bound_key;
-      if (attempt >= 1) {
-        // second overflow: grow the buffers
+    if (attempt >= 3) {
+      B.pending = false;
+      return set_err(APEX_ELIMIT, "candidate buffer overflow persists (massive exact ties?)");
+    }
+    ++B.st.retries;
+    if (attempt >= 1) {
+      // repeated overflow (e.g. huge exact ties in one key bin): grow the buffers
+      std::vector<ScanQuery> hq = c->uploaded;
+      for (int i = 0; i < nq; ++i) {
         Slot& S = c->slots[i];
         const size_t nb = S.buf.bytes * 4;
         APEX_TRY(S.buf.ensure(nb));
@@ -578,13 +632,17 @@ int run_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize, Run
         hq[i].comp = S.comp.as<Entry>();
         hq[i].cap = S.buf.bytes / sizeof(Entry);
       }
+      const size_t bytes = nq * sizeof(ScanQuery);
+      std::memcpy(c->h_queries.p, hq.data(), bytes);
+      APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, bytes, cudaMemcpyHostToDevice, c->stream));
+      APEX_CU(cudaEventRecord(c->upload_ev, c->stream));
+      c->uploaded = hq;
     }
-    APEX_CU(cudaMemcpyAsync(c->d_queries.p, hq, nq * sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+    APEX_TRY(enqueue_batch(c, tau0.data()));
   }
-  for (int e = 0; e < 5; ++e) APEX_CU(cudaEventElapsedTime(&st.ms[e], c->ev[e], c->ev[e + 1]));
-  float last_scan = 0;
-  APEX_CU(cudaEventElapsedTime(&last_scan, c->ev[6], c->ev[7]));
-  st.scan_kernel_ms = last_scan;
+  B.pending = false;
+  for (int e = 0; e < 5; ++e) APEX_CU(cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]));
+  APEX_CU(cudaEventElapsedTime(&B.st.scan_kernel_ms, c->ev[6], c->ev[7]));
   return APEX_OK;
 }
 
@@ -619,6 +677,8 @@ void fill_stats(apex_stats* stats, const RunStats& st, float d2h, float total, i
   stats->scan_launches = st.scans;
   stats->kernel_launches = st.launches;
   stats->retries = st.retries;
+  stats->h2d_bytes = st.h2d_bytes;
+  stats->d2h_bytes = st.d2h_bytes;
 }
 
 // Copy materialized rows of slot i to the caller's result.
@@ -700,6 +760,7 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
     c->own_stream = true;
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&c->upload_ev, cudaEventDisableTiming);
   *out = c;
   return APEX_OK;
 }
@@ -709,7 +770,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto& s : c->slots) s.release();
-  for (auto& p : c->plans) p.d_tiles.release();
+  c->plans.clear();
   c->d_rx.release();
   c->d_goff.release();
   c->d_values.release();
@@ -721,6 +782,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_out.release();
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  if (c->upload_ev) cudaEventDestroy(c->upload_ev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -782,7 +844,8 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   c->total = (uint64_t)total;
   c->lib_pairs = n_pairs;
   c->lib_loaded = true;
-  for (auto& p : c->plans) p.d_tiles.release();
+  c->batch.plan = nullptr;
+  c->batch.pending = false;
   c->plans.clear();
   return APEX_OK;
 }
@@ -856,6 +919,51 @@ int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, co
   return APEX_OK;
 }
 
+int apex_query_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_stats* stats) {
+  APEX_TRY(check_ctx(c, true));
+  APEX_TRY(validate_queries(c, qs, nq));
+  if (nq < 1) return set_err(APEX_EINVAL, "apex_query_async needs at least one query");
+  for (int i = 0; i < nq; ++i) {
+    if (qs[i].start != qs[0].start || qs[i].end != qs[0].end)
+      return set_err(APEX_EINVAL, "apex_query_async: all queries must share one index range");
+    if (qs[i].k < 1 || qs[i].end == qs[i].start)
+      return set_err(APEX_EINVAL, "apex_query_async: k >= 1 and a non-empty range required (use apex_query)");
+  }
+  APEX_TRY(prepare_batch(c, qs, nq, true));
+  APEX_TRY(enqueue_batch(c, nullptr));
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->kernel_launches = c->batch.st.launches;
+    stats->scan_launches = c->batch.st.scans;
+    stats->h2d_bytes = c->batch.st.h2d_bytes;
+  }
+  return APEX_OK;
+}
+
+int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
+  APEX_TRY(check_ctx(c, true));
+  Batch& B = c->batch;
+  if (!B.pending) return set_err(APEX_ESTATE, "no query batch in flight");
+  if (!res) return set_err(APEX_EINVAL, "null results");
+  APEX_TRY(check_batch(c));
+  APEX_CU(cudaEventRecord(c->ev[6], c->stream));
+  APEX_TRY(copy_results(c, B.qs.data(), B.nq, res));
+  APEX_CU(cudaEventRecord(c->ev[7], c->stream));
+  APEX_CU(cudaEventSynchronize(c->ev[7]));
+  float d2h = 0;
+  cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]);
+  int64_t cand = 0, out = 0;
+  for (int i = 0; i < B.nq; ++i) {
+    cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
+    out += (int64_t)out_bytes(std::max<int64_t>(B.qs[i].k, 1), B.qs[i].n_constraints);
+  }
+  B.st.d2h_bytes += out;
+  float total = d2h;
+  for (int e = 0; e < 5; ++e) total += B.st.ms[e];
+  fill_stats(stats, B.st, d2h, total, cand);
+  return APEX_OK;
+}
+
 int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* res, apex_stats* stats) {
   APEX_TRY(check_ctx(c, true));
   APEX_TRY(validate_queries(c, qs, nq));
@@ -867,9 +975,8 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return qs[a].start != qs[b].start ? qs[a].start < qs[b].start : qs[a].end < qs[b].end;
   });
-  RunStats agg;
-  float total_ms = 0, d2h_ms = 0;
-  int64_t cand = 0;
+  apex_stats agg;
+  std::memset(&agg, 0, sizeof(agg));
   size_t g0 = 0;
   while (g0 < order.size()) {
     size_t g1 = g0 + 1;
@@ -889,32 +996,30 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
       }
     }
     if (!grp.empty()) {
-      RunStats st;
-      APEX_TRY(run_batch(c, grp.data(), (int)grp.size(), true, st));
-      APEX_CU(cudaEventRecord(c->ev[6], c->stream));
+      apex_stats st;
+      APEX_TRY(apex_query_async(c, grp.data(), (int)grp.size(), nullptr));
       std::vector<apex_result> tmp(grp.size());
       for (size_t i = 0; i < grp.size(); ++i) tmp[i] = res[live[i]];
-      APEX_TRY(copy_results(c, grp.data(), (int)grp.size(), tmp.data()));
-      APEX_CU(cudaEventRecord(c->ev[7], c->stream));
-      APEX_CU(cudaEventSynchronize(c->ev[7]));
-      float d2h = 0;
-      cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]);
-      for (size_t i = 0; i < grp.size(); ++i) {
-        res[live[i]] = tmp[i];
-        cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
-      }
-      for (int e = 0; e < 5; ++e) agg.ms[e] += st.ms[e];
+      APEX_TRY(apex_query_fetch(c, tmp.data(), &st));
+      for (size_t i = 0; i < grp.size(); ++i) res[live[i]] = tmp[i];
+      agg.pack_ms += st.pack_ms;
+      agg.seed_ms += st.seed_ms;
+      agg.scan_ms += st.scan_ms;
+      agg.select_ms += st.select_ms;
+      agg.finalize_ms += st.finalize_ms;
+      agg.d2h_ms += st.d2h_ms;
+      agg.total_ms += st.total_ms;
       agg.scan_kernel_ms += st.scan_kernel_ms;
-      agg.launches += st.launches;
-      agg.scans += st.scans;
+      agg.candidates += st.candidates;
+      agg.scan_launches += st.scan_launches;
+      agg.kernel_launches += st.kernel_launches;
       agg.retries += st.retries;
-      for (int e = 0; e < 5; ++e) total_ms += st.ms[e];
-      total_ms += d2h;
-      d2h_ms += d2h;
+      agg.h2d_bytes += st.h2d_bytes;
+      agg.d2h_bytes += st.d2h_bytes;
     }
     g0 = g1;
   }
-  fill_stats(stats, agg, d2h_ms, total_ms, cand);
+  if (stats) *stats = agg;
   return APEX_OK;
 }
 
@@ -933,8 +1038,9 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
     for (int i = 0; i < nq; ++i) counts[i] = 0;
     return APEX_OK;
   }
-  RunStats st;
-  APEX_TRY(run_batch(c, qs, nq, false, st));
+  APEX_TRY(prepare_batch(c, qs, nq, false));
+  APEX_TRY(enqueue_batch(c, nullptr));
+  APEX_TRY(check_batch(c));
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
   export_kernel<<<dim3((unsigned)((k + 255) / 256), nq), 256, 0, c->stream>>>(dq, reinterpret_cast<Entry*>(out_dev));
   APEX_CU(cudaGetLastError());
@@ -945,8 +1051,9 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
     cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
   }
   float total = 0;
-  for (int e = 0; e < 5; ++e) total += st.ms[e];
-  fill_stats(stats, st, 0.f, total, cand);
+  for (int e = 0; e < 5; ++e) total += c->batch.st.ms[e];
+  c->batch.st.launches += 1;
+  fill_stats(stats, c->batch.st, 0.f, total, cand);
   return APEX_OK;
 }
 
@@ -979,7 +1086,10 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
   APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
   APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
+  APEX_CU(cudaEventSynchronize(c->upload_ev));
   APEX_TRY(c->h_queries.ensure(sizeof(ScanQuery)));
+  c->uploaded.clear();
+  c->batch.pending = false;
   ScanQuery& Q = *c->h_queries.as<ScanQuery>();
   std::memset(&Q, 0, sizeof(Q));
   Q.buf = S.buf.as<Entry>();
@@ -1006,6 +1116,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
   APEX_CU(cudaEventRecord(c->ev[0], s));
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, &Q, sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+  APEX_CU(cudaEventRecord(c->upload_ev, s));
   init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr);
   merge_load_kernel<<<(unsigned)std::min<int64_t>((n_entries + 255) / 256, c->sm_count * 4), 256, 0, s>>>(
       dq, reinterpret_cast<const Entry*>(entries_dev), (unsigned long long)n_entries);
@@ -1056,10 +1167,12 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   } else if (n == "rl") c->opt_rl = v;
   else if (n == "samples") c->opt_samples = v;
   else if (n == "chunk_div") c->opt_chunk_div = v;
+  else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
   else if (n == "tile_products") {
     c->opt_tile_products = v;
-    for (auto& p : c->plans) p.d_tiles.release();
+    c->batch.plan = nullptr;
+    c->batch.pending = false;
     c->plans.clear();
   } else if (n == "select_ctas") c->opt_select_ctas = std::max<int64_t>(1, v);
   else return set_err(APEX_EINVAL, "unknown option " + n);
