@@ -270,7 +270,10 @@ def main():
 
     shape, queries_named = workload(args.config, world)
     u, w, b = build_model(shape)
-    stream = torch.cuda.current_stream()
+    # a real (non-default) torch stream shared with the C-ABI context, so the
+    # CUDA events below bracket exactly the work the library enqueues
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = _native.DeviceContext(local, stream.cuda_stream)
     ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
     values = ctx.load_cache(u, w, b)

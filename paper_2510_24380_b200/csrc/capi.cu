@@ -135,7 +135,9 @@ struct RunStats {
 
 // The last enqueued batch: queries sharing one range (deep copies).
 struct Batch {
-  std::vector<apex_query_spec> qs;
+  std::vector<apex_query_spec> qs;       // sorted by kernel test class
+  std::vector<int> perm;                 // qs[i] is the caller's query perm[i]
+  std::vector<int> cls_nt, cls_begin;    // scan launches: test class, first query (cls_begin.back() == nq)
   std::vector<std::vector<apex_constraint>> cons;
   std::vector<QTests> tests;
   int nq = 0, NT = 0, rl = 0, ntp = 0;
@@ -183,10 +185,11 @@ struct apex_ctx {
   int64_t opt_rl = 0;               // rows per lane (0 = auto)
   int64_t opt_samples = 0;          // seed samples (0 = auto)
   int64_t opt_chunk_div = 16;       // first scan chunk = 1/opt_chunk_div of the range
-  int64_t opt_chunk_min = 1 << 26;  // ranges at least this large are scanned in two chunks
+  int64_t opt_chunk_min = 1ll << 62;  // ranges at least this large are scanned in two chunks (off)
   int64_t opt_tile_products = 0;    // target products per tile (0 = auto)
   int64_t opt_select_ctas = 16;     // CTAs per query in the select kernel
   int64_t opt_force_upload = 0;     // re-upload query descriptors on every call
+  int64_t opt_refresh = 0;          // in-kernel tau refresh interval (0 = k)
 };
 
 namespace {
@@ -222,9 +225,9 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) 
   P.end = end;
   P.rows = rows;
   const uint64_t span = end - start;
-  int64_t warp_slots = (int64_t)c->sm_count * 16 * 2;
-  int64_t target = c->opt_tile_products > 0 ? c->opt_tile_products : (int64_t)(span / (uint64_t)(32 * warp_slots));
-  int64_t cols = std::max<int64_t>(64, std::min<int64_t>(2048, target / rows));
+  int64_t warp_slots = (int64_t)c->sm_count * 24;
+  int64_t target = c->opt_tile_products > 0 ? c->opt_tile_products : (int64_t)(span / (uint64_t)(8 * warp_slots));
+  int64_t cols = std::max<int64_t>(64, std::min<int64_t>(4096, target / rows));
   cols = (cols + 63) / 64 * 64;
   P.cols = cols;
   P.pair_lo = INT64_MAX;
@@ -346,9 +349,18 @@ size_t scan_smem(int nt, int cb) {
 }
 
 int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
+  // cached per (kernel, smem): the attribute call and the occupancy query cost
+  // microseconds on every launch otherwise
+  static thread_local std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+  for (auto& e : cache)
+    if (e.first.first == (const void*)fn && e.first.second == smem) {
+      *occ = e.second;
+      return APEX_OK;
+    }
   APEX_CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, (const void*)fn, kScanWarps * 32, smem));
   if (*occ < 1) return set_err(APEX_ELIMIT, "enumeration kernel does not fit on an SM");
+  cache.push_back({{(const void*)fn, smem}, *occ});
   return APEX_OK;
 }
 
@@ -357,31 +369,50 @@ int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
 // enqueue (device pipeline, no host sync), check (one sync: overflow check and
 // exact re-run with the final bound if the candidate buffer overflowed).
 
-int prepare_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize) {
+int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finalize) {
   Batch& B = c->batch;
-  B.qs.assign(qs, qs + nq);
-  B.cons.assign(nq, {});
+  // tests per query, then group queries by the kernel's test class (one scan
+  // launch per class, so no query pays for another's padding)
+  std::vector<QTests> tests_in(nq);
+  std::vector<int> cls(nq);
+  int nt_max = 1;
   for (int i = 0; i < nq; ++i) {
-    B.cons[i].assign(qs[i].constraints, qs[i].constraints + qs[i].n_constraints);
-    B.qs[i].constraints = B.cons[i].data();
+    APEX_TRY(make_tests(c, qs_in[i], tests_in[i]));
+    if (qs_in[i].n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+    cls[i] = kernel_nt(tests_in[i].nt);
+    if (cls[i] < 0) return set_err(APEX_ELIMIT, "too many tests");
+    nt_max = std::max(nt_max, tests_in[i].nt);
   }
+  B.perm.resize(nq);
+  std::iota(B.perm.begin(), B.perm.end(), 0);
+  std::stable_sort(B.perm.begin(), B.perm.end(), [&](int a, int b) { return cls[a] < cls[b]; });
+  B.qs.resize(nq);
+  B.cons.assign(nq, {});
+  B.tests.resize(nq);
+  B.cls_nt.clear();
+  B.cls_begin.clear();
+  for (int i = 0; i < nq; ++i) {
+    const int o = B.perm[i];
+    B.qs[i] = qs_in[o];
+    B.cons[i].assign(qs_in[o].constraints, qs_in[o].constraints + qs_in[o].n_constraints);
+    B.qs[i].constraints = B.cons[i].data();
+    B.tests[i] = tests_in[o];
+    if (B.cls_nt.empty() || B.cls_nt.back() != cls[o]) {
+      B.cls_nt.push_back(cls[o]);
+      B.cls_begin.push_back(i);
+    }
+  }
+  B.cls_begin.push_back(nq);
+  const apex_query_spec* qs = B.qs.data();
   B.nq = nq;
   B.finalize = finalize;
-  B.tests.assign(nq, QTests());
   B.st = RunStats();
-  int nt_max = 1;
   B.k_max = 0;
-  for (int i = 0; i < nq; ++i) {
-    APEX_TRY(make_tests(c, qs[i], B.tests[i]));
-    nt_max = std::max(nt_max, B.tests[i].nt);
-    B.k_max = std::max<int64_t>(B.k_max, qs[i].k);
-    if (qs[i].n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
-  }
+  for (int i = 0; i < nq; ++i) B.k_max = std::max<int64_t>(B.k_max, qs[i].k);
   B.NT = kernel_nt(nt_max);
-  if (B.NT < 0) return set_err(APEX_ELIMIT, "too many tests");
   B.ntp = (B.NT + 3) / 4 * 4;
   B.rl = (int)c->opt_rl;
-  if (B.rl != 1 && B.rl != 2) B.rl = B.NT <= 8 ? 2 : 1;
+  if (B.rl != 1 && B.rl != 2) B.rl = 1;
   APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, B.plan));
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
@@ -389,13 +420,14 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize)
     Slot& S = c->slots[i];
     const int64_t k = qs[i].k;
     const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
-    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * B.ntp * sizeof(float)));
+    const int ntp_i = (kernel_nt(B.tests[i].nt) + 3) / 4 * 4;
+    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp_i * sizeof(float)));
     APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
-    APEX_TRY(S.hist.ensure(kHistBins * sizeof(unsigned)));
+    APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
     APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
     APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
     APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
@@ -414,12 +446,15 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs, int nq, bool finalize)
     Q.sorted = S.sorted.as<Entry>();
     Q.rank = S.rank.as<unsigned>();
     Q.hist = S.hist.as<unsigned>();
+    Q.coarse = S.hist.as<unsigned>() + kHistBins;
     Q.seed_hist = S.seed_hist.as<unsigned>();
     Q.ctl = S.ctl.as<QCtl>();
     Q.cap = S.buf.bytes / sizeof(Entry);
+    Q.refresh = (unsigned long long)std::max<int64_t>(c->opt_refresh > 0 ? c->opt_refresh : q.k, 256);
     Q.k = q.k;
     Q.nt = T.nt;
-    Q.ntp = B.ntp;
+    Q.ntp = (kernel_nt(T.nt) + 3) / 4 * 4;
+    Q.slot = B.perm[i];
     Q.maximize = q.maximize ? 1 : 0;
     Q.obj_task = q.objective_task;
     Q.n_cons = q.n_constraints;
@@ -479,7 +514,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // K2 pack
   if (plan->pair_hi > plan->pair_lo) {
     const int64_t n = (plan->pair_hi - plan->pair_lo) * B.ntp;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8 / nq));
     pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
     ++st.launches;
   }
@@ -487,7 +522,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // seed threshold from exact samples
   if (!tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
-                                     : (uint64_t)std::min<int64_t>(1 << 21, std::max<int64_t>(1 << 18, 64 * B.k_max));
+                                     : (uint64_t)std::min<int64_t>(1 << 20, std::max<int64_t>(1 << 18, 64 * B.k_max));
     S = std::min<uint64_t>(S, span);
     if (S > 0) {
       SampleLaunch P;
@@ -501,19 +536,14 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       P.end = end;
       P.samples = S;
       const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
-      sample_kernel<<<dim3(blocks, nq), 256, 0, s>>>(P);
+      sample_kernel<<<blocks, 256, 0, s>>>(P, nq);
       tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
       st.launches += 2;
     }
   }
   APEX_CU(cudaEventRecord(c->ev[2], s));
-  // K3 enumeration chunks
-  ScanFn fn = pick_scan(B.NT, B.rl);
-  if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
+  // K3 enumeration: chunks x test classes
   const int cb = (int)c->opt_cb;
-  const size_t smem = scan_smem(B.NT, cb);
-  int occ = 0;
-  APEX_TRY(scan_occupancy(fn, smem, &occ));
   const size_t n_tiles = plan->tiles.size();
   std::vector<size_t> bounds;  // chunk ends in tile indices
   if (span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && n_tiles > 1) {
@@ -537,13 +567,23 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.n_pairs = c->n_pairs;
       L.queries = dq;
       L.cb = cb;
-      const int64_t blocks =
-          std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
       if (ci == 0) APEX_CU(cudaEventRecord(c->ev[6], s));
-      fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(L);
-      APEX_CU(cudaGetLastError());
-      ++st.launches;
-      ++st.scans;
+      for (size_t k = 0; k + 1 < B.cls_begin.size(); ++k) {
+        ScanFn fn = pick_scan(B.cls_nt[k], B.rl);
+        if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
+        const size_t smem = scan_smem(B.cls_nt[k], cb);
+        int occ = 0;
+        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        const int nqc = B.cls_begin[k + 1] - B.cls_begin[k];
+        const int64_t blocks =
+            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
+        ScanLaunch Lc = L;
+        Lc.queries = dq + B.cls_begin[k];
+        fn<<<dim3((unsigned)blocks, nqc), kScanWarps * 32, smem, s>>>(Lc);
+        APEX_CU(cudaGetLastError());
+        ++st.launches;
+        ++st.scans;
+      }
       if (ci + 1 < bounds.size()) {
         tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);  // raise tau from the candidates so far
         ++st.launches;
@@ -557,11 +597,11 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   APEX_CU(cudaEventRecord(c->ev[3], s));
   // final bound, compaction, exact select
   tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
-  compact_kernel<<<dim3(c->sm_count * 4, nq), 256, 0, s>>>(dq);
-  st.launches += 2;
+  ++st.launches;
   {
-    int occ_sel = 0;
-    APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
+    static thread_local int occ_sel = 0;
+    if (!occ_sel)
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
     const int resident = std::max(1, occ_sel * c->sm_count);
     const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / nq));
     if (per_q * nq > resident) return set_err(APEX_ELIMIT, "too many queries in one batch for the select kernel");
@@ -682,7 +722,10 @@ void fill_stats(apex_stats* stats, const RunStats& st, float d2h, float total, i
 }
 
 // Copy materialized rows of slot i to the caller's result.
-int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* res) {
+int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* res_caller, const int* perm) {
+  std::vector<apex_result> res_sorted(nq);
+  for (int i = 0; i < nq; ++i) res_sorted[i] = res_caller[perm ? perm[i] : i];
+  apex_result* res = res_sorted.data();
   size_t total = 0;
   std::vector<size_t> offs(nq);
   for (int i = 0; i < nq; ++i) {
@@ -716,6 +759,7 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
       if (r.digits) std::memcpy(r.digits, o + (20 + 8 * (size_t)m) * kk, 4 * (size_t)kMaxRg * n);
     }
   }
+  for (int i = 0; i < nq; ++i) res_caller[perm ? perm[i] : i] = res_sorted[i];
   return APEX_OK;
 }
 
@@ -947,7 +991,7 @@ int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
   if (!res) return set_err(APEX_EINVAL, "null results");
   APEX_TRY(check_batch(c));
   APEX_CU(cudaEventRecord(c->ev[6], c->stream));
-  APEX_TRY(copy_results(c, B.qs.data(), B.nq, res));
+  APEX_TRY(copy_results(c, B.qs.data(), B.nq, res, B.perm.data()));
   APEX_CU(cudaEventRecord(c->ev[7], c->stream));
   APEX_CU(cudaEventSynchronize(c->ev[7]));
   float d2h = 0;
@@ -1047,7 +1091,7 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
   APEX_CU(cudaStreamSynchronize(c->stream));
   int64_t cand = 0;
   for (int i = 0; i < nq; ++i) {
-    counts[i] = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
+    counts[c->batch.perm[i]] = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
     cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
   }
   float total = 0;
@@ -1076,12 +1120,12 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   if (c->slots.empty()) c->slots.resize(1);
   Slot& S = c->slots[0];
   const int64_t cap = std::max<int64_t>(n_entries, 1024);
-  APEX_TRY(S.buf.ensure(sizeof(Entry)));
-  APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
+  APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
+  APEX_TRY(S.comp.ensure(sizeof(Entry)));
   APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
   APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
   APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
-  APEX_TRY(S.hist.ensure(kHistBins * sizeof(unsigned)));
+  APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
   APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
   APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
   APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
@@ -1098,9 +1142,11 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   Q.sorted = S.sorted.as<Entry>();
   Q.rank = S.rank.as<unsigned>();
   Q.hist = S.hist.as<unsigned>();
+  Q.coarse = S.hist.as<unsigned>() + kHistBins;
   Q.seed_hist = S.seed_hist.as<unsigned>();
   Q.ctl = S.ctl.as<QCtl>();
   Q.cap = (unsigned long long)cap;
+  Q.refresh = 1ull << 62;
   Q.k = k;
   Q.maximize = q->maximize ? 1 : 0;
   Q.obj_task = q->objective_task;
@@ -1146,7 +1192,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   apex_query_spec qq = *q;
   qq.start = 0;
   qq.end = total_scanned;
-  APEX_TRY(copy_results(c, &qq, 1, res));
+  APEX_TRY(copy_results(c, &qq, 1, res, nullptr));
   if (stats) {
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
@@ -1168,6 +1214,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "samples") c->opt_samples = v;
   else if (n == "chunk_div") c->opt_chunk_div = v;
   else if (n == "force_upload") c->opt_force_upload = v;
+  else if (n == "refresh") c->opt_refresh = v;
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
   else if (n == "tile_products") {
     c->opt_tile_products = v;

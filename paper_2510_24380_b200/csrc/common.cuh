@@ -57,6 +57,10 @@ struct QCtl {
   unsigned long long sel_count;   // entries selected (<= k)
   unsigned long long bound_key;   // final compaction bound
   unsigned long long min_key;     // select scratch
+  unsigned long long hist_base;   // candidate histogram: bin = min((key - base) >> shift, 65535)
+  unsigned long long seed_max;    // max key among feasible samples
+  unsigned int hist_shift;
+  unsigned int _pad1;
   unsigned int active;            // participates in the current launch
   unsigned int tile_counter;      // scan work distribution
   unsigned int barrier;           // select grid barrier
@@ -64,7 +68,17 @@ struct QCtl {
   unsigned int hist[3][256];      // select histograms (triple-buffered)
 };
 
-constexpr int kHistBins = 65536;  // candidate histogram over key >> 48
+constexpr int kHistBins = 65536;  // candidate histogram bins
+
+// Candidate histogram bin of a key (relative to the seed threshold, see
+// tau_kernel mode 0); the top bin absorbs everything above its lower edge.
+__host__ __device__ __forceinline__ unsigned hist_bin(unsigned long long key, unsigned long long base, unsigned shift) {
+  const unsigned long long rel = (key - base) >> shift;
+  return rel > 65535ull ? 65535u : (unsigned)rel;
+}
+__host__ __device__ __forceinline__ unsigned long long bin_edge(unsigned bin, unsigned long long base, unsigned shift) {
+  return base + ((unsigned long long)bin << shift);
+}
 
 // Per-query parameters (device, read-only during a launch).
 struct ScanQuery {
@@ -74,17 +88,19 @@ struct ScanQuery {
   Entry* sel;                     // selected top-k (k entries, unordered)
   Entry* sorted;                  // best-first (k entries)
   unsigned int* rank;             // [k]
-  unsigned int* hist;             // [kHistBins] histogram of appended keys
+  unsigned int* hist;             // [kHistBins] histogram of appended keys (key >> 48)
+  unsigned int* coarse;           // [256] histogram of appended keys (key >> 56)
   unsigned int* seed_hist;        // [kHistBins] histogram of feasible sampled keys
   QCtl* ctl;
   unsigned long long cap;         // capacity of buf / comp (entries)
+  unsigned long long refresh;     // in-kernel tau refresh every `refresh` appended candidates
   long long k;
   int32_t nt;                     // live tests (test 0 = objective admission)
   int32_t ntp;                    // packed row stride (floats, multiple of 4)
   int32_t maximize;
   int32_t obj_task;
   int32_t n_cons;                 // constraints (materialization order)
-  int32_t _pad;
+  int32_t slot;                   // position of the query in the caller's array
   int32_t test_task[kMaxTests];
   int32_t test_lower[kMaxTests];  // 1: lower-bound test (y = -x), 0: upper (y = x)
   double test_beta[kMaxTests];    // bound (ignored for test 0: derived from tau)

@@ -166,8 +166,12 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
     Q.hist[i] = 0u;
     Q.seed_hist[i] = 0u;
   }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) Q.coarse[i] = 0u;
   if (threadIdx.x == 0) {
     c->tau_key = tau0 ? tau0[blockIdx.x] : kNoTau;
+    c->hist_base = 0;
+    c->hist_shift = 48;
+    c->seed_max = 0;
     c->count = 0;
     c->comp_count = 0;
     c->sel_count = 0;
@@ -198,6 +202,52 @@ __global__ void pack_kernel(const ScanQuery* __restrict__ qs, const float* __res
       if (Q.test_lower[t]) v = -v;
     }
     dst[p * ntp + t] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast exact thresholds: the rounded guess fl32((beta - b) - p) is within one
+// fp32 ulp of the boundary unless fp64 absorption is extreme, so two probes
+// usually settle it; anything else falls back to the general search above.
+__device__ __forceinline__ float next_up(float x) { return fromkey(fkey(x) + 1); }
+__device__ __forceinline__ float next_down(float x) { return fromkey(fkey(x) - 1); }
+
+__device__ __forceinline__ float thr_upper_fast(double p, double b, double beta) {
+  const double gd = __dsub_rn(__dsub_rn(beta, b), p);
+  if (fabs(gd) < 3.0e38) {
+    const float x = __double2float_rn(gd);
+    if (fx(p, x, b) <= beta) {
+      if (!(fx(p, next_up(x), b) <= beta)) return x;
+    } else {
+      const float xd = next_down(x);
+      if (fx(p, xd, b) <= beta) return xd;
+    }
+  }
+  return thr_upper(p, b, beta);
+}
+
+__device__ __forceinline__ float thr_lower_fast(double p, double b, double beta) {
+  const double gd = __dsub_rn(__dsub_rn(beta, b), p);
+  if (fabs(gd) < 3.0e38) {
+    const float x = __double2float_rn(gd);
+    if (fx(p, x, b) >= beta) {
+      if (!(fx(p, next_down(x), b) >= beta)) return x;
+    } else {
+      const float xu = next_up(x);
+      if (fx(p, xu, b) >= beta) return xu;
+    }
+  }
+  return thr_lower(p, b, beta);
+}
+
+__device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n, uint64_t d) {
+  if ((n >> 32) == 0 && (d >> 32) == 0) {
+    const uint32_t n32 = (uint32_t)n, d32 = (uint32_t)d;
+    q = n32 / d32;
+    r = n32 - (uint32_t)q * d32;
+  } else {
+    q = n / d;
+    r = n - q * d;
   }
 }
 
@@ -252,8 +302,65 @@ __device__ __forceinline__ bool test_cols(const float* __restrict__ ys, int j, c
   return any;
 }
 
+// In-kernel threshold refresh (one warp): B = highest key>>48 bin such that the
+// candidates appended so far with key >= B<<48 number at least k; counts are
+// read while other warps keep appending, and a stale (smaller) count only
+// lowers B, so tau = B<<48 is always a valid lower bound on the final k-th
+// best key.  Two levels: 256 coarse bins (key>>56), then the 256 fine bins of
+// the chosen coarse bin.
+__device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
+  const unsigned lane = lane_id();
+  const unsigned long long k = (unsigned long long)Q.k;
+  unsigned long long above = 0;
+  int coarse_bin = -1;
+  for (int base = 255; base >= 0 && coarse_bin < 0; base -= 32) {
+    const unsigned long long v = __ldcg(Q.coarse + (base - (int)lane));
+    unsigned long long incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += o;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      coarse_bin = base - l;
+      above += __shfl_sync(0xffffffffu, incl - v, l);
+    } else {
+      above += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (coarse_bin < 0) return;  // fewer than k candidates so far
+  int fine_bin = -1;
+  for (int base = 255; base >= 0 && fine_bin < 0; base -= 32) {
+    const unsigned long long v = __ldcg(Q.hist + ((coarse_bin << 8) | (base - (int)lane)));
+    unsigned long long incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += o;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
+    if (m) {
+      fine_bin = base - (__ffs(m) - 1);
+    } else {
+      above += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  // the fine counts may lag the coarse ones: if the coarse bin's fine bins do
+  // not (yet) reach k, fall back to the coarse bin's lower edge
+  const unsigned long long base = Q.ctl->hist_base;
+  const unsigned shift = Q.ctl->hist_shift;
+  const unsigned long long key = fine_bin >= 0 ? bin_edge((unsigned)((coarse_bin << 8) | fine_bin), base, shift)
+                                               : bin_edge((unsigned)(coarse_bin << 8), base, shift);
+  if (lane == 0) atomicMax(&Q.ctl->tau_key, key);
+}
+
+template <int NT>
+constexpr int scan_min_blocks() { return NT <= 12 ? 3 : 2; }
+
 template <int NT, int RL>
-__global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch L) {
+__global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_kernel(const ScanLaunch L) {
   constexpr int NTP = Ntp<NT>::value;
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const ScanQuery& Q = L.queries[blockIdx.y];
@@ -280,6 +387,9 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
   const int maximize = Q.maximize;
   const float* packed = Q.packed;
   const double b_obj = Q.test_bias[0];
+  const int nt = Q.nt;
+  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
+  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
 
   for (;;) {
     unsigned t = 0;
@@ -295,7 +405,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
 
     // kick off the first column block before the threshold arithmetic
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(T.ncols < (uint32_t)cb ? T.ncols : (uint32_t)cb) * NTP * 4u;
+      const uint32_t bytes = (T.ncols < (uint32_t)cb ? T.ncols : (uint32_t)cb) * NTP * 4u;
       fence_proxy_async();
       mbar_expect_tx(&bars[bi], bytes);
       bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
@@ -303,6 +413,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
 
     const unsigned long long tau = *(volatile unsigned long long*)&ctl->tau_key;
     const double tau_s = key_to_score(tau);
+    unsigned long long tau_seen = tau;
 
     float thr[RL][NT];
     double p_obj[RL];
@@ -312,30 +423,38 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
       const unsigned local = lane + 32u * r;
       const bool valid = local < T.nrows;
       const uint64_t row = T.row0 + (valid ? local : 0u);
-      int64_t dig[kMaxRg];
+      // prefix digits -> table rows of the first c-1 R-groups (registers)
+      int64_t pr[kMaxRg - 1];
       {
         uint64_t rem = row;
-        for (int j = c - 2; j >= 1; --j) {
-          const uint64_t sz = (uint64_t)R.size[j];
-          dig[j] = (int64_t)(rem % sz);
-          rem /= sz;
+#pragma unroll
+        for (int j = kMaxRg - 2; j >= 1; --j) {
+          pr[j] = 0;
+          if (j <= c - 2) {
+            uint64_t q, d;
+            divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+            pr[j] = R.pair_off[j] + (int64_t)d;
+            rem = q;
+          }
         }
-        dig[0] = (int64_t)rem;
+        pr[0] = R.pair_off[0] + (int64_t)rem;
       }
       gbase[r] = R.g_off + row * (uint64_t)n_last + T.col0;
 #pragma unroll
       for (int i = 0; i < NT; ++i) {
         float th = __int_as_float(0x7f800000);  // +inf: padding test always passes
-        if (i < Q.nt) {
+        if (i < nt) {
           const float* vrow = L.values + (int64_t)Q.test_task[i] * L.n_pairs;
-          double p = c > 1 ? (double)__ldg(vrow + R.pair_off[0] + dig[0]) : 0.0;  // c == 1: no prefix
-          for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(vrow + R.pair_off[j] + dig[j]));
+          double p = c > 1 ? (double)__ldg(vrow + pr[0]) : 0.0;  // c == 1: no prefix
+#pragma unroll
+          for (int j = 1; j < kMaxRg - 1; ++j)
+            if (j < c - 1) p = __dadd_rn(p, (double)__ldg(vrow + pr[j]));
           const double b = Q.test_bias[i];
           if (i == 0) {
             p_obj[r] = p;
-            if (tau != kNoTau) th = maximize ? -thr_lower(p, b, tau_s) : thr_upper(p, b, -tau_s);
+            if (tau != kNoTau) th = maximize ? -thr_lower_fast(p, b, tau_s) : thr_upper_fast(p, b, -tau_s);
           } else {
-            th = Q.test_lower[i] ? -thr_lower(p, b, Q.test_beta[i]) : thr_upper(p, b, Q.test_beta[i]);
+            th = Q.test_lower[i] ? -thr_lower_fast(p, b, Q.test_beta[i]) : thr_upper_fast(p, b, Q.test_beta[i]);
           }
         }
         thr[r][i] = th;
@@ -353,23 +472,36 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
         mbar_expect_tx(&bars[nb], bytes);
         bulk_g2s(nb ? sbuf1 : sbuf0, col_src + (size_t)(col_base + cb) * NTP, bytes, &bars[nb]);
       }
+      // tighten the admission threshold if another warp raised tau
+      const unsigned long long tau_now = *(volatile unsigned long long*)&ctl->tau_key;
+      if (tau_now != tau_seen) {
+        tau_seen = tau_now;
+        const double ts = key_to_score(tau_now);
+#pragma unroll
+        for (int r = 0; r < RL; ++r)
+          if (lane + 32u * r < T.nrows)
+            thr[r][0] = maximize ? -thr_lower_fast(p_obj[r], b_obj, ts) : thr_upper_fast(p_obj[r], b_obj, -ts);
+      }
       if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
       else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
-      const float* ys = bi ? sbuf1 : sbuf0;
+      float* ys = bi ? sbuf1 : sbuf0;
+      const int ngroups = (ncol + 7) >> 3;
+      if (ncol & 7) {
+        // pad the last group with NaN columns (never pass: NaN <= t is false)
+        const int pad = (ngroups << 3) - ncol;
+        for (int idx = (int)lane; idx < pad * NTP; idx += 32) ys[ncol * NTP + idx] = __int_as_float(0x7fffffff);
+        __syncwarp();
+      }
 
-      for (int j0 = 0; j0 < ncol; j0 += 8) {
-        const int jn = min(8, ncol - j0);
+      for (int gi = 0; gi < ngroups; ++gi) {
+        const int j0 = gi << 3;
         bool any = false;
         bool pass[RL];
-        if (jn == 8) {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
-        } else {
-          for (int jj = 0; jj < jn; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
-        }
+        for (int jj = 0; jj < 8; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
         if (__any_sync(0xffffffffu, any)) {
           // slow path: exact fp64 score, warp-aggregated append
-          for (int jj = 0; jj < jn; ++jj) {
+          for (int jj = 0; jj < 8; ++jj) {
             test_cols<NT, RL>(ys, j0 + jj, thr, pass);
             const float y0 = ys[(j0 + jj) * NTP];
 #pragma unroll
@@ -389,7 +521,15 @@ __global__ void __launch_bounds__(kScanWarps * 32) scan_kernel(const ScanLaunch 
                   e.g = gbase[r] + (unsigned long long)(col_base + j0 + jj);
                   const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
                   if (idx < cap) buf[idx] = e;
-                  atomicAdd(&hist[e.key >> 48], 1u);
+                  const unsigned hb = hist_bin(e.key, hbase, hshift);
+                  atomicAdd(&hist[hb], 1u);
+                  atomicAdd(&Q.coarse[hb >> 8], 1u);
+                }
+                // every `refresh` candidates, the warp that crosses the mark
+                // recomputes tau from the histograms
+                if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
+                  __threadfence();
+                  refresh_tau(Q);
                 }
               }
             }
@@ -422,43 +562,60 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   return x;
 }
 
-__global__ void sample_kernel(const SampleLaunch P) {
-  const ScanQuery& Q = P.queries[blockIdx.y];
-  if (!*(volatile unsigned int*)&Q.ctl->active) return;
+__global__ void sample_kernel(const SampleLaunch P, int nq) {
   const unsigned long long span = P.end - P.start, S = P.samples;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride) {
-    const unsigned long long lo = (unsigned long long)(((unsigned __int128)span * i) / S);
-    const unsigned long long hi = (unsigned long long)(((unsigned __int128)span * (i + 1)) / S);
-    const unsigned long long g = P.start + lo + mix64(i * 0x9e3779b97f4a7c15ull + 17) % (hi - lo);
-    int a = 0, b = P.n_rx;
-    while (b - a > 1) {
-      const int mid = (a + b) >> 1;
-      if (P.g_off[mid] <= g) a = mid; else b = mid;
-    }
-    const DevReaction& R = P.rx[a];
-    unsigned long long rem = g - R.g_off;
+  const unsigned lane = lane_id();
+  for (unsigned long long base_i = (unsigned long long)blockIdx.x * blockDim.x; base_i < S; base_i += stride) {
+    const unsigned long long i = base_i + threadIdx.x;
+    const bool live = i < S;
     int64_t pr[kMaxRg];
-    for (int j = R.c - 1; j >= 0; --j) {
-      const unsigned long long sz = (unsigned long long)R.size[j];
-      pr[j] = R.pair_off[j] + (int64_t)(rem % sz);
-      rem /= sz;
+    int c = 0;
+    if (live) {
+      const unsigned long long lo = (unsigned long long)(((unsigned __int128)span * i) / S);
+      const unsigned long long hi = (unsigned long long)(((unsigned __int128)span * (i + 1)) / S);
+      const unsigned long long g = P.start + lo + mix64(i * 0x9e3779b97f4a7c15ull + 17) % (hi - lo);
+      int a = 0, b = P.n_rx;
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (P.g_off[mid] <= g) a = mid; else b = mid;
+      }
+      const DevReaction& R = P.rx[a];
+      c = R.c;
+      uint64_t rem = g - R.g_off;
+      for (int j = c - 1; j >= 0; --j) {
+        uint64_t q, d;
+        divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+        pr[j] = R.pair_off[j] + (int64_t)d;
+        rem = q;
+      }
     }
-    bool feasible = true;
-    for (int t = 1; t < Q.nt && feasible; ++t) {
-      const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
-      double val = (double)__ldg(v + pr[0]);
-      for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
-      val = __dadd_rn(val, Q.test_bias[t]);
-      feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
-    }
-    if (feasible) {
-      const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
-      double val = (double)__ldg(v + pr[0]);
-      for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
-      val = __dadd_rn(val, Q.test_bias[0]);
-      const double s = Q.maximize ? val : -val;
-      atomicAdd(&Q.seed_hist[skey(s) >> 48], 1u);
+    // every query of the batch evaluates the same sampled product
+    for (int qi = 0; qi < nq; ++qi) {
+      const ScanQuery& Q = P.queries[qi];
+      unsigned long long key = 0;
+      if (live) {
+        bool feasible = true;
+        for (int t = 1; t < Q.nt && feasible; ++t) {
+          const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
+          double val = (double)__ldg(v + pr[0]);
+          for (int j = 1; j < c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+          val = __dadd_rn(val, Q.test_bias[t]);
+          feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
+        }
+        if (feasible) {
+          const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
+          double val = (double)__ldg(v + pr[0]);
+          for (int j = 1; j < c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+          val = __dadd_rn(val, Q.test_bias[0]);
+          key = skey(Q.maximize ? val : -val);
+          atomicAdd(&Q.seed_hist[key >> 48], 1u);
+        }
+      }
+      unsigned long long mx = key;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      if (lane == 0 && mx) atomicMax(&Q.ctl->seed_max, mx);
     }
   }
 }
@@ -469,6 +626,12 @@ __global__ void sample_kernel(const SampleLaunch P) {
 // lower bound on the final k-th best key (never discards a true top-k
 // product).  mode 0: seed_hist -> raise tau_key; mode 1: hist -> raise
 // tau_key; mode 2: hist -> bound_key (final compaction bound).
+__device__ __forceinline__ unsigned long long wsum_total(const unsigned long long* w) {
+  unsigned long long t = 0;
+  for (int i = 0; i < 32; ++i) t += w[i];
+  return t;
+}
+
 __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* ctl = Q.ctl;
@@ -507,16 +670,31 @@ __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__
       acc += __ldcg(h + b);
       if (acc >= k) { B = b; break; }
     }
-    const unsigned long long key = (unsigned long long)B << 48;
-    if (mode < 2) {
+    const unsigned long long key =
+        mode == 0 ? ((unsigned long long)B << 48) : bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift);
+    if (mode == 0) {
+      // seed threshold; candidate histogram re-based on it, with the sampled
+      // range [tau, seed_max] spread over ~1/4 of the bins
+      if (key > ctl->tau_key) ctl->tau_key = key;
+      const unsigned long long base = ctl->tau_key;
+      const unsigned long long range = ctl->seed_max > base ? ctl->seed_max - base : 0ull;
+      unsigned shift = 0;
+      while (shift < 48 && (range >> shift) >= 16384ull) ++shift;
+      ctl->hist_base = base;
+      ctl->hist_shift = shift;
+    } else if (mode == 1) {
       if (key > ctl->tau_key) ctl->tau_key = key;
     } else {
       ctl->bound_key = key;
+      ctl->comp_count = acc;  // candidates with key >= bound
     }
     found = 1;
   }
   __syncthreads();
-  if (t == 0 && !found && mode == 2) ctl->bound_key = 0;  // fewer than k candidates: keep all
+  if (t == 0 && !found && mode == 2) {  // fewer than k candidates: keep all
+    ctl->bound_key = 0;
+    ctl->comp_count = wsum_total(wsum);
+  }
 }
 
 // Compact candidates with key >= bound_key into comp (order arbitrary).
@@ -597,13 +775,17 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
   __shared__ unsigned long long s_min[kSelectThreads / 32];
   const unsigned tid = threadIdx.x, nb = gridDim.x;
   unsigned gen = 0;
-  const unsigned long long n = *(volatile unsigned long long*)&ctl->comp_count;
+  // candidates at/above the final bound (counted by tau_kernel mode 2); the
+  // select reads the candidate buffer directly and ignores keys below it
+  const unsigned long long n_valid = *(volatile unsigned long long*)&ctl->comp_count;
+  const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
+  const unsigned long long bound = *(volatile unsigned long long*)&ctl->bound_key;
   const unsigned long long k = (unsigned long long)Q.k;
-  const Entry* __restrict__ in = Q.comp;
+  const Entry* __restrict__ in = Q.buf;
   const unsigned long long start = (unsigned long long)blockIdx.x * blockDim.x + tid;
   const unsigned long long stride = (unsigned long long)nb * blockDim.x;
 
-  const bool take_all = n <= k;
+  const bool take_all = n_valid <= k;
   unsigned long long phi = 0, plo = 0;
   int depth = 0;
   if (!take_all) {
@@ -614,7 +796,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
       phi = s_phi; plo = s_plo;
       for (unsigned long long i = start; i < n; i += stride) {
         const Entry e = in[i];
-        if (match_prefix(e, phi, plo, p)) atomicAdd(&sh[digit_of(e, p)], 1u);
+        if (e.key >= bound && match_prefix(e, phi, plo, p)) atomicAdd(&sh[digit_of(e, p)], 1u);
       }
       __syncthreads();
       unsigned int* gh = ctl->hist[p % 3];
@@ -652,7 +834,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
     bool keep = false;
     if (i < n) {
       e = in[i];
-      keep = take_all || ge_prefix(e, phi, plo, depth);
+      keep = e.key >= bound && (take_all || ge_prefix(e, phi, plo, depth));
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (m) {
@@ -775,7 +957,7 @@ __global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restric
   const ScanQuery& Q = qs[blockIdx.y];
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[(unsigned long long)blockIdx.y * Q.k + i] = Q.sel[i];
+  if (i < n) out[(unsigned long long)Q.slot * Q.k + i] = Q.sel[i];
 }
 
 // Multi-GPU: load gathered entries (skip padding g == ~0) as the compacted set.
@@ -798,9 +980,12 @@ __global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry*
     if (m) {
       const int leader = __ffs(m) - 1;
       unsigned long long pos = 0;
-      if ((int)lane == leader) pos = atomicAdd(&ctl->comp_count, (unsigned long long)__popc(m));
+      if ((int)lane == leader) {
+        pos = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
+        atomicAdd(&ctl->comp_count, (unsigned long long)__popc(m));
+      }
       pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (keep) Q.comp[pos + __popc(m & ((1u << lane) - 1u))] = e;
+      if (keep) Q.buf[pos + __popc(m & ((1u << lane) - 1u))] = e;
     }
   }
 }
