@@ -108,6 +108,7 @@ typedef struct {
   int64_t retries;         /* re-runs after a candidate-buffer overflow */
   int64_t h2d_bytes;       /* host->device bytes copied by the call */
   int64_t d2h_bytes;       /* device->host bytes copied by the call */
+  int64_t admitted;        /* products that passed the admission test (admission-first kernel) */
 } apex_stats;
 
 /* Caller-allocated host output for one query; arrays sized for k entries

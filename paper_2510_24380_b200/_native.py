@@ -79,6 +79,7 @@ class Stats(C.Structure):
         ("retries", C.c_int64),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("admitted", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

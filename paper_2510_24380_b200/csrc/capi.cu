@@ -96,9 +96,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, buf, comp, sel, sorted, rank, hist, seed_hist, ctl, out;
+  DBuf packed, obj_col, buf, comp, sel, sorted, rank, hist, seed_hist, ctl, out;
   void release() {
-    for (DBuf* b : {&packed, &buf, &comp, &sel, &sorted, &rank, &hist, &seed_hist, &ctl, &out}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &hist, &seed_hist, &ctl, &out}) b->release();
   }
 };
 
@@ -161,6 +161,7 @@ struct apex_ctx {
   std::vector<unsigned long long> goff;  // n_rx + 1
   uint64_t total = 0;
   int64_t lib_pairs = 0;
+  int64_t pcols = 0;                     // packed objective-column length (16-B aligned segments)
   DBuf d_rx, d_goff;
   bool lib_loaded = false;
   // table
@@ -190,6 +191,9 @@ struct apex_ctx {
   int64_t opt_select_ctas = 16;     // CTAs per query in the select kernel
   int64_t opt_force_upload = 0;     // re-upload query descriptors on every call
   int64_t opt_refresh = 0;          // in-kernel tau refresh interval (0 = k)
+  int64_t opt_mode = 2;             // enumeration kernel: 2 = admission-first (exact short-circuit),
+                                    // 0 = full predicate (FSETP chain), 1 = full predicate (FADD2 sign bits)
+  int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
 };
 
 namespace {
@@ -328,13 +332,14 @@ int kernel_nt(int nt) {
 
 using ScanFn = void (*)(const ScanLaunch);
 
-template <int NT, int RL>
-ScanFn scan_ptr() { return scan_kernel<NT, RL>; }
+template <int NT, int RL, int MODE>
+ScanFn scan_ptr() { return scan_kernel<NT, RL, MODE>; }
 
-ScanFn pick_scan(int nt, int rl) {
-#define CASE(N)                                         \
-  case N:                                               \
-    return rl == 1 ? scan_ptr<N, 1>() : scan_ptr<N, 2>();
+ScanFn pick_scan(int nt, int rl, int mode) {
+#define CASE(N)                                                                         \
+  case N:                                                                               \
+    if (mode == 1) return rl == 1 ? scan_ptr<N, 1, 1>() : scan_ptr<N, 2, 1>();        \
+    return rl == 1 ? scan_ptr<N, 1, 0>() : scan_ptr<N, 2, 0>();
   switch (nt) {
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(14)
     CASE(16) CASE(20) CASE(24)
@@ -420,8 +425,12 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Slot& S = c->slots[i];
     const int64_t k = qs[i].k;
     const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
-    const int ntp_i = (kernel_nt(B.tests[i].nt) + 3) / 4 * 4;
-    APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp_i * sizeof(float)));
+    if (c->opt_mode == 2) {
+      APEX_TRY(S.obj_col.ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
+    } else {
+      const int ntp_i = (kernel_nt(B.tests[i].nt) + 3) / 4 * 4;
+      APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp_i * sizeof(float)));
+    }
     APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
@@ -440,6 +449,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     ScanQuery& Q = hq[i];
     std::memset(&Q, 0, sizeof(Q));
     Q.packed = S.packed.as<float>();
+    Q.obj_col = S.obj_col.as<float>();
     Q.buf = S.buf.as<Entry>();
     Q.comp = S.comp.as<Entry>();
     Q.sel = S.sel.as<Entry>();
@@ -512,7 +522,15 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr);
   ++st.launches;
   // K2 pack
-  if (plan->pair_hi > plan->pair_lo) {
+  const bool admit = c->opt_mode == 2;
+  if (admit) {
+    int64_t max_last = 1;
+    for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
+    const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
+    pack_obj_kernel<<<dim3(gx, (unsigned)c->rx.size(), nq), 256, 0, s>>>(dq, c->d_rx.as<DevReaction>(),
+                                                                        c->d_values.as<float>(), c->n_pairs);
+    ++st.launches;
+  } else if (plan->pair_hi > plan->pair_lo) {
     const int64_t n = (plan->pair_hi - plan->pair_lo) * B.ntp;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8 / nq));
     pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
@@ -568,8 +586,23 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.queries = dq;
       L.cb = cb;
       if (ci == 0) APEX_CU(cudaEventRecord(c->ev[6], s));
-      for (size_t k = 0; k + 1 < B.cls_begin.size(); ++k) {
-        ScanFn fn = pick_scan(B.cls_nt[k], B.rl);
+      if (admit) {
+        const int cba = (int)c->opt_cb_admit;
+        ScanFn fn = B.rl == 2 ? scan_admit_kernel<2> : scan_admit_kernel<1>;
+        const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
+        int occ = 0;
+        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        const int64_t blocks =
+            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
+        ScanLaunch La = L;
+        La.cb = cba;
+        fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(La);
+        APEX_CU(cudaGetLastError());
+        ++st.launches;
+        ++st.scans;
+      }
+      for (size_t k = 0; !admit && k + 1 < B.cls_begin.size(); ++k) {
+        ScanFn fn = pick_scan(B.cls_nt[k], B.rl, (int)c->opt_mode);
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
         int occ = 0;
@@ -853,6 +886,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   std::vector<DevReaction> rx(n_rx);
   std::vector<unsigned long long> goff(n_rx + 1, 0);
   unsigned __int128 total = 0;
+  int64_t pcols = 0;
   for (int t = 0; t < n_rx; ++t) {
     const apex_reaction& a = rxs[t];
     if (a.n_rgroups < 1 || a.n_rgroups > kMaxRg)
@@ -872,6 +906,8 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
     }
     if (R.size[R.c - 1] > 0xffffffffll) return set_err(APEX_ELIMIT, "last R-group larger than 2^32");
     R.n_rows = (uint64_t)(size / (unsigned __int128)R.size[R.c - 1]);
+    R.pcol_off = pcols;
+    pcols += (R.size[R.c - 1] + 3) / 4 * 4;
     if ((uint64_t)total != a.g_offset) return set_err(APEX_EINVAL, "reaction offsets are not the running product count");
     R.g_off = a.g_offset;
     goff[t] = (unsigned long long)total;
@@ -887,6 +923,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   c->goff = std::move(goff);
   c->total = (uint64_t)total;
   c->lib_pairs = n_pairs;
+  c->pcols = pcols;
   c->lib_loaded = true;
   c->batch.plan = nullptr;
   c->batch.pending = false;
@@ -996,8 +1033,9 @@ int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
   APEX_CU(cudaEventSynchronize(c->ev[7]));
   float d2h = 0;
   cudaEventElapsedTime(&d2h, c->ev[6], c->ev[7]);
-  int64_t cand = 0, out = 0;
+  int64_t cand = 0, out = 0, admitted = 0;
   for (int i = 0; i < B.nq; ++i) {
+    admitted += (int64_t)c->h_ctl.as<QCtl>()[i].admitted;
     cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
     out += (int64_t)out_bytes(std::max<int64_t>(B.qs[i].k, 1), B.qs[i].n_constraints);
   }
@@ -1005,6 +1043,7 @@ int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
   float total = d2h;
   for (int e = 0; e < 5; ++e) total += B.st.ms[e];
   fill_stats(stats, B.st, d2h, total, cand);
+  if (stats) stats->admitted = admitted;
   return APEX_OK;
 }
 
@@ -1060,6 +1099,7 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
       agg.retries += st.retries;
       agg.h2d_bytes += st.h2d_bytes;
       agg.d2h_bytes += st.d2h_bytes;
+      agg.admitted += st.admitted;
     }
     g0 = g1;
   }
@@ -1215,6 +1255,13 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "chunk_div") c->opt_chunk_div = v;
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
+  else if (n == "mode") {
+    if (v < 0 || v > 2) return set_err(APEX_EINVAL, "mode must be 0, 1 or 2");
+    c->opt_mode = v;
+  } else if (n == "cb_admit") {
+    if (v < 8 || v % 8 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 8 in [8, 4096]");
+    c->opt_cb_admit = v;
+  }
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
   else if (n == "tile_products") {
     c->opt_tile_products = v;

@@ -29,6 +29,8 @@ struct DevReaction {
   int64_t pair_off[kMaxRg];       // table row of digit 0 for each R-group
   uint64_t g_off;                 // reaction_offset
   uint64_t n_rows;                // product of sizes[0..c-2]
+  int64_t pcol_off;               // offset of the last R-group in the packed objective column (16-B aligned)
+  int64_t _pad2;
 };
 
 // One enumeration tile: rows [row0, row0+nrows) x columns [col0, col0+ncols)
@@ -59,6 +61,7 @@ struct QCtl {
   unsigned long long min_key;     // select scratch
   unsigned long long hist_base;   // candidate histogram: bin = min((key - base) >> shift, 65535)
   unsigned long long seed_max;    // max key among feasible samples
+  unsigned long long admitted;    // products that passed admission (admission-first kernel, stats)
   unsigned int hist_shift;
   unsigned int _pad1;
   unsigned int active;            // participates in the current launch
@@ -82,7 +85,8 @@ __host__ __device__ __forceinline__ unsigned long long bin_edge(unsigned bin, un
 
 // Per-query parameters (device, read-only during a launch).
 struct ScanQuery {
-  const float* packed;            // [n_pairs][ntp] signed test columns
+  const float* packed;            // [n_pairs][ntp] signed test columns (full-predicate kernel)
+  const float* obj_col;           // [pcols] signed objective column of every last R-group (admission kernel)
   Entry* buf;                     // candidate buffer (cap entries)
   Entry* comp;                    // compacted candidates (cap entries)
   Entry* sel;                     // selected top-k (k entries, unordered)

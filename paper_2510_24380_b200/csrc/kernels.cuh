@@ -172,6 +172,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
     c->hist_base = 0;
     c->hist_shift = 48;
     c->seed_max = 0;
+    c->admitted = 0;
     c->count = 0;
     c->comp_count = 0;
     c->sel_count = 0;
@@ -200,6 +201,7 @@ __global__ void pack_kernel(const ScanQuery* __restrict__ qs, const float* __res
     if (t < Q.nt) {
       v = __ldg(values + (int64_t)Q.test_task[t] * n_pairs + p);
       if (Q.test_lower[t]) v = -v;
+      if (v == 0.0f) v = 0.0f;  // never -0: the packed compare reads sign bits
     }
     dst[p * ntp + t] = v;
   }
@@ -251,6 +253,23 @@ __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n,
   }
 }
 
+// K2b: signed objective column of every reaction's last R-group, laid out at
+// 16-byte aligned per-reaction offsets (TMA bulk copies need 16-B alignment).
+__global__ void pack_obj_kernel(const ScanQuery* __restrict__ qs, const DevReaction* __restrict__ rx,
+                                const float* __restrict__ values, int64_t n_pairs) {
+  const ScanQuery& Q = qs[blockIdx.z];
+  const DevReaction& R = rx[blockIdx.y];
+  const int64_t n_last = R.size[R.c - 1];
+  const float* v = values + (int64_t)Q.test_task[0] * n_pairs + R.pair_off[R.c - 1];
+  float* dst = const_cast<float*>(Q.obj_col) + R.pcol_off;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_last; j += (int64_t)gridDim.x * blockDim.x) {
+    float y = __ldg(v + j);
+    if (Q.test_lower[0]) y = -y;
+    if (y == 0.0f) y = 0.0f;
+    dst[j] = y;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K3: fused enumeration.
 //
@@ -278,29 +297,6 @@ struct ScanLaunch {
   const ScanQuery* queries;
   int cb;                 // columns per smem block (multiple of 8)
 };
-
-template <int NT, int RL>
-__device__ __forceinline__ bool test_cols(const float* __restrict__ ys, int j, const float (&thr)[RL][NT],
-                                          bool (&pass)[RL]) {
-  constexpr int NTP = Ntp<NT>::value;
-  float y[NTP];
-  const float4* yp = reinterpret_cast<const float4*>(ys + j * NTP);
-#pragma unroll
-  for (int q = 0; q < NTP / 4; ++q) {
-    const float4 v = yp[q];
-    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
-  }
-  bool any = false;
-#pragma unroll
-  for (int r = 0; r < RL; ++r) {
-    bool p = y[0] <= thr[r][0];
-#pragma unroll
-    for (int i = 1; i < NT; ++i) p = p & (y[i] <= thr[r][i]);
-    pass[r] = p;
-    any = any | p;
-  }
-  return any;
-}
 
 // In-kernel threshold refresh (one warp): B = highest key>>48 bin such that the
 // candidates appended so far with key >= B<<48 number at least k; counts are
@@ -356,12 +352,86 @@ __device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
   if (lane == 0) atomicMax(&Q.ctl->tau_key, key);
 }
 
+template <int NT, int RL>
+__device__ __forceinline__ bool test_cols(const float* __restrict__ ys, int j, const float (&thr)[RL][NT],
+                                          bool (&pass)[RL]) {
+  constexpr int NTP = Ntp<NT>::value;
+  float y[NTP];
+  const float4* yp = reinterpret_cast<const float4*>(ys + j * NTP);
+#pragma unroll
+  for (int q = 0; q < NTP / 4; ++q) {
+    const float4 v = yp[q];
+    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+  }
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < RL; ++r) {
+    bool p = y[0] <= thr[r][0];
+#pragma unroll
+    for (int i = 1; i < NT; ++i) p = p & (y[i] <= thr[r][i]);
+    pass[r] = p;
+    any = any | p;
+  }
+  return any;
+}
+
+// Packed variant: two tests per instruction.  With t' = nextup(t) (t' = -inf
+// for "no x qualifies", +inf for "all"), y <= t  <=>  fl(y - t') < 0, whose
+// sign bit is exact (IEEE subtraction never rounds across zero; y is never -0
+// after packing).  d = y - t' for a pair of tests is one FADD2 (fp32x2,
+// FMA pipe); the pass bits are ANDed with LOP3 (ALU).
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+template <int NT>
+struct Np { static constexpr int value = (NT + 1) / 2; };
+
+template <int NT, int RL>
+__device__ __forceinline__ unsigned test_cols2(const float* __restrict__ ys, int j,
+                                               const unsigned long long (&tp)[RL][Np<NT>::value],
+                                               unsigned (&acc)[RL]) {
+  constexpr int NTP = Ntp<NT>::value;
+  constexpr int NP = Np<NT>::value;
+  unsigned long long y[NTP / 2];
+  const ulonglong2* yp = reinterpret_cast<const ulonglong2*>(ys + j * NTP);
+#pragma unroll
+  for (int q = 0; q < NTP / 4; ++q) {
+    const ulonglong2 v = yp[q];
+    y[2 * q] = v.x;
+    y[2 * q + 1] = v.y;
+  }
+  unsigned any = 0;
+#pragma unroll
+  for (int r = 0; r < RL; ++r) {
+    unsigned a = 0xffffffffu;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const unsigned long long d = fsub2(y[p], tp[r][p]);
+      a = a & (unsigned)d & (unsigned)(d >> 32);
+    }
+    acc[r] = a;
+    any = any | a;
+  }
+  return any;
+}
+
+// threshold t (y <= t) -> t' for the packed form
+__device__ __forceinline__ float tprime(float t) {
+  if (t != t) return __int_as_float(0xff800000);          // none: -inf
+  if (t == __int_as_float(0x7f800000)) return t;          // all: +inf
+  return next_up(t);
+}
+
 template <int NT>
 constexpr int scan_min_blocks() { return NT <= 12 ? 3 : 2; }
 
-template <int NT, int RL>
+template <int NT, int RL, int MODE>
 __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_kernel(const ScanLaunch L) {
   constexpr int NTP = Ntp<NT>::value;
+  constexpr int NP = Np<NT>::value;
   extern __shared__ __align__(128) unsigned char sm_raw[];
   const ScanQuery& Q = L.queries[blockIdx.y];
   QCtl* ctl = Q.ctl;
@@ -390,6 +460,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
   const int nt = Q.nt;
   const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
   const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
+  // value of padding columns: never passes in either compare form
+  const float pad_y = MODE == 1 ? __int_as_float(0x7f800000) : __int_as_float(0x7fffffff);
 
   for (;;) {
     unsigned t = 0;
@@ -461,6 +533,17 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
       }
       if (!valid) thr[r][0] = __int_as_float(0x7fffffff);  // NaN: never passes
     }
+    unsigned long long tp[RL][NP];
+    if constexpr (MODE == 1) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const float lo = tprime(thr[r][2 * p]);
+          const float hi = 2 * p + 1 < NT ? tprime(thr[r][2 * p + 1]) : __int_as_float(0x7f800000);
+          tp[r][p] = (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+        }
+    }
 
     for (int blk = 0; blk < nblk; ++blk) {
       const int col_base = blk * cb;
@@ -479,30 +562,49 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
         const double ts = key_to_score(tau_now);
 #pragma unroll
         for (int r = 0; r < RL; ++r)
-          if (lane + 32u * r < T.nrows)
+          if (lane + 32u * r < T.nrows) {
             thr[r][0] = maximize ? -thr_lower_fast(p_obj[r], b_obj, ts) : thr_upper_fast(p_obj[r], b_obj, -ts);
+            if constexpr (MODE == 1)
+              tp[r][0] = (tp[r][0] & 0xffffffff00000000ull) | __float_as_uint(tprime(thr[r][0]));
+          }
       }
       if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
       else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
       float* ys = bi ? sbuf1 : sbuf0;
       const int ngroups = (ncol + 7) >> 3;
       if (ncol & 7) {
-        // pad the last group with NaN columns (never pass: NaN <= t is false)
+        // pad the last group with columns that never pass
         const int pad = (ngroups << 3) - ncol;
-        for (int idx = (int)lane; idx < pad * NTP; idx += 32) ys[ncol * NTP + idx] = __int_as_float(0x7fffffff);
+        for (int idx = (int)lane; idx < pad * NTP; idx += 32) ys[ncol * NTP + idx] = pad_y;
         __syncwarp();
       }
 
       for (int gi = 0; gi < ngroups; ++gi) {
         const int j0 = gi << 3;
         bool any = false;
-        bool pass[RL];
+        if constexpr (MODE == 1) {
+          unsigned acc[RL];
+          unsigned anyw = 0;
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+          for (int jj = 0; jj < 8; ++jj) anyw = anyw | test_cols2<NT, RL>(ys, j0 + jj, tp, acc);
+          any = (int)anyw < 0;
+        } else {
+          bool pass[RL];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) any = any | test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+        }
         if (__any_sync(0xffffffffu, any)) {
           // slow path: exact fp64 score, warp-aggregated append
           for (int jj = 0; jj < 8; ++jj) {
-            test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+            bool pass[RL];
+            if constexpr (MODE == 1) {
+              unsigned acc[RL];
+              test_cols2<NT, RL>(ys, j0 + jj, tp, acc);
+#pragma unroll
+              for (int r = 0; r < RL; ++r) pass[r] = (int)acc[r] < 0;
+            } else {
+              test_cols<NT, RL>(ys, j0 + jj, thr, pass);
+            }
             const float y0 = ys[(j0 + jj) * NTP];
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
@@ -527,6 +629,223 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
                 }
                 // every `refresh` candidates, the warp that crosses the mark
                 // recomputes tau from the histograms
+                if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
+                  __threadfence();
+                  refresh_tau(Q);
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      bi ^= 1u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 (admission-first form).  Same tiles, same exact per-row threshold for the
+// admission test (s >= tau), but the hot loop streams only the signed
+// objective column: per product ONE fp32 compare (an FSETP.OR chain over 8
+// columns) and a warp vote.  The constraint predicate is evaluated, exactly in
+// fp64 in the reference's order, only for products that pass admission: the
+// predicate is a conjunction, so this short-circuit yields the same candidate
+// set as evaluating every test on every product.
+// Exact constraint predicate of one admitted product: val_i = ((p_i + x_i) + b_i)
+// for every constraint test, p_i = the row's fp64 prefix for test i's task.
+// All column loads are issued before any compare (one memory latency).
+__device__ __forceinline__ bool feasible_exact(const ScanQuery& Q, const float* __restrict__ values, int64_t n_pairs,
+                                               const double* pc, int64_t last_pair) {
+  bool ok = true;
+  for (int i0 = 1; i0 < Q.nt; i0 += 4) {
+    float x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      x[u] = i0 + u < Q.nt ? __ldg(values + (int64_t)Q.test_task[i0 + u] * n_pairs + last_pair) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u;
+      if (i < Q.nt) {
+        const double val = fx(pc[i], x[u], Q.test_bias[i]);
+        ok = ok && (Q.test_lower[i] ? (val >= Q.test_beta[i]) : (val <= Q.test_beta[i]));
+      }
+    }
+  }
+  return ok;
+}
+
+template <int RL>
+__global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const ScanLaunch L) {
+  extern __shared__ __align__(128) unsigned char sm_raw[];
+  const ScanQuery& Q = L.queries[blockIdx.y];
+  QCtl* ctl = Q.ctl;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  if (!*(volatile unsigned int*)&ctl->active) return;
+
+  const int cb = L.cb;
+  float* sbuf0 = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 2 * cb;
+  float* sbuf1 = sbuf0 + cb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + (size_t)kScanWarps * 2 * cb * sizeof(float)) + warp * 2;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  uint32_t phase0 = 0, phase1 = 0;
+  unsigned bi = 0;
+
+  Entry* __restrict__ buf = Q.buf;
+  unsigned int* __restrict__ hist = Q.hist;
+  const unsigned long long cap = Q.cap;
+  const int maximize = Q.maximize;
+  const double b_obj = Q.test_bias[0];
+  const float* __restrict__ values = L.values;
+  const int64_t n_pairs = L.n_pairs;
+  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
+  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
+  const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
+
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&ctl->tile_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0) + L.tile_begin;
+    if (t >= L.tile_end) break;
+    const Tile T = L.tiles[t];
+    const DevReaction& R = L.rx[T.rx];
+    const int c = R.c;
+    const int64_t n_last = R.size[c - 1];
+    // bulk copies need 16-B aligned sources: start the tile at col0 & ~3 and
+    // mask the `lead` columns before col0 (partial rows at range cuts)
+    const uint32_t lead = T.col0 & 3u;
+    const uint32_t ac0 = T.col0 - lead;
+    const uint32_t ncols = T.ncols + lead;
+    const int64_t last_pair0 = R.pair_off[c - 1] + ac0;
+    const float* col_src = Q.obj_col + R.pcol_off + ac0;
+    const int nblk = (int)((ncols + cb - 1) / cb);
+    if (lane == 0) {
+      const uint32_t bytes = ((ncols < (uint32_t)cb ? ncols : (uint32_t)cb) * 4u + 15u) & ~15u;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[bi], bytes);
+      bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
+    }
+    const unsigned long long tau = *(volatile unsigned long long*)&ctl->tau_key;
+    unsigned long long tau_seen = tau;
+
+    float thr[RL];
+    double p_obj[RL];
+    double pc[RL][kMaxTests];   // per-row prefix of every test's task (rare path; local memory)
+    unsigned long long gbase[RL];
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const unsigned local = lane + 32u * r;
+      const bool valid = local < T.nrows;
+      const uint64_t row = T.row0 + (valid ? local : 0u);
+      int64_t pr[kMaxRg - 1];
+      {
+        uint64_t rem = row;
+#pragma unroll
+        for (int j = kMaxRg - 2; j >= 1; --j) {
+          pr[j] = 0;
+          if (j <= c - 2) {
+            uint64_t q, d;
+            divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+            pr[j] = R.pair_off[j] + (int64_t)d;
+            rem = q;
+          }
+        }
+        pr[0] = R.pair_off[0] + (int64_t)rem;
+      }
+      gbase[r] = R.g_off + row * (uint64_t)n_last + ac0;
+      for (int i = 0; i < Q.nt; ++i) {
+        const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
+        double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+#pragma unroll
+        for (int j = 1; j < kMaxRg - 1; ++j)
+          if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+        pc[r][i] = p;
+      }
+      const double p = pc[r][0];
+      p_obj[r] = p;
+      float th = __int_as_float(0x7f800000);
+      if (tau != kNoTau) {
+        const double ts = key_to_score(tau);
+        th = maximize ? -thr_lower_fast(p, b_obj, ts) : thr_upper_fast(p, b_obj, -ts);
+      }
+      thr[r] = valid ? th : __int_as_float(0x7fffffff);
+    }
+
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int col_base = blk * cb;
+      const int ncol = min(cb, (int)ncols - col_base);
+      if (blk + 1 < nblk && lane == 0) {
+        const unsigned nb = bi ^ 1u;
+        const uint32_t bytes = ((uint32_t)min(cb, (int)ncols - col_base - cb) * 4u + 15u) & ~15u;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[nb], bytes);
+        bulk_g2s(nb ? sbuf1 : sbuf0, col_src + col_base + cb, bytes, &bars[nb]);
+      }
+      const unsigned long long tau_now = *(volatile unsigned long long*)&ctl->tau_key;
+      if (tau_now != tau_seen) {
+        tau_seen = tau_now;
+        const double ts = key_to_score(tau_now);
+#pragma unroll
+        for (int r = 0; r < RL; ++r)
+          if (lane + 32u * r < T.nrows)
+            thr[r] = maximize ? -thr_lower_fast(p_obj[r], b_obj, ts) : thr_upper_fast(p_obj[r], b_obj, -ts);
+      }
+      if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
+      else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
+      float* ys = bi ? sbuf1 : sbuf0;
+      const int ngroups = (ncol + 7) >> 3;
+      if ((ncol & 7) || (blk == 0 && lead)) {
+        const int pad = (ngroups << 3) - ncol;
+        if ((int)lane < pad) ys[ncol + lane] = pad_y;
+        if (blk == 0 && lane < lead) ys[lane] = pad_y;
+        __syncwarp();
+      }
+      for (int gi = 0; gi < ngroups; ++gi) {
+        const int j0 = gi << 3;
+        const float4 ya = *reinterpret_cast<const float4*>(ys + j0);
+        const float4 yb = *reinterpret_cast<const float4*>(ys + j0 + 4);
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const float th = thr[r];
+          any = any | (ya.x <= th) | (ya.y <= th) | (ya.z <= th) | (ya.w <= th) | (yb.x <= th) | (yb.y <= th) |
+                (yb.z <= th) | (yb.w <= th);
+        }
+        if (__any_sync(0xffffffffu, any)) {
+          // rare path: admitted products -> exact constraint check -> append
+          for (int jj = 0; jj < 8; ++jj) {
+            const float y0 = ys[j0 + jj];
+            const int col = col_base + j0 + jj;
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+              bool pass = y0 <= thr[r];
+              const unsigned adm = __ballot_sync(0xffffffffu, pass);
+              if (!adm) continue;
+              if (lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)__popc(adm));
+              if (pass) pass = feasible_exact(Q, values, n_pairs, pc[r], last_pair0 + col);
+              const unsigned m = __ballot_sync(0xffffffffu, pass);
+              if (m) {
+                const int leader = __ffs(m) - 1;
+                unsigned long long base = 0;
+                if ((int)lane == leader) base = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (pass) {
+                  const float x = maximize ? -y0 : y0;
+                  const double val = fx(p_obj[r], x, b_obj);
+                  Entry e;
+                  e.key = skey(maximize ? val : -val);
+                  e.g = gbase[r] + (unsigned long long)col;
+                  const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
+                  if (idx < cap) buf[idx] = e;
+                  const unsigned hb = hist_bin(e.key, hbase, hshift);
+                  atomicAdd(&hist[hb], 1u);
+                  atomicAdd(&Q.coarse[hb >> 8], 1u);
+                }
                 if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
                   __threadfence();
                   refresh_tau(Q);

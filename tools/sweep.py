@@ -45,6 +45,7 @@ def main():
         keys = ("pack_ms", "seed_ms", "scan_ms", "select_ms", "finalize_ms", "d2h_ms", "total_ms", "scan_kernel_ms")
         med = {k_: float(np.median([s[k_] for s in sts])) for k_ in keys}
         med["candidates"] = sts[-1]["candidates"]
+        med["admitted"] = sts[-1]["admitted"]
         med["wall_ms"] = wall * 1e3
         med["products_per_s_scan"] = shape.total * len(nq) / (med["scan_kernel_ms"] * 1e-3)
         print(json.dumps({"config": cfg, "opts": v, **{k_: round(x, 4) if isinstance(x, float) else x
