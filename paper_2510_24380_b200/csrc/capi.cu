@@ -20,6 +20,7 @@
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.cuh"
@@ -166,7 +167,13 @@ struct apex_ctx {
   bool lib_loaded = false;
   // table
   DBuf d_values, d_biases;
+  std::vector<float> h_values;           // host copy of the table (corner lists)
   std::vector<double> biases;
+  // corner seed lists (built lazily once library + table are resident)
+  DBuf d_lists, d_slot_off, d_m, d_coff;
+  int64_t corner_slots = 0;
+  unsigned long long corner_total = 0;
+  bool corners_ok = false;
   int n_tasks = 0;
   int64_t n_pairs = 0;
   bool table_loaded = false;
@@ -194,6 +201,7 @@ struct apex_ctx {
   int64_t opt_mode = 2;             // enumeration kernel: 2 = admission-first (exact short-circuit),
                                     // 0 = full predicate (FSETP chain), 1 = full predicate (FADD2 sign bits)
   int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
+  int64_t opt_corner = 1;           // corner seed on/off
 };
 
 namespace {
@@ -356,16 +364,91 @@ size_t scan_smem(int nt, int cb) {
 int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
   // cached per (kernel, smem): the attribute call and the occupancy query cost
   // microseconds on every launch otherwise
+  // (the dynamic-smem attribute is per kernel: only ever raise it, so a cached
+  // occupancy for a larger request stays launchable)
   static thread_local std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
+  static thread_local std::vector<std::pair<const void*, size_t>> attr;
   for (auto& e : cache)
     if (e.first.first == (const void*)fn && e.first.second == smem) {
       *occ = e.second;
       return APEX_OK;
     }
-  APEX_CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  size_t cur = 0;
+  for (auto& a : attr)
+    if (a.first == (const void*)fn) cur = a.second;
+  if (smem > cur) {
+    APEX_CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bool found = false;
+    for (auto& a : attr)
+      if (a.first == (const void*)fn) { a.second = smem; found = true; }
+    if (!found) attr.push_back({(const void*)fn, smem});
+  }
   APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, (const void*)fn, kScanWarps * 32, smem));
   if (*occ < 1) return set_err(APEX_ELIMIT, "enumeration kernel does not fit on an SM");
   cache.push_back({{(const void*)fn, smem}, *occ});
+  return APEX_OK;
+}
+
+// Corner seed lists: for every task, direction and (reaction, R-group) the
+// digits of the best-m synthons (largest values for maximize, smallest for
+// minimize), m chosen so a reaction's corner has ~4096 products.
+int build_corners(apex_ctx* c) {
+  const int n_rx = (int)c->rx.size();
+  std::vector<int32_t> slot_off((size_t)n_rx * kMaxRg, 0), m((size_t)n_rx * kMaxRg, 0);
+  std::vector<unsigned long long> coff(n_rx + 1, 0);
+  static const int base_c[kMaxRg + 1] = {1, 4096, 64, 16, 8, 5, 4};
+  int64_t slots = 0;
+  for (int t = 0; t < n_rx; ++t) {
+    const DevReaction& R = c->rx[t];
+    unsigned long long prod = 1;
+    for (int j = 0; j < R.c; ++j) {
+      const int mj = (int)std::min<int64_t>(R.size[j], base_c[R.c]);
+      m[(size_t)t * kMaxRg + j] = mj;
+      slot_off[(size_t)t * kMaxRg + j] = (int32_t)slots;
+      slots += mj;
+      prod *= (unsigned long long)mj;
+    }
+    coff[t + 1] = coff[t] + prod;
+  }
+  if (slots > INT32_MAX) return set_err(APEX_ELIMIT, "corner lists too large");
+  std::vector<int32_t> lists((size_t)c->n_tasks * 2 * slots);
+  auto work = [&](int task) {
+    std::vector<int32_t> idx;
+    for (int dir = 0; dir < 2; ++dir) {
+      int32_t* out = lists.data() + ((size_t)task * 2 + dir) * slots;
+      for (int t = 0; t < n_rx; ++t) {
+        const DevReaction& R = c->rx[t];
+        for (int j = 0; j < R.c; ++j) {
+          const float* v = c->h_values.data() + (size_t)task * c->n_pairs + R.pair_off[j];
+          const int64_t n = R.size[j];
+          const int mj = m[(size_t)t * kMaxRg + j];
+          idx.resize(n);
+          std::iota(idx.begin(), idx.end(), 0);
+          if (mj < n) {
+            if (dir == 0)
+              std::nth_element(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] > v[b]; });
+            else
+              std::nth_element(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b]; });
+          }
+          std::copy(idx.begin(), idx.begin() + mj, out + slot_off[(size_t)t * kMaxRg + j]);
+        }
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int task = 0; task < c->n_tasks; ++task) th.emplace_back(work, task);
+  for (auto& x : th) x.join();
+  APEX_TRY(c->d_lists.ensure(std::max<size_t>(1, lists.size()) * sizeof(int32_t)));
+  APEX_TRY(c->d_slot_off.ensure(std::max<size_t>(1, slot_off.size()) * sizeof(int32_t)));
+  APEX_TRY(c->d_m.ensure(std::max<size_t>(1, m.size()) * sizeof(int32_t)));
+  APEX_TRY(c->d_coff.ensure(coff.size() * sizeof(unsigned long long)));
+  if (!lists.empty()) APEX_CU(cudaMemcpy(c->d_lists.p, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice));
+  if (!slot_off.empty()) APEX_CU(cudaMemcpy(c->d_slot_off.p, slot_off.data(), slot_off.size() * 4, cudaMemcpyHostToDevice));
+  if (!m.empty()) APEX_CU(cudaMemcpy(c->d_m.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(c->d_coff.p, coff.data(), coff.size() * 8, cudaMemcpyHostToDevice));
+  c->corner_slots = slots;
+  c->corner_total = coff[n_rx];
+  c->corners_ok = true;
   return APEX_OK;
 }
 
@@ -376,6 +459,7 @@ int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
 
 int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finalize) {
   Batch& B = c->batch;
+  if (!c->corners_ok) APEX_TRY(build_corners(c));
   // tests per query, then group queries by the kernel's test class (one scan
   // launch per class, so no query pays for another's padding)
   std::vector<QTests> tests_in(nq);
@@ -437,7 +521,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
     APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
-    APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
+    APEX_TRY(S.seed_hist.ensure(2 * kHistBins * sizeof(unsigned)));
     APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
     APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
   }
@@ -555,8 +639,30 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       P.samples = S;
       const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
       sample_kernel<<<blocks, 256, 0, s>>>(P, nq);
+      ++st.launches;
+    }
+    if (c->opt_corner && c->corners_ok) {
+      CornerLaunch CL;
+      CL.queries = dq;
+      CL.rx = c->d_rx.as<DevReaction>();
+      CL.values = c->d_values.as<float>();
+      CL.n_pairs = c->n_pairs;
+      CL.lists = c->d_lists.as<int32_t>();
+      CL.slot_off = c->d_slot_off.as<int32_t>();
+      CL.m = c->d_m.as<int32_t>();
+      CL.coff = c->d_coff.as<unsigned long long>();
+      CL.n_rx = (int)c->rx.size();
+      CL.slots = c->corner_slots;
+      CL.start = start;
+      CL.end = end;
+      const unsigned long long tot = c->corner_total;
+      const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((tot + 255) / 256, (uint64_t)c->sm_count * 8));
+      corner_kernel<<<dim3(blocks, nq), 256, 0, s>>>(CL);
+      ++st.launches;
+    }
+    {
       tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
-      st.launches += 2;
+      ++st.launches;
     }
   }
   APEX_CU(cudaEventRecord(c->ev[2], s));
@@ -852,6 +958,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_goff.release();
   c->d_values.release();
   c->d_biases.release();
+  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff}) b->release();
   c->d_queries.release();
   c->d_tau0.release();
   c->h_queries.release();
@@ -928,6 +1035,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   c->batch.plan = nullptr;
   c->batch.pending = false;
   c->plans.clear();
+  c->corners_ok = false;
   return APEX_OK;
 }
 
@@ -944,9 +1052,11 @@ int apex_load_table(apex_ctx* c, const float* values, const double* biases, int3
   if (n) APEX_CU(cudaMemcpy(c->d_values.p, values, n * sizeof(float), cudaMemcpyHostToDevice));
   APEX_CU(cudaMemcpy(c->d_biases.p, biases, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
   c->biases.assign(biases, biases + n_tasks);
+  c->h_values.assign(values, values + n);
   c->n_tasks = n_tasks;
   c->n_pairs = n_pairs;
   c->table_loaded = true;
+  c->corners_ok = false;
   return APEX_OK;
 }
 
@@ -994,9 +1104,13 @@ int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, co
   du.release();
   dw.release();
   c->biases.assign(head_b, head_b + n_tasks);
+  c->h_values.resize((size_t)n_tasks * n_pairs);
+  if (n_pairs > 0)
+    APEX_CU(cudaMemcpy(c->h_values.data(), c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float), cudaMemcpyDeviceToHost));
   c->n_tasks = n_tasks;
   c->n_pairs = n_pairs;
   c->table_loaded = true;
+  c->corners_ok = false;
   return APEX_OK;
 }
 
@@ -1166,7 +1280,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
   APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
   APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
-  APEX_TRY(S.seed_hist.ensure(kHistBins * sizeof(unsigned)));
+  APEX_TRY(S.seed_hist.ensure(2 * kHistBins * sizeof(unsigned)));
   APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
   APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
   APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
@@ -1255,11 +1369,12 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "chunk_div") c->opt_chunk_div = v;
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
+  else if (n == "corner") c->opt_corner = v;
   else if (n == "mode") {
     if (v < 0 || v > 2) return set_err(APEX_EINVAL, "mode must be 0, 1 or 2");
     c->opt_mode = v;
   } else if (n == "cb_admit") {
-    if (v < 8 || v % 8 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 8 in [8, 4096]");
+    if (v < 16 || v % 16 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 16 in [16, 4096]");
     c->opt_cb_admit = v;
   }
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);

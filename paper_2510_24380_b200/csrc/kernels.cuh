@@ -165,6 +165,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
   for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) {
     Q.hist[i] = 0u;
     Q.seed_hist[i] = 0u;
+    Q.seed_hist[kHistBins + i] = 0u;
   }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) Q.coarse[i] = 0u;
   if (threadIdx.x == 0) {
@@ -707,11 +708,16 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
   const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
 
+  // the next tile index and the admission threshold are fetched one step
+  // ahead (L2 round trips on addresses every warp shares), so their latency
+  // overlaps the current tile / column block instead of stalling it
+  unsigned t_next = 0;
+  if (lane == 0) t_next = atomicAdd(&ctl->tile_counter, 1u);
+  unsigned long long tau_pref = *(volatile unsigned long long*)&ctl->tau_key;
   for (;;) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->tile_counter, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0) + L.tile_begin;
+    unsigned t = __shfl_sync(0xffffffffu, t_next, 0) + L.tile_begin;
     if (t >= L.tile_end) break;
+    if (lane == 0) t_next = atomicAdd(&ctl->tile_counter, 1u);
     const Tile T = L.tiles[t];
     const DevReaction& R = L.rx[T.rx];
     const int c = R.c;
@@ -730,7 +736,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
       mbar_expect_tx(&bars[bi], bytes);
       bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
     }
-    const unsigned long long tau = *(volatile unsigned long long*)&ctl->tau_key;
+    const unsigned long long tau = tau_pref;
     unsigned long long tau_seen = tau;
 
     float thr[RL];
@@ -786,7 +792,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
         mbar_expect_tx(&bars[nb], bytes);
         bulk_g2s(nb ? sbuf1 : sbuf0, col_src + col_base + cb, bytes, &bars[nb]);
       }
-      const unsigned long long tau_now = *(volatile unsigned long long*)&ctl->tau_key;
+      const unsigned long long tau_now = tau_pref;
+      tau_pref = *(volatile unsigned long long*)&ctl->tau_key;  // consumed at the next block
       if (tau_now != tau_seen) {
         tau_seen = tau_now;
         const double ts = key_to_score(tau_now);
@@ -798,27 +805,28 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
       if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
       else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
       float* ys = bi ? sbuf1 : sbuf0;
-      const int ngroups = (ncol + 7) >> 3;
-      if ((ncol & 7) || (blk == 0 && lead)) {
-        const int pad = (ngroups << 3) - ncol;
+      const int ngroups = (ncol + 15) >> 4;
+      if ((ncol & 15) || (blk == 0 && lead)) {
+        const int pad = (ngroups << 4) - ncol;
         if ((int)lane < pad) ys[ncol + lane] = pad_y;
         if (blk == 0 && lane < lead) ys[lane] = pad_y;
         __syncwarp();
       }
       for (int gi = 0; gi < ngroups; ++gi) {
-        const int j0 = gi << 3;
+        const int j0 = gi << 4;
         const float4 ya = *reinterpret_cast<const float4*>(ys + j0);
         const float4 yb = *reinterpret_cast<const float4*>(ys + j0 + 4);
+        const float4 yc = *reinterpret_cast<const float4*>(ys + j0 + 8);
+        const float4 yd = *reinterpret_cast<const float4*>(ys + j0 + 12);
+        // min over the 16 columns (FMNMX3 chain), one compare per row
+        const float ymin = fminf(fminf(fminf(fminf(ya.x, ya.y), fminf(ya.z, ya.w)), fminf(fminf(yb.x, yb.y), fminf(yb.z, yb.w))),
+                                 fminf(fminf(fminf(yc.x, yc.y), fminf(yc.z, yc.w)), fminf(fminf(yd.x, yd.y), fminf(yd.z, yd.w))));
         bool any = false;
 #pragma unroll
-        for (int r = 0; r < RL; ++r) {
-          const float th = thr[r];
-          any = any | (ya.x <= th) | (ya.y <= th) | (ya.z <= th) | (ya.w <= th) | (yb.x <= th) | (yb.y <= th) |
-                (yb.z <= th) | (yb.w <= th);
-        }
+        for (int r = 0; r < RL; ++r) any = any | (ymin <= thr[r]);
         if (__any_sync(0xffffffffu, any)) {
           // rare path: admitted products -> exact constraint check -> append
-          for (int jj = 0; jj < 8; ++jj) {
+          for (int jj = 0; jj < 16; ++jj) {
             const float y0 = ys[j0 + jj];
             const int col = col_base + j0 + jj;
 #pragma unroll
@@ -940,26 +948,97 @@ __global__ void sample_kernel(const SampleLaunch P, int nq) {
 }
 
 // ---------------------------------------------------------------------------
+// Seed, part 2: the "corner" of every reaction — all combinations of the
+// best-m synthons of each R-group for the query's objective direction (lists
+// precomputed per task at table load).  For additive scores the top-k products
+// concentrate there, so the k-th best feasible corner product is a tight,
+// valid admission threshold.  Counted in seed_hist[kHistBins ..] (disjoint
+// from the uniform samples' histogram).
+struct CornerLaunch {
+  const ScanQuery* queries;
+  const DevReaction* rx;
+  const float* values;
+  int64_t n_pairs;
+  const int32_t* lists;              // [n_tasks][2][slots] digits (dir 0 = largest, 1 = smallest)
+  const int32_t* slot_off;           // [n_rx * kMaxRg] offset of (t, j)'s list within a (task, dir) block
+  const int32_t* m;                  // [n_rx * kMaxRg] list length of (t, j)
+  const unsigned long long* coff;    // [n_rx + 1] corner product prefix sums
+  int n_rx;
+  int64_t slots;                     // list entries per (task, dir)
+  unsigned long long start, end;
+};
+
+__global__ void corner_kernel(const CornerLaunch P) {
+  const ScanQuery& Q = P.queries[blockIdx.y];
+  if (!*(volatile unsigned int*)&Q.ctl->active) return;
+  const unsigned long long total = P.coff[P.n_rx];
+  const int dir = Q.maximize ? 0 : 1;
+  const int32_t* list = P.lists + ((int64_t)Q.test_task[0] * 2 + dir) * P.slots;
+  const unsigned lane = lane_id();
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base_i = (unsigned long long)blockIdx.x * blockDim.x; base_i < total; base_i += stride) {
+    const unsigned long long i = base_i + threadIdx.x;
+    unsigned long long key = 0;
+    if (i < total) {
+      int a = 0, b = P.n_rx;
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (P.coff[mid] <= i) a = mid; else b = mid;
+      }
+      const DevReaction& R = P.rx[a];
+      unsigned long long rem = i - P.coff[a];
+      int64_t pr[kMaxRg];
+      unsigned long long g = 0;
+      int64_t dig[kMaxRg];
+      for (int j = R.c - 1; j >= 0; --j) {
+        const int mj = P.m[a * kMaxRg + j];
+        const int idx = (int)(rem % (unsigned long long)mj);
+        rem /= (unsigned long long)mj;
+        dig[j] = list[P.slot_off[a * kMaxRg + j] + idx];
+        pr[j] = R.pair_off[j] + dig[j];
+      }
+      for (int j = 0; j < R.c; ++j) g = g * (unsigned long long)R.size[j] + (unsigned long long)dig[j];
+      g += R.g_off;
+      if (g >= P.start && g < P.end) {
+        bool feasible = true;
+        for (int t = 1; t < Q.nt && feasible; ++t) {
+          const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
+          double val = (double)__ldg(v + pr[0]);
+          for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+          val = __dadd_rn(val, Q.test_bias[t]);
+          feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
+        }
+        if (feasible) {
+          const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
+          double val = (double)__ldg(v + pr[0]);
+          for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+          val = __dadd_rn(val, Q.test_bias[0]);
+          key = skey(Q.maximize ? val : -val);
+          atomicAdd(&Q.seed_hist[kHistBins + (key >> 48)], 1u);
+        }
+      }
+    }
+    unsigned long long mx = key;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0 && mx) atomicMax(&Q.ctl->seed_max, mx);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // tau from a key histogram: B = highest bin with sum_{b >= B} hist[b] >= k.
 // At least k distinct feasible products have key >= B<<48, so it is a valid
 // lower bound on the final k-th best key (never discards a true top-k
 // product).  mode 0: seed_hist -> raise tau_key; mode 1: hist -> raise
 // tau_key; mode 2: hist -> bound_key (final compaction bound).
-__device__ __forceinline__ unsigned long long wsum_total(const unsigned long long* w) {
-  unsigned long long t = 0;
-  for (int i = 0; i < 32; ++i) t += w[i];
-  return t;
-}
-
-__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode) {
-  const ScanQuery& Q = qs[blockIdx.x];
-  QCtl* ctl = Q.ctl;
-  if (!*(volatile unsigned int*)&ctl->active) return;
-  const unsigned long long k = (unsigned long long)Q.k;
+// Block-wide search (1024 threads) of the highest bin B with
+// sum_{b >= B} h[b] >= k.  Returns B (or -1 if the total is below k) and the
+// count at/above B in *count_ge (the total if B == -1).
+__device__ int kth_bin(const unsigned int* __restrict__ h, unsigned long long k, unsigned long long* count_ge) {
   __shared__ unsigned long long wsum[32];
-  __shared__ unsigned int found;
+  __shared__ int s_bin;
+  __shared__ unsigned long long s_cnt;
   const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
-  const unsigned int* h = mode == 0 ? Q.seed_hist : Q.hist;
   constexpr int PER = kHistBins / 1024;
   unsigned long long s = 0;
   const uint4* h4 = reinterpret_cast<const uint4*>(h + t * PER);
@@ -968,51 +1047,88 @@ __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__
     const uint4 v = __ldcg(h4 + i);
     s += (unsigned long long)v.x + v.y + v.z + v.w;
   }
-  // inclusive suffix sum over threads (t .. 1023)
-  unsigned long long incl = s;
+  unsigned long long incl = s;  // inclusive suffix sum over lanes (lane .. 31)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const unsigned long long o = __shfl_down_sync(0xffffffffu, incl, off);
     if (lane + off < 32) incl += o;
   }
   if (lane == 0) wsum[w] = incl;
-  if (t == 0) found = 0;
+  if (t == 0) {
+    s_bin = -1;
+    s_cnt = 0;
+  }
   __syncthreads();
-  unsigned long long above = 0;  // sum over warps > w
-  for (unsigned v = w + 1; v < 32; ++v) above += wsum[v];
+  unsigned long long above = 0, total = 0;
+  for (unsigned v = 0; v < 32; ++v) {
+    total += wsum[v];
+    if (v > w) above += wsum[v];
+  }
   const unsigned long long suffix_incl = incl + above;   // bins >= t*PER
   const unsigned long long suffix_excl = suffix_incl - s; // bins >= (t+1)*PER
   if (suffix_excl < k && suffix_incl >= k) {
     unsigned long long acc = suffix_excl;
-    int B = t * PER;
     for (int b = (int)(t * PER + PER - 1); b >= (int)(t * PER); --b) {
       acc += __ldcg(h + b);
-      if (acc >= k) { B = b; break; }
+      if (acc >= k) {
+        s_bin = b;
+        s_cnt = acc;
+        break;
+      }
     }
-    const unsigned long long key =
-        mode == 0 ? ((unsigned long long)B << 48) : bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift);
-    if (mode == 0) {
-      // seed threshold; candidate histogram re-based on it, with the sampled
-      // range [tau, seed_max] spread over ~1/4 of the bins
-      if (key > ctl->tau_key) ctl->tau_key = key;
-      const unsigned long long base = ctl->tau_key;
-      const unsigned long long range = ctl->seed_max > base ? ctl->seed_max - base : 0ull;
-      unsigned shift = 0;
-      while (shift < 48 && (range >> shift) >= 16384ull) ++shift;
-      ctl->hist_base = base;
-      ctl->hist_shift = shift;
-    } else if (mode == 1) {
-      if (key > ctl->tau_key) ctl->tau_key = key;
-    } else {
-      ctl->bound_key = key;
-      ctl->comp_count = acc;  // candidates with key >= bound
-    }
-    found = 1;
   }
   __syncthreads();
-  if (t == 0 && !found && mode == 2) {  // fewer than k candidates: keep all
-    ctl->bound_key = 0;
-    ctl->comp_count = wsum_total(wsum);
+  const int B = s_bin;
+  *count_ge = B >= 0 ? s_cnt : total;
+  __syncthreads();
+  return B;
+}
+
+// tau from key histograms (one CTA of 1024 threads per query).  At least k
+// distinct feasible products have key >= the returned bin's lower edge, so it
+// is a valid lower bound on the final k-th best key.
+//   mode 0: seed — max over the uniform-sample and the corner histograms
+//           (separate, so no product is counted twice); the candidate
+//           histogram is then re-based on tau with the seeded range [tau,
+//           seed_max] spread over ~1/4 of its bins;
+//   mode 1: raise tau from the candidate histogram;
+//   mode 2: final bound (and the count at/above it) for the select.
+__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode) {
+  const ScanQuery& Q = qs[blockIdx.x];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  const unsigned long long k = (unsigned long long)Q.k;
+  unsigned long long cnt = 0;
+  if (mode == 0) {
+    const int b0 = kth_bin(Q.seed_hist, k, &cnt);
+    const int b1 = kth_bin(Q.seed_hist + kHistBins, k, &cnt);
+    if (threadIdx.x == 0) {
+      unsigned long long key = kNoTau;
+      if (b0 >= 0) key = (unsigned long long)b0 << 48;
+      if (b1 >= 0) key = max(key, (unsigned long long)b1 << 48);
+      if (key > ctl->tau_key) ctl->tau_key = key;
+      if (ctl->tau_key != kNoTau) {
+        const unsigned long long base = ctl->tau_key;
+        const unsigned long long range = ctl->seed_max > base ? ctl->seed_max - base : 0ull;
+        unsigned shift = 0;
+        while (shift < 48 && (range >> shift) >= 16384ull) ++shift;
+        ctl->hist_base = base;
+        ctl->hist_shift = shift;
+      }
+    }
+  } else {
+    const int B = kth_bin(Q.hist, k, &cnt);
+    if (threadIdx.x == 0) {
+      if (mode == 1) {
+        if (B >= 0) {
+          const unsigned long long key = bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift);
+          if (key > ctl->tau_key) ctl->tau_key = key;
+        }
+      } else {
+        ctl->bound_key = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
+        ctl->comp_count = cnt;  // candidates with key >= bound
+      }
+    }
   }
 }
 
