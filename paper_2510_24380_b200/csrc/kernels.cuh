@@ -653,41 +653,47 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
 // fp64 in the reference's order, only for products that pass admission: the
 // predicate is a conjunction, so this short-circuit yields the same candidate
 // set as evaluating every test on every product.
-// Exact constraint predicate of one admitted product: val_i = ((p_i + x_i) + b_i)
-// for every constraint test, p_i = the row's fp64 prefix for test i's task.
-// All column loads are issued before any compare (one memory latency).
+// Exact constraint predicate of one admitted product: for every constraint
+// test, val = ((prefix + x) + bias) in the reference order, with the row's
+// prefix recomputed from the table (admitted products are rare, so the
+// kernel keeps no per-row constraint state in the hot loop).
 __device__ __forceinline__ bool feasible_exact(const ScanQuery& Q, const float* __restrict__ values, int64_t n_pairs,
-                                               const double* pc, int64_t last_pair) {
-  bool ok = true;
-  for (int i0 = 1; i0 < Q.nt; i0 += 4) {
-    float x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      x[u] = i0 + u < Q.nt ? __ldg(values + (int64_t)Q.test_task[i0 + u] * n_pairs + last_pair) : 0.0f;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u;
-      if (i < Q.nt) {
-        const double val = fx(pc[i], x[u], Q.test_bias[i]);
-        ok = ok && (Q.test_lower[i] ? (val >= Q.test_beta[i]) : (val <= Q.test_beta[i]));
-      }
-    }
+                                               const int64_t* pr, int c, int64_t last_pair) {
+  for (int i = 1; i < Q.nt; ++i) {
+    const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
+    const float x = __ldg(v + last_pair);
+    double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+    for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+    const double val = fx(p, x, Q.test_bias[i]);
+    if (Q.test_lower[i] ? !(val >= Q.test_beta[i]) : !(val <= Q.test_beta[i])) return false;
   }
-  return ok;
+  return true;
+}
+
+// min of 16 consecutive fp32 in shared memory (32-bit shared address)
+__device__ __forceinline__ float min16_shared(uint32_t addr) {
+  float a0, a1, a2, a3, b0, b1, b2, b3, c0, c1, c2, c3, d0, d1, d2, d3;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];" : "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+32];" : "=f"(c0), "=f"(c1), "=f"(c2), "=f"(c3) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+48];" : "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3) : "r"(addr));
+  return fminf(fminf(fminf(fminf(a0, a1), fminf(a2, a3)), fminf(fminf(b0, b1), fminf(b2, b3))),
+               fminf(fminf(fminf(c0, c1), fminf(c2, c3)), fminf(fminf(d0, d1), fminf(d2, d3))));
 }
 
 template <int RL>
 __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const ScanLaunch L) {
-  extern __shared__ __align__(128) unsigned char sm_raw[];
+  extern __shared__ __align__(128) float sm_f[];
   const ScanQuery& Q = L.queries[blockIdx.y];
   QCtl* ctl = Q.ctl;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   if (!*(volatile unsigned int*)&ctl->active) return;
 
   const int cb = L.cb;
-  float* sbuf0 = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 2 * cb;
-  float* sbuf1 = sbuf0 + cb;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_raw + (size_t)kScanWarps * 2 * cb * sizeof(float)) + warp * 2;
+  // shared-memory word offsets of this warp's two column buffers; indexing the
+  // extern array (not a generic pointer) keeps the loads plain LDS
+  const int off0 = (int)warp * 2 * cb, off1 = off0 + cb;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cb) + warp * 2;
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -704,16 +710,18 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   const double b_obj = Q.test_bias[0];
   const float* __restrict__ values = L.values;
   const int64_t n_pairs = L.n_pairs;
+  const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
   const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
   const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
   const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
+  constexpr int kTauPoll = 8;                      // column blocks between admission-threshold polls
 
-  // the next tile index and the admission threshold are fetched one step
-  // ahead (L2 round trips on addresses every warp shares), so their latency
-  // overlaps the current tile / column block instead of stalling it
+  // the next tile index and the admission threshold are fetched ahead of use
+  // (L2 round trips on addresses every warp shares)
   unsigned t_next = 0;
   if (lane == 0) t_next = atomicAdd(&ctl->tile_counter, 1u);
   unsigned long long tau_pref = *(volatile unsigned long long*)&ctl->tau_key;
+  int poll = 0;
   for (;;) {
     unsigned t = __shfl_sync(0xffffffffu, t_next, 0) + L.tile_begin;
     if (t >= L.tile_end) break;
@@ -734,45 +742,39 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
       const uint32_t bytes = ((ncols < (uint32_t)cb ? ncols : (uint32_t)cb) * 4u + 15u) & ~15u;
       fence_proxy_async();
       mbar_expect_tx(&bars[bi], bytes);
-      bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
+      bulk_g2s(sm_f + (bi ? off1 : off0), col_src, bytes, &bars[bi]);
     }
     const unsigned long long tau = tau_pref;
     unsigned long long tau_seen = tau;
 
     float thr[RL];
     double p_obj[RL];
-    double pc[RL][kMaxTests];   // per-row prefix of every test's task (rare path; local memory)
+    int64_t pr[RL][kMaxRg - 1];
     unsigned long long gbase[RL];
 #pragma unroll
     for (int r = 0; r < RL; ++r) {
       const unsigned local = lane + 32u * r;
       const bool valid = local < T.nrows;
       const uint64_t row = T.row0 + (valid ? local : 0u);
-      int64_t pr[kMaxRg - 1];
       {
         uint64_t rem = row;
 #pragma unroll
         for (int j = kMaxRg - 2; j >= 1; --j) {
-          pr[j] = 0;
+          pr[r][j] = 0;
           if (j <= c - 2) {
             uint64_t q, d;
             divmod_u64(q, d, rem, (uint64_t)R.size[j]);
-            pr[j] = R.pair_off[j] + (int64_t)d;
+            pr[r][j] = R.pair_off[j] + (int64_t)d;
             rem = q;
           }
         }
-        pr[0] = R.pair_off[0] + (int64_t)rem;
+        pr[r][0] = R.pair_off[0] + (int64_t)rem;
       }
       gbase[r] = R.g_off + row * (uint64_t)n_last + ac0;
-      for (int i = 0; i < Q.nt; ++i) {
-        const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
-        double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+      double p = c > 1 ? (double)__ldg(vobj + pr[r][0]) : 0.0;
 #pragma unroll
-        for (int j = 1; j < kMaxRg - 1; ++j)
-          if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-        pc[r][i] = p;
-      }
-      const double p = pc[r][0];
+      for (int j = 1; j < kMaxRg - 1; ++j)
+        if (j < c - 1) p = __dadd_rn(p, (double)__ldg(vobj + pr[r][j]));
       p_obj[r] = p;
       float th = __int_as_float(0x7f800000);
       if (tau != kNoTau) {
@@ -790,44 +792,44 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
         const uint32_t bytes = ((uint32_t)min(cb, (int)ncols - col_base - cb) * 4u + 15u) & ~15u;
         fence_proxy_async();
         mbar_expect_tx(&bars[nb], bytes);
-        bulk_g2s(nb ? sbuf1 : sbuf0, col_src + col_base + cb, bytes, &bars[nb]);
+        bulk_g2s(sm_f + (nb ? off1 : off0), col_src + col_base + cb, bytes, &bars[nb]);
       }
-      const unsigned long long tau_now = tau_pref;
-      tau_pref = *(volatile unsigned long long*)&ctl->tau_key;  // consumed at the next block
-      if (tau_now != tau_seen) {
-        tau_seen = tau_now;
-        const double ts = key_to_score(tau_now);
+      if (++poll == kTauPoll) {
+        poll = 0;
+        const unsigned long long tau_now = tau_pref;
+        tau_pref = *(volatile unsigned long long*)&ctl->tau_key;  // consumed at the next poll
+        if (tau_now != tau_seen) {
+          tau_seen = tau_now;
+          const double ts = key_to_score(tau_now);
 #pragma unroll
-        for (int r = 0; r < RL; ++r)
-          if (lane + 32u * r < T.nrows)
-            thr[r] = maximize ? -thr_lower_fast(p_obj[r], b_obj, ts) : thr_upper_fast(p_obj[r], b_obj, -ts);
+          for (int r = 0; r < RL; ++r)
+            if (lane + 32u * r < T.nrows)
+              thr[r] = maximize ? -thr_lower_fast(p_obj[r], b_obj, ts) : thr_upper_fast(p_obj[r], b_obj, -ts);
+        }
       }
       if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
       else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
-      float* ys = bi ? sbuf1 : sbuf0;
+      const int yo = bi ? off1 : off0;
       const int ngroups = (ncol + 15) >> 4;
       if ((ncol & 15) || (blk == 0 && lead)) {
         const int pad = (ngroups << 4) - ncol;
-        if ((int)lane < pad) ys[ncol + lane] = pad_y;
-        if (blk == 0 && lane < lead) ys[lane] = pad_y;
+        if ((int)lane < pad) sm_f[yo + ncol + lane] = pad_y;
+        if (blk == 0 && lane < lead) sm_f[yo + lane] = pad_y;
         __syncwarp();
       }
+      float thr_min = thr[0];
+#pragma unroll
+      for (int r = 1; r < RL; ++r) thr_min = fmaxf(thr_min, thr[r]);
+      const uint32_t ybase = smem_u32(sm_f) + (uint32_t)yo * 4u;
       for (int gi = 0; gi < ngroups; ++gi) {
         const int j0 = gi << 4;
-        const float4 ya = *reinterpret_cast<const float4*>(ys + j0);
-        const float4 yb = *reinterpret_cast<const float4*>(ys + j0 + 4);
-        const float4 yc = *reinterpret_cast<const float4*>(ys + j0 + 8);
-        const float4 yd = *reinterpret_cast<const float4*>(ys + j0 + 12);
-        // min over the 16 columns (FMNMX3 chain), one compare per row
-        const float ymin = fminf(fminf(fminf(fminf(ya.x, ya.y), fminf(ya.z, ya.w)), fminf(fminf(yb.x, yb.y), fminf(yb.z, yb.w))),
-                                 fminf(fminf(fminf(yc.x, yc.y), fminf(yc.z, yc.w)), fminf(fminf(yd.x, yd.y), fminf(yd.z, yd.w))));
-        bool any = false;
-#pragma unroll
-        for (int r = 0; r < RL; ++r) any = any | (ymin <= thr[r]);
-        if (__any_sync(0xffffffffu, any)) {
+        // min over the 16 columns (4 broadcast LDS.128 + FMNMX3 chain), one
+        // compare per lane, one vote per warp
+        const float ymin = min16_shared(ybase + (uint32_t)j0 * 4u);
+        if (__any_sync(0xffffffffu, ymin <= thr_min)) {
           // rare path: admitted products -> exact constraint check -> append
           for (int jj = 0; jj < 16; ++jj) {
-            const float y0 = ys[j0 + jj];
+            const float y0 = sm_f[yo + j0 + jj];
             const int col = col_base + j0 + jj;
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
@@ -835,7 +837,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
               const unsigned adm = __ballot_sync(0xffffffffu, pass);
               if (!adm) continue;
               if (lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)__popc(adm));
-              if (pass) pass = feasible_exact(Q, values, n_pairs, pc[r], last_pair0 + col);
+              if (pass) pass = feasible_exact(Q, values, n_pairs, pr[r], c, last_pair0 + col);
               const unsigned m = __ballot_sync(0xffffffffu, pass);
               if (m) {
                 const int leader = __ffs(m) - 1;
