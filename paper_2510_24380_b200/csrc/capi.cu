@@ -198,8 +198,10 @@ struct apex_ctx {
   int64_t opt_select_ctas = 16;     // CTAs per query in the select kernel
   int64_t opt_force_upload = 0;     // re-upload query descriptors on every call
   int64_t opt_refresh = 0;          // in-kernel tau refresh interval (0 = k)
-  int64_t opt_mode = 2;             // enumeration kernel: 2 = admission-first (exact short-circuit),
-                                    // 0 = full predicate (FSETP chain), 1 = full predicate (FADD2 sign bits)
+  int64_t opt_mode = 3;             // enumeration kernel: 3 = automatic per query (admission-first when
+                                    // the seed found a threshold, else full predicate), 2 = admission-first
+                                    // (exact short-circuit), 0 = full predicate (FSETP chain),
+                                    // 1 = full predicate (FADD2 sign bits)
   int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
 };
@@ -509,9 +511,8 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Slot& S = c->slots[i];
     const int64_t k = qs[i].k;
     const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
-    if (c->opt_mode == 2) {
-      APEX_TRY(S.obj_col.ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
-    } else {
+    if (c->opt_mode >= 2) APEX_TRY(S.obj_col.ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
+    if (c->opt_mode != 2) {
       const int ntp_i = (kernel_nt(B.tests[i].nt) + 3) / 4 * 4;
       APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp_i * sizeof(float)));
     }
@@ -603,21 +604,20 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     st.h2d_bytes += nq * 8;
   }
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr);
+  // kernel choice: admission-first (admit), full predicate (full), or per query (auto)
+  const bool admit = c->opt_mode >= 2;
+  const bool full = c->opt_mode != 2;
+  const bool autok = c->opt_mode == 3 && !tau0;
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
+                                      (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
-  // K2 pack
-  const bool admit = c->opt_mode == 2;
+  // K2 pack of the streamed objective column
   if (admit) {
     int64_t max_last = 1;
     for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
     const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
     pack_obj_kernel<<<dim3(gx, (unsigned)c->rx.size(), nq), 256, 0, s>>>(dq, c->d_rx.as<DevReaction>(),
                                                                         c->d_values.as<float>(), c->n_pairs);
-    ++st.launches;
-  } else if (plan->pair_hi > plan->pair_lo) {
-    const int64_t n = (plan->pair_hi - plan->pair_lo) * B.ntp;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8 / nq));
-    pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
     ++st.launches;
   }
   APEX_CU(cudaEventRecord(c->ev[1], s));
@@ -661,9 +661,16 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       ++st.launches;
     }
     {
-      tau_kernel<<<nq, 1024, 0, s>>>(dq, 0);
+      tau_kernel<<<nq, 1024, 0, s>>>(dq, 0, autok ? 1 : 0);
       ++st.launches;
     }
+  }
+  // K2 pack of the full-predicate columns (queries that use that kernel)
+  if (full && plan->pair_hi > plan->pair_lo) {
+    const int64_t n = (plan->pair_hi - plan->pair_lo) * B.ntp;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8 / nq));
+    pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
+    ++st.launches;
   }
   APEX_CU(cudaEventRecord(c->ev[2], s));
   // K3 enumeration: chunks x test classes
@@ -695,7 +702,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       if (admit) {
         const int cba = (int)c->opt_cb_admit;
         ScanFn fn = B.rl == 2 ? scan_admit_kernel<2> : scan_admit_kernel<1>;
-        const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
+        const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) +
+                            (size_t)kScanWarps * 16 * kMaxTests * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
         int occ = 0;
         APEX_TRY(scan_occupancy(fn, smem, &occ));
         const int64_t blocks =
@@ -707,8 +715,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         ++st.launches;
         ++st.scans;
       }
-      for (size_t k = 0; !admit && k + 1 < B.cls_begin.size(); ++k) {
-        ScanFn fn = pick_scan(B.cls_nt[k], B.rl, (int)c->opt_mode);
+      for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
+        ScanFn fn = pick_scan(B.cls_nt[k], B.rl, c->opt_mode == 1 ? 1 : 0);
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
         int occ = 0;
@@ -1317,7 +1325,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_CU(cudaEventRecord(c->ev[0], s));
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, &Q, sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
-  init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr);
+  init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr, 0u);
   merge_load_kernel<<<(unsigned)std::min<int64_t>((n_entries + 255) / 256, c->sm_count * 4), 256, 0, s>>>(
       dq, reinterpret_cast<const Entry*>(entries_dev), (unsigned long long)n_entries);
   {
@@ -1371,7 +1379,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
   else if (n == "mode") {
-    if (v < 0 || v > 2) return set_err(APEX_EINVAL, "mode must be 0, 1 or 2");
+    if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;
   } else if (n == "cb_admit") {
     if (v < 16 || v % 16 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 16 in [16, 4096]");

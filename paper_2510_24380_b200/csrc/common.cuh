@@ -63,7 +63,7 @@ struct QCtl {
   unsigned long long seed_max;    // max key among feasible samples
   unsigned long long admitted;    // products that passed admission (admission-first kernel, stats)
   unsigned int hist_shift;
-  unsigned int _pad1;
+  unsigned int use_full;          // 1: full-predicate kernel, 0: admission-first kernel
   unsigned int active;            // participates in the current launch
   unsigned int tile_counter;      // scan work distribution
   unsigned int barrier;           // select grid barrier

@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(256) precompute_kernel(const double* __restric
 // ---------------------------------------------------------------------------
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
-__global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned long long* __restrict__ tau0) {
+__global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned long long* __restrict__ tau0,
+                                unsigned use_full) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
@@ -172,6 +173,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
     c->tau_key = tau0 ? tau0[blockIdx.x] : kNoTau;
     c->hist_base = 0;
     c->hist_shift = 48;
+    c->use_full = use_full;
     c->seed_max = 0;
     c->admitted = 0;
     c->count = 0;
@@ -192,6 +194,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
 __global__ void pack_kernel(const ScanQuery* __restrict__ qs, const float* __restrict__ values, int64_t n_pairs,
                             int64_t row_lo, int64_t row_hi) {
   const ScanQuery& Q = qs[blockIdx.y];
+  if (!*(volatile unsigned*)&Q.ctl->use_full) return;
   float* dst = const_cast<float*>(Q.packed);
   const int ntp = Q.ntp;
   const int64_t n = (row_hi - row_lo) * ntp;
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
   const ScanQuery& Q = L.queries[blockIdx.y];
   QCtl* ctl = Q.ctl;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  if (!*(volatile unsigned int*)&ctl->active) return;
+  if (!*(volatile unsigned int*)&ctl->active || !*(volatile unsigned int*)&ctl->use_full) return;
 
   const int cb = L.cb;
   float* sbuf0 = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 2 * cb * NTP;
@@ -653,10 +656,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
 // fp64 in the reference's order, only for products that pass admission: the
 // predicate is a conjunction, so this short-circuit yields the same candidate
 // set as evaluating every test on every product.
-// Exact constraint predicate of one admitted product: for every constraint
-// test, val = ((prefix + x) + bias) in the reference order, with the row's
-// prefix recomputed from the table (admitted products are rare, so the
-// kernel keeps no per-row constraint state in the hot loop).
+// Exact constraint predicate of one product evaluated directly in fp64:
+// val = ((prefix + x) + bias) in the reference order (kept for tests/debug).
 __device__ __forceinline__ bool feasible_exact(const ScanQuery& Q, const float* __restrict__ values, int64_t n_pairs,
                                                const int64_t* pr, int c, int64_t last_pair) {
   for (int i = 1; i < Q.nt; ++i) {
@@ -687,13 +688,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   const ScanQuery& Q = L.queries[blockIdx.y];
   QCtl* ctl = Q.ctl;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  if (!*(volatile unsigned int*)&ctl->active) return;
+  if (!*(volatile unsigned int*)&ctl->active || *(volatile unsigned int*)&ctl->use_full) return;
 
   const int cb = L.cb;
   // shared-memory word offsets of this warp's two column buffers; indexing the
   // extern array (not a generic pointer) keeps the loads plain LDS
   const int off0 = (int)warp * 2 * cb, off1 = off0 + cb;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cb) + warp * 2;
+  const int xo = kScanWarps * 2 * cb + (int)warp * 16 * kMaxTests;  // rare-path scratch: 16 columns x tests
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cb + kScanWarps * 16 * kMaxTests) + warp * 2;
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -711,6 +713,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   const float* __restrict__ values = L.values;
   const int64_t n_pairs = L.n_pairs;
   const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
+  const int nt = Q.nt;
   const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
   const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
   const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
@@ -748,6 +751,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
     unsigned long long tau_seen = tau;
 
     float thr[RL];
+    float thrc[RL][kMaxTests];  // constraint thresholds (rare path, local memory)
+    bool thr_ready = false;
     double p_obj[RL];
     int64_t pr[RL][kMaxRg - 1];
     unsigned long long gbase[RL];
@@ -827,7 +832,31 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
         // compare per lane, one vote per warp
         const float ymin = min16_shared(ybase + (uint32_t)j0 * 4u);
         if (__any_sync(0xffffffffu, ymin <= thr_min)) {
-          // rare path: admitted products -> exact constraint check -> append
+          // rare path.  Admitted products (s >= tau) get the constraint
+          // predicate with exact per-row fp32 thresholds (computed once per
+          // tile, on first use) against the 16 columns' contributions staged
+          // in this warp's scratch; a dense cluster of admitted-but-
+          // infeasible products then costs compares, not fp64 chains.
+          if (!thr_ready) {
+            thr_ready = true;
+#pragma unroll
+            for (int r = 0; r < RL; ++r)
+              for (int i = 1; i < nt; ++i) {
+                const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
+                double p = c > 1 ? (double)__ldg(v + pr[r][0]) : 0.0;
+                for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[r][j]));
+                thrc[r][i] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
+                                             : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
+              }
+          }
+          for (int idx = (int)lane; idx < (nt - 1) * 16; idx += 32) {
+            const int i = 1 + (idx >> 4), jj = idx & 15;
+            const int col = col_base + j0 + jj;
+            float x = 0.0f;
+            if (col < (int)ncols) x = __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair0 + col);
+            sm_f[xo + idx] = Q.test_lower[i] ? -x : x;
+          }
+          __syncwarp();
           for (int jj = 0; jj < 16; ++jj) {
             const float y0 = sm_f[yo + j0 + jj];
             const int col = col_base + j0 + jj;
@@ -837,7 +866,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
               const unsigned adm = __ballot_sync(0xffffffffu, pass);
               if (!adm) continue;
               if (lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)__popc(adm));
-              if (pass) pass = feasible_exact(Q, values, n_pairs, pr[r], c, last_pair0 + col);
+              if (pass)
+                for (int i = 1; i < nt; ++i) pass = pass && (sm_f[xo + ((i - 1) << 4) + jj] <= thrc[r][i]);
               const unsigned m = __ballot_sync(0xffffffffu, pass);
               if (m) {
                 const int leader = __ffs(m) - 1;
@@ -863,6 +893,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
               }
             }
           }
+          __syncwarp();
         }
       }
       __syncwarp();
@@ -1095,7 +1126,7 @@ __device__ int kth_bin(const unsigned int* __restrict__ h, unsigned long long k,
 //           seed_max] spread over ~1/4 of its bins;
 //   mode 1: raise tau from the candidate histogram;
 //   mode 2: final bound (and the count at/above it) for the select.
-__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode) {
+__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode, int auto_kernel = 0) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* ctl = Q.ctl;
   if (!*(volatile unsigned int*)&ctl->active) return;
@@ -1117,6 +1148,10 @@ __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__
         ctl->hist_base = base;
         ctl->hist_shift = shift;
       }
+      // automatic kernel choice: without a seeded threshold (fewer than k
+      // feasible seed products) the admission test admits nearly everything,
+      // so the full-predicate kernel is cheaper
+      if (auto_kernel) ctl->use_full = ctl->tau_key == kNoTau ? 1u : 0u;
     }
   } else {
     const int B = kth_bin(Q.hist, k, &cnt);
