@@ -97,9 +97,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, obj_col, buf, comp, sel, sorted, rank, hist, seed_hist, ctl, out;
+  DBuf packed, obj_col, buf, comp, sel, sorted, rank, ctl, out;
   void release() {
-    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &hist, &seed_hist, &ctl, &out}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &ctl, &out}) b->release();
   }
 };
 
@@ -114,6 +114,8 @@ struct Plan {
   uint64_t stamp = 0;
   ~Plan() { d_tiles.release(); }
 };
+
+constexpr size_t kHistWords = (size_t)kHistBins + 256 + 2 * (size_t)kHistBins;  // hist, coarse, seed x2
 
 size_t out_bytes(int64_t k, int m) { return (size_t)k * (8 + 8 + 8 * (size_t)m + 4 + 4 * kMaxRg); }
 
@@ -180,6 +182,7 @@ struct apex_ctx {
   // query workspaces
   std::vector<Slot> slots;
   DBuf d_queries, d_tau0;
+  DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
   HBuf h_queries, h_ctl, h_out, h_tau0;
   std::vector<std::unique_ptr<Plan>> plans;
   uint64_t stamp = 0;
@@ -225,9 +228,20 @@ int check_ctx(apex_ctx* c, bool need_table) {
 // the range ends (engine.py:182-189 clipping) become single-row tiles.  Tiles
 // are shuffled with a fixed seed so any prefix of the list is a representative
 // sample of the range (used for the first chunk's threshold).
-int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) {
+int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan*& out) {
+  // tile size from the launch's total work (range x queries): big enough to
+  // amortize the per-tile setup, small enough for ~6 tiles per warp slot
+  const uint64_t span = end - start;
+  const int64_t warp_slots = (int64_t)c->sm_count * 24;
+  const int64_t target = c->opt_tile_products > 0
+                             ? c->opt_tile_products
+                             : std::max<int64_t>(8192, (int64_t)(span * (uint64_t)nq / (uint64_t)(6 * warp_slots)));
+  int64_t cols = std::max<int64_t>(64, std::min<int64_t>(4096, target / rows));
+  int64_t p2 = 64;
+  while (p2 < cols) p2 <<= 1;  // power of two: few distinct cached plans
+  cols = p2;
   for (auto& p : c->plans) {
-    if (p->start == start && p->end == end && p->rows == rows) {
+    if (p->start == start && p->end == end && p->rows == rows && p->cols == cols) {
       p->stamp = ++c->stamp;
       out = p.get();
       return APEX_OK;
@@ -238,11 +252,6 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, Plan*& out) 
   P.start = start;
   P.end = end;
   P.rows = rows;
-  const uint64_t span = end - start;
-  int64_t warp_slots = (int64_t)c->sm_count * 24;
-  int64_t target = c->opt_tile_products > 0 ? c->opt_tile_products : (int64_t)(span / (uint64_t)(8 * warp_slots));
-  int64_t cols = std::max<int64_t>(64, std::min<int64_t>(4096, target / rows));
-  cols = (cols + 63) / 64 * 64;
   P.cols = cols;
   P.pair_lo = INT64_MAX;
   P.pair_hi = 0;
@@ -426,12 +435,11 @@ int build_corners(apex_ctx* c) {
           const int mj = m[(size_t)t * kMaxRg + j];
           idx.resize(n);
           std::iota(idx.begin(), idx.end(), 0);
-          if (mj < n) {
-            if (dir == 0)
-              std::nth_element(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] > v[b]; });
-            else
-              std::nth_element(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b]; });
-          }
+          // best-first: a prefix of the list is the best-m' synthons for any m' <= m
+          if (dir == 0)
+            std::partial_sort(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] > v[b]; });
+          else
+            std::partial_sort(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b]; });
           std::copy(idx.begin(), idx.begin() + mj, out + slot_off[(size_t)t * kMaxRg + j]);
         }
       }
@@ -504,7 +512,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   B.ntp = (B.NT + 3) / 4 * 4;
   B.rl = (int)c->opt_rl;
   if (B.rl != 1 && B.rl != 2) B.rl = 1;
-  APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, B.plan));
+  APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, nq, B.plan));
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
   for (int i = 0; i < nq; ++i) {
@@ -521,11 +529,10 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
-    APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
-    APEX_TRY(S.seed_hist.ensure(2 * kHistBins * sizeof(unsigned)));
     APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
     APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
   }
+  APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
   std::vector<ScanQuery> hq(nq);
   for (int i = 0; i < nq; ++i) {
     Slot& S = c->slots[i];
@@ -540,9 +547,9 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.sel = S.sel.as<Entry>();
     Q.sorted = S.sorted.as<Entry>();
     Q.rank = S.rank.as<unsigned>();
-    Q.hist = S.hist.as<unsigned>();
-    Q.coarse = S.hist.as<unsigned>() + kHistBins;
-    Q.seed_hist = S.seed_hist.as<unsigned>();
+    Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
+    Q.coarse = Q.hist + kHistBins;
+    Q.seed_hist = Q.coarse + 256;
     Q.ctl = S.ctl.as<QCtl>();
     Q.cap = S.buf.bytes / sizeof(Entry);
     Q.refresh = (unsigned long long)std::max<int64_t>(c->opt_refresh > 0 ? c->opt_refresh : q.k, 256);
@@ -608,6 +615,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   const bool admit = c->opt_mode >= 2;
   const bool full = c->opt_mode != 2;
   const bool autok = c->opt_mode == 3 && !tau0;
+  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
@@ -624,8 +632,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // seed threshold from exact samples
   if (!tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
-                                     : (uint64_t)std::min<int64_t>(1 << 20, std::max<int64_t>(1 << 18, 64 * B.k_max));
-    S = std::min<uint64_t>(S, span);
+                                     : (uint64_t)std::min<int64_t>(1 << 18, std::max<int64_t>(1 << 15, 16 * B.k_max));
+    S = std::min<uint64_t>(S, std::max<uint64_t>(span / 32, std::min<uint64_t>(span, 4096)));
     if (S > 0) {
       SampleLaunch P;
       P.queries = dq;
@@ -655,9 +663,11 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       CL.slots = c->corner_slots;
       CL.start = start;
       CL.end = end;
-      const unsigned long long tot = c->corner_total;
-      const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((tot + 255) / 256, (uint64_t)c->sm_count * 8));
-      corner_kernel<<<dim3(blocks, nq), 256, 0, s>>>(CL);
+      // corner budget per reaction: enough corner products for ~16k feasible
+      // seeds across the reactions, within the precomputed list lengths
+      const int64_t nrx = std::max<int64_t>(1, (int64_t)c->rx.size());
+      CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, 16 * B.k_max / nrx));
+      corner_kernel<<<dim3((unsigned)c->rx.size(), nq), 256, 0, s>>>(CL);
       ++st.launches;
     }
     {
@@ -969,6 +979,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff}) b->release();
   c->d_queries.release();
   c->d_tau0.release();
+  c->d_hists.release();
   c->h_queries.release();
   c->h_ctl.release();
   c->h_out.release();
@@ -1287,8 +1298,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
   APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
   APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
-  APEX_TRY(S.hist.ensure((kHistBins + 256) * sizeof(unsigned)));
-  APEX_TRY(S.seed_hist.ensure(2 * kHistBins * sizeof(unsigned)));
+  APEX_TRY(c->d_hists.ensure(kHistWords * sizeof(unsigned)));
   APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
   APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
   APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
@@ -1303,9 +1313,9 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   Q.sel = S.sel.as<Entry>();
   Q.sorted = S.sorted.as<Entry>();
   Q.rank = S.rank.as<unsigned>();
-  Q.hist = S.hist.as<unsigned>();
-  Q.coarse = S.hist.as<unsigned>() + kHistBins;
-  Q.seed_hist = S.seed_hist.as<unsigned>();
+  Q.hist = c->d_hists.as<unsigned>();
+  Q.coarse = Q.hist + kHistBins;
+  Q.seed_hist = Q.coarse + 256;
   Q.ctl = S.ctl.as<QCtl>();
   Q.cap = (unsigned long long)cap;
   Q.refresh = 1ull << 62;
@@ -1325,6 +1335,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_CU(cudaEventRecord(c->ev[0], s));
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, &Q, sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
+  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr, 0u);
   merge_load_kernel<<<(unsigned)std::min<int64_t>((n_entries + 255) / 256, c->sm_count * 4), 256, 0, s>>>(
       dq, reinterpret_cast<const Entry*>(entries_dev), (unsigned long long)n_entries);

@@ -163,12 +163,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
-  for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) {
-    Q.hist[i] = 0u;
-    Q.seed_hist[i] = 0u;
-    Q.seed_hist[kHistBins + i] = 0u;
-  }
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) Q.coarse[i] = 0u;
+  // (the candidate / seed histograms are zeroed by one memset per batch)
   if (threadIdx.x == 0) {
     c->tau_key = tau0 ? tau0[blockIdx.x] : kNoTau;
     c->hist_base = 0;
@@ -992,54 +987,64 @@ struct CornerLaunch {
   const DevReaction* rx;
   const float* values;
   int64_t n_pairs;
-  const int32_t* lists;              // [n_tasks][2][slots] digits (dir 0 = largest, 1 = smallest)
+  const int32_t* lists;              // [n_tasks][2][slots] digits, best-first (dir 0 = largest, 1 = smallest)
   const int32_t* slot_off;           // [n_rx * kMaxRg] offset of (t, j)'s list within a (task, dir) block
   const int32_t* m;                  // [n_rx * kMaxRg] list length of (t, j)
-  const unsigned long long* coff;    // [n_rx + 1] corner product prefix sums
+  const unsigned long long* coff;    // (unused)
   int n_rx;
   int64_t slots;                     // list entries per (task, dir)
   unsigned long long start, end;
+  int budget;                        // corner products per reaction
 };
 
+// one CTA per (reaction, query): the best-m' x ... x best-m' combinations,
+// m' = floor(budget^(1/c)) capped by the list lengths
 __global__ void corner_kernel(const CornerLaunch P) {
   const ScanQuery& Q = P.queries[blockIdx.y];
   if (!*(volatile unsigned int*)&Q.ctl->active) return;
-  const unsigned long long total = P.coff[P.n_rx];
+  const int t = blockIdx.x;
+  const DevReaction& R = P.rx[t];
+  const unsigned long long off = R.g_off;
+  const unsigned long long rsize = R.n_rows * (unsigned long long)R.size[R.c - 1];
+  if (off + rsize <= P.start || off >= P.end) return;
+  int mb = P.budget;
+  if (R.c == 2) mb = (int)sqrtf((float)P.budget);
+  else if (R.c == 3) mb = (int)cbrtf((float)P.budget + 0.5f);
+  else if (R.c >= 4) mb = (int)powf((float)P.budget, 1.0f / R.c);
+  mb = max(mb, 1);
+  int mj[kMaxRg];
+  unsigned total = 1;
+  for (int j = 0; j < R.c; ++j) {
+    mj[j] = min(mb, P.m[t * kMaxRg + j]);
+    total *= (unsigned)mj[j];
+  }
   const int dir = Q.maximize ? 0 : 1;
   const int32_t* list = P.lists + ((int64_t)Q.test_task[0] * 2 + dir) * P.slots;
   const unsigned lane = lane_id();
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long base_i = (unsigned long long)blockIdx.x * blockDim.x; base_i < total; base_i += stride) {
-    const unsigned long long i = base_i + threadIdx.x;
+  for (unsigned base_i = 0; base_i < total; base_i += blockDim.x) {
+    const unsigned i = base_i + threadIdx.x;
     unsigned long long key = 0;
     if (i < total) {
-      int a = 0, b = P.n_rx;
-      while (b - a > 1) {
-        const int mid = (a + b) >> 1;
-        if (P.coff[mid] <= i) a = mid; else b = mid;
-      }
-      const DevReaction& R = P.rx[a];
-      unsigned long long rem = i - P.coff[a];
+      unsigned rem = i;
       int64_t pr[kMaxRg];
-      unsigned long long g = 0;
       int64_t dig[kMaxRg];
       for (int j = R.c - 1; j >= 0; --j) {
-        const int mj = P.m[a * kMaxRg + j];
-        const int idx = (int)(rem % (unsigned long long)mj);
-        rem /= (unsigned long long)mj;
-        dig[j] = list[P.slot_off[a * kMaxRg + j] + idx];
+        const unsigned idx = rem % (unsigned)mj[j];
+        rem /= (unsigned)mj[j];
+        dig[j] = list[P.slot_off[t * kMaxRg + j] + idx];
         pr[j] = R.pair_off[j] + dig[j];
       }
+      unsigned long long g = 0;
       for (int j = 0; j < R.c; ++j) g = g * (unsigned long long)R.size[j] + (unsigned long long)dig[j];
-      g += R.g_off;
+      g += off;
       if (g >= P.start && g < P.end) {
         bool feasible = true;
-        for (int t = 1; t < Q.nt && feasible; ++t) {
-          const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
+        for (int tt = 1; tt < Q.nt && feasible; ++tt) {
+          const float* v = P.values + (int64_t)Q.test_task[tt] * P.n_pairs;
           double val = (double)__ldg(v + pr[0]);
           for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
-          val = __dadd_rn(val, Q.test_bias[t]);
-          feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
+          val = __dadd_rn(val, Q.test_bias[tt]);
+          feasible = Q.test_lower[tt] ? (val >= Q.test_beta[tt]) : (val <= Q.test_beta[tt]);
         }
         if (feasible) {
           const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
@@ -1053,17 +1058,11 @@ __global__ void corner_kernel(const CornerLaunch P) {
     }
     unsigned long long mx = key;
 #pragma unroll
-    for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx) atomicMax(&Q.ctl->seed_max, mx);
   }
 }
 
-// ---------------------------------------------------------------------------
-// tau from a key histogram: B = highest bin with sum_{b >= B} hist[b] >= k.
-// At least k distinct feasible products have key >= B<<48, so it is a valid
-// lower bound on the final k-th best key (never discards a true top-k
-// product).  mode 0: seed_hist -> raise tau_key; mode 1: hist -> raise
-// tau_key; mode 2: hist -> bound_key (final compaction bound).
 // Block-wide search (1024 threads) of the highest bin B with
 // sum_{b >= B} h[b] >= k.  Returns B (or -1 if the total is below k) and the
 // count at/above B in *count_ge (the total if B == -1).
