@@ -122,6 +122,10 @@ typedef struct {
   int64_t n;                  /* out: retained entries (best-first) */
   int64_t discarded;          /* out: min(k, end-start) - retained */
   uint64_t scanned;           /* out: end - start */
+  int64_t candidates;         /* out: feasible products with s >= tau appended by the scan */
+  int64_t admitted;           /* out: products that passed the admission test (admission-first kernel) */
+  int32_t full_predicate;     /* out: 1 if the full-predicate kernel scanned this query */
+  int32_t _pad;
 } apex_result;
 
 /* Entry exchanged between ranks: order-preserving key of the signed

@@ -96,6 +96,10 @@ class ResultC(C.Structure):
         ("n", C.c_int64),
         ("discarded", C.c_int64),
         ("scanned", C.c_uint64),
+        ("candidates", C.c_int64),
+        ("admitted", C.c_int64),
+        ("full_predicate", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 
@@ -280,6 +284,9 @@ class DeviceContext:
                 "n": n,
                 "discarded": results[i].discarded,
                 "scanned": results[i].scanned,
+                "candidates": results[i].candidates,
+                "admitted": results[i].admitted,
+                "full_predicate": results[i].full_predicate,
             })
         return out
 

@@ -903,7 +903,16 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
     const int64_t kk = std::max<int64_t>(q.k, 1);
     const int m = q.n_constraints;
     int64_t n = 0;
-    if (q.k > 0 && span > 0) n = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
+    if (q.k > 0 && span > 0) {
+      const QCtl& C = c->h_ctl.as<QCtl>()[i];
+      n = (int64_t)C.sel_count;
+      r.candidates = (int64_t)C.count;
+      r.admitted = (int64_t)C.admitted;
+      r.full_predicate = (int32_t)C.use_full;
+    } else {
+      r.candidates = r.admitted = 0;
+      r.full_predicate = 0;
+    }
     r.n = n;
     r.scanned = span;
     r.discarded = (int64_t)std::min<uint64_t>((uint64_t)q.k, span) - n;
@@ -1209,6 +1218,8 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
         r.n = 0;
         r.scanned = q.end - q.start;
         r.discarded = 0;
+        r.candidates = r.admitted = 0;
+        r.full_predicate = 0;
       }
     }
     if (!grp.empty()) {
@@ -1287,6 +1298,8 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   res->scanned = total_scanned;
   if (k == 0 || n_entries == 0) {
     res->n = 0;
+    res->candidates = res->admitted = 0;
+    res->full_predicate = 0;
     res->discarded = (int64_t)std::min<uint64_t>((uint64_t)k, total_scanned);
     return APEX_OK;
   }
