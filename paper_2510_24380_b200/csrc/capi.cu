@@ -183,6 +183,10 @@ struct apex_ctx {
   std::vector<Slot> slots;
   DBuf d_queries, d_tau0;
   DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
+  std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
+  DBuf d_groups, d_tctr;                 // multi-query kernel: group descriptors, work counters
+  HBuf h_groups;
+  cudaEvent_t groups_ev = nullptr;
   HBuf h_queries, h_ctl, h_out, h_tau0;
   std::vector<std::unique_ptr<Plan>> plans;
   uint64_t stamp = 0;
@@ -207,6 +211,7 @@ struct apex_ctx {
                                     // 1 = full predicate (FADD2 sign bits)
   int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
+  int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
 };
 
 namespace {
@@ -512,6 +517,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   B.ntp = (B.NT + 3) / 4 * 4;
   B.rl = (int)c->opt_rl;
   if (B.rl != 1 && B.rl != 2) B.rl = 1;
+  if (c->opt_mode >= 2 && c->opt_multi) B.rl = 1;  // the multi-query kernel owns one row per lane
   APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, nq, B.plan));
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
@@ -619,8 +625,64 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
-  // K2 pack of the streamed objective column
-  if (admit) {
+  // K2 pack of the streamed objective column(s)
+  const bool multi = admit && c->opt_multi;
+  std::vector<MultiGroup> groups;
+  if (multi) {
+    // distinct (objective task, direction) columns of the batch, packed once
+    std::vector<std::pair<int, int>> keys;
+    std::vector<int> qcol(nq);
+    for (int i = 0; i < nq; ++i) {
+      const std::pair<int, int> kk(B.qs[i].objective_task, B.qs[i].maximize ? 1 : 0);
+      auto it = std::find(keys.begin(), keys.end(), kk);
+      qcol[i] = (int)(it - keys.begin());
+      if (it == keys.end()) keys.push_back(kk);
+    }
+    if (c->colbufs.size() < keys.size()) c->colbufs.resize(keys.size());
+    for (size_t o = 0; o < keys.size(); ++o)
+      APEX_TRY(c->colbufs[o].ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
+    int64_t max_last = 1;
+    for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
+    const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
+    for (size_t o0 = 0; o0 < keys.size(); o0 += kMaxGroupQ) {
+      PackCols P;
+      P.ncols = (int)std::min<size_t>(kMaxGroupQ, keys.size() - o0);
+      for (int o = 0; o < P.ncols; ++o) {
+        P.task[o] = keys[o0 + o].first;
+        P.lower[o] = keys[o0 + o].second;  // maximize -> admission is a lower bound on x -> y = -x
+        P.dst[o] = c->colbufs[o0 + o].as<float>();
+      }
+      pack_cols_kernel<<<dim3(gx, (unsigned)c->rx.size(), P.ncols), 256, 0, s>>>(P, c->d_rx.as<DevReaction>(),
+                                                                                 c->d_values.as<float>(), c->n_pairs);
+      ++st.launches;
+    }
+    // groups of <= 32 queries; a group's columns are local indices into its own list
+    for (int q0 = 0; q0 < nq; q0 += kMaxGroupQ) {
+      MultiGroup Gp;
+      std::memset(&Gp, 0, sizeof(Gp));
+      Gp.q0 = q0;
+      Gp.nq = std::min(kMaxGroupQ, nq - q0);
+      std::vector<int> loc;
+      for (int q = 0; q < Gp.nq; ++q) {
+        const int gcol = qcol[q0 + q];
+        auto it = std::find(loc.begin(), loc.end(), gcol);
+        Gp.oc[q] = (int)(it - loc.begin());
+        if (it == loc.end()) loc.push_back(gcol);
+      }
+      Gp.ncols = (int)loc.size();
+      for (int o = 0; o < Gp.ncols; ++o) Gp.col[o] = c->colbufs[loc[o]].as<float>();
+      groups.push_back(Gp);
+    }
+    const size_t gb = groups.size() * sizeof(MultiGroup);
+    APEX_CU(cudaEventSynchronize(c->groups_ev));
+    APEX_TRY(c->h_groups.ensure(gb));
+    APEX_TRY(c->d_groups.ensure(gb));
+    APEX_TRY(c->d_tctr.ensure(groups.size() * sizeof(unsigned)));
+    std::memcpy(c->h_groups.p, groups.data(), gb);
+    APEX_CU(cudaMemcpyAsync(c->d_groups.p, c->h_groups.p, gb, cudaMemcpyHostToDevice, s));
+    APEX_CU(cudaEventRecord(c->groups_ev, s));
+    st.h2d_bytes += (int64_t)gb;
+  } else if (admit) {
     int64_t max_last = 1;
     for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
     const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
@@ -709,7 +771,48 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.queries = dq;
       L.cb = cb;
       if (ci == 0) APEX_CU(cudaEventRecord(c->ev[6], s));
-      if (admit) {
+      if (multi) {
+        int ncmax = 1;
+        for (const auto& Gp : groups) ncmax = std::max(ncmax, Gp.ncols);
+        int MQ = 1;
+        while (MQ < ncmax) MQ <<= 1;
+        ScanFn fnm = nullptr;
+        switch (MQ) {
+          case 1: fnm = (ScanFn)(void*)scan_multi_kernel<1>; break;
+          case 2: fnm = (ScanFn)(void*)scan_multi_kernel<2>; break;
+          case 4: fnm = (ScanFn)(void*)scan_multi_kernel<4>; break;
+          case 8: fnm = (ScanFn)(void*)scan_multi_kernel<8>; break;
+          case 16: fnm = (ScanFn)(void*)scan_multi_kernel<16>; break;
+          default: fnm = (ScanFn)(void*)scan_multi_kernel<32>; break;
+        }
+        // column block: ~1 KB of columns per buffer per warp
+        int cbm = (int)std::max<int64_t>(16, std::min<int64_t>(c->opt_cb_admit, 256 / ncmax) / 16 * 16);
+        const size_t smem = ((size_t)kScanWarps * 2 * ncmax * cbm + (size_t)kScanWarps * kMaxGroupQ * 32 +
+                             (size_t)kScanWarps * 16 * kMaxTests) * sizeof(float) +
+                            (size_t)kScanWarps * 2 * sizeof(uint64_t);
+        int occ = 0;
+        APEX_TRY(scan_occupancy(fnm, smem, &occ));
+        const int64_t blocks =
+            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
+        MultiLaunch ML;
+        ML.tiles = plan->d_tiles.as<Tile>();
+        ML.tile_begin = (unsigned)tb;
+        ML.tile_end = (unsigned)te;
+        ML.rx = c->d_rx.as<DevReaction>();
+        ML.values = c->d_values.as<float>();
+        ML.n_pairs = c->n_pairs;
+        ML.queries = dq;
+        ML.groups = c->d_groups.as<MultiGroup>();
+        ML.tile_counters = c->d_tctr.as<unsigned>();
+        ML.cb = cbm;
+        ML.ncols_max = ncmax;
+        APEX_CU(cudaMemsetAsync(c->d_tctr.p, 0, groups.size() * sizeof(unsigned), s));
+        void (*kfn)(const MultiLaunch) = reinterpret_cast<void (*)(const MultiLaunch)>(fnm);
+        kfn<<<dim3((unsigned)blocks, (unsigned)groups.size()), kScanWarps * 32, smem, s>>>(ML);
+        APEX_CU(cudaGetLastError());
+        ++st.launches;
+        ++st.scans;
+      } else if (admit) {
         const int cba = (int)c->opt_cb_admit;
         ScanFn fn = B.rl == 2 ? scan_admit_kernel<2> : scan_admit_kernel<1>;
         const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) +
@@ -971,6 +1074,7 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&c->upload_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->groups_ev, cudaEventDisableTiming);
   *out = c;
   return APEX_OK;
 }
@@ -995,6 +1099,11 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   if (c->upload_ev) cudaEventDestroy(c->upload_ev);
+  if (c->groups_ev) cudaEventDestroy(c->groups_ev);
+  for (auto& b : c->colbufs) b.release();
+  c->d_groups.release();
+  c->d_tctr.release();
+  c->h_groups.release();
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1402,6 +1511,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
+  else if (n == "multi") c->opt_multi = v;
   else if (n == "mode") {
     if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;
