@@ -49,11 +49,16 @@ int set_err(int code, const std::string& m) {
     if (r__ != APEX_OK) return r__; \
   } while (0)
 
+// bumped on every (re)allocation: device pointers baked into a captured CUDA
+// graph are only valid while this is unchanged
+thread_local uint64_t g_alloc_gen = 0;
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t b) {
     if (b <= bytes) return APEX_OK;
+    ++g_alloc_gen;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -79,6 +84,7 @@ struct HBuf {
   size_t bytes = 0;
   int ensure(size_t b) {
     if (b <= bytes) return APEX_OK;
+    ++g_alloc_gen;
     if (p) cudaFreeHost(p);
     p = nullptr;
     bytes = 0;
@@ -97,9 +103,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, obj_col, buf, comp, sel, sorted, rank, ctl, out;
+  DBuf packed, obj_col, buf, comp, sel, sorted, rank, ctl;
   void release() {
-    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &ctl, &out}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &ctl}) b->release();
   }
 };
 
@@ -183,6 +189,8 @@ struct apex_ctx {
   std::vector<Slot> slots;
   DBuf d_queries, d_tau0;
   DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
+  DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
+  std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
   DBuf d_groups, d_tctr;                 // multi-query kernel: group descriptors, work counters
   HBuf h_groups;
@@ -212,6 +220,13 @@ struct apex_ctx {
   int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
   int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
+  int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
+  uint64_t opt_gen = 0;             // bumped by apex_set_option
+  // CUDA graph of the last batch signature
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t gkey = 0;
+  bool graph_broken = false;
+  RunStats graph_stats;
 };
 
 namespace {
@@ -536,7 +551,21 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
     APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
-    APEX_TRY(S.out.ensure(out_bytes(std::max<int64_t>(k, 1), qs[i].n_constraints)));
+  }
+  c->out_off.assign(nq + 1, 0);
+  for (int i = 0; i < nq; ++i)
+    c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
+  APEX_TRY(c->d_out.ensure(c->out_off[nq]));
+  // everything enqueue_batch touches is allocated here (no allocation may
+  // happen while the pipeline is being captured into a CUDA graph)
+  APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
+  if (c->opt_mode >= 2 && c->opt_multi) {
+    const int ng = (nq + kMaxGroupQ - 1) / kMaxGroupQ;
+    if ((int)c->colbufs.size() < nq) c->colbufs.resize(nq);
+    for (int i = 0; i < nq; ++i) APEX_TRY(c->colbufs[i].ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
+    APEX_TRY(c->h_groups.ensure(ng * sizeof(MultiGroup)));
+    APEX_TRY(c->d_groups.ensure(ng * sizeof(MultiGroup)));
+    APEX_TRY(c->d_tctr.ensure(ng * sizeof(unsigned)));
   }
   APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
   std::vector<ScanQuery> hq(nq);
@@ -574,7 +603,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     }
     for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
     const int64_t kk = std::max<int64_t>(q.k, 1);
-    unsigned char* o = S.out.as<unsigned char>();
+    unsigned char* o = c->d_out.as<unsigned char>() + c->out_off[i];
     Q.out_g = reinterpret_cast<unsigned long long*>(o);
     Q.out_obj = reinterpret_cast<double*>(o + 8 * kk);
     Q.out_cons = reinterpret_cast<double*>(o + 16 * kk);
@@ -600,6 +629,15 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
 
 // Enqueue the device pipeline of the prepared batch.  tau0: preset admission
 // keys (re-run after an overflow), or nullptr.
+// Stage timing event; inside a stream capture it is recorded as an external
+// event-record node so the graph replay still timestamps it.
+cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(c->ev[e], s, cudaEventRecordExternal);
+  return cudaEventRecord(c->ev[e], s);
+}
+
 int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   Batch& B = c->batch;
   RunStats& st = B.st;
@@ -608,7 +646,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   const uint64_t start = B.qs[0].start, end = B.qs[0].end, span = end - start;
   cudaStream_t s = c->stream;
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
-  APEX_CU(cudaEventRecord(c->ev[0], s));
+  APEX_CU(stage_mark(c, 0, s));
   if (tau0) {
     APEX_TRY(c->d_tau0.ensure(nq * sizeof(unsigned long long)));
     APEX_TRY(c->h_tau0.ensure(nq * sizeof(unsigned long long)));
@@ -690,7 +728,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
                                                                         c->d_values.as<float>(), c->n_pairs);
     ++st.launches;
   }
-  APEX_CU(cudaEventRecord(c->ev[1], s));
+  APEX_CU(stage_mark(c, 1, s));
   // seed threshold from exact samples
   if (!tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
@@ -744,7 +782,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     pack_kernel<<<dim3(blocks, nq), 256, 0, s>>>(dq, c->d_values.as<float>(), c->n_pairs, plan->pair_lo, plan->pair_hi);
     ++st.launches;
   }
-  APEX_CU(cudaEventRecord(c->ev[2], s));
+  APEX_CU(stage_mark(c, 2, s));
   // K3 enumeration: chunks x test classes
   const int cb = (int)c->opt_cb;
   const size_t n_tiles = plan->tiles.size();
@@ -770,7 +808,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.n_pairs = c->n_pairs;
       L.queries = dq;
       L.cb = cb;
-      if (ci == 0) APEX_CU(cudaEventRecord(c->ev[6], s));
+      if (ci == 0) APEX_CU(stage_mark(c, 6, s));
       if (multi) {
         int ncmax = 1;
         for (const auto& Gp : groups) ncmax = std::max(ncmax, Gp.ncols);
@@ -848,16 +886,35 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);  // raise tau from the candidates so far
         ++st.launches;
       }
-      for (int i = 0; i < nq; ++i)
-        APEX_CU(cudaMemsetAsync(&c->slots[i].ctl.as<QCtl>()->tile_counter, 0, sizeof(unsigned), s));
     }
     tb = te;
   }
-  APEX_CU(cudaEventRecord(c->ev[7], s));
-  APEX_CU(cudaEventRecord(c->ev[3], s));
+  APEX_CU(stage_mark(c, 7, s));
+  APEX_CU(stage_mark(c, 3, s));
   // final bound, compaction, exact select
   tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
   ++st.launches;
+  MatLaunch M;
+  M.queries = dq;
+  M.rx = c->d_rx.as<DevReaction>();
+  M.g_off = c->d_goff.as<unsigned long long>();
+  M.n_rx = (int)c->rx.size();
+  M.values = c->d_values.as<float>();
+  M.n_pairs = c->n_pairs;
+  M.biases = c->d_biases.as<double>();
+  {
+    // small candidate sets: one CTA per query sorts them in shared memory and
+    // materializes; the large path below skips those queries
+    static thread_local bool attr_small = false;
+    const size_t smem_small = (size_t)kSmallSel * sizeof(Entry);
+    if (!attr_small) {
+      APEX_CU(cudaFuncSetAttribute((const void*)finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_small));
+      attr_small = true;
+    }
+    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, B.finalize ? 1 : 0);
+    ++st.launches;
+  }
   {
     static thread_local int occ_sel = 0;
     if (!occ_sel)
@@ -869,27 +926,17 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, nq), dim3(kSelectThreads), args, 0, s));
     ++st.launches;
   }
-  APEX_CU(cudaEventRecord(c->ev[4], s));
+  APEX_CU(stage_mark(c, 4, s));
   if (B.finalize) {
-    for (int i = 0; i < nq; ++i)
-      APEX_CU(cudaMemsetAsync(c->slots[i].rank.p, 0, std::max<int64_t>(B.qs[i].k, 1) * sizeof(unsigned), s));
     const int ib = (int)((B.k_max + 255) / 256);
     const int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
     rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
     scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
-    MatLaunch M;
-    M.queries = dq;
-    M.rx = c->d_rx.as<DevReaction>();
-    M.g_off = c->d_goff.as<unsigned long long>();
-    M.n_rx = (int)c->rx.size();
-    M.values = c->d_values.as<float>();
-    M.n_pairs = c->n_pairs;
-    M.biases = c->d_biases.as<double>();
     materialize_kernel<<<dim3((unsigned)((B.k_max + 127) / 128), nq), 128, 0, s>>>(M);
     st.launches += 3;
   }
   APEX_CU(cudaGetLastError());
-  APEX_CU(cudaEventRecord(c->ev[5], s));
+  APEX_CU(stage_mark(c, 5, s));
   // control blocks to host (read by check_batch)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
   for (int i = 0; i < nq; ++i)
@@ -941,8 +988,80 @@ int check_batch(apex_ctx* c) {
     APEX_TRY(enqueue_batch(c, tau0.data()));
   }
   B.pending = false;
-  for (int e = 0; e < 5; ++e) APEX_CU(cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]));
-  APEX_CU(cudaEventElapsedTime(&B.st.scan_kernel_ms, c->ev[6], c->ev[7]));
+  // (stage times are informational: never fail the query on them)
+  for (int e = 0; e < 5; ++e)
+    if (cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]) != cudaSuccess) B.st.ms[e] = 0.f;
+  if (cudaEventElapsedTime(&B.st.scan_kernel_ms, c->ev[6], c->ev[7]) != cudaSuccess) B.st.scan_kernel_ms = 0.f;
+  cudaGetLastError();
+  return APEX_OK;
+}
+
+// Signature of the prepared batch: query contents, options and the
+// allocation generation (device / pinned pointers baked into a graph).
+uint64_t batch_key(const apex_ctx* c) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  const Batch& B = c->batch;
+  mix(&B.nq, sizeof(B.nq));
+  mix(&B.finalize, sizeof(B.finalize));
+  for (int i = 0; i < B.nq; ++i) {
+    const apex_query_spec& q = B.qs[i];
+    mix(&q.objective_task, sizeof(q.objective_task));
+    mix(&q.maximize, sizeof(q.maximize));
+    mix(&q.n_constraints, sizeof(q.n_constraints));
+    mix(&q.k, sizeof(q.k));
+    mix(&q.start, sizeof(q.start));
+    mix(&q.end, sizeof(q.end));
+    mix(B.cons[i].data(), B.cons[i].size() * sizeof(apex_constraint));
+    mix(&B.perm[i], sizeof(int));
+  }
+  const void* plan = B.plan;
+  mix(&plan, sizeof(plan));
+  mix(&c->opt_gen, sizeof(c->opt_gen));
+  mix(&g_alloc_gen, sizeof(g_alloc_gen));
+  return h;
+}
+
+// Enqueue the prepared batch: replay the captured CUDA graph when the batch
+// signature repeats, otherwise capture it (or launch directly if capture is
+// unavailable).  One graph launch replaces ~30 kernel/memset/memcpy launches.
+int launch_batch(apex_ctx* c) {
+  if (!c->opt_graph || c->graph_broken) return enqueue_batch(c, nullptr);
+  const uint64_t key = batch_key(c);
+  if (c->gexec && key == c->gkey) {
+    APEX_CU(cudaGraphLaunch(c->gexec, c->stream));
+    c->batch.pending = true;
+    c->batch.st = c->graph_stats;  // launch counts / bytes as captured
+    return APEX_OK;
+  }
+  if (c->gexec) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+  }
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    c->graph_broken = true;
+    return enqueue_batch(c, nullptr);
+  }
+  const int rc = enqueue_batch(c, nullptr);
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = (rc == APEX_OK && ec == cudaSuccess) ? cudaGraphInstantiate(&exec, graph, 0) : ec;
+  if (graph) cudaGraphDestroy(graph);
+  if (rc != APEX_OK || ec != cudaSuccess || ei != cudaSuccess) {
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    c->graph_broken = true;  // fall back to direct launches for this context
+    return enqueue_batch(c, nullptr);
+  }
+  c->gexec = exec;
+  c->gkey = key;
+  c->graph_stats = c->batch.st;
+  APEX_CU(cudaGraphLaunch(c->gexec, c->stream));
   return APEX_OK;
 }
 
@@ -986,18 +1105,12 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
   std::vector<apex_result> res_sorted(nq);
   for (int i = 0; i < nq; ++i) res_sorted[i] = res_caller[perm ? perm[i] : i];
   apex_result* res = res_sorted.data();
-  size_t total = 0;
-  std::vector<size_t> offs(nq);
-  for (int i = 0; i < nq; ++i) {
-    offs[i] = total;
-    total += out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints);
-  }
+  // one D2H of every query's rows (contiguous in d_out), then host copies of
+  // the retained rows into the caller's arrays
+  const std::vector<size_t>& offs = c->out_off;
+  const size_t total = offs[nq];
   APEX_TRY(c->h_out.ensure(total));
-  for (int i = 0; i < nq; ++i)
-    if (qs[i].k > 0 && qs[i].start < qs[i].end)
-      APEX_CU(cudaMemcpyAsync(c->h_out.as<unsigned char>() + offs[i], c->slots[i].out.p,
-                              out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints), cudaMemcpyDeviceToHost,
-                              c->stream));
+  APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, total, cudaMemcpyDeviceToHost, c->stream));
   APEX_CU(cudaStreamSynchronize(c->stream));
   for (int i = 0; i < nq; ++i) {
     const apex_query_spec& q = qs[i];
@@ -1093,6 +1206,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_queries.release();
   c->d_tau0.release();
   c->d_hists.release();
+  c->d_out.release();
   c->h_queries.release();
   c->h_ctl.release();
   c->h_out.release();
@@ -1100,6 +1214,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   if (c->upload_ev) cudaEventDestroy(c->upload_ev);
   if (c->groups_ev) cudaEventDestroy(c->groups_ev);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
   for (auto& b : c->colbufs) b.release();
   c->d_groups.release();
   c->d_tctr.release();
@@ -1262,7 +1377,7 @@ int apex_query_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_st
       return set_err(APEX_EINVAL, "apex_query_async: k >= 1 and a non-empty range required (use apex_query)");
   }
   APEX_TRY(prepare_batch(c, qs, nq, true));
-  APEX_TRY(enqueue_batch(c, nullptr));
+  APEX_TRY(launch_batch(c));
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     stats->kernel_launches = c->batch.st.launches;
@@ -1376,7 +1491,7 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
     return APEX_OK;
   }
   APEX_TRY(prepare_batch(c, qs, nq, false));
-  APEX_TRY(enqueue_batch(c, nullptr));
+  APEX_TRY(launch_batch(c));
   APEX_TRY(check_batch(c));
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
   export_kernel<<<dim3((unsigned)((k + 255) / 256), nq), 256, 0, c->stream>>>(dq, reinterpret_cast<Entry*>(out_dev));
@@ -1422,7 +1537,9 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
   APEX_TRY(c->d_hists.ensure(kHistWords * sizeof(unsigned)));
   APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
-  APEX_TRY(S.out.ensure(out_bytes(k, q->n_constraints)));
+  c->out_off.assign(2, 0);
+  c->out_off[1] = (out_bytes(k, q->n_constraints) + 15) / 16 * 16;
+  APEX_TRY(c->d_out.ensure(c->out_off[1]));
   APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
   APEX_CU(cudaEventSynchronize(c->upload_ev));
   APEX_TRY(c->h_queries.ensure(sizeof(ScanQuery)));
@@ -1446,7 +1563,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   Q.obj_task = q->objective_task;
   Q.n_cons = q->n_constraints;
   for (int m = 0; m < q->n_constraints; ++m) Q.cons_task[m] = q->constraints[m].task;
-  unsigned char* o = S.out.as<unsigned char>();
+  unsigned char* o = c->d_out.as<unsigned char>();
   Q.out_g = reinterpret_cast<unsigned long long*>(o);
   Q.out_obj = reinterpret_cast<double*>(o + 8 * k);
   Q.out_cons = reinterpret_cast<double*>(o + 16 * k);
@@ -1466,7 +1583,6 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
     APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, c->sm_count)), 1),
                                         dim3(kSelectThreads), args, 0, s));
   }
-  APEX_CU(cudaMemsetAsync(S.rank.p, 0, k * sizeof(unsigned), s));
   const int ib = (int)((k + 255) / 256);
   const int js = std::max(1, std::min(ib, (2 * c->sm_count + ib - 1) / ib));
   rank_kernel<<<dim3(ib, js, 1), 256, 0, s>>>(dq, js);
@@ -1501,6 +1617,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
 int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   if (!c || !name) return set_err(APEX_EINVAL, "bad option arguments");
   std::string n(name);
+  ++c->opt_gen;
   if (n == "cap") c->opt_cap = std::max<int64_t>(v, 1024);
   else if (n == "cb") {
     if (v < 8 || v % 8 || v > 256) return set_err(APEX_EINVAL, "cb must be a multiple of 8 in [8, 256]");
@@ -1512,6 +1629,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
   else if (n == "multi") c->opt_multi = v;
+  else if (n == "graph") c->opt_graph = v;
   else if (n == "mode") {
     if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;

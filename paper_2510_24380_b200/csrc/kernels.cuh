@@ -169,6 +169,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned
     c->hist_base = 0;
     c->hist_shift = 48;
     c->use_full = use_full;
+    c->small_done = 0;
     c->seed_max = 0;
     c->admitted = 0;
     c->count = 0;
@@ -1466,6 +1467,7 @@ __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__
           const unsigned long long key = bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift);
           if (key > ctl->tau_key) ctl->tau_key = key;
         }
+        ctl->tile_counter = 0;  // the next chunk's scan redistributes its tiles
       } else {
         ctl->bound_key = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
         ctl->comp_count = cnt;  // candidates with key >= bound
@@ -1545,7 +1547,7 @@ __device__ __forceinline__ bool ge_prefix(const Entry& e, unsigned long long phi
 __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery* __restrict__ qs) {
   const ScanQuery& Q = qs[blockIdx.y];
   QCtl* ctl = Q.ctl;
-  if (!*(volatile unsigned int*)&ctl->active) return;
+  if (!*(volatile unsigned int*)&ctl->active || *(volatile unsigned int*)&ctl->small_done) return;
   __shared__ unsigned int sh[256];
   __shared__ unsigned long long s_phi, s_plo, s_need;
   __shared__ int s_depth;
@@ -1562,6 +1564,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
   const unsigned long long start = (unsigned long long)blockIdx.x * blockDim.x + tid;
   const unsigned long long stride = (unsigned long long)nb * blockDim.x;
 
+  for (unsigned long long i = start; i < k; i += stride) Q.rank[i] = 0u;  // for rank_kernel (stream order)
   const bool take_all = n_valid <= k;
   unsigned long long phi = 0, plo = 0;
   int depth = 0;
@@ -1650,6 +1653,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
 __global__ void __launch_bounds__(256) rank_kernel(const ScanQuery* __restrict__ qs, int jsplit) {
   const ScanQuery& Q = qs[blockIdx.z];
   QCtl* ctl = Q.ctl;
+  if (*(volatile unsigned*)&ctl->small_done) return;
   const unsigned long long n = *(volatile unsigned long long*)&ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x;
   if ((unsigned long long)blockIdx.x * 256 >= n) return;
@@ -1671,6 +1675,7 @@ __global__ void __launch_bounds__(256) rank_kernel(const ScanQuery* __restrict__
 
 __global__ void scatter_kernel(const ScanQuery* __restrict__ qs) {
   const ScanQuery& Q = qs[blockIdx.y];
+  if (*(volatile unsigned*)&Q.ctl->small_done) return;
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) Q.sorted[Q.rank[i]] = Q.sel[i];
@@ -1690,12 +1695,7 @@ struct MatLaunch {
   const double* biases;
 };
 
-__global__ void materialize_kernel(const MatLaunch M) {
-  const ScanQuery& Q = M.queries[blockIdx.y];
-  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
-  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const unsigned long long g = Q.sorted[i].g;
+__device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned long long i, unsigned long long g) {
   int lo = 0, hi = M.n_rx;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -1727,6 +1727,82 @@ __global__ void materialize_kernel(const MatLaunch M) {
   Q.out_g[i] = g;
   Q.out_rx[i] = lo;
   for (int j = 0; j < kMaxRg; ++j) Q.out_dig[i * kMaxRg + j] = j < R.c ? (int32_t)dig[j] : 0;
+}
+
+__global__ void materialize_kernel(const MatLaunch M) {
+  const ScanQuery& Q = M.queries[blockIdx.y];
+  if (*(volatile unsigned*)&Q.ctl->small_done) return;
+  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  materialize_row(M, Q, i, Q.sorted[i].g);
+}
+
+// Small-candidate-set finalize (one 1024-thread CTA per query): when at most
+// kSmallSel candidates are at/above the final bound, load them into shared
+// memory, bitonic-sort by (key desc, g asc), keep the first k, and (single-GPU
+// path) materialize them — replacing select + rank + scatter + materialize.
+constexpr int kSmallSel = 8192;
+
+__global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M, int materialize) {
+  const ScanQuery& Q = M.queries[blockIdx.x];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  const unsigned long long n_valid = *(volatile unsigned long long*)&ctl->comp_count;
+  if (n_valid > (unsigned long long)kSmallSel) return;  // large path
+  extern __shared__ __align__(16) unsigned char sm_e[];
+  Entry* es = reinterpret_cast<Entry*>(sm_e);
+  __shared__ unsigned cnt;
+  const unsigned tid = threadIdx.x;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
+  const unsigned long long bound = *(volatile unsigned long long*)&ctl->bound_key;
+  for (unsigned long long i = tid; i < n; i += blockDim.x) {
+    const Entry e = Q.buf[i];
+    if (e.key >= bound) {
+      const unsigned pos = atomicAdd(&cnt, 1u);
+      if (pos < (unsigned)kSmallSel) es[pos] = e;
+    }
+  }
+  __syncthreads();
+  const unsigned m = min(cnt, (unsigned)kSmallSel);
+  unsigned P = 1;
+  while (P < m) P <<= 1;
+  for (unsigned i = m + tid; i < P; i += blockDim.x) {
+    es[i].key = 0;
+    es[i].g = ~0ull;
+  }
+  __syncthreads();
+  for (unsigned size = 2; size <= P; size <<= 1) {
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      for (unsigned i = tid; i < P; i += blockDim.x) {
+        const unsigned j = i ^ stride;
+        if (j > i) {
+          const Entry a = es[i], b = es[j];
+          // best-first within ascending-index segments of the final order
+          const bool want_a_first = (i & size) == 0;
+          const bool b_better = entry_better(b, a);
+          if (want_a_first ? b_better : !b_better) {
+            es[i] = b;
+            es[j] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const unsigned kk = (unsigned long long)Q.k < (unsigned long long)m ? (unsigned)Q.k : m;
+  for (unsigned i = tid; i < kk; i += blockDim.x) {
+    Q.sel[i] = es[i];
+    Q.sorted[i] = es[i];
+    if (materialize) materialize_row(M, Q, i, es[i].g);
+  }
+  if (tid == 0) {
+    ctl->sel_count = kk;
+    ctl->small_done = 1;
+    if (kk == (unsigned long long)Q.k && kk > 0 && es[kk - 1].key > ctl->tau_key) ctl->tau_key = es[kk - 1].key;
+  }
 }
 
 // Multi-GPU: export the local selected set (unordered) to out + q*k.
