@@ -193,6 +193,7 @@ struct apex_ctx {
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
   DBuf d_groups, d_tctr;                 // multi-query kernel: group descriptors, work counters
+  DBuf d_work;                           // flattened-work counters of the scan launches
   HBuf h_groups;
   cudaEvent_t groups_ev = nullptr;
   HBuf h_queries, h_ctl, h_out, h_tau0;
@@ -221,6 +222,7 @@ struct apex_ctx {
   int64_t opt_corner = 1;           // corner seed on/off
   int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
+  int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   uint64_t opt_gen = 0;             // bumped by apex_set_option
   // CUDA graph of the last batch signature
   cudaGraphExec_t gexec = nullptr;
@@ -559,6 +561,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   // everything enqueue_batch touches is allocated here (no allocation may
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
+  APEX_TRY(c->d_work.ensure(64 * sizeof(unsigned)));
   if (c->opt_mode >= 2 && c->opt_multi) {
     const int ng = (nq + kMaxGroupQ - 1) / kMaxGroupQ;
     if ((int)c->colbufs.size() < nq) c->colbufs.resize(nq);
@@ -796,6 +799,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   bounds.push_back(n_tiles);
   size_t tb = 0;
   st.scan_kernel_ms = 0;
+  int wi = 0;  // flattened-work counter index (one per scan launch)
+  APEX_CU(cudaMemsetAsync(c->d_work.p, 0, 64 * sizeof(unsigned), s));
   for (size_t ci = 0; ci < bounds.size(); ++ci) {
     const size_t te = bounds[ci];
     if (te > tb) {
@@ -808,6 +813,9 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.n_pairs = c->n_pairs;
       L.queries = dq;
       L.cb = cb;
+      L.nq = nq;
+      L.work = c->d_work.as<unsigned>();
+      L.chunk = (int)c->opt_chunk;
       if (ci == 0) APEX_CU(stage_mark(c, 6, s));
       if (multi) {
         int ncmax = 1;
@@ -857,14 +865,21 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
                             (size_t)kScanWarps * 16 * kMaxTests * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
         int occ = 0;
         APEX_TRY(scan_occupancy(fn, smem, &occ));
-        const int64_t blocks =
-            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
-        ScanLaunch La = L;
-        La.cb = cba;
-        fn<<<dim3((unsigned)blocks, nq), kScanWarps * 32, smem, s>>>(La);
-        APEX_CU(cudaGetLastError());
-        ++st.launches;
-        ++st.scans;
+        for (int q0 = 0; q0 < nq; q0 += 64) {
+          const int nql = std::min(64, nq - q0);
+          const int64_t items = (int64_t)(te - tb) * nql;
+          const int64_t blocks = std::max<int64_t>(
+              1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
+          ScanLaunch La = L;
+          La.cb = cba;
+          La.queries = dq + q0;
+          La.nq = nql;
+          La.work = c->d_work.as<unsigned>() + (wi++ % 64);
+          fn<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La);
+          APEX_CU(cudaGetLastError());
+          ++st.launches;
+          ++st.scans;
+        }
       }
       for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
         ScanFn fn = pick_scan(B.cls_nt[k], B.rl, c->opt_mode == 1 ? 1 : 0);
@@ -872,15 +887,20 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         const size_t smem = scan_smem(B.cls_nt[k], cb);
         int occ = 0;
         APEX_TRY(scan_occupancy(fn, smem, &occ));
-        const int nqc = B.cls_begin[k + 1] - B.cls_begin[k];
-        const int64_t blocks =
-            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
-        ScanLaunch Lc = L;
-        Lc.queries = dq + B.cls_begin[k];
-        fn<<<dim3((unsigned)blocks, nqc), kScanWarps * 32, smem, s>>>(Lc);
-        APEX_CU(cudaGetLastError());
-        ++st.launches;
-        ++st.scans;
+        for (int q0 = B.cls_begin[k]; q0 < B.cls_begin[k + 1]; q0 += 64) {
+          const int nql = std::min(64, B.cls_begin[k + 1] - q0);
+          const int64_t items = (int64_t)(te - tb) * nql;
+          const int64_t blocks = std::max<int64_t>(
+              1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
+          ScanLaunch Lc = L;
+          Lc.queries = dq + q0;
+          Lc.nq = nql;
+          Lc.work = c->d_work.as<unsigned>() + (wi++ % 64);
+          fn<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(Lc);
+          APEX_CU(cudaGetLastError());
+          ++st.launches;
+          ++st.scans;
+        }
       }
       if (ci + 1 < bounds.size()) {
         tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);  // raise tau from the candidates so far
@@ -1207,6 +1227,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_tau0.release();
   c->d_hists.release();
   c->d_out.release();
+  c->d_work.release();
   c->h_queries.release();
   c->h_ctl.release();
   c->h_out.release();
@@ -1630,6 +1651,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "corner") c->opt_corner = v;
   else if (n == "multi") c->opt_multi = v;
   else if (n == "graph") c->opt_graph = v;
+  else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
   else if (n == "mode") {
     if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;

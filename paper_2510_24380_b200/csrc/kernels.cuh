@@ -296,7 +296,53 @@ struct ScanLaunch {
   int64_t n_pairs;
   const ScanQuery* queries;
   int cb;                 // columns per smem block (multiple of 8)
+  int nq;                 // queries of this launch (<= 64)
+  unsigned int* work;     // flattened (tile x query) work counter, zeroed before the launch
+  int chunk;              // work items per atomic
 };
+
+// Flattened persistent work distribution: item -> (tile = item / nq,
+// query = item % nq), so the queries of a batch advance together over the
+// same tiles (shared column data stays hot in L1/L2) and one launch keeps
+// every SM busy however many queries there are.  Warps take `chunk` items per
+// atomic; items of queries this kernel does not scan (mask) are skipped.
+struct WorkCursor {
+  unsigned cur = 0, lim = 0;
+  unsigned nxt = 0;      // lane 0: base of the next chunk, fetched one chunk ahead
+  bool primed = false;
+};
+
+__device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, unsigned long long live, unsigned lane,
+                                          unsigned& q, unsigned& t) {
+  const unsigned total = (L.tile_end - L.tile_begin) * (unsigned)L.nq;
+  if (!wc.primed) {
+    wc.primed = true;
+    if (lane == 0) wc.nxt = atomicAdd(L.work, (unsigned)L.chunk);
+  }
+  for (;;) {
+    if (wc.cur >= wc.lim) {
+      const unsigned base = __shfl_sync(0xffffffffu, wc.nxt, 0);
+      if (lane == 0 && base < total) wc.nxt = atomicAdd(L.work, (unsigned)L.chunk);  // latency hidden by this chunk
+      wc.cur = base;
+      wc.lim = base + (unsigned)L.chunk;
+    }
+    const unsigned item = wc.cur++;
+    if (item >= total) return false;
+    q = item % (unsigned)L.nq;
+    t = L.tile_begin + item / (unsigned)L.nq;
+    if ((live >> q) & 1ull) return true;
+  }
+}
+
+// queries of the launch that this kernel form scans
+__device__ __forceinline__ unsigned long long live_mask(const ScanLaunch& L, unsigned want_full) {
+  unsigned long long m = 0;
+  for (int q = 0; q < L.nq; ++q) {
+    const QCtl* c = L.queries[q].ctl;
+    if (*(volatile unsigned*)&c->active && *(volatile unsigned*)&c->use_full == want_full) m |= 1ull << q;
+  }
+  return m;
+}
 
 // In-kernel threshold refresh (one warp): B = highest key>>48 bin such that the
 // candidates appended so far with key >= B<<48 number at least k; counts are
@@ -433,10 +479,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
   constexpr int NTP = Ntp<NT>::value;
   constexpr int NP = Np<NT>::value;
   extern __shared__ __align__(128) unsigned char sm_raw[];
-  const ScanQuery& Q = L.queries[blockIdx.y];
-  QCtl* ctl = Q.ctl;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  if (!*(volatile unsigned int*)&ctl->active || !*(volatile unsigned int*)&ctl->use_full) return;
+  const unsigned long long live = live_mask(L, 1u);
+  if (!live) return;
+  WorkCursor wc;
 
   const int cb = L.cb;
   float* sbuf0 = reinterpret_cast<float*>(sm_raw) + (size_t)warp * 2 * cb * NTP;
@@ -451,23 +497,22 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
   uint32_t phase0 = 0, phase1 = 0;
   unsigned bi = 0;
 
-  Entry* __restrict__ buf = Q.buf;
-  unsigned int* __restrict__ hist = Q.hist;
-  const unsigned long long cap = Q.cap;
-  const int maximize = Q.maximize;
-  const float* packed = Q.packed;
-  const double b_obj = Q.test_bias[0];
-  const int nt = Q.nt;
-  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
-  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
   // value of padding columns: never passes in either compare form
   const float pad_y = MODE == 1 ? __int_as_float(0x7f800000) : __int_as_float(0x7fffffff);
 
-  for (;;) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(&ctl->tile_counter, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0) + L.tile_begin;
-    if (t >= L.tile_end) break;
+  unsigned qi, t;
+  while (next_item(L, wc, live, lane, qi, t)) {
+    const ScanQuery& Q = L.queries[qi];
+    QCtl* ctl = Q.ctl;
+    Entry* __restrict__ buf = Q.buf;
+    unsigned int* __restrict__ hist = Q.hist;
+    const unsigned long long cap = Q.cap;
+    const int maximize = Q.maximize;
+    const float* packed = Q.packed;
+    const double b_obj = Q.test_bias[0];
+    const int nt = Q.nt;
+    const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
+    const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
     const Tile T = L.tiles[t];
     const DevReaction& R = L.rx[T.rx];
     const int c = R.c;
@@ -681,10 +726,10 @@ __device__ __forceinline__ float min16_shared(uint32_t addr) {
 template <int RL>
 __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const ScanLaunch L) {
   extern __shared__ __align__(128) float sm_f[];
-  const ScanQuery& Q = L.queries[blockIdx.y];
-  QCtl* ctl = Q.ctl;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  if (!*(volatile unsigned int*)&ctl->active || *(volatile unsigned int*)&ctl->use_full) return;
+  const unsigned long long live = live_mask(L, 0u);
+  if (!live) return;
+  WorkCursor wc;
 
   const int cb = L.cb;
   // shared-memory word offsets of this warp's two column buffers; indexing the
@@ -701,30 +746,26 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   uint32_t phase0 = 0, phase1 = 0;
   unsigned bi = 0;
 
-  Entry* __restrict__ buf = Q.buf;
-  unsigned int* __restrict__ hist = Q.hist;
-  const unsigned long long cap = Q.cap;
-  const int maximize = Q.maximize;
-  const double b_obj = Q.test_bias[0];
   const float* __restrict__ values = L.values;
   const int64_t n_pairs = L.n_pairs;
-  const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
-  const int nt = Q.nt;
-  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
-  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
   const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
   constexpr int kTauPoll = 8;                      // column blocks between admission-threshold polls
-
-  // the next tile index and the admission threshold are fetched ahead of use
-  // (L2 round trips on addresses every warp shares)
-  unsigned t_next = 0;
-  if (lane == 0) t_next = atomicAdd(&ctl->tile_counter, 1u);
-  unsigned long long tau_pref = *(volatile unsigned long long*)&ctl->tau_key;
   int poll = 0;
-  for (;;) {
-    unsigned t = __shfl_sync(0xffffffffu, t_next, 0) + L.tile_begin;
-    if (t >= L.tile_end) break;
-    if (lane == 0) t_next = atomicAdd(&ctl->tile_counter, 1u);
+
+  unsigned qi, t;
+  while (next_item(L, wc, live, lane, qi, t)) {
+    const ScanQuery& Q = L.queries[qi];
+    QCtl* ctl = Q.ctl;
+    Entry* __restrict__ buf = Q.buf;
+    unsigned int* __restrict__ hist = Q.hist;
+    const unsigned long long cap = Q.cap;
+    const int maximize = Q.maximize;
+    const double b_obj = Q.test_bias[0];
+    const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
+    const int nt = Q.nt;
+    const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
+    const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
+    unsigned long long tau_pref = *(volatile unsigned long long*)&ctl->tau_key;
     const Tile T = L.tiles[t];
     const DevReaction& R = L.rx[T.rx];
     const int c = R.c;
