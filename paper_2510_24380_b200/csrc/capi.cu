@@ -121,7 +121,8 @@ struct Plan {
   ~Plan() { d_tiles.release(); }
 };
 
-constexpr size_t kHistWords = (size_t)kHistBins + 256 + 2 * (size_t)kHistBins;  // hist, coarse, seed x2
+// per query: candidate hist + coarse, seed hists (uniform, corner) + their coarse
+constexpr size_t kHistWords = (size_t)kHistBins + 256 + 2 * (size_t)kHistBins + 512;
 
 size_t out_bytes(int64_t k, int m) { return (size_t)k * (8 + 8 + 8 * (size_t)m + 4 + 4 * kMaxRg); }
 
@@ -223,6 +224,7 @@ struct apex_ctx {
   int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
+  int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
   uint64_t opt_gen = 0;             // bumped by apex_set_option
   // CUDA graph of the last batch signature
   cudaGraphExec_t gexec = nullptr;
@@ -257,10 +259,10 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan
   const int64_t warp_slots = (int64_t)c->sm_count * 24;
   const int64_t target = c->opt_tile_products > 0
                              ? c->opt_tile_products
-                             : std::max<int64_t>(8192, (int64_t)(span * (uint64_t)nq / (uint64_t)(6 * warp_slots)));
+                             : std::max<int64_t>(8192, (int64_t)(span * (uint64_t)nq / (uint64_t)(c->opt_tiles_per_slot * warp_slots)));
   int64_t cols = std::max<int64_t>(64, std::min<int64_t>(4096, target / rows));
   int64_t p2 = 64;
-  while (p2 < cols) p2 <<= 1;  // power of two: few distinct cached plans
+  while (p2 * 2 <= cols) p2 <<= 1;  // power of two (rounded down): few distinct cached plans
   cols = p2;
   for (auto& p : c->plans) {
     if (p->start == start && p->end == end && p->rows == rows && p->cols == cols) {
@@ -735,7 +737,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // seed threshold from exact samples
   if (!tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
-                                     : (uint64_t)std::min<int64_t>(1 << 18, std::max<int64_t>(1 << 15, 16 * B.k_max));
+                                     : (uint64_t)std::min<int64_t>(1 << 17, std::max<int64_t>(1 << 13, 8 * B.k_max));
     S = std::min<uint64_t>(S, std::max<uint64_t>(span / 32, std::min<uint64_t>(span, 4096)));
     if (S > 0) {
       SampleLaunch P;
@@ -774,7 +776,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       ++st.launches;
     }
     {
-      tau_kernel<<<nq, 1024, 0, s>>>(dq, 0, autok ? 1 : 0);
+      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok ? 1 : 0);
       ++st.launches;
     }
   }
@@ -903,7 +905,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         }
       }
       if (ci + 1 < bounds.size()) {
-        tau_kernel<<<nq, 1024, 0, s>>>(dq, 1);  // raise tau from the candidates so far
+        tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 1);  // raise tau from the candidates so far
         ++st.launches;
       }
     }
@@ -912,7 +914,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   APEX_CU(stage_mark(c, 7, s));
   APEX_CU(stage_mark(c, 3, s));
   // final bound, compaction, exact select
-  tau_kernel<<<nq, 1024, 0, s>>>(dq, 2);
+  tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 2);
   ++st.launches;
   MatLaunch M;
   M.queries = dq;
@@ -1652,6 +1654,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "multi") c->opt_multi = v;
   else if (n == "graph") c->opt_graph = v;
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
+  else if (n == "tiles_per_slot") c->opt_tiles_per_slot = std::max<int64_t>(1, v);
   else if (n == "mode") {
     if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;

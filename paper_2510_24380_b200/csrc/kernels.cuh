@@ -344,19 +344,20 @@ __device__ __forceinline__ unsigned long long live_mask(const ScanLaunch& L, uns
   return m;
 }
 
-// In-kernel threshold refresh (one warp): B = highest key>>48 bin such that the
-// candidates appended so far with key >= B<<48 number at least k; counts are
-// read while other warps keep appending, and a stale (smaller) count only
-// lowers B, so tau = B<<48 is always a valid lower bound on the final k-th
-// best key.  Two levels: 256 coarse bins (key>>56), then the 256 fine bins of
-// the chosen coarse bin.
-__device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
+// Two-level (256 coarse x 256 fine) search by ONE warp of the highest fine
+// bin B with sum_{b >= B} fine[b] >= k, where coarse[c] = sum of fine bins
+// c*256 .. c*256+255.  Returns B (-1 if the coarse total is below k) and, in
+// *count_ge, the number of entries at/above B (or the total).  When the fine
+// counts lag the coarse ones (concurrent appends) and do not reach k inside
+// the chosen coarse bin, returns that coarse bin's lowest fine bin (still a
+// valid bound: the coarse counts above and at it reach k).
+__device__ int kth_two_level(const unsigned int* __restrict__ fine, const unsigned int* __restrict__ coarse,
+                             unsigned long long k, unsigned long long* count_ge) {
   const unsigned lane = lane_id();
-  const unsigned long long k = (unsigned long long)Q.k;
   unsigned long long above = 0;
   int coarse_bin = -1;
   for (int base = 255; base >= 0 && coarse_bin < 0; base -= 32) {
-    const unsigned long long v = __ldcg(Q.coarse + (base - (int)lane));
+    const unsigned long long v = __ldcg(coarse + (base - (int)lane));
     unsigned long long incl = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -372,10 +373,12 @@ __device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
       above += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
-  if (coarse_bin < 0) return;  // fewer than k candidates so far
-  int fine_bin = -1;
-  for (int base = 255; base >= 0 && fine_bin < 0; base -= 32) {
-    const unsigned long long v = __ldcg(Q.hist + ((coarse_bin << 8) | (base - (int)lane)));
+  if (coarse_bin < 0) {
+    if (count_ge) *count_ge = above;
+    return -1;
+  }
+  for (int base = 255; base >= 0; base -= 32) {
+    const unsigned long long v = __ldcg(fine + ((coarse_bin << 8) | (base - (int)lane)));
     unsigned long long incl = v;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -384,18 +387,25 @@ __device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
     }
     const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
     if (m) {
-      fine_bin = base - (__ffs(m) - 1);
-    } else {
-      above += __shfl_sync(0xffffffffu, incl, 31);
+      const int l = __ffs(m) - 1;
+      if (count_ge) *count_ge = above + __shfl_sync(0xffffffffu, incl, l);
+      return (coarse_bin << 8) | (base - l);
     }
+    above += __shfl_sync(0xffffffffu, incl, 31);
   }
-  // the fine counts may lag the coarse ones: if the coarse bin's fine bins do
-  // not (yet) reach k, fall back to the coarse bin's lower edge
-  const unsigned long long base = Q.ctl->hist_base;
-  const unsigned shift = Q.ctl->hist_shift;
-  const unsigned long long key = fine_bin >= 0 ? bin_edge((unsigned)((coarse_bin << 8) | fine_bin), base, shift)
-                                               : bin_edge((unsigned)(coarse_bin << 8), base, shift);
-  if (lane == 0) atomicMax(&Q.ctl->tau_key, key);
+  if (count_ge) *count_ge = above;
+  return coarse_bin << 8;
+}
+
+// In-kernel threshold refresh (one warp): tau = lower edge of the k-th best
+// candidate bin, read while other warps keep appending; a stale (smaller)
+// count only lowers the bound, so it stays a valid lower bound on the final
+// k-th best key.
+__device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
+  const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, nullptr);
+  if (B < 0) return;
+  const unsigned long long key = bin_edge((unsigned)B, Q.ctl->hist_base, Q.ctl->hist_shift);
+  if (lane_id() == 0) atomicMax(&Q.ctl->tau_key, key);
 }
 
 template <int NT, int RL>
@@ -752,9 +762,26 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   constexpr int kTauPoll = 8;                      // column blocks between admission-threshold polls
   int poll = 0;
 
+  // software-pipelined work items: the next item's tile descriptor and its
+  // query's admission threshold are loaded while the current item runs
   unsigned qi, t;
-  while (next_item(L, wc, live, lane, qi, t)) {
-    const ScanQuery& Q = L.queries[qi];
+  bool have = next_item(L, wc, live, lane, qi, t);
+  Tile T_n;
+  unsigned long long tau_n = 0;
+  if (have) {
+    T_n = L.tiles[t];
+    tau_n = *(volatile unsigned long long*)&L.queries[qi].ctl->tau_key;
+  }
+  while (have) {
+    const unsigned q_cur = qi;
+    const Tile T = T_n;
+    unsigned long long tau_pref = tau_n;
+    have = next_item(L, wc, live, lane, qi, t);
+    if (have) {
+      T_n = L.tiles[t];
+      tau_n = *(volatile unsigned long long*)&L.queries[qi].ctl->tau_key;
+    }
+    const ScanQuery& Q = L.queries[q_cur];
     QCtl* ctl = Q.ctl;
     Entry* __restrict__ buf = Q.buf;
     unsigned int* __restrict__ hist = Q.hist;
@@ -763,10 +790,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
     const double b_obj = Q.test_bias[0];
     const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
     const int nt = Q.nt;
-    const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
-    const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
-    unsigned long long tau_pref = *(volatile unsigned long long*)&ctl->tau_key;
-    const Tile T = L.tiles[t];
     const DevReaction& R = L.rx[T.rx];
     const int c = R.c;
     const int64_t n_last = R.size[c - 1];
@@ -919,6 +942,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
                   e.g = gbase[r] + (unsigned long long)col;
                   const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
                   if (idx < cap) buf[idx] = e;
+                  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
+                  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
                   const unsigned hb = hist_bin(e.key, hbase, hshift);
                   atomicAdd(&hist[hb], 1u);
                   atomicAdd(&Q.coarse[hb >> 8], 1u);
@@ -1313,6 +1338,7 @@ __global__ void sample_kernel(const SampleLaunch P, int nq) {
           val = __dadd_rn(val, Q.test_bias[0]);
           key = skey(Q.maximize ? val : -val);
           atomicAdd(&Q.seed_hist[key >> 48], 1u);
+          atomicAdd(&Q.seed_hist[2 * kHistBins + (key >> 56)], 1u);
         }
       }
       unsigned long long mx = key;
@@ -1401,6 +1427,7 @@ __global__ void corner_kernel(const CornerLaunch P) {
           val = __dadd_rn(val, Q.test_bias[0]);
           key = skey(Q.maximize ? val : -val);
           atomicAdd(&Q.seed_hist[kHistBins + (key >> 48)], 1u);
+          atomicAdd(&Q.seed_hist[2 * kHistBins + 256 + (key >> 56)], 1u);
         }
       }
     }
@@ -1464,7 +1491,7 @@ __device__ int kth_bin(const unsigned int* __restrict__ h, unsigned long long k,
   return B;
 }
 
-// tau from key histograms (one CTA of 1024 threads per query).  At least k
+// tau from key histograms, one warp per query (two-level search).  At least k
 // distinct feasible products have key >= the returned bin's lower edge, so it
 // is a valid lower bound on the final k-th best key.
 //   mode 0: seed — max over the uniform-sample and the corner histograms
@@ -1473,16 +1500,19 @@ __device__ int kth_bin(const unsigned int* __restrict__ h, unsigned long long k,
 //           seed_max] spread over ~1/4 of its bins;
 //   mode 1: raise tau from the candidate histogram;
 //   mode 2: final bound (and the count at/above it) for the select.
-__global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__ qs, int mode, int auto_kernel = 0) {
-  const ScanQuery& Q = qs[blockIdx.x];
+__global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, int auto_kernel = 0) {
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const ScanQuery& Q = qs[q];
   QCtl* ctl = Q.ctl;
   if (!*(volatile unsigned int*)&ctl->active) return;
   const unsigned long long k = (unsigned long long)Q.k;
+  const bool lead = lane_id() == 0;
   unsigned long long cnt = 0;
   if (mode == 0) {
-    const int b0 = kth_bin(Q.seed_hist, k, &cnt);
-    const int b1 = kth_bin(Q.seed_hist + kHistBins, k, &cnt);
-    if (threadIdx.x == 0) {
+    const int b0 = kth_two_level(Q.seed_hist, Q.seed_hist + 2 * kHistBins, k, nullptr);
+    const int b1 = kth_two_level(Q.seed_hist + kHistBins, Q.seed_hist + 2 * kHistBins + 256, k, nullptr);
+    if (lead) {
       unsigned long long key = kNoTau;
       if (b0 >= 0) key = (unsigned long long)b0 << 48;
       if (b1 >= 0) key = max(key, (unsigned long long)b1 << 48);
@@ -1501,14 +1531,14 @@ __global__ void __launch_bounds__(1024) tau_kernel(const ScanQuery* __restrict__
       if (auto_kernel) ctl->use_full = ctl->tau_key == kNoTau ? 1u : 0u;
     }
   } else {
-    const int B = kth_bin(Q.hist, k, &cnt);
-    if (threadIdx.x == 0) {
+    const int B = kth_two_level(Q.hist, Q.coarse, k, &cnt);
+    if (lead) {
       if (mode == 1) {
         if (B >= 0) {
           const unsigned long long key = bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift);
           if (key > ctl->tau_key) ctl->tau_key = key;
         }
-        ctl->tile_counter = 0;  // the next chunk's scan redistributes its tiles
+        ctl->tile_counter = 0;
       } else {
         ctl->bound_key = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
         ctl->comp_count = cnt;  // candidates with key >= bound
