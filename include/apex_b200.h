@@ -202,6 +202,12 @@ int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);
  * ((p + x) + b) >= beta, -inf if all, NaN if none. */
 int apex_debug_thresholds(apex_ctx* ctx, const double* p, const double* b, const double* beta, int64_t n,
                           float* up, float* lo);
+/* Profiling hook: per-work-item records of the last admission scan, enabled by
+ * apex_set_option(ctx, "trace", capacity).  Eight words per record:
+ * start ns, end ns, smid | rare-path entries << 8 | query << 32,
+ * ncols << 8 | nrows | reaction << 32, rare-path cycles, threshold cycles,
+ * staging cycles, candidates.  *n = records copied. */
+int apex_debug_trace(apex_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n);
 int apex_get_device_info(apex_ctx* ctx, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
 
 #ifdef __cplusplus

@@ -26,7 +26,7 @@ EXPORTED = (
     "apex_last_error", "apex_version", "apex_ctx_create", "apex_ctx_destroy", "apex_set_stream",
     "apex_load_library", "apex_load_table", "apex_load_cache", "apex_precompute_device", "apex_query",
     "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_set_option", "apex_get_device_info",
-    "apex_debug_thresholds",
+    "apex_debug_thresholds", "apex_debug_trace",
 )
 
 
@@ -140,8 +140,11 @@ def load_library(path: Path | None = None):
         "apex_set_option": ([vp, C.c_char_p, C.c_int64], C.c_int),
         "apex_get_device_info": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
         "apex_debug_thresholds": ([vp, vp, vp, vp, C.c_int64, vp, vp], C.c_int),
+        "apex_debug_trace": ([vp, vp, C.c_int64, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if name.startswith("apex_debug_") and not hasattr(lib, name):
+            continue  # profiling hooks are optional (older builds in A/B runs)
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
@@ -359,3 +362,10 @@ class DeviceContext:
         lo = np.empty(len(p), dtype=np.float32)
         _check(self.lib.apex_debug_thresholds(self._ctx, _ptr(p), _ptr(b), _ptr(beta), len(p), _ptr(up), _ptr(lo)))
         return up, lo
+
+    def debug_trace(self, cap: int) -> np.ndarray:
+        """Per-item records of the last admission scan (needs set_option("trace", cap))."""
+        out = np.zeros((cap, 8), dtype=np.uint64)
+        n = C.c_int64(0)
+        _check(self.lib.apex_debug_trace(self._ctx, _ptr(out), cap, C.byref(n)))
+        return out[:n.value]

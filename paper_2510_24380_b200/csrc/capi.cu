@@ -195,6 +195,8 @@ struct apex_ctx {
   std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
   DBuf d_groups, d_tctr;                 // multi-query kernel: group descriptors, work counters
   DBuf d_work;                           // flattened-work counters of the scan launches
+  DBuf d_trace;                          // optional per-item timing records of the admission scan
+  int64_t trace_cap = 0, trace_n = 0;
   HBuf h_groups;
   cudaEvent_t groups_ev = nullptr;
   HBuf h_queries, h_ctl, h_out, h_tau0;
@@ -219,8 +221,10 @@ struct apex_ctx {
                                     // the seed found a threshold, else full predicate), 2 = admission-first
                                     // (exact short-circuit), 0 = full predicate (FSETP chain),
                                     // 1 = full predicate (FADD2 sign bits)
-  int64_t opt_cb_admit = 256;       // columns per smem block in the admission-first kernel
+  int64_t opt_cb_admit = 512;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
+  int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
+  int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
@@ -806,7 +810,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   for (size_t ci = 0; ci < bounds.size(); ++ci) {
     const size_t te = bounds[ci];
     if (te > tb) {
-      ScanLaunch L;
+      ScanLaunch L{};
       L.tiles = plan->d_tiles.as<Tile>();
       L.tile_begin = (unsigned)tb;
       L.tile_end = (unsigned)te;
@@ -862,9 +866,13 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         ++st.scans;
       } else if (admit) {
         const int cba = (int)c->opt_cb_admit;
-        ScanFn fn = B.rl == 2 ? scan_admit_kernel<2> : scan_admit_kernel<1>;
+        const bool tr = c->trace_cap > 0;
+        ScanFn fn = B.rl == 2 ? (tr ? scan_admit_kernel<2, true> : scan_admit_kernel<2, false>)
+                              : (tr ? scan_admit_kernel<1, true> : scan_admit_kernel<1, false>);
         const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) +
-                            (size_t)kScanWarps * 16 * kMaxTests * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
+                            (size_t)kScanWarps * 16 * kMaxTests * sizeof(float) +
+                            (size_t)kScanWarps * 512 * B.rl * sizeof(unsigned short) +
+                            (size_t)kScanWarps * 2 * sizeof(uint64_t) + kBlockDq * sizeof(DenseItem) + 16;
         int occ = 0;
         APEX_TRY(scan_occupancy(fn, smem, &occ));
         for (int q0 = 0; q0 < nq; q0 += 64) {
@@ -874,9 +882,17 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           ScanLaunch La = L;
           La.cb = cba;
+          La.vote64 = (int)c->opt_vote64;
+          La.dense_min = c->opt_dense > 0 ? (int)c->opt_dense : 1 << 20;
+          if (c->trace_cap > 0) {
+            La.trace = c->d_trace.as<unsigned long long>();
+            La.trace_cap = (unsigned)c->trace_cap;
+            c->trace_n = std::min<int64_t>(c->trace_cap, (int64_t)(te - tb) * nql);
+          }
           La.queries = dq + q0;
           La.nq = nql;
-          La.work = c->d_work.as<unsigned>() + (wi++ % 64);
+          const int slot = wi++ % 64;
+          La.work = c->d_work.as<unsigned>() + slot;
           fn<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La);
           APEX_CU(cudaGetLastError());
           ++st.launches;
@@ -1230,6 +1246,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_hists.release();
   c->d_out.release();
   c->d_work.release();
+  c->d_trace.release();
   c->h_queries.release();
   c->h_ctl.release();
   c->h_out.release();
@@ -1651,6 +1668,17 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
+  else if (n == "vote64") c->opt_vote64 = v;
+  else if (n == "dense") c->opt_dense = v;
+  else if (n == "trace") {
+    // records of the admission scan's per-item trace (0: off); debug only
+    c->trace_cap = std::max<int64_t>(0, std::min<int64_t>(v, 1ll << 26));
+    c->trace_n = 0;
+    if (c->trace_cap) {
+      APEX_TRY(c->d_trace.ensure((size_t)c->trace_cap * 64));
+      APEX_CU(cudaMemset(c->d_trace.p, 0, (size_t)c->trace_cap * 64));
+    }
+  }
   else if (n == "multi") c->opt_multi = v;
   else if (n == "graph") c->opt_graph = v;
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
@@ -1659,7 +1687,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
     if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
     c->opt_mode = v;
   } else if (n == "cb_admit") {
-    if (v < 16 || v % 16 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 16 in [16, 4096]");
+    if (v < 64 || v % 64 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 64 in [64, 4096]");
     c->opt_cb_admit = v;
   }
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
@@ -1702,6 +1730,16 @@ int apex_debug_thresholds(apex_ctx* c, const double* p, const double* b, const d
   APEX_CU(cudaMemcpy(up, du.p, n * 4, cudaMemcpyDeviceToHost));
   APEX_CU(cudaMemcpy(lo, dl.p, n * 4, cudaMemcpyDeviceToHost));
   for (DBuf* d : {&dp, &db, &dbeta, &du, &dl}) d->release();
+  return APEX_OK;
+}
+
+int apex_debug_trace(apex_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
+  APEX_TRY(check_ctx(c, false));
+  const int64_t m = std::min<int64_t>(cap, c->trace_n);
+  if (n) *n = std::max<int64_t>(m, 0);
+  if (m <= 0) return APEX_OK;
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  APEX_CU(cudaMemcpy(out, c->d_trace.p, (size_t)m * 64, cudaMemcpyDeviceToHost));
   return APEX_OK;
 }
 

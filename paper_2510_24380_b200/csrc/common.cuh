@@ -77,7 +77,19 @@ constexpr int kHistBins = 65536;  // candidate histogram bins
 
 // Candidate histogram bin of a key (relative to the seed threshold, see
 // tau_kernel mode 0); the top bin absorbs everything above its lower edge.
-__host__ __device__ __forceinline__ unsigned hist_bin(unsigned long long key, unsigned long long base, unsigned shift) {
+__host__ __device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ unsigned hist_bin(unsigned long long key, unsigned long long base, unsigned shift) {
   const unsigned long long rel = (key - base) >> shift;
   return rel > 65535ull ? 65535u : (unsigned)rel;
 }
@@ -204,6 +216,9 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

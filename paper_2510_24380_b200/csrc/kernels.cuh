@@ -299,6 +299,10 @@ struct ScanLaunch {
   int nq;                 // queries of this launch (<= 64)
   unsigned int* work;     // flattened (tile x query) work counter, zeroed before the launch
   int chunk;              // work items per atomic
+  int vote64;             // admission kernel: 64-column pre-vote on/off
+  int dense_min;          // admission kernel: admitted products of a row in a tile that flag it dense
+  unsigned long long* trace;  // per-item timing records (8 words) or null
+  unsigned trace_cap;         // records
 };
 
 // Flattened persistent work distribution: item -> (tile = item / nq,
@@ -733,8 +737,161 @@ __device__ __forceinline__ float min16_shared(uint32_t addr) {
                fminf(fminf(fminf(c0, c1), fminf(c2, c3)), fminf(fminf(d0, d1), fminf(d2, d3))));
 }
 
-template <int RL>
-__global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const ScanLaunch L) {
+// Dense-row work item: the rest of one row of a tile whose objective
+// threshold admits many columns, with the row's exact thresholds; pushed by
+// the warp that found the row dense, finished by whichever warp is free.
+struct DenseItem {
+  const float* col_src;        // signed objective column at the tile's aligned start
+  long long last_pair0;        // table row of the tile's aligned first column
+  unsigned long long gbase;    // global index of that column in this row
+  double p_obj;                // fp64 objective prefix of the row
+  float thr_obj;               // admission threshold (signed objective) when pushed
+  int from, ncols;             // columns [from, ncols) of the tile remain
+  int q;                       // query of the launch
+  unsigned ready;              // 1 once written; reset by the consumer
+  unsigned _pad;
+  float thrc[kMaxTests];       // constraint thresholds (index 1..nt-1)
+};
+
+// One dense row with all 32 lanes across its columns (two per lane), the
+// objective and constraint contributions read from L2 with every test's loads
+// issued together; candidates appended warp-aggregated.  ts: thresholds
+// (ts[i]) and test descriptors (task << 1 | lower, as int bits at
+// ts[kMaxTests + i]) in the warp's shared scratch.  Returns admitted products.
+__device__ __noinline__ unsigned dense_row(const ScanQuery& Q, const float* __restrict__ values, int64_t n_pairs,
+                                           const float* col_src, int64_t last_pair0, unsigned long long gb, double po,
+                                           float to, int from, int ncols, const float* ts,
+                                           unsigned long long hbase, unsigned hshift) {
+  const unsigned lane = lane_id();
+  const float pad_y = __int_as_float(0x7fffffff);
+  const int nt = Q.nt;
+  const int maximize = Q.maximize;
+  const double b_obj = Q.test_bias[0];
+  QCtl* ctl = Q.ctl;
+  unsigned admitted = 0;
+  for (int cc = from; cc < ncols; cc += 64) {
+    const int col0 = cc + (int)lane, col1 = col0 + 32;
+    const bool in0 = col0 < ncols, in1 = col1 < ncols;
+    const float y0 = in0 ? __ldcg(col_src + col0) : pad_y;
+    const float y1 = in1 ? __ldcg(col_src + col1) : pad_y;
+    bool p0 = y0 <= to, p1 = y1 <= to;
+    admitted += (p0 ? 1u : 0u) + (p1 ? 1u : 0u);
+    if (__any_sync(0xffffffffu, p0 || p1)) {
+#pragma unroll 4
+      for (int i = 1; i < nt; ++i) {
+        const int tl = __float_as_int(ts[kMaxTests + i]);
+        const float* vx = values + (int64_t)(tl >> 1) * n_pairs + last_pair0;
+        float x0 = in0 ? __ldg(vx + col0) : 0.0f;
+        float x1 = in1 ? __ldg(vx + col1) : 0.0f;
+        if (tl & 1) {
+          x0 = -x0;
+          x1 = -x1;
+        }
+        const float t = ts[i];
+        p0 = p0 && x0 <= t;
+        p1 = p1 && x1 <= t;
+      }
+    }
+    const unsigned cnt = (p0 ? 1u : 0u) + (p1 ? 1u : 0u);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += o;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) continue;
+    unsigned long long cbase = 0;
+    if (lane == 31) cbase = atomicAdd(&ctl->count, (unsigned long long)tot);
+    cbase = __shfl_sync(0xffffffffu, cbase, 31);
+    unsigned long long idx = cbase + (incl - cnt);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!(h ? p1 : p0)) continue;
+      const float y = h ? y1 : y0;
+      const float x = maximize ? -y : y;
+      const double val = fx(po, x, b_obj);
+      Entry e;
+      e.key = skey(maximize ? val : -val);
+      e.g = gb + (unsigned long long)(h ? col1 : col0);
+      if (idx < Q.cap) Q.buf[idx] = e;
+      ++idx;
+      const unsigned hb = hist_bin(e.key, hbase, hshift);
+      atomicAdd(&Q.hist[hb], 1u);
+      atomicAdd(&Q.coarse[hb >> 8], 1u);
+    }
+    if (cbase / Q.refresh != (cbase + tot) / Q.refresh) {
+      __threadfence();
+      refresh_tau(Q);
+    }
+  }
+  return admitted;
+}
+
+constexpr int kBlockDq = 32;  // dense-row queue slots per block (shared memory)
+
+// Claim one queued dense row of the block (lane 0 CAS on the shared head,
+// bounded by the tail); returns the slot or ~0u.
+__device__ __forceinline__ unsigned claim_dense(unsigned* ctr, unsigned lane) {
+  unsigned tk = ~0u;
+  if (lane == 0) {
+    for (;;) {
+      const unsigned h = *(volatile unsigned*)&ctr[0];
+      const unsigned tl = *(volatile unsigned*)&ctr[1];
+      const unsigned lim = tl < (unsigned)kBlockDq ? tl : (unsigned)kBlockDq;
+      if (h >= lim) break;
+      if (atomicCAS(&ctr[0], h, h + 1u) == h) {
+        tk = h;
+        break;
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, tk, 0);
+}
+
+// Run a claimed dense row: wait for its writer, stage its thresholds, scan
+// the row with the admission threshold of the query's current tau.
+__device__ __noinline__ void run_dense(const ScanLaunch& L, DenseItem* it, float* scratch) {
+  const unsigned lane = lane_id();
+  if (lane == 0)
+    while (*(volatile unsigned*)&it->ready == 0u) {
+    }
+  __syncwarp();
+  __threadfence_block();
+  const int q = it->q;
+  const ScanQuery& Q = L.queries[q];
+  const int nt = Q.nt;
+  for (int i = 1 + (int)lane; i < nt; i += 32) {
+    scratch[i] = it->thrc[i];
+    scratch[kMaxTests + i] = __int_as_float((Q.test_task[i] << 1) | (Q.test_lower[i] ? 1 : 0));
+  }
+  const float* col_src = it->col_src;
+  const long long last_pair0 = it->last_pair0;
+  const unsigned long long gb = it->gbase;
+  const double po = it->p_obj;
+  float to = it->thr_obj;
+  const int from = it->from, ncols = it->ncols;
+  __syncwarp();
+  if (ncols <= from) return;
+  // the admission threshold may have risen since the push
+  const unsigned long long tau = *(volatile unsigned long long*)&Q.ctl->tau_key;
+  if (tau != kNoTau) {
+    const double ts = key_to_score(tau);
+    to = Q.maximize ? -thr_lower_fast(po, Q.test_bias[0], ts) : thr_upper_fast(po, Q.test_bias[0], -ts);
+  }
+  const unsigned long long hbase = __ldcg(&Q.ctl->hist_base);
+  const unsigned hshift = __ldcg(&Q.ctl->hist_shift);
+  const unsigned a = dense_row(Q, L.values, L.n_pairs, col_src, last_pair0, gb, po, to, from, ncols, scratch, hbase,
+                               hshift);
+  const unsigned as = __reduce_add_sync(0xffffffffu, a);
+  if (lane == 0 && as) atomicAdd(&Q.ctl->admitted, (unsigned long long)as);
+}
+
+#ifndef APEX_ADMIT_MINB
+#define APEX_ADMIT_MINB 2
+#endif
+template <int RL, bool TRACE>
+__global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_kernel(const ScanLaunch L) {
   extern __shared__ __align__(128) float sm_f[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   const unsigned long long live = live_mask(L, 0u);
@@ -746,7 +903,21 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
   // extern array (not a generic pointer) keeps the loads plain LDS
   const int off0 = (int)warp * 2 * cb, off1 = off0 + cb;
   const int xo = kScanWarps * 2 * cb + (int)warp * 16 * kMaxTests;  // rare-path scratch: 16 columns x tests
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cb + kScanWarps * 16 * kMaxTests) + warp * 2;
+  // admitted-pair list of the rare path: up to 16 columns x 32*RL rows
+  unsigned short* pairs = reinterpret_cast<unsigned short*>(sm_f + kScanWarps * 2 * cb + kScanWarps * 16 * kMaxTests) +
+                          warp * (512 * RL);
+  uint64_t* bars_all = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cb + kScanWarps * 16 * kMaxTests +
+                                                   kScanWarps * 256 * RL);
+  uint64_t* bars = bars_all + warp * 2;
+  // block dense-row queue: kBlockDq items, then [head, tail]
+  DenseItem* sdq = reinterpret_cast<DenseItem*>(bars_all + kScanWarps * 2);
+  unsigned* sdq_ctr = reinterpret_cast<unsigned*>(sdq + kBlockDq);
+  if (threadIdx.x == 0) {
+    sdq_ctr[0] = 0u;
+    sdq_ctr[1] = 0u;
+  }
+  for (int i = (int)threadIdx.x; i < kBlockDq; i += (int)blockDim.x) sdq[i].ready = 0u;
+  __syncthreads();
   if (lane == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -772,9 +943,23 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
     T_n = L.tiles[t];
     tau_n = *(volatile unsigned long long*)&L.queries[qi].ctl->tau_key;
   }
-  while (have) {
+  for (;;) {
+    // queued dense rows first (they are what the tail of the launch waits on)
+    if (!have || *(volatile unsigned*)&sdq_ctr[1] > *(volatile unsigned*)&sdq_ctr[0]) {
+      for (;;) {
+        const unsigned tk = claim_dense(sdq_ctr, lane);
+        if (tk == ~0u) break;
+        run_dense(L, sdq + tk, sm_f + xo);
+      }
+    }
+    if (!have) break;
     const unsigned q_cur = qi;
+    const unsigned t_cur = t;
+    const unsigned long long t_start = TRACE ? globaltimer_ns() : 0ull;
+    unsigned rare = 0;
+    unsigned long long cyc_thr = 0, cyc_stage = 0, cyc_rare = 0, n_cand = 0;
     const Tile T = T_n;
+    unsigned admitted = 0;
     unsigned long long tau_pref = tau_n;
     have = next_item(L, wc, live, lane, qi, t);
     if (have) {
@@ -813,6 +998,19 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
     float thr[RL];
     float thrc[RL][kMaxTests];  // constraint thresholds (rare path, local memory)
     bool thr_ready = false;
+    // dense rows (dense_min admitted products so far in this tile): taken out
+    // of the column-group vote and finished row-parallel after the tile
+    // (below), so a tile whose good rows admit a few columns of every group
+    // does not pay the rare path per group
+    bool dense[RL];
+    int dense_from[RL];
+    unsigned adm_row[RL];  // admitted products of the row so far in this tile
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      dense[r] = false;
+      dense_from[r] = 0;
+      adm_row[r] = 0;
+    }
     double p_obj[RL];
     int64_t pr[RL][kMaxRg - 1];
     unsigned long long gbase[RL];
@@ -876,22 +1074,36 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
       else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
       const int yo = bi ? off1 : off0;
       const int ngroups = (ncol + 15) >> 4;
-      if ((ncol & 15) || (blk == 0 && lead)) {
-        const int pad = (ngroups << 4) - ncol;
-        if ((int)lane < pad) sm_f[yo + ncol + lane] = pad_y;
+      if ((ncol & 63) || (blk == 0 && lead)) {
+        // pad to a multiple of 64 columns with values that never pass
+        const int pad = ((ncol + 63) & ~63) - ncol;
+        for (int i = (int)lane; i < pad; i += 32) sm_f[yo + ncol + i] = pad_y;
         if (blk == 0 && lane < lead) sm_f[yo + lane] = pad_y;
         __syncwarp();
       }
-      float thr_min = thr[0];
+      float thr_min = dense[0] ? pad_y : thr[0];
 #pragma unroll
-      for (int r = 1; r < RL; ++r) thr_min = fmaxf(thr_min, thr[r]);
+      for (int r = 1; r < RL; ++r) thr_min = fmaxf(thr_min, dense[r] ? pad_y : thr[r]);
       const uint32_t ybase = smem_u32(sm_f) + (uint32_t)yo * 4u;
       for (int gi = 0; gi < ngroups; ++gi) {
         const int j0 = gi << 4;
-        // min over the 16 columns (4 broadcast LDS.128 + FMNMX3 chain), one
-        // compare per lane, one vote per warp
+        if (L.vote64 && (gi & 3) == 0) {
+          // 64 columns per vote: 16 broadcast LDS.128 in flight, four min
+          // trees, one compare per lane; skip all four 16-column groups when
+          // no lane admits anything
+          const uint32_t a0 = ybase + (uint32_t)j0 * 4u;
+          const float m64 = fminf(fminf(min16_shared(a0), min16_shared(a0 + 64u)),
+                                  fminf(min16_shared(a0 + 128u), min16_shared(a0 + 192u)));
+          if (!__any_sync(0xffffffffu, m64 <= thr_min)) {
+            gi += 3;
+            continue;
+          }
+        }
+        // min over the 16 columns, one compare per lane, one vote per warp
         const float ymin = min16_shared(ybase + (uint32_t)j0 * 4u);
         if (__any_sync(0xffffffffu, ymin <= thr_min)) {
+          if (TRACE) ++rare;
+          const unsigned long long c_r0 = TRACE ? clock64() : 0ull;
           // rare path.  Admitted products (s >= tau) get the constraint
           // predicate with exact per-row fp32 thresholds (computed once per
           // tile, on first use) against the 16 columns' contributions staged
@@ -899,6 +1111,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
           // infeasible products then costs compares, not fp64 chains.
           if (!thr_ready) {
             thr_ready = true;
+            const unsigned long long c_t0 = TRACE ? clock64() : 0ull;
 #pragma unroll
             for (int r = 0; r < RL; ++r)
               for (int i = 1; i < nt; ++i) {
@@ -908,7 +1121,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
                 thrc[r][i] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
                                              : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
               }
+            if (TRACE) cyc_thr += clock64() - c_t0;
           }
+          const unsigned long long c_s0 = TRACE ? clock64() : 0ull;
           for (int idx = (int)lane; idx < (nt - 1) * 16; idx += 32) {
             const int i = 1 + (idx >> 4), jj = idx & 15;
             const int col = col_base + j0 + jj;
@@ -917,49 +1132,207 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_admit_kernel(const Sc
             sm_f[xo + idx] = Q.test_lower[i] ? -x : x;
           }
           __syncwarp();
+          if (TRACE) cyc_stage += clock64() - c_s0;
+          // admission masks of this lane's rows over the 16 columns, then the
+          // admitted (row, column) pairs are listed in the warp's scratch and
+          // the constraint tests run ONE PAIR PER LANE (the row's thresholds
+          // fetched by shuffle): a hot row admitted in every column costs the
+          // warp one round per 32 admitted products, not 16 lock-step columns
+          unsigned am[RL];
+#pragma unroll
+          for (int r = 0; r < RL; ++r) am[r] = 0u;
+#pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
             const float y0 = sm_f[yo + j0 + jj];
-            const int col = col_base + j0 + jj;
+#pragma unroll
+            for (int r = 0; r < RL; ++r) am[r] |= (!dense[r] && y0 <= thr[r] ? 1u : 0u) << jj;
+          }
+          {
+            bool newly = false;
+#pragma unroll
+            for (int r = 0; r < RL; ++r)
+              if (!dense[r] && (adm_row[r] += __popc(am[r])) >= (unsigned)L.dense_min) {
+                dense[r] = true;
+                dense_from[r] = col_base + j0 + 16;
+                newly = true;
+              }
+            if (newly) {
+              thr_min = dense[0] ? pad_y : thr[0];
+#pragma unroll
+              for (int r = 1; r < RL; ++r) thr_min = fmaxf(thr_min, dense[r] ? pad_y : thr[r]);
+            }
+          }
+          unsigned cnt = 0;
+#pragma unroll
+          for (int r = 0; r < RL; ++r) cnt += __popc(am[r]);
+          admitted += cnt;
+          unsigned incl = cnt;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+            if ((int)lane >= off) incl += o;
+          }
+          const unsigned n_adm = __shfl_sync(0xffffffffu, incl, 31);
+          {
+            unsigned o = incl - cnt;
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
-              bool pass = y0 <= thr[r];
-              const unsigned adm = __ballot_sync(0xffffffffu, pass);
-              if (!adm) continue;
-              if (lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)__popc(adm));
-              if (pass)
-                for (int i = 1; i < nt; ++i) pass = pass && (sm_f[xo + ((i - 1) << 4) + jj] <= thrc[r][i]);
-              const unsigned m = __ballot_sync(0xffffffffu, pass);
-              if (m) {
-                const int leader = __ffs(m) - 1;
-                unsigned long long base = 0;
-                if ((int)lane == leader) base = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (pass) {
-                  const float x = maximize ? -y0 : y0;
-                  const double val = fx(p_obj[r], x, b_obj);
-                  Entry e;
-                  e.key = skey(maximize ? val : -val);
-                  e.g = gbase[r] + (unsigned long long)col;
-                  const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
-                  if (idx < cap) buf[idx] = e;
-                  const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
-                  const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
-                  const unsigned hb = hist_bin(e.key, hbase, hshift);
-                  atomicAdd(&hist[hb], 1u);
-                  atomicAdd(&Q.coarse[hb >> 8], 1u);
-                }
-                if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
-                  __threadfence();
-                  refresh_tau(Q);
-                }
+              unsigned m = am[r];
+              while (m) {
+                const unsigned jj = (unsigned)__ffs(m) - 1u;
+                m &= m - 1u;
+                pairs[o++] = (unsigned short)(((lane + 32u * r) << 4) | jj);
               }
             }
           }
           __syncwarp();
+          for (unsigned base = 0; base < n_adm; base += 32) {
+            const unsigned pi = base + lane;
+            const bool valid = pi < n_adm;
+            const unsigned pv = valid ? pairs[pi] : 0u;
+            const unsigned row = pv >> 4, jj = pv & 15u, src = row & 31u;
+            bool pass = valid;
+            for (int i = 1; i < nt; ++i) {
+              float t = __shfl_sync(0xffffffffu, thrc[0][i], src);
+              if (RL == 2) {
+                const float t1 = __shfl_sync(0xffffffffu, thrc[RL - 1][i], src);
+                if (row >= 32u) t = t1;
+              }
+              pass = pass && (sm_f[xo + ((i - 1) << 4) + jj] <= t);
+            }
+            double po = __shfl_sync(0xffffffffu, p_obj[0], src);
+            unsigned long long gb = __shfl_sync(0xffffffffu, gbase[0], src);
+            if (RL == 2) {
+              const double po1 = __shfl_sync(0xffffffffu, p_obj[RL - 1], src);
+              const unsigned long long gb1 = __shfl_sync(0xffffffffu, gbase[RL - 1], src);
+              if (row >= 32u) {
+                po = po1;
+                gb = gb1;
+              }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (TRACE) n_cand += __popc(m);
+            if (!m) continue;
+            unsigned long long cbase = 0;
+            if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
+            cbase = __shfl_sync(0xffffffffu, cbase, 0);
+            if (pass) {
+              const float y0 = sm_f[yo + j0 + jj];
+              const float x = maximize ? -y0 : y0;
+              const double val = fx(po, x, b_obj);
+              Entry e;
+              e.key = skey(maximize ? val : -val);
+              e.g = gb + (unsigned long long)(col_base + j0 + (int)jj);
+              const unsigned long long idx = cbase + __popc(m & ((1u << lane) - 1u));
+              if (idx < cap) buf[idx] = e;
+              const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+              atomicAdd(&hist[hb], 1u);
+              atomicAdd(&Q.coarse[hb >> 8], 1u);
+            }
+            if (cbase / Q.refresh != (cbase + __popc(m)) / Q.refresh) {
+              __threadfence();
+              refresh_tau(Q);
+            }
+          }
+          __syncwarp();
+          if (TRACE) cyc_rare += clock64() - c_r0;
         }
       }
       __syncwarp();
       bi ^= 1u;
+    }
+    // dense rows: the rest of each such row (from the group after the one
+    // that flagged it) is pushed to the block's dense-row queue, where any
+    // warp of the block takes it at its next item boundary (dense_row: all 32 lanes across the row's columns);
+    // the tile itself stays short, so hot tiles do not become stragglers
+    {
+      unsigned dn = 0;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) dn += dense[r] ? 1u : 0u;
+      if (__any_sync(0xffffffffu, dn != 0u)) {
+        unsigned incl = dn;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const unsigned o = __shfl_up_sync(0xffffffffu, incl, off);
+          if ((int)lane >= off) incl += o;
+        }
+        const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&sdq_ctr[1], tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + tot <= (unsigned)kBlockDq) {
+          unsigned slot = base + incl - dn;
+#pragma unroll
+          for (int r = 0; r < RL; ++r) {
+            if (!dense[r]) continue;
+            DenseItem* it = sdq + slot++;
+            it->col_src = col_src;
+            it->last_pair0 = last_pair0;
+            it->gbase = gbase[r];
+            it->p_obj = p_obj[r];
+            it->thr_obj = thr[r];
+            it->from = dense_from[r];
+            it->ncols = (int)ncols;
+            it->q = (int)q_cur;
+            for (int i = 1; i < nt; ++i) it->thrc[i] = thrc[r][i];
+            __threadfence_block();
+            *(volatile unsigned*)&it->ready = 1u;
+          }
+        } else {
+          // queue full: empty items for the reserved slots that exist (so no
+          // claimer waits forever), then the rows are finished here
+          for (unsigned sl = base + lane; sl < (unsigned)kBlockDq && sl < base + tot; sl += 32) {
+            DenseItem* it = sdq + sl;
+            it->from = 0;
+            it->ncols = 0;
+            it->q = (int)q_cur;
+            __threadfence_block();
+            *(volatile unsigned*)&it->ready = 1u;
+          }
+          float* scratch = sm_f + xo;
+          for (int i = 1 + (int)lane; i < nt; i += 32)
+            scratch[kMaxTests + i] = __int_as_float((Q.test_task[i] << 1) | (Q.test_lower[i] ? 1 : 0));
+#pragma unroll
+          for (int r = 0; r < RL; ++r) {
+            unsigned dm = __ballot_sync(0xffffffffu, dense[r]);
+            while (dm) {
+              const int src = __ffs(dm) - 1;
+              dm &= dm - 1u;
+              for (int i = 1; i < nt; ++i) {
+                const float tv = __shfl_sync(0xffffffffu, thrc[r][i], src);
+                if (lane == 0) scratch[i] = tv;
+              }
+              const float to = __shfl_sync(0xffffffffu, thr[r], src);
+              const double po = __shfl_sync(0xffffffffu, p_obj[r], src);
+              const unsigned long long gb = __shfl_sync(0xffffffffu, gbase[r], src);
+              const int from = __shfl_sync(0xffffffffu, dense_from[r], src);
+              __syncwarp();
+              admitted += dense_row(Q, values, n_pairs, col_src, last_pair0, gb, po, to, from, (int)ncols, scratch,
+                                    __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+    {
+      const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
+      if (a && lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)a);
+    }
+    if (TRACE && lane == 0) {
+      const unsigned rec = (t_cur - L.tile_begin) * (unsigned)L.nq + q_cur;
+      if (rec < L.trace_cap) {
+        unsigned long long* w = L.trace + 8ull * rec;
+        w[4] = cyc_rare;
+        w[5] = cyc_thr;
+        w[6] = cyc_stage;
+        w[7] = n_cand;
+        w[0] = t_start;
+        w[1] = globaltimer_ns();
+        w[2] = (unsigned long long)smid() | ((unsigned long long)(rare < 0xffffffu ? rare : 0xffffffu) << 8) |
+               ((unsigned long long)q_cur << 32);
+        w[3] = ((unsigned long long)T.rx << 32) | ((unsigned long long)T.ncols << 8) | T.nrows;
+      }
     }
   }
 }
