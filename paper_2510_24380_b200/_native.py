@@ -30,6 +30,13 @@ EXPORTED = (
 )
 
 
+class PreparedBatch:
+    """A query batch with its C descriptors and result arrays (DeviceContext.prepare)."""
+
+    def __init__(self, queries, specs, keep, results, bufs):
+        self.queries, self.specs, self.keep, self.results, self.bufs = queries, specs, keep, results, bufs
+
+
 class NativeError(RuntimeError):
     def __init__(self, code: int, message: str):
         super().__init__(message)
@@ -301,6 +308,24 @@ class DeviceContext:
         _check(self.lib.apex_query(self._ctx, specs, len(queries), results, C.byref(st)))
         del keep
         return self._unpack(results, bufs), st.as_dict()
+
+    def prepare(self, queries: list[dict]) -> "PreparedBatch":
+        """Descriptors and caller-owned result arrays built once, for callers
+        that run the same batch shape repeatedly (the C-ABI usage pattern:
+        host buffers allocated by the caller and reused)."""
+        specs, keep = self._specs(queries)
+        results, bufs = self._result_buffers(queries)
+        for b in bufs:  # touch the pages once so no call pays first-touch faults
+            for a in b.values():
+                a.fill(0)
+        return PreparedBatch(queries, specs, keep, results, bufs)
+
+    def run(self, pb: "PreparedBatch") -> tuple[list[dict], dict]:
+        """apex_query on a prepared batch; the returned arrays are views of the
+        batch's buffers (overwritten by the next run of the same batch)."""
+        st = Stats()
+        _check(self.lib.apex_query(self._ctx, pb.specs, len(pb.queries), pb.results, C.byref(st)))
+        return self._unpack(pb.results, pb.bufs), st.as_dict()
 
     def query_async(self, queries: list[dict]) -> dict:
         """Enqueue a batch (one shared range, k >= 1) without a host sync."""

@@ -754,8 +754,10 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       P.start = start;
       P.end = end;
       P.samples = S;
-      const int blocks = (int)std::min<uint64_t>((S + 255) / 256, (uint64_t)c->sm_count * 8);
-      sample_kernel<<<blocks, 256, 0, s>>>(P, nq);
+      // (sample x query) threads: about two waves of the whole GPU
+      const uint64_t want = std::max<uint64_t>(1, (uint64_t)c->sm_count * 16 / (uint64_t)nq);
+      const unsigned blocks = (unsigned)std::min<uint64_t>((S + 255) / 256, want);
+      sample_kernel<<<dim3(blocks, (unsigned)nq), 256, 0, s>>>(P, nq);
       ++st.launches;
     }
     if (c->opt_corner && c->corners_ok) {
@@ -877,9 +879,6 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         APEX_TRY(scan_occupancy(fn, smem, &occ));
         for (int q0 = 0; q0 < nq; q0 += 64) {
           const int nql = std::min(64, nq - q0);
-          const int64_t items = (int64_t)(te - tb) * nql;
-          const int64_t blocks = std::max<int64_t>(
-              1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           ScanLaunch La = L;
           La.cb = cba;
           La.vote64 = (int)c->opt_vote64;
@@ -887,8 +886,11 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
           if (c->trace_cap > 0) {
             La.trace = c->d_trace.as<unsigned long long>();
             La.trace_cap = (unsigned)c->trace_cap;
-            c->trace_n = std::min<int64_t>(c->trace_cap, (int64_t)(te - tb) * nql);
+            c->trace_n = std::min<int64_t>(c->trace_cap, (int64_t)(La.tile_end - La.tile_begin) * nql);
           }
+          const int64_t items = (int64_t)(La.tile_end - La.tile_begin) * nql;
+          const int64_t blocks = std::max<int64_t>(
+              1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           La.queries = dq + q0;
           La.nq = nql;
           const int slot = wi++ % 64;

@@ -1664,15 +1664,23 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 }
 
 __global__ void sample_kernel(const SampleLaunch P, int nq) {
+  // grid.y = query: every query evaluates the same sampled products (the
+  // decode is repeated per query, it is ALU-only); each test's fp64 sum is
+  // formed without short-circuit so all of a sample's loads are in flight
+  // together (the kernel is gather-latency bound)
+  const ScanQuery& Q = P.queries[blockIdx.y];
+  if (!*(volatile unsigned int*)&Q.ctl->active) return;
+  (void)nq;
   const unsigned long long span = P.end - P.start, S = P.samples;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned lane = lane_id();
+  const int nt = Q.nt;
+  unsigned long long mx = 0;
   for (unsigned long long base_i = (unsigned long long)blockIdx.x * blockDim.x; base_i < S; base_i += stride) {
     const unsigned long long i = base_i + threadIdx.x;
-    const bool live = i < S;
-    int64_t pr[kMaxRg];
-    int c = 0;
-    if (live) {
+    unsigned long long key = 0;
+    if (i < S) {
+      int64_t pr[kMaxRg];
       const unsigned long long lo = (unsigned long long)(((unsigned __int128)span * i) / S);
       const unsigned long long hi = (unsigned long long)(((unsigned __int128)span * (i + 1)) / S);
       const unsigned long long g = P.start + lo + mix64(i * 0x9e3779b97f4a7c15ull + 17) % (hi - lo);
@@ -1682,44 +1690,41 @@ __global__ void sample_kernel(const SampleLaunch P, int nq) {
         if (P.g_off[mid] <= g) a = mid; else b = mid;
       }
       const DevReaction& R = P.rx[a];
-      c = R.c;
+      const int c = R.c;
       uint64_t rem = g - R.g_off;
-      for (int j = c - 1; j >= 0; --j) {
-        uint64_t q, d;
-        divmod_u64(q, d, rem, (uint64_t)R.size[j]);
-        pr[j] = R.pair_off[j] + (int64_t)d;
-        rem = q;
-      }
-    }
-    // every query of the batch evaluates the same sampled product
-    for (int qi = 0; qi < nq; ++qi) {
-      const ScanQuery& Q = P.queries[qi];
-      unsigned long long key = 0;
-      if (live) {
-        bool feasible = true;
-        for (int t = 1; t < Q.nt && feasible; ++t) {
-          const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
-          double val = (double)__ldg(v + pr[0]);
-          for (int j = 1; j < c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
-          val = __dadd_rn(val, Q.test_bias[t]);
-          feasible = Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]);
-        }
-        if (feasible) {
-          const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
-          double val = (double)__ldg(v + pr[0]);
-          for (int j = 1; j < c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
-          val = __dadd_rn(val, Q.test_bias[0]);
-          key = skey(Q.maximize ? val : -val);
-          atomicAdd(&Q.seed_hist[key >> 48], 1u);
-          atomicAdd(&Q.seed_hist[2 * kHistBins + (key >> 56)], 1u);
-        }
-      }
-      unsigned long long mx = key;
 #pragma unroll
-      for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-      if (lane == 0 && mx) atomicMax(&Q.ctl->seed_max, mx);
+      for (int j = kMaxRg - 1; j >= 0; --j) {
+        pr[j] = 0;
+        if (j < c) {
+          uint64_t q, d;
+          divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+          pr[j] = R.pair_off[j] + (int64_t)d;
+          rem = q;
+        }
+      }
+      bool feasible = true;
+      double vobj = 0.0;
+      for (int t = 0; t < nt; ++t) {
+        const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
+        double val = (double)__ldg(v + pr[0]);
+#pragma unroll
+        for (int j = 1; j < kMaxRg; ++j)
+          if (j < c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+        val = __dadd_rn(val, Q.test_bias[t]);
+        if (t == 0) vobj = val;
+        else feasible = feasible && (Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]));
+      }
+      if (feasible) {
+        key = skey(Q.maximize ? vobj : -vobj);
+        atomicAdd(&Q.seed_hist[key >> 48], 1u);
+        atomicAdd(&Q.seed_hist[2 * kHistBins + (key >> 56)], 1u);
+      }
     }
+    mx = max(mx, key);
   }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0 && mx) atomicMax(&Q.ctl->seed_max, mx);
 }
 
 // ---------------------------------------------------------------------------
