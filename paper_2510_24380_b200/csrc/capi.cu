@@ -596,7 +596,13 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.seed_hist = Q.coarse + 256;
     Q.ctl = S.ctl.as<QCtl>();
     Q.cap = S.buf.bytes / sizeof(Entry);
-    Q.refresh = (unsigned long long)std::max<int64_t>(c->opt_refresh > 0 ? c->opt_refresh : q.k, 256);
+    {
+      // power of two >= max(refresh interval, 256): the kernels test crossings with a shift
+      const int64_t want = std::max<int64_t>(c->opt_refresh > 0 ? c->opt_refresh : q.k, 256);
+      unsigned sh = 8;
+      while ((1ll << sh) < want && sh < 62) ++sh;
+      Q.refresh_shift = sh;
+    }
     Q.k = q.k;
     Q.nt = T.nt;
     Q.ntp = (kernel_nt(T.nt) + 3) / 4 * 4;
@@ -1599,7 +1605,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
   Q.seed_hist = Q.coarse + 256;
   Q.ctl = S.ctl.as<QCtl>();
   Q.cap = (unsigned long long)cap;
-  Q.refresh = 1ull << 62;
+  Q.refresh_shift = 62;
   Q.k = k;
   Q.maximize = q->maximize ? 1 : 0;
   Q.obj_task = q->objective_task;

@@ -111,7 +111,7 @@ struct ScanQuery {
   unsigned int* seed_hist;        // [kHistBins] histogram of feasible sampled keys
   QCtl* ctl;
   unsigned long long cap;         // capacity of buf / comp (entries)
-  unsigned long long refresh;     // in-kernel tau refresh every `refresh` appended candidates
+  unsigned long long refresh_shift;  // in-kernel tau refresh every 2^refresh_shift appended candidates
   long long k;
   int32_t nt;                     // live tests (test 0 = objective admission)
   int32_t ntp;                    // packed row stride (floats, multiple of 4)
@@ -215,6 +215,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// relaxed gpu-scope loads of values other CTAs update during a kernel
+// (cheaper than volatile, which is system scope)
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {

@@ -340,10 +340,17 @@ __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, u
 
 // queries of the launch that this kernel form scans
 __device__ __forceinline__ unsigned long long live_mask(const ScanLaunch& L, unsigned want_full) {
+  // flags written by earlier kernels of the stream: plain loads, one query per lane
+  const unsigned lane = lane_id();
   unsigned long long m = 0;
-  for (int q = 0; q < L.nq; ++q) {
-    const QCtl* c = L.queries[q].ctl;
-    if (*(volatile unsigned*)&c->active && *(volatile unsigned*)&c->use_full == want_full) m |= 1ull << q;
+  for (int q0 = 0; q0 < L.nq; q0 += 32) {
+    const int q = q0 + (int)lane;
+    bool ok = false;
+    if (q < L.nq) {
+      const QCtl* c = L.queries[q].ctl;
+      ok = __ldcg(&c->active) && __ldcg(&c->use_full) == want_full;
+    }
+    m |= (unsigned long long)__ballot_sync(0xffffffffu, ok) << q0;
   }
   return m;
 }
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
       bulk_g2s(bi ? sbuf1 : sbuf0, col_src, bytes, &bars[bi]);
     }
 
-    const unsigned long long tau = *(volatile unsigned long long*)&ctl->tau_key;
+    const unsigned long long tau = ld_relaxed_u64(&ctl->tau_key);
     const double tau_s = key_to_score(tau);
     unsigned long long tau_seen = tau;
 
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
         bulk_g2s(nb ? sbuf1 : sbuf0, col_src + (size_t)(col_base + cb) * NTP, bytes, &bars[nb]);
       }
       // tighten the admission threshold if another warp raised tau
-      const unsigned long long tau_now = *(volatile unsigned long long*)&ctl->tau_key;
+      const unsigned long long tau_now = ld_relaxed_u64(&ctl->tau_key);
       if (tau_now != tau_seen) {
         tau_seen = tau_now;
         const double ts = key_to_score(tau_now);
@@ -688,7 +695,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
                 }
                 // every `refresh` candidates, the warp that crosses the mark
                 // recomputes tau from the histograms
-                if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
+                if ((base >> Q.refresh_shift) != ((base + __popc(m)) >> Q.refresh_shift)) {
                   __threadfence();
                   refresh_tau(Q);
                 }
@@ -820,7 +827,7 @@ __device__ __noinline__ unsigned dense_row(const ScanQuery& Q, const float* __re
       atomicAdd(&Q.hist[hb], 1u);
       atomicAdd(&Q.coarse[hb >> 8], 1u);
     }
-    if (cbase / Q.refresh != (cbase + tot) / Q.refresh) {
+    if ((cbase >> Q.refresh_shift) != ((cbase + tot) >> Q.refresh_shift)) {
       __threadfence();
       refresh_tau(Q);
     }
@@ -941,7 +948,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
   unsigned long long tau_n = 0;
   if (have) {
     T_n = L.tiles[t];
-    tau_n = *(volatile unsigned long long*)&L.queries[qi].ctl->tau_key;
+    tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
   }
   for (;;) {
     // queued dense rows first (they are what the tail of the launch waits on)
@@ -964,7 +971,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
     have = next_item(L, wc, live, lane, qi, t);
     if (have) {
       T_n = L.tiles[t];
-      tau_n = *(volatile unsigned long long*)&L.queries[qi].ctl->tau_key;
+      tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
     }
     const ScanQuery& Q = L.queries[q_cur];
     QCtl* ctl = Q.ctl;
@@ -1060,7 +1067,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
       if (++poll == kTauPoll) {
         poll = 0;
         const unsigned long long tau_now = tau_pref;
-        tau_pref = *(volatile unsigned long long*)&ctl->tau_key;  // consumed at the next poll
+        tau_pref = ld_relaxed_u64(&ctl->tau_key);  // consumed at the next poll
         if (tau_now != tau_seen) {
           tau_seen = tau_now;
           const double ts = key_to_score(tau_now);
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
               atomicAdd(&hist[hb], 1u);
               atomicAdd(&Q.coarse[hb >> 8], 1u);
             }
-            if (cbase / Q.refresh != (cbase + __popc(m)) / Q.refresh) {
+            if ((cbase >> Q.refresh_shift) != ((cbase + __popc(m)) >> Q.refresh_shift)) {
               __threadfence();
               refresh_tau(Q);
             }
@@ -1602,7 +1609,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_multi_kernel(const Mu
                   atomicAdd(&Q.hist[hb], 1u);
                   atomicAdd(&Q.coarse[hb >> 8], 1u);
                 }
-                if (base / Q.refresh != (base + __popc(m)) / Q.refresh) {
+                if ((base >> Q.refresh_shift) != ((base + __popc(m)) >> Q.refresh_shift)) {
                   __threadfence();
                   refresh_tau(Q);
                 }

@@ -72,3 +72,20 @@ def top_sass(rep, n=40):
     for r in data[:n]:
         print(f"{int(r[0], 16) - a0:6x} {100 * int(r[ix['Warp Stall Sampling (All Samples)']]) / tot:6.2f}% "
               f"{int(r[ix['Instructions Executed']] or 0):10d}  {r[1].strip()}")
+
+
+def by_inst(rep, kernel, so="paper_2510_24380_b200/libapexb200.so", n=40):
+    amap = sass_lines(so, kernel)
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h = rows[1]
+    ix = {x: i for i, x in enumerate(h)}
+    data = [r for r in rows[2:] if len(r) == len(h)]
+    a0 = int(data[0][0], 16)
+    inst = defaultdict(int)
+    for r in data:
+        inst[amap.get(int(r[0], 16) - a0, "?")] += int(r[ix["Instructions Executed"]] or 0)
+    ti = sum(inst.values())
+    for line in sorted(inst, key=lambda k: -inst[k])[:n]:
+        print(f"{line:28s} {100 * inst[line] / ti:7.2f}  {inst[line]}")
