@@ -155,6 +155,18 @@ __global__ void __launch_bounds__(256) precompute_kernel(const double* __restric
 }
 
 
+// 64-bit division with a 32-bit fast path (operands below 2^32)
+__device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n, uint64_t d) {
+  if ((n >> 32) == 0 && (d >> 32) == 0) {
+    const uint32_t n32 = (uint32_t)n, d32 = (uint32_t)d;
+    q = n32 / d32;
+    r = n32 - (uint32_t)q * d32;
+  } else {
+    q = n / d;
+    r = n - q * d;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
@@ -195,8 +207,10 @@ __global__ void pack_kernel(const ScanQuery* __restrict__ qs, const float* __res
   const int ntp = Q.ntp;
   const int64_t n = (row_hi - row_lo) * ntp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = row_lo + i / ntp;
-    const int t = (int)(i % ntp);
+    uint64_t qd, rd;
+    divmod_u64(qd, rd, (uint64_t)i, (uint64_t)ntp);  // 32-bit path for all realistic tables
+    const int64_t p = row_lo + (int64_t)qd;
+    const int t = (int)rd;
     float v = 0.0f;
     if (t < Q.nt) {
       v = __ldg(values + (int64_t)Q.test_task[t] * n_pairs + p);
@@ -240,17 +254,6 @@ __device__ __forceinline__ float thr_lower_fast(double p, double b, double beta)
     }
   }
   return thr_lower(p, b, beta);
-}
-
-__device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n, uint64_t d) {
-  if ((n >> 32) == 0 && (d >> 32) == 0) {
-    const uint32_t n32 = (uint32_t)n, d32 = (uint32_t)d;
-    q = n32 / d32;
-    r = n32 - (uint32_t)q * d32;
-  } else {
-    q = n / d;
-    r = n - q * d;
-  }
 }
 
 // K2b: signed objective column of every reaction's last R-group, laid out at
@@ -355,57 +358,67 @@ __device__ __forceinline__ unsigned long long live_mask(const ScanLaunch& L, uns
   return m;
 }
 
+__device__ __forceinline__ void load_bins256(const unsigned int* __restrict__ h, unsigned (&v)[8]) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __ldcg(h + (255 - 32 * i - (int)lane));
+}
+
+// Highest bin B (as 255 - 32 i - lane order, i.e. scanning from the top) with
+// above + sum_{b >= B} v[b] >= k over 256 bins held 8 per lane (lane l, slot i
+// = bin 255 - 32 i - l).  Returns B or -1; *above_io += bins above B (or all).
+__device__ __forceinline__ int kth_bins256(const unsigned (&v)[8], unsigned long long k, unsigned long long& above,
+                                           unsigned long long* incl_at) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long incl = v[i];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += o;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      const unsigned long long il = __shfl_sync(0xffffffffu, incl, l);
+      const unsigned long long vl = __shfl_sync(0xffffffffu, (unsigned long long)v[i], l);
+      if (incl_at) *incl_at = above + il;
+      above += il - vl;
+      return 255 - 32 * i - l;
+    }
+    above += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return -1;
+}
+
 // Two-level (256 coarse x 256 fine) search by ONE warp of the highest fine
 // bin B with sum_{b >= B} fine[b] >= k, where coarse[c] = sum of fine bins
 // c*256 .. c*256+255.  Returns B (-1 if the coarse total is below k) and, in
 // *count_ge, the number of entries at/above B (or the total).  When the fine
 // counts lag the coarse ones (concurrent appends) and do not reach k inside
 // the chosen coarse bin, returns that coarse bin's lowest fine bin (still a
-// valid bound: the coarse counts above and at it reach k).
+// valid bound: the coarse counts above and at it reach k).  Every level's 256
+// counts are loaded at once (8 per lane): two dependent L2 round trips.
 __device__ int kth_two_level(const unsigned int* __restrict__ fine, const unsigned int* __restrict__ coarse,
                              unsigned long long k, unsigned long long* count_ge) {
-  const unsigned lane = lane_id();
+  unsigned v[8];
+  load_bins256(coarse, v);
   unsigned long long above = 0;
-  int coarse_bin = -1;
-  for (int base = 255; base >= 0 && coarse_bin < 0; base -= 32) {
-    const unsigned long long v = __ldcg(coarse + (base - (int)lane));
-    unsigned long long incl = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += o;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
-    if (m) {
-      const int l = __ffs(m) - 1;
-      coarse_bin = base - l;
-      above += __shfl_sync(0xffffffffu, incl - v, l);
-    } else {
-      above += __shfl_sync(0xffffffffu, incl, 31);
-    }
-  }
-  if (coarse_bin < 0) {
+  const int cbin = kth_bins256(v, k, above, nullptr);
+  if (cbin < 0) {
     if (count_ge) *count_ge = above;
     return -1;
   }
-  for (int base = 255; base >= 0; base -= 32) {
-    const unsigned long long v = __ldcg(fine + ((coarse_bin << 8) | (base - (int)lane)));
-    unsigned long long incl = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += o;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
-    if (m) {
-      const int l = __ffs(m) - 1;
-      if (count_ge) *count_ge = above + __shfl_sync(0xffffffffu, incl, l);
-      return (coarse_bin << 8) | (base - l);
-    }
-    above += __shfl_sync(0xffffffffu, incl, 31);
+  load_bins256(fine + (cbin << 8), v);
+  unsigned long long at = 0;
+  const int fb = kth_bins256(v, k, above, &at);
+  if (fb < 0) {
+    if (count_ge) *count_ge = above;
+    return cbin << 8;
   }
-  if (count_ge) *count_ge = above;
-  return coarse_bin << 8;
+  if (count_ge) *count_ge = at;
+  return (cbin << 8) | fb;
 }
 
 // In-kernel threshold refresh (one warp): tau = lower edge of the k-th best
@@ -1895,8 +1908,25 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
   const bool lead = lane_id() == 0;
   unsigned long long cnt = 0;
   if (mode == 0) {
-    const int b0 = kth_two_level(Q.seed_hist, Q.seed_hist + 2 * kHistBins, k, nullptr);
-    const int b1 = kth_two_level(Q.seed_hist + kHistBins, Q.seed_hist + 2 * kHistBins + 256, k, nullptr);
+    // the two seed histograms (uniform samples, corner) searched together:
+    // both coarse levels in flight, then both fine levels
+    unsigned v0[8], v1[8];
+    load_bins256(Q.seed_hist + 2 * kHistBins, v0);
+    load_bins256(Q.seed_hist + 2 * kHistBins + 256, v1);
+    unsigned long long a0 = 0, a1 = 0;
+    const int c0 = kth_bins256(v0, k, a0, nullptr);
+    const int c1 = kth_bins256(v1, k, a1, nullptr);
+    if (c0 >= 0) load_bins256(Q.seed_hist + (c0 << 8), v0);
+    if (c1 >= 0) load_bins256(Q.seed_hist + kHistBins + (c1 << 8), v1);
+    int b0 = -1, b1 = -1;
+    if (c0 >= 0) {
+      const int f = kth_bins256(v0, k, a0, nullptr);
+      b0 = f < 0 ? c0 << 8 : (c0 << 8) | f;
+    }
+    if (c1 >= 0) {
+      const int f = kth_bins256(v1, k, a1, nullptr);
+      b1 = f < 0 ? c1 << 8 : (c1 << 8) | f;
+    }
     if (lead) {
       unsigned long long key = kNoTau;
       if (b0 >= 0) key = (unsigned long long)b0 << 48;

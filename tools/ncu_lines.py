@@ -11,6 +11,9 @@ import sys
 import tempfile
 from collections import defaultdict
 
+# optional kernel filter for multi-kernel reports: NCU_K=finalize_small_kernel
+KF = ["-k", os.environ["NCU_K"]] if os.environ.get("NCU_K") else []
+
 
 def sass_lines(so, kernel):
     d = tempfile.mkdtemp()
@@ -36,12 +39,14 @@ def sass_lines(so, kernel):
 
 def main(rep, kernel, so="paper_2510_24380_b200/libapexb200.so"):
     amap = sass_lines(so, kernel)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + KF,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    rows = rows[hi - 1:]
     h = rows[1]
     ix = {x: i for i, x in enumerate(h)}
-    data = [r for r in rows[2:] if len(r) == len(h)]
+    data = [r for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
     a0 = int(data[0][0], 16)
     samp = defaultdict(int)
     inst = defaultdict(int)
@@ -60,12 +65,14 @@ if __name__ == "__main__":
 
 
 def top_sass(rep, n=40):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + KF,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    rows = rows[hi - 1:]
     h = rows[1]
     ix = {x: i for i, x in enumerate(h)}
-    data = [r for r in rows[2:] if len(r) == len(h)]
+    data = [r for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
     a0 = int(data[0][0], 16)
     tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
     data.sort(key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))
@@ -76,12 +83,14 @@ def top_sass(rep, n=40):
 
 def by_inst(rep, kernel, so="paper_2510_24380_b200/libapexb200.so", n=40):
     amap = sass_lines(so, kernel)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + KF,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    rows = rows[hi - 1:]
     h = rows[1]
     ix = {x: i for i, x in enumerate(h)}
-    data = [r for r in rows[2:] if len(r) == len(h)]
+    data = [r for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
     a0 = int(data[0][0], 16)
     inst = defaultdict(int)
     for r in data:
