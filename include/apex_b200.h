@@ -193,6 +193,16 @@ int apex_merge_finalize(apex_ctx* ctx, const apex_query_spec* query, const apex_
                         int64_t n_entries, uint64_t total_scanned, apex_result* result,
                         apex_stats* stats);
 
+/* Multi-GPU final step for a whole batch: entries_dev (device) holds the
+ * all-gathered local entries of n_queries queries from n_src ranks, laid out
+ * entries_dev[(src * n_queries + q) * stride + i] (i < stride; padding
+ * g == UINT64_MAX ignored) — what all-gathering every rank's [n_queries][k]
+ * apex_query_local buffer produces.  One device pass selects, orders and
+ * materializes every query's global top-k into results[q]. */
+int apex_merge_finalize_batch(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,
+                              const apex_entry* entries_dev, int32_t n_src, int64_t stride,
+                              uint64_t total_scanned, apex_result* results, apex_stats* stats);
+
 /* Tuning / introspection. */
 int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);
 

@@ -25,7 +25,8 @@ APEX_OK, APEX_EINVAL, APEX_ERANGE, APEX_ETASK, APEX_ECUDA, APEX_ESTATE, APEX_ENO
 EXPORTED = (
     "apex_last_error", "apex_version", "apex_ctx_create", "apex_ctx_destroy", "apex_set_stream",
     "apex_load_library", "apex_load_table", "apex_load_cache", "apex_precompute_device", "apex_query",
-    "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_set_option", "apex_get_device_info",
+    "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_merge_finalize_batch",
+    "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
 )
 
@@ -144,6 +145,8 @@ def load_library(path: Path | None = None):
                              C.c_int),
         "apex_merge_finalize": ([vp, C.POINTER(QuerySpecC), vp, C.c_int64, C.c_uint64, C.POINTER(ResultC),
                                  C.POINTER(Stats)], C.c_int),
+        "apex_merge_finalize_batch": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int32, C.c_int64, C.c_uint64,
+                                       C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_set_option": ([vp, C.c_char_p, C.c_int64], C.c_int),
         "apex_get_device_info": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
         "apex_debug_thresholds": ([vp, vp, vp, vp, C.c_int64, vp, vp], C.c_int),
@@ -350,6 +353,17 @@ class DeviceContext:
         _check(self.lib.apex_query_local(self._ctx, specs, len(queries), C.c_void_p(out_dev_ptr), counts, C.byref(st)))
         del keep
         return [counts[i] for i in range(len(queries))], st.as_dict()
+
+    def merge_finalize_batch(self, queries: list[dict], entries_dev_ptr: int, n_src: int, stride: int,
+                             total_scanned: int, prepared: "PreparedBatch | None" = None):
+        """Global top-k of every query from all-gathered local entries laid out
+        [n_src][len(queries)][stride] (apex_merge_finalize_batch)."""
+        pb = prepared if prepared is not None else self.prepare(queries)
+        st = Stats()
+        _check(self.lib.apex_merge_finalize_batch(self._ctx, pb.specs, len(queries), C.c_void_p(entries_dev_ptr),
+                                                  int(n_src), int(stride), int(total_scanned), pb.results,
+                                                  C.byref(st)))
+        return self._unpack(pb.results, pb.bufs), st.as_dict()
 
     def merge_finalize(self, query: dict, entries_dev_ptr: int, n_entries: int, total_scanned: int):
         specs, keep = self._specs([query])

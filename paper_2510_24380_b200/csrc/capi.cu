@@ -103,9 +103,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, obj_col, buf, comp, sel, sorted, rank, ctl;
+  DBuf packed, obj_col, buf, comp, sel, sorted, rank;
   void release() {
-    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank, &ctl}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank}) b->release();
   }
 };
 
@@ -190,6 +190,7 @@ struct apex_ctx {
   std::vector<Slot> slots;
   DBuf d_queries, d_tau0;
   DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
+  DBuf d_ctls;                           // per-query control blocks, contiguous (one strided D2H of the headers)
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
@@ -558,8 +559,8 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
-    APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
   }
+  APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
   c->out_off.assign(nq + 1, 0);
   for (int i = 0; i < nq; ++i)
     c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
@@ -594,7 +595,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
     Q.coarse = Q.hist + kHistBins;
     Q.seed_hist = Q.coarse + 256;
-    Q.ctl = S.ctl.as<QCtl>();
+    Q.ctl = c->d_ctls.as<QCtl>() + i;
     Q.cap = S.buf.bytes / sizeof(Entry);
     {
       // power of two >= max(refresh interval, 256): the kernels test crossings with a shift
@@ -651,6 +652,58 @@ cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
   cudaStreamIsCapturing(s, &cs);
   if (cs == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(c->ev[e], s, cudaEventRecordExternal);
   return cudaEventRecord(c->ev[e], s);
+}
+
+// Final exact selection of a batch whose candidate buffers and bounds are
+// set: small sets sort + materialize in one CTA per query; the rest go
+// through the cooperative radix select (launched over chunks of queries that
+// fit co-resident), rank, scatter and (finalize) materialization.
+int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool finalize, RunStats& st,
+                   cudaStream_t s, bool mark) {
+  MatLaunch M;
+  M.queries = dq;
+  M.rx = c->d_rx.as<DevReaction>();
+  M.g_off = c->d_goff.as<unsigned long long>();
+  M.n_rx = (int)c->rx.size();
+  M.values = c->d_values.as<float>();
+  M.n_pairs = c->n_pairs;
+  M.biases = c->d_biases.as<double>();
+  {
+    static thread_local bool attr_small = false;
+    const size_t smem_small = (size_t)kSmallSel * sizeof(Entry);
+    if (!attr_small) {
+      APEX_CU(cudaFuncSetAttribute((const void*)finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_small));
+      attr_small = true;
+    }
+    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, finalize ? 1 : 0);
+    ++st.launches;
+  }
+  {
+    static thread_local int occ_sel = 0;
+    if (!occ_sel)
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
+    const int resident = std::max(1, occ_sel * c->sm_count);
+    const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / std::max(nq, 1)));
+    const int q_chunk = std::max(1, resident / per_q);
+    for (int q0 = 0; q0 < nq; q0 += q_chunk) {
+      const ScanQuery* dqc = dq + q0;
+      void* args[] = {(void*)&dqc};
+      APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, std::min(q_chunk, nq - q0)),
+                                          dim3(kSelectThreads), args, 0, s));
+      ++st.launches;
+    }
+  }
+  if (mark) APEX_CU(stage_mark(c, 4, s));
+  if (finalize) {
+    const int ib = (int)((k_max + 255) / 256);
+    const int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
+    rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
+    scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+    materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
+    st.launches += 3;
+  }
+  return APEX_OK;
 }
 
 int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
@@ -880,7 +933,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         const size_t smem = (size_t)kScanWarps * 2 * cba * sizeof(float) +
                             (size_t)kScanWarps * 16 * kMaxTests * sizeof(float) +
                             (size_t)kScanWarps * 512 * B.rl * sizeof(unsigned short) +
-                            (size_t)kScanWarps * 2 * sizeof(uint64_t) + kBlockDq * sizeof(DenseItem) + 16;
+                            (size_t)kScanWarps * 2 * sizeof(uint64_t) + kBlockDq * sizeof(DenseItem) + 16 +
+                            (size_t)kScanWarps * B.rl * kMaxTests * 32 * sizeof(float);
         int occ = 0;
         APEX_TRY(scan_occupancy(fn, smem, &occ));
         for (int q0 = 0; q0 < nq; q0 += 64) {
@@ -940,54 +994,14 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // final bound, compaction, exact select
   tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 2);
   ++st.launches;
-  MatLaunch M;
-  M.queries = dq;
-  M.rx = c->d_rx.as<DevReaction>();
-  M.g_off = c->d_goff.as<unsigned long long>();
-  M.n_rx = (int)c->rx.size();
-  M.values = c->d_values.as<float>();
-  M.n_pairs = c->n_pairs;
-  M.biases = c->d_biases.as<double>();
-  {
-    // small candidate sets: one CTA per query sorts them in shared memory and
-    // materializes; the large path below skips those queries
-    static thread_local bool attr_small = false;
-    const size_t smem_small = (size_t)kSmallSel * sizeof(Entry);
-    if (!attr_small) {
-      APEX_CU(cudaFuncSetAttribute((const void*)finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_small));
-      attr_small = true;
-    }
-    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, B.finalize ? 1 : 0);
-    ++st.launches;
-  }
-  {
-    static thread_local int occ_sel = 0;
-    if (!occ_sel)
-      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
-    const int resident = std::max(1, occ_sel * c->sm_count);
-    const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / nq));
-    if (per_q * nq > resident) return set_err(APEX_ELIMIT, "too many queries in one batch for the select kernel");
-    void* args[] = {(void*)&dq};
-    APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(per_q, nq), dim3(kSelectThreads), args, 0, s));
-    ++st.launches;
-  }
-  APEX_CU(stage_mark(c, 4, s));
-  if (B.finalize) {
-    const int ib = (int)((B.k_max + 255) / 256);
-    const int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
-    rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
-    scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
-    materialize_kernel<<<dim3((unsigned)((B.k_max + 127) / 128), nq), 128, 0, s>>>(M);
-    st.launches += 3;
-  }
+  APEX_TRY(enqueue_select(c, dq, nq, B.k_max, B.finalize, st, s, true));
   APEX_CU(cudaGetLastError());
   APEX_CU(stage_mark(c, 5, s));
-  // control blocks to host (read by check_batch)
+  // control-block headers to host (read by check_batch): one strided copy
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
-  for (int i = 0; i < nq; ++i)
-    APEX_CU(cudaMemcpyAsync(c->h_ctl.as<QCtl>() + i, c->slots[i].ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
-  st.d2h_bytes += nq * (int64_t)sizeof(QCtl);
+  APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
+                            cudaMemcpyDeviceToHost, s));
+  st.d2h_bytes += nq * (int64_t)offsetof(QCtl, hist);
   B.pending = true;
   return APEX_OK;
 }
@@ -1252,6 +1266,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_queries.release();
   c->d_tau0.release();
   c->d_hists.release();
+  c->d_ctls.release();
   c->d_out.release();
   c->d_work.release();
   c->d_trace.release();
@@ -1557,109 +1572,138 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
   return APEX_OK;
 }
 
-int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry* entries_dev, int64_t n_entries,
-                        uint64_t total_scanned, apex_result* res, apex_stats* stats) {
+int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq, const apex_entry* entries_dev,
+                              int32_t n_src, int64_t stride, uint64_t total_scanned, apex_result* res,
+                              apex_stats* stats) {
   APEX_TRY(check_ctx(c, true));
-  if (!q || !res || n_entries < 0 || (n_entries > 0 && !entries_dev)) return set_err(APEX_EINVAL, "bad merge arguments");
-  if (q->objective_task < 0 || q->objective_task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
-  if (q->n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
-  for (int i = 0; i < q->n_constraints; ++i)
-    if (q->constraints[i].task < 0 || q->constraints[i].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
-  if (stats) std::memset(stats, 0, sizeof(*stats));
-  const int64_t k = q->k;
-  res->scanned = total_scanned;
-  if (k == 0 || n_entries == 0) {
-    res->n = 0;
-    res->candidates = res->admitted = 0;
-    res->full_predicate = 0;
-    res->discarded = (int64_t)std::min<uint64_t>((uint64_t)k, total_scanned);
-    return APEX_OK;
+  if (nq < 0 || n_src < 0 || stride < 0 || (nq > 0 && (!qs || !res)) ||
+      (n_src > 0 && stride > 0 && nq > 0 && !entries_dev))
+    return set_err(APEX_EINVAL, "bad merge arguments");
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    if (q.objective_task < 0 || q.objective_task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+    if (q.n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+    if (q.k < 0) return set_err(APEX_EINVAL, "k must be >= 0");
+    for (int m = 0; m < q.n_constraints; ++m)
+      if (q.constraints[m].task < 0 || q.constraints[m].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
   }
-  if (c->slots.empty()) c->slots.resize(1);
-  Slot& S = c->slots[0];
-  const int64_t cap = std::max<int64_t>(n_entries, 1024);
-  APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
-  APEX_TRY(S.comp.ensure(sizeof(Entry)));
-  APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
-  APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
-  APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
-  APEX_TRY(c->d_hists.ensure(kHistWords * sizeof(unsigned)));
-  APEX_TRY(S.ctl.ensure(sizeof(QCtl)));
-  c->out_off.assign(2, 0);
-  c->out_off[1] = (out_bytes(k, q->n_constraints) + 15) / 16 * 16;
-  APEX_TRY(c->d_out.ensure(c->out_off[1]));
-  APEX_TRY(c->d_queries.ensure(sizeof(ScanQuery)));
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const int64_t n_in = (int64_t)n_src * stride;
+  bool any = false;
+  for (int i = 0; i < nq; ++i) {
+    res[i].scanned = total_scanned;
+    if (qs[i].k == 0 || n_in == 0) {
+      res[i].n = 0;
+      res[i].candidates = res[i].admitted = 0;
+      res[i].full_predicate = 0;
+      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
+    } else {
+      any = true;
+    }
+  }
+  if (!any) return APEX_OK;
+  // one slot per query: candidate buffer = every gathered entry of the query
+  if ((int)c->slots.size() < nq) c->slots.resize(nq);
+  int64_t k_max = 1;
+  for (int i = 0; i < nq; ++i) {
+    Slot& S = c->slots[i];
+    const int64_t k = std::max<int64_t>(qs[i].k, 1);
+    k_max = std::max(k_max, k);
+    APEX_TRY(S.buf.ensure((size_t)std::max<int64_t>(n_in, 1024) * sizeof(Entry)));
+    APEX_TRY(S.comp.ensure(sizeof(Entry)));
+    APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
+    APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
+    APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
+  }
+  APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
+  APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
+  c->out_off.assign(nq + 1, 0);
+  for (int i = 0; i < nq; ++i)
+    c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
+  APEX_TRY(c->d_out.ensure(c->out_off[nq]));
+  const size_t qbytes = (size_t)nq * sizeof(ScanQuery);
+  APEX_TRY(c->d_queries.ensure(qbytes));
   APEX_CU(cudaEventSynchronize(c->upload_ev));
-  APEX_TRY(c->h_queries.ensure(sizeof(ScanQuery)));
+  APEX_TRY(c->h_queries.ensure(qbytes));
+  APEX_TRY(c->h_ctl.ensure((size_t)nq * sizeof(QCtl)));
   c->uploaded.clear();
   c->batch.pending = false;
-  ScanQuery& Q = *c->h_queries.as<ScanQuery>();
-  std::memset(&Q, 0, sizeof(Q));
-  Q.buf = S.buf.as<Entry>();
-  Q.comp = S.comp.as<Entry>();
-  Q.sel = S.sel.as<Entry>();
-  Q.sorted = S.sorted.as<Entry>();
-  Q.rank = S.rank.as<unsigned>();
-  Q.hist = c->d_hists.as<unsigned>();
-  Q.coarse = Q.hist + kHistBins;
-  Q.seed_hist = Q.coarse + 256;
-  Q.ctl = S.ctl.as<QCtl>();
-  Q.cap = (unsigned long long)cap;
-  Q.refresh_shift = 62;
-  Q.k = k;
-  Q.maximize = q->maximize ? 1 : 0;
-  Q.obj_task = q->objective_task;
-  Q.n_cons = q->n_constraints;
-  for (int m = 0; m < q->n_constraints; ++m) Q.cons_task[m] = q->constraints[m].task;
-  unsigned char* o = c->d_out.as<unsigned char>();
-  Q.out_g = reinterpret_cast<unsigned long long*>(o);
-  Q.out_obj = reinterpret_cast<double*>(o + 8 * k);
-  Q.out_cons = reinterpret_cast<double*>(o + 16 * k);
-  Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q->n_constraints) * k);
-  Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q->n_constraints) * k);
+  ScanQuery* hq = c->h_queries.as<ScanQuery>();
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    Slot& S = c->slots[i];
+    ScanQuery& Q = hq[i];
+    std::memset(&Q, 0, sizeof(Q));
+    const int64_t kk = std::max<int64_t>(q.k, 1);
+    Q.buf = S.buf.as<Entry>();
+    Q.comp = S.comp.as<Entry>();
+    Q.sel = S.sel.as<Entry>();
+    Q.sorted = S.sorted.as<Entry>();
+    Q.rank = S.rank.as<unsigned>();
+    Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
+    Q.coarse = Q.hist + kHistBins;
+    Q.seed_hist = Q.coarse + 256;
+    Q.ctl = c->d_ctls.as<QCtl>() + i;
+    Q.cap = S.buf.bytes / sizeof(Entry);
+    Q.refresh_shift = 62;
+    Q.k = std::max<int64_t>(q.k, 1);  // k == 0 queries are reported empty below
+    Q.maximize = q.maximize ? 1 : 0;
+    Q.obj_task = q.objective_task;
+    Q.n_cons = q.n_constraints;
+    for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
+    unsigned char* o = c->d_out.as<unsigned char>() + c->out_off[i];
+    Q.out_g = reinterpret_cast<unsigned long long*>(o);
+    Q.out_obj = reinterpret_cast<double*>(o + 8 * kk);
+    Q.out_cons = reinterpret_cast<double*>(o + 16 * kk);
+    Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
+    Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
+  }
   cudaStream_t s = c->stream;
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  RunStats st;
   APEX_CU(cudaEventRecord(c->ev[0], s));
-  APEX_CU(cudaMemcpyAsync(c->d_queries.p, &Q, sizeof(ScanQuery), cudaMemcpyHostToDevice, s));
+  APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
-  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<1, 1024, 0, s>>>(dq, nullptr, 0u);
-  merge_load_kernel<<<(unsigned)std::min<int64_t>((n_entries + 255) / 256, c->sm_count * 4), 256, 0, s>>>(
-      dq, reinterpret_cast<const Entry*>(entries_dev), (unsigned long long)n_entries);
-  {
-    void* args[] = {(void*)&dq};
-    APEX_CU(cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, c->sm_count)), 1),
-                                        dim3(kSelectThreads), args, 0, s));
+  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u);
+  if (n_in > 0) {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_in + 255) / 256, 4 * c->sm_count / std::max(nq, 1) + 1));
+    merge_load_kernel<<<dim3(gx, nq), 256, 0, s>>>(dq, reinterpret_cast<const Entry*>(entries_dev), n_src, nq,
+                                                    (unsigned long long)stride);
   }
-  const int ib = (int)((k + 255) / 256);
-  const int js = std::max(1, std::min(ib, (2 * c->sm_count + ib - 1) / ib));
-  rank_kernel<<<dim3(ib, js, 1), 256, 0, s>>>(dq, js);
-  scatter_kernel<<<dim3(ib, 1), 256, 0, s>>>(dq);
-  MatLaunch M;
-  M.queries = dq;
-  M.rx = c->d_rx.as<DevReaction>();
-  M.g_off = c->d_goff.as<unsigned long long>();
-  M.n_rx = (int)c->rx.size();
-  M.values = c->d_values.as<float>();
-  M.n_pairs = c->n_pairs;
-  M.biases = c->d_biases.as<double>();
-  materialize_kernel<<<dim3((unsigned)((k + 127) / 128), 1), 128, 0, s>>>(M);
+  st.launches = 2;
+  // bound_key = 0 (init): every loaded entry is a candidate
+  APEX_TRY(enqueue_select(c, dq, nq, k_max, true, st, s, false));
   APEX_CU(cudaGetLastError());
-  APEX_TRY(c->h_ctl.ensure(sizeof(QCtl)));
-  APEX_CU(cudaMemcpyAsync(c->h_ctl.p, S.ctl.p, sizeof(QCtl), cudaMemcpyDeviceToHost, s));
+  APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
+                            cudaMemcpyDeviceToHost, s));
   APEX_CU(cudaEventRecord(c->ev[1], s));
-  apex_query_spec qq = *q;
-  qq.start = 0;
-  qq.end = total_scanned;
-  APEX_TRY(copy_results(c, &qq, 1, res, nullptr));
+  std::vector<apex_query_spec> qq(qs, qs + nq);
+  for (auto& x : qq) {
+    x.start = 0;
+    x.end = total_scanned;
+  }
+  APEX_TRY(copy_results(c, qq.data(), nq, res, nullptr));
+  for (int i = 0; i < nq; ++i)
+    if (qs[i].k == 0 || n_in == 0) {
+      res[i].n = 0;
+      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
+    }
   if (stats) {
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     stats->select_ms = ms;
     stats->total_ms = ms;
-    stats->kernel_launches = 6;
+    stats->kernel_launches = st.launches;
+    stats->d2h_bytes = (int64_t)c->out_off[nq];
   }
   return APEX_OK;
+}
+
+int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry* entries_dev, int64_t n_entries,
+                        uint64_t total_scanned, apex_result* res, apex_stats* stats) {
+  if (!q || !res || n_entries < 0 || (n_entries > 0 && !entries_dev)) return set_err(APEX_EINVAL, "bad merge arguments");
+  return apex_merge_finalize_batch(c, q, 1, entries_dev, 1, n_entries, total_scanned, res, stats);
 }
 
 int apex_set_option(apex_ctx* c, const char* name, int64_t v) {

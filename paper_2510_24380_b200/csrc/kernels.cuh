@@ -932,6 +932,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
   // block dense-row queue: kBlockDq items, then [head, tail]
   DenseItem* sdq = reinterpret_cast<DenseItem*>(bars_all + kScanWarps * 2);
   unsigned* sdq_ctr = reinterpret_cast<unsigned*>(sdq + kBlockDq);
+  // per-row constraint thresholds of the rare path, [r][test][lane] per warp:
+  // lane-major (conflict-free for the owner) and readable by any lane of the
+  // warp (the pair rounds read the pair's row directly)
+  float* sthr = reinterpret_cast<float*>(sdq_ctr + 4) + (size_t)warp * RL * kMaxTests * 32;
   if (threadIdx.x == 0) {
     sdq_ctr[0] = 0u;
     sdq_ctr[1] = 0u;
@@ -1016,7 +1020,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
     unsigned long long tau_seen = tau;
 
     float thr[RL];
-    float thrc[RL][kMaxTests];  // constraint thresholds (rare path, local memory)
     bool thr_ready = false;
     // dense rows (dense_min admitted products so far in this tile): taken out
     // of the column-group vote and finished row-parallel after the tile
@@ -1138,7 +1141,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
                 const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
                 double p = c > 1 ? (double)__ldg(v + pr[r][0]) : 0.0;
                 for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[r][j]));
-                thrc[r][i] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
+                sthr[(r * kMaxTests + i) * 32 + lane] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
                                              : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
               }
             if (TRACE) cyc_thr += clock64() - c_t0;
@@ -1213,11 +1216,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
             const unsigned row = pv >> 4, jj = pv & 15u, src = row & 31u;
             bool pass = valid;
             for (int i = 1; i < nt; ++i) {
-              float t = __shfl_sync(0xffffffffu, thrc[0][i], src);
-              if (RL == 2) {
-                const float t1 = __shfl_sync(0xffffffffu, thrc[RL - 1][i], src);
-                if (row >= 32u) t = t1;
-              }
+              const float t = sthr[((row >> 5) * kMaxTests + i) * 32 + src];
               pass = pass && (sm_f[xo + ((i - 1) << 4) + jj] <= t);
             }
             double po = __shfl_sync(0xffffffffu, p_obj[0], src);
@@ -1294,7 +1293,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
             it->from = dense_from[r];
             it->ncols = (int)ncols;
             it->q = (int)q_cur;
-            for (int i = 1; i < nt; ++i) it->thrc[i] = thrc[r][i];
+            for (int i = 1; i < nt; ++i) it->thrc[i] = sthr[(r * kMaxTests + i) * 32 + lane];
             __threadfence_block();
             *(volatile unsigned*)&it->ready = 1u;
           }
@@ -1319,8 +1318,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
               const int src = __ffs(dm) - 1;
               dm &= dm - 1u;
               for (int i = 1; i < nt; ++i) {
-                const float tv = __shfl_sync(0xffffffffu, thrc[r][i], src);
-                if (lane == 0) scratch[i] = tv;
+                if (lane == 0) scratch[i] = sthr[(r * kMaxTests + i) * 32 + src];
               }
               const float to = __shfl_sync(0xffffffffu, thr[r], src);
               const double po = __shfl_sync(0xffffffffu, p_obj[r], src);
@@ -2300,19 +2298,26 @@ __global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restric
 }
 
 // Multi-GPU: load gathered entries (skip padding g == ~0) as the compacted set.
-__global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry* __restrict__ in,
-                                  unsigned long long n) {
-  const ScanQuery& Q = qs[0];
+// Multi-GPU: load the gathered entries of query blockIdx.y (skipping padding
+// g == ~0) as its candidate set.  Layout: in[(src * nq + q) * stride + i],
+// i < stride, for src < n_src (what an all-gather of per-rank [nq][stride]
+// buffers produces).
+__global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry* __restrict__ in, int n_src,
+                                  int nq, unsigned long long stride) {
+  const int q = blockIdx.y;
+  const ScanQuery& Q = qs[q];
   QCtl* ctl = Q.ctl;
   const unsigned lane = lane_id();
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long n = (unsigned long long)n_src * stride;
+  const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
-       base += stride) {
+       base += gstride) {
     const unsigned long long i = base + lane;
     Entry e;
     bool keep = false;
     if (i < n) {
-      e = in[i];
+      const unsigned long long src = i / stride, j = i - src * stride;
+      e = in[(src * (unsigned long long)nq + (unsigned long long)q) * stride + j];
       keep = e.g != ~0ull;
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);

@@ -3,8 +3,9 @@
 The product index space [start, end) is cut into contiguous g ranges, one per
 rank; every rank computes its exact local top-min(k, feasible) on its GPU
 (apex_query_local), the per-rank (key, g) entries (16 B each, padded to k) are
-all-gathered with NCCL over NVLink, and every rank runs the exact merge kernel
-(apex_merge_finalize) on the gathered buffer.  Exactness: the global top-k is
+all-gathered with NCCL over NVLink, and every rank runs the exact merge
+(apex_merge_finalize / apex_merge_finalize_batch: one device pass for a whole
+batch) on the gathered buffer.  Exactness: the global top-k is
 contained in the union of the local top-k's, and the (key, g) order is global.
 """
 
@@ -36,8 +37,11 @@ def all_gather_entries(local, group=None):
 
     world = dist.get_world_size(group)
     out = torch.empty((world * local.shape[0], 2), dtype=local.dtype, device=local.device)
-    if local.is_cuda:
+    if local.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    elif local.is_cuda:
+        # non-NCCL group (tests): gather through host memory
+        return all_gather_entries(local.cpu(), group).to(local.device)
     else:
         parts = [torch.empty_like(local) for _ in range(world)]
         dist.all_gather(parts, local.contiguous(), group=group)
@@ -61,3 +65,23 @@ def sharded_query(ctx, query: dict, group=None, stream_sync=True):
     torch.cuda.current_stream().synchronize()
     res, st_merge = ctx.merge_finalize(query, gathered.data_ptr(), gathered.shape[0], query["end"] - query["start"])
     return res, {"local": st_local, "merge": st_merge, "local_count": counts[0]}
+
+
+def sharded_batch(ctx, queries: list[dict], group=None, prepared=None):
+    """A batch of native queries sharing one global range [start, end): every
+    rank scans its shard for all of them (one apex_query_local), ONE all-gather
+    of the [n_queries][k] entry buffers, and one batched exact merge."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    start, end = queries[0]["start"], queries[0]["end"]
+    if any(q["start"] != start or q["end"] != end for q in queries):
+        raise ValueError("sharded_batch: all queries must share one index range")
+    k = max(max(int(q["k"]) for q in queries), 1)
+    a, b = shard_range(start, end, rank, world)
+    local = torch.full((len(queries) * k, 2), PAD, dtype=torch.int64, device="cuda")
+    counts, st_local = ctx.query_local([dict(q, start=a, end=b) for q in queries], local.data_ptr())
+    gathered = all_gather_entries(local, group)
+    res, st_merge = ctx.merge_finalize_batch(queries, gathered.data_ptr(), world, k, end - start, prepared)
+    return res, {"local": st_local, "merge": st_merge, "local_counts": counts}

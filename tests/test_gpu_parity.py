@@ -267,6 +267,40 @@ def test_local_plus_merge_equals_global(native):
                                                                      full[0]["scanned"])
 
 
+@pytest.mark.parametrize("k", [1, 50, 3000])
+def test_local_plus_batched_merge_equals_global(native, k):
+    """Batched multi-GPU protocol on one device: every shard runs the whole
+    batch locally (apex_query_local), the [shard][query][k] buffers are
+    stacked as an all-gather would, and ONE apex_merge_finalize_batch equals
+    the global batch query for every query (k up to well past the small-sort
+    path, and k exceeding some queries' feasible counts)."""
+    import torch
+
+    from paper_2510_24380_b200.dist import PAD, shard_range
+
+    sizes, pair_off, n_pairs, values, biases, rng = _random_case(12, n_rx=12, mu=3.5)
+    ctx, lib = _ctx(native, sizes, pair_off, n_pairs, values, biases)
+    qs = [{"obj": 1, "maximize": False, "cons": [(0, -3.0, 3.0), (2, -np.inf, 2.0)], "k": k},
+          {"obj": 2, "maximize": True, "cons": [], "k": k},
+          {"obj": 0, "maximize": False, "cons": [(1, -0.5, 0.5), (2, -0.5, 0.5), (3, -0.5, 0.5)], "k": k},
+          {"obj": 3, "maximize": True, "cons": [(1, -1.0, np.inf)], "k": k}]
+    qs = [dict(q, start=0, end=lib.total) for q in qs]
+    full, _ = ctx.query(qs)
+    world, nq = 3, len(qs)
+    buf = torch.full((world * nq * k, 2), PAD, dtype=torch.int64, device="cuda")
+    for r in range(world):
+        a, b = shard_range(0, lib.total, r, world)
+        part = buf[r * nq * k:(r + 1) * nq * k]
+        ctx.query_local([dict(q, start=a, end=b) for q in qs], part.data_ptr())
+        torch.cuda.synchronize()
+    merged, _ = ctx.merge_finalize_batch(qs, buf.data_ptr(), world, k, lib.total)
+    for qi in range(nq):
+        for key in ("g", "objective", "constraint_values", "reaction", "digits"):
+            assert np.array_equal(merged[qi][key], full[qi][key]), (qi, key)
+        assert (merged[qi]["n"], merged[qi]["discarded"], merged[qi]["scanned"]) == (
+            full[qi]["n"], full[qi]["discarded"], full[qi]["scanned"])
+
+
 def test_c1_shape_vs_oracle(native):
     """Config-1 shape (10M products, random-init heads, calibrated properties)
     against the oracle for the config-1 query and one preset query."""
