@@ -548,7 +548,11 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   for (int i = 0; i < nq; ++i) {
     Slot& S = c->slots[i];
     const int64_t k = qs[i].k;
-    const int64_t cap = std::max<int64_t>(c->opt_cap, 8 * k + 1024);
+    // candidate buffer: opt_cap entries, shared out over large batches (an
+    // overflow is detected and re-run exactly, so this only trades memory
+    // for the rare re-run)
+    const int64_t cap = std::max<int64_t>(std::min<int64_t>(c->opt_cap, (int64_t)(1ll << 27) / std::max(nq, 1)),
+                                          16 * k + 4096);
     if (c->opt_mode >= 2) APEX_TRY(S.obj_col.ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
     if (c->opt_mode != 2) {
       const int ntp_i = (kernel_nt(B.tests[i].nt) + 3) / 4 * 4;

@@ -21,7 +21,7 @@ from paper_2510_24380_b200 import _native, synth  # noqa: E402
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
     variants = [dict(kv.split("=") for kv in a.split(",")) if a != "-" else {} for a in sys.argv[2:]] or [{}]
-    base = "c1" if cfg == "c2" else cfg
+    base = "c1" if cfg in ("c2", "c5") else cfg
     shape = synth.make_shape(synth.SHAPES[base])
     u = synth.random_cache(shape.n_pairs, seed=1)
     w, b = synth.random_heads(seed=1)
@@ -30,7 +30,7 @@ def main():
     ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
     ctx.load_cache(u, w, b, want_values=False)
     qs = {"c1": [synth.c1_query()], "c2": synth.c2_queries(), "c3": [synth.c3_query()],
-          "c4": [synth.c4_query()]}[cfg]
+          "c4": [synth.c4_query()], "c5": synth.c5_queries()}[cfg]
     nq = [synth.to_native(q, 0, shape.total) for q in qs]
     for v in variants:
         for k_, val in v.items():
