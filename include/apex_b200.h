@@ -109,6 +109,8 @@ typedef struct {
   int64_t h2d_bytes;       /* host->device bytes copied by the call */
   int64_t d2h_bytes;       /* device->host bytes copied by the call */
   int64_t admitted;        /* products that passed the admission test (admission-first kernel) */
+  double host_prepare_us;  /* host time of descriptor checks / staging in the call */
+  double host_launch_us;   /* host time of the launches (graph replay or direct) */
 } apex_stats;
 
 /* Caller-allocated host output for one query; arrays sized for k entries

@@ -88,6 +88,8 @@ class Stats(C.Structure):
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
         ("admitted", C.c_int64),
+        ("host_prepare_us", C.c_double),
+        ("host_launch_us", C.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -329,6 +331,13 @@ class DeviceContext:
         st = Stats()
         _check(self.lib.apex_query(self._ctx, pb.specs, len(pb.queries), pb.results, C.byref(st)))
         return self._unpack(pb.results, pb.bufs), st.as_dict()
+
+    def run_async(self, pb: "PreparedBatch") -> dict:
+        """apex_query_async on a prepared batch (descriptors built once)."""
+        st = Stats()
+        _check(self.lib.apex_query_async(self._ctx, pb.specs, len(pb.queries), C.byref(st)))
+        self._inflight = pb.queries
+        return st.as_dict()
 
     def query_async(self, queries: list[dict]) -> dict:
         """Enqueue a batch (one shared range, k >= 1) without a host sync."""

@@ -14,6 +14,7 @@
 // A candidate-buffer overflow is detected (count > cap) and the query is re-run
 // with the final (valid) bound as its starting threshold.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -1443,13 +1444,18 @@ int apex_query_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_st
     if (qs[i].k < 1 || qs[i].end == qs[i].start)
       return set_err(APEX_EINVAL, "apex_query_async: k >= 1 and a non-empty range required (use apex_query)");
   }
+  const auto t0 = std::chrono::steady_clock::now();
   APEX_TRY(prepare_batch(c, qs, nq, true));
+  const auto t1 = std::chrono::steady_clock::now();
   APEX_TRY(launch_batch(c));
+  const auto t2 = std::chrono::steady_clock::now();
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     stats->kernel_launches = c->batch.st.launches;
     stats->scan_launches = c->batch.st.scans;
     stats->h2d_bytes = c->batch.st.h2d_bytes;
+    stats->host_prepare_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+    stats->host_launch_us = std::chrono::duration<double, std::micro>(t2 - t1).count();
   }
   return APEX_OK;
 }
