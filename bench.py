@@ -359,7 +359,9 @@ def main():
 
     # e2e: public C-ABI call with host buffers, descriptors H2D every step
     ctx.set_option("force_upload", 1)
-    prepared = ctx.prepare(nqueries) if world == 1 else None  # caller-owned host result buffers, reused
+    # results returned as views into the library's pinned host block (D2H in
+    # the same device pass, no host-side copy): the C-ABI view mode
+    prepared = ctx.prepare_views(nqueries) if world == 1 else None
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     scan_ms, h2d, d2h = [], 0, 0
     for i in range(args.steps):
@@ -367,7 +369,7 @@ def main():
         e2e_ev[i][0].record(stream)
         t0 = time.perf_counter()
         if world == 1:
-            res, st = ctx.run(prepared)
+            res, st = ctx.run_views(prepared)
             scan_ms.append(st["scan_kernel_ms"])
             h2d += st["h2d_bytes"]
             d2h += st["d2h_bytes"]

@@ -114,7 +114,11 @@ typedef struct {
 } apex_stats;
 
 /* Caller-allocated host output for one query; arrays sized for k entries
- * (constraint_values: k * n_constraints, digits: k * APEX_MAX_RGROUPS). */
+ * (constraint_values: k * n_constraints, digits: k * APEX_MAX_RGROUPS).
+ * View mode: if all five array pointers are NULL, apex_query / _fetch set
+ * them to the rows in the context's pinned host block instead of copying
+ * (valid until the next call on the context; all queries of the call must
+ * share one range). */
 typedef struct {
   uint64_t* global_index;
   double* objective;          /* value in the user's direction (engine.py:254) */

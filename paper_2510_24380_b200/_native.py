@@ -325,6 +325,47 @@ class DeviceContext:
                 a.fill(0)
         return PreparedBatch(queries, specs, keep, results, bufs)
 
+    def prepare_views(self, queries: list[dict]) -> "PreparedBatch":
+        """Descriptors built once; results come back as views into the
+        context's pinned host block (no host copy; valid until the next call)."""
+        specs, keep = self._specs(queries)
+        return PreparedBatch(queries, specs, keep, None, None)
+
+    def run_views(self, pb: "PreparedBatch") -> tuple[list[dict], dict]:
+        results = (ResultC * len(pb.queries))()  # all arrays NULL: view mode
+        st = Stats()
+        _check(self.lib.apex_query(self._ctx, pb.specs, len(pb.queries), results, C.byref(st)))
+        # one numpy view over the pinned block, sliced per query
+        addr = [C.cast(results[i].global_index, C.c_void_p).value or 0 for i in range(len(pb.queries))]
+        base = min(a for a in addr if a) if any(addr) else 0
+        end = 0
+        for i, q in enumerate(pb.queries):
+            if addr[i]:
+                kk = max(int(q["k"]), 1)
+                end = max(end, addr[i] + kk * (8 + 8 + 8 * len(q.get("cons", [])) + 4 + 4 * MAX_RGROUPS))
+        block = np.frombuffer((C.c_uint8 * (end - base)).from_address(base), dtype=np.uint8) if base else None
+        out = []
+        u64, f64, i32 = np.uint64, np.float64, np.int32
+        for i, q in enumerate(pb.queries):
+            r = results[i]
+            n, m = r.n, len(q.get("cons", []))
+            kk = max(int(q["k"]), 1)
+            o = addr[i] - base
+            if n and block is not None and addr[i]:
+                cv = (np.frombuffer(block, f64, n * m, o + 16 * kk).reshape(n, m) if m
+                      else np.empty((n, 0), f64))
+                d = {"g": np.frombuffer(block, u64, n, o), "objective": np.frombuffer(block, f64, n, o + 8 * kk),
+                     "constraint_values": cv, "reaction": np.frombuffer(block, i32, n, o + (16 + 8 * m) * kk),
+                     "digits": np.frombuffer(block, i32, n * MAX_RGROUPS,
+                                             o + (20 + 8 * m) * kk).reshape(n, MAX_RGROUPS)}
+            else:
+                d = {"g": np.empty(0, u64), "objective": np.empty(0, f64), "constraint_values": np.empty((0, m), f64),
+                     "reaction": np.empty(0, i32), "digits": np.empty((0, MAX_RGROUPS), i32)}
+            d.update(n=n, discarded=r.discarded, scanned=r.scanned, candidates=r.candidates, admitted=r.admitted,
+                     full_predicate=r.full_predicate)
+            out.append(d)
+        return out, st.as_dict()
+
     def run(self, pb: "PreparedBatch") -> tuple[list[dict], dict]:
         """apex_query on a prepared batch; the returned arrays are views of the
         batch's buffers (overwritten by the next run of the same batch)."""

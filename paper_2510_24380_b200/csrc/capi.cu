@@ -154,6 +154,7 @@ struct Batch {
   int nq = 0, NT = 0, rl = 0, ntp = 0;
   int64_t k_max = 0;
   bool finalize = false;
+  bool copy_out = false;       // result rows D2H inside the pass (synchronous apex_query)
   Plan* plan = nullptr;
   bool pending = false;
   RunStats st;
@@ -192,6 +193,7 @@ struct apex_ctx {
   DBuf d_queries, d_tau0;
   DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
   DBuf d_ctls;                           // per-query control blocks, contiguous (one strided D2H of the headers)
+  bool copy_next = false;                // next prepare_batch: result D2H inside the pass
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
@@ -535,6 +537,8 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   const apex_query_spec* qs = B.qs.data();
   B.nq = nq;
   B.finalize = finalize;
+  B.copy_out = finalize && c->copy_next;
+  c->copy_next = false;
   B.st = RunStats();
   B.k_max = 0;
   for (int i = 0; i < nq; ++i) B.k_max = std::max<int64_t>(B.k_max, qs[i].k);
@@ -570,6 +574,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   for (int i = 0; i < nq; ++i)
     c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
   APEX_TRY(c->d_out.ensure(c->out_off[nq]));
+  if (finalize) APEX_TRY(c->h_out.ensure(c->out_off[nq]));
   // everything enqueue_batch touches is allocated here (no allocation may
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
@@ -1007,6 +1012,11 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
                             cudaMemcpyDeviceToHost, s));
   st.d2h_bytes += nq * (int64_t)offsetof(QCtl, hist);
+  if (B.copy_out) {
+    // result rows to pinned host memory in the same pass (one host sync per
+    // call; an overflow re-run copies again)
+    APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, c->out_off[nq], cudaMemcpyDeviceToHost, s));
+  }
   B.pending = true;
   return APEX_OK;
 }
@@ -1072,6 +1082,7 @@ uint64_t batch_key(const apex_ctx* c) {
   const Batch& B = c->batch;
   mix(&B.nq, sizeof(B.nq));
   mix(&B.finalize, sizeof(B.finalize));
+  mix(&B.copy_out, sizeof(B.copy_out));
   for (int i = 0; i < B.nq; ++i) {
     const apex_query_spec& q = B.qs[i];
     mix(&q.objective_task, sizeof(q.objective_task));
@@ -1166,7 +1177,8 @@ void fill_stats(apex_stats* stats, const RunStats& st, float d2h, float total, i
 }
 
 // Copy materialized rows of slot i to the caller's result.
-int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* res_caller, const int* perm) {
+int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* res_caller, const int* perm,
+                 bool copied = false) {
   std::vector<apex_result> res_sorted(nq);
   for (int i = 0; i < nq; ++i) res_sorted[i] = res_caller[perm ? perm[i] : i];
   apex_result* res = res_sorted.data();
@@ -1174,9 +1186,11 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
   // the retained rows into the caller's arrays
   const std::vector<size_t>& offs = c->out_off;
   const size_t total = offs[nq];
-  APEX_TRY(c->h_out.ensure(total));
-  APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, total, cudaMemcpyDeviceToHost, c->stream));
-  APEX_CU(cudaStreamSynchronize(c->stream));
+  if (!copied) {
+    APEX_TRY(c->h_out.ensure(total));
+    APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, total, cudaMemcpyDeviceToHost, c->stream));
+    APEX_CU(cudaStreamSynchronize(c->stream));
+  }
   for (int i = 0; i < nq; ++i) {
     const apex_query_spec& q = qs[i];
     apex_result& r = res[i];
@@ -1197,8 +1211,16 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
     r.n = n;
     r.scanned = span;
     r.discarded = (int64_t)std::min<uint64_t>((uint64_t)q.k, span) - n;
-    if (n > 0) {
-      const unsigned char* o = c->h_out.as<unsigned char>() + offs[i];
+    unsigned char* o = c->h_out.as<unsigned char>() + offs[i];
+    if (!r.global_index && !r.objective && !r.constraint_values && !r.reaction && !r.digits) {
+      // view mode: point at the rows in the context's pinned host block
+      // (valid until the next call on this context)
+      r.global_index = reinterpret_cast<uint64_t*>(o);
+      r.objective = reinterpret_cast<double*>(o + 8 * kk);
+      r.constraint_values = reinterpret_cast<double*>(o + 16 * kk);
+      r.reaction = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)m) * kk);
+      r.digits = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)m) * kk);
+    } else if (n > 0) {
       if (r.global_index) std::memcpy(r.global_index, o, 8 * n);
       if (r.objective) std::memcpy(r.objective, o + 8 * kk, 8 * n);
       if (r.constraint_values && m) std::memcpy(r.constraint_values, o + 16 * kk, 8 * (size_t)m * n);
@@ -1467,7 +1489,7 @@ int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
   if (!res) return set_err(APEX_EINVAL, "null results");
   APEX_TRY(check_batch(c));
   APEX_CU(cudaEventRecord(c->ev[6], c->stream));
-  APEX_TRY(copy_results(c, B.qs.data(), B.nq, res, B.perm.data()));
+  APEX_TRY(copy_results(c, B.qs.data(), B.nq, res, B.perm.data(), B.copy_out));
   APEX_CU(cudaEventRecord(c->ev[7], c->stream));
   APEX_CU(cudaEventSynchronize(c->ev[7]));
   float d2h = 0;
@@ -1499,6 +1521,16 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
   });
   apex_stats agg;
   std::memset(&agg, 0, sizeof(agg));
+  {
+    bool view = false, multi_range = false;
+    for (int i = 0; i < nq; ++i) {
+      const apex_result& r = res[i];
+      view = view || (!r.global_index && !r.objective && !r.constraint_values && !r.reaction && !r.digits);
+      multi_range = multi_range || qs[i].start != qs[0].start || qs[i].end != qs[0].end;
+    }
+    if (view && multi_range)
+      return set_err(APEX_EINVAL, "result views (null output arrays) need all queries of the call to share one range");
+  }
   size_t g0 = 0;
   while (g0 < order.size()) {
     size_t g1 = g0 + 1;
@@ -1521,7 +1553,10 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
     }
     if (!grp.empty()) {
       apex_stats st;
-      APEX_TRY(apex_query_async(c, grp.data(), (int)grp.size(), nullptr));
+      c->copy_next = true;  // the rows go to the host right away: copy them inside the pass
+      const int rq = apex_query_async(c, grp.data(), (int)grp.size(), nullptr);
+      c->copy_next = false;
+      if (rq != APEX_OK) return rq;
       std::vector<apex_result> tmp(grp.size());
       for (size_t i = 0; i < grp.size(); ++i) tmp[i] = res[live[i]];
       APEX_TRY(apex_query_fetch(c, tmp.data(), &st));

@@ -301,6 +301,27 @@ def test_local_plus_batched_merge_equals_global(native, k):
             full[qi]["n"], full[qi]["discarded"], full[qi]["scanned"])
 
 
+def test_result_views_equal_copies(native):
+    """View mode (null output arrays: rows returned as views into the
+    context's pinned block) equals the copying call, query by query."""
+    sizes, pair_off, n_pairs, values, biases, rng = _random_case(13, n_rx=9, mu=3.5)
+    ctx, lib = _ctx(native, sizes, pair_off, n_pairs, values, biases)
+    qs = [{"obj": 1, "maximize": False, "cons": [(0, -3.0, 3.0)], "k": 200},
+          {"obj": 2, "maximize": True, "cons": [], "k": 7},
+          {"obj": 0, "maximize": False, "cons": [(1, -0.5, 0.5), (2, -0.5, 0.5)], "k": 50}]
+    qs = [dict(q, start=3, end=lib.total - 5) for q in qs]
+    ref, _ = ctx.query(qs)
+    pb = ctx.prepare_views(qs)
+    for _ in range(2):
+        got, _ = ctx.run_views(pb)
+        for a, b in zip(got, ref):
+            for key in ("g", "objective", "constraint_values", "reaction", "digits"):
+                assert np.array_equal(a[key], b[key]), key
+            assert (a["n"], a["discarded"], a["scanned"]) == (b["n"], b["discarded"], b["scanned"])
+    with pytest.raises(native.NativeError):
+        ctx.run_views(ctx.prepare_views([qs[0], dict(qs[1], start=0)]))
+
+
 def test_c1_shape_vs_oracle(native):
     """Config-1 shape (10M products, random-init heads, calibrated properties)
     against the oracle for the config-1 query and one preset query."""

@@ -38,3 +38,12 @@ for _ in range(20):
     t0 = time.perf_counter(); s2 = ctx.run_async(pb); t1 = time.perf_counter(); ts.append(t1 - t0)
     ctx.query_fetch()
 print("run_async (prepared) host us: median", sorted(ts)[10] * 1e6, s2["host_prepare_us"], s2["host_launch_us"])
+
+for name, fn, arg in (("run (copy)", ctx.run, ctx.prepare(nq)), ("run_views", ctx.run_views, ctx.prepare_views(nq))):
+    for _ in range(3):
+        fn(arg)
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter(); r, st = fn(arg); ts.append(time.perf_counter() - t0)
+    print(name, "wall us median", sorted(ts)[10] * 1e6, "prep", st["host_prepare_us"], "launch", st["host_launch_us"],
+          "d2h_ms", st["d2h_ms"], "total_ms", st["total_ms"])
