@@ -177,7 +177,7 @@ def _random_case(seed, n_rx=6, mu=3.0, sigma=0.7, n_tasks=4, c3=0.5, max_c=3):
                                   {"mode": 0, "chunk_min": 1000, "tile_products": 64},
                                   {"chunk_min": 1000, "tile_products": 64, "cb_admit": 64},
                                   {"cap": 1024, "samples": 16}, {"refresh": 256, "samples": 64}, {"multi": 1}, {"graph": 0},
-                                  {"mode": 2, "dense": 1}, {"mode": 2, "dense": 5, "rl": 2}, {"mode": 2, "dense": 3}, {"mode": 2, "dense": 1, "rl": 2, "tile_products": 8192},
+                                  {"mode": 2, "dense": 1}, {"mode": 2, "dense": 5, "rl": 2}, {"mode": 2, "dense": 3}, {"mode": 2, "dense": 1, "rl": 2, "tile_products": 8192}, {"mode": 2, "dense": 2},
                                   {"mode": 2, "dense": 0}])
 def test_random_libraries_vs_oracle(native, seed, opts):
     from oracle import scan_oracle as orc
@@ -207,6 +207,35 @@ def test_random_libraries_vs_oracle(native, seed, opts):
                         for q, a, b in qs])
     for r, (q, a, b) in zip(res, qs):
         _check_against_oracle(r, values, biases, lib, q, a, b)
+    ctx.close()
+
+
+@pytest.mark.parametrize("opts", [{}, {"dense": 1}, {"dense": 3}, {"cb_admit": 64}, {"mode": 2}])
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_shared_objective_batches_vs_oracle(native, seed, opts):
+    """Batches whose queries share objective columns (same task and
+    direction, different constraints and k) against the oracle, query by
+    query."""
+    from oracle import scan_oracle as orc
+
+    sizes, pair_off, n_pairs, values, biases, rng = _random_case(seed)
+    ctx, lib = _ctx(native, sizes, pair_off, n_pairs, values, biases, **opts)
+    qs = []
+    for obj in (0, 2):
+        for maximize in (False, True):
+            for ci in range(3):
+                cons = []
+                for t in rng.choice(4, size=int(rng.integers(0, 4)), replace=False):
+                    v = values[t]
+                    lo = float(np.quantile(v, rng.uniform(0, 0.3)) * 2) if rng.random() < 0.5 else -np.inf
+                    hi = float(np.quantile(v, rng.uniform(0.7, 1.0)) * 2) if rng.random() < 0.7 else np.inf
+                    if lo < hi:
+                        cons.append((int(t), lo, hi))
+                qs.append(orc.Query(obj, maximize, cons, int(rng.choice([1, 20, 300, 2000]))))
+    res, _ = ctx.query([{"obj": q.obj, "maximize": q.maximize, "cons": q.cons, "k": q.k, "start": 0,
+                         "end": lib.total} for q in qs])
+    for r, q in zip(res, qs):
+        _check_against_oracle(r, values, biases, lib, q, 0, lib.total)
     ctx.close()
 
 

@@ -6,6 +6,7 @@ wall clock incl. result D2H), the batched throughput (all queries in one
 pass), and a consistency check of a sample of batched results against the
 single-query results.  Usage: python tools/c5_check.py [n_queries] [c3|c1]"""
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -24,6 +25,8 @@ from paper_2510_24380_b200 import _native, synth  # noqa: E402
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
     lib = sys.argv[2] if len(sys.argv) > 2 else "c3"
+    opts = dict(kv.split("=") for kv in sys.argv[3].split(",")) if len(sys.argv) > 3 and sys.argv[3] != "-" else {}
+    single = os.environ.get("C5_SINGLE", "1") == "1"
     shape = synth.make_shape(synth.SHAPES[lib])
     u = synth.random_cache(shape.n_pairs, seed=1)
     w, b = synth.random_heads(seed=1)
@@ -31,9 +34,11 @@ def main():
     ctx = _native.DeviceContext(0)
     ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
     ctx.load_cache(u, w, b, want_values=False)
+    for k_, v in opts.items():
+        ctx.set_option(k_, int(v))
     qs = [synth.to_native(q, 0, shape.total) for q in synth.c5_queries(n)]
     # per-query latency (each query alone, prepared host buffers)
-    pbs = [ctx.prepare([q]) for q in qs]
+    pbs = [ctx.prepare([q]) for q in qs] if single else []
     for pb in pbs[:5]:
         ctx.run(pb)
     lat, single, full, kern, cand = [], [], [], [], []
@@ -45,7 +50,7 @@ def main():
         full.append(r[0]["full_predicate"])
         kern.append(st1["scan_kernel_ms"])
         cand.append(st1["candidates"])
-    lat, full, kern = np.array(lat), np.array(full, dtype=bool), np.array(kern)
+    lat, full, kern = np.array(lat or [0.0]), np.array(full or [False], dtype=bool), np.array(kern or [0.0])
     # batched: all queries in one pass
     pb = ctx.prepare(qs)
     ctx.run(pb)
@@ -53,7 +58,7 @@ def main():
     res, st = ctx.run(pb)
     wall = time.perf_counter() - t0
     ok = all(np.array_equal(res[i]["g"], single[i][0]) and np.array_equal(res[i]["objective"], single[i][1])
-             for i in range(len(qs)))
+             for i in range(len(single)))
     print(json.dumps({
         "config": f"c5: {len(qs)} random objective/constraint queries (k in 100/1000/10000) over {shape.total} products",
         "latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
