@@ -156,6 +156,7 @@ struct Batch {
   bool finalize = false;
   bool copy_out = false;       // result rows D2H inside the pass (synchronous apex_query)
   Plan* plan = nullptr;
+  Plan* plan_rows = nullptr;    // whole-row tiles (sorted-column admission kernel)
   bool pending = false;
   RunStats st;
 };
@@ -185,6 +186,7 @@ struct apex_ctx {
   int64_t corner_slots = 0;
   unsigned long long corner_total = 0;
   bool corners_ok = false;
+  DBuf d_sorted_x, d_sorted_col;         // per task: each reaction's last R-group sorted ascending (value, column)
   int n_tasks = 0;
   int64_t n_pairs = 0;
   bool table_loaded = false;
@@ -228,6 +230,7 @@ struct apex_ctx {
   int64_t opt_cb_admit = 512;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
+  int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
@@ -260,7 +263,9 @@ int check_ctx(apex_ctx* c, bool need_table) {
 // the range ends (engine.py:182-189 clipping) become single-row tiles.  Tiles
 // are shuffled with a fixed seed so any prefix of the list is a representative
 // sample of the range (used for the first chunk's threshold).
-int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan*& out) {
+// force_cols > 0: tiles span whole rows up to that many columns (the
+// sorted-column kernel does per-row work, not per-column work)
+int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan*& out, int64_t force_cols = 0) {
   // tile size from the launch's total work (range x queries): big enough to
   // amortize the per-tile setup, small enough for ~6 tiles per warp slot
   const uint64_t span = end - start;
@@ -271,7 +276,7 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan
   int64_t cols = std::max<int64_t>(64, std::min<int64_t>(4096, target / rows));
   int64_t p2 = 64;
   while (p2 * 2 <= cols) p2 <<= 1;  // power of two (rounded down): few distinct cached plans
-  cols = p2;
+  cols = force_cols > 0 ? force_cols : p2;
   for (auto& p : c->plans) {
     if (p->start == start && p->end == end && p->rows == rows && p->cols == cols) {
       p->stamp = ++c->stamp;
@@ -339,6 +344,7 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan
                                  return a->stamp < b->stamp;
                                });
     if (c->batch.plan == it->get()) c->batch.plan = nullptr;
+    if (c->batch.plan_rows == it->get()) c->batch.plan_rows = nullptr;
     (*it)->d_tiles.release();
     c->plans.erase(it);
   }
@@ -455,8 +461,27 @@ int build_corners(apex_ctx* c) {
   }
   if (slots > INT32_MAX) return set_err(APEX_ELIMIT, "corner lists too large");
   std::vector<int32_t> lists((size_t)c->n_tasks * 2 * slots);
+  // sorted last-R-group columns (sorted-column admission kernel): per task, at
+  // every reaction's pcol_off, values ascending with their column index
+  const size_t pc = (size_t)std::max<int64_t>(c->pcols, 4);
+  std::vector<float> sx((size_t)c->n_tasks * pc, 0.0f);
+  std::vector<uint32_t> scol((size_t)c->n_tasks * pc, 0u);
   auto work = [&](int task) {
     std::vector<int32_t> idx;
+    for (int t = 0; t < n_rx; ++t) {
+      const DevReaction& R = c->rx[t];
+      const float* v = c->h_values.data() + (size_t)task * c->n_pairs + R.pair_off[R.c - 1];
+      const int64_t n = R.size[R.c - 1];
+      idx.resize(n);
+      std::iota(idx.begin(), idx.end(), 0);
+      std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b] || (v[a] == v[b] && a < b); });
+      float* ox = sx.data() + (size_t)task * pc + R.pcol_off;
+      uint32_t* oc = scol.data() + (size_t)task * pc + R.pcol_off;
+      for (int64_t i = 0; i < n; ++i) {
+        ox[i] = v[idx[i]];
+        oc[i] = (uint32_t)idx[i];
+      }
+    }
     for (int dir = 0; dir < 2; ++dir) {
       int32_t* out = lists.data() + ((size_t)task * 2 + dir) * slots;
       for (int t = 0; t < n_rx; ++t) {
@@ -488,6 +513,10 @@ int build_corners(apex_ctx* c) {
   if (!slot_off.empty()) APEX_CU(cudaMemcpy(c->d_slot_off.p, slot_off.data(), slot_off.size() * 4, cudaMemcpyHostToDevice));
   if (!m.empty()) APEX_CU(cudaMemcpy(c->d_m.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
   APEX_CU(cudaMemcpy(c->d_coff.p, coff.data(), coff.size() * 8, cudaMemcpyHostToDevice));
+  APEX_TRY(c->d_sorted_x.ensure(sx.size() * sizeof(float)));
+  APEX_TRY(c->d_sorted_col.ensure(scol.size() * sizeof(uint32_t)));
+  APEX_CU(cudaMemcpy(c->d_sorted_x.p, sx.data(), sx.size() * sizeof(float), cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(c->d_sorted_col.p, scol.data(), scol.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
   c->corner_slots = slots;
   c->corner_total = coff[n_rx];
   c->corners_ok = true;
@@ -548,6 +577,14 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   if (B.rl != 1 && B.rl != 2) B.rl = 1;
   if (c->opt_mode >= 2 && c->opt_multi) B.rl = 1;  // the multi-query kernel owns one row per lane
   APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, nq, B.plan));
+  B.plan_rows = nullptr;
+  if (c->opt_mode >= 2 && c->opt_sorted && !c->opt_multi && c->trace_cap == 0) {
+    Plan* keep = B.plan;
+    int64_t max_last = 1;
+    for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
+    APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32, nq, B.plan_rows, max_last));
+    B.plan = keep;  // still cached: build_plan never evicts the most recently used plan
+  }
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
   for (int i = 0; i < nq; ++i) {
@@ -935,6 +972,35 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         APEX_CU(cudaGetLastError());
         ++st.launches;
         ++st.scans;
+      } else if (admit && B.plan_rows && bounds.size() == 1) {
+        // sorted-column admission: whole-row tiles, one launch per 64 queries
+        const Plan* pr_ = B.plan_rows;
+        const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
+        ScanFn fn = reinterpret_cast<ScanFn>(scan_sorted_kernel);
+        int occ = 0;
+        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        SortedLaunch SL;
+        SL.sx = c->d_sorted_x.as<float>();
+        SL.scol = c->d_sorted_col.as<uint32_t>();
+        SL.pcols = std::max<int64_t>(c->pcols, 4);
+        for (int q0 = 0; q0 < nq; q0 += 64) {
+          const int nql = std::min(64, nq - q0);
+          ScanLaunch La = L;
+          La.tiles = pr_->d_tiles.as<Tile>();
+          La.tile_begin = 0;
+          La.tile_end = (unsigned)pr_->tiles.size();
+          La.queries = dq + q0;
+          La.nq = nql;
+          const int64_t items = (int64_t)pr_->tiles.size() * nql;
+          const int64_t blocks = std::max<int64_t>(
+              1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
+          const int slot = wi++ % 64;
+          La.work = c->d_work.as<unsigned>() + slot;
+          scan_sorted_kernel<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
+          APEX_CU(cudaGetLastError());
+          ++st.launches;
+          ++st.scans;
+        }
       } else if (admit) {
         const int cba = (int)c->opt_cb_admit;
         const bool tr = c->trace_cap > 0;
@@ -1096,6 +1162,8 @@ uint64_t batch_key(const apex_ctx* c) {
   }
   const void* plan = B.plan;
   mix(&plan, sizeof(plan));
+  const void* plan_rows = B.plan_rows;
+  mix(&plan_rows, sizeof(plan_rows));
   mix(&c->opt_gen, sizeof(c->opt_gen));
   mix(&g_alloc_gen, sizeof(g_alloc_gen));
   return h;
@@ -1289,7 +1357,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_goff.release();
   c->d_values.release();
   c->d_biases.release();
-  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff}) b->release();
+  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff, &c->d_sorted_x, &c->d_sorted_col}) b->release();
   c->d_queries.release();
   c->d_tau0.release();
   c->d_hists.release();
@@ -1767,6 +1835,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "corner") c->opt_corner = v;
   else if (n == "vote64") c->opt_vote64 = v;
   else if (n == "dense") c->opt_dense = v;
+  else if (n == "sorted") c->opt_sorted = v;
   else if (n == "trace") {
     // records of the admission scan's per-item trace (0: off); debug only
     c->trace_cap = std::max<int64_t>(0, std::min<int64_t>(v, 1ll << 26));

@@ -757,6 +757,23 @@ __device__ __forceinline__ float min16_shared(uint32_t addr) {
                fminf(fminf(fminf(c0, c1), fminf(c2, c3)), fminf(fminf(d0, d1), fminf(d2, d3))));
 }
 
+// Table rows of the first c-1 R-groups of enumeration row `row` (the last
+// R-group varies along the row); mixed-radix digits, least significant last.
+__device__ __forceinline__ void decode_prefix(const DevReaction& R, int c, uint64_t row, int64_t (&pr)[kMaxRg - 1]) {
+  uint64_t rem = row;
+#pragma unroll
+  for (int j = kMaxRg - 2; j >= 1; --j) {
+    pr[j] = 0;
+    if (j <= c - 2) {
+      uint64_t q, d;
+      divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+      pr[j] = R.pair_off[j] + (int64_t)d;
+      rem = q;
+    }
+  }
+  pr[0] = c > 1 ? R.pair_off[0] + (int64_t)rem : 0;
+}
+
 // Dense-row work item: the rest of one row of a tile whose objective
 // threshold admits many columns, with the row's exact thresholds; pushed by
 // the warp that found the row dense, finished by whichever warp is free.
@@ -1352,6 +1369,189 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
         w[3] = ((unsigned long long)T.rx << 32) | ((unsigned long long)T.ncols << 8) | T.nrows;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3 (sorted-column form, the default admission kernel).  For one row the
+// admission test y <= thr is a threshold on the last R-group's value alone,
+// so the admitted columns are a prefix (minimize: x ascending, x <= thr) or a
+// suffix (maximize: x >= -thr) of that R-group's values sorted once per task
+// at table load (build_corners).  A tile of 32 whole rows costs one exact
+// fp64 threshold and one galloping search per row; after that, work is spent
+// only on admitted (row, column) pairs: exact per-row constraint thresholds
+// against the pairs' gathered constraint values, candidates appended exactly
+// as in the streaming forms.  The candidate set is identical (feasible and
+// s >= tau, both exact), so nothing downstream changes.
+struct SortedLaunch {
+  const float* sx;        // [task][pcols]: each reaction's last R-group values ascending, at pcol_off
+  const uint32_t* scol;   // same layout: column index of each sorted value
+  int64_t pcols;
+};
+
+// first index i in [0, n) with !(xs[i] <= t) (n if none); xs ascending
+__device__ __forceinline__ int first_gt(const float* __restrict__ xs, int n, float t) {
+  int lo = 0, p = 0, step = 1;
+  while (p < n && __ldg(xs + p) <= t) {
+    lo = p + 1;
+    p += step;
+    step <<= 1;
+  }
+  int hi = p < n ? p : n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(xs + mid) <= t) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// first index i in [0, n) with !(xs[i] < t) (n if none); xs ascending
+__device__ __forceinline__ int first_ge(const float* __restrict__ xs, int n, float t) {
+  int lo = 0, p = 0, step = 1;
+  while (p < n && __ldg(xs + p) < t) {
+    lo = p + 1;
+    p += step;
+    step <<= 1;
+  }
+  int hi = p < n ? p : n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(xs + mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kScanWarps * 32, 4) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
+  extern __shared__ __align__(16) float sm_s[];
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  const unsigned long long live = live_mask(L, 0u);
+  if (!live) return;
+  float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: constraint thresholds of the warp's rows
+  WorkCursor wc;
+  const float* __restrict__ values = L.values;
+  const int64_t n_pairs = L.n_pairs;
+
+  unsigned qi, t;
+  bool have = next_item(L, wc, live, lane, qi, t);
+  Tile T_n;
+  unsigned long long tau_n = 0;
+  if (have) {
+    T_n = L.tiles[t];
+    tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
+  }
+  while (have) {
+    const unsigned q_cur = qi;
+    const Tile T = T_n;
+    const unsigned long long tau = tau_n;
+    have = next_item(L, wc, live, lane, qi, t);
+    if (have) {
+      T_n = L.tiles[t];
+      tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
+    }
+    const ScanQuery& Q = L.queries[q_cur];
+    QCtl* ctl = Q.ctl;
+    const int maximize = Q.maximize;
+    const double b_obj = Q.test_bias[0];
+    const int nt = Q.nt;
+    const DevReaction& R = L.rx[T.rx];
+    const int c = R.c;
+    const int n_last = (int)R.size[c - 1];
+    const int col_lo = (int)T.col0, col_hi = (int)(T.col0 + T.ncols);
+    const int64_t last_pair = R.pair_off[c - 1];
+    const float* __restrict__ xs = S.sx + (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
+    const uint32_t* __restrict__ cs = S.scol + (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
+
+    const bool valid = lane < T.nrows;
+    const uint64_t row = T.row0 + (valid ? lane : 0u);
+    int64_t pr[kMaxRg - 1];
+    decode_prefix(R, c, row, pr);
+    const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
+    double p_obj = c > 1 ? (double)__ldg(vobj + pr[0]) : 0.0;
+#pragma unroll
+    for (int j = 1; j < kMaxRg - 1; ++j)
+      if (j < c - 1) p_obj = __dadd_rn(p_obj, (double)__ldg(vobj + pr[j]));
+    const unsigned long long gbase = R.g_off + row * (uint64_t)n_last;
+    // this row's admitted range [start, start + cnt) of the sorted column
+    int start = 0, cnt = 0;
+    if (valid) {
+      float th = __int_as_float(0x7f800000);
+      if (tau != kNoTau) {
+        const double ts = key_to_score(tau);
+        th = maximize ? -thr_lower_fast(p_obj, b_obj, ts) : thr_upper_fast(p_obj, b_obj, -ts);
+      }
+      if (th == th) {  // NaN: nothing passes
+        if (!maximize) {
+          cnt = first_gt(xs, n_last, th);
+        } else {
+          start = first_ge(xs, n_last, -th);
+          cnt = n_last - start;
+        }
+      }
+    }
+    const unsigned rows = __ballot_sync(0xffffffffu, cnt > 0);
+    if (!rows) continue;
+    // exact constraint thresholds of the rows that admit anything
+    if (cnt > 0) {
+      for (int i = 1; i < nt; ++i) {
+        const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
+        double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+        for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+        sthr[i * 32 + lane] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
+                                              : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
+      }
+    }
+    __syncwarp();
+    unsigned admitted = 0;
+    unsigned rr = rows;
+    while (rr) {
+      const int r = __ffs(rr) - 1;
+      rr &= rr - 1u;
+      const int cnt_r = __shfl_sync(0xffffffffu, cnt, r);
+      const int start_r = __shfl_sync(0xffffffffu, start, r);
+      const double po = __shfl_sync(0xffffffffu, p_obj, r);
+      const unsigned long long gb = __shfl_sync(0xffffffffu, gbase, r);
+      for (int j0 = 0; j0 < cnt_r; j0 += 32) {
+        const int j = j0 + (int)lane;
+        bool ok = j < cnt_r;
+        int col = 0;
+        float xo = 0.0f;
+        if (ok) {
+          col = (int)__ldg(cs + start_r + j);
+          xo = __ldg(xs + start_r + j);
+          ok = col >= col_lo && col < col_hi;
+        }
+        admitted += ok ? 1u : 0u;
+        bool pass = ok;
+        for (int i = 1; i < nt; ++i) {
+          float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
+          if (Q.test_lower[i]) x = -x;
+          pass = pass && (x <= sthr[i * 32 + r]);
+        }
+        const unsigned mk = __ballot_sync(0xffffffffu, pass);
+        if (!mk) continue;
+        unsigned long long cbase = 0;
+        if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
+        cbase = __shfl_sync(0xffffffffu, cbase, 0);
+        if (pass) {
+          const double val = fx(po, xo, b_obj);
+          Entry e;
+          e.key = skey(maximize ? val : -val);
+          e.g = gb + (unsigned long long)col;
+          const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
+          if (idx < Q.cap) Q.buf[idx] = e;
+          const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+          atomicAdd(&Q.hist[hb], 1u);
+          atomicAdd(&Q.coarse[hb >> 8], 1u);
+        }
+        if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
+          __threadfence();
+          refresh_tau(Q);
+        }
+      }
+    }
+    __syncwarp();
+    const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
+    if (a && lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)a);
   }
 }
 
