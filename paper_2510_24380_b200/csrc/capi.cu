@@ -187,6 +187,7 @@ struct apex_ctx {
   unsigned long long corner_total = 0;
   bool corners_ok = false;
   DBuf d_sorted_x, d_sorted_col;         // per task: each reaction's last R-group sorted ascending (value, column)
+  DBuf d_quant;                          // per task, reaction: kQuant + 1 evenly spaced values of the sorted column
   int n_tasks = 0;
   int64_t n_pairs = 0;
   bool table_loaded = false;
@@ -466,6 +467,7 @@ int build_corners(apex_ctx* c) {
   const size_t pc = (size_t)std::max<int64_t>(c->pcols, 4);
   std::vector<float> sx((size_t)c->n_tasks * pc, 0.0f);
   std::vector<uint32_t> scol((size_t)c->n_tasks * pc, 0u);
+  std::vector<float> quant((size_t)c->n_tasks * n_rx * (kQuant + 1), 0.0f);
   auto work = [&](int task) {
     std::vector<int32_t> idx;
     for (int t = 0; t < n_rx; ++t) {
@@ -481,6 +483,8 @@ int build_corners(apex_ctx* c) {
         ox[i] = v[idx[i]];
         oc[i] = (uint32_t)idx[i];
       }
+      float* oq = quant.data() + ((size_t)task * n_rx + t) * (kQuant + 1);
+      for (int qq = 0; qq <= kQuant; ++qq) oq[qq] = n > 0 ? ox[std::min<int64_t>(n - 1, qq * n / kQuant)] : 0.0f;
     }
     for (int dir = 0; dir < 2; ++dir) {
       int32_t* out = lists.data() + ((size_t)task * 2 + dir) * slots;
@@ -517,6 +521,8 @@ int build_corners(apex_ctx* c) {
   APEX_TRY(c->d_sorted_col.ensure(scol.size() * sizeof(uint32_t)));
   APEX_CU(cudaMemcpy(c->d_sorted_x.p, sx.data(), sx.size() * sizeof(float), cudaMemcpyHostToDevice));
   APEX_CU(cudaMemcpy(c->d_sorted_col.p, scol.data(), scol.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  APEX_TRY(c->d_quant.ensure(std::max<size_t>(1, quant.size()) * sizeof(float)));
+  if (!quant.empty()) APEX_CU(cudaMemcpy(c->d_quant.p, quant.data(), quant.size() * sizeof(float), cudaMemcpyHostToDevice));
   c->corner_slots = slots;
   c->corner_total = coff[n_rx];
   c->corners_ok = true;
@@ -772,8 +778,15 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   }
   // kernel choice: admission-first (admit), full predicate (full), or per query (auto)
   const bool admit = c->opt_mode >= 2;
-  const bool full = c->opt_mode != 2;
-  const bool autok = c->opt_mode == 3 && !tau0;
+  // the sorted-column kernel takes every query that has a constraint (it
+  // enumerates the most selective test's range per row); in auto mode the
+  // full-predicate kernel is only needed for unconstrained queries left
+  // without a seeded threshold
+  bool any_uncons = false;
+  for (int i = 0; i < nq; ++i) any_uncons = any_uncons || B.qs[i].n_constraints == 0;
+  const bool sorted_all = c->opt_mode == 3 && B.plan_rows;
+  const bool full = c->opt_mode != 2 && (!sorted_all || any_uncons);
+  const int autok = (c->opt_mode == 3 && !tau0) ? (sorted_all ? 2 : 1) : 0;
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
@@ -888,7 +901,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       ++st.launches;
     }
     {
-      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok ? 1 : 0);
+      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok);
       ++st.launches;
     }
   }
@@ -983,6 +996,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         SL.sx = c->d_sorted_x.as<float>();
         SL.scol = c->d_sorted_col.as<uint32_t>();
         SL.pcols = std::max<int64_t>(c->pcols, 4);
+        SL.quant = c->d_quant.as<float>();
+        SL.n_rx = (int)c->rx.size();
         for (int q0 = 0; q0 < nq; q0 += 64) {
           const int nql = std::min(64, nq - q0);
           ScanLaunch La = L;
@@ -1038,6 +1053,11 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         }
       }
       for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
+        if (sorted_all) {
+          bool need = false;  // only unconstrained queries can end up in the full-predicate kernel
+          for (int q = B.cls_begin[k]; q < B.cls_begin[k + 1]; ++q) need = need || B.qs[q].n_constraints == 0;
+          if (!need) continue;
+        }
         ScanFn fn = pick_scan(B.cls_nt[k], B.rl, c->opt_mode == 1 ? 1 : 0);
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
@@ -1357,7 +1377,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_goff.release();
   c->d_values.release();
   c->d_biases.release();
-  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff, &c->d_sorted_x, &c->d_sorted_col}) b->release();
+  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff, &c->d_sorted_x, &c->d_sorted_col, &c->d_quant}) b->release();
   c->d_queries.release();
   c->d_tau0.release();
   c->d_hists.release();

@@ -17,6 +17,7 @@ namespace apexb200 {
 constexpr int kMaxRg = APEX_MAX_RGROUPS;
 constexpr int kMaxTests = 24;       // compiled maximum of per-product tests
 constexpr int kMaxCons = 32;        // constraints per query (materialization)
+constexpr int kQuant = 32;        // quantile steps per sorted column (test choice)
 constexpr int kScanWarps = 8;       // warps per enumeration CTA
 constexpr int kSelectThreads = 512;
 constexpr uint64_t kNoTau = 0ull;   // "no admission threshold yet" (key 0 is never a finite score)

@@ -1387,6 +1387,8 @@ struct SortedLaunch {
   const float* sx;        // [task][pcols]: each reaction's last R-group values ascending, at pcol_off
   const uint32_t* scol;   // same layout: column index of each sorted value
   int64_t pcols;
+  const float* quant;     // [task][n_rx][kQuant + 1]: evenly spaced values of each sorted column
+  int n_rx;
 };
 
 // first index i in [0, n) with !(xs[i] <= t) (n if none); xs ascending
@@ -1421,12 +1423,31 @@ __device__ __forceinline__ int first_ge(const float* __restrict__ xs, int n, flo
   return lo;
 }
 
+// Approximate passing count (in kQuant+1 quantile steps) of a test on a sorted
+// column: upper tests pass x <= t, lower tests pass x >= t.  Used only to pick
+// which test's exact range to enumerate.
+__device__ __forceinline__ int quant_count(const float* __restrict__ q, bool lower, float t) {
+  int lo = 0, hi = kQuant + 1;  // first index failing the monotone predicate
+  if (!lower) {
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(q + mid) <= t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  }
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(q + mid) < t) lo = mid + 1; else hi = mid;
+  }
+  return kQuant + 1 - lo;
+}
+
 __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
   extern __shared__ __align__(16) float sm_s[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   const unsigned long long live = live_mask(L, 0u);
   if (!live) return;
-  float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: constraint thresholds of the warp's rows
+  float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: signed-value thresholds of every test
   WorkCursor wc;
   const float* __restrict__ values = L.values;
   const int64_t n_pairs = L.n_pairs;
@@ -1458,75 +1479,101 @@ __global__ void __launch_bounds__(kScanWarps * 32, 4) scan_sorted_kernel(const S
     const int n_last = (int)R.size[c - 1];
     const int col_lo = (int)T.col0, col_hi = (int)(T.col0 + T.ncols);
     const int64_t last_pair = R.pair_off[c - 1];
-    const float* __restrict__ xs = S.sx + (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
-    const uint32_t* __restrict__ cs = S.scol + (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
 
     const bool valid = lane < T.nrows;
     const uint64_t row = T.row0 + (valid ? lane : 0u);
     int64_t pr[kMaxRg - 1];
     decode_prefix(R, c, row, pr);
-    const float* __restrict__ vobj = values + (int64_t)Q.test_task[0] * n_pairs;
-    double p_obj = c > 1 ? (double)__ldg(vobj + pr[0]) : 0.0;
-#pragma unroll
-    for (int j = 1; j < kMaxRg - 1; ++j)
-      if (j < c - 1) p_obj = __dadd_rn(p_obj, (double)__ldg(vobj + pr[j]));
     const unsigned long long gbase = R.g_off + row * (uint64_t)n_last;
-    // this row's admitted range [start, start + cnt) of the sorted column
-    int start = 0, cnt = 0;
-    if (valid) {
-      float th = __int_as_float(0x7f800000);
-      if (tau != kNoTau) {
-        const double ts = key_to_score(tau);
-        th = maximize ? -thr_lower_fast(p_obj, b_obj, ts) : thr_upper_fast(p_obj, b_obj, -ts);
-      }
-      if (th == th) {  // NaN: nothing passes
-        if (!maximize) {
-          cnt = first_gt(xs, n_last, th);
-        } else {
-          start = first_ge(xs, n_last, -th);
-          cnt = n_last - start;
-        }
-      }
+    // the objective's exact per-row threshold (against tau, +inf without one)
+    // and its approximate passing count; only when that is not already small
+    // are the constraint thresholds derived to find a more selective test
+    double p_obj;
+    {
+      const float* v = values + (int64_t)Q.test_task[0] * n_pairs;
+      double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+#pragma unroll
+      for (int j = 1; j < kMaxRg - 1; ++j)
+        if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+      p_obj = p;
     }
-    const unsigned rows = __ballot_sync(0xffffffffu, cnt > 0);
-    if (!rows) continue;
-    // exact constraint thresholds of the rows that admit anything
-    if (cnt > 0) {
+    float th0 = __int_as_float(0x7f800000);
+    if (tau != kNoTau) {
+      const double ts = key_to_score(tau);
+      th0 = maximize ? -thr_lower_fast(p_obj, b_obj, ts) : thr_upper_fast(p_obj, b_obj, -ts);
+    }
+    sthr[lane] = th0;
+    int best = 0;
+    int best_q = th0 == th0 ? quant_count(S.quant + ((int64_t)Q.test_task[0] * S.n_rx + T.rx) * (kQuant + 1),
+                                          maximize != 0, maximize ? -th0 : th0)
+                            : 0;
+    bool cons_ready = false;
+    auto constraint_thresholds = [&](bool choose) {
       for (int i = 1; i < nt; ++i) {
-        const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
+        const int task = Q.test_task[i];
+        const float* v = values + (int64_t)task * n_pairs;
         double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
         for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-        sthr[i * 32 + lane] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
-                                              : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
+        const bool lower = Q.test_lower[i] != 0;
+        const float th = lower ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
+                               : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
+        sthr[i * 32 + lane] = th;
+        if (choose) {
+          const int qc = th == th ? quant_count(S.quant + ((int64_t)task * S.n_rx + T.rx) * (kQuant + 1), lower,
+                                                lower ? -th : th)
+                                  : 0;
+          if (qc < best_q) {
+            best_q = qc;
+            best = i;
+          }
+        }
+      }
+      cons_ready = true;
+    };
+    if (valid && best_q > 2 && nt > 1) constraint_thresholds(true);
+    // exact passing range of the chosen test in its sorted column
+    int start = 0, cnt = 0;
+    if (valid && best_q > 0) {
+      const float th = sthr[best * 32 + lane];
+      const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
+      if (!Q.test_lower[best]) {
+        cnt = first_gt(S.sx + base, n_last, th);
+      } else {
+        start = first_ge(S.sx + base, n_last, -th);
+        cnt = n_last - start;
       }
     }
+    if (cnt > 0 && !cons_ready) constraint_thresholds(false);
+    unsigned rows = __ballot_sync(0xffffffffu, cnt > 0);
     __syncwarp();
     unsigned admitted = 0;
-    unsigned rr = rows;
-    while (rr) {
-      const int r = __ffs(rr) - 1;
-      rr &= rr - 1u;
+    while (rows) {
+      const int r = __ffs(rows) - 1;
+      rows &= rows - 1u;
       const int cnt_r = __shfl_sync(0xffffffffu, cnt, r);
       const int start_r = __shfl_sync(0xffffffffu, start, r);
+      const int best_r = __shfl_sync(0xffffffffu, best, r);
       const double po = __shfl_sync(0xffffffffu, p_obj, r);
       const unsigned long long gb = __shfl_sync(0xffffffffu, gbase, r);
+      const int64_t sbase = (int64_t)Q.test_task[best_r] * S.pcols + R.pcol_off + start_r;
       for (int j0 = 0; j0 < cnt_r; j0 += 32) {
         const int j = j0 + (int)lane;
         bool ok = j < cnt_r;
         int col = 0;
-        float xo = 0.0f;
         if (ok) {
-          col = (int)__ldg(cs + start_r + j);
-          xo = __ldg(xs + start_r + j);
+          col = (int)__ldg(S.scol + sbase + j);
           ok = col >= col_lo && col < col_hi;
         }
-        admitted += ok ? 1u : 0u;
+        // every test on the pair (the chosen one passes by construction);
+        // gathers issued without short-circuit
         bool pass = ok;
-        for (int i = 1; i < nt; ++i) {
-          float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
-          if (Q.test_lower[i]) x = -x;
-          pass = pass && (x <= sthr[i * 32 + r]);
+        float xo = 0.0f;
+        for (int i = 0; i < nt; ++i) {
+          const float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
+          if (i == 0) xo = x;
+          pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
         }
+        admitted += ok ? 1u : 0u;
         const unsigned mk = __ballot_sync(0xffffffffu, pass);
         if (!mk) continue;
         unsigned long long cbase = 0;
@@ -2141,7 +2188,11 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
       // automatic kernel choice: without a seeded threshold (fewer than k
       // feasible seed products) the admission test admits nearly everything,
       // so the full-predicate kernel is cheaper
-      if (auto_kernel) ctl->use_full = ctl->tau_key == kNoTau ? 1u : 0u;
+      // (auto 2: the sorted-column kernel enumerates the most selective
+      // test per row, so only an unconstrained query without a threshold
+      // needs the full predicate)
+      if (auto_kernel == 1) ctl->use_full = ctl->tau_key == kNoTau ? 1u : 0u;
+      if (auto_kernel == 2) ctl->use_full = (ctl->tau_key == kNoTau && Q.nt == 1) ? 1u : 0u;
     }
   } else {
     const int B = kth_two_level(Q.hist, Q.coarse, k, &cnt);
