@@ -848,7 +848,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     APEX_CU(cudaMemcpyAsync(c->d_groups.p, c->h_groups.p, gb, cudaMemcpyHostToDevice, s));
     APEX_CU(cudaEventRecord(c->groups_ev, s));
     st.h2d_bytes += (int64_t)gb;
-  } else if (admit) {
+  } else if (admit && !(B.plan_rows && span < (uint64_t)c->opt_chunk_min)) {
+    // (the sorted-column kernel reads the table's sorted lists, not a packed column)
     int64_t max_last = 1;
     for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
     const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
