@@ -230,6 +230,7 @@ struct apex_ctx {
                                     // 1 = full predicate (FADD2 sign bits)
   int64_t opt_cb_admit = 512;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
+  int64_t opt_corner_mult = 16;     // corner products per reaction ~ corner_mult * k / reactions
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
@@ -861,7 +862,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   // seed threshold from exact samples
   if (!tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
-                                     : (uint64_t)std::min<int64_t>(1 << 17, std::max<int64_t>(1 << 13, 8 * B.k_max));
+                                     : (uint64_t)std::min<int64_t>(1 << 15, std::max<int64_t>(1 << 11, 2 * B.k_max));
     S = std::min<uint64_t>(S, std::max<uint64_t>(span / 32, std::min<uint64_t>(span, 4096)));
     if (S > 0) {
       SampleLaunch P;
@@ -897,7 +898,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       // corner budget per reaction: enough corner products for ~16k feasible
       // seeds across the reactions, within the precomputed list lengths
       const int64_t nrx = std::max<int64_t>(1, (int64_t)c->rx.size());
-      CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, 16 * B.k_max / nrx));
+      CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, c->opt_corner_mult * B.k_max / nrx));
       corner_kernel<<<dim3((unsigned)c->rx.size(), nq), 256, 0, s>>>(CL);
       ++st.launches;
     }
@@ -1854,6 +1855,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
+  else if (n == "corner_mult") c->opt_corner_mult = std::max<int64_t>(1, v);
   else if (n == "vote64") c->opt_vote64 = v;
   else if (n == "dense") c->opt_dense = v;
   else if (n == "sorted") c->opt_sorted = v;
