@@ -1442,7 +1442,10 @@ __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool low
   return kQuant + 1 - lo;
 }
 
-__global__ void __launch_bounds__(kScanWarps * 32, 4) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
+#ifndef APEX_SORTED_MINB
+#define APEX_SORTED_MINB 4
+#endif
+__global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
   extern __shared__ __align__(16) float sm_s[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   const unsigned long long live = live_mask(L, 0u);
