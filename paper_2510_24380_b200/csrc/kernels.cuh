@@ -1507,9 +1507,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     }
     sthr[lane] = th0;
     int best = 0;
-    int best_q = th0 == th0 ? quant_count(S.quant + ((int64_t)Q.test_task[0] * S.n_rx + T.rx) * (kQuant + 1),
-                                          maximize != 0, maximize ? -th0 : th0)
-                            : 0;
+    // objective range small (<= 2 quantile steps) is read off one table entry;
+    // the full count is taken only when other tests are compared with it
+    const float* q0 = S.quant + ((int64_t)Q.test_task[0] * S.n_rx + T.rx) * (kQuant + 1);
+    int best_q = 0;
+    if (th0 == th0) {
+      const bool wide = maximize ? (__ldg(q0 + kQuant - 2) >= -th0) : (__ldg(q0 + 2) <= th0);
+      best_q = wide ? quant_count(q0, maximize != 0, maximize ? -th0 : th0) : 2;
+    }
     bool cons_ready = false;
     auto constraint_thresholds = [&](bool choose) {
       for (int i = 1; i < nt; ++i) {
