@@ -166,6 +166,8 @@ struct Batch {
 struct apex_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;           // second stream: the corner seed runs beside the sample seed
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   bool own_stream = false;
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
@@ -199,13 +201,9 @@ struct apex_ctx {
   bool copy_next = false;                // next prepare_batch: result D2H inside the pass
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
-  std::vector<DBuf> colbufs;             // multi-query kernel: packed objective columns
-  DBuf d_groups, d_tctr;                 // multi-query kernel: group descriptors, work counters
   DBuf d_work;                           // flattened-work counters of the scan launches
   DBuf d_trace;                          // optional per-item timing records of the admission scan
   int64_t trace_cap = 0, trace_n = 0;
-  HBuf h_groups;
-  cudaEvent_t groups_ev = nullptr;
   HBuf h_queries, h_ctl, h_out, h_tau0;
   std::vector<std::unique_ptr<Plan>> plans;
   uint64_t stamp = 0;
@@ -234,7 +232,6 @@ struct apex_ctx {
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
-  int64_t opt_multi = 0;            // admission-first queries of a batch share one multi-query pass
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
@@ -582,10 +579,9 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   B.ntp = (B.NT + 3) / 4 * 4;
   B.rl = (int)c->opt_rl;
   if (B.rl != 1 && B.rl != 2) B.rl = 1;
-  if (c->opt_mode >= 2 && c->opt_multi) B.rl = 1;  // the multi-query kernel owns one row per lane
   APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, nq, B.plan));
   B.plan_rows = nullptr;
-  if (c->opt_mode >= 2 && c->opt_sorted && !c->opt_multi && c->trace_cap == 0) {
+  if (c->opt_mode >= 2 && c->opt_sorted && c->trace_cap == 0) {
     Plan* keep = B.plan;
     int64_t max_last = 1;
     for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
@@ -623,14 +619,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
   APEX_TRY(c->d_work.ensure(64 * sizeof(unsigned)));
-  if (c->opt_mode >= 2 && c->opt_multi) {
-    const int ng = (nq + kMaxGroupQ - 1) / kMaxGroupQ;
-    if ((int)c->colbufs.size() < nq) c->colbufs.resize(nq);
-    for (int i = 0; i < nq; ++i) APEX_TRY(c->colbufs[i].ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
-    APEX_TRY(c->h_groups.ensure(ng * sizeof(MultiGroup)));
-    APEX_TRY(c->d_groups.ensure(ng * sizeof(MultiGroup)));
-    APEX_TRY(c->d_tctr.ensure(ng * sizeof(unsigned)));
-  }
   APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
   std::vector<ScanQuery> hq(nq);
   for (int i = 0; i < nq; ++i) {
@@ -792,64 +780,8 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
-  // K2 pack of the streamed objective column(s)
-  const bool multi = admit && c->opt_multi;
-  std::vector<MultiGroup> groups;
-  if (multi) {
-    // distinct (objective task, direction) columns of the batch, packed once
-    std::vector<std::pair<int, int>> keys;
-    std::vector<int> qcol(nq);
-    for (int i = 0; i < nq; ++i) {
-      const std::pair<int, int> kk(B.qs[i].objective_task, B.qs[i].maximize ? 1 : 0);
-      auto it = std::find(keys.begin(), keys.end(), kk);
-      qcol[i] = (int)(it - keys.begin());
-      if (it == keys.end()) keys.push_back(kk);
-    }
-    if (c->colbufs.size() < keys.size()) c->colbufs.resize(keys.size());
-    for (size_t o = 0; o < keys.size(); ++o)
-      APEX_TRY(c->colbufs[o].ensure((size_t)std::max<int64_t>(c->pcols, 4) * sizeof(float)));
-    int64_t max_last = 1;
-    for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
-    const unsigned gx = (unsigned)std::min<int64_t>((max_last + 255) / 256, 64);
-    for (size_t o0 = 0; o0 < keys.size(); o0 += kMaxGroupQ) {
-      PackCols P;
-      P.ncols = (int)std::min<size_t>(kMaxGroupQ, keys.size() - o0);
-      for (int o = 0; o < P.ncols; ++o) {
-        P.task[o] = keys[o0 + o].first;
-        P.lower[o] = keys[o0 + o].second;  // maximize -> admission is a lower bound on x -> y = -x
-        P.dst[o] = c->colbufs[o0 + o].as<float>();
-      }
-      pack_cols_kernel<<<dim3(gx, (unsigned)c->rx.size(), P.ncols), 256, 0, s>>>(P, c->d_rx.as<DevReaction>(),
-                                                                                 c->d_values.as<float>(), c->n_pairs);
-      ++st.launches;
-    }
-    // groups of <= 32 queries; a group's columns are local indices into its own list
-    for (int q0 = 0; q0 < nq; q0 += kMaxGroupQ) {
-      MultiGroup Gp;
-      std::memset(&Gp, 0, sizeof(Gp));
-      Gp.q0 = q0;
-      Gp.nq = std::min(kMaxGroupQ, nq - q0);
-      std::vector<int> loc;
-      for (int q = 0; q < Gp.nq; ++q) {
-        const int gcol = qcol[q0 + q];
-        auto it = std::find(loc.begin(), loc.end(), gcol);
-        Gp.oc[q] = (int)(it - loc.begin());
-        if (it == loc.end()) loc.push_back(gcol);
-      }
-      Gp.ncols = (int)loc.size();
-      for (int o = 0; o < Gp.ncols; ++o) Gp.col[o] = c->colbufs[loc[o]].as<float>();
-      groups.push_back(Gp);
-    }
-    const size_t gb = groups.size() * sizeof(MultiGroup);
-    APEX_CU(cudaEventSynchronize(c->groups_ev));
-    APEX_TRY(c->h_groups.ensure(gb));
-    APEX_TRY(c->d_groups.ensure(gb));
-    APEX_TRY(c->d_tctr.ensure(groups.size() * sizeof(unsigned)));
-    std::memcpy(c->h_groups.p, groups.data(), gb);
-    APEX_CU(cudaMemcpyAsync(c->d_groups.p, c->h_groups.p, gb, cudaMemcpyHostToDevice, s));
-    APEX_CU(cudaEventRecord(c->groups_ev, s));
-    st.h2d_bytes += (int64_t)gb;
-  } else if (admit && !(B.plan_rows && span < (uint64_t)c->opt_chunk_min)) {
+  // K2 pack of the streamed objective column
+  if (admit && !(B.plan_rows && span < (uint64_t)c->opt_chunk_min)) {
     // (the sorted-column kernel reads the table's sorted lists, not a packed column)
     int64_t max_last = 1;
     for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
@@ -859,8 +791,14 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     ++st.launches;
   }
   APEX_CU(stage_mark(c, 1, s));
-  // seed threshold from exact samples
+  // seed threshold from exact samples (uniform samples on the main stream,
+  // the corner on the side stream: independent, they overlap)
   if (!tau0) {
+    const bool corner = c->opt_corner && c->corners_ok;
+    if (corner) {
+      APEX_CU(cudaEventRecord(c->fork_ev, s));
+      APEX_CU(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+    }
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
                                      : (uint64_t)std::min<int64_t>(1 << 15, std::max<int64_t>(1 << 11, 2 * B.k_max));
     S = std::min<uint64_t>(S, std::max<uint64_t>(span / 32, std::min<uint64_t>(span, 4096)));
@@ -881,7 +819,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       sample_kernel<<<dim3(blocks, (unsigned)nq), 256, 0, s>>>(P, nq);
       ++st.launches;
     }
-    if (c->opt_corner && c->corners_ok) {
+    if (corner) {
       CornerLaunch CL;
       CL.queries = dq;
       CL.rx = c->d_rx.as<DevReaction>();
@@ -899,8 +837,10 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       // seeds across the reactions, within the precomputed list lengths
       const int64_t nrx = std::max<int64_t>(1, (int64_t)c->rx.size());
       CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, c->opt_corner_mult * B.k_max / nrx));
-      corner_kernel<<<dim3((unsigned)c->rx.size(), nq), 256, 0, s>>>(CL);
+      corner_kernel<<<dim3((unsigned)c->rx.size(), nq), 256, 0, c->side>>>(CL);
       ++st.launches;
+      APEX_CU(cudaEventRecord(c->join_ev, c->side));
+      APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
     }
     {
       tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok);
@@ -946,48 +886,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       L.work = c->d_work.as<unsigned>();
       L.chunk = (int)c->opt_chunk;
       if (ci == 0) APEX_CU(stage_mark(c, 6, s));
-      if (multi) {
-        int ncmax = 1;
-        for (const auto& Gp : groups) ncmax = std::max(ncmax, Gp.ncols);
-        int MQ = 1;
-        while (MQ < ncmax) MQ <<= 1;
-        ScanFn fnm = nullptr;
-        switch (MQ) {
-          case 1: fnm = (ScanFn)(void*)scan_multi_kernel<1>; break;
-          case 2: fnm = (ScanFn)(void*)scan_multi_kernel<2>; break;
-          case 4: fnm = (ScanFn)(void*)scan_multi_kernel<4>; break;
-          case 8: fnm = (ScanFn)(void*)scan_multi_kernel<8>; break;
-          case 16: fnm = (ScanFn)(void*)scan_multi_kernel<16>; break;
-          default: fnm = (ScanFn)(void*)scan_multi_kernel<32>; break;
-        }
-        // column block: ~1 KB of columns per buffer per warp
-        int cbm = (int)std::max<int64_t>(16, std::min<int64_t>(c->opt_cb_admit, 256 / ncmax) / 16 * 16);
-        const size_t smem = ((size_t)kScanWarps * 2 * ncmax * cbm + (size_t)kScanWarps * kMaxGroupQ * 32 +
-                             (size_t)kScanWarps * 16 * kMaxTests) * sizeof(float) +
-                            (size_t)kScanWarps * 2 * sizeof(uint64_t);
-        int occ = 0;
-        APEX_TRY(scan_occupancy(fnm, smem, &occ));
-        const int64_t blocks =
-            std::min<int64_t>((int64_t)((te - tb + kScanWarps - 1) / kScanWarps), (int64_t)c->sm_count * occ);
-        MultiLaunch ML;
-        ML.tiles = plan->d_tiles.as<Tile>();
-        ML.tile_begin = (unsigned)tb;
-        ML.tile_end = (unsigned)te;
-        ML.rx = c->d_rx.as<DevReaction>();
-        ML.values = c->d_values.as<float>();
-        ML.n_pairs = c->n_pairs;
-        ML.queries = dq;
-        ML.groups = c->d_groups.as<MultiGroup>();
-        ML.tile_counters = c->d_tctr.as<unsigned>();
-        ML.cb = cbm;
-        ML.ncols_max = ncmax;
-        APEX_CU(cudaMemsetAsync(c->d_tctr.p, 0, groups.size() * sizeof(unsigned), s));
-        void (*kfn)(const MultiLaunch) = reinterpret_cast<void (*)(const MultiLaunch)>(fnm);
-        kfn<<<dim3((unsigned)blocks, (unsigned)groups.size()), kScanWarps * 32, smem, s>>>(ML);
-        APEX_CU(cudaGetLastError());
-        ++st.launches;
-        ++st.scans;
-      } else if (admit && B.plan_rows && bounds.size() == 1) {
+      if (admit && B.plan_rows && bounds.size() == 1) {
         // sorted-column admission: whole-row tiles, one launch per 64 queries
         const Plan* pr_ = B.plan_rows;
         const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
@@ -1364,7 +1263,9 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&c->upload_ev, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&c->groups_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   *out = c;
   return APEX_OK;
 }
@@ -1393,12 +1294,10 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   if (c->upload_ev) cudaEventDestroy(c->upload_ev);
-  if (c->groups_ev) cudaEventDestroy(c->groups_ev);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
-  for (auto& b : c->colbufs) b.release();
-  c->d_groups.release();
-  c->d_tctr.release();
-  c->h_groups.release();
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1868,7 +1767,6 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
       APEX_CU(cudaMemset(c->d_trace.p, 0, (size_t)c->trace_cap * 64));
     }
   }
-  else if (n == "multi") c->opt_multi = v;
   else if (n == "graph") c->opt_graph = v;
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
   else if (n == "tiles_per_slot") c->opt_tiles_per_slot = std::max<int64_t>(1, v);

@@ -731,21 +731,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
 // fp64 in the reference's order, only for products that pass admission: the
 // predicate is a conjunction, so this short-circuit yields the same candidate
 // set as evaluating every test on every product.
-// Exact constraint predicate of one product evaluated directly in fp64:
-// val = ((prefix + x) + bias) in the reference order (kept for tests/debug).
-__device__ __forceinline__ bool feasible_exact(const ScanQuery& Q, const float* __restrict__ values, int64_t n_pairs,
-                                               const int64_t* pr, int c, int64_t last_pair) {
-  for (int i = 1; i < Q.nt; ++i) {
-    const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
-    const float x = __ldg(v + last_pair);
-    double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
-    for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-    const double val = fx(p, x, Q.test_bias[i]);
-    if (Q.test_lower[i] ? !(val >= Q.test_beta[i]) : !(val <= Q.test_beta[i])) return false;
-  }
-  return true;
-}
-
 // min of 16 consecutive fp32 in shared memory (32-bit shared address)
 __device__ __forceinline__ float min16_shared(uint32_t addr) {
   float a0, a1, a2, a3, b0, b1, b2, b3, c0, c1, c2, c3, d0, d1, d2, d3;
@@ -1611,312 +1596,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
 }
 
 // ---------------------------------------------------------------------------
-// K3 (multi-query admission-first form).  One pass over the tiles answers a
-// whole group of up to MAXQ queries: the rows are decoded once, each distinct
-// signed objective column (objective task x direction) is staged once per
-// column block by TMA, and per 16 columns every query costs ONE compare of the
-// column-min of its objective against its per-row exact threshold.  The rare
-// path (some product of some query admitted) is the single-query one, per query.
-constexpr int kMaxGroupQ = 32;
-
-struct MultiGroup {
-  int nq;                            // queries in this group
-  int ncols;                         // distinct objective columns
-  int q0;                            // first query (index into the batch's ScanQuery array)
-  int _pad;
-  int oc[kMaxGroupQ];                // column of each query
-  const float* col[kMaxGroupQ];      // packed signed objective columns (16-B aligned per reaction)
-};
-
-struct MultiLaunch {
-  const Tile* tiles;
-  unsigned int tile_begin, tile_end;
-  const DevReaction* rx;
-  const float* values;
-  int64_t n_pairs;
-  const ScanQuery* queries;
-  const MultiGroup* groups;          // [gridDim.y]
-  unsigned int* tile_counters;       // [gridDim.y] work counters
-  int cb;                            // columns per block (multiple of 16)
-  int ncols_max;                     // smem sizing
-};
-
-template <int MAXC>
-__global__ void __launch_bounds__(kScanWarps * 32, 2) scan_multi_kernel(const MultiLaunch L) {
-  // MAXC: compiled maximum of distinct objective columns per group; queries
-  // per group (<= 32) are handled by runtime loops, their per-row thresholds
-  // live in shared memory ([q][lane]), only the per-column maxima in registers
-  extern __shared__ __align__(128) float sm_f[];
-  const MultiGroup& G = L.groups[blockIdx.y];
-  const ScanQuery* __restrict__ QS = L.queries + G.q0;
-  const int nq = G.nq, ncols = G.ncols;
-  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  const int cb = L.cb;
-  const int cstride = L.ncols_max * cb;                       // floats per buffer
-  const int off0 = (int)warp * 2 * cstride, off1 = off0 + cstride;
-  const int tso = kScanWarps * 2 * cstride + (int)warp * kMaxGroupQ * 32;         // thresholds [q][lane]
-  const int xo = kScanWarps * 2 * cstride + kScanWarps * kMaxGroupQ * 32 + (int)warp * 16 * kMaxTests;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_f + kScanWarps * 2 * cstride + kScanWarps * kMaxGroupQ * 32 +
-                                               kScanWarps * 16 * kMaxTests) + warp * 2;
-  unsigned live = 0;
-  for (int q = 0; q < nq; ++q) {
-    const QCtl* cq = QS[q].ctl;
-    if (*(volatile unsigned*)&cq->active && !*(volatile unsigned*)&cq->use_full) live |= 1u << q;
-  }
-  if (!live) return;
-  if (lane == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  uint32_t phase0 = 0, phase1 = 0;
-  unsigned bi = 0;
-  const float* __restrict__ values = L.values;
-  const int64_t n_pairs = L.n_pairs;
-  const float pad_y = __int_as_float(0x7fffffff);  // NaN: never passes
-  constexpr int kTauPoll = 8;
-  unsigned int* tctr = L.tile_counters + blockIdx.y;
-
-  unsigned t_next = 0;
-  if (lane == 0) t_next = atomicAdd(tctr, 1u);
-  unsigned long long tau_seen[kMaxGroupQ];  // local memory
-  for (int q = 0; q < nq; ++q) tau_seen[q] = *(volatile unsigned long long*)&QS[q].ctl->tau_key;
-  int poll = 0;
-  double pobj[kMaxGroupQ];                  // local memory
-  int cached_q = -1;
-  float thrc[kMaxTests];
-  float thrmax[MAXC];
-  float* thr_s = sm_f + tso + lane;         // thr_s[q * 32]
-
-  for (;;) {
-    unsigned t = __shfl_sync(0xffffffffu, t_next, 0) + L.tile_begin;
-    if (t >= L.tile_end) break;
-    if (lane == 0) t_next = atomicAdd(tctr, 1u);
-    const Tile T = L.tiles[t];
-    const DevReaction& R = L.rx[T.rx];
-    const int c = R.c;
-    const int64_t n_last = R.size[c - 1];
-    const uint32_t lead = T.col0 & 3u;
-    const uint32_t ac0 = T.col0 - lead;
-    const uint32_t ncols_t = T.ncols + lead;
-    const int64_t last_pair0 = R.pair_off[c - 1] + ac0;
-    const int64_t src0 = R.pcol_off + ac0;
-    const int nblk = (int)((ncols_t + cb - 1) / cb);
-    if (lane == 0) {
-      const uint32_t bytes = ((ncols_t < (uint32_t)cb ? ncols_t : (uint32_t)cb) * 4u + 15u) & ~15u;
-      fence_proxy_async();
-      mbar_expect_tx(&bars[bi], bytes * ncols);
-      for (int o = 0; o < ncols; ++o) bulk_g2s(sm_f + (bi ? off1 : off0) + o * cb, G.col[o] + src0, bytes, &bars[bi]);
-    }
-    cached_q = -1;
-    const bool valid = lane < T.nrows;
-    const uint64_t row = T.row0 + (valid ? lane : 0u);
-    int64_t pr[kMaxRg - 1];
-    {
-      uint64_t rem = row;
-#pragma unroll
-      for (int j = kMaxRg - 2; j >= 1; --j) {
-        pr[j] = 0;
-        if (j <= c - 2) {
-          uint64_t qq, d;
-          divmod_u64(qq, d, rem, (uint64_t)R.size[j]);
-          pr[j] = R.pair_off[j] + (int64_t)d;
-          rem = qq;
-        }
-      }
-      pr[0] = R.pair_off[0] + (int64_t)rem;
-    }
-    const unsigned long long gbase = R.g_off + row * (uint64_t)n_last + ac0;
-#pragma unroll 1
-    for (int q = 0; q < nq; ++q) {
-      float th = __int_as_float(0x7fffffff);
-      if ((live >> q) & 1u) {
-        const ScanQuery& Q = QS[q];
-        const float* v = values + (int64_t)Q.test_task[0] * n_pairs;
-        double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
-        for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-        pobj[q] = p;
-        if (valid) {
-          th = __int_as_float(0x7f800000);
-          if (tau_seen[q] != kNoTau) {
-            const double ts = key_to_score(tau_seen[q]);
-            th = Q.maximize ? -thr_lower_fast(p, Q.test_bias[0], ts) : thr_upper_fast(p, Q.test_bias[0], -ts);
-          }
-        }
-      }
-      thr_s[q * 32] = th;
-    }
-    // per objective column, the loosest threshold of the queries reading it:
-    // some query admits a product of column o iff y <= max_q thr_q
-    auto update_thrmax = [&]() {
-#pragma unroll
-      for (int o = 0; o < MAXC; ++o) thrmax[o] = __int_as_float(0xff800000);
-#pragma unroll 1
-      for (int q = 0; q < nq; ++q) {
-        const float th = thr_s[q * 32];
-        const int oq = G.oc[q];
-#pragma unroll
-        for (int o = 0; o < MAXC; ++o)
-          if (o == oq && th == th) thrmax[o] = fmaxf(thrmax[o], th);
-      }
-    };
-    update_thrmax();
-
-    for (int blk = 0; blk < nblk; ++blk) {
-      const int col_base = blk * cb;
-      const int ncol = min(cb, (int)ncols_t - col_base);
-      if (blk + 1 < nblk && lane == 0) {
-        const unsigned nb = bi ^ 1u;
-        const uint32_t bytes = ((uint32_t)min(cb, (int)ncols_t - col_base - cb) * 4u + 15u) & ~15u;
-        fence_proxy_async();
-        mbar_expect_tx(&bars[nb], bytes * ncols);
-        for (int o = 0; o < ncols; ++o)
-          bulk_g2s(sm_f + (nb ? off1 : off0) + o * cb, G.col[o] + src0 + col_base + cb, bytes, &bars[nb]);
-      }
-      if (++poll == kTauPoll) {
-        poll = 0;
-        bool changed = false;
-#pragma unroll 1
-        for (int q = 0; q < nq; ++q) {
-          if (!((live >> q) & 1u)) continue;
-          const unsigned long long tn = *(volatile unsigned long long*)&QS[q].ctl->tau_key;
-          if (tn != tau_seen[q]) {
-            tau_seen[q] = tn;
-            changed = true;
-            if (valid) {
-              const ScanQuery& Q = QS[q];
-              const double ts = key_to_score(tn);
-              thr_s[q * 32] = Q.maximize ? -thr_lower_fast(pobj[q], Q.test_bias[0], ts)
-                                         : thr_upper_fast(pobj[q], Q.test_bias[0], -ts);
-            }
-          }
-        }
-        if (changed) update_thrmax();
-      }
-      if (bi) { mbar_wait(&bars[1], phase1); phase1 ^= 1u; }
-      else    { mbar_wait(&bars[0], phase0); phase0 ^= 1u; }
-      const int yo = bi ? off1 : off0;
-      const int ngroups = (ncol + 15) >> 4;
-      if ((ncol & 15) || (blk == 0 && lead)) {
-        const int pad = (ngroups << 4) - ncol;
-        for (int o = 0; o < ncols; ++o) {
-          if ((int)lane < pad) sm_f[yo + o * cb + ncol + lane] = pad_y;
-          if (blk == 0 && lane < lead) sm_f[yo + o * cb + lane] = pad_y;
-        }
-        __syncwarp();
-      }
-      const uint32_t ybase = smem_u32(sm_f) + (uint32_t)yo * 4u;
-      for (int gi = 0; gi < ngroups; ++gi) {
-        const int j0 = gi << 4;
-        bool any = false;
-#pragma unroll
-        for (int o = 0; o < MAXC; ++o)
-          if (o < ncols) any = any | (min16_shared(ybase + (uint32_t)(o * cb + j0) * 4u) <= thrmax[o]);
-        if (__any_sync(0xffffffffu, any)) {
-          // rare path, per query: admitted products -> exact constraint
-          // thresholds for this row (cached for one query at a time) against
-          // the 16 columns' staged constraint values -> append
-#pragma unroll 1
-          for (int q = 0; q < nq; ++q) {
-            if (!((live >> q) & 1u)) continue;
-            const ScanQuery& Q = QS[q];
-            const float tq = thr_s[q * 32];
-            const int yq = yo + G.oc[q] * cb + j0;
-            bool anyq = false;
-            for (int jj = 0; jj < 16; ++jj) anyq = anyq | (sm_f[yq + jj] <= tq);
-            if (!__any_sync(0xffffffffu, anyq)) continue;
-            QCtl* ctl = Q.ctl;
-            const int nt = Q.nt;
-            if (cached_q != q) {
-              cached_q = q;
-              for (int i = 1; i < nt; ++i) {
-                const float* v = values + (int64_t)Q.test_task[i] * n_pairs;
-                double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
-                for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-                thrc[i] = Q.test_lower[i] ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
-                                          : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
-              }
-            }
-            for (int idx = (int)lane; idx < (nt - 1) * 16; idx += 32) {
-              const int i = 1 + (idx >> 4), jj = idx & 15;
-              const int col = col_base + j0 + jj;
-              float x = 0.0f;
-              if (col < (int)ncols_t) x = __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair0 + col);
-              sm_f[xo + idx] = Q.test_lower[i] ? -x : x;
-            }
-            __syncwarp();
-            const unsigned long long hbase = *(volatile unsigned long long*)&ctl->hist_base;
-            const unsigned hshift = *(volatile unsigned*)&ctl->hist_shift;
-            for (int jj = 0; jj < 16; ++jj) {
-              const float y0 = sm_f[yq + jj];
-              const int col = col_base + j0 + jj;
-              bool pass = y0 <= tq;
-              const unsigned adm = __ballot_sync(0xffffffffu, pass);
-              if (!adm) continue;
-              if (lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)__popc(adm));
-              if (pass)
-                for (int i = 1; i < nt; ++i) pass = pass && (sm_f[xo + ((i - 1) << 4) + jj] <= thrc[i]);
-              const unsigned m = __ballot_sync(0xffffffffu, pass);
-              if (m) {
-                const int leader = __ffs(m) - 1;
-                unsigned long long base = 0;
-                if ((int)lane == leader) base = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (pass) {
-                  const float x = Q.maximize ? -y0 : y0;
-                  const double val = fx(pobj[q], x, Q.test_bias[0]);
-                  Entry e;
-                  e.key = skey(Q.maximize ? val : -val);
-                  e.g = gbase + (unsigned long long)col;
-                  const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
-                  if (idx < Q.cap) Q.buf[idx] = e;
-                  const unsigned hb = hist_bin(e.key, hbase, hshift);
-                  atomicAdd(&Q.hist[hb], 1u);
-                  atomicAdd(&Q.coarse[hb >> 8], 1u);
-                }
-                if ((base >> Q.refresh_shift) != ((base + __popc(m)) >> Q.refresh_shift)) {
-                  __threadfence();
-                  refresh_tau(Q);
-                }
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-      __syncwarp();
-      bi ^= 1u;
-    }
-  }
-}
-
-// K2b for the multi-query kernel: one packed signed objective column per
-// distinct (task, direction) of a group.
-struct PackCols {
-  int ncols;
-  int _pad;
-  int task[kMaxGroupQ];
-  int lower[kMaxGroupQ];
-  float* dst[kMaxGroupQ];
-};
-
-__global__ void pack_cols_kernel(const PackCols P, const DevReaction* __restrict__ rx, const float* __restrict__ values,
-                                 int64_t n_pairs) {
-  const int o = blockIdx.z;
-  const DevReaction& R = rx[blockIdx.y];
-  const int64_t n_last = R.size[R.c - 1];
-  const float* v = values + (int64_t)P.task[o] * n_pairs + R.pair_off[R.c - 1];
-  float* dst = P.dst[o] + R.pcol_off;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_last; j += (int64_t)gridDim.x * blockDim.x) {
-    float y = __ldg(v + j);
-    if (P.lower[o]) y = -y;
-    if (y == 0.0f) y = 0.0f;
-    dst[j] = y;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Seed: exact evaluation of S sampled products (without replacement: one per
 // equal cell of [start, end), jittered inside the cell).  Feasible samples are
 // counted in seed_hist by key >> 48; the k-th best sampled key bin is a valid
@@ -2089,59 +1768,6 @@ __global__ void corner_kernel(const CornerLaunch P) {
   }
 }
 
-// Block-wide search (1024 threads) of the highest bin B with
-// sum_{b >= B} h[b] >= k.  Returns B (or -1 if the total is below k) and the
-// count at/above B in *count_ge (the total if B == -1).
-__device__ int kth_bin(const unsigned int* __restrict__ h, unsigned long long k, unsigned long long* count_ge) {
-  __shared__ unsigned long long wsum[32];
-  __shared__ int s_bin;
-  __shared__ unsigned long long s_cnt;
-  const unsigned t = threadIdx.x, lane = t & 31u, w = t >> 5;
-  constexpr int PER = kHistBins / 1024;
-  unsigned long long s = 0;
-  const uint4* h4 = reinterpret_cast<const uint4*>(h + t * PER);
-#pragma unroll 4
-  for (int i = 0; i < PER / 4; ++i) {
-    const uint4 v = __ldcg(h4 + i);
-    s += (unsigned long long)v.x + v.y + v.z + v.w;
-  }
-  unsigned long long incl = s;  // inclusive suffix sum over lanes (lane .. 31)
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned long long o = __shfl_down_sync(0xffffffffu, incl, off);
-    if (lane + off < 32) incl += o;
-  }
-  if (lane == 0) wsum[w] = incl;
-  if (t == 0) {
-    s_bin = -1;
-    s_cnt = 0;
-  }
-  __syncthreads();
-  unsigned long long above = 0, total = 0;
-  for (unsigned v = 0; v < 32; ++v) {
-    total += wsum[v];
-    if (v > w) above += wsum[v];
-  }
-  const unsigned long long suffix_incl = incl + above;   // bins >= t*PER
-  const unsigned long long suffix_excl = suffix_incl - s; // bins >= (t+1)*PER
-  if (suffix_excl < k && suffix_incl >= k) {
-    unsigned long long acc = suffix_excl;
-    for (int b = (int)(t * PER + PER - 1); b >= (int)(t * PER); --b) {
-      acc += __ldcg(h + b);
-      if (acc >= k) {
-        s_bin = b;
-        s_cnt = acc;
-        break;
-      }
-    }
-  }
-  __syncthreads();
-  const int B = s_bin;
-  *count_ge = B >= 0 ? s_cnt : total;
-  __syncthreads();
-  return B;
-}
-
 // tau from key histograms, one warp per query (two-level search).  At least k
 // distinct feasible products have key >= the returned bin's lower edge, so it
 // is a valid lower bound on the final k-th best key.
@@ -2215,35 +1841,6 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
         ctl->bound_key = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
         ctl->comp_count = cnt;  // candidates with key >= bound
       }
-    }
-  }
-}
-
-// Compact candidates with key >= bound_key into comp (order arbitrary).
-__global__ void compact_kernel(const ScanQuery* __restrict__ qs) {
-  const ScanQuery& Q = qs[blockIdx.y];
-  QCtl* ctl = Q.ctl;
-  if (!*(volatile unsigned int*)&ctl->active) return;
-  const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
-  const unsigned long long bound = *(volatile unsigned long long*)&ctl->bound_key;
-  const unsigned lane = lane_id();
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
-       base += stride) {
-    const unsigned long long i = base + lane;
-    Entry e;
-    bool keep = false;
-    if (i < n) {
-      e = Q.buf[i];
-      keep = e.key >= bound;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      unsigned long long pos = 0;
-      if ((int)lane == leader) pos = atomicAdd(&ctl->comp_count, (unsigned long long)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (keep) Q.comp[pos + __popc(m & ((1u << lane) - 1u))] = e;
     }
   }
 }
