@@ -1,0 +1,74 @@
+#!/usr/bin/env python3
+"""End-to-end latency of the public drop-in API (engine.search_topk_stream on
+mirror CslLibrary / ContributionTable / QuerySpec objects, results as
+ScoredCompound entries) for a config shape: the first call (binding: library
+descriptors, table upload, sorted lists) and warm calls.
+Usage: python tools/api_latency.py c4 [repeats]"""
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+import __graft_entry__ as g  # noqa: E402
+
+g.build()
+from paper_2510_24380_b200 import csl, engine, synth  # noqa: E402
+
+
+def mirror_objects(shape, values, biases):
+    """CslLibrary / ContributionTable mirrors of a synthetic shape: R-group r of
+    reaction t has id 1000*t + r, its synthons distinct ids; table rows follow
+    shape.pair_off (R-group-major)."""
+    reactions, rg_ids, rg_off, members = [], [], [], np.zeros(shape.n_pairs, dtype=np.int64)
+    sid = 0
+    for t, (sizes, offs) in enumerate(zip(shape.sizes, shape.pair_off)):
+        rgs = []
+        for r, (n, o) in enumerate(zip(sizes, offs)):
+            ids = tuple(range(sid, sid + int(n)))
+            sid += int(n)
+            rgs.append(csl.RgroupSpec(1000 * t + r, ids))
+            rg_ids.append(1000 * t + r)
+            rg_off.append(int(o))
+            members[int(o):int(o) + int(n)] = ids
+        reactions.append(csl.ReactionSpec(t, tuple(rgs)))
+    lib = csl.CslLibrary(tuple(reactions), tuple(csl.SynthonRecord(i, f"s{i}") for i in range(sid)))
+    order = np.argsort(rg_off)
+    table = engine.ContributionTable(values=values, biases=biases, task_names=list(synth.TASKS),
+                                     member_ids=members, rg_offsets=np.append(np.asarray(rg_off)[order], shape.n_pairs),
+                                     rg_ids=np.asarray(rg_ids)[order], fingerprint=csl.library_fingerprint(lib))
+    return lib, table
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    shape = synth.make_shape(synth.SHAPES[cfg])
+    u = synth.random_cache(shape.n_pairs, seed=1)
+    w, b = synth.random_heads(seed=1)
+    w, b = synth.calibrate_heads(shape, u, w, b, n_sample=20000, seed=1)
+    values = synth.host_table(u, w)
+    lib, table = mirror_objects(shape, values, np.asarray(b, dtype=np.float64))
+    qd = {"c1": synth.c1_query(), "c3": synth.c3_query(), "c4": synth.c4_query()}[cfg]
+    q = engine.QuerySpec(qd["objective"], qd["direction"],
+                         tuple(engine.Constraint(t, lo, hi) for t, lo, hi in qd["constraints"]), qd["k"])
+    t0 = time.perf_counter()
+    r = engine.search_topk_stream(lib, table, q)
+    first = time.perf_counter() - t0
+    warm = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = engine.search_topk_stream(lib, table, q)
+        warm.append(time.perf_counter() - t0)
+    print(json.dumps({"config": cfg, "products": shape.total, "k": q.k, "retained": r.retained,
+                      "first_call_s": first, "warm_call_ms_median": float(np.median(warm)) * 1e3,
+                      "warm_call_ms_min": float(np.min(warm)) * 1e3,
+                      "device_total_ms": r.timing.get("device_total_ms")}))
+
+
+if __name__ == "__main__":
+    main()
