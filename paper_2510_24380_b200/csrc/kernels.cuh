@@ -1492,13 +1492,24 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     }
     sthr[lane] = th0;
     int best = 0;
-    // objective range small (<= 2 quantile steps) is read off one table entry;
-    // the full count is taken only when other tests are compared with it
-    const float* q0 = S.quant + ((int64_t)Q.test_task[0] * S.n_rx + T.rx) * (kQuant + 1);
+    // the objective's exact range first (narrow in the common, seeded case);
+    // only a wide one makes the constraints compete (in quantile steps)
+    int start = 0, cnt = 0;
     int best_q = 0;
-    if (th0 == th0) {
-      const bool wide = maximize ? (__ldg(q0 + kQuant - 2) >= -th0) : (__ldg(q0 + 2) <= th0);
-      best_q = wide ? quant_count(q0, maximize != 0, maximize ? -th0 : th0) : 2;
+    if (valid && th0 == th0) {
+      if (th0 == __int_as_float(0x7f800000)) {
+        cnt = n_last;  // no threshold: every column passes the objective
+        best_q = kQuant + 1;
+      } else {
+        const int64_t base0 = (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
+        if (!maximize) {
+          cnt = first_gt(S.sx + base0, n_last, th0);
+        } else {
+          start = first_ge(S.sx + base0, n_last, -th0);
+          cnt = n_last - start;
+        }
+        best_q = n_last > 0 ? (int)(((int64_t)cnt * (kQuant + 1) + n_last - 1) / n_last) : 0;
+      }
     }
     bool cons_ready = false;
     auto constraint_thresholds = [&](bool choose) {
@@ -1524,9 +1535,12 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       cons_ready = true;
     };
     if (valid && best_q > 2 && nt > 1) constraint_thresholds(true);
-    // exact passing range of the chosen test in its sorted column
-    int start = 0, cnt = 0;
-    if (valid && best_q > 0) {
+    // exact passing range of a constraint that won (the objective's is known)
+    if (valid && best != 0) {
+      start = 0;
+      cnt = 0;
+    }
+    if (valid && best != 0 && best_q > 0) {
       const float th = sthr[best * 32 + lane];
       const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
       if (!Q.test_lower[best]) {
