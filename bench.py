@@ -448,6 +448,37 @@ def main():
                     "kernel_ms": fm, "F_per_product": F, "products": scanned,
                     "peak_basis": f"{sm_count} SMs x 128 FP32 lanes x {clk_mhz:.0f} MHz (median SM clock under load)"}
 
+    # K1 precompute (HBM-bound) at the C4 table size: u fp64
+    # [n_pairs, 64] generated on the device, one timed launch after warm-up;
+    # algorithmic bytes = 8*d*n_pairs (u) + 8*n_tasks*d (heads) + 4*n_tasks*n_pairs (table)
+    precompute = None
+    if world == 1 and not args.profile:
+        try:
+            c4 = synth.make_shape(synth.SHAPES["c4"])
+            n_p, d_, n_t = c4.n_pairs, 64, len(synth.TASKS)
+            u_dev = torch.randn((n_p, d_), dtype=torch.float64, device="cuda")
+            w_dev = torch.randn((n_t, d_), dtype=torch.float64, device="cuda") * 0.01
+            v_dev = torch.empty((n_t, n_p), dtype=torch.float32, device="cuda")
+            for _ in range(3):
+                ctx.precompute_device(u_dev.data_ptr(), n_p, d_, w_dev.data_ptr(), n_t, v_dev.data_ptr())
+            pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for e0, e1 in pe:
+                flush.zero_()
+                e0.record(stream)
+                ctx.precompute_device(u_dev.data_ptr(), n_p, d_, w_dev.data_ptr(), n_t, v_dev.data_ptr())
+                e1.record(stream)
+            torch.cuda.synchronize()
+            pms = statistics.median(s_.elapsed_time(t_) for s_, t_ in pe)
+            pbytes = 8 * d_ * n_p + 8 * n_t * d_ + 4 * n_t * n_p
+            hbm = float(peaks.get("hbm_gbs", 6550.7))
+            precompute = {"kernel": "precompute_kernel (K1, fp64 head x u dots, fp32 table)", "n_pairs": n_p, "d": d_,
+                          "n_tasks": n_t, "ms": pms, "bytes": pbytes, "achieved_GBps": pbytes / (pms * 1e-3) / 1e9,
+                          "peak_GBps": hbm, "frac": pbytes / (pms * 1e-3) / 1e9 / hbm,
+                          "peak_basis": "MEASURED_PEAKS hbm_gbs (copy bandwidth)"}
+            del u_dev, w_dev, v_dev
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal for the headline line
+            precompute = {"error": str(exc)[:200]}
+
     line = {
         "metric": "products scored/sec", "value": value, "unit": "products/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -456,7 +487,7 @@ def main():
         "config": config_dict(args, shape, queries_named, world),
         "e2e": {"value": e2e_value, "unit": "products/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                 "d2h_bytes_per_step": d2h // max(args.steps, 1), "ms_per_step": e2e_ms / args.steps},
-        "gpu_launches": launches, "roofline": roofline, "effective": effective,
+        "gpu_launches": launches, "roofline": roofline, "effective": effective, "precompute": precompute,
         "clocks": sampler.summary() if sampler else None,
     }
     if world == 1:

@@ -228,7 +228,8 @@ struct apex_ctx {
                                     // 1 = full predicate (FADD2 sign bits)
   int64_t opt_cb_admit = 512;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
-  int64_t opt_corner_mult = 16;     // corner products per reaction ~ corner_mult * k / reactions
+  int64_t opt_corner_mult = 16;
+  int64_t opt_pre_rows = 1;         // K1: row-parallel precompute kernel (0: smem-tile form)     // corner products per reaction ~ corner_mult * k / reactions
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
@@ -1397,6 +1398,22 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
   if (n_pairs < 0 || d < 1 || n_tasks < 1 || !w_dev || !values_dev || (n_pairs > 0 && !u_dev))
     return set_err(APEX_EINVAL, "bad precompute arguments");
   if (n_pairs == 0) return APEX_OK;
+  if (n_tasks <= kPvTasks && d % kPvCols == 0 && c->opt_pre_rows) {
+    // row-parallel form: every task per thread, u streamed in 16-column chunks
+    const size_t smem2 = ((size_t)((n_tasks * d + 1) & ~1) + 2 * (size_t)kPvRows * kPvLd) * sizeof(double);
+    if (smem2 <= 200 * 1024) {
+      APEX_CU(cudaFuncSetAttribute((const void*)precompute_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem2));
+      int occ2 = 0;
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)precompute_rows_kernel, kPvRows, smem2));
+      const int64_t blocks2 =
+          std::min<int64_t>((n_pairs + kPvRows - 1) / kPvRows, (int64_t)c->sm_count * std::max(occ2, 1));
+      precompute_rows_kernel<<<(unsigned)blocks2, kPvRows, smem2, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks,
+                                                                              values_dev);
+      APEX_CU(cudaGetLastError());
+      return APEX_OK;
+    }
+  }
   const size_t smem = ((size_t)n_tasks * d + (size_t)kPreRows * (d + 1)) * sizeof(double);
   if (smem > 220 * 1024) return set_err(APEX_ELIMIT, "precompute: n_tasks * d too large for shared memory");
   APEX_CU(cudaFuncSetAttribute((const void*)precompute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1754,6 +1771,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "force_upload") c->opt_force_upload = v;
   else if (n == "refresh") c->opt_refresh = v;
   else if (n == "corner") c->opt_corner = v;
+  else if (n == "pre_rows") c->opt_pre_rows = v;
   else if (n == "corner_mult") c->opt_corner_mult = std::max<int64_t>(1, v);
   else if (n == "vote64") c->opt_vote64 = v;
   else if (n == "dense") c->opt_dense = v;

@@ -155,6 +155,71 @@ __global__ void __launch_bounds__(256) precompute_kernel(const double* __restric
 }
 
 
+// K1, row-parallel form (n_tasks <= 16, d a multiple of 16): one thread per
+// pair row computes every task's dot (16 independent FMA chains), u streamed
+// through shared memory in 16-column chunks with the next chunk's loads in
+// flight during the current chunk's FMAs (coalesced 8-byte loads, double
+// buffered), the heads read as broadcast 16-byte shared loads.  Per (task,
+// row) the accumulation order is the same as precompute_kernel's (c = 0..d-1).
+constexpr int kPvRows = 128, kPvCols = 16, kPvTasks = 16, kPvLd = kPvCols + 2;
+__global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* __restrict__ u, int64_t n_pairs, int d,
+                                                                  const double* __restrict__ head_w, int n_tasks,
+                                                                  float* __restrict__ values) {
+  extern __shared__ __align__(16) double pv[];
+  double* w_s = pv;                                   // [n_tasks][d]
+  double* u_s = pv + ((n_tasks * d + 1) & ~1);        // [2][kPvRows][kPvLd], 16-B aligned rows
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n_tasks * d; i += blockDim.x) w_s[i] = head_w[i];
+  for (int64_t base = (int64_t)blockIdx.x * kPvRows; base < n_pairs; base += (int64_t)gridDim.x * kPvRows) {
+    const int rows = (int)(n_pairs - base < kPvRows ? n_pairs - base : kPvRows);
+    double acc[kPvTasks];
+#pragma unroll
+    for (int t = 0; t < kPvTasks; ++t) acc[t] = 0.0;
+    double pf[kPvCols];
+    // chunk element e = tid + kPvRows * k: row e / kPvCols, column e % kPvCols
+#pragma unroll
+    for (int k = 0; k < kPvCols; ++k) {
+      const int e = tid + kPvRows * k, r = e / kPvCols, col = e % kPvCols;
+      pf[k] = r < rows ? __ldg(u + (base + r) * d + col) : 0.0;
+    }
+    for (int c0 = 0, b = 0; c0 < d; c0 += kPvCols, b ^= 1) {
+      double* ub = u_s + b * kPvRows * kPvLd;
+      __syncthreads();  // the buffer's previous chunk has been consumed
+#pragma unroll
+      for (int k = 0; k < kPvCols; ++k) {
+        const int e = tid + kPvRows * k, r = e / kPvCols, col = e % kPvCols;
+        ub[r * kPvLd + col] = pf[k];
+      }
+      __syncthreads();
+      if (c0 + kPvCols < d) {
+#pragma unroll
+        for (int k = 0; k < kPvCols; ++k) {
+          const int e = tid + kPvRows * k, r = e / kPvCols, col = e % kPvCols;
+          pf[k] = r < rows ? __ldg(u + (base + r) * d + c0 + kPvCols + col) : 0.0;
+        }
+      }
+      const double* ur = ub + tid * kPvLd;
+#pragma unroll
+      for (int cc = 0; cc < kPvCols; cc += 2) {
+        const double2 uv = *reinterpret_cast<const double2*>(ur + cc);
+#pragma unroll
+        for (int t = 0; t < kPvTasks; ++t) {
+          if (t < n_tasks) {
+            const double2 wv = *reinterpret_cast<const double2*>(w_s + t * d + c0 + cc);
+            acc[t] = __fma_rn(wv.x, uv.x, acc[t]);
+            acc[t] = __fma_rn(wv.y, uv.y, acc[t]);
+          }
+        }
+      }
+    }
+    if (tid < rows) {
+#pragma unroll
+      for (int t = 0; t < kPvTasks; ++t)
+        if (t < n_tasks) values[(int64_t)t * n_pairs + base + tid] = __double2float_rn(acc[t]);
+    }
+  }
+}
+
 // 64-bit division with a 32-bit fast path (operands below 2^32)
 __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n, uint64_t d) {
   if ((n >> 32) == 0 && (d >> 32) == 0) {
