@@ -471,7 +471,7 @@ def main():
             pms = statistics.median(s_.elapsed_time(t_) for s_, t_ in pe)
             pbytes = 8 * d_ * n_p + 8 * n_t * d_ + 4 * n_t * n_p
             hbm = float(peaks.get("hbm_gbs", 6550.7))
-            precompute = {"kernel": "precompute_kernel (K1, fp64 head x u dots, fp32 table)", "n_pairs": n_p, "d": d_,
+            precompute = {"kernel": "precompute_rows_kernel<11,64> (K1, fp64 head x u dots, fp32 table)", "n_pairs": n_p, "d": d_,
                           "n_tasks": n_t, "ms": pms, "bytes": pbytes, "achieved_GBps": pbytes / (pms * 1e-3) / 1e9,
                           "peak_GBps": hbm, "frac": pbytes / (pms * 1e-3) / 1e9 / hbm,
                           "peak_basis": "MEASURED_PEAKS hbm_gbs (copy bandwidth)"}

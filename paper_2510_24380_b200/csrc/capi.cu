@@ -1402,14 +1402,14 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
     // row-parallel form: every task per thread, u streamed in 16-column chunks
     const size_t smem2 = ((size_t)((n_tasks * d + 1) & ~1) + 2 * (size_t)kPvRows * kPvLd) * sizeof(double);
     if (smem2 <= 200 * 1024) {
-      APEX_CU(cudaFuncSetAttribute((const void*)precompute_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem2));
+      using PFn = void (*)(const double*, int64_t, int, const double*, int, float*);
+      const PFn fn = (n_tasks == 11 && d == 64) ? precompute_rows_kernel<11, 64> : precompute_rows_kernel<0, 0>;
+      APEX_CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       int occ2 = 0;
-      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)precompute_rows_kernel, kPvRows, smem2));
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)fn, kPvRows, smem2));
       const int64_t blocks2 =
           std::min<int64_t>((n_pairs + kPvRows - 1) / kPvRows, (int64_t)c->sm_count * std::max(occ2, 1));
-      precompute_rows_kernel<<<(unsigned)blocks2, kPvRows, smem2, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks,
-                                                                              values_dev);
+      fn<<<(unsigned)blocks2, kPvRows, smem2, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks, values_dev);
       APEX_CU(cudaGetLastError());
       return APEX_OK;
     }

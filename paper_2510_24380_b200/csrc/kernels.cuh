@@ -162,9 +162,15 @@ __global__ void __launch_bounds__(256) precompute_kernel(const double* __restric
 // buffered), the heads read as broadcast 16-byte shared loads.  Per (task,
 // row) the accumulation order is the same as precompute_kernel's (c = 0..d-1).
 constexpr int kPvRows = 128, kPvCols = 16, kPvTasks = 16, kPvLd = kPvCols + 2;
-__global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* __restrict__ u, int64_t n_pairs, int d,
-                                                                  const double* __restrict__ head_w, int n_tasks,
+// NT / D > 0: compile-time task count and width (the APEX model: 11 x 64), so
+// no lane work is predicated off and every head offset is an immediate
+template <int NT, int D>
+__global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* __restrict__ u, int64_t n_pairs, int d_rt,
+                                                                  const double* __restrict__ head_w, int n_tasks_rt,
                                                                   float* __restrict__ values) {
+  const int d = D > 0 ? D : d_rt;
+  const int n_tasks = NT > 0 ? NT : n_tasks_rt;
+  constexpr int TMAX = NT > 0 ? NT : kPvTasks;
   extern __shared__ __align__(16) double pv[];
   double* w_s = pv;                                   // [n_tasks][d]
   double* u_s = pv + ((n_tasks * d + 1) & ~1);        // [2][kPvRows][kPvLd], 16-B aligned rows
@@ -172,9 +178,9 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
   for (int i = tid; i < n_tasks * d; i += blockDim.x) w_s[i] = head_w[i];
   for (int64_t base = (int64_t)blockIdx.x * kPvRows; base < n_pairs; base += (int64_t)gridDim.x * kPvRows) {
     const int rows = (int)(n_pairs - base < kPvRows ? n_pairs - base : kPvRows);
-    double acc[kPvTasks];
+    double acc[TMAX];
 #pragma unroll
-    for (int t = 0; t < kPvTasks; ++t) acc[t] = 0.0;
+    for (int t = 0; t < TMAX; ++t) acc[t] = 0.0;
     double pf[kPvCols];
     // chunk element e = tid + kPvRows * k: row e / kPvCols, column e % kPvCols
 #pragma unroll
@@ -203,8 +209,8 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
       for (int cc = 0; cc < kPvCols; cc += 2) {
         const double2 uv = *reinterpret_cast<const double2*>(ur + cc);
 #pragma unroll
-        for (int t = 0; t < kPvTasks; ++t) {
-          if (t < n_tasks) {
+        for (int t = 0; t < TMAX; ++t) {
+          if (NT > 0 || t < n_tasks) {
             const double2 wv = *reinterpret_cast<const double2*>(w_s + t * d + c0 + cc);
             acc[t] = __fma_rn(wv.x, uv.x, acc[t]);
             acc[t] = __fma_rn(wv.y, uv.y, acc[t]);
@@ -214,8 +220,8 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
     }
     if (tid < rows) {
 #pragma unroll
-      for (int t = 0; t < kPvTasks; ++t)
-        if (t < n_tasks) values[(int64_t)t * n_pairs + base + tid] = __double2float_rn(acc[t]);
+      for (int t = 0; t < TMAX; ++t)
+        if (NT > 0 || t < n_tasks) values[(int64_t)t * n_pairs + base + tid] = __double2float_rn(acc[t]);
     }
   }
 }
