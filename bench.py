@@ -334,6 +334,9 @@ def main():
         counts, st = ctx.query_local(nqueries, local_buf.data_ptr())
         gathered = all_gather_entries(local_buf)
         res, st2 = ctx.merge_finalize_batch(gqueries, gathered.data_ptr(), world, k, shape.total, merge_prepared)
+        step_multi.h2d = st["h2d_bytes"]
+        step_multi.scan_ms = st["scan_kernel_ms"]
+        step_multi.d2h = st2["d2h_bytes"]
         return st["kernel_launches"] + st2["kernel_launches"], res
 
     # warmup
@@ -390,6 +393,9 @@ def main():
             d2h += st["d2h_bytes"]
         else:
             _, res_multi = step_multi()
+            h2d += step_multi.h2d
+            d2h += step_multi.d2h
+            scan_ms.append(step_multi.scan_ms)
         e2e_ev[i][1].record(stream)
     torch.cuda.synchronize()
     e2e_ms = sum(s.elapsed_time(t) for s, t in e2e_ev)
