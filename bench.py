@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks, no baselines)")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (5e9-product) roofline and effective passes")
     return ap.parse_args()
 
 
@@ -454,6 +455,45 @@ def main():
                     "kernel_ms": fm, "F_per_product": F, "products": scanned,
                     "peak_basis": f"{sm_count} SMs x 128 FP32 lanes x {clk_mhz:.0f} MHz (median SM clock under load)"}
 
+    # the SURVEY's roofline reference point: the C4 query over the ~5e9-product
+    # library (F = 15 per product), full-predicate pass (mode 0) and the
+    # default sorted-column pass, on a second context with that table resident
+    roofline_c4 = effective_c4 = None
+    if world == 1 and not args.profile and not args.no_c4 and args.config != "c4":
+        try:
+            c4shape, c4q = workload("c4", 1)
+            u4, w4, b4 = build_model(c4shape)
+            ctx4 = _native.DeviceContext(local, stream.cuda_stream)
+            ctx4.load_library(c4shape.sizes, c4shape.pair_off, c4shape.g_offsets(), c4shape.n_pairs)
+            ctx4.load_cache(u4, w4, b4, want_values=False)
+            del u4
+            q4 = [synth.to_native(q, 0, c4shape.total) for q in c4q]
+            F4 = f_ops(c4q)
+            pb4 = ctx4.prepare_views(q4)
+            times = {}
+            for mode in (0, 3):
+                ctx4.set_option("mode", mode)
+                ctx4.run_views(pb4)
+                ms4 = []
+                for _ in range(3):
+                    flush.zero_()
+                    _, st4 = ctx4.run_views(pb4)
+                    ms4.append(st4["scan_kernel_ms"])
+                times[mode] = statistics.median(ms4)
+            ach4 = c4shape.total * F4 / (times[0] * 1e-3) / 1e12
+            roofline_c4 = {"bound": "fp32", "achieved": ach4, "peak": peak_tops, "unit": "TFLOP/s",
+                           "frac": ach4 / peak_tops, "kernel": "scan_kernel<NT,1,0> full predicate (mode 0)",
+                           "kernel_ms": times[0], "F_per_product": F4, "products": c4shape.total,
+                           "workload": "c4: one query (5 property windows, k=10000) over the synthetic "
+                                       f"{c4shape.total / 1e9:.2f}e9-product CSL"}
+            eq4 = c4shape.total * F4 / (times[3] * 1e-3) / 1e12
+            effective_c4 = {"products_per_s": c4shape.total / (times[3] * 1e-3), "kernel_ms": times[3],
+                            "F_equivalent_tops": eq4, "frac_equivalent": eq4 / peak_tops,
+                            "kernel": "scan_sorted_kernel"}
+            ctx4.close()
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal for the headline line
+            roofline_c4 = {"error": str(exc)[:200]}
+
     # K1 precompute (HBM-bound) at the C4 table size: u fp64
     # [n_pairs, 64] generated on the device, one timed launch after warm-up;
     # algorithmic bytes = 8*d*n_pairs (u) + 8*n_tasks*d (heads) + 4*n_tasks*n_pairs (table)
@@ -493,7 +533,8 @@ def main():
         "config": config_dict(args, shape, queries_named, world),
         "e2e": {"value": e2e_value, "unit": "products/s", "h2d_bytes_per_step": h2d // max(args.steps, 1),
                 "d2h_bytes_per_step": d2h // max(args.steps, 1), "ms_per_step": e2e_ms / args.steps},
-        "gpu_launches": launches, "roofline": roofline, "effective": effective, "precompute": precompute,
+        "gpu_launches": launches, "roofline": roofline, "effective": effective, "roofline_c4": roofline_c4,
+        "effective_c4": effective_c4, "precompute": precompute,
         "clocks": sampler.summary() if sampler else None,
     }
     if world == 1:
