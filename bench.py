@@ -481,8 +481,14 @@ def main():
                     ms4.append(st4["scan_kernel_ms"])
                 times[mode] = statistics.median(ms4)
             ach4 = c4shape.total * F4 / (times[0] * 1e-3) / 1e12
+            tr4 = None
+            try:
+                tr4 = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get("c4")
+            except Exception:
+                pass
             roofline_c4 = {"bound": "fp32", "achieved": ach4, "peak": peak_tops, "unit": "TFLOP/s",
-                           "frac": ach4 / peak_tops, "kernel": "scan_kernel<NT,1,0> full predicate (mode 0)",
+                           "frac": ach4 / peak_tops, "traffic": tr4,
+                           "kernel": "scan_kernel<NT,1,0> full predicate (mode 0)",
                            "kernel_ms": times[0], "F_per_product": F4, "products": c4shape.total,
                            "workload": "c4: one query (5 property windows, k=10000) over the synthetic "
                                        f"{c4shape.total / 1e9:.2f}e9-product CSL"}
