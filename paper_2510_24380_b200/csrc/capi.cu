@@ -954,6 +954,9 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
           ++st.scans;
         }
       }
+      // full-predicate launches per test class alternate between the main and
+      // the side stream so consecutive classes overlap (disjoint queries)
+      int n_full_launch = 0;
       for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
         if (sorted_all) {
           bool need = false;  // only unconstrained queries can end up in the full-predicate kernel
@@ -974,11 +977,24 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
           Lc.queries = dq + q0;
           Lc.nq = nql;
           Lc.work = c->d_work.as<unsigned>() + (wi++ % 64);
-          fn<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(Lc);
+          cudaStream_t ls = s;
+          if (n_full_launch % 2 == 1) {
+            if (n_full_launch == 1) {
+              APEX_CU(cudaEventRecord(c->fork_ev, s));
+              APEX_CU(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+            }
+            ls = c->side;
+          }
+          ++n_full_launch;
+          fn<<<(unsigned)blocks, kScanWarps * 32, smem, ls>>>(Lc);
           APEX_CU(cudaGetLastError());
           ++st.launches;
           ++st.scans;
         }
+      }
+      if (n_full_launch > 1) {
+        APEX_CU(cudaEventRecord(c->join_ev, c->side));
+        APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
       }
       if (ci + 1 < bounds.size()) {
         tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 1);  // raise tau from the candidates so far
