@@ -702,7 +702,7 @@ cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
 // through the cooperative radix select (launched over chunks of queries that
 // fit co-resident), rank, scatter and (finalize) materialization.
 int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool finalize, RunStats& st,
-                   cudaStream_t s, bool mark) {
+                   cudaStream_t s, bool mark, bool compute_bound = true) {
   MatLaunch M;
   M.queries = dq;
   M.rx = c->d_rx.as<DevReaction>();
@@ -719,7 +719,7 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
                                    (int)smem_small));
       attr_small = true;
     }
-    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, finalize ? 1 : 0);
+    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, finalize ? 1 : 0, compute_bound ? 1 : 0);
     ++st.launches;
   }
   {
@@ -1005,9 +1005,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   }
   APEX_CU(stage_mark(c, 7, s));
   APEX_CU(stage_mark(c, 3, s));
-  // final bound, compaction, exact select
-  tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 2);
-  ++st.launches;
+  // final bound (inside the small-set finalize), exact select
   APEX_TRY(enqueue_select(c, dq, nq, B.k_max, B.finalize, st, s, true));
   APEX_CU(cudaGetLastError());
   APEX_CU(stage_mark(c, 5, s));
@@ -1740,7 +1738,7 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
   }
   st.launches = 2;
   // bound_key = 0 (init): every loaded entry is a candidate
-  APEX_TRY(enqueue_select(c, dq, nq, k_max, true, st, s, false));
+  APEX_TRY(enqueue_select(c, dq, nq, k_max, true, st, s, false, false));
   APEX_CU(cudaGetLastError());
   APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
                             cudaMemcpyDeviceToHost, s));

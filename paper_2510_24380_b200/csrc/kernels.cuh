@@ -2169,11 +2169,32 @@ __global__ void materialize_kernel(const MatLaunch M) {
 // path) materialize them — replacing select + rank + scatter + materialize.
 constexpr int kSmallSel = 8192;
 
-__global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M, int materialize) {
+__global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M, int materialize, int compute_bound) {
   const ScanQuery& Q = M.queries[blockIdx.x];
   QCtl* ctl = Q.ctl;
   if (!*(volatile unsigned int*)&ctl->active) return;
-  const unsigned long long n_valid = *(volatile unsigned long long*)&ctl->comp_count;
+  // final bound first (tau_kernel mode 2, folded in: warp 0): the k-th best
+  // candidate bin's lower edge and the count at/above it, for this kernel and
+  // for the large path that follows
+  __shared__ unsigned long long s_bound, s_valid;
+  if (!compute_bound) {  // bound and count preset (multi-GPU merge: every entry is a candidate)
+    if (threadIdx.x == 0) {
+      s_bound = *(volatile unsigned long long*)&ctl->bound_key;
+      s_valid = *(volatile unsigned long long*)&ctl->comp_count;
+    }
+  } else if (threadIdx.x < 32) {
+    unsigned long long cnt_ge = 0;
+    const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, &cnt_ge);
+    if (threadIdx.x == 0) {
+      const unsigned long long bound = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
+      ctl->bound_key = bound;
+      ctl->comp_count = cnt_ge;
+      s_bound = bound;
+      s_valid = cnt_ge;
+    }
+  }
+  __syncthreads();
+  const unsigned long long n_valid = s_valid;
   if (n_valid > (unsigned long long)kSmallSel) return;  // large path
   extern __shared__ __align__(16) unsigned char sm_e[];
   Entry* es = reinterpret_cast<Entry*>(sm_e);
@@ -2182,7 +2203,7 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
   if (tid == 0) cnt = 0;
   __syncthreads();
   const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
-  const unsigned long long bound = *(volatile unsigned long long*)&ctl->bound_key;
+  const unsigned long long bound = s_bound;
   for (unsigned long long i = tid; i < n; i += blockDim.x) {
     const Entry e = Q.buf[i];
     if (e.key >= bound) {
