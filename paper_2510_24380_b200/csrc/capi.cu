@@ -155,6 +155,8 @@ struct Batch {
   int64_t k_max = 0;
   bool finalize = false;
   bool copy_out = false;       // result rows D2H inside the pass (synchronous apex_query)
+  bool no_full = false;        // this signature needed no full-predicate kernel last time: skip its launches
+  uint64_t key0 = 0;           // signature before no_full (history key)
   Plan* plan = nullptr;
   Plan* plan_rows = nullptr;    // whole-row tiles (sorted-column admission kernel)
   bool pending = false;
@@ -199,6 +201,8 @@ struct apex_ctx {
   DBuf d_hists;                          // per-query histograms, contiguous (one memset per batch)
   DBuf d_ctls;                           // per-query control blocks, contiguous (one strided D2H of the headers)
   bool copy_next = false;                // next prepare_batch: result D2H inside the pass
+  std::vector<uint64_t> seen_keys;       // recent batch signatures (graph capture on the second sighting)
+  std::vector<uint64_t> nofull_keys;     // signatures whose last run sent no query to the full predicate
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   DBuf d_work;                           // flattened-work counters of the scan launches
@@ -768,15 +772,12 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   }
   // kernel choice: admission-first (admit), full predicate (full), or per query (auto)
   const bool admit = c->opt_mode >= 2;
-  // the sorted-column kernel takes every query that has a constraint (it
-  // enumerates the most selective test's range per row); in auto mode the
-  // full-predicate kernel is only needed for unconstrained queries left
-  // without a seeded threshold
-  bool any_uncons = false;
-  for (int i = 0; i < nq; ++i) any_uncons = any_uncons || B.qs[i].n_constraints == 0;
+  // the sorted-column kernel takes every query except (auto, on the device)
+  // threshold-less ones with a non-sparse feasible set, which stream the
+  // full predicate; signatures that needed none of those skip its launches
   const bool sorted_all = c->opt_mode == 3 && B.plan_rows;
-  const bool full = c->opt_mode != 2 && (!sorted_all || any_uncons);
-  const int autok = (c->opt_mode == 3 && !tau0) ? (sorted_all ? 2 : 1) : 0;
+  const bool full = c->opt_mode != 2 && !B.no_full;
+  const int autok = (c->opt_mode == 3 && !tau0) ? (B.no_full ? 3 : sorted_all ? 2 : 1) : 0;
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
@@ -794,6 +795,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   APEX_CU(stage_mark(c, 1, s));
   // seed threshold from exact samples (uniform samples on the main stream,
   // the corner on the side stream: independent, they overlap)
+  uint64_t S_used = 0;
   if (!tau0) {
     const bool corner = c->opt_corner && c->corners_ok;
     if (corner) {
@@ -803,6 +805,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
     uint64_t S = c->opt_samples > 0 ? (uint64_t)c->opt_samples
                                      : (uint64_t)std::min<int64_t>(1 << 15, std::max<int64_t>(1 << 11, 2 * B.k_max));
     S = std::min<uint64_t>(S, std::max<uint64_t>(span / 32, std::min<uint64_t>(span, 4096)));
+    S_used = S;
     if (S > 0) {
       SampleLaunch P;
       P.queries = dq;
@@ -844,7 +847,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
     }
     {
-      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok);
+      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used);
       ++st.launches;
     }
   }
@@ -958,11 +961,6 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
       // the side stream so consecutive classes overlap (disjoint queries)
       int n_full_launch = 0;
       for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
-        if (sorted_all) {
-          bool need = false;  // only unconstrained queries can end up in the full-predicate kernel
-          for (int q = B.cls_begin[k]; q < B.cls_begin[k + 1]; ++q) need = need || B.qs[q].n_constraints == 0;
-          if (!need) continue;
-        }
         ScanFn fn = pick_scan(B.cls_nt[k], B.rl, c->opt_mode == 1 ? 1 : 0);
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
@@ -1065,6 +1063,14 @@ int check_batch(apex_ctx* c) {
     APEX_TRY(enqueue_batch(c, tau0.data()));
   }
   B.pending = false;
+  if (!B.no_full && c->opt_mode == 3 && B.plan_rows) {
+    bool any_full = false;
+    for (int i = 0; i < nq; ++i) any_full = any_full || c->h_ctl.as<QCtl>()[i].use_full;
+    if (!any_full && std::find(c->nofull_keys.begin(), c->nofull_keys.end(), B.key0) == c->nofull_keys.end()) {
+      if (c->nofull_keys.size() >= 64) c->nofull_keys.erase(c->nofull_keys.begin());
+      c->nofull_keys.push_back(B.key0);
+    }
+  }
   // (stage times are informational: never fail the query on them)
   for (int e = 0; e < 5; ++e)
     if (cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]) != cudaSuccess) B.st.ms[e] = 0.f;
@@ -1085,6 +1091,7 @@ uint64_t batch_key(const apex_ctx* c) {
   mix(&B.nq, sizeof(B.nq));
   mix(&B.finalize, sizeof(B.finalize));
   mix(&B.copy_out, sizeof(B.copy_out));
+  mix(&B.no_full, sizeof(B.no_full));
   for (int i = 0; i < B.nq; ++i) {
     const apex_query_spec& q = B.qs[i];
     mix(&q.objective_task, sizeof(q.objective_task));
@@ -1109,6 +1116,14 @@ uint64_t batch_key(const apex_ctx* c) {
 // signature repeats, otherwise capture it (or launch directly if capture is
 // unavailable).  One graph launch replaces ~30 kernel/memset/memcpy launches.
 int launch_batch(apex_ctx* c) {
+  // full-predicate launches are skipped for a signature whose previous run
+  // sent no query there (the device then never picks that kernel; every query
+  // stays exact in the sorted-column kernel either way)
+  Batch& Bq = c->batch;
+  Bq.no_full = false;
+  Bq.key0 = batch_key(c);
+  Bq.no_full = c->opt_mode == 3 && Bq.plan_rows &&
+               std::find(c->nofull_keys.begin(), c->nofull_keys.end(), Bq.key0) != c->nofull_keys.end();
   if (!c->opt_graph || c->graph_broken) return enqueue_batch(c, nullptr);
   const uint64_t key = batch_key(c);
   if (c->gexec && key == c->gkey) {
@@ -1116,6 +1131,14 @@ int launch_batch(apex_ctx* c) {
     c->batch.pending = true;
     c->batch.st = c->graph_stats;  // launch counts / bytes as captured
     return APEX_OK;
+  }
+  // capture (and pay the instantiation) only for a batch signature seen
+  // before: a stream of distinct one-off queries launches directly
+  auto seen = std::find(c->seen_keys.begin(), c->seen_keys.end(), key);
+  if (seen == c->seen_keys.end()) {
+    if (c->seen_keys.size() >= 32) c->seen_keys.erase(c->seen_keys.begin());
+    c->seen_keys.push_back(key);
+    return enqueue_batch(c, nullptr);
   }
   if (c->gexec) {
     cudaGraphExecDestroy(c->gexec);

@@ -1862,7 +1862,8 @@ __global__ void corner_kernel(const CornerLaunch P) {
 //           seed_max] spread over ~1/4 of its bins;
 //   mode 1: raise tau from the candidate histogram;
 //   mode 2: final bound (and the count at/above it) for the select.
-__global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, int auto_kernel = 0) {
+__global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, int auto_kernel = 0,
+                           unsigned long long samples = 0) {
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const ScanQuery& Q = qs[q];
@@ -1911,7 +1912,13 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
       // test per row, so only an unconstrained query without a threshold
       // needs the full predicate)
       if (auto_kernel == 1) ctl->use_full = ctl->tau_key == kNoTau ? 1u : 0u;
-      if (auto_kernel == 2) ctl->use_full = (ctl->tau_key == kNoTau && Q.nt == 1) ? 1u : 0u;
+      // (auto 2 keeps the full predicate for threshold-less queries whose
+      // feasible set is not sparse — the uniform samples found more than
+      // 1/512 feasible: there the streaming full predicate beats enumerating
+      // broad sorted ranges; sparse ones (e.g. Astex RO3) take the sorted kernel)
+      if (auto_kernel == 2)
+        ctl->use_full = (ctl->tau_key == kNoTau && (Q.nt == 1 || a0 * 512ull > samples)) ? 1u : 0u;
+      if (auto_kernel == 3) ctl->use_full = 0u;  // no full-predicate launch in this pass
     }
   } else {
     const int B = kth_two_level(Q.hist, Q.coarse, k, &cnt);

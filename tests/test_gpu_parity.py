@@ -381,6 +381,25 @@ def test_result_views_equal_copies(native):
         ctx.run_views(ctx.prepare_views([qs[0], dict(qs[1], start=0)]))
 
 
+@pytest.mark.parametrize("seed", [31, 32])
+def test_repeated_batches_identical(native, seed):
+    """A batch signature runs directly, then is captured as a graph, then
+    replayed (and, when no query needed the full predicate, without those
+    launches): every run returns the oracle's result."""
+    from oracle import scan_oracle as orc
+
+    sizes, pair_off, n_pairs, values, biases, rng = _random_case(seed)
+    ctx, lib = _ctx(native, sizes, pair_off, n_pairs, values, biases)
+    qs = [orc.Query(1, False, [(0, -1.0, 1.0)], 50), orc.Query(2, True, [], 20),
+          orc.Query(0, False, [(2, -0.3, 0.3), (3, -2.0, 2.0)], 300), orc.Query(3, True, [], 10 ** 6)]
+    spec = [{"obj": q.obj, "maximize": q.maximize, "cons": q.cons, "k": q.k, "start": 0, "end": lib.total} for q in qs]
+    for _ in range(4):
+        res, _ = ctx.query(spec)
+        for r, q in zip(res, qs):
+            _check_against_oracle(r, values, biases, lib, q, 0, lib.total)
+    ctx.close()
+
+
 def test_c1_shape_vs_oracle(native):
     """Config-1 shape (10M products, random-init heads, calibrated properties)
     against the oracle for the config-1 query and one preset query."""

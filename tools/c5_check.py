@@ -41,7 +41,7 @@ def main():
     pbs = [ctx.prepare([q]) for q in qs] if single else []
     for pb in pbs[:5]:
         ctx.run(pb)
-    lat, single, full, kern, cand = [], [], [], [], []
+    lat, single, full, kern, cand, tot = [], [], [], [], [], []
     for pb in pbs:
         t0 = time.perf_counter()
         r, st1 = ctx.run(pb)
@@ -49,8 +49,10 @@ def main():
         single.append((r[0]["g"].copy(), r[0]["objective"].copy()))
         full.append(r[0]["full_predicate"])
         kern.append(st1["scan_kernel_ms"])
+        tot.append(st1["total_ms"])
         cand.append(st1["candidates"])
     lat, full, kern = np.array(lat or [0.0]), np.array(full or [False], dtype=bool), np.array(kern or [0.0])
+    tot = np.array(tot)
     # batched: all queries in one pass
     pb = ctx.prepare(qs)
     ctx.run(pb)
@@ -71,7 +73,10 @@ def main():
         "full_predicate_queries": int(full.sum()),
         "scan_kernel_ms_mean": {"admission": float(kern[~full].mean()) if (~full).any() else None,
                                 "full": float(kern[full].mean()) if full.any() else None},
-        "retries_batched": st["retries"], "candidates_mean": float(np.mean(cand))}))
+        "retries_batched": st["retries"], "candidates_mean": float(np.mean(cand)),
+        "scan_kernel_ms_p50": float(np.percentile(kern, 50)), "scan_kernel_ms_p99": float(np.percentile(kern, 99)),
+        "device_total_ms_p50": float(np.percentile(tot, 50)) if len(tot) else None,
+        "host_ms_p50": float(np.percentile(lat - tot, 50)) if len(tot) == len(lat) else None}))
 
 
 if __name__ == "__main__":
