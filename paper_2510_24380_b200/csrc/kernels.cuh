@@ -1483,7 +1483,17 @@ __device__ __forceinline__ int first_ge(const float* __restrict__ xs, int n, flo
 // column: upper tests pass x <= t, lower tests pass x >= t.  Used only to pick
 // which test's exact range to enumerate.
 __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool lower, float t) {
-  int lo = 0, hi = kQuant + 1;  // first index failing the monotone predicate
+  // the two ends first (independent loads): most tests pass nothing or
+  // everything of a row and need no search
+  const float q_lo = __ldg(q), q_hi = __ldg(q + kQuant);
+  if (!lower) {
+    if (!(q_lo <= t)) return 0;
+    if (q_hi <= t) return kQuant + 1;
+  } else {
+    if (!(q_hi >= t)) return 0;
+    if (q_lo >= t) return kQuant + 1;
+  }
+  int lo = 1, hi = kQuant;  // first index failing the monotone predicate, in [1, kQuant]
   if (!lower) {
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
