@@ -104,9 +104,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, obj_col, buf, comp, sel, sorted, rank;
+  DBuf packed, obj_col, buf, comp, sel, sorted;
   void release() {
-    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted, &rank}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted}) b->release();
   }
 };
 
@@ -612,7 +612,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
-    APEX_TRY(S.rank.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(unsigned)));
   }
   APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
   c->out_off.assign(nq + 1, 0);
@@ -638,7 +637,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.comp = S.comp.as<Entry>();
     Q.sel = S.sel.as<Entry>();
     Q.sorted = S.sorted.as<Entry>();
-    Q.rank = S.rank.as<unsigned>();
     Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
     Q.coarse = Q.hist + kHistBins;
     Q.seed_hist = Q.coarse + 256;
@@ -744,9 +742,8 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
   if (mark) APEX_CU(stage_mark(c, 4, s));
   if (finalize) {
     const int ib = (int)((k_max + 255) / 256);
-    const int js = (int)std::max<int64_t>(1, std::min<int64_t>(ib, (2 * c->sm_count + ib * nq - 1) / (ib * nq)));
-    rank_kernel<<<dim3(ib, js, nq), 256, 0, s>>>(dq, js);
-    scatter_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+    sort_chunks_kernel<<<dim3((unsigned)((k_max + kSortChunk - 1) / kSortChunk), nq), 1024, 0, s>>>(dq);
+    merge_rank_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
     materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
     st.launches += 3;
   }
@@ -1708,7 +1705,6 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
     APEX_TRY(S.comp.ensure(sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
-    APEX_TRY(S.rank.ensure((size_t)k * sizeof(unsigned)));
   }
   APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
   APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
@@ -1734,7 +1730,6 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
     Q.comp = S.comp.as<Entry>();
     Q.sel = S.sel.as<Entry>();
     Q.sorted = S.sorted.as<Entry>();
-    Q.rank = S.rank.as<unsigned>();
     Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
     Q.coarse = Q.hist + kHistBins;
     Q.seed_hist = Q.coarse + 256;

@@ -106,7 +106,6 @@ struct ScanQuery {
   Entry* comp;                    // compacted candidates (cap entries)
   Entry* sel;                     // selected top-k (k entries, unordered)
   Entry* sorted;                  // best-first (k entries)
-  unsigned int* rank;             // [k]
   unsigned int* hist;             // [kHistBins] histogram of appended keys (key >> 48)
   unsigned int* coarse;           // [256] histogram of appended keys (key >> 56)
   unsigned int* seed_hist;        // [kHistBins] histogram of feasible sampled keys

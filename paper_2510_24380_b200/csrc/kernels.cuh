@@ -1710,6 +1710,17 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   return x;
 }
 
+// Warp-aggregated histogram increment (the whole warp calls it, converged):
+// lanes with on == true and the same bin add once, by their lowest lane.
+// Seed products of one warp mostly share bins (16-bit key prefixes of
+// near-equal top values), so this removes most same-address atomics.
+__device__ __forceinline__ void hist_add_warp(unsigned int* h, unsigned bin, bool on) {
+  const unsigned am = __ballot_sync(0xffffffffu, on);
+  if (!on) return;
+  const unsigned peers = __match_any_sync(am, bin);
+  if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
+}
+
 __global__ void sample_kernel(const SampleLaunch P, int nq) {
   // grid.y = query: every query evaluates the same sampled products (the
   // decode is repeated per query, it is ALU-only); each test's fp64 sum is
@@ -1761,12 +1772,10 @@ __global__ void sample_kernel(const SampleLaunch P, int nq) {
         if (t == 0) vobj = val;
         else feasible = feasible && (Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]));
       }
-      if (feasible) {
-        key = skey(Q.maximize ? vobj : -vobj);
-        atomicAdd(&Q.seed_hist[key >> 48], 1u);
-        atomicAdd(&Q.seed_hist[2 * kHistBins + (key >> 56)], 1u);
-      }
+      if (feasible) key = skey(Q.maximize ? vobj : -vobj);
     }
+    hist_add_warp(Q.seed_hist, (unsigned)(key >> 48), key != 0);
+    hist_add_warp(Q.seed_hist + 2 * kHistBins, (unsigned)(key >> 56), key != 0);
     mx = max(mx, key);
   }
 #pragma unroll
@@ -1851,11 +1860,11 @@ __global__ void corner_kernel(const CornerLaunch P) {
           for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
           val = __dadd_rn(val, Q.test_bias[0]);
           key = skey(Q.maximize ? val : -val);
-          atomicAdd(&Q.seed_hist[kHistBins + (key >> 48)], 1u);
-          atomicAdd(&Q.seed_hist[2 * kHistBins + 256 + (key >> 56)], 1u);
         }
       }
     }
+    hist_add_warp(Q.seed_hist + kHistBins, (unsigned)(key >> 48), key != 0);
+    hist_add_warp(Q.seed_hist + 2 * kHistBins + 256, (unsigned)(key >> 56), key != 0);
     unsigned long long mx = key;
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -2006,7 +2015,6 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
   const unsigned long long start = (unsigned long long)blockIdx.x * blockDim.x + tid;
   const unsigned long long stride = (unsigned long long)nb * blockDim.x;
 
-  for (unsigned long long i = start; i < k; i += stride) Q.rank[i] = 0u;  // for rank_kernel (stream order)
   const bool take_all = n_valid <= k;
   unsigned long long phi = 0, plo = 0;
   int depth = 0;
@@ -2089,38 +2097,82 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
 }
 
 // ---------------------------------------------------------------------------
-// K6: best-first order of the selected set by rank counting.  rank[i] =
-// #{j : sel[j] better than sel[i]}; keys (key, g) are unique so ranks are a
-// permutation.  Grid (i-blocks, j-splits, queries).
-__global__ void __launch_bounds__(256) rank_kernel(const ScanQuery* __restrict__ qs, int jsplit) {
-  const ScanQuery& Q = qs[blockIdx.z];
-  QCtl* ctl = Q.ctl;
-  if (*(volatile unsigned*)&ctl->small_done) return;
-  const unsigned long long n = *(volatile unsigned long long*)&ctl->sel_count;
-  const unsigned long long i = (unsigned long long)blockIdx.x * 256 + threadIdx.x;
-  if ((unsigned long long)blockIdx.x * 256 >= n) return;
-  __shared__ Entry tile[256];
-  const unsigned long long j_lo = n * blockIdx.y / jsplit, j_hi = n * (blockIdx.y + 1) / jsplit;
-  Entry ei;
-  ei.key = 0; ei.g = ~0ull;
-  if (i < n) ei = Q.sel[i];
-  unsigned cnt = 0;
-  for (unsigned long long jb = j_lo; jb < j_hi; jb += 256) {
-    __syncthreads();
-    if (jb + threadIdx.x < j_hi) tile[threadIdx.x] = Q.sel[jb + threadIdx.x];
-    __syncthreads();
-    const int m = (int)(j_hi - jb < 256ull ? j_hi - jb : 256ull);
-    for (int jj = 0; jj < m; ++jj) cnt += entry_better(tile[jj], ei) ? 1u : 0u;
+// Best-first bitonic sort of P (a power of two) entries in shared memory by
+// the whole block; (key, g) pairs are unique, so the order is total.
+__device__ void bitonic_best_first(Entry* es, unsigned P) {
+  for (unsigned size = 2; size <= P; size <<= 1) {
+    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+      // one compare-exchange per thread and pair: pair p -> (i, i + stride)
+      for (unsigned p = threadIdx.x; p < (P >> 1); p += blockDim.x) {
+        const unsigned i = ((p & ~(stride - 1)) << 1) | (p & (stride - 1));
+        const unsigned j = i + stride;
+        const Entry a = es[i], b = es[j];
+        // best-first within ascending-index segments of the final order
+        const bool want_a_first = (i & size) == 0;
+        const bool b_better = entry_better(b, a);
+        if (want_a_first ? b_better : !b_better) {
+          es[i] = b;
+          es[j] = a;
+        }
+      }
+      __syncthreads();
+    }
   }
-  if (i < n && cnt) atomicAdd(&Q.rank[i], cnt);
 }
 
-__global__ void scatter_kernel(const ScanQuery* __restrict__ qs) {
+// K6: best-first order of a large selected set in two launches.  (1) every
+// kSortChunk-entry chunk of sel is sorted in shared memory, in place;
+// (2) an entry's global rank is its position in its own chunk plus, for each
+// other chunk, the number of that chunk's entries better than it (a binary
+// search of the sorted chunk) — exact because the order is total — and it is
+// scattered straight to sorted[rank].  O(n log n) work instead of the O(n^2)
+// of rank counting.  Grids (chunks, queries) / (entry blocks, queries).
+constexpr int kSortChunk = 2048;
+
+__global__ void __launch_bounds__(1024) sort_chunks_kernel(const ScanQuery* __restrict__ qs) {
+  const ScanQuery& Q = qs[blockIdx.y];
+  if (*(volatile unsigned*)&Q.ctl->small_done) return;
+  const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
+  const unsigned long long c0 = (unsigned long long)blockIdx.x * kSortChunk;
+  if (c0 >= n) return;
+  const unsigned len = (unsigned)min((unsigned long long)kSortChunk, n - c0);
+  __shared__ Entry es[kSortChunk];
+  unsigned P = 1;
+  while (P < len) P <<= 1;
+  for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+    if (i < len) {
+      es[i] = Q.sel[c0 + i];
+    } else {
+      es[i].key = 0;
+      es[i].g = ~0ull;
+    }
+  }
+  __syncthreads();
+  bitonic_best_first(es, P);
+  for (unsigned i = threadIdx.x; i < len; i += blockDim.x) Q.sel[c0 + i] = es[i];
+}
+
+__global__ void __launch_bounds__(256) merge_rank_kernel(const ScanQuery* __restrict__ qs) {
   const ScanQuery& Q = qs[blockIdx.y];
   if (*(volatile unsigned*)&Q.ctl->small_done) return;
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) Q.sorted[Q.rank[i]] = Q.sel[i];
+  if (i >= n) return;
+  const Entry e = Q.sel[i];
+  const unsigned long long own = i / kSortChunk;
+  unsigned long long rank = i - own * kSortChunk;
+  const unsigned long long n_chunks = (n + kSortChunk - 1) / kSortChunk;
+  for (unsigned long long c = 0; c < n_chunks; ++c) {
+    if (c == own) continue;
+    const Entry* __restrict__ ch = Q.sel + c * kSortChunk;
+    unsigned lo = 0, hi = (unsigned)min((unsigned long long)kSortChunk, n - c * kSortChunk);
+    while (lo < hi) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (entry_better(ch[mid], e)) lo = mid + 1; else hi = mid;
+    }
+    rank += lo;
+  }
+  Q.sorted[rank] = e;
 }
 
 // ---------------------------------------------------------------------------
@@ -2183,7 +2235,7 @@ __global__ void materialize_kernel(const MatLaunch M) {
 // Small-candidate-set finalize (one 1024-thread CTA per query): when at most
 // kSmallSel candidates are at/above the final bound, load them into shared
 // memory, bitonic-sort by (key desc, g asc), keep the first k, and (single-GPU
-// path) materialize them — replacing select + rank + scatter + materialize.
+// path) materialize them — replacing select + sort + materialize.
 constexpr int kSmallSel = 8192;
 
 __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M, int materialize, int compute_bound) {
@@ -2237,24 +2289,7 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
     es[i].g = ~0ull;
   }
   __syncthreads();
-  for (unsigned size = 2; size <= P; size <<= 1) {
-    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
-      for (unsigned i = tid; i < P; i += blockDim.x) {
-        const unsigned j = i ^ stride;
-        if (j > i) {
-          const Entry a = es[i], b = es[j];
-          // best-first within ascending-index segments of the final order
-          const bool want_a_first = (i & size) == 0;
-          const bool b_better = entry_better(b, a);
-          if (want_a_first ? b_better : !b_better) {
-            es[i] = b;
-            es[j] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
+  bitonic_best_first(es, P);
   const unsigned kk = (unsigned long long)Q.k < (unsigned long long)m ? (unsigned)Q.k : m;
   for (unsigned i = tid; i < kk; i += blockDim.x) {
     Q.sel[i] = es[i];

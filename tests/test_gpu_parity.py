@@ -300,6 +300,34 @@ def test_all_ties_large_k_exceeds_buffer(native):
     assert np.array_equal(res[0]["g"], np.arange(700, dtype=np.uint64))
 
 
+@pytest.mark.parametrize("k", [8193, 12000, 30000])
+def test_large_k_sorted_in_chunks_vs_oracle(native, k):
+    """k past the one-CTA sort: radix select, chunk sort + merge rank, and
+    materialization equal the oracle (several chunks, a ragged last one)."""
+    from oracle import scan_oracle as orc
+
+    sizes, pair_off, n_pairs, values, biases, rng = _random_case(21, n_rx=10, mu=3.8)
+    ctx, lib = _ctx(native, sizes, pair_off, n_pairs, values, biases)
+    assert lib.total > 2 * k
+    for q in (orc.Query(1, False, [(0, -3.0, 3.0)], k), orc.Query(3, True, [], k)):
+        res, _ = ctx.query([{"obj": q.obj, "maximize": q.maximize, "cons": q.cons, "k": q.k, "start": 0,
+                             "end": lib.total}])
+        _check_against_oracle(res[0], values, biases, lib, q, 0, lib.total)
+
+
+def test_large_k_all_ties_order(native):
+    """All-equal objective with k past the one-CTA sort: the chunked order
+    breaks ties by ascending global index, as the reference does."""
+    sizes = [[300, 200], [40, 30, 20]]
+    pair_off = [[0, 300], [500, 540, 570]]
+    values = np.zeros((1, 590), dtype=np.float32)
+    biases = np.zeros(1)
+    ctx, lib = _ctx(native, sizes, pair_off, 590, values, biases)
+    res, _ = ctx.query([{"obj": 0, "maximize": True, "cons": [], "k": 10000, "start": 0, "end": lib.total}])
+    assert res[0]["n"] == 10000
+    assert np.array_equal(res[0]["g"], np.arange(10000, dtype=np.uint64))
+
+
 def test_local_plus_merge_equals_global(native):
     """Multi-GPU protocol on one device: two range shards -> local top-k ->
     gathered buffer -> merge kernel == one global query."""
