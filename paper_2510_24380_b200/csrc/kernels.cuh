@@ -1632,56 +1632,69 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       }
     }
     if (cnt > 0 && !cons_ready) constraint_thresholds(false);
-    unsigned rows = __ballot_sync(0xffffffffu, cnt > 0);
+    // flatten the warp's admitted (row, sorted position) pairs so every lane
+    // has one per round: rows pass only a few columns each in batched passes,
+    // and a row-at-a-time walk leaves most lanes idle
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    // sorted position of flat index j of this lane's row: sbase + j
+    const int64_t sbase = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off + start - (incl - cnt);
     __syncwarp();
     unsigned admitted = 0;
-    while (rows) {
-      const int r = __ffs(rows) - 1;
-      rows &= rows - 1u;
-      const int cnt_r = __shfl_sync(0xffffffffu, cnt, r);
-      const int start_r = __shfl_sync(0xffffffffu, start, r);
-      const int best_r = __shfl_sync(0xffffffffu, best, r);
+    for (int j0 = 0; j0 < total; j0 += 32) {
+      const int jj = j0 + (int)lane;
+      const int j = jj < total ? jj : total - 1;
+      // owning row: smallest r with incl[r] > j
+      int lo = 0, hi = 31;
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const int mid = (lo + hi) >> 1;
+        if (__shfl_sync(0xffffffffu, incl, mid) > j) hi = mid; else lo = mid + 1;
+      }
+      const int r = lo;
+      const int64_t sb = __shfl_sync(0xffffffffu, sbase, r);
       const double po = __shfl_sync(0xffffffffu, p_obj, r);
       const unsigned long long gb = __shfl_sync(0xffffffffu, gbase, r);
-      const int64_t sbase = (int64_t)Q.test_task[best_r] * S.pcols + R.pcol_off + start_r;
-      for (int j0 = 0; j0 < cnt_r; j0 += 32) {
-        const int j = j0 + (int)lane;
-        bool ok = j < cnt_r;
-        int col = 0;
-        if (ok) {
-          col = (int)__ldg(S.scol + sbase + j);
-          ok = col >= col_lo && col < col_hi;
-        }
-        // every test on the pair (the chosen one passes by construction);
-        // gathers issued without short-circuit
-        bool pass = ok;
-        float xo = 0.0f;
-        for (int i = 0; i < nt; ++i) {
-          const float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
-          if (i == 0) xo = x;
-          pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
-        }
-        admitted += ok ? 1u : 0u;
-        const unsigned mk = __ballot_sync(0xffffffffu, pass);
-        if (!mk) continue;
-        unsigned long long cbase = 0;
-        if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
-        cbase = __shfl_sync(0xffffffffu, cbase, 0);
-        if (pass) {
-          const double val = fx(po, xo, b_obj);
-          Entry e;
-          e.key = skey(maximize ? val : -val);
-          e.g = gb + (unsigned long long)col;
-          const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
-          if (idx < Q.cap) Q.buf[idx] = e;
-          const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
-          atomicAdd(&Q.hist[hb], 1u);
-          atomicAdd(&Q.coarse[hb >> 8], 1u);
-        }
-        if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
-          __threadfence();
-          refresh_tau(Q);
-        }
+      bool ok = jj < total;
+      int col = 0;
+      if (ok) {
+        col = (int)__ldg(S.scol + sb + j);
+        ok = col >= col_lo && col < col_hi;
+      }
+      // every test on the pair (the chosen one passes by construction);
+      // gathers issued without short-circuit
+      bool pass = ok;
+      float xo = 0.0f;
+      for (int i = 0; i < nt; ++i) {
+        const float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
+        if (i == 0) xo = x;
+        pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
+      }
+      admitted += ok ? 1u : 0u;
+      const unsigned mk = __ballot_sync(0xffffffffu, pass);
+      if (!mk) continue;
+      unsigned long long cbase = 0;
+      if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
+      cbase = __shfl_sync(0xffffffffu, cbase, 0);
+      if (pass) {
+        const double val = fx(po, xo, b_obj);
+        Entry e;
+        e.key = skey(maximize ? val : -val);
+        e.g = gb + (unsigned long long)col;
+        const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
+        if (idx < Q.cap) Q.buf[idx] = e;
+        const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+        atomicAdd(&Q.hist[hb], 1u);
+        atomicAdd(&Q.coarse[hb >> 8], 1u);
+      }
+      if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
+        __threadfence();
+        refresh_tau(Q);
       }
     }
     __syncwarp();

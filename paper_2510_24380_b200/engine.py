@@ -236,7 +236,25 @@ def _types_for(library, query):
     return mi, sc, tk
 
 
+def _plain_fields(cls, names):
+    """True when ``cls`` is a dataclass whose instances are exactly their
+    ``__dict__`` of these fields (no __post_init__, no slots, no defaults that
+    __init__ would compute), so an instance can be made without running the
+    generated __init__ — a frozen dataclass's __init__ pays an
+    object.__setattr__ per field, ~1 µs per result row."""
+    fields = getattr(cls, "__dataclass_fields__", None)
+    return (fields is not None and tuple(fields) == names and not hasattr(cls, "__post_init__")
+            and "__slots__" not in cls.__dict__ and "__dict__" in dir(cls))
+
+
+_MI_FIELDS = ("reaction_id", "assignment")
+_SC_FIELDS = ("global_index", "chi", "objective", "violation", "constraint_values")
+
+
 def _build_result(library, query, res: dict, timing: dict):
+    """TopKResult from the device rows (engine.py:238-262 output shape):
+    entries best-first, chi = (reaction_id, ((rgroup_id, synthon_id), ...)),
+    violation +0.0, constraint values in constraint order."""
     mi_cls, sc_cls, tk_cls = _types_for(library, query)
     n = int(res["n"])
     g = res["g"].tolist()
@@ -244,13 +262,28 @@ def _build_result(library, query, res: dict, timing: dict):
     cons = res["constraint_values"].tolist()
     rxi = res["reaction"].tolist()
     dig = res["digits"].tolist()
-    entries = []
     reactions = library.reactions
+    fast = _plain_fields(mi_cls, _MI_FIELDS) and _plain_fields(sc_cls, _SC_FIELDS)
+    new = object.__new__
+    per_rx = {}
+    entries = [None] * n
     for i in range(n):
-        rx = reactions[rxi[i]]
+        t = rxi[i]
+        rx = per_rx.get(t)
+        if rx is None:
+            spec = reactions[t]
+            rx = per_rx[t] = (spec.reaction_id, [(rg.rgroup_id, rg.synthon_ids) for rg in spec.rgroups])
         d = dig[i]
-        chi = mi_cls(rx.reaction_id, tuple((rg.rgroup_id, rg.synthon_ids[d[j]]) for j, rg in enumerate(rx.rgroups)))
-        entries.append(sc_cls(g[i], chi, obj[i], 0.0, tuple(cons[i])))
+        assignment = tuple([(rid, sids[d[j]]) for j, (rid, sids) in enumerate(rx[1])])
+        if fast:
+            chi = new(mi_cls)
+            chi.__dict__.update(reaction_id=rx[0], assignment=assignment)
+            sc = new(sc_cls)
+            sc.__dict__.update(global_index=g[i], chi=chi, objective=obj[i], violation=0.0,
+                               constraint_values=tuple(cons[i]))
+        else:
+            sc = sc_cls(g[i], mi_cls(rx[0], assignment), obj[i], 0.0, tuple(cons[i]))
+        entries[i] = sc
     return tk_cls(entries=entries, scanned=int(res["scanned"]), retained=n,
                   discarded_for_violation=int(res["discarded"]), timing=timing)
 
