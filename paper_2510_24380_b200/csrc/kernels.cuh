@@ -2110,17 +2110,54 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(const ScanQuery*
 }
 
 // ---------------------------------------------------------------------------
+// Strides s_hi..1 (s_hi < 32) of the bitonic merge of blocks of `size`, in
+// registers: lane (i & 31) holds element i, its partner i ^ s is a lane of the
+// same warp.  Best-first within segments whose `size` bit is clear.
+__device__ __forceinline__ void bitonic_warp_steps(Entry& e, unsigned i, unsigned size, unsigned s_hi) {
+  for (unsigned s = s_hi; s > 0; s >>= 1) {
+    Entry o;
+    o.key = __shfl_xor_sync(0xffffffffu, e.key, s);
+    o.g = __shfl_xor_sync(0xffffffffu, e.g, s);
+    const bool lower = (i & s) == 0, best_first = (i & size) == 0;
+    const bool o_better = entry_better(o, e);
+    if (lower == best_first ? o_better : !o_better) e = o;
+  }
+}
+
 // Best-first bitonic sort of P (a power of two) entries in shared memory by
-// the whole block; (key, g) pairs are unique, so the order is total.
+// the whole block (blockDim a multiple of 32); (key, g) pairs are unique, so
+// the order is total.  Strides >= 32 compare-exchange through shared memory
+// (one pair per thread, a barrier per stride); the strides below 32 of every
+// merge run in registers with warp shuffles, one barrier per merge size.
 __device__ void bitonic_best_first(Entry* es, unsigned P) {
-  for (unsigned size = 2; size <= P; size <<= 1) {
-    for (unsigned stride = size >> 1; stride > 0; stride >>= 1) {
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+  const unsigned chunks = P >= 32 ? P >> 5 : 0;
+  if (chunks == 0) {  // tiny: thread 0 insertion sort
+    if (threadIdx.x == 0) {
+      for (unsigned i = 1; i < P; ++i) {
+        const Entry x = es[i];
+        unsigned j = i;
+        for (; j > 0 && entry_better(x, es[j - 1]); --j) es[j] = es[j - 1];
+        es[j] = x;
+      }
+    }
+    __syncthreads();
+    return;
+  }
+  for (unsigned c = warp; c < chunks; c += n_warps) {
+    const unsigned i = (c << 5) | lane;
+    Entry e = es[i];
+    for (unsigned size = 2; size <= 32; size <<= 1) bitonic_warp_steps(e, i, size, size >> 1);
+    es[i] = e;
+  }
+  __syncthreads();
+  for (unsigned size = 64; size <= P; size <<= 1) {
+    for (unsigned stride = size >> 1; stride >= 32; stride >>= 1) {
       // one compare-exchange per thread and pair: pair p -> (i, i + stride)
       for (unsigned p = threadIdx.x; p < (P >> 1); p += blockDim.x) {
         const unsigned i = ((p & ~(stride - 1)) << 1) | (p & (stride - 1));
         const unsigned j = i + stride;
         const Entry a = es[i], b = es[j];
-        // best-first within ascending-index segments of the final order
         const bool want_a_first = (i & size) == 0;
         const bool b_better = entry_better(b, a);
         if (want_a_first ? b_better : !b_better) {
@@ -2130,6 +2167,13 @@ __device__ void bitonic_best_first(Entry* es, unsigned P) {
       }
       __syncthreads();
     }
+    for (unsigned c = warp; c < chunks; c += n_warps) {
+      const unsigned i = (c << 5) | lane;
+      Entry e = es[i];
+      bitonic_warp_steps(e, i, size, 16);
+      es[i] = e;
+    }
+    __syncthreads();
   }
 }
 
@@ -2206,34 +2250,42 @@ __device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned
   int lo = 0, hi = M.n_rx;
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (M.g_off[mid] <= g) lo = mid; else hi = mid;
+    if (__ldg(M.g_off + mid) <= g) lo = mid; else hi = mid;
   }
   const DevReaction& R = M.rx[lo];
-  unsigned long long rem = g - R.g_off;
-  int64_t dig[kMaxRg];
-  for (int j = R.c - 1; j >= 0; --j) {
-    const unsigned long long sz = (unsigned long long)R.size[j];
-    dig[j] = (int64_t)(rem % sz);
-    rem /= sz;
+  const int c = R.c;
+  uint64_t rem = g - R.g_off;
+  int64_t dig[kMaxRg], pr[kMaxRg];
+#pragma unroll
+  for (int j = kMaxRg - 1; j >= 0; --j) {
+    dig[j] = 0;
+    pr[j] = 0;
+    if (j < c) {
+      uint64_t q, d;
+      divmod_u64(q, d, rem, (uint64_t)R.size[j]);
+      dig[j] = (int64_t)d;
+      pr[j] = R.pair_off[j] + (int64_t)d;
+      rem = q;
+    }
   }
-  {
-    const float* v = M.values + (int64_t)Q.obj_task * M.n_pairs;
-    double val = (double)v[R.pair_off[0] + dig[0]];
-    for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)v[R.pair_off[j] + dig[j]]);
-    val = __dadd_rn(val, M.biases[Q.obj_task]);
-    Q.out_obj[i] = val;
-  }
-  for (int ci = 0; ci < Q.n_cons; ++ci) {
-    const int task = Q.cons_task[ci];
-    const float* v = M.values + (int64_t)task * M.n_pairs;
-    double acc = 0.0;
-    for (int j = 0; j < R.c; ++j) acc = __dadd_rn(acc, (double)v[R.pair_off[j] + dig[j]]);
-    acc = __dadd_rn(acc, M.biases[task]);
-    Q.out_cons[i * Q.n_cons + ci] = acc;
-  }
+  // read-only (__ldg) gathers, so stores to the outputs do not order them
+  // zero_start: apex_score's acc = 0.0; acc += v_r order (differs from the
+  // scan's v0 + v1 + ... only in the sign of an all-zero sum)
+  auto sum = [&](int task, bool zero_start) {
+    const float* __restrict__ v = M.values + (int64_t)task * M.n_pairs;
+    const double v0 = (double)__ldg(v + pr[0]);
+    double acc = zero_start ? __dadd_rn(0.0, v0) : v0;
+#pragma unroll
+    for (int j = 1; j < kMaxRg; ++j)
+      if (j < c) acc = __dadd_rn(acc, (double)__ldg(v + pr[j]));
+    return __dadd_rn(acc, __ldg(M.biases + task));
+  };
+  Q.out_obj[i] = sum(Q.obj_task, false);
+  for (int ci = 0; ci < Q.n_cons; ++ci) Q.out_cons[i * Q.n_cons + ci] = sum(Q.cons_task[ci], true);
   Q.out_g[i] = g;
   Q.out_rx[i] = lo;
-  for (int j = 0; j < kMaxRg; ++j) Q.out_dig[i * kMaxRg + j] = j < R.c ? (int32_t)dig[j] : 0;
+#pragma unroll
+  for (int j = 0; j < kMaxRg; ++j) Q.out_dig[i * kMaxRg + j] = (int32_t)dig[j];
 }
 
 __global__ void materialize_kernel(const MatLaunch M) {
