@@ -23,6 +23,7 @@ fallback — without the library or a B200 the call raises.
 from __future__ import annotations
 
 import math
+import operator
 import os
 import sys
 import time
@@ -265,25 +266,31 @@ def _build_result(library, query, res: dict, timing: dict):
     reactions = library.reactions
     fast = _plain_fields(mi_cls, _MI_FIELDS) and _plain_fields(sc_cls, _SC_FIELDS)
     new = object.__new__
-    per_rx = {}
-    entries = [None] * n
-    for i in range(n):
-        t = rxi[i]
+    getitem = operator.getitem
+    per_rx = {}  # reaction position -> (reaction_id, rgroup ids, synthon id sequences)
+    entries = []
+    append = entries.append
+    for gi, oi, ci, t, d in zip(g, obj, cons, rxi, dig):
         rx = per_rx.get(t)
         if rx is None:
             spec = reactions[t]
-            rx = per_rx[t] = (spec.reaction_id, [(rg.rgroup_id, rg.synthon_ids) for rg in spec.rgroups])
-        d = dig[i]
-        assignment = tuple([(rid, sids[d[j]]) for j, (rid, sids) in enumerate(rx[1])])
+            rx = per_rx[t] = (spec.reaction_id, tuple(rg.rgroup_id for rg in spec.rgroups),
+                              tuple(rg.synthon_ids for rg in spec.rgroups))
+        rid, rgids, sids = rx
+        if len(rgids) == 2:
+            assignment = ((rgids[0], sids[0][d[0]]), (rgids[1], sids[1][d[1]]))
+        elif len(rgids) == 3:
+            assignment = ((rgids[0], sids[0][d[0]]), (rgids[1], sids[1][d[1]]), (rgids[2], sids[2][d[2]]))
+        else:
+            assignment = tuple(zip(rgids, map(getitem, sids, d)))
         if fast:
             chi = new(mi_cls)
-            chi.__dict__.update(reaction_id=rx[0], assignment=assignment)
+            chi.__dict__.update(reaction_id=rid, assignment=assignment)
             sc = new(sc_cls)
-            sc.__dict__.update(global_index=g[i], chi=chi, objective=obj[i], violation=0.0,
-                               constraint_values=tuple(cons[i]))
+            sc.__dict__.update(global_index=gi, chi=chi, objective=oi, violation=0.0, constraint_values=tuple(ci))
         else:
-            sc = sc_cls(g[i], mi_cls(rx[0], assignment), obj[i], 0.0, tuple(cons[i]))
-        entries[i] = sc
+            sc = sc_cls(gi, mi_cls(rid, assignment), oi, 0.0, tuple(ci))
+        append(sc)
     return tk_cls(entries=entries, scanned=int(res["scanned"]), retained=n,
                   discarded_for_violation=int(res["discarded"]), timing=timing)
 
