@@ -13,8 +13,10 @@ def page(rep, name, extra=()):
     return list(csv.reader(io.StringIO(out)))
 
 
-def main(rep):
-    rows = page(rep, "raw")
+def main(rep, kernel=None):
+    # multi-kernel reports: pass a kernel name (regex, as ncu -k) to pick one
+    kf = ["-k", f"regex:{kernel}"] if kernel else []
+    rows = page(rep, "raw", kf)
     hdr, vals = rows[0], rows[2]
     raw = dict(zip(hdr, vals))
     keys = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -29,7 +31,7 @@ def main(rep):
     for k in keys:
         if k in raw:
             print(f"{k:70s} {raw[k]}")
-    src = page(rep, "source", ["--print-source", "sass"])
+    src = page(rep, "source", ["--print-source", "sass", *kf])
     h = src[1]
     ix = {x: i for i, x in enumerate(h)}
     data = src[2:]
@@ -37,11 +39,17 @@ def main(rep):
     tot = Counter()
     for r in data:
         for s in stalls:
-            tot[s] += int(r[ix[s]] or 0)
+            try:
+                tot[s] += int(r[ix[s]] or 0)
+            except (ValueError, IndexError):
+                continue
     print("stalls:", ", ".join(f"{k[6:]}={v}" for k, v in tot.most_common(9)))
     groups = Counter()
     for r in data:
-        groups[int(r[ix["Instructions Executed"]] or 0)] += 1
+        try:
+            groups[int(r[ix["Instructions Executed"]] or 0)] += 1
+        except (ValueError, IndexError):
+            continue
     total = sum(n * c for n, c in groups.items())
     print("instruction groups (exec count x #instr = share):")
     for n, c in sorted(groups.items(), key=lambda x: -x[0] * x[1])[:10]:
@@ -49,4 +57,4 @@ def main(rep):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
