@@ -1598,7 +1598,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         const int task = Q.test_task[i];
         const float* v = values + (int64_t)task * n_pairs;
         double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
-        for (int j = 1; j < c - 1; ++j) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+        // fixed trip count: pr stays in registers (a runtime-indexed pr
+        // would live in local memory)
+#pragma unroll
+        for (int j = 1; j < kMaxRg - 1; ++j)
+          if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
         const bool lower = Q.test_lower[i] != 0;
         const float th = lower ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
                                : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
@@ -1833,11 +1837,17 @@ __global__ void corner_kernel(const CornerLaunch P) {
   else if (R.c == 3) mb = (int)cbrtf((float)P.budget + 0.5f);
   else if (R.c >= 4) mb = (int)powf((float)P.budget, 1.0f / R.c);
   mb = max(mb, 1);
+  // fixed trip counts with guards throughout: the per-R-group arrays stay in
+  // registers (runtime-indexed, they would live in local memory)
   int mj[kMaxRg];
   unsigned total = 1;
-  for (int j = 0; j < R.c; ++j) {
-    mj[j] = min(mb, P.m[t * kMaxRg + j]);
-    total *= (unsigned)mj[j];
+#pragma unroll
+  for (int j = 0; j < kMaxRg; ++j) {
+    mj[j] = 1;
+    if (j < R.c) {
+      mj[j] = min(mb, P.m[t * kMaxRg + j]);
+      total *= (unsigned)mj[j];
+    }
   }
   const int dir = Q.maximize ? 0 : 1;
   const int32_t* list = P.lists + ((int64_t)Q.test_task[0] * 2 + dir) * P.slots;
@@ -1849,28 +1859,39 @@ __global__ void corner_kernel(const CornerLaunch P) {
       unsigned rem = i;
       int64_t pr[kMaxRg];
       int64_t dig[kMaxRg];
-      for (int j = R.c - 1; j >= 0; --j) {
-        const unsigned idx = rem % (unsigned)mj[j];
-        rem /= (unsigned)mj[j];
-        dig[j] = list[P.slot_off[t * kMaxRg + j] + idx];
-        pr[j] = R.pair_off[j] + dig[j];
+#pragma unroll
+      for (int j = kMaxRg - 1; j >= 0; --j) {
+        dig[j] = 0;
+        pr[j] = 0;
+        if (j < R.c) {
+          const unsigned idx = rem % (unsigned)mj[j];
+          rem /= (unsigned)mj[j];
+          dig[j] = list[P.slot_off[t * kMaxRg + j] + idx];
+          pr[j] = R.pair_off[j] + dig[j];
+        }
       }
       unsigned long long g = 0;
-      for (int j = 0; j < R.c; ++j) g = g * (unsigned long long)R.size[j] + (unsigned long long)dig[j];
+#pragma unroll
+      for (int j = 0; j < kMaxRg; ++j)
+        if (j < R.c) g = g * (unsigned long long)R.size[j] + (unsigned long long)dig[j];
       g += off;
       if (g >= P.start && g < P.end) {
         bool feasible = true;
         for (int tt = 1; tt < Q.nt && feasible; ++tt) {
           const float* v = P.values + (int64_t)Q.test_task[tt] * P.n_pairs;
           double val = (double)__ldg(v + pr[0]);
-          for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+#pragma unroll
+          for (int j = 1; j < kMaxRg; ++j)
+            if (j < R.c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
           val = __dadd_rn(val, Q.test_bias[tt]);
           feasible = Q.test_lower[tt] ? (val >= Q.test_beta[tt]) : (val <= Q.test_beta[tt]);
         }
         if (feasible) {
           const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
           double val = (double)__ldg(v + pr[0]);
-          for (int j = 1; j < R.c; ++j) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+#pragma unroll
+          for (int j = 1; j < kMaxRg; ++j)
+            if (j < R.c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
           val = __dadd_rn(val, Q.test_bias[0]);
           key = skey(Q.maximize ? val : -val);
         }
