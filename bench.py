@@ -105,10 +105,7 @@ def f_ops(queries) -> int:
 
 
 def build_model(shape, seed=1):
-    u = synth.random_cache(shape.n_pairs, seed=seed)
-    w, b = synth.random_heads(seed=seed)
-    w, b = synth.calibrate_heads(shape, u, w, b, n_sample=20000, seed=seed)
-    return u, w, b
+    return synth.build_model(shape, seed=seed)
 
 
 # ---------------------------------------------------------------------------

@@ -14,10 +14,12 @@
 // A candidate-buffer overflow is detected (count > cap) and the query is re-run
 // with the final (valid) bound as its starting threshold.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <random>
 #include <string>
@@ -44,15 +46,22 @@ int set_err(int code, const std::string& m) {
       return set_err(APEX_ECUDA, std::string(#x) + " failed: " + cudaGetErrorString(e__));       \
   } while (0)
 
+// serialize calls on one context (apex_ctx::mu); recursive: apex_query calls
+// apex_query_async / apex_query_fetch on the same context
+#define APEX_LOCK(c)                                                  \
+  if (!(c)) return set_err(APEX_EINVAL, "null context");              \
+  std::lock_guard<std::recursive_mutex> lock__((c)->mu)
+
 #define APEX_TRY(x)           \
   do {                        \
     int r__ = (x);            \
     if (r__ != APEX_OK) return r__; \
   } while (0)
 
-// bumped on every (re)allocation: device pointers baked into a captured CUDA
-// graph are only valid while this is unchanged
-thread_local uint64_t g_alloc_gen = 0;
+// bumped on every (re)allocation by any thread: device pointers baked into a
+// captured CUDA graph are only valid while this is unchanged (process-wide, so
+// a reallocation on one thread invalidates every context's graph key)
+std::atomic<uint64_t> g_alloc_gen{0};
 
 struct DBuf {
   void* p = nullptr;
@@ -104,9 +113,9 @@ struct HBuf {
 };
 
 struct Slot {
-  DBuf packed, obj_col, buf, comp, sel, sorted;
+  DBuf packed, obj_col, buf, sel, sorted;
   void release() {
-    for (DBuf* b : {&packed, &obj_col, &buf, &comp, &sel, &sorted}) b->release();
+    for (DBuf* b : {&packed, &obj_col, &buf, &sel, &sorted}) b->release();
   }
 };
 
@@ -241,6 +250,14 @@ struct apex_ctx {
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
   uint64_t opt_gen = 0;             // bumped by apex_set_option
+  // per-context (= per-device) launch caches
+  std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
+  std::vector<std::pair<const void*, size_t>> attr_cache;
+  bool attr_small = false;
+  int occ_sel = 0;
+  // a context is driven by one thread at a time: every C-ABI call on it holds
+  // this lock (calls on different contexts run concurrently)
+  std::recursive_mutex mu;
   // CUDA graph of the last batch signature
   cudaGraphExec_t gexec = nullptr;
   uint64_t gkey = 0;
@@ -414,13 +431,14 @@ size_t scan_smem(int nt, int cb) {
   return (size_t)kScanWarps * 2 * cb * ntp * sizeof(float) + (size_t)kScanWarps * 2 * sizeof(uint64_t);
 }
 
-int scan_occupancy(ScanFn fn, size_t smem, int* occ) {
-  // cached per (kernel, smem): the attribute call and the occupancy query cost
-  // microseconds on every launch otherwise
-  // (the dynamic-smem attribute is per kernel: only ever raise it, so a cached
-  // occupancy for a larger request stays launchable)
-  static thread_local std::vector<std::pair<std::pair<const void*, size_t>, int>> cache;
-  static thread_local std::vector<std::pair<const void*, size_t>> attr;
+int scan_occupancy(apex_ctx* c, ScanFn fn, size_t smem, int* occ) {
+  // cached per (kernel, smem) in the context (one device per context; the
+  // dynamic-smem attribute is per device): the attribute call and the
+  // occupancy query cost microseconds on every launch otherwise
+  // (the attribute is per kernel: only ever raise it, so a cached occupancy
+  // for a larger request stays launchable)
+  auto& cache = c->occ_cache;
+  auto& attr = c->attr_cache;
   for (auto& e : cache)
     if (e.first.first == (const void*)fn && e.first.second == smem) {
       *occ = e.second;
@@ -609,7 +627,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
       APEX_TRY(S.packed.ensure((size_t)std::max<int64_t>(c->n_pairs, 1) * ntp_i * sizeof(float)));
     }
     APEX_TRY(S.buf.ensure((size_t)cap * sizeof(Entry)));
-    APEX_TRY(S.comp.ensure((size_t)cap * sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)std::max<int64_t>(k, 1) * sizeof(Entry)));
   }
@@ -634,7 +651,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.packed = S.packed.as<float>();
     Q.obj_col = S.obj_col.as<float>();
     Q.buf = S.buf.as<Entry>();
-    Q.comp = S.comp.as<Entry>();
     Q.sel = S.sel.as<Entry>();
     Q.sorted = S.sorted.as<Entry>();
     Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
@@ -688,8 +704,8 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   return APEX_OK;
 }
 
-// Enqueue the device pipeline of the prepared batch.  tau0: preset admission
-// keys (re-run after an overflow), or nullptr.
+// Enqueue the device pipeline of the prepared batch.  pre: per-query presets
+// of an exact re-run after an overflow (check_batch), or nullptr.
 // Stage timing event; inside a stream capture it is recorded as an external
 // event-record node so the graph replay still timestamps it.
 cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
@@ -714,21 +730,19 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
   M.n_pairs = c->n_pairs;
   M.biases = c->d_biases.as<double>();
   {
-    static thread_local bool attr_small = false;
     const size_t smem_small = (size_t)kSmallSel * sizeof(Entry);
-    if (!attr_small) {
+    if (!c->attr_small) {  // per context = per device (the attribute is per device)
       APEX_CU(cudaFuncSetAttribute((const void*)finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_small));
-      attr_small = true;
+      c->attr_small = true;
     }
     finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, finalize ? 1 : 0, compute_bound ? 1 : 0);
     ++st.launches;
   }
   {
-    static thread_local int occ_sel = 0;
-    if (!occ_sel)
-      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sel, (const void*)select_kernel, kSelectThreads, 0));
-    const int resident = std::max(1, occ_sel * c->sm_count);
+    if (!c->occ_sel)
+      APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sel, (const void*)select_kernel, kSelectThreads, 0));
+    const int resident = std::max(1, c->occ_sel * c->sm_count);
     const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_select_ctas, resident / std::max(nq, 1)));
     const int q_chunk = std::max(1, resident / per_q);
     for (int q0 = 0; q0 < nq; q0 += q_chunk) {
@@ -750,7 +764,7 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
   return APEX_OK;
 }
 
-int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
+int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   Batch& B = c->batch;
   RunStats& st = B.st;
   const int nq = B.nq;
@@ -760,12 +774,12 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
   APEX_CU(stage_mark(c, 0, s));
   if (tau0) {
-    APEX_TRY(c->d_tau0.ensure(nq * sizeof(unsigned long long)));
-    APEX_TRY(c->h_tau0.ensure(nq * sizeof(unsigned long long)));
+    APEX_TRY(c->d_tau0.ensure(nq * sizeof(RunPreset)));
+    APEX_TRY(c->h_tau0.ensure(nq * sizeof(RunPreset)));
     APEX_CU(cudaStreamSynchronize(s));
-    std::memcpy(c->h_tau0.p, tau0, nq * sizeof(unsigned long long));
-    APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    st.h2d_bytes += nq * 8;
+    std::memcpy(c->h_tau0.p, tau0, nq * sizeof(RunPreset));
+    APEX_CU(cudaMemcpyAsync(c->d_tau0.p, c->h_tau0.p, nq * sizeof(RunPreset), cudaMemcpyHostToDevice, s));
+    st.h2d_bytes += nq * (int64_t)sizeof(RunPreset);
   }
   // kernel choice: admission-first (admit), full predicate (full), or per query (auto)
   const bool admit = c->opt_mode >= 2;
@@ -776,7 +790,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   const bool full = c->opt_mode != 2 && !B.no_full;
   const int autok = (c->opt_mode == 3 && !tau0) ? (B.no_full ? 3 : sorted_all ? 2 : 1) : 0;
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<unsigned long long>() : nullptr,
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
   // K2 pack of the streamed objective column
@@ -893,7 +907,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
         ScanFn fn = reinterpret_cast<ScanFn>(scan_sorted_kernel);
         int occ = 0;
-        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        APEX_TRY(scan_occupancy(c, fn, smem, &occ));
         SortedLaunch SL;
         SL.sx = c->d_sorted_x.as<float>();
         SL.scol = c->d_sorted_col.as<uint32_t>();
@@ -929,7 +943,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
                             (size_t)kScanWarps * 2 * sizeof(uint64_t) + kBlockDq * sizeof(DenseItem) + 16 +
                             (size_t)kScanWarps * B.rl * kMaxTests * 32 * sizeof(float);
         int occ = 0;
-        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        APEX_TRY(scan_occupancy(c, fn, smem, &occ));
         for (int q0 = 0; q0 < nq; q0 += 64) {
           const int nql = std::min(64, nq - q0);
           ScanLaunch La = L;
@@ -962,7 +976,7 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
         int occ = 0;
-        APEX_TRY(scan_occupancy(fn, smem, &occ));
+        APEX_TRY(scan_occupancy(c, fn, smem, &occ));
         for (int q0 = B.cls_begin[k]; q0 < B.cls_begin[k + 1]; q0 += 64) {
           const int nql = std::min(64, B.cls_begin[k + 1] - q0);
           const int64_t items = (int64_t)(te - tb) * nql;
@@ -1018,46 +1032,74 @@ int enqueue_batch(apex_ctx* c, const unsigned long long* tau0) {
   return APEX_OK;
 }
 
-// Sync, detect candidate-buffer overflow, re-run exactly if needed.
+// Sync, detect candidate-buffer overflow, re-run exactly if needed.  A re-run
+// is preset from the overflowed run's control block (finalize_small_kernel
+// nx_*): the admission threshold at the k-th best bin and a 16-bit narrower
+// candidate histogram there, or — when that bin is one exact key K (massive
+// exact ties) — the composite bound (key > K, or key == K and g below a limit
+// narrowed 16 bits per run).  The buffers never grow; each step shrinks the
+// admitted set, so the protocol converges (<= 4 key steps + 4 g steps for
+// 64-bit keys and indices).
 int check_batch(apex_ctx* c) {
   Batch& B = c->batch;
   if (!B.pending) return set_err(APEX_ESTATE, "no query batch in flight");
   const int nq = B.nq;
-  std::vector<unsigned long long> tau0(nq);
+  std::vector<RunPreset> pre(nq);
   for (int attempt = 0;; ++attempt) {
     APEX_CU(cudaStreamSynchronize(c->stream));
     bool overflow = false;
     for (int i = 0; i < nq; ++i) {
       const QCtl& C = c->h_ctl.as<QCtl>()[i];
-      const unsigned long long cap = c->uploaded[i].cap;
-      if (C.count > cap) overflow = true;
-      tau0[i] = std::max<unsigned long long>(C.bound_key, C.tau_key);
+      const apex_query_spec& q = B.qs[i];
+      RunPreset& P = pre[i];
+      std::memset(&P, 0, sizeof(P));
+      P.tie_glimit = ~0ull;
+      P.tie_gshift = 48;
+      if (C.count > c->uploaded[i].cap) {
+        overflow = true;
+        P.tau = C.nx_tau;
+        if (C.nx_tie) {
+          P.tie_on = 1;
+          P.tie_key = C.nx_tau;
+          P.shift = 48;
+          if (C.nx_tie_enter) {
+            const uint64_t span = q.end - q.start;
+            unsigned gs = 0;
+            while (gs < 63 && (span >> gs) >= 65535ull) ++gs;
+            P.tie_gbase = q.start;
+            P.tie_glimit = q.end;
+            P.tie_gshift = gs;
+          } else {
+            P.tie_gbase = C.nx_gbase;
+            P.tie_glimit = C.nx_glimit;
+            P.tie_gshift = C.nx_gshift;
+          }
+        } else {
+          P.base = C.nx_base;
+          P.shift = C.nx_shift;
+        }
+      } else {
+        // a query that fit re-runs with its valid final bound (same result)
+        P.tau = std::max<unsigned long long>(C.bound_key, C.tau_key);
+        P.base = P.tau;
+        P.shift = C.hist_shift;
+        if (C.tie_on) {
+          P.tie_on = 1;
+          P.tie_key = C.tie_key;
+          P.tie_gbase = C.tie_gbase;
+          P.tie_glimit = C.tie_glimit;
+          P.tie_gshift = C.tie_gshift;
+          P.tau = C.tie_key;
+        }
+      }
     }
     if (!overflow) break;
-    if (attempt >= 3) {
+    if (attempt >= 12) {
       B.pending = false;
-      return set_err(APEX_ELIMIT, "candidate buffer overflow persists (massive exact ties?)");
+      return set_err(APEX_ELIMIT, "candidate buffer overflow did not converge");
     }
     ++B.st.retries;
-    if (attempt >= 1) {
-      // repeated overflow (e.g. huge exact ties in one key bin): grow the buffers
-      std::vector<ScanQuery> hq = c->uploaded;
-      for (int i = 0; i < nq; ++i) {
-        Slot& S = c->slots[i];
-        const size_t nb = S.buf.bytes * 4;
-        APEX_TRY(S.buf.ensure(nb));
-        APEX_TRY(S.comp.ensure(nb));
-        hq[i].buf = S.buf.as<Entry>();
-        hq[i].comp = S.comp.as<Entry>();
-        hq[i].cap = S.buf.bytes / sizeof(Entry);
-      }
-      const size_t bytes = nq * sizeof(ScanQuery);
-      std::memcpy(c->h_queries.p, hq.data(), bytes);
-      APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, bytes, cudaMemcpyHostToDevice, c->stream));
-      APEX_CU(cudaEventRecord(c->upload_ev, c->stream));
-      c->uploaded = hq;
-    }
-    APEX_TRY(enqueue_batch(c, tau0.data()));
+    APEX_TRY(enqueue_batch(c, pre.data()));
   }
   B.pending = false;
   if (!B.no_full && c->opt_mode == 3 && B.plan_rows) {
@@ -1105,7 +1147,8 @@ uint64_t batch_key(const apex_ctx* c) {
   const void* plan_rows = B.plan_rows;
   mix(&plan_rows, sizeof(plan_rows));
   mix(&c->opt_gen, sizeof(c->opt_gen));
-  mix(&g_alloc_gen, sizeof(g_alloc_gen));
+  const uint64_t gen = g_alloc_gen.load();
+  mix(&gen, sizeof(gen));
   return h;
 }
 
@@ -1338,6 +1381,7 @@ void apex_ctx_destroy(apex_ctx* c) {
 }
 
 int apex_set_stream(apex_ctx* c, void* stream) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (c->own_stream) {
     cudaStreamSynchronize(c->stream);
@@ -1354,6 +1398,7 @@ int apex_set_stream(apex_ctx* c, void* stream) {
 }
 
 int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64_t n_pairs) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (n_rx < 0 || (n_rx > 0 && !rxs) || n_pairs < 0) return set_err(APEX_EINVAL, "bad library arguments");
   std::vector<DevReaction> rx(n_rx);
@@ -1406,6 +1451,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
 }
 
 int apex_load_table(apex_ctx* c, const float* values, const double* biases, int32_t n_tasks, int64_t n_pairs) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (n_tasks < 1 || n_pairs < 0 || !biases || (n_pairs > 0 && !values)) return set_err(APEX_EINVAL, "bad table arguments");
   const size_t n = (size_t)n_tasks * n_pairs;
@@ -1428,6 +1474,7 @@ int apex_load_table(apex_ctx* c, const float* values, const double* biases, int3
 
 int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, int32_t d, const double* w_dev,
                            int32_t n_tasks, float* values_dev) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (n_pairs < 0 || d < 1 || n_tasks < 1 || !w_dev || !values_dev || (n_pairs > 0 && !u_dev))
     return set_err(APEX_EINVAL, "bad precompute arguments");
@@ -1461,6 +1508,7 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
 
 int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, const double* head_w,
                     const double* head_b, int32_t n_tasks, float* values_out) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (!u || !head_w || !head_b || n_pairs < 0 || d < 1 || n_tasks < 1) return set_err(APEX_EINVAL, "bad cache arguments");
   for (int t = 0; t < n_tasks; ++t)
@@ -1497,6 +1545,7 @@ int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, co
 }
 
 int apex_query_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_stats* stats) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, true));
   APEX_TRY(validate_queries(c, qs, nq));
   if (nq < 1) return set_err(APEX_EINVAL, "apex_query_async needs at least one query");
@@ -1523,6 +1572,7 @@ int apex_query_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_st
 }
 
 int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, true));
   Batch& B = c->batch;
   if (!B.pending) return set_err(APEX_ESTATE, "no query batch in flight");
@@ -1556,6 +1606,7 @@ int apex_query_fetch(apex_ctx* c, apex_result* res, apex_stats* stats) {
 }
 
 int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* res, apex_stats* stats) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, true));
   APEX_TRY(validate_queries(c, qs, nq));
   if (nq > 0 && !res) return set_err(APEX_EINVAL, "null results");
@@ -1632,6 +1683,7 @@ int apex_query(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_result* 
 
 int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_entry* out_dev, int64_t* counts,
                      apex_stats* stats) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, true));
   APEX_TRY(validate_queries(c, qs, nq));
   if (nq <= 0) return APEX_OK;
@@ -1667,6 +1719,7 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
 int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq, const apex_entry* entries_dev,
                               int32_t n_src, int64_t stride, uint64_t total_scanned, apex_result* res,
                               apex_stats* stats) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, true));
   if (nq < 0 || n_src < 0 || stride < 0 || (nq > 0 && (!qs || !res)) ||
       (n_src > 0 && stride > 0 && nq > 0 && !entries_dev))
@@ -1702,7 +1755,6 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
     const int64_t k = std::max<int64_t>(qs[i].k, 1);
     k_max = std::max(k_max, k);
     APEX_TRY(S.buf.ensure((size_t)std::max<int64_t>(n_in, 1024) * sizeof(Entry)));
-    APEX_TRY(S.comp.ensure(sizeof(Entry)));
     APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
     APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
   }
@@ -1727,7 +1779,6 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
     std::memset(&Q, 0, sizeof(Q));
     const int64_t kk = std::max<int64_t>(q.k, 1);
     Q.buf = S.buf.as<Entry>();
-    Q.comp = S.comp.as<Entry>();
     Q.sel = S.sel.as<Entry>();
     Q.sorted = S.sorted.as<Entry>();
     Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
@@ -1797,6 +1848,7 @@ int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry*
 }
 
 int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
+  APEX_LOCK(c);
   if (!c || !name) return set_err(APEX_EINVAL, "bad option arguments");
   std::string n(name);
   ++c->opt_gen;
@@ -1855,6 +1907,7 @@ int apex_get_device_info(apex_ctx* c, int32_t* sm, int32_t* ma, int32_t* mi) {
 
 int apex_debug_thresholds(apex_ctx* c, const double* p, const double* b, const double* beta, int64_t n, float* up,
                           float* lo) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   if (n <= 0) return APEX_OK;
   DBuf dp, db, dbeta, du, dl;
@@ -1878,6 +1931,7 @@ int apex_debug_thresholds(apex_ctx* c, const double* p, const double* b, const d
 }
 
 int apex_debug_trace(apex_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
+  APEX_LOCK(c);
   APEX_TRY(check_ctx(c, false));
   const int64_t m = std::min<int64_t>(cap, c->trace_n);
   if (n) *n = std::max<int64_t>(m, 0);

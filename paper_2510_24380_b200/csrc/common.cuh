@@ -71,7 +71,40 @@ struct QCtl {
   unsigned int tile_counter;      // scan work distribution
   unsigned int barrier;           // select grid barrier
   unsigned int out_count;         // select compaction counter
+  // Tie mode (a re-run after an overflow whose k-th best key K is exact,
+  // capi.cu check_batch): admission is the composite (key, g) bound
+  // key > K or (key == K and g < tie_glimit), and the candidate histogram
+  // bins the tied products by g (tie_gbase, tie_gshift) instead of keys.
+  unsigned long long tie_key;
+  unsigned long long tie_gbase;
+  unsigned long long tie_glimit;
+  unsigned int tie_on;
+  unsigned int tie_gshift;
+  // Parameters of the next run if this one overflowed (finalize_small_kernel):
+  // a narrower key histogram at the k-th best bin, or tie mode at its key.
+  unsigned long long nx_tau;
+  unsigned long long nx_base;
+  unsigned long long nx_gbase;
+  unsigned long long nx_glimit;
+  unsigned int nx_shift;
+  unsigned int nx_tie;            // 1: tie mode at key nx_tau
+  unsigned int nx_gshift;
+  unsigned int nx_tie_enter;      // 1: first tie run (host sets the g range from the query range)
   unsigned int hist[3][256];      // select histograms (triple-buffered)
+};
+
+// Preset of a re-run (one per query, uploaded by check_batch): admission
+// threshold, candidate-histogram base/shift and the tie-mode fields above.
+struct RunPreset {
+  unsigned long long tau;
+  unsigned long long base;
+  unsigned long long tie_key;
+  unsigned long long tie_gbase;
+  unsigned long long tie_glimit;
+  unsigned int shift;
+  unsigned int tie_on;
+  unsigned int tie_gshift;
+  unsigned int _pad;
 };
 
 constexpr int kHistBins = 65536;  // candidate histogram bins
@@ -103,8 +136,7 @@ struct ScanQuery {
   const float* packed;            // [n_pairs][ntp] signed test columns (full-predicate kernel)
   const float* obj_col;           // [pcols] signed objective column of every last R-group (admission kernel)
   Entry* buf;                     // candidate buffer (cap entries)
-  Entry* comp;                    // compacted candidates (cap entries)
-  Entry* sel;                     // selected top-k (k entries, unordered)
+  Entry* sel;                    // selected top-k (k entries, unordered)
   Entry* sorted;                  // best-first (k entries)
   unsigned int* hist;             // [kHistBins] histogram of appended keys (key >> 48)
   unsigned int* coarse;           // [256] histogram of appended keys (key >> 56)

@@ -241,16 +241,24 @@ __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n,
 // ---------------------------------------------------------------------------
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
-__global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const unsigned long long* __restrict__ tau0,
+__global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPreset* __restrict__ pre,
                                 unsigned use_full) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
   // (the candidate / seed histograms are zeroed by one memset per batch)
   if (threadIdx.x == 0) {
-    c->tau_key = tau0 ? tau0[blockIdx.x] : kNoTau;
-    c->hist_base = 0;
-    c->hist_shift = 48;
+    const RunPreset* P = pre ? pre + blockIdx.x : nullptr;
+    c->tau_key = P ? P->tau : kNoTau;
+    c->hist_base = P ? P->base : 0ull;
+    c->hist_shift = P ? P->shift : 48u;
+    c->tie_on = P ? P->tie_on : 0u;
+    c->tie_key = P ? P->tie_key : 0ull;
+    c->tie_gbase = P ? P->tie_gbase : 0ull;
+    c->tie_glimit = P ? P->tie_glimit : ~0ull;
+    c->tie_gshift = P ? P->tie_gshift : 48u;
+    c->nx_tie = 0;
+    c->nx_tie_enter = 0;
     c->use_full = use_full;
     c->small_done = 0;
     c->seed_max = 0;
@@ -492,11 +500,33 @@ __device__ int kth_two_level(const unsigned int* __restrict__ fine, const unsign
   return (cbin << 8) | fb;
 }
 
+// Tie mode (QCtl): composite admission of a re-run whose k-th best key K is
+// exact — products with key == K pass only below the g limit — and the
+// candidate histogram over g for the tied key (better = smaller g = higher
+// bin; keys above K and tied products below tie_gbase are all "above").
+__device__ __forceinline__ bool tie_reject(const QCtl* ctl, unsigned long long key, unsigned long long g) {
+  if (!__ldcg(&ctl->tie_on)) return false;
+  const unsigned long long K = __ldcg(&ctl->tie_key);
+  return key < K || (key == K && g >= __ldcg(&ctl->tie_glimit));
+}
+__device__ __forceinline__ unsigned cand_bin(const QCtl* ctl, unsigned long long key, unsigned long long g,
+                                             unsigned long long hbase, unsigned hshift) {
+  if (__ldcg(&ctl->tie_on)) {
+    if (key > __ldcg(&ctl->tie_key)) return 65535u;
+    const unsigned long long gb = __ldcg(&ctl->tie_gbase);
+    if (g < gb) return 65535u;
+    const unsigned long long rel = (g - gb) >> __ldcg(&ctl->tie_gshift);
+    return rel >= 65535ull ? 0u : (unsigned)(65534ull - rel);
+  }
+  return hist_bin(key, hbase, hshift);
+}
+
 // In-kernel threshold refresh (one warp): tau = lower edge of the k-th best
 // candidate bin, read while other warps keep appending; a stale (smaller)
 // count only lowers the bound, so it stays a valid lower bound on the final
 // k-th best key.
 __device__ __noinline__ void refresh_tau(const ScanQuery& Q) {
+  if (__ldcg(&Q.ctl->tie_on)) return;  // tie mode: the bins are g ranges of the tied key, not keys
   const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, nullptr);
   if (B < 0) return;
   const unsigned long long key = bin_edge((unsigned)B, Q.ctl->hist_base, Q.ctl->hist_shift);
@@ -758,6 +788,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
             const float y0 = ys[(j0 + jj) * NTP];
 #pragma unroll
             for (int r = 0; r < RL; ++r) {
+              Entry e;
+              if (pass[r]) {
+                const float x = maximize ? -y0 : y0;
+                const double val = fx(p_obj[r], x, b_obj);
+                e.key = skey(maximize ? val : -val);
+                e.g = gbase[r] + (unsigned long long)(col_base + j0 + jj);
+                pass[r] = !tie_reject(ctl, e.key, e.g);
+              }
               const unsigned m = __ballot_sync(0xffffffffu, pass[r]);
               if (m) {
                 const int leader = __ffs(m) - 1;
@@ -765,15 +803,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks<NT>()) scan_k
                 if ((int)lane == leader) base = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
                 base = __shfl_sync(0xffffffffu, base, leader);
                 if (pass[r]) {
-                  const float x = maximize ? -y0 : y0;
-                  const double val = fx(p_obj[r], x, b_obj);
-                  const double s = maximize ? val : -val;
-                  Entry e;
-                  e.key = skey(s);
-                  e.g = gbase[r] + (unsigned long long)(col_base + j0 + jj);
                   const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
                   if (idx < cap) buf[idx] = e;
-                  const unsigned hb = hist_bin(e.key, hbase, hshift);
+                  const unsigned hb = cand_bin(ctl, e.key, e.g, hbase, hshift);
                   atomicAdd(&hist[hb], 1u);
                   atomicAdd(&Q.coarse[hb >> 8], 1u);
                 }
@@ -885,6 +917,19 @@ __device__ __noinline__ unsigned dense_row(const ScanQuery& Q, const float* __re
         p1 = p1 && x1 <= t;
       }
     }
+    Entry ee[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!(h ? p1 : p0)) continue;
+      const float y = h ? y1 : y0;
+      const float x = maximize ? -y : y;
+      const double val = fx(po, x, b_obj);
+      ee[h].key = skey(maximize ? val : -val);
+      ee[h].g = gb + (unsigned long long)(h ? col1 : col0);
+      if (tie_reject(ctl, ee[h].key, ee[h].g)) {
+        if (h) p1 = false; else p0 = false;
+      }
+    }
     const unsigned cnt = (p0 ? 1u : 0u) + (p1 ? 1u : 0u);
     unsigned incl = cnt;
 #pragma unroll
@@ -901,15 +946,10 @@ __device__ __noinline__ unsigned dense_row(const ScanQuery& Q, const float* __re
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (!(h ? p1 : p0)) continue;
-      const float y = h ? y1 : y0;
-      const float x = maximize ? -y : y;
-      const double val = fx(po, x, b_obj);
-      Entry e;
-      e.key = skey(maximize ? val : -val);
-      e.g = gb + (unsigned long long)(h ? col1 : col0);
+      const Entry e = ee[h];
       if (idx < Q.cap) Q.buf[idx] = e;
       ++idx;
-      const unsigned hb = hist_bin(e.key, hbase, hshift);
+      const unsigned hb = cand_bin(ctl, e.key, e.g, hbase, hshift);
       atomicAdd(&Q.hist[hb], 1u);
       atomicAdd(&Q.coarse[hb >> 8], 1u);
     }
@@ -1302,6 +1342,15 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
                 gb = gb1;
               }
             }
+            Entry e;
+            if (pass) {
+              const float y0 = sm_f[yo + j0 + jj];
+              const float x = maximize ? -y0 : y0;
+              const double val = fx(po, x, b_obj);
+              e.key = skey(maximize ? val : -val);
+              e.g = gb + (unsigned long long)(col_base + j0 + (int)jj);
+              pass = !tie_reject(ctl, e.key, e.g);
+            }
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (TRACE) n_cand += __popc(m);
             if (!m) continue;
@@ -1309,15 +1358,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
             if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(m));
             cbase = __shfl_sync(0xffffffffu, cbase, 0);
             if (pass) {
-              const float y0 = sm_f[yo + j0 + jj];
-              const float x = maximize ? -y0 : y0;
-              const double val = fx(po, x, b_obj);
-              Entry e;
-              e.key = skey(maximize ? val : -val);
-              e.g = gb + (unsigned long long)(col_base + j0 + (int)jj);
               const unsigned long long idx = cbase + __popc(m & ((1u << lane) - 1u));
               if (idx < cap) buf[idx] = e;
-              const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+              const unsigned hb = cand_bin(ctl, e.key, e.g, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
               atomicAdd(&hist[hb], 1u);
               atomicAdd(&Q.coarse[hb >> 8], 1u);
             }
@@ -1680,19 +1723,22 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
       }
       admitted += ok ? 1u : 0u;
+      Entry e;
+      if (pass) {
+        const double val = fx(po, xo, b_obj);
+        e.key = skey(maximize ? val : -val);
+        e.g = gb + (unsigned long long)col;
+        pass = !tie_reject(ctl, e.key, e.g);
+      }
       const unsigned mk = __ballot_sync(0xffffffffu, pass);
       if (!mk) continue;
       unsigned long long cbase = 0;
       if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
       cbase = __shfl_sync(0xffffffffu, cbase, 0);
       if (pass) {
-        const double val = fx(po, xo, b_obj);
-        Entry e;
-        e.key = skey(maximize ? val : -val);
-        e.g = gb + (unsigned long long)col;
         const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
         if (idx < Q.cap) Q.buf[idx] = e;
-        const unsigned hb = hist_bin(e.key, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+        const unsigned hb = cand_bin(ctl, e.key, e.g, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
         atomicAdd(&Q.hist[hb], 1u);
         atomicAdd(&Q.coarse[hb >> 8], 1u);
       }
@@ -1974,6 +2020,7 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
       if (auto_kernel == 3) ctl->use_full = 0u;  // no full-predicate launch in this pass
     }
   } else {
+    if (*(volatile unsigned int*)&ctl->tie_on) return;  // tie mode: bins are g ranges (finalize_small_kernel)
     const int B = kth_two_level(Q.hist, Q.coarse, k, &cnt);
     if (lead) {
       if (mode == 1) {
@@ -2341,11 +2388,51 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
     unsigned long long cnt_ge = 0;
     const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, &cnt_ge);
     if (threadIdx.x == 0) {
-      const unsigned long long bound = B >= 0 ? bin_edge((unsigned)B, ctl->hist_base, ctl->hist_shift) : 0ull;
+      const bool tie = ctl->tie_on != 0;
+      const unsigned long long base = ctl->hist_base;
+      const unsigned shift = ctl->hist_shift;
+      unsigned long long bound = B >= 0 ? bin_edge((unsigned)B, base, shift) : 0ull;
+      if (tie) {  // every admitted product has key >= K; the select orders them exactly
+        bound = ctl->tie_key;
+        cnt_ge = ctl->count;
+      }
       ctl->bound_key = bound;
       ctl->comp_count = cnt_ge;
       s_bound = bound;
       s_valid = cnt_ge;
+      // overflow (count > cap): parameters of the exact re-run (capi.cu
+      // check_batch).  Every step either narrows the key bins holding the
+      // k-th best by 16 bits, or — once that bin is one exact key K — bins
+      // the tied products by g and narrows the admitted g range by 16 bits,
+      // so the admitted set shrinks to at most k + one bin.
+      if (ctl->count > Q.cap && B >= 0) {
+        if (!tie) {
+          if (B == 65535) {  // the absorbing top bin: re-spread [edge, 2^64) over the bins
+            unsigned s2 = shift;
+            while (s2 < 63 && ((~0ull - bound) >> s2) >= 65535ull) ++s2;
+            ctl->nx_tau = bound;
+            ctl->nx_base = bound;
+            ctl->nx_shift = s2;
+          } else if (shift == 0) {  // bin B is the single key K = bound
+            ctl->nx_tau = bound;
+            ctl->nx_tie = 1;
+            ctl->nx_tie_enter = 1;
+          } else {
+            ctl->nx_tau = bound;
+            ctl->nx_base = bound;
+            ctl->nx_shift = shift >= 16 ? shift - 16 : 0u;
+          }
+        } else {
+          const unsigned gs = ctl->tie_gshift;
+          const unsigned long long glo = ctl->tie_gbase + ((unsigned long long)(65534 - min(B, 65534)) << gs);
+          const unsigned long long ghi = glo + (1ull << gs);
+          ctl->nx_tau = ctl->tie_key;
+          ctl->nx_tie = 1;
+          ctl->nx_gbase = glo;
+          ctl->nx_glimit = (ghi > glo && ghi < ctl->tie_glimit) ? ghi : ctl->tie_glimit;
+          ctl->nx_gshift = gs >= 16 ? gs - 16 : 0u;
+        }
+      }
     }
   }
   __syncthreads();

@@ -174,21 +174,39 @@ class _Bound:
         self.task_names = list(table.task_names)
 
 
-_BOUND: dict[tuple[int, int, int], tuple[weakref.ref, weakref.ref, _Bound]] = {}
+_BOUND: dict[tuple[int, int, int], tuple[weakref.ref, weakref.ref, _Bound, tuple]] = {}
 _MAX_BOUND = 4
 
 
+def _content_token(table) -> tuple:
+    """Cheap identity of the table's current contents: the arrays' buffers and
+    shapes plus a CRC of a strided sample of the values and all biases.  The
+    reference re-reads the table on every call (engine.py:285); a device copy
+    must not survive an in-place edit or a reassignment of values/biases."""
+    import zlib
+
+    v = np.asarray(table.values)
+    bias = np.asarray(table.biases)
+    flat = v.reshape(-1)
+    step = max(1, flat.size // 4096)
+    sample = np.ascontiguousarray(flat[::step])
+    return (v.__array_interface__["data"][0], v.shape, v.dtype.str, bias.__array_interface__["data"][0],
+            zlib.crc32(sample.tobytes(), zlib.crc32(np.ascontiguousarray(bias).tobytes())))
+
+
 def bind(library, table, device: int | None = None) -> _Bound:
-    """Device context for (library, table), created on first use and reused."""
+    """Device context for (library, table), created on first use and reused
+    while the table's contents are unchanged (see _content_token)."""
     dev = default_device() if device is None else device
     key = (id(library), id(table), dev)
+    token = _content_token(table)
     hit = _BOUND.get(key)
-    if hit is not None and hit[0]() is library and hit[1]() is table:
+    if hit is not None and hit[0]() is library and hit[1]() is table and hit[3] == token:
         return hit[2]
     b = _Bound(library, table, dev)
-    if len(_BOUND) >= _MAX_BOUND:
+    if len(_BOUND) >= _MAX_BOUND and key not in _BOUND:
         _BOUND.pop(next(iter(_BOUND)))
-    _BOUND[key] = (weakref.ref(library), weakref.ref(table), b)
+    _BOUND[key] = (weakref.ref(library), weakref.ref(table), b, token)
     return b
 
 

@@ -235,3 +235,12 @@ def to_native(q: dict, start: int, end: int) -> dict:
     return {"obj": TASKS.index(q["objective"]), "maximize": q["direction"] == "maximize",
             "cons": [(TASKS.index(t), lo, hi) for t, lo, hi in q["constraints"]], "k": q["k"],
             "start": start, "end": end}
+
+
+def build_model(shape: Shape, seed: int = 1, n_sample: int = 20000):
+    """The benchmark model of a shape: synthetic pair-embedding cache, random
+    heads, property heads calibrated on a uniform product sample."""
+    u = random_cache(shape.n_pairs, seed=seed)
+    w, b = random_heads(seed=seed)
+    w, b = calibrate_heads(shape, u, w, b, n_sample=n_sample, seed=seed)
+    return u, w, b

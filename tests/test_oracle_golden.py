@@ -48,3 +48,55 @@ def test_sharded_merge_is_exact(shards):
             a = orc.search_topk(case.values, case.biases, lib, q, start, end)
             b = orc.search_topk_sharded(case.values, case.biases, lib, q, start, end, shards)
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2:] == b[2:]
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_c_oracle_matches_reference(threads):
+    """The threaded C restatement (oracle/scan_oracle.c, the scale checker)
+    reproduces every golden query recorded from the reference, bit for bit."""
+    from oracle import fast_oracle as fo
+
+    fo.build()
+    for case in golden_cases():
+        lib = case.lib_arrays()
+        for qd in case.queries:
+            q = case.oracle_query(qd)
+            rng = qd["query"]["index_range"]
+            start, end = rng if rng is not None else (0, lib.total)
+            s, g, ret, disc, scanned = fo.search_topk(case.values, case.biases, lib, q, start, end, threads=threads)
+            assert (ret, disc, scanned) == (qd["retained"], qd["discarded"], qd["scanned"])
+            assert [int(x) for x in g] == [e[0] for e in qd["entries"]]
+            obj = s if q.maximize else -s
+            assert [x.hex() for x in obj.tolist()] == [unhex(e[1]).hex() for e in qd["entries"]]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_c_oracle_matches_numpy_port(seed):
+    """C oracle == numpy oracle on random libraries (2/3/4-component reactions,
+    ragged sub-ranges, constraints with both bounds, k past the feasible count)."""
+    from oracle import fast_oracle as fo
+
+    rng = np.random.default_rng(100 + seed)
+    sizes, pair_off, p = [], [], 0
+    for _ in range(int(rng.integers(3, 8))):
+        c = int(rng.integers(1, 5))
+        s = [int(x) for x in rng.integers(2, 30 if c > 2 else 200, size=c)]
+        sizes.append(s)
+        pair_off.append([p + sum(s[:j]) for j in range(c)])
+        p += sum(s)
+    values = rng.standard_normal((4, p)).astype(np.float32)
+    if seed % 2:
+        values = np.round(values * 2).astype(np.float32)  # integer-valued: exact ties and bounds hit exactly
+    biases = rng.standard_normal(4)
+    lib = orc.Lib(sizes, pair_off)
+    for trial in range(6):
+        a = int(rng.integers(0, lib.total // 3))
+        b = int(rng.integers(2 * lib.total // 3, lib.total + 1))
+        cons = [(int(rng.integers(0, 4)), float(rng.normal(-1, 0.5)), float(rng.normal(1, 0.5)))
+                for _ in range(int(rng.integers(0, 3)))]
+        cons = [c for c in cons if c[1] < c[2]]
+        q = orc.Query(int(rng.integers(0, 4)), bool(rng.integers(0, 2)), cons, int(rng.integers(1, 400)))
+        x = orc.search_topk(values, biases, lib, q, a, b)
+        y = fo.search_topk(values, biases, lib, q, a, b, threads=int(rng.integers(1, 6)))
+        assert np.array_equal(x[0].view(np.uint64), y[0].view(np.uint64)) and np.array_equal(x[1], y[1])
+        assert x[2:] == y[2:]
