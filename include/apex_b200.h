@@ -111,6 +111,8 @@ typedef struct {
   int64_t admitted;        /* products that passed the admission test (admission-first kernel) */
   double host_prepare_us;  /* host time of descriptor checks / staging in the call */
   double host_launch_us;   /* host time of the launches (graph replay or direct) */
+  int64_t stale_sources;   /* merge: gathered local results marked stale (a source
+                              overflowed and re-ran: gather and merge again) */
 } apex_stats;
 
 /* Caller-allocated host output for one query; arrays sized for k entries
@@ -208,6 +210,39 @@ int apex_merge_finalize(apex_ctx* ctx, const apex_query_spec* query, const apex_
 int apex_merge_finalize_batch(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,
                               const apex_entry* entries_dev, int32_t n_src, int64_t stride,
                               uint64_t total_scanned, apex_result* results, apex_stats* stats);
+
+/* Multi-GPU local step, asynchronous form (one process per GPU): enqueues
+ * the exact local pipeline of a batch (queries share range; 1 <= k <= stride)
+ * and the export of each query's selected entries to out_dev + q*stride
+ * (device; unused slots padded with g == UINT64_MAX) on the context stream,
+ * with no host sync, so an all-gather and apex_merge_finalize_batch can be
+ * enqueued behind it.  apex_query_local_finish then syncs and validates: if a
+ * candidate buffer overflowed the batch is re-run exactly, re-exported and
+ * *rerun = 1 (the caller must gather and merge again); counts (optional) =
+ * entries selected per query. */
+int apex_query_local_async(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries, apex_entry* out_dev,
+                           int64_t stride, apex_stats* stats);
+int apex_query_local_finish(apex_ctx* ctx, int64_t* counts_host, int32_t* rerun, apex_stats* stats);
+
+/* Multi-GPU context: ONE process and host thread driving n_devices GPUs
+ * (SURVEY.md §8b "one host thread drives all devices").  Every query batch's
+ * index range is cut into n_devices contiguous g ranges; each device runs the
+ * exact local top-k; the merge on device_ids[0] reads every shard's entries
+ * through peer pointers over NVLink inside its load kernel (the gather fused
+ * into the merge) and materializes the global result.  A device id may repeat
+ * (several shards on one GPU).  Results are identical to apex_query on one
+ * device.  Result arrays must be caller-allocated (no view mode). */
+typedef struct apex_multi apex_multi;
+int apex_multi_create(int32_t n_devices, const int32_t* device_ids, apex_multi** out);
+void apex_multi_destroy(apex_multi* m);
+int apex_multi_load_library(apex_multi* m, const apex_reaction* reactions, int32_t n_reactions, int64_t n_pairs);
+int apex_multi_load_table(apex_multi* m, const float* values, const double* biases, int32_t n_tasks, int64_t n_pairs);
+int apex_multi_load_cache(apex_multi* m, const double* u, int64_t n_pairs, int32_t d, const double* head_w,
+                          const double* head_b, int32_t n_tasks, float* values_out);
+int apex_multi_set_option(apex_multi* m, const char* name, int64_t value);
+int apex_multi_query(apex_multi* m, const apex_query_spec* queries, int32_t n_queries, apex_result* results,
+                     apex_stats* stats);
+int apex_multi_info(apex_multi* m, int32_t* n_devices, int32_t* peer_access);
 
 /* Tuning / introspection. */
 int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);

@@ -28,6 +28,9 @@ EXPORTED = (
     "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_merge_finalize_batch",
     "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
+    "apex_query_local_async", "apex_query_local_finish",
+    "apex_multi_create", "apex_multi_destroy", "apex_multi_load_library", "apex_multi_load_table",
+    "apex_multi_load_cache", "apex_multi_set_option", "apex_multi_query", "apex_multi_info",
 )
 
 
@@ -90,6 +93,7 @@ class Stats(C.Structure):
         ("admitted", C.c_int64),
         ("host_prepare_us", C.c_double),
         ("host_launch_us", C.c_double),
+        ("stale_sources", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -149,6 +153,16 @@ def load_library(path: Path | None = None):
                                  C.POINTER(Stats)], C.c_int),
         "apex_merge_finalize_batch": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int32, C.c_int64, C.c_uint64,
                                        C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
+        "apex_query_local_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int64, C.POINTER(Stats)], C.c_int),
+        "apex_query_local_finish": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(Stats)], C.c_int),
+        "apex_multi_create": ([C.c_int32, C.POINTER(C.c_int32), C.POINTER(vp)], C.c_int),
+        "apex_multi_destroy": ([vp], None),
+        "apex_multi_load_library": ([vp, C.POINTER(Reaction), C.c_int32, C.c_int64], C.c_int),
+        "apex_multi_load_table": ([vp, vp, vp, C.c_int32, C.c_int64], C.c_int),
+        "apex_multi_load_cache": ([vp, vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, vp], C.c_int),
+        "apex_multi_set_option": ([vp, C.c_char_p, C.c_int64], C.c_int),
+        "apex_multi_query": ([vp, C.POINTER(QuerySpecC), C.c_int32, C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
+        "apex_multi_info": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
         "apex_set_option": ([vp, C.c_char_p, C.c_int64], C.c_int),
         "apex_get_device_info": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
         "apex_debug_thresholds": ([vp, vp, vp, vp, C.c_int64, vp, vp], C.c_int),
@@ -404,6 +418,26 @@ class DeviceContext:
         del keep
         return [counts[i] for i in range(len(queries))], st.as_dict()
 
+    def query_local_async(self, queries: list[dict], out_dev_ptr: int, stride: int) -> dict:
+        """Enqueue the local step + padded export ([query][stride] entries at
+        out_dev_ptr) on the context stream; no host sync (apex_query_local_async)."""
+        specs, keep = self._specs(queries)
+        st = Stats()
+        _check(self.lib.apex_query_local_async(self._ctx, specs, len(queries), C.c_void_p(out_dev_ptr), int(stride),
+                                               C.byref(st)))
+        self._local_n = len(queries)
+        del keep
+        return st.as_dict()
+
+    def query_local_finish(self) -> tuple[list[int], bool, dict]:
+        """Validate the local step in flight: (counts, rerun, stats); rerun is
+        True when an overflow forced an exact re-run (gather + merge again)."""
+        counts = (C.c_int64 * self._local_n)()
+        rerun = C.c_int32(0)
+        st = Stats()
+        _check(self.lib.apex_query_local_finish(self._ctx, counts, C.byref(rerun), C.byref(st)))
+        return [counts[i] for i in range(self._local_n)], bool(rerun.value), st.as_dict()
+
     def merge_finalize_batch(self, queries: list[dict], entries_dev_ptr: int, n_src: int, stride: int,
                              total_scanned: int, prepared: "PreparedBatch | None" = None):
         """Global top-k of every query from all-gathered local entries laid out
@@ -458,3 +492,72 @@ class DeviceContext:
         n = C.c_int64(0)
         _check(self.lib.apex_debug_trace(self._ctx, _ptr(out), cap, C.byref(n)))
         return out[:n.value]
+
+
+class MultiDeviceContext:
+    """Owns one apex_multi: one process and host thread driving several GPUs
+    (index range sharded per device, exact local top-k per device, merge on the
+    first device with the gather fused into its load kernel over NVLink peer
+    pointers).  Same query results as DeviceContext; device ids may repeat."""
+
+    def __init__(self, devices: list[int]):
+        self.lib = load_library()
+        self._m = C.c_void_p()
+        ids = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        _check(self.lib.apex_multi_create(len(devices), ids, C.byref(self._m)))
+        self.devices = list(devices)
+
+    def close(self) -> None:
+        if self._m:
+            self.lib.apex_multi_destroy(self._m)
+            self._m = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> tuple[int, bool]:
+        n, peer = C.c_int32(), C.c_int32()
+        _check(self.lib.apex_multi_info(self._m, C.byref(n), C.byref(peer)))
+        return n.value, bool(peer.value)
+
+    def set_option(self, name: str, value: int) -> None:
+        _check(self.lib.apex_multi_set_option(self._m, name.encode(), int(value)))
+
+    def load_library(self, sizes, pair_offsets, g_offsets, n_pairs) -> None:
+        n = len(sizes)
+        arr = (Reaction * max(n, 1))()
+        for t in range(n):
+            c = len(sizes[t])
+            if c > MAX_RGROUPS:
+                raise NativeError(APEX_ELIMIT, f"reaction {t} has {c} R-groups (max {MAX_RGROUPS})")
+            arr[t].n_rgroups = c
+            for j in range(c):
+                arr[t].sizes[j] = int(sizes[t][j])
+                arr[t].pair_offset[j] = int(pair_offsets[t][j])
+            arr[t].g_offset = int(g_offsets[t])
+        _check(self.lib.apex_multi_load_library(self._m, arr, n, int(n_pairs)))
+
+    def load_table(self, values: np.ndarray, biases: np.ndarray) -> None:
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        b = np.ascontiguousarray(biases, dtype=np.float64)
+        _check(self.lib.apex_multi_load_table(self._m, _ptr(v), _ptr(b), v.shape[0], v.shape[1]))
+
+    def load_cache(self, u: np.ndarray, head_w: np.ndarray, head_b: np.ndarray) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        w = np.ascontiguousarray(head_w, dtype=np.float64)
+        b = np.ascontiguousarray(head_b, dtype=np.float64)
+        out = np.empty((w.shape[0], u.shape[0]), dtype=np.float32)
+        _check(self.lib.apex_multi_load_cache(self._m, _ptr(u), u.shape[0], u.shape[1], _ptr(w), _ptr(b), w.shape[0],
+                                              _ptr(out)))
+        return out
+
+    def query(self, queries: list[dict]) -> tuple[list[dict], dict]:
+        specs, keep = DeviceContext._specs(queries)
+        results, bufs = DeviceContext._result_buffers(queries)
+        st = Stats()
+        _check(self.lib.apex_multi_query(self._m, specs, len(queries), results, C.byref(st)))
+        del keep
+        return DeviceContext._unpack(results, bufs), st.as_dict()

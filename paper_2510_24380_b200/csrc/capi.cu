@@ -169,6 +169,10 @@ struct Batch {
   Plan* plan = nullptr;
   Plan* plan_rows = nullptr;    // whole-row tiles (sorted-column admission kernel)
   bool pending = false;
+  // multi-GPU local step (apex_query_local_async): where the selected entries
+  // are exported, with what per-query stride
+  Entry* export_out = nullptr;
+  unsigned long long export_stride = 0;
   RunStats st;
 };
 
@@ -1299,6 +1303,172 @@ int copy_results(apex_ctx* c, const apex_query_spec* qs, int nq, apex_result* re
   return APEX_OK;
 }
 
+// Multi-GPU local step, enqueue half: the exact local pipeline of a batch
+// (queries share range and, for the export layout, a stride >= every k) and
+// the export of each query's selected entries to out + slot * stride (padded),
+// all on the context stream with no host sync.
+int local_enqueue(apex_ctx* c, const apex_query_spec* qs, int nq, Entry* out, unsigned long long stride) {
+  APEX_TRY(prepare_batch(c, qs, nq, false));
+  APEX_TRY(launch_batch(c));
+  c->batch.export_out = out;
+  c->batch.export_stride = stride;
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  const unsigned gx = (unsigned)std::min<unsigned long long>((stride + 255) / 256, 1024);
+  export_kernel<<<dim3(gx, nq), 256, 0, c->stream>>>(dq, out, stride);
+  APEX_CU(cudaGetLastError());
+  ++c->batch.st.launches;
+  return APEX_OK;
+}
+
+// Multi-GPU local step, validate half: sync, and if a candidate buffer
+// overflowed re-run exactly (check_batch) and export again; *rerun = 1 then
+// (the entries a peer read before are stale).  counts (optional, caller's
+// query order) = entries selected per query.
+int local_finish(apex_ctx* c, int64_t* counts, int* rerun) {
+  Batch& B = c->batch;
+  if (!B.pending) return set_err(APEX_ESTATE, "no local step in flight");
+  const int64_t retries0 = B.st.retries;
+  APEX_TRY(check_batch(c));
+  const bool again = B.st.retries != retries0;
+  if (again) {
+    const unsigned gx = (unsigned)std::min<unsigned long long>((B.export_stride + 255) / 256, 1024);
+    export_kernel<<<dim3(gx, B.nq), 256, 0, c->stream>>>(c->d_queries.as<ScanQuery>(), B.export_out,
+                                                         B.export_stride);
+    APEX_CU(cudaGetLastError());
+    ++B.st.launches;
+    APEX_CU(cudaStreamSynchronize(c->stream));
+  }
+  if (rerun) *rerun = again ? 1 : 0;
+  if (counts)
+    for (int i = 0; i < B.nq; ++i) counts[B.perm[i]] = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
+  return APEX_OK;
+}
+
+// Exact merge of gathered local entries (one device pass for a batch): the
+// entries of query q from source r are entries[(r * nq + q) * stride + i]
+// (one contiguous all-gathered buffer), or srcs[r][q * stride + i] when srcs
+// (a device array of n_src device pointers, possibly peers) is given.
+// Selects, orders and materializes every query's global top-k into res.
+int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entries, const Entry* const* srcs,
+               int n_src, int64_t stride, uint64_t total_scanned, apex_result* res, apex_stats* stats) {
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    if (q.objective_task < 0 || q.objective_task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+    if (q.n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+    if (q.k < 0) return set_err(APEX_EINVAL, "k must be >= 0");
+    for (int m = 0; m < q.n_constraints; ++m)
+      if (q.constraints[m].task < 0 || q.constraints[m].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+  }
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const int64_t n_in = (int64_t)n_src * stride;
+  bool any = false;
+  for (int i = 0; i < nq; ++i) {
+    res[i].scanned = total_scanned;
+    if (qs[i].k == 0 || n_in == 0) {
+      res[i].n = 0;
+      res[i].candidates = res[i].admitted = 0;
+      res[i].full_predicate = 0;
+      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
+    } else {
+      any = true;
+    }
+  }
+  if (!any) return APEX_OK;
+  // one slot per query: candidate buffer = every gathered entry of the query
+  if ((int)c->slots.size() < nq) c->slots.resize(nq);
+  int64_t k_max = 1;
+  for (int i = 0; i < nq; ++i) {
+    Slot& S = c->slots[i];
+    const int64_t k = std::max<int64_t>(qs[i].k, 1);
+    k_max = std::max(k_max, k);
+    APEX_TRY(S.buf.ensure((size_t)std::max<int64_t>(n_in, 1024) * sizeof(Entry)));
+    APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
+    APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
+  }
+  APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
+  APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
+  c->out_off.assign(nq + 1, 0);
+  for (int i = 0; i < nq; ++i)
+    c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
+  APEX_TRY(c->d_out.ensure(c->out_off[nq]));
+  const size_t qbytes = (size_t)nq * sizeof(ScanQuery);
+  APEX_TRY(c->d_queries.ensure(qbytes));
+  APEX_CU(cudaEventSynchronize(c->upload_ev));
+  APEX_TRY(c->h_queries.ensure(qbytes));
+  APEX_TRY(c->h_ctl.ensure((size_t)nq * sizeof(QCtl)));
+  c->uploaded.clear();
+  c->batch.pending = false;
+  ScanQuery* hq = c->h_queries.as<ScanQuery>();
+  for (int i = 0; i < nq; ++i) {
+    const apex_query_spec& q = qs[i];
+    Slot& S = c->slots[i];
+    ScanQuery& Q = hq[i];
+    std::memset(&Q, 0, sizeof(Q));
+    const int64_t kk = std::max<int64_t>(q.k, 1);
+    Q.buf = S.buf.as<Entry>();
+    Q.sel = S.sel.as<Entry>();
+    Q.sorted = S.sorted.as<Entry>();
+    Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
+    Q.coarse = Q.hist + kHistBins;
+    Q.seed_hist = Q.coarse + 256;
+    Q.ctl = c->d_ctls.as<QCtl>() + i;
+    Q.cap = S.buf.bytes / sizeof(Entry);
+    Q.refresh_shift = 62;
+    Q.k = std::max<int64_t>(q.k, 1);  // k == 0 queries are reported empty below
+    Q.maximize = q.maximize ? 1 : 0;
+    Q.obj_task = q.objective_task;
+    Q.n_cons = q.n_constraints;
+    for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
+    unsigned char* o = c->d_out.as<unsigned char>() + c->out_off[i];
+    Q.out_g = reinterpret_cast<unsigned long long*>(o);
+    Q.out_obj = reinterpret_cast<double*>(o + 8 * kk);
+    Q.out_cons = reinterpret_cast<double*>(o + 16 * kk);
+    Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
+    Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
+  }
+  cudaStream_t s = c->stream;
+  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
+  RunStats st;
+  APEX_CU(cudaEventRecord(c->ev[0], s));
+  APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
+  APEX_CU(cudaEventRecord(c->upload_ev, s));
+  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u);
+  if (n_in > 0) {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_in + 255) / 256, 4 * c->sm_count / std::max(nq, 1) + 1));
+    merge_load_kernel<<<dim3(gx, nq), 256, 0, s>>>(dq, entries, n_src, nq, (unsigned long long)stride, srcs);
+  }
+  st.launches = 2;
+  // bound_key = 0 (init): every loaded entry is a candidate
+  APEX_TRY(enqueue_select(c, dq, nq, k_max, true, st, s, false, false));
+  APEX_CU(cudaGetLastError());
+  APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
+                            cudaMemcpyDeviceToHost, s));
+  APEX_CU(cudaEventRecord(c->ev[1], s));
+  std::vector<apex_query_spec> qq(qs, qs + nq);
+  for (auto& x : qq) {
+    x.start = 0;
+    x.end = total_scanned;
+  }
+  APEX_TRY(copy_results(c, qq.data(), nq, res, nullptr));
+  for (int i = 0; i < nq; ++i)
+    if (qs[i].k == 0 || n_in == 0) {
+      res[i].n = 0;
+      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
+    }
+  if (stats) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    stats->select_ms = ms;
+    stats->total_ms = ms;
+    stats->kernel_launches = st.launches;
+    stats->d2h_bytes = (int64_t)c->out_off[nq] + (int64_t)nq * (int64_t)offsetof(QCtl, hist);
+    stats->h2d_bytes = (int64_t)qbytes;
+    for (int i = 0; i < nq; ++i) stats->stale_sources += c->h_ctl.as<QCtl>()[i].stale ? 1 : 0;
+  }
+  return APEX_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1697,22 +1867,51 @@ int apex_query_local(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_en
     for (int i = 0; i < nq; ++i) counts[i] = 0;
     return APEX_OK;
   }
-  APEX_TRY(prepare_batch(c, qs, nq, false));
-  APEX_TRY(launch_batch(c));
-  APEX_TRY(check_batch(c));
-  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
-  export_kernel<<<dim3((unsigned)((k + 255) / 256), nq), 256, 0, c->stream>>>(dq, reinterpret_cast<Entry*>(out_dev));
-  APEX_CU(cudaGetLastError());
+  APEX_TRY(local_enqueue(c, qs, nq, reinterpret_cast<Entry*>(out_dev), (unsigned long long)k));
+  APEX_TRY(local_finish(c, counts, nullptr));
   APEX_CU(cudaStreamSynchronize(c->stream));
   int64_t cand = 0;
-  for (int i = 0; i < nq; ++i) {
-    counts[c->batch.perm[i]] = (int64_t)c->h_ctl.as<QCtl>()[i].sel_count;
-    cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
-  }
+  for (int i = 0; i < nq; ++i) cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
   float total = 0;
   for (int e = 0; e < 5; ++e) total += c->batch.st.ms[e];
-  c->batch.st.launches += 1;
   fill_stats(stats, c->batch.st, 0.f, total, cand);
+  return APEX_OK;
+}
+
+int apex_query_local_async(apex_ctx* c, const apex_query_spec* qs, int32_t nq, apex_entry* out_dev, int64_t stride,
+                           apex_stats* stats) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, true));
+  APEX_TRY(validate_queries(c, qs, nq));
+  if (nq < 1 || !out_dev) return set_err(APEX_EINVAL, "apex_query_local_async: queries and an output buffer required");
+  for (int i = 0; i < nq; ++i) {
+    if (qs[i].start != qs[0].start || qs[i].end != qs[0].end)
+      return set_err(APEX_EINVAL, "apex_query_local_async: all queries must share one index range");
+    if (qs[i].k < 1 || qs[i].k > stride) return set_err(APEX_EINVAL, "apex_query_local_async: need 1 <= k <= stride");
+  }
+  if (qs[0].end == qs[0].start) return set_err(APEX_EINVAL, "apex_query_local_async: empty range");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  APEX_TRY(local_enqueue(c, qs, nq, reinterpret_cast<Entry*>(out_dev), (unsigned long long)stride));
+  if (stats) {
+    stats->kernel_launches = c->batch.st.launches;
+    stats->h2d_bytes = c->batch.st.h2d_bytes;
+  }
+  return APEX_OK;
+}
+
+int apex_query_local_finish(apex_ctx* c, int64_t* counts, int32_t* rerun, apex_stats* stats) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, true));
+  int again = 0;
+  APEX_TRY(local_finish(c, counts, &again));
+  if (rerun) *rerun = again;
+  if (stats) {
+    int64_t cand = 0;
+    for (int i = 0; i < c->batch.nq; ++i) cand += (int64_t)c->h_ctl.as<QCtl>()[i].count;
+    float total = 0;
+    for (int e = 0; e < 5; ++e) total += c->batch.st.ms[e];
+    fill_stats(stats, c->batch.st, 0.f, total, cand);
+  }
   return APEX_OK;
 }
 
@@ -1724,121 +1923,8 @@ int apex_merge_finalize_batch(apex_ctx* c, const apex_query_spec* qs, int32_t nq
   if (nq < 0 || n_src < 0 || stride < 0 || (nq > 0 && (!qs || !res)) ||
       (n_src > 0 && stride > 0 && nq > 0 && !entries_dev))
     return set_err(APEX_EINVAL, "bad merge arguments");
-  for (int i = 0; i < nq; ++i) {
-    const apex_query_spec& q = qs[i];
-    if (q.objective_task < 0 || q.objective_task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
-    if (q.n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
-    if (q.k < 0) return set_err(APEX_EINVAL, "k must be >= 0");
-    for (int m = 0; m < q.n_constraints; ++m)
-      if (q.constraints[m].task < 0 || q.constraints[m].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
-  }
-  if (stats) std::memset(stats, 0, sizeof(*stats));
-  const int64_t n_in = (int64_t)n_src * stride;
-  bool any = false;
-  for (int i = 0; i < nq; ++i) {
-    res[i].scanned = total_scanned;
-    if (qs[i].k == 0 || n_in == 0) {
-      res[i].n = 0;
-      res[i].candidates = res[i].admitted = 0;
-      res[i].full_predicate = 0;
-      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
-    } else {
-      any = true;
-    }
-  }
-  if (!any) return APEX_OK;
-  // one slot per query: candidate buffer = every gathered entry of the query
-  if ((int)c->slots.size() < nq) c->slots.resize(nq);
-  int64_t k_max = 1;
-  for (int i = 0; i < nq; ++i) {
-    Slot& S = c->slots[i];
-    const int64_t k = std::max<int64_t>(qs[i].k, 1);
-    k_max = std::max(k_max, k);
-    APEX_TRY(S.buf.ensure((size_t)std::max<int64_t>(n_in, 1024) * sizeof(Entry)));
-    APEX_TRY(S.sel.ensure((size_t)k * sizeof(Entry)));
-    APEX_TRY(S.sorted.ensure((size_t)k * sizeof(Entry)));
-  }
-  APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
-  APEX_TRY(c->d_ctls.ensure((size_t)nq * sizeof(QCtl)));
-  c->out_off.assign(nq + 1, 0);
-  for (int i = 0; i < nq; ++i)
-    c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
-  APEX_TRY(c->d_out.ensure(c->out_off[nq]));
-  const size_t qbytes = (size_t)nq * sizeof(ScanQuery);
-  APEX_TRY(c->d_queries.ensure(qbytes));
-  APEX_CU(cudaEventSynchronize(c->upload_ev));
-  APEX_TRY(c->h_queries.ensure(qbytes));
-  APEX_TRY(c->h_ctl.ensure((size_t)nq * sizeof(QCtl)));
-  c->uploaded.clear();
-  c->batch.pending = false;
-  ScanQuery* hq = c->h_queries.as<ScanQuery>();
-  for (int i = 0; i < nq; ++i) {
-    const apex_query_spec& q = qs[i];
-    Slot& S = c->slots[i];
-    ScanQuery& Q = hq[i];
-    std::memset(&Q, 0, sizeof(Q));
-    const int64_t kk = std::max<int64_t>(q.k, 1);
-    Q.buf = S.buf.as<Entry>();
-    Q.sel = S.sel.as<Entry>();
-    Q.sorted = S.sorted.as<Entry>();
-    Q.hist = c->d_hists.as<unsigned>() + (size_t)i * kHistWords;
-    Q.coarse = Q.hist + kHistBins;
-    Q.seed_hist = Q.coarse + 256;
-    Q.ctl = c->d_ctls.as<QCtl>() + i;
-    Q.cap = S.buf.bytes / sizeof(Entry);
-    Q.refresh_shift = 62;
-    Q.k = std::max<int64_t>(q.k, 1);  // k == 0 queries are reported empty below
-    Q.maximize = q.maximize ? 1 : 0;
-    Q.obj_task = q.objective_task;
-    Q.n_cons = q.n_constraints;
-    for (int m = 0; m < q.n_constraints; ++m) Q.cons_task[m] = q.constraints[m].task;
-    unsigned char* o = c->d_out.as<unsigned char>() + c->out_off[i];
-    Q.out_g = reinterpret_cast<unsigned long long*>(o);
-    Q.out_obj = reinterpret_cast<double*>(o + 8 * kk);
-    Q.out_cons = reinterpret_cast<double*>(o + 16 * kk);
-    Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
-    Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
-  }
-  cudaStream_t s = c->stream;
-  const ScanQuery* dq = c->d_queries.as<ScanQuery>();
-  RunStats st;
-  APEX_CU(cudaEventRecord(c->ev[0], s));
-  APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
-  APEX_CU(cudaEventRecord(c->upload_ev, s));
-  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u);
-  if (n_in > 0) {
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_in + 255) / 256, 4 * c->sm_count / std::max(nq, 1) + 1));
-    merge_load_kernel<<<dim3(gx, nq), 256, 0, s>>>(dq, reinterpret_cast<const Entry*>(entries_dev), n_src, nq,
-                                                    (unsigned long long)stride);
-  }
-  st.launches = 2;
-  // bound_key = 0 (init): every loaded entry is a candidate
-  APEX_TRY(enqueue_select(c, dq, nq, k_max, true, st, s, false, false));
-  APEX_CU(cudaGetLastError());
-  APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
-                            cudaMemcpyDeviceToHost, s));
-  APEX_CU(cudaEventRecord(c->ev[1], s));
-  std::vector<apex_query_spec> qq(qs, qs + nq);
-  for (auto& x : qq) {
-    x.start = 0;
-    x.end = total_scanned;
-  }
-  APEX_TRY(copy_results(c, qq.data(), nq, res, nullptr));
-  for (int i = 0; i < nq; ++i)
-    if (qs[i].k == 0 || n_in == 0) {
-      res[i].n = 0;
-      res[i].discarded = (int64_t)std::min<uint64_t>((uint64_t)qs[i].k, total_scanned);
-    }
-  if (stats) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-    stats->select_ms = ms;
-    stats->total_ms = ms;
-    stats->kernel_launches = st.launches;
-    stats->d2h_bytes = (int64_t)c->out_off[nq];
-  }
-  return APEX_OK;
+  return merge_impl(c, qs, nq, reinterpret_cast<const Entry*>(entries_dev), nullptr, n_src, stride, total_scanned,
+                    res, stats);
 }
 
 int apex_merge_finalize(apex_ctx* c, const apex_query_spec* q, const apex_entry* entries_dev, int64_t n_entries,
@@ -1938,6 +2024,257 @@ int apex_debug_trace(apex_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
   if (m <= 0) return APEX_OK;
   APEX_CU(cudaStreamSynchronize(c->stream));
   APEX_CU(cudaMemcpy(out, c->d_trace.p, (size_t)m * 64, cudaMemcpyDeviceToHost));
+  return APEX_OK;
+}
+
+// ===========================================================================
+// Multi-GPU context (one process, one host thread, N devices)
+// ===========================================================================
+// Shards the index range of every query batch into N contiguous g ranges, one
+// per device; each device runs its exact local top-k and exports it (padded
+// [query][stride] entries) into its own HBM; the merge context on the first
+// device waits on the shards' events and runs the exact merge with the
+// gather FUSED into its load kernel: merge_load_kernel reads every shard's
+// entries through peer pointers over NVLink (no staging copy, no separate
+// collective).  Without peer access the entries are staged with
+// cudaMemcpyPeerAsync first.  One host sync per batch; a shard whose candidate
+// buffer overflowed re-runs exactly and the merge is repeated.
+}  // extern "C"
+
+struct apex_multi {
+  std::vector<int> dev;               // device of each shard
+  std::vector<apex_ctx*> shard;       // local-step context per shard
+  apex_ctx* merge = nullptr;          // merge + materialization context (first device)
+  std::vector<DBuf> exp;              // per shard: exported entries (on the shard's device)
+  std::vector<cudaEvent_t> done;      // per shard: local step + export enqueued
+  DBuf d_srcs, d_stage;               // first device: shard pointer array / staged entries
+  HBuf h_srcs;
+  bool peer = true;
+  std::recursive_mutex mu;
+};
+
+extern "C" {
+
+static int multi_create(int32_t n_devices, const int32_t* device_ids, apex_multi* m);
+
+int apex_multi_create(int32_t n_devices, const int32_t* device_ids, apex_multi** out) {
+  if (!out || n_devices < 1 || !device_ids) return set_err(APEX_EINVAL, "bad multi-device arguments");
+  *out = nullptr;
+  apex_multi* m = new apex_multi();
+  const int rc = multi_create(n_devices, device_ids, m);
+  if (rc != APEX_OK) {
+    const std::string err = t_err;
+    apex_multi_destroy(m);
+    t_err = err;
+    return rc;
+  }
+  *out = m;
+  return APEX_OK;
+}
+
+static int multi_create(int32_t n_devices, const int32_t* device_ids, apex_multi* m) {
+  for (int i = 0; i < n_devices; ++i) {
+    apex_ctx* c = nullptr;
+    APEX_TRY(apex_ctx_create(device_ids[i], nullptr, &c));
+    m->shard.push_back(c);
+    m->dev.push_back(device_ids[i]);
+    m->exp.emplace_back();
+    cudaEvent_t e = nullptr;
+    APEX_CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m->done.push_back(e);
+  }
+  APEX_TRY(apex_ctx_create(device_ids[0], nullptr, &m->merge));
+  for (int i = 1; i < n_devices; ++i) {
+    if (device_ids[i] == device_ids[0]) continue;
+    int can = 0;
+    APEX_CU(cudaDeviceCanAccessPeer(&can, device_ids[0], device_ids[i]));
+    if (!can) {
+      m->peer = false;
+      continue;
+    }
+    APEX_CU(cudaSetDevice(device_ids[0]));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(device_ids[i], 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return set_err(APEX_ECUDA, std::string("peer access: ") + cudaGetErrorString(e));
+  }
+  return APEX_OK;
+}
+
+void apex_multi_destroy(apex_multi* m) {
+  if (!m) return;
+  for (size_t i = 0; i < m->shard.size(); ++i) {
+    cudaSetDevice(m->dev[i]);
+    if (m->shard[i]) cudaStreamSynchronize(m->shard[i]->stream);
+    if (i < m->exp.size()) m->exp[i].release();
+    if (i < m->done.size() && m->done[i]) cudaEventDestroy(m->done[i]);
+  }
+  if (m->merge) {
+    cudaSetDevice(m->merge->device);
+    cudaStreamSynchronize(m->merge->stream);
+    m->d_srcs.release();
+    m->d_stage.release();
+  }
+  m->h_srcs.release();
+  for (apex_ctx* c : m->shard) apex_ctx_destroy(c);
+  if (m->merge) apex_ctx_destroy(m->merge);
+  delete m;
+}
+
+int apex_multi_load_library(apex_multi* m, const apex_reaction* rx, int32_t n_rx, int64_t n_pairs) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  for (apex_ctx* c : m->shard) APEX_TRY(apex_load_library(c, rx, n_rx, n_pairs));
+  return apex_load_library(m->merge, rx, n_rx, n_pairs);
+}
+
+int apex_multi_load_table(apex_multi* m, const float* values, const double* biases, int32_t n_tasks, int64_t n_pairs) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  for (apex_ctx* c : m->shard) APEX_TRY(apex_load_table(c, values, biases, n_tasks, n_pairs));
+  return apex_load_table(m->merge, values, biases, n_tasks, n_pairs);
+}
+
+// K1 once, on the first device; the table then becomes resident on every device.
+int apex_multi_load_cache(apex_multi* m, const double* u, int64_t n_pairs, int32_t d, const double* head_w,
+                          const double* head_b, int32_t n_tasks, float* values_out) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  std::vector<float> own;
+  float* v = values_out;
+  if (!v) {
+    own.resize((size_t)std::max<int64_t>(n_tasks, 1) * std::max<int64_t>(n_pairs, 1));
+    v = own.data();
+  }
+  APEX_TRY(apex_load_cache(m->merge, u, n_pairs, d, head_w, head_b, n_tasks, v));
+  for (apex_ctx* c : m->shard) APEX_TRY(apex_load_table(c, v, head_b, n_tasks, n_pairs));
+  return APEX_OK;
+}
+
+int apex_multi_set_option(apex_multi* m, const char* name, int64_t value) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  for (apex_ctx* c : m->shard) APEX_TRY(apex_set_option(c, name, value));
+  return APEX_OK;
+}
+
+int apex_multi_query(apex_multi* m, const apex_query_spec* qs, int32_t nq, apex_result* res, apex_stats* stats) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  std::lock_guard<std::recursive_mutex> lk(m->mu);
+  apex_ctx* M = m->merge;
+  APEX_TRY(check_ctx(M, true));
+  APEX_TRY(validate_queries(M, qs, nq));
+  if (nq > 0 && !res) return set_err(APEX_EINVAL, "null results");
+  for (int i = 0; i < nq; ++i)
+    if (!res[i].global_index || !res[i].objective || !res[i].constraint_values || !res[i].reaction || !res[i].digits)
+      return set_err(APEX_EINVAL, "apex_multi_query needs caller-allocated result arrays");
+  const auto t0 = std::chrono::steady_clock::now();
+  apex_stats agg;
+  std::memset(&agg, 0, sizeof(agg));
+  std::vector<int> order(nq);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return qs[a].start != qs[b].start ? qs[a].start < qs[b].start : qs[a].end < qs[b].end;
+  });
+  const int N = (int)m->shard.size();
+  size_t g0 = 0;
+  while (g0 < order.size()) {
+    size_t g1 = g0 + 1;
+    while (g1 < order.size() && qs[order[g1]].start == qs[order[g0]].start && qs[order[g1]].end == qs[order[g0]].end) ++g1;
+    std::vector<apex_query_spec> grp;
+    std::vector<int> live;
+    int64_t stride = 1;
+    for (size_t i = g0; i < g1; ++i) {
+      const apex_query_spec& q = qs[order[i]];
+      if (q.k > 0 && q.end > q.start) {
+        grp.push_back(q);
+        live.push_back(order[i]);
+        stride = std::max<int64_t>(stride, q.k);
+      } else {
+        apex_result& r = res[order[i]];
+        r.n = 0;
+        r.scanned = q.end - q.start;
+        r.discarded = 0;
+        r.candidates = r.admitted = 0;
+        r.full_predicate = 0;
+      }
+    }
+    g0 = g1;
+    if (grp.empty()) continue;
+    const int ng = (int)grp.size();
+    const uint64_t S = grp[0].start, E = grp[0].end, span = E - S;
+    const size_t blk = (size_t)ng * (size_t)stride * sizeof(Entry);
+    // local steps: every shard enqueued before any host wait
+    std::vector<int> used;
+    for (int i = 0; i < N; ++i) {
+      const uint64_t a = S + (uint64_t)(((unsigned __int128)span * (unsigned)i) / (unsigned)N);
+      const uint64_t b = S + (uint64_t)(((unsigned __int128)span * (unsigned)(i + 1)) / (unsigned)N);
+      if (a == b) continue;
+      apex_ctx* c = m->shard[i];
+      APEX_CU(cudaSetDevice(m->dev[i]));
+      APEX_TRY(m->exp[i].ensure(blk));
+      std::vector<apex_query_spec> local = grp;
+      for (auto& q : local) {
+        q.start = a;
+        q.end = b;
+      }
+      APEX_TRY(local_enqueue(c, local.data(), ng, m->exp[i].as<Entry>(), (unsigned long long)stride));
+      APEX_CU(cudaEventRecord(m->done[i], c->stream));
+      used.push_back(i);
+    }
+    std::vector<apex_result> rg(ng);
+    for (int j = 0; j < ng; ++j) rg[j] = res[live[j]];
+    for (int attempt = 0;; ++attempt) {
+      APEX_CU(cudaSetDevice(M->device));
+      const int ns = (int)used.size();
+      for (int i : used) APEX_CU(cudaStreamWaitEvent(M->stream, m->done[i], 0));
+      apex_stats st;
+      if (m->peer) {
+        APEX_TRY(m->h_srcs.ensure(ns * sizeof(void*)));
+        APEX_TRY(m->d_srcs.ensure(ns * sizeof(void*)));
+        APEX_CU(cudaStreamSynchronize(M->stream));  // the pinned pointer block is reused
+        for (int j = 0; j < ns; ++j) m->h_srcs.as<const Entry*>()[j] = m->exp[used[j]].as<Entry>();
+        APEX_CU(cudaMemcpyAsync(m->d_srcs.p, m->h_srcs.p, ns * sizeof(void*), cudaMemcpyHostToDevice, M->stream));
+        APEX_TRY(merge_impl(M, grp.data(), ng, nullptr, m->d_srcs.as<const Entry*>(), ns, stride, span, rg.data(), &st));
+      } else {
+        APEX_TRY(m->d_stage.ensure((size_t)ns * blk));
+        for (int j = 0; j < ns; ++j)
+          APEX_CU(cudaMemcpyPeerAsync(m->d_stage.as<unsigned char>() + (size_t)j * blk, M->device,
+                                      m->exp[used[j]].p, m->dev[used[j]], blk, M->stream));
+        APEX_TRY(merge_impl(M, grp.data(), ng, m->d_stage.as<Entry>(), nullptr, ns, stride, span, rg.data(), &st));
+      }
+      agg.select_ms += st.select_ms;
+      agg.kernel_launches += st.kernel_launches;
+      agg.d2h_bytes += st.d2h_bytes;
+      // validate every shard (overflow => exact re-run + re-export, then merge again)
+      bool again = false;
+      for (int i : used) {
+        APEX_CU(cudaSetDevice(m->dev[i]));
+        int rr = 0;
+        APEX_TRY(local_finish(m->shard[i], nullptr, &rr));
+        if (rr) APEX_CU(cudaEventRecord(m->done[i], m->shard[i]->stream));
+        again = again || rr;
+        const RunStats& lst = m->shard[i]->batch.st;
+        agg.kernel_launches += lst.launches;
+        agg.h2d_bytes += lst.h2d_bytes;
+        agg.retries += lst.retries;
+        agg.scan_kernel_ms = std::max<double>(agg.scan_kernel_ms, lst.scan_kernel_ms);
+        agg.scan_ms = std::max<double>(agg.scan_ms, lst.ms[2]);
+        for (int q = 0; q < ng; ++q) agg.candidates += (int64_t)m->shard[i]->h_ctl.as<QCtl>()[q].count;
+      }
+      if (!again) break;
+      if (attempt >= 2) return set_err(APEX_ELIMIT, "multi-device merge did not settle");
+    }
+    for (int j = 0; j < ng; ++j) res[live[j]] = rg[j];
+  }
+  agg.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (stats) *stats = agg;
+  return APEX_OK;
+}
+
+int apex_multi_info(apex_multi* m, int32_t* n_devices, int32_t* peer_access) {
+  if (!m) return set_err(APEX_EINVAL, "null multi-device context");
+  if (n_devices) *n_devices = (int32_t)m->shard.size();
+  if (peer_access) *peer_access = m->peer ? 1 : 0;
   return APEX_OK;
 }
 

@@ -21,6 +21,9 @@ constexpr int kQuant = 32;        // quantile steps per sorted column (test choi
 constexpr int kScanWarps = 8;       // warps per enumeration CTA
 constexpr int kSelectThreads = 512;
 constexpr uint64_t kNoTau = 0ull;   // "no admission threshold yet" (key 0 is never a finite score)
+// exported-entry marker of a local result whose candidate buffer overflowed
+// (the source re-runs; every merge that sees it reports the gather stale)
+constexpr unsigned long long kStaleG = ~0ull - 1ull;
 
 // Reaction descriptor in device memory (positional, csl.py:90-97).
 struct DevReaction {
@@ -90,6 +93,8 @@ struct QCtl {
   unsigned int nx_tie;            // 1: tie mode at key nx_tau
   unsigned int nx_gshift;
   unsigned int nx_tie_enter;      // 1: first tie run (host sets the g range from the query range)
+  unsigned int stale;             // merge: some source exported an overflowed (stale) local result
+  unsigned int _pad5;
   unsigned int hist[3][256];      // select histograms (triple-buffered)
 };
 

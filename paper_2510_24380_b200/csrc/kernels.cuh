@@ -259,6 +259,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPrese
     c->tie_gshift = P ? P->tie_gshift : 48u;
     c->nx_tie = 0;
     c->nx_tie_enter = 0;
+    c->stale = 0;
     c->use_full = use_full;
     c->small_done = 0;
     c->seed_max = 0;
@@ -2476,12 +2477,25 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
   }
 }
 
-// Multi-GPU: export the local selected set (unordered) to out + q*k.
-__global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restrict__ out) {
+// Multi-GPU: export the local selected set (unordered) to out + slot*stride;
+// the slots past the selected count are written as padding (g == ~0), so the
+// exported block is complete without a separate memset.
+__global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restrict__ out, unsigned long long stride) {
   const ScanQuery& Q = qs[blockIdx.y];
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
-  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[(unsigned long long)Q.slot * Q.k + i] = Q.sel[i];
+  const bool stale = *(volatile unsigned long long*)&Q.ctl->count > Q.cap;  // overflowed: re-run pending
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < stride;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    Entry e;
+    if (i < n) {
+      e = Q.sel[i];
+    } else {
+      e.key = ~0ull;
+      e.g = ~0ull;
+    }
+    if (stale && i == 0) e.g = kStaleG;
+    out[(unsigned long long)Q.slot * stride + i] = e;
+  }
 }
 
 // Multi-GPU: load gathered entries (skip padding g == ~0) as the compacted set.
@@ -2489,8 +2503,12 @@ __global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restric
 // g == ~0) as its candidate set.  Layout: in[(src * nq + q) * stride + i],
 // i < stride, for src < n_src (what an all-gather of per-rank [nq][stride]
 // buffers produces).
+// srcs (optional): one pointer per source rank to its [nq][stride] block —
+// on a multi-GPU context these are PEER device pointers, so this kernel is the
+// all-gather itself: every entry is loaded over NVLink straight into the
+// merge's candidate buffer (no staging copy, no separate collective).
 __global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry* __restrict__ in, int n_src,
-                                  int nq, unsigned long long stride) {
+                                  int nq, unsigned long long stride, const Entry* const* __restrict__ srcs = nullptr) {
   const int q = blockIdx.y;
   const ScanQuery& Q = qs[q];
   QCtl* ctl = Q.ctl;
@@ -2504,8 +2522,10 @@ __global__ void merge_load_kernel(const ScanQuery* __restrict__ qs, const Entry*
     bool keep = false;
     if (i < n) {
       const unsigned long long src = i / stride, j = i - src * stride;
-      e = in[(src * (unsigned long long)nq + (unsigned long long)q) * stride + j];
-      keep = e.g != ~0ull;
+      e = srcs ? srcs[src][(unsigned long long)q * stride + j]
+               : in[(src * (unsigned long long)nq + (unsigned long long)q) * stride + j];
+      keep = e.g < kStaleG;
+      if (e.g == kStaleG) atomicOr(&ctl->stale, 1u);
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (m) {

@@ -1,12 +1,15 @@
-"""Multi-GPU sharding of one query: one process per GPU.
+"""Multi-GPU sharding, one process per GPU.
 
 The product index space [start, end) is cut into contiguous g ranges, one per
-rank; every rank computes its exact local top-min(k, feasible) on its GPU
-(apex_query_local), the per-rank (key, g) entries (16 B each, padded to k) are
-all-gathered with NCCL over NVLink, and every rank runs the exact merge
-(apex_merge_finalize / apex_merge_finalize_batch: one device pass for a whole
-batch) on the gathered buffer.  Exactness: the global top-k is
-contained in the union of the local top-k's, and the (key, g) order is global.
+rank; every rank computes its exact local top-min(k, feasible) on its GPU, the
+per-rank (key, g) entries (16 B each, padded to k) are all-gathered with NCCL
+over NVLink, and every rank runs the exact merge (apex_merge_finalize_batch:
+one device pass for a whole batch) on the gathered buffer.  Exactness: the
+global top-k is contained in the union of the local top-k's, and the (key, g)
+order is global.  ``sharded_batch`` is the stream-ordered form (local step,
+all-gather and merge enqueued back to back; one host sync).  The one-process
+form driving several GPUs is ``_native.MultiDeviceContext`` (apex_multi_*),
+whose merge reads the shards' entries over NVLink peer pointers directly.
 """
 
 from __future__ import annotations
@@ -67,10 +70,18 @@ def sharded_query(ctx, query: dict, group=None, stream_sync=True):
     return res, {"local": st_local, "merge": st_merge, "local_count": counts[0]}
 
 
-def sharded_batch(ctx, queries: list[dict], group=None, prepared=None):
+def sharded_batch(ctx, queries: list[dict], group=None, prepared=None, local=None):
     """A batch of native queries sharing one global range [start, end): every
-    rank scans its shard for all of them (one apex_query_local), ONE all-gather
-    of the [n_queries][k] entry buffers, and one batched exact merge."""
+    rank scans its shard for all of them, ONE all-gather of the [n_queries][k]
+    entry buffers, and one batched exact merge — stream-ordered on the
+    context's stream (which must be torch's current stream): the local step
+    and its padded export (apex_query_local_async), the NCCL all-gather and
+    the merge are enqueued back to back, and the only host sync is the merge's
+    result copy.  A local candidate-buffer overflow is resolved exactly: the
+    overflowed rank exports a stale marker, every rank's merge sees it in the
+    same gathered data (so all ranks agree without another collective), the
+    overflowed rank re-runs in apex_query_local_finish, and all ranks gather
+    and merge again."""
     import torch
     import torch.distributed as dist
 
@@ -80,8 +91,23 @@ def sharded_batch(ctx, queries: list[dict], group=None, prepared=None):
         raise ValueError("sharded_batch: all queries must share one index range")
     k = max(max(int(q["k"]) for q in queries), 1)
     a, b = shard_range(start, end, rank, world)
-    local = torch.full((len(queries) * k, 2), PAD, dtype=torch.int64, device="cuda")
-    counts, st_local = ctx.query_local([dict(q, start=a, end=b) for q in queries], local.data_ptr())
+    if local is None:
+        local = torch.empty((len(queries) * k, 2), dtype=torch.int64, device="cuda")
+    live = b > a
+    if live:
+        st_local = ctx.query_local_async([dict(q, start=a, end=b) for q in queries], local.data_ptr(), k)
+    else:  # an empty shard contributes padding only
+        local.fill_(PAD)
+        st_local = {}
     gathered = all_gather_entries(local, group)
     res, st_merge = ctx.merge_finalize_batch(queries, gathered.data_ptr(), world, k, end - start, prepared)
-    return res, {"local": st_local, "merge": st_merge, "local_counts": counts}
+    counts, st_fin = [0] * len(queries), {}
+    if live:
+        counts, _, st_fin = ctx.query_local_finish()
+    rounds = 1
+    while st_merge.get("stale_sources", 0):
+        gathered = all_gather_entries(local, group)
+        res, st_merge = ctx.merge_finalize_batch(queries, gathered.data_ptr(), world, k, end - start, prepared)
+        rounds += 1
+    return res, {"local": st_local, "local_finish": st_fin, "merge": st_merge, "local_counts": counts,
+                 "gather_rounds": rounds}

@@ -133,18 +133,35 @@ _ERROR_CLASS = [EngineError]
 # device contexts, memoized per (library, table)
 # ---------------------------------------------------------------------------
 
-def default_device() -> int:
+def default_device():
+    """Device(s) the operator API runs on: ``APEX_B200_DEVICES="0,1,...,7"``
+    selects the single-process multi-GPU context (index range sharded over
+    those devices), else ``APEX_B200_DEVICE`` / ``LOCAL_RANK`` /
+    0 — one device."""
+    multi = os.environ.get("APEX_B200_DEVICES", "").strip()
+    if multi:
+        ids = tuple(int(x) for x in multi.split(",") if x.strip())
+        return ids if len(ids) > 1 else ids[0]
     for var in ("APEX_B200_DEVICE", "LOCAL_RANK"):
         if var in os.environ:
             return int(os.environ[var])
     return 0
 
 
-class _Bound:
-    """A device context with one library + table resident."""
+def _open_context(device):
+    """One device (int) -> DeviceContext; several (sequence) -> MultiDeviceContext."""
+    if isinstance(device, (list, tuple)):
+        if len(device) > 1:
+            return _native.MultiDeviceContext(list(device))
+        device = device[0]
+    return _native.DeviceContext(int(device))
 
-    def __init__(self, library, table, device: int):
-        self.ctx = _native.DeviceContext(device)
+
+class _Bound:
+    """A device context (one GPU, or several) with one library + table resident."""
+
+    def __init__(self, library, table, device):
+        self.ctx = _open_context(device)
         rg_pos = {int(r): i for i, r in enumerate(table.rg_ids)}
         offs = np.asarray(table.rg_offsets, dtype=np.int64)
         sizes, pair_offsets, g_offsets = [], [], []
@@ -174,7 +191,7 @@ class _Bound:
         self.task_names = list(table.task_names)
 
 
-_BOUND: dict[tuple[int, int, int], tuple[weakref.ref, weakref.ref, _Bound, tuple]] = {}
+_BOUND: dict[tuple, tuple[weakref.ref, weakref.ref, _Bound, tuple]] = {}
 _MAX_BOUND = 4
 
 
@@ -194,10 +211,11 @@ def _content_token(table) -> tuple:
             zlib.crc32(sample.tobytes(), zlib.crc32(np.ascontiguousarray(bias).tobytes())))
 
 
-def bind(library, table, device: int | None = None) -> _Bound:
+def bind(library, table, device=None) -> _Bound:
     """Device context for (library, table), created on first use and reused
     while the table's contents are unchanged (see _content_token)."""
     dev = default_device() if device is None else device
+    dev = tuple(dev) if isinstance(dev, (list, tuple)) else int(dev)
     key = (id(library), id(table), dev)
     token = _content_token(table)
     hit = _BOUND.get(key)
@@ -326,13 +344,14 @@ def _timing(t0: float, start: int, end: int, stats: dict) -> dict:
 # operator API
 # ---------------------------------------------------------------------------
 
-def search_topk_stream(library, table, query, index_range=None, device: int | None = None):
-    """Exact constrained top-k (engine.py:265-313), on the B200."""
+def search_topk_stream(library, table, query, index_range=None, device=None):
+    """Exact constrained top-k (engine.py:265-313), on the B200 — on several
+    B200s when ``device`` is a sequence of ids (or APEX_B200_DEVICES is set)."""
     start, end = _validate(library, table, query, index_range)
     return _run([query], library, table, start, end, device)[0]
 
 
-def search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None, device: int | None = None):
+def search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None, device=None):
     """Chain-of-batches variant (engine.py:345-398).  Results are identical to
     the stream variant by contract (test_engine.py:138-145), so both run the
     same device pipeline; ``chunk_size`` is validated as the reference does.
@@ -350,7 +369,7 @@ def search_topk_batched(library, table, query, chunk_size, index_range=None, tra
     return _run([query], library, table, start, end, device)[0]
 
 
-def search_topk_many(library, table, queries, index_range=None, device: int | None = None):
+def search_topk_many(library, table, queries, index_range=None, device=None):
     """Several queries in one batched device pass; same results as one
     ``search_topk_stream`` call per query."""
     if not queries:
@@ -383,12 +402,12 @@ def _run(queries, library, table, start, end, device):
     return out
 
 
-def precompute_contributions(cache, surrogate, device: int | None = None):
+def precompute_contributions(cache, surrogate, device=None):
     """Dot each task head with every cached associative embedding
     (engine.py:80-92) on the device: fp64 products and accumulation, fp32
     rounding.  Returns a table of the caller's class when available."""
     dev = default_device() if device is None else device
-    ctx = _native.DeviceContext(dev)
+    ctx = _native.DeviceContext(int(dev[0] if isinstance(dev, (list, tuple)) else dev))
     try:
         values = ctx.load_cache(np.asarray(cache.u, dtype=np.float64), np.asarray(surrogate.head_w, dtype=np.float64),
                                 np.asarray(surrogate.head_b, dtype=np.float64))

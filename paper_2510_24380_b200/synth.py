@@ -244,3 +244,40 @@ def build_model(shape: Shape, seed: int = 1, n_sample: int = 20000):
     w, b = random_heads(seed=seed)
     w, b = calibrate_heads(shape, u, w, b, n_sample=n_sample, seed=seed)
     return u, w, b
+
+
+def mirror_objects(shape: Shape, values: np.ndarray, biases: np.ndarray):
+    """CslLibrary / ContributionTable mirror objects of a synthetic shape, for
+    driving the public operator API (engine.search_topk_stream): R-group r of
+    reaction t has id 1000*t + r, synthon ids are distinct and dense, table
+    rows follow shape.pair_off (R-group-major, factorizer.py:87-106)."""
+    from . import csl, engine
+
+    reactions, rg_ids, rg_off = [], [], []
+    members = np.zeros(shape.n_pairs, dtype=np.int64)
+    sid = 0
+    for t, (sizes, offs) in enumerate(zip(shape.sizes, shape.pair_off)):
+        rgs = []
+        for r, (n, o) in enumerate(zip(sizes, offs)):
+            ids = tuple(range(sid, sid + int(n)))
+            sid += int(n)
+            rgs.append(csl.RgroupSpec(1000 * t + r, ids))
+            rg_ids.append(1000 * t + r)
+            rg_off.append(int(o))
+            members[int(o):int(o) + int(n)] = ids
+        reactions.append(csl.ReactionSpec(t, tuple(rgs)))
+    lib = csl.CslLibrary(tuple(reactions), tuple(csl.SynthonRecord(i, f"s{i}") for i in range(sid)))
+    order = np.argsort(rg_off)
+    table = engine.ContributionTable(values=values, biases=np.asarray(biases, dtype=np.float64),
+                                     task_names=list(TASKS), member_ids=members,
+                                     rg_offsets=np.append(np.asarray(rg_off)[order], shape.n_pairs),
+                                     rg_ids=np.asarray(rg_ids)[order], fingerprint=csl.library_fingerprint(lib))
+    return lib, table
+
+
+def query_spec(q: dict):
+    """engine.QuerySpec mirror of a query dict (task names)."""
+    from . import engine
+
+    return engine.QuerySpec(q["objective"], q["direction"],
+                            tuple(engine.Constraint(t, lo, hi) for t, lo, hi in q["constraints"]), q["k"])

@@ -20,28 +20,7 @@ g.build()
 from paper_2510_24380_b200 import csl, engine, synth  # noqa: E402
 
 
-def mirror_objects(shape, values, biases):
-    """CslLibrary / ContributionTable mirrors of a synthetic shape: R-group r of
-    reaction t has id 1000*t + r, its synthons distinct ids; table rows follow
-    shape.pair_off (R-group-major)."""
-    reactions, rg_ids, rg_off, members = [], [], [], np.zeros(shape.n_pairs, dtype=np.int64)
-    sid = 0
-    for t, (sizes, offs) in enumerate(zip(shape.sizes, shape.pair_off)):
-        rgs = []
-        for r, (n, o) in enumerate(zip(sizes, offs)):
-            ids = tuple(range(sid, sid + int(n)))
-            sid += int(n)
-            rgs.append(csl.RgroupSpec(1000 * t + r, ids))
-            rg_ids.append(1000 * t + r)
-            rg_off.append(int(o))
-            members[int(o):int(o) + int(n)] = ids
-        reactions.append(csl.ReactionSpec(t, tuple(rgs)))
-    lib = csl.CslLibrary(tuple(reactions), tuple(csl.SynthonRecord(i, f"s{i}") for i in range(sid)))
-    order = np.argsort(rg_off)
-    table = engine.ContributionTable(values=values, biases=biases, task_names=list(synth.TASKS),
-                                     member_ids=members, rg_offsets=np.append(np.asarray(rg_off)[order], shape.n_pairs),
-                                     rg_ids=np.asarray(rg_ids)[order], fingerprint=csl.library_fingerprint(lib))
-    return lib, table
+mirror_objects = synth.mirror_objects
 
 
 def main():
