@@ -254,6 +254,17 @@ struct apex_ctx {
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
   uint64_t opt_gen = 0;             // bumped by apex_set_option
+  // the merge's own workspace (merge_impl swaps it in): a local step in
+  // flight on this context keeps its buffers while the merge of gathered
+  // entries runs on the same stream (dist.sharded_batch enqueues both)
+  struct Workspace {
+    std::vector<Slot> slots;
+    DBuf d_hists, d_ctls, d_queries, d_out;
+    HBuf h_queries, h_ctl, h_out;
+    std::vector<size_t> out_off;
+    std::vector<ScanQuery> uploaded;
+  } mws;
+  cudaEvent_t mev[2] = {};
   // per-context (= per-device) launch caches
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
   std::vector<std::pair<const void*, size_t>> attr_cache;
@@ -740,7 +751,8 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
                                    (int)smem_small));
       c->attr_small = true;
     }
-    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, finalize ? 1 : 0, compute_bound ? 1 : 0);
+    // (materialization runs after, for every query, in materialize_kernel)
+    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, 0, compute_bound ? 1 : 0);
     ++st.launches;
   }
   {
@@ -1344,6 +1356,26 @@ int local_finish(apex_ctx* c, int64_t* counts, int* rerun) {
   return APEX_OK;
 }
 
+// Swaps the context's query workspace with its merge workspace for a scope.
+struct MergeScope {
+  apex_ctx* c;
+  explicit MergeScope(apex_ctx* c_) : c(c_) { swap(); }
+  ~MergeScope() { swap(); }
+  void swap() {
+    auto& w = c->mws;
+    std::swap(c->slots, w.slots);
+    std::swap(c->d_hists, w.d_hists);
+    std::swap(c->d_ctls, w.d_ctls);
+    std::swap(c->d_queries, w.d_queries);
+    std::swap(c->d_out, w.d_out);
+    std::swap(c->h_queries, w.h_queries);
+    std::swap(c->h_ctl, w.h_ctl);
+    std::swap(c->h_out, w.h_out);
+    std::swap(c->out_off, w.out_off);
+    std::swap(c->uploaded, w.uploaded);
+  }
+};
+
 // Exact merge of gathered local entries (one device pass for a batch): the
 // entries of query q from source r are entries[(r * nq + q) * stride + i]
 // (one contiguous all-gathered buffer), or srcs[r][q * stride + i] when srcs
@@ -1360,6 +1392,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
       if (q.constraints[m].task < 0 || q.constraints[m].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
   }
   if (stats) std::memset(stats, 0, sizeof(*stats));
+  MergeScope scope(c);  // never touches the buffers of a local step in flight
   const int64_t n_in = (int64_t)n_src * stride;
   bool any = false;
   for (int i = 0; i < nq; ++i) {
@@ -1397,7 +1430,6 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
   APEX_TRY(c->h_queries.ensure(qbytes));
   APEX_TRY(c->h_ctl.ensure((size_t)nq * sizeof(QCtl)));
   c->uploaded.clear();
-  c->batch.pending = false;
   ScanQuery* hq = c->h_queries.as<ScanQuery>();
   for (int i = 0; i < nq; ++i) {
     const apex_query_spec& q = qs[i];
@@ -1429,7 +1461,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
   cudaStream_t s = c->stream;
   const ScanQuery* dq = c->d_queries.as<ScanQuery>();
   RunStats st;
-  APEX_CU(cudaEventRecord(c->ev[0], s));
+  APEX_CU(cudaEventRecord(c->mev[0], s));
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
@@ -1444,7 +1476,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
   APEX_CU(cudaGetLastError());
   APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
                             cudaMemcpyDeviceToHost, s));
-  APEX_CU(cudaEventRecord(c->ev[1], s));
+  APEX_CU(cudaEventRecord(c->mev[1], s));
   std::vector<apex_query_spec> qq(qs, qs + nq);
   for (auto& x : qq) {
     x.start = 0;
@@ -1458,7 +1490,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
     }
   if (stats) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&ms, c->mev[0], c->mev[1]);
     stats->select_ms = ms;
     stats->total_ms = ms;
     stats->kernel_launches = st.launches;
@@ -1510,6 +1542,7 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
     c->own_stream = true;
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  for (auto& ev : c->mev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&c->upload_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
@@ -1541,6 +1574,13 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_out.release();
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
+  for (auto& ev : c->mev) cudaEventDestroy(ev);
+  {
+    auto& w = c->mws;
+    for (auto& sl : w.slots) sl.release();
+    for (DBuf* b : {&w.d_hists, &w.d_ctls, &w.d_queries, &w.d_out}) b->release();
+    for (HBuf* b : {&w.h_queries, &w.h_ctl, &w.h_out}) b->release();
+  }
   if (c->upload_ev) cudaEventDestroy(c->upload_ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
@@ -2245,7 +2285,9 @@ int apex_multi_query(apex_multi* m, const apex_query_spec* qs, int32_t nq, apex_
       agg.select_ms += st.select_ms;
       agg.kernel_launches += st.kernel_launches;
       agg.d2h_bytes += st.d2h_bytes;
-      // validate every shard (overflow => exact re-run + re-export, then merge again)
+      // validate every shard once (overflow => exact re-run + re-export,
+      // then one more merge over the now-valid entries)
+      if (attempt > 0) break;
       bool again = false;
       for (int i : used) {
         APEX_CU(cudaSetDevice(m->dev[i]));
@@ -2262,7 +2304,6 @@ int apex_multi_query(apex_multi* m, const apex_query_spec* qs, int32_t nq, apex_
         for (int q = 0; q < ng; ++q) agg.candidates += (int64_t)m->shard[i]->h_ctl.as<QCtl>()[q].count;
       }
       if (!again) break;
-      if (attempt >= 2) return set_err(APEX_ELIMIT, "multi-device merge did not settle");
     }
     for (int j = 0; j < ng; ++j) res[live[j]] = rg[j];
   }

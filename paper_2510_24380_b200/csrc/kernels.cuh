@@ -2358,8 +2358,11 @@ __device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned
 }
 
 __global__ void materialize_kernel(const MatLaunch M) {
+  // every query (small-set or radix path): rows of sorted[0, sel_count), one
+  // thread per row, the whole grid in parallel (a row is a chain of dependent
+  // gathers, so rows spread over many SMs rather than one CTA per query)
   const ScanQuery& Q = M.queries[blockIdx.y];
-  if (*(volatile unsigned*)&Q.ctl->small_done) return;
+  if (!*(volatile unsigned int*)&Q.ctl->active) return;
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -2447,12 +2450,17 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
   __syncthreads();
   const unsigned long long n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
   const unsigned long long bound = s_bound;
-  for (unsigned long long i = tid; i < n; i += blockDim.x) {
-    const Entry e = Q.buf[i];
-    if (e.key >= bound) {
-      const unsigned pos = atomicAdd(&cnt, 1u);
-      if (pos < (unsigned)kSmallSel) es[pos] = e;
-    }
+  const unsigned lane = tid & 31u;
+  for (unsigned long long base = tid & ~31u; base < n; base += blockDim.x) {
+    const unsigned long long i = base + lane;
+    Entry e;
+    const bool keep = i < n && (e = Q.buf[i], e.key >= bound);
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    unsigned pos = 0;
+    if (lane == 0) pos = atomicAdd(&cnt, (unsigned)__popc(m));  // one shared atomic per warp round
+    pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+    if (keep && pos < (unsigned)kSmallSel) es[pos] = e;
   }
   __syncthreads();
   const unsigned m = min(cnt, (unsigned)kSmallSel);

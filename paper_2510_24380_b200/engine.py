@@ -22,6 +22,7 @@ fallback — without the library or a B200 the call raises.
 
 from __future__ import annotations
 
+import gc
 import math
 import operator
 import os
@@ -288,12 +289,53 @@ _MI_FIELDS = ("reaction_id", "assignment")
 _SC_FIELDS = ("global_index", "chi", "objective", "violation", "constraint_values")
 
 
+try:
+    from . import _rowbuild  # native row builder (csrc/rowbuild.c, built by __graft_entry__.build)
+except ImportError:  # pragma: no cover - host object construction only; the compute path has no fallback
+    _rowbuild = None
+
+_RX_TABLES: dict[int, tuple[weakref.ref, list]] = {}
+
+
+def _rx_table(library) -> list:
+    """Per reaction position: (reaction_id, rgroup ids, synthon id tuples),
+    built once per library object (libraries are immutable)."""
+    hit = _RX_TABLES.get(id(library))
+    if hit is not None and hit[0]() is library:
+        return hit[1]
+    table = [(rx.reaction_id, tuple(rg.rgroup_id for rg in rx.rgroups), tuple(rg.synthon_ids for rg in rx.rgroups))
+             for rx in library.reactions]
+    try:
+        _RX_TABLES[id(library)] = (weakref.ref(library), table)
+    except TypeError:
+        pass
+    return table
+
+
 def _build_result(library, query, res: dict, timing: dict):
     """TopKResult from the device rows (engine.py:238-262 output shape):
     entries best-first, chi = (reaction_id, ((rgroup_id, synthon_id), ...)),
     violation +0.0, constraint values in constraint order."""
     mi_cls, sc_cls, tk_cls = _types_for(library, query)
     n = int(res["n"])
+    if _rowbuild is not None and n:
+        fast = _plain_fields(mi_cls, _MI_FIELDS) and _plain_fields(sc_cls, _SC_FIELDS)
+        # the rows create no reference cycles: pause the cyclic GC, whose
+        # generation sweeps otherwise fire every ~700 of these allocations
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            entries = _rowbuild.build_entries(
+            mi_cls, sc_cls, fast, n, np.ascontiguousarray(res["g"], dtype=np.uint64),
+            np.ascontiguousarray(res["objective"], dtype=np.float64),
+            np.ascontiguousarray(res["constraint_values"], dtype=np.float64), len(query.constraints),
+            np.ascontiguousarray(res["reaction"], dtype=np.int32), np.ascontiguousarray(res["digits"], dtype=np.int32),
+            _rx_table(library))
+        finally:
+            if gc_on:
+                gc.enable()
+        return tk_cls(entries=entries, scanned=int(res["scanned"]), retained=n,
+                      discarded_for_violation=int(res["discarded"]), timing=timing)
     g = res["g"].tolist()
     obj = res["objective"].tolist()
     cons = res["constraint_values"].tolist()
@@ -441,6 +483,12 @@ def save_result(result, query, path, library=None) -> None:
     if library is not None:
         cols += "\tassembled"
         tokens = {s.synthon_id: s.token for s in library.synthons}
+    if tokens is None and _rowbuild is not None:
+        # native formatter (csrc/rowbuild.c): the same bytes, without per-row bytecode
+        with open(path, "w") as fh:
+            fh.write(cols + "\n")
+            fh.write(_rowbuild.format_rows(result.entries))
+        return
     lines = [cols]
     for rank, e in enumerate(result.entries):
         sids = ",".join(map(str, e.chi.synthon_ids()))

@@ -57,8 +57,17 @@ def test_errors_before_device():
         Q("obj", "maximize", k=-1)
 
 
-def test_save_result_matches_reference_tsv(tmp_path):
-    """The mirror's TSV writer reproduces the reference's bytes from the same entries."""
+@pytest.mark.parametrize("native", [True, False])
+def test_save_result_matches_reference_tsv(tmp_path, native, monkeypatch):
+    """The mirror's TSV writer (native formatter, csrc/rowbuild.c, and the
+    Python one) reproduces the reference's bytes from the same entries."""
+    import __graft_entry__ as gr
+
+    gr._build_rowbuild()
+    if not native:
+        monkeypatch.setattr(engine, "_rowbuild", None)
+    else:
+        assert engine._rowbuild is not None
     for case in golden_cases():
         lib = case.library()
         for qi, qd in enumerate(case.queries):
@@ -122,3 +131,54 @@ def test_shard_ranges_partition():
             parts = [shard_range(start, end, r, world) for r in range(world)]
             assert parts[0][0] == start and parts[-1][1] == end
             assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def _fake_rows(library, n, m, seed=0):
+    from paper_2510_24380_b200 import csl
+
+    rng = np.random.default_rng(seed)
+    total = csl.product_count(library)
+    g = np.sort(rng.choice(total, size=n, replace=False)).astype(np.uint64)
+    offs = np.asarray(csl.reaction_offsets(library), dtype=np.uint64)
+    t = (np.searchsorted(offs, g, side="right") - 1).astype(np.int32)
+    dig = np.zeros((n, 6), dtype=np.int32)
+    for i, (gi, ti) in enumerate(zip(g.tolist(), t.tolist())):
+        rem = gi - int(offs[ti])
+        rgs = library.reactions[ti].rgroups
+        for j in range(len(rgs) - 1, -1, -1):
+            rem, dig[i, j] = divmod(rem, len(rgs[j].synthon_ids))
+    return {"n": n, "g": g, "objective": rng.standard_normal(n), "constraint_values": rng.standard_normal((n, m)),
+            "reaction": t, "digits": dig, "scanned": total, "discarded": 0}
+
+
+@pytest.mark.parametrize("use_reference", [False, True])
+def test_native_row_builder_equals_python(use_reference, monkeypatch):
+    """csrc/rowbuild.c builds the same ScoredCompound / MultiIndex rows as the
+    Python builder (mirror classes, and the reference's own classes)."""
+    import __graft_entry__ as gr
+
+    gr._build_rowbuild()
+    from conftest import golden_cases
+    from paper_2510_24380_b200 import engine
+
+    assert engine._rowbuild is not None
+    case = golden_cases()[0]
+    if use_reference:
+        rcsl, rengine = import_reference()
+        library = rcsl.deserialize_library(case.library_text)
+        query = rengine.QuerySpec("obj" if "obj" in case.task_names else case.task_names[0], "maximize",
+                                  tuple(rengine.Constraint(t) for t in case.task_names[:2]), 10)
+    else:
+        library = case.library()
+        query = engine.QuerySpec(case.task_names[0], "maximize",
+                                 tuple(engine.Constraint(t) for t in case.task_names[:2]), 10)
+    rows = _fake_rows(library, 25, len(query.constraints))
+    fast = engine._build_result(library, query, rows, {"x": 1.0})
+    monkeypatch.setattr(engine, "_rowbuild", None)
+    slow = engine._build_result(library, query, rows, {"x": 1.0})
+    assert type(fast) is type(slow)
+    assert fast.entries == slow.entries
+    assert [type(e) for e in fast.entries] == [type(e) for e in slow.entries]
+    assert [e.violation.hex() for e in fast.entries] == ["0x0.0p+0"] * 25
+    assert (fast.scanned, fast.retained, fast.discarded_for_violation) == (slow.scanned, slow.retained,
+                                                                           slow.discarded_for_violation)
