@@ -161,7 +161,10 @@ def _rank_main(rank, world, port, seed, ties, out):
     else:
         qs = [q for q in _queries(lib.total) if q["k"] > 0]
     res, info = sharded_batch(ctx, qs)
-    glob, _ = _native.DeviceContext(0).query(qs)
+    ref = _native.DeviceContext(0)
+    ref.load_library(sizes, pair_off, lib.offsets[:-1], p)
+    ref.load_table(values, biases)
+    glob, _ = ref.query(qs)
     ok = all(all(np.array_equal(a[k], b[k]) for k in FIELDS) and a["n"] == b["n"] and
              a["discarded"] == b["discarded"] for a, b in zip(res, glob))
     out[rank] = (ok, info["gather_rounds"])
