@@ -1552,6 +1552,95 @@ __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool low
   return kQuant + 1 - lo;
 }
 
+// quant_count for up to four tests at once (q tables at qbase + task * qstride):
+// the ends of every table first, then the binary searches in lockstep, so the
+// four dependent-load chains overlap.  th[u] is the signed-value threshold
+// (lower tests compare -x <= th, i.e. x >= -th); NaN means nothing passes.
+__device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride, const int (&task)[4],
+                                             const bool (&lower)[4], const float (&th)[4], int (&qc)[4]) {
+  const float* q[4];
+  float t[4], qlo[4], qhi[4];
+  int lo[4], hi[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    q[u] = qbase + (int64_t)task[u] * qstride;
+    t[u] = lower[u] ? -th[u] : th[u];
+    qlo[u] = __ldg(q[u]);
+    qhi[u] = __ldg(q[u] + kQuant);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    lo[u] = 1;
+    hi[u] = kQuant;
+    qc[u] = -1;  // undecided: search
+    if (!(th[u] == th[u])) qc[u] = 0;
+    else if (!lower[u]) {
+      if (!(qlo[u] <= t[u])) qc[u] = 0;
+      else if (qhi[u] <= t[u]) qc[u] = kQuant + 1;
+    } else {
+      if (!(qhi[u] >= t[u])) qc[u] = 0;
+      else if (qlo[u] >= t[u]) qc[u] = kQuant + 1;
+    }
+    if (qc[u] >= 0) lo[u] = hi[u];
+  }
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {  // ceil(log2(kQuant)) halvings of [1, kQuant]
+    float x[4];
+    int mid[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      mid[u] = (lo[u] + hi[u]) >> 1;
+      x[u] = lo[u] < hi[u] ? __ldg(q[u] + mid[u]) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (lo[u] < hi[u]) {
+        const bool go = lower[u] ? (x[u] < t[u]) : (x[u] <= t[u]);
+        if (go) lo[u] = mid[u] + 1; else hi[u] = mid[u];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (qc[u] < 0) qc[u] = lower[u] ? kQuant + 1 - lo[u] : lo[u];
+}
+
+// sorted position of quantile qq: quant[qq] = xs[qpos(qq)] (capi.cu build_corners)
+__device__ __forceinline__ int qpos(int qq, int n) { return min(n - 1, (int)(((long long)qq * n) / kQuant)); }
+
+// Exact passing range [start, start + cnt) of a test on a sorted column xs of
+// length n: upper tests pass x <= t (a prefix), lower tests x >= t (a suffix).
+// qc = the test's quant_count, which brackets the boundary between two
+// quantile positions, so only that window is binary-searched.
+__device__ __forceinline__ void exact_range(const float* __restrict__ xs, int n, bool lower, float t, int qc,
+                                            int& start, int& cnt) {
+  if (!lower) {
+    // boundary B = first index with xs[B] > t
+    int a, b;
+    if (qc <= 0) { a = 0; b = 0; }
+    else if (qc > kQuant) { a = n; b = n; }
+    else { a = qpos(qc - 1, n) + 1; b = qpos(qc, n); }
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (__ldg(xs + mid) <= t) a = mid + 1; else b = mid;
+    }
+    start = 0;
+    cnt = a;
+  } else {
+    // start = first index with xs[start] >= t; the bracket index is lo = kQuant + 1 - qc
+    int a, b;
+    if (qc <= 0) { a = n; b = n; }
+    else if (qc > kQuant) { a = 0; b = 0; }
+    else { const int lo = kQuant + 1 - qc; a = qpos(lo - 1, n) + 1; b = qpos(lo, n); }
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (__ldg(xs + mid) < t) a = mid + 1; else b = mid;
+    }
+    start = a;
+    cnt = n - a;
+  }
+}
+
 #ifndef APEX_SORTED_MINB
 #define APEX_SORTED_MINB 4
 #endif
@@ -1599,8 +1688,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     decode_prefix(R, c, row, pr);
     const unsigned long long gbase = R.g_off + row * (uint64_t)n_last;
     // the objective's exact per-row threshold (against tau, +inf without one)
-    // and its approximate passing count; only when that is not already small
-    // are the constraint thresholds derived to find a more selective test
+    // and its passing count in quantile steps; only when that is not already
+    // small are the constraint thresholds derived to find a more selective test
     double p_obj;
     {
       const float* v = values + (int64_t)Q.test_task[0] * n_pairs;
@@ -1617,66 +1706,77 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     }
     sthr[lane] = th0;
     int best = 0;
-    // the objective's exact range first (narrow in the common, seeded case);
-    // only a wide one makes the constraints compete (in quantile steps)
     int start = 0, cnt = 0;
     int best_q = 0;
+    const float* qbase = S.quant + (int64_t)T.rx * (kQuant + 1);  // + task * n_rx * (kQuant + 1)
+    const int64_t qstride = (int64_t)S.n_rx * (kQuant + 1);
     if (valid && th0 == th0) {
       if (th0 == __int_as_float(0x7f800000)) {
         cnt = n_last;  // no threshold: every column passes the objective
         best_q = kQuant + 1;
       } else {
+        const float* q = qbase + Q.test_task[0] * qstride;
+        best_q = quant_count(q, maximize != 0, maximize ? -th0 : th0);
         const int64_t base0 = (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
-        if (!maximize) {
-          cnt = first_gt(S.sx + base0, n_last, th0);
-        } else {
-          start = first_ge(S.sx + base0, n_last, -th0);
-          cnt = n_last - start;
-        }
-        best_q = n_last > 0 ? (int)(((int64_t)cnt * (kQuant + 1) + n_last - 1) / n_last) : 0;
+        exact_range(S.sx + base0, n_last, maximize != 0, maximize ? -th0 : th0, best_q, start, cnt);
       }
     }
     bool cons_ready = false;
+    // every constraint's exact threshold (and, when choosing, its passing
+    // count in quantile steps), four tests at a time so their gathers,
+    // fp64 threshold math and quantile searches overlap instead of forming
+    // one dependent chain per test
     auto constraint_thresholds = [&](bool choose) {
-      for (int i = 1; i < nt; ++i) {
-        const int task = Q.test_task[i];
-        const float* v = values + (int64_t)task * n_pairs;
-        double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
-        // fixed trip count: pr stays in registers (a runtime-indexed pr
-        // would live in local memory)
+      for (int i0 = 1; i0 < nt; i0 += 4) {
+        double p[4];
+        int task[4];
 #pragma unroll
-        for (int j = 1; j < kMaxRg - 1; ++j)
-          if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
-        const bool lower = Q.test_lower[i] != 0;
-        const float th = lower ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
-                               : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
-        sthr[i * 32 + lane] = th;
+        for (int u = 0; u < 4; ++u) {
+          const int i = min(i0 + u, nt - 1);
+          task[u] = Q.test_task[i];
+          const float* v = values + (int64_t)task[u] * n_pairs;
+          double pp = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+          // fixed trip counts: pr stays in registers (a runtime-indexed pr
+          // would live in local memory)
+#pragma unroll
+          for (int j = 1; j < kMaxRg - 1; ++j)
+            if (j < c - 1) pp = __dadd_rn(pp, (double)__ldg(v + pr[j]));
+          p[u] = pp;
+        }
+        float th[4];
+        bool lower[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = min(i0 + u, nt - 1);
+          lower[u] = Q.test_lower[i] != 0;
+          th[u] = lower[u] ? -thr_lower_fast(p[u], Q.test_bias[i], Q.test_beta[i])
+                           : thr_upper_fast(p[u], Q.test_bias[i], Q.test_beta[i]);
+          if (i0 + u < nt) sthr[(i0 + u) * 32 + lane] = th[u];
+        }
         if (choose) {
-          const int qc = th == th ? quant_count(S.quant + ((int64_t)task * S.n_rx + T.rx) * (kQuant + 1), lower,
-                                                lower ? -th : th)
-                                  : 0;
-          if (qc < best_q) {
-            best_q = qc;
-            best = i;
-          }
+          int qc[4];
+          quant_count4(qbase, qstride, task, lower, th, qc);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i0 + u < nt && qc[u] < best_q) {
+              best_q = qc[u];
+              best = i0 + u;
+            }
         }
       }
       cons_ready = true;
     };
     if (valid && best_q > 2 && nt > 1) constraint_thresholds(true);
-    // exact passing range of a constraint that won (the objective's is known)
+    // exact passing range of a constraint that won (the objective's is known),
+    // searched only inside the quantile bracket its count identifies
     if (valid && best != 0) {
       start = 0;
       cnt = 0;
-    }
-    if (valid && best != 0 && best_q > 0) {
-      const float th = sthr[best * 32 + lane];
-      const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
-      if (!Q.test_lower[best]) {
-        cnt = first_gt(S.sx + base, n_last, th);
-      } else {
-        start = first_ge(S.sx + base, n_last, -th);
-        cnt = n_last - start;
+      if (best_q > 0) {
+        const float th = sthr[best * 32 + lane];
+        const bool lw = Q.test_lower[best] != 0;
+        const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
+        exact_range(S.sx + base, n_last, lw, lw ? -th : th, best_q, start, cnt);
       }
     }
     if (cnt > 0 && !cons_ready) constraint_thresholds(false);
