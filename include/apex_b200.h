@@ -173,6 +173,11 @@ int apex_load_cache(apex_ctx* ctx, const double* u, int64_t n_pairs, int32_t d,
 int apex_precompute_device(apex_ctx* ctx, const double* u_dev, int64_t n_pairs, int32_t d,
                            const double* head_w_dev, int32_t n_tasks, float* values_dev);
 
+/* Device time (ms) of the last K1 launch of apex_precompute_device /
+ * apex_load_cache (CUDA events around the kernel alone), or -1 when that
+ * launch used a form without the timer. */
+int apex_precompute_time(apex_ctx* ctx, double* kernel_ms);
+
 /* Run n_queries queries (batched: one enumeration schedule, all queries per
  * launch) and materialize each result into results[i] (host buffers). */
 int apex_query(apex_ctx* ctx, const apex_query_spec* queries, int32_t n_queries,

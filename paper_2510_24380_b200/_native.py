@@ -28,7 +28,7 @@ EXPORTED = (
     "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_merge_finalize_batch",
     "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
-    "apex_query_local_async", "apex_query_local_finish",
+    "apex_query_local_async", "apex_query_local_finish", "apex_precompute_time",
     "apex_multi_create", "apex_multi_destroy", "apex_multi_load_library", "apex_multi_load_table",
     "apex_multi_load_cache", "apex_multi_set_option", "apex_multi_query", "apex_multi_info",
 )
@@ -153,6 +153,7 @@ def load_library(path: Path | None = None):
                                  C.POINTER(Stats)], C.c_int),
         "apex_merge_finalize_batch": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int32, C.c_int64, C.c_uint64,
                                        C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
+        "apex_precompute_time": ([vp, C.POINTER(C.c_double)], C.c_int),
         "apex_query_local_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int64, C.POINTER(Stats)], C.c_int),
         "apex_query_local_finish": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(Stats)], C.c_int),
         "apex_multi_create": ([C.c_int32, C.POINTER(C.c_int32), C.POINTER(vp)], C.c_int),
@@ -169,8 +170,8 @@ def load_library(path: Path | None = None):
         "apex_debug_trace": ([vp, vp, C.c_int64, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
-        if name.startswith("apex_debug_") and not hasattr(lib, name):
-            continue  # profiling hooks are optional (older builds in A/B runs)
+        if (name.startswith("apex_debug_") or "APEX_B200_LIB" in os.environ) and not hasattr(lib, name):
+            continue  # profiling hooks are optional; A/B runs may load older builds
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
@@ -249,6 +250,12 @@ class DeviceContext:
         _check(self.lib.apex_load_cache(self._ctx, _ptr(u), u.shape[0], u.shape[1], _ptr(w), _ptr(b), w.shape[0],
                                         _ptr(out) if out is not None else None))
         return out
+
+    def precompute_time(self) -> float:
+        """Device ms of the last K1 kernel (events around the launch), -1 if untimed."""
+        ms = C.c_double(-1.0)
+        _check(self.lib.apex_precompute_time(self._ctx, C.byref(ms)))
+        return ms.value
 
     def precompute_device(self, u_ptr: int, n_pairs: int, d: int, w_ptr: int, n_tasks: int, out_ptr: int) -> None:
         _check(self.lib.apex_precompute_device(self._ctx, C.c_void_p(u_ptr), n_pairs, d, C.c_void_p(w_ptr), n_tasks,

@@ -246,7 +246,7 @@ struct apex_ctx {
   int64_t opt_cb_admit = 512;       // columns per smem block in the admission-first kernel
   int64_t opt_corner = 1;           // corner seed on/off
   int64_t opt_corner_mult = 16;
-  int64_t opt_pre_rows = 1;         // K1: row-parallel precompute kernel (0: smem-tile form)     // corner products per reaction ~ corner_mult * k / reactions
+  int64_t opt_pre_rows = 2;         // K1 form: 2 = TMA bulk ring (11 x 64), 1 = row-parallel, 0 = smem tiles
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
@@ -265,6 +265,7 @@ struct apex_ctx {
     std::vector<ScanQuery> uploaded;
   } mws;
   cudaEvent_t mev[2] = {};
+  bool k1_timed = false;             // mev brackets the last K1 launch (apex_precompute_time)
   // per-context (= per-device) launch caches
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
   std::vector<std::pair<const void*, size_t>> attr_cache;
@@ -1689,6 +1690,25 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
   if (n_pairs < 0 || d < 1 || n_tasks < 1 || !w_dev || !values_dev || (n_pairs > 0 && !u_dev))
     return set_err(APEX_EINVAL, "bad precompute arguments");
   if (n_pairs == 0) return APEX_OK;
+  if (n_tasks == 11 && d == 64 && c->opt_pre_rows == 2) {
+    // bulk-copy form (the APEX model's 11 x 64): one persistent CTA per SM,
+    // TMA ring of u tiles, head weights as kernel parameters
+    HeadParams<11, 64> W;
+    APEX_CU(cudaMemcpyAsync(W.w, w_dev, sizeof(W.w), cudaMemcpyDeviceToHost, c->stream));
+    APEX_CU(cudaStreamSynchronize(c->stream));
+    const size_t smem = bulk_smem_bytes<11, 64>();
+    APEX_CU(cudaFuncSetAttribute((const void*)precompute_bulk_kernel<11, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    const int64_t tiles = (n_pairs + kBulkRows - 1) / kBulkRows;
+    const int blocks = (int)std::min<int64_t>(tiles, c->sm_count);
+    APEX_CU(cudaEventRecord(c->mev[0], c->stream));
+    precompute_bulk_kernel<11, 64><<<blocks, kBulkRows, smem, c->stream>>>(u_dev, n_pairs, W, values_dev);
+    APEX_CU(cudaGetLastError());
+    APEX_CU(cudaEventRecord(c->mev[1], c->stream));
+    c->k1_timed = true;
+    return APEX_OK;
+  }
+  c->k1_timed = false;
   if (n_tasks <= kPvTasks && d % kPvCols == 0 && c->opt_pre_rows) {
     // row-parallel form: every task per thread, u streamed in 16-column chunks
     const size_t smem2 = ((size_t)((n_tasks * d + 1) & ~1) + 2 * (size_t)kPvRows * kPvLd) * sizeof(double);
@@ -1713,6 +1733,19 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
   const int64_t blocks = std::min<int64_t>((n_pairs + kPreRows - 1) / kPreRows, (int64_t)c->sm_count * std::max(occ, 1));
   precompute_kernel<<<(unsigned)blocks, 256, smem, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks, values_dev);
   APEX_CU(cudaGetLastError());
+  return APEX_OK;
+}
+
+int apex_precompute_time(apex_ctx* c, double* kernel_ms) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, false));
+  if (!kernel_ms) return set_err(APEX_EINVAL, "null output");
+  *kernel_ms = -1.0;
+  if (!c->k1_timed) return APEX_OK;
+  APEX_CU(cudaEventSynchronize(c->mev[1]));
+  float ms = 0.f;
+  APEX_CU(cudaEventElapsedTime(&ms, c->mev[0], c->mev[1]));
+  *kernel_ms = ms;
   return APEX_OK;
 }
 

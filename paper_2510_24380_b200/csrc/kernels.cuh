@@ -226,6 +226,95 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
   }
 }
 
+// K1, bulk-copy form (compile-time task count x width, the APEX model's
+// 11 x 64): HBM-bound by design.  One persistent CTA per SM streams tiles of
+// kBulkRows consecutive pair rows of u (kBulkRows x D doubles, 64 KB) into a
+// kBulkStages-deep shared-memory ring with 1-D TMA bulk copies (one
+// cp.async.bulk per row, into rows padded to D + 2 doubles so the LDS.128 row
+// reads of a warp are bank-conflict free), completion on an mbarrier per
+// stage, so two tiles (128 KB) are always in flight while the third is
+// consumed.  Thread r owns row r of the tile and computes every task's dot
+// with the head weights taken straight from the kernel-parameter constant
+// bank (DFMA constant operands: no shared-memory broadcast loads).  Per
+// (task, row) the fp64 FMA chain runs c = 0..D-1 from 0.0, the same order as
+// the other forms, then rounds to fp32 (engine.py:82).
+constexpr int kBulkRows = 128, kBulkStages = 3;
+template <int NT, int D>
+struct HeadParams {
+  double w[NT * D];
+};
+template <int NT, int D>
+constexpr size_t bulk_smem_bytes() {
+  return (size_t)kBulkStages * kBulkRows * (D + 2) * sizeof(double) + kBulkStages * sizeof(uint64_t);
+}
+
+template <int NT, int D>
+__global__ void __launch_bounds__(kBulkRows, 1) precompute_bulk_kernel(const double* __restrict__ u, int64_t n_pairs,
+                                                                       const __grid_constant__ HeadParams<NT, D> W,
+                                                                       float* __restrict__ values) {
+  constexpr int LD = D + 2;
+  extern __shared__ __align__(128) unsigned char bulk_sm[];
+  double* ring = reinterpret_cast<double*>(bulk_sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kBulkStages * kBulkRows * LD);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t n_tiles = (n_pairs + kBulkRows - 1) / kBulkRows;
+  const int64_t grid = gridDim.x;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // warp 0 fills stage s with tile `tile`: lane 0 posts the byte count, then
+  // the 32 lanes issue the row copies
+  auto issue = [&](int64_t tile, int s) {
+    const int64_t base = tile * kBulkRows;
+    const int rows = (int)min((int64_t)kBulkRows, n_pairs - base);
+    if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(rows * D * sizeof(double)));
+    __syncwarp();
+    double* dst = ring + (size_t)s * kBulkRows * LD;
+    for (int r = lane; r < rows; r += 32) bulk_g2s(dst + r * LD, u + (base + r) * D, D * sizeof(double), &full[s]);
+  };
+  if (tid < 32) {
+#pragma unroll
+    for (int s = 0; s < kBulkStages; ++s) {
+      const int64_t tile = blockIdx.x + s * grid;
+      if (tile < n_tiles) issue(tile, s);
+    }
+  }
+  for (int64_t it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + it * grid;
+    if (tile >= n_tiles) break;
+    const int s = (int)(it % kBulkStages);
+    mbar_wait(&full[s], (uint32_t)((it / kBulkStages) & 1));
+    const int64_t base = tile * kBulkRows;
+    const int rows = (int)min((int64_t)kBulkRows, n_pairs - base);
+    if (tid < rows) {
+      const double* ur = ring + ((size_t)s * kBulkRows + tid) * LD;
+      double acc[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) acc[t] = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; c += 2) {
+        const double2 uv = *reinterpret_cast<const double2*>(ur + c);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          acc[t] = __fma_rn(W.w[t * D + c], uv.x, acc[t]);
+          acc[t] = __fma_rn(W.w[t * D + c + 1], uv.y, acc[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) values[(int64_t)t * n_pairs + base + tid] = __double2float_rn(acc[t]);
+    }
+    __syncthreads();  // every thread has read stage s
+    const int64_t next = tile + kBulkStages * grid;
+    if (tid < 32 && next < n_tiles) {
+      fence_proxy_async();  // order the generic-proxy reads of stage s before the async-proxy refill
+      issue(next, s);
+    }
+  }
+}
+
 // 64-bit division with a 32-bit fast path (operands below 2^32)
 __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n, uint64_t d) {
   if ((n >> 32) == 0 && (d >> 32) == 0) {
@@ -1556,20 +1645,25 @@ __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool low
 // the ends of every table first, then the binary searches in lockstep, so the
 // four dependent-load chains overlap.  th[u] is the signed-value threshold
 // (lower tests compare -x <= th, i.e. x >= -th); NaN means nothing passes.
-__device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride, const int (&task)[4],
-                                             const bool (&lower)[4], const float (&th)[4], int (&qc)[4]) {
-  const float* q[4];
-  float t[4], qlo[4], qhi[4];
-  int lo[4], hi[4];
+#ifndef APEX_THR_BATCH
+#define APEX_THR_BATCH 2
+#endif
+constexpr int kThrBatch = APEX_THR_BATCH;  // tests whose threshold chains are interleaved
+__device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride,
+                                             const int (&task)[kThrBatch], const bool (&lower)[kThrBatch],
+                                             const float (&th)[kThrBatch], int (&qc)[kThrBatch]) {
+  const float* q[kThrBatch];
+  float t[kThrBatch], qlo[kThrBatch], qhi[kThrBatch];
+  int lo[kThrBatch], hi[kThrBatch];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kThrBatch; ++u) {
     q[u] = qbase + (int64_t)task[u] * qstride;
     t[u] = lower[u] ? -th[u] : th[u];
     qlo[u] = __ldg(q[u]);
     qhi[u] = __ldg(q[u] + kQuant);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < kThrBatch; ++u) {
     lo[u] = 1;
     hi[u] = kQuant;
     qc[u] = -1;  // undecided: search
@@ -1585,15 +1679,15 @@ __device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, in
   }
 #pragma unroll
   for (int step = 0; step < 5; ++step) {  // ceil(log2(kQuant)) halvings of [1, kQuant]
-    float x[4];
-    int mid[4];
+    float x[kThrBatch];
+    int mid[kThrBatch];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kThrBatch; ++u) {
       mid[u] = (lo[u] + hi[u]) >> 1;
       x[u] = lo[u] < hi[u] ? __ldg(q[u] + mid[u]) : 0.0f;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kThrBatch; ++u) {
       if (lo[u] < hi[u]) {
         const bool go = lower[u] ? (x[u] < t[u]) : (x[u] <= t[u]);
         if (go) lo[u] = mid[u] + 1; else hi[u] = mid[u];
@@ -1601,7 +1695,7 @@ __device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, in
     }
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < kThrBatch; ++u)
     if (qc[u] < 0) qc[u] = lower[u] ? kQuant + 1 - lo[u] : lo[u];
 }
 
@@ -1723,15 +1817,15 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     }
     bool cons_ready = false;
     // every constraint's exact threshold (and, when choosing, its passing
-    // count in quantile steps), four tests at a time so their gathers,
+    // count in quantile steps), kThrBatch tests at a time so their gathers,
     // fp64 threshold math and quantile searches overlap instead of forming
     // one dependent chain per test
     auto constraint_thresholds = [&](bool choose) {
-      for (int i0 = 1; i0 < nt; i0 += 4) {
-        double p[4];
-        int task[4];
+      for (int i0 = 1; i0 < nt; i0 += kThrBatch) {
+        double p[kThrBatch];
+        int task[kThrBatch];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kThrBatch; ++u) {
           const int i = min(i0 + u, nt - 1);
           task[u] = Q.test_task[i];
           const float* v = values + (int64_t)task[u] * n_pairs;
@@ -1743,10 +1837,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
             if (j < c - 1) pp = __dadd_rn(pp, (double)__ldg(v + pr[j]));
           p[u] = pp;
         }
-        float th[4];
-        bool lower[4];
+        float th[kThrBatch];
+        bool lower[kThrBatch];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kThrBatch; ++u) {
           const int i = min(i0 + u, nt - 1);
           lower[u] = Q.test_lower[i] != 0;
           th[u] = lower[u] ? -thr_lower_fast(p[u], Q.test_bias[i], Q.test_beta[i])
@@ -1754,10 +1848,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
           if (i0 + u < nt) sthr[(i0 + u) * 32 + lane] = th[u];
         }
         if (choose) {
-          int qc[4];
+          int qc[kThrBatch];
           quant_count4(qbase, qstride, task, lower, th, qc);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < kThrBatch; ++u)
             if (i0 + u < nt && qc[u] < best_q) {
               best_q = qc[u];
               best = i0 + u;

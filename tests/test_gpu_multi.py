@@ -156,7 +156,8 @@ def _rank_main(rank, world, port, seed, ties, out):
     ctx.load_table(values, biases)
     if ties:
         qs = [{"obj": 0, "maximize": True, "cons": [], "k": 700, "start": 0, "end": lib.total}]
-        if rank == 1:
+        if rank == 1:  # only rank 1 overflows: the ranks must still agree on the re-gather
+            ctx.set_option("cap", 1024)
             ctx.set_option("samples", 16)
     else:
         qs = [q for q in _queries(lib.total) if q["k"] > 0]

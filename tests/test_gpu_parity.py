@@ -101,10 +101,10 @@ def test_golden_batch_equals_single(native):
         assert [e.objective for e in r.entries] == [e.objective for e in one.entries]
 
 
-@pytest.mark.parametrize("pre_rows", [1, 0])
+@pytest.mark.parametrize("pre_rows", [2, 1, 0])
 def test_precompute_matches_reference_table(native, pre_rows):
     """K1 (fp64 head_w @ u^T, fp32 rounding) == reference precompute_contributions,
-    for both kernel forms (row-parallel, shared-memory tiles)."""
+    for every kernel form (TMA bulk ring, row-parallel, shared-memory tiles)."""
     arr = golden_arrays()
     ctx = native.DeviceContext(0)
     ctx.set_option("pre_rows", pre_rows)
@@ -114,17 +114,19 @@ def test_precompute_matches_reference_table(native, pre_rows):
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
-@pytest.mark.parametrize("n_pairs,d,n_tasks", [(1, 16, 1), (300, 64, 11), (1000, 32, 16), (257, 48, 5), (5000, 64, 17)])
+@pytest.mark.parametrize("n_pairs,d,n_tasks", [(1, 16, 1), (300, 64, 11), (1000, 32, 16), (257, 48, 5), (5000, 64, 17),
+                                               (1, 64, 11), (100_003, 64, 11), (1_231_528, 64, 11)])
 def test_precompute_forms_agree_with_numpy_order(native, n_pairs, d, n_tasks):
-    """Both K1 forms give the same fp32 table (same per-entry FMA order) on odd
-    sizes: partial row blocks, d not 64, and > 16 tasks (tile form only)."""
+    """Every K1 form gives the same fp32 table (same per-entry FMA order) on odd
+    sizes: partial row blocks and tiles, d not 64, > 16 tasks (tile form only),
+    and the C4 table size through the TMA bulk ring (11 x 64)."""
     import torch
 
     rng = np.random.default_rng(n_pairs + d)
     u = rng.standard_normal((n_pairs, d))
     w = rng.standard_normal((n_tasks, d)) * 0.01
     outs = []
-    for pre in (1, 0):
+    for pre in (2, 1, 0):
         ctx = native.DeviceContext(0)
         ctx.set_option("pre_rows", pre)
         ud = torch.tensor(u, device="cuda")
@@ -135,6 +137,7 @@ def test_precompute_forms_agree_with_numpy_order(native, n_pairs, d, n_tasks):
         outs.append(vd.cpu().numpy())
         ctx.close()
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+    assert np.array_equal(outs[0].view(np.uint32), outs[2].view(np.uint32))
     # and close to the plain fp64 product (the exact order is pinned by the golden test above)
     assert np.allclose(outs[0], (w @ u.T).astype(np.float32), rtol=1e-6, atol=1e-6)
 
