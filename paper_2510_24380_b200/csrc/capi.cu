@@ -1702,7 +1702,7 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
     const int64_t tiles = (n_pairs + kBulkRows - 1) / kBulkRows;
     const int blocks = (int)std::min<int64_t>(tiles, c->sm_count);
     APEX_CU(cudaEventRecord(c->mev[0], c->stream));
-    precompute_bulk_kernel<11, 64><<<blocks, kBulkRows, smem, c->stream>>>(u_dev, n_pairs, W, values_dev);
+    precompute_bulk_kernel<11, 64><<<blocks, kBulkThreads, smem, c->stream>>>(u_dev, n_pairs, W, values_dev);
     APEX_CU(cudaGetLastError());
     APEX_CU(cudaEventRecord(c->mev[1], c->stream));
     c->k1_timed = true;
@@ -1720,8 +1720,11 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
       APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)fn, kPvRows, smem2));
       const int64_t blocks2 =
           std::min<int64_t>((n_pairs + kPvRows - 1) / kPvRows, (int64_t)c->sm_count * std::max(occ2, 1));
+      APEX_CU(cudaEventRecord(c->mev[0], c->stream));
       fn<<<(unsigned)blocks2, kPvRows, smem2, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks, values_dev);
       APEX_CU(cudaGetLastError());
+      APEX_CU(cudaEventRecord(c->mev[1], c->stream));
+      c->k1_timed = true;
       return APEX_OK;
     }
   }
@@ -1731,8 +1734,11 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
   int occ = 0;
   APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)precompute_kernel, 256, smem));
   const int64_t blocks = std::min<int64_t>((n_pairs + kPreRows - 1) / kPreRows, (int64_t)c->sm_count * std::max(occ, 1));
+  APEX_CU(cudaEventRecord(c->mev[0], c->stream));
   precompute_kernel<<<(unsigned)blocks, 256, smem, c->stream>>>(u_dev, n_pairs, d, w_dev, n_tasks, values_dev);
   APEX_CU(cudaGetLastError());
+  APEX_CU(cudaEventRecord(c->mev[1], c->stream));
+  c->k1_timed = true;
   return APEX_OK;
 }
 

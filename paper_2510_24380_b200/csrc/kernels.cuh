@@ -233,12 +233,13 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
 // cp.async.bulk per row, into rows padded to D + 2 doubles so the LDS.128 row
 // reads of a warp are bank-conflict free), completion on an mbarrier per
 // stage, so two tiles (128 KB) are always in flight while the third is
-// consumed.  Thread r owns row r of the tile and computes every task's dot
-// with the head weights taken straight from the kernel-parameter constant
-// bank (DFMA constant operands: no shared-memory broadcast loads).  Per
-// (task, row) the fp64 FMA chain runs c = 0..D-1 from 0.0, the same order as
-// the other forms, then rounds to fp32 (engine.py:82).
-constexpr int kBulkRows = 128, kBulkStages = 3;
+// consumed.  Warp w owns rows (w % 4) * 32 + lane of the tile and the task
+// group w / 4 (tasks [6g, 6g + 6)), so two warps per scheduler hide the
+// latency of the head weights, which come straight from the kernel-parameter
+// constant bank (uniform-register DFMA operands, no shared-memory broadcast
+// loads).  Per (task, row) the fp64 FMA chain runs c = 0..D-1 from 0.0, the
+// same order as the other forms, then rounds to fp32 (engine.py:82).
+constexpr int kBulkRows = 128, kBulkStages = 3, kBulkGroups = 2, kBulkThreads = kBulkRows * kBulkGroups;
 template <int NT, int D>
 struct HeadParams {
   double w[NT * D];
@@ -248,15 +249,39 @@ constexpr size_t bulk_smem_bytes() {
   return (size_t)kBulkStages * kBulkRows * (D + 2) * sizeof(double) + kBulkStages * sizeof(uint64_t);
 }
 
+template <int NT, int D, int G>
+__device__ __forceinline__ void bulk_dots(const double* __restrict__ ur, const HeadParams<NT, D>& W, int64_t n_pairs,
+                                          int64_t row, float* __restrict__ values) {
+  constexpr int TG = (NT + kBulkGroups - 1) / kBulkGroups;
+  constexpr int T0 = G * TG, T1 = (T0 + TG < NT) ? T0 + TG : NT;
+  double acc[TG];
+#pragma unroll
+  for (int t = 0; t < TG; ++t) acc[t] = 0.0;
+#pragma unroll
+  for (int c = 0; c < D; c += 2) {
+    const double2 uv = *reinterpret_cast<const double2*>(ur + c);
+#pragma unroll
+    for (int t = T0; t < T1; ++t) {
+      acc[t - T0] = __fma_rn(W.w[t * D + c], uv.x, acc[t - T0]);
+      acc[t - T0] = __fma_rn(W.w[t * D + c + 1], uv.y, acc[t - T0]);
+    }
+  }
+#pragma unroll
+  for (int t = T0; t < T1; ++t) values[(int64_t)t * n_pairs + row] = __double2float_rn(acc[t - T0]);
+}
+
 template <int NT, int D>
-__global__ void __launch_bounds__(kBulkRows, 1) precompute_bulk_kernel(const double* __restrict__ u, int64_t n_pairs,
-                                                                       const __grid_constant__ HeadParams<NT, D> W,
-                                                                       float* __restrict__ values) {
+__global__ void __launch_bounds__(kBulkThreads, 1) precompute_bulk_kernel(const double* __restrict__ u, int64_t n_pairs,
+                                                                          const __grid_constant__ HeadParams<NT, D> W,
+                                                                          float* __restrict__ values) {
+  static_assert(kBulkGroups == 2, "bulk_dots dispatch assumes two task groups");
   constexpr int LD = D + 2;
   extern __shared__ __align__(128) unsigned char bulk_sm[];
   double* ring = reinterpret_cast<double*>(bulk_sm);
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + kBulkStages * kBulkRows * LD);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = (warp % (kBulkRows / 32)) * 32 + lane;  // row within the tile
+  const int grp = warp / (kBulkRows / 32);              // task group (warp-uniform)
   const int64_t n_tiles = (n_pairs + kBulkRows - 1) / kBulkRows;
   const int64_t grid = gridDim.x;
   if (tid == 0) {
@@ -273,9 +298,9 @@ __global__ void __launch_bounds__(kBulkRows, 1) precompute_bulk_kernel(const dou
     if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(rows * D * sizeof(double)));
     __syncwarp();
     double* dst = ring + (size_t)s * kBulkRows * LD;
-    for (int r = lane; r < rows; r += 32) bulk_g2s(dst + r * LD, u + (base + r) * D, D * sizeof(double), &full[s]);
+    for (int rr = lane; rr < rows; rr += 32) bulk_g2s(dst + rr * LD, u + (base + rr) * D, D * sizeof(double), &full[s]);
   };
-  if (tid < 32) {
+  if (warp == 0) {
 #pragma unroll
     for (int s = 0; s < kBulkStages; ++s) {
       const int64_t tile = blockIdx.x + s * grid;
@@ -289,26 +314,14 @@ __global__ void __launch_bounds__(kBulkRows, 1) precompute_bulk_kernel(const dou
     mbar_wait(&full[s], (uint32_t)((it / kBulkStages) & 1));
     const int64_t base = tile * kBulkRows;
     const int rows = (int)min((int64_t)kBulkRows, n_pairs - base);
-    if (tid < rows) {
-      const double* ur = ring + ((size_t)s * kBulkRows + tid) * LD;
-      double acc[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) acc[t] = 0.0;
-#pragma unroll
-      for (int c = 0; c < D; c += 2) {
-        const double2 uv = *reinterpret_cast<const double2*>(ur + c);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          acc[t] = __fma_rn(W.w[t * D + c], uv.x, acc[t]);
-          acc[t] = __fma_rn(W.w[t * D + c + 1], uv.y, acc[t]);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t) values[(int64_t)t * n_pairs + base + tid] = __double2float_rn(acc[t]);
+    if (r < rows) {
+      const double* ur = ring + ((size_t)s * kBulkRows + r) * LD;
+      if (grp == 0) bulk_dots<NT, D, 0>(ur, W, n_pairs, base + r, values);
+      else bulk_dots<NT, D, 1>(ur, W, n_pairs, base + r, values);
     }
     __syncthreads();  // every thread has read stage s
     const int64_t next = tile + kBulkStages * grid;
-    if (tid < 32 && next < n_tiles) {
+    if (warp == 0 && next < n_tiles) {
       fence_proxy_async();  // order the generic-proxy reads of stage s before the async-proxy refill
       issue(next, s);
     }
@@ -1646,7 +1659,7 @@ __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool low
 // four dependent-load chains overlap.  th[u] is the signed-value threshold
 // (lower tests compare -x <= th, i.e. x >= -th); NaN means nothing passes.
 #ifndef APEX_THR_BATCH
-#define APEX_THR_BATCH 2
+#define APEX_THR_BATCH 1
 #endif
 constexpr int kThrBatch = APEX_THR_BATCH;  // tests whose threshold chains are interleaved
 __device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride,
