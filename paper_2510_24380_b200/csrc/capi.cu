@@ -26,6 +26,8 @@
 #include <thread>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
 
 using namespace apexb200;
@@ -1683,6 +1685,21 @@ int apex_load_table(apex_ctx* c, const float* values, const double* biases, int3
   return APEX_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
 int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, int32_t d, const double* w_dev,
                            int32_t n_tasks, float* values_dev) {
   APEX_LOCK(c);
@@ -1690,19 +1707,30 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
   if (n_pairs < 0 || d < 1 || n_tasks < 1 || !w_dev || !values_dev || (n_pairs > 0 && !u_dev))
     return set_err(APEX_EINVAL, "bad precompute arguments");
   if (n_pairs == 0) return APEX_OK;
-  if (n_tasks == 11 && d == 64 && c->opt_pre_rows == 2) {
-    // bulk-copy form (the APEX model's 11 x 64): one persistent CTA per SM,
-    // TMA ring of u tiles, head weights as kernel parameters
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (n_tasks == 11 && d == 64 && c->opt_pre_rows == 2 && encode && n_pairs < (int64_t(1) << 31) &&
+      (reinterpret_cast<uintptr_t>(u_dev) & 15) == 0) {
+    // TMA form (the APEX model's 11 x 64): one persistent CTA per SM, swizzled
+    // 2-D tensor copies of u tiles into a 3-stage ring, heads as kernel parameters
     HeadParams<11, 64> W;
     APEX_CU(cudaMemcpyAsync(W.w, w_dev, sizeof(W.w), cudaMemcpyDeviceToHost, c->stream));
     APEX_CU(cudaStreamSynchronize(c->stream));
+    CUtensorMap tmap;
+    const cuuint64_t dims[2] = {64, (cuuint64_t)n_pairs};
+    const cuuint64_t strides[1] = {64 * sizeof(double)};
+    const cuuint32_t box[2] = {kBulkBoxCols, kBulkRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult er = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(u_dev), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (er != CUDA_SUCCESS) return set_err(APEX_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)er) + ")");
     const size_t smem = bulk_smem_bytes<11, 64>();
     APEX_CU(cudaFuncSetAttribute((const void*)precompute_bulk_kernel<11, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     const int64_t tiles = (n_pairs + kBulkRows - 1) / kBulkRows;
     const int blocks = (int)std::min<int64_t>(tiles, c->sm_count);
     APEX_CU(cudaEventRecord(c->mev[0], c->stream));
-    precompute_bulk_kernel<11, 64><<<blocks, kBulkThreads, smem, c->stream>>>(u_dev, n_pairs, W, values_dev);
+    precompute_bulk_kernel<11, 64><<<blocks, kBulkThreads, smem, c->stream>>>(tmap, n_pairs, W, values_dev);
     APEX_CU(cudaGetLastError());
     APEX_CU(cudaEventRecord(c->mev[1], c->stream));
     c->k1_timed = true;

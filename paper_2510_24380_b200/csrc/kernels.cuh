@@ -13,6 +13,8 @@
 //
 // Included exactly once (by capi.cu): one translation unit, no -rdc.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace apexb200 {
@@ -226,59 +228,84 @@ __global__ void __launch_bounds__(kPvRows) precompute_rows_kernel(const double* 
   }
 }
 
-// K1, bulk-copy form (compile-time task count x width, the APEX model's
-// 11 x 64): HBM-bound by design.  One persistent CTA per SM streams tiles of
-// kBulkRows consecutive pair rows of u (kBulkRows x D doubles, 64 KB) into a
-// kBulkStages-deep shared-memory ring with 1-D TMA bulk copies (one
-// cp.async.bulk per row, into rows padded to D + 2 doubles so the LDS.128 row
-// reads of a warp are bank-conflict free), completion on an mbarrier per
-// stage, so two tiles (128 KB) are always in flight while the third is
-// consumed.  Warp w owns rows (w % 4) * 32 + lane of the tile and the task
-// group w / 4 (tasks [6g, 6g + 6)), so two warps per scheduler hide the
-// latency of the head weights, which come straight from the kernel-parameter
-// constant bank (uniform-register DFMA operands, no shared-memory broadcast
-// loads).  Per (task, row) the fp64 FMA chain runs c = 0..D-1 from 0.0, the
-// same order as the other forms, then rounds to fp32 (engine.py:82).
+// K1, TMA form (compile-time task count x width, the APEX model's 11 x 64):
+// HBM-bound by design.  One persistent CTA per SM streams tiles of kBulkRows
+// consecutive pair rows of u (kBulkRows x 64 doubles = 64 KB) into a
+// kBulkStages-deep shared-memory ring with 2-D TMA tensor copies
+// (cp.async.bulk.tensor, four 128-row x 16-column boxes per tile, 128-byte
+// swizzle: the 16-byte chunk j of a box row r lands at chunk j ^ (r & 7), so
+// the LDS.128 row reads of a warp are bank-conflict free without padding).
+// Completion is signalled on a per-stage "full" mbarrier; every warp arrives
+// on the stage's "empty" mbarrier when it has read the stage, and warp 0
+// refills it after waiting on that barrier alone (no CTA-wide barrier per
+// tile: the other warps run ahead on the stages already in flight).  Warp w
+// owns rows (w % 4) * 32 + lane of the tile and task group w / 4 (tasks
+// [6g, 6g + 6)); the head weights come straight from the kernel-parameter
+// constant bank (uniform-register DFMA operands).  Per (task, row) the fp64
+// FMA chain runs c = 0..63 from 0.0, the same order as the other forms, then
+// rounds to fp32 (engine.py:82).
 constexpr int kBulkRows = 128, kBulkStages = 3, kBulkGroups = 2, kBulkThreads = kBulkRows * kBulkGroups;
+constexpr int kBulkBoxCols = 16;  // doubles per box row (128 B: the 128-byte swizzle span)
 template <int NT, int D>
 struct HeadParams {
   double w[NT * D];
 };
 template <int NT, int D>
 constexpr size_t bulk_smem_bytes() {
-  return (size_t)kBulkStages * kBulkRows * (D + 2) * sizeof(double) + kBulkStages * sizeof(uint64_t);
+  return 1024 + (size_t)kBulkStages * kBulkRows * D * sizeof(double) + 2 * kBulkStages * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 template <int NT, int D, int G>
-__device__ __forceinline__ void bulk_dots(const double* __restrict__ ur, const HeadParams<NT, D>& W, int64_t n_pairs,
-                                          int64_t row, float* __restrict__ values) {
+__device__ __forceinline__ void bulk_dots(const unsigned char* __restrict__ tile, int r, const HeadParams<NT, D>& W,
+                                          int64_t n_pairs, int64_t row, float* __restrict__ values) {
   constexpr int TG = (NT + kBulkGroups - 1) / kBulkGroups;
   constexpr int T0 = G * TG, T1 = (T0 + TG < NT) ? T0 + TG : NT;
   double acc[TG];
 #pragma unroll
   for (int t = 0; t < TG; ++t) acc[t] = 0.0;
+  const int sw = r & 7;
 #pragma unroll
-  for (int c = 0; c < D; c += 2) {
-    const double2 uv = *reinterpret_cast<const double2*>(ur + c);
+  for (int box = 0; box < D / kBulkBoxCols; ++box) {
+    const unsigned char* rowp = tile + ((size_t)box * kBulkRows + r) * (kBulkBoxCols * sizeof(double));
 #pragma unroll
-    for (int t = T0; t < T1; ++t) {
-      acc[t - T0] = __fma_rn(W.w[t * D + c], uv.x, acc[t - T0]);
-      acc[t - T0] = __fma_rn(W.w[t * D + c + 1], uv.y, acc[t - T0]);
+    for (int j = 0; j < kBulkBoxCols / 2; ++j) {
+      const double2 uv = *reinterpret_cast<const double2*>(rowp + ((j ^ sw) << 4));
+      const int c = box * kBulkBoxCols + 2 * j;
+#pragma unroll
+      for (int t = T0; t < T1; ++t) {
+        acc[t - T0] = __fma_rn(W.w[t * D + c], uv.x, acc[t - T0]);
+        acc[t - T0] = __fma_rn(W.w[t * D + c + 1], uv.y, acc[t - T0]);
+      }
     }
   }
 #pragma unroll
   for (int t = T0; t < T1; ++t) values[(int64_t)t * n_pairs + row] = __double2float_rn(acc[t - T0]);
 }
 
+// tmap: 2-D tensor map of u (dims {D, n_pairs}, box {16, kBulkRows}, 128-byte swizzle), built by capi.cu
 template <int NT, int D>
-__global__ void __launch_bounds__(kBulkThreads, 1) precompute_bulk_kernel(const double* __restrict__ u, int64_t n_pairs,
+__global__ void __launch_bounds__(kBulkThreads, 1) precompute_bulk_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                          int64_t n_pairs,
                                                                           const __grid_constant__ HeadParams<NT, D> W,
                                                                           float* __restrict__ values) {
-  static_assert(kBulkGroups == 2, "bulk_dots dispatch assumes two task groups");
-  constexpr int LD = D + 2;
-  extern __shared__ __align__(128) unsigned char bulk_sm[];
-  double* ring = reinterpret_cast<double*>(bulk_sm);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kBulkStages * kBulkRows * LD);
+  static_assert(kBulkGroups == 2 && D % kBulkBoxCols == 0, "bulk form: two task groups, 16-column boxes");
+  constexpr uint32_t kTileBytes = kBulkRows * D * sizeof(double);
+  extern __shared__ unsigned char bulk_raw[];
+  // the 128-byte swizzle pattern repeats every 1024 bytes: align the ring to that
+  unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(bulk_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)kBulkStages * kTileBytes);
+  uint64_t* empty = full + kBulkStages;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = (warp % (kBulkRows / 32)) * 32 + lane;  // row within the tile
   const int grp = warp / (kBulkRows / 32);              // task group (warp-uniform)
@@ -286,21 +313,22 @@ __global__ void __launch_bounds__(kBulkThreads, 1) precompute_bulk_kernel(const 
   const int64_t grid = gridDim.x;
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkThreads / 32);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  // warp 0 fills stage s with tile `tile`: lane 0 posts the byte count, then
-  // the 32 lanes issue the row copies
-  auto issue = [&](int64_t tile, int s) {
-    const int64_t base = tile * kBulkRows;
-    const int rows = (int)min((int64_t)kBulkRows, n_pairs - base);
-    if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)(rows * D * sizeof(double)));
-    __syncwarp();
-    double* dst = ring + (size_t)s * kBulkRows * LD;
-    for (int rr = lane; rr < rows; rr += 32) bulk_g2s(dst + rr * LD, u + (base + rr) * D, D * sizeof(double), &full[s]);
+  auto issue = [&](int64_t tile, int s) {  // one thread
+    mbar_expect_tx(&full[s], kTileBytes);  // out-of-range rows of the last tile are zero-filled and counted
+    unsigned char* dst = ring + (size_t)s * kTileBytes;
+#pragma unroll
+    for (int box = 0; box < D / kBulkBoxCols; ++box)
+      tma_load_2d(dst + (size_t)box * kBulkRows * kBulkBoxCols * sizeof(double), &tmap, box * kBulkBoxCols,
+                  (int)(tile * kBulkRows), &full[s]);
   };
-  if (warp == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < kBulkStages; ++s) {
       const int64_t tile = blockIdx.x + s * grid;
@@ -311,18 +339,20 @@ __global__ void __launch_bounds__(kBulkThreads, 1) precompute_bulk_kernel(const 
     const int64_t tile = blockIdx.x + it * grid;
     if (tile >= n_tiles) break;
     const int s = (int)(it % kBulkStages);
-    mbar_wait(&full[s], (uint32_t)((it / kBulkStages) & 1));
+    const uint32_t phase = (uint32_t)((it / kBulkStages) & 1);
+    mbar_wait(&full[s], phase);
     const int64_t base = tile * kBulkRows;
-    const int rows = (int)min((int64_t)kBulkRows, n_pairs - base);
-    if (r < rows) {
-      const double* ur = ring + ((size_t)s * kBulkRows + r) * LD;
-      if (grp == 0) bulk_dots<NT, D, 0>(ur, W, n_pairs, base + r, values);
-      else bulk_dots<NT, D, 1>(ur, W, n_pairs, base + r, values);
+    const unsigned char* tp = ring + (size_t)s * kTileBytes;
+    if (base + r < n_pairs) {
+      if (grp == 0) bulk_dots<NT, D, 0>(tp, r, W, n_pairs, base + r, values);
+      else bulk_dots<NT, D, 1>(tp, r, W, n_pairs, base + r, values);
     }
-    __syncthreads();  // every thread has read stage s
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     const int64_t next = tile + kBulkStages * grid;
-    if (warp == 0 && next < n_tiles) {
-      fence_proxy_async();  // order the generic-proxy reads of stage s before the async-proxy refill
+    if (tid == 0 && next < n_tiles) {
+      mbar_wait(&empty[s], phase);  // every warp has read stage s
+      fence_proxy_async();          // their generic-proxy reads before the async-proxy refill
       issue(next, s);
     }
   }
