@@ -168,8 +168,10 @@ int apex_load_cache(apex_ctx* ctx, const double* u, int64_t n_pairs, int32_t d,
                     const double* head_w, const double* head_b, int32_t n_tasks,
                     float* values_out);
 
-/* Same as apex_load_cache but u / head_w / values_out are DEVICE pointers
- * (no host copies); used to time K1 alone. */
+/* Same as apex_load_cache but u / values_out are DEVICE pointers (no host
+ * copies); head_w may be device or host memory (the 11 x 64 TMA form passes
+ * the heads as kernel parameters: host heads need no device round trip).
+ * Used to time K1 alone (apex_precompute_time). */
 int apex_precompute_device(apex_ctx* ctx, const double* u_dev, int64_t n_pairs, int32_t d,
                            const double* head_w_dev, int32_t n_tasks, float* values_dev);
 

@@ -1713,8 +1713,16 @@ int apex_precompute_device(apex_ctx* c, const double* u_dev, int64_t n_pairs, in
     // TMA form (the APEX model's 11 x 64): one persistent CTA per SM, swizzled
     // 2-D tensor copies of u tiles into a 3-stage ring, heads as kernel parameters
     HeadParams<11, 64> W;
-    APEX_CU(cudaMemcpyAsync(W.w, w_dev, sizeof(W.w), cudaMemcpyDeviceToHost, c->stream));
-    APEX_CU(cudaStreamSynchronize(c->stream));
+    cudaPointerAttributes pa;
+    const bool w_on_host = cudaPointerGetAttributes(&pa, w_dev) == cudaSuccess &&
+                           (pa.type == cudaMemoryTypeHost || pa.type == cudaMemoryTypeUnregistered);
+    cudaGetLastError();
+    if (w_on_host) {
+      std::memcpy(W.w, w_dev, sizeof(W.w));  // heads given in host memory: no device round trip, no sync
+    } else {
+      APEX_CU(cudaMemcpyAsync(W.w, w_dev, sizeof(W.w), cudaMemcpyDeviceToHost, c->stream));
+      APEX_CU(cudaStreamSynchronize(c->stream));
+    }
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {64, (cuuint64_t)n_pairs};
     const cuuint64_t strides[1] = {64 * sizeof(double)};
@@ -1798,7 +1806,10 @@ int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, co
   APEX_CU(cudaMemcpyAsync(du.p, u, (size_t)n_pairs * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   APEX_CU(cudaMemcpyAsync(dw.p, head_w, (size_t)n_tasks * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   APEX_CU(cudaMemcpyAsync(c->d_biases.p, head_b, n_tasks * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  int rc = apex_precompute_device(c, du.as<double>(), n_pairs, d, dw.as<double>(), n_tasks, c->d_values.as<float>());
+  // (the TMA form takes the host heads directly as kernel parameters)
+  const bool host_heads = n_tasks == 11 && d == 64 && c->opt_pre_rows == 2;
+  int rc = apex_precompute_device(c, du.as<double>(), n_pairs, d, host_heads ? head_w : dw.as<double>(), n_tasks,
+                                  c->d_values.as<float>());
   if (rc != APEX_OK) {
     du.release();
     dw.release();
