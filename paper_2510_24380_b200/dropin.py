@@ -5,7 +5,8 @@
     # or run the reference CLI on the B200 path:
     python -m paper_2510_24380_b200.dropin search --library ... --table ... --query ... --out ...
 
-install() rebinds the reference's operator API for this path — the names its
+install() rebinds the reference's operator API for this path (the three
+search / precompute functions and load_table, memory-mapped) — the names its
 callers resolve at call time (cli.py:166, 180-183, 199-202 via
 `engine.<name>`; evalkit.py:12-20 imports `search_topk_stream` by name, so
 that module attribute is rebound too) — and makes the drop-in raise the
@@ -26,9 +27,13 @@ def install() -> None:
     import apexcsl.engine as ref_engine
 
     _b200._ERROR_CLASS[0] = ref_engine.EngineError
+    def load_table(path):  # memory-mapped arrays, the reference's table class
+        return _b200.load_table(path, mmap=True, cls=ref_engine.ContributionTable)
+
     targets = [(ref_engine, "search_topk_stream", _b200.search_topk_stream),
                (ref_engine, "search_topk_batched", _b200.search_topk_batched),
-               (ref_engine, "precompute_contributions", _b200.precompute_contributions)]
+               (ref_engine, "precompute_contributions", _b200.precompute_contributions),
+               (ref_engine, "load_table", load_table)]
     try:
         import apexcsl.evalkit as ref_evalkit
         targets.append((ref_evalkit, "search_topk_stream", _b200.search_topk_stream))

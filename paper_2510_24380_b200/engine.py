@@ -471,6 +471,69 @@ def precompute_contributions(cache, surrogate, device=None):
     )
 
 
+# ---------------------------------------------------------------------------
+# contribution-table files (engine.py:425-460 over blobio.py:14-44)
+# ---------------------------------------------------------------------------
+
+BLOB_MAGIC = "apexblob1"
+TABLE_VERSION = 1
+
+
+def save_table(table, path) -> None:
+    """The reference's apexblob1 table file, byte for byte: one JSON header
+    line (sort_keys) with the array specs, then the raw little-endian arrays
+    in order values, biases, member_ids, rg_offsets, rg_ids."""
+    import json
+
+    arrays = {"values": np.asarray(table.values), "biases": np.asarray(table.biases),
+              "member_ids": np.asarray(table.member_ids), "rg_offsets": np.asarray(table.rg_offsets),
+              "rg_ids": np.asarray(table.rg_ids)}
+    meta = {"kind": "contribution_table", "version": TABLE_VERSION, "task_names": list(table.task_names),
+            "fingerprint": table.fingerprint}
+    header = {"magic": BLOB_MAGIC, "meta": meta,
+              "arrays": [{"name": k, "dtype": str(v.dtype), "shape": list(v.shape)} for k, v in arrays.items()]}
+    with open(path, "wb") as fh:
+        fh.write(json.dumps(header, sort_keys=True).encode() + b"\n")
+        for v in arrays.values():
+            fh.write(np.ascontiguousarray(v).tobytes())
+
+
+def load_table(path, mmap: bool = True, cls=None):
+    """Read a table file written by ``save_table`` / the reference's
+    ``save_table``.  With ``mmap`` (default) the arrays are read-only views of
+    the memory-mapped file: nothing is copied on the host, and the device
+    upload at the first query (apex_load_table) reads the pages straight from
+    the mapping — the 5e9-product table (58 MB) loads without a host copy.
+    ``mmap=False`` copies like the reference (engine.py:448-460).  ``cls``:
+    the table class to build (the reference's, under dropin.install())."""
+    import json
+
+    with open(path, "rb") as fh:
+        line = fh.readline()
+        header = json.loads(line.decode())
+        if header.get("magic") != BLOB_MAGIC:
+            raise ValueError(f"{path}: not an {BLOB_MAGIC} file")
+        offset = len(line)
+        arrays = {}
+        for spec in header["arrays"]:
+            dtype = np.dtype(spec["dtype"])
+            shape = tuple(spec["shape"])
+            n = int(np.prod(shape)) if shape else 1
+            if mmap and n > 0:
+                arrays[spec["name"]] = np.memmap(path, dtype=dtype, mode="r", offset=offset, shape=shape)
+            else:
+                fh.seek(offset)
+                arrays[spec["name"]] = np.frombuffer(fh.read(n * dtype.itemsize), dtype=dtype).reshape(shape).copy()
+            offset += n * dtype.itemsize
+    meta = header["meta"]
+    if meta.get("kind") != "contribution_table" or meta.get("version") != TABLE_VERSION:
+        raise _error(f"{path}: not a version-{TABLE_VERSION} contribution table")
+    return (cls or ContributionTable)(values=arrays["values"], biases=arrays["biases"],
+                                      task_names=list(meta["task_names"]), member_ids=arrays["member_ids"],
+                                      rg_offsets=arrays["rg_offsets"], rg_ids=arrays["rg_ids"],
+                                      fingerprint=meta["fingerprint"])
+
+
 RESULT_HEADER_PREFIX = "rank\tglobal_index\treaction_id\tsynthon_ids\tobjective\tviolation"
 
 

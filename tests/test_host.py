@@ -182,3 +182,29 @@ def test_native_row_builder_equals_python(use_reference, monkeypatch):
     assert [e.violation.hex() for e in fast.entries] == ["0x0.0p+0"] * 25
     assert (fast.scanned, fast.retained, fast.discarded_for_violation) == (slow.scanned, slow.retained,
                                                                            slow.discarded_for_violation)
+
+
+@pytest.mark.parametrize("mmap", [True, False])
+def test_table_file_roundtrip_and_reference_bytes(tmp_path, mmap):
+    """save_table writes the reference's apexblob1 bytes; load_table (memory
+    mapped or copied) returns the same arrays, bit for bit."""
+    case = golden_cases()[0]
+    table = case.table()
+    p = tmp_path / "t.blob"
+    engine.save_table(table, p)
+    back = engine.load_table(p, mmap=mmap)
+    for name in ("values", "biases", "member_ids", "rg_offsets", "rg_ids"):
+        a, b = np.asarray(getattr(table, name)), np.asarray(getattr(back, name))
+        assert a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes(), name
+    assert back.task_names == list(table.task_names) and back.fingerprint == table.fingerprint
+    if mmap:
+        assert isinstance(back.values, np.memmap) and not back.values.flags.writeable
+    rcsl, rengine = import_reference()
+    rt = rengine.ContributionTable(values=table.values, biases=table.biases, task_names=list(table.task_names),
+                                   member_ids=table.member_ids, rg_offsets=table.rg_offsets, rg_ids=table.rg_ids,
+                                   fingerprint=table.fingerprint)
+    q = tmp_path / "r.blob"
+    rengine.save_table(rt, q)
+    assert q.read_bytes() == p.read_bytes()
+    ref_back = rengine.load_table(p)
+    assert ref_back.values.tobytes() == np.asarray(back.values).tobytes()
