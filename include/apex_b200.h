@@ -251,6 +251,31 @@ int apex_multi_query(apex_multi* m, const apex_query_spec* queries, int32_t n_qu
                      apex_stats* stats);
 int apex_multi_info(apex_multi* m, int32_t* n_devices, int32_t* peer_access);
 
+/* Ground-truth evaluation on the device: the exhaustive
+ * oracle top-j of evalkit.oracle_topk (evalkit.py:49-90) over the synthetic
+ * ground-truth oracle (props.oracle_block_values, props.py:218-264), without
+ * the reference's 1e8-product guard.  Task t of the oracle: latent values per
+ * synthon id (row t of latents), +nonlinear (flags & 1): value +=
+ * nonlinear_scale * tanh(nonlinear_alpha * base), +pairwise (flags & 2): the
+ * splitmix pair coefficients keyed by salt (props.py:162-195). */
+typedef struct {
+  int32_t flags;            /* 1 = +nonlinear, 2 = +pairwise */
+  uint32_t salt;            /* _task_salt(oracle, task) (props.py:198-199) */
+  double nonlinear_scale;
+  double nonlinear_alpha;
+  double pair_scale;
+  double pair_density;
+} apex_gt_task;
+
+/* member_ids[p]: synthon id of pair row p (the library's pair rows as loaded
+ * by apex_load_library); latents: float64 [n_tasks][n_synthons]. */
+int apex_gt_load(apex_ctx* ctx, const int64_t* member_ids, int64_t n_pairs, const double* latents, int64_t n_synthons,
+                 const apex_gt_task* tasks, int32_t n_tasks);
+/* Oracle top-j (j = query->k; tasks index the oracle's tasks) over
+ * [start, end): result rows best-first by (s desc, g asc) among oracle-feasible
+ * products; objective / constraint_values are the oracle's values. */
+int apex_gt_topk(apex_ctx* ctx, const apex_query_spec* query, apex_result* result, apex_stats* stats);
+
 /* Tuning / introspection. */
 int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);
 

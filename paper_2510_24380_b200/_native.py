@@ -28,7 +28,7 @@ EXPORTED = (
     "apex_query_async", "apex_query_fetch", "apex_query_local", "apex_merge_finalize", "apex_merge_finalize_batch",
     "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
-    "apex_query_local_async", "apex_query_local_finish", "apex_precompute_time",
+    "apex_query_local_async", "apex_query_local_finish", "apex_precompute_time", "apex_gt_load", "apex_gt_topk",
     "apex_multi_create", "apex_multi_destroy", "apex_multi_load_library", "apex_multi_load_table",
     "apex_multi_load_cache", "apex_multi_set_option", "apex_multi_query", "apex_multi_info",
 )
@@ -117,6 +117,11 @@ class ResultC(C.Structure):
     ]
 
 
+class GtTaskC(C.Structure):
+    _fields_ = [("flags", C.c_int32), ("salt", C.c_uint32), ("nonlinear_scale", C.c_double),
+                ("nonlinear_alpha", C.c_double), ("pair_scale", C.c_double), ("pair_density", C.c_double)]
+
+
 class EntryC(C.Structure):
     _fields_ = [("key", C.c_uint64), ("g", C.c_uint64)]
 
@@ -154,6 +159,8 @@ def load_library(path: Path | None = None):
         "apex_merge_finalize_batch": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int32, C.c_int64, C.c_uint64,
                                        C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_precompute_time": ([vp, C.POINTER(C.c_double)], C.c_int),
+        "apex_gt_load": ([vp, vp, C.c_int64, vp, C.c_int64, vp, C.c_int32], C.c_int),
+        "apex_gt_topk": ([vp, C.POINTER(QuerySpecC), C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_query_local_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int64, C.POINTER(Stats)], C.c_int),
         "apex_query_local_finish": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(Stats)], C.c_int),
         "apex_multi_create": ([C.c_int32, C.POINTER(C.c_int32), C.POINTER(vp)], C.c_int),
@@ -483,6 +490,27 @@ class DeviceContext:
             "reaction": b["reaction"][:n], "digits": b["digits"][:n], "n": n, "discarded": res.discarded,
             "scanned": res.scanned,
         }, st.as_dict()
+
+    def gt_load(self, member_ids: np.ndarray, latents: np.ndarray, tasks: list[dict]) -> None:
+        """Ground-truth oracle tables (apex_gt_load): member_ids [n_pairs],
+        latents [n_tasks][n_synthons], per task {flags, salt, nonlinear_scale,
+        nonlinear_alpha, pair_scale, pair_density}."""
+        m = np.ascontiguousarray(member_ids, dtype=np.int64)
+        lat = np.ascontiguousarray(latents, dtype=np.float64)
+        arr = (GtTaskC * len(tasks))()
+        for i, t in enumerate(tasks):
+            for k, v in t.items():
+                setattr(arr[i], k, v)
+        _check(self.lib.apex_gt_load(self._ctx, _ptr(m), len(m), _ptr(lat), lat.shape[1], arr, len(tasks)))
+
+    def gt_topk(self, query: dict) -> tuple[dict, dict]:
+        """Oracle top-j of one query dict {obj, maximize, cons, k=j, start, end}."""
+        specs, keep = self._specs([query])
+        results, bufs = self._result_buffers([query])
+        st = Stats()
+        _check(self.lib.apex_gt_topk(self._ctx, specs, results, C.byref(st)))
+        del keep
+        return self._unpack(results, bufs)[0], st.as_dict()
 
     def debug_thresholds(self, p: np.ndarray, b: np.ndarray, beta: np.ndarray):
         p = np.ascontiguousarray(p, dtype=np.float64)

@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include "kernels.cuh"
+#include "gt.cuh"
 
 using namespace apexb200;
 
@@ -267,6 +268,11 @@ struct apex_ctx {
     std::vector<ScanQuery> uploaded;
   } mws;
   cudaEvent_t mev[2] = {};
+  // ground-truth oracle (apex_gt_load): members, latents, task parameters
+  DBuf d_gt_members, d_gt_latent, d_gt_tasks, d_gt_hist, d_gt_buf, d_gt_misc;
+  std::vector<GtTask> gt_tasks;
+  int64_t gt_synthons = 0;
+  bool gt_loaded = false;
   bool k1_timed = false;             // mev brackets the last K1 launch (apex_precompute_time)
   // per-context (= per-device) launch caches
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
@@ -1578,6 +1584,8 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   for (auto& ev : c->mev) cudaEventDestroy(ev);
+  for (DBuf* b : {&c->d_gt_members, &c->d_gt_latent, &c->d_gt_tasks, &c->d_gt_hist, &c->d_gt_buf, &c->d_gt_misc})
+    b->release();
   {
     auto& w = c->mws;
     for (auto& sl : w.slots) sl.release();
@@ -2142,6 +2150,213 @@ int apex_debug_trace(apex_ctx* c, uint64_t* out, int64_t cap, int64_t* n) {
   if (m <= 0) return APEX_OK;
   APEX_CU(cudaStreamSynchronize(c->stream));
   APEX_CU(cudaMemcpy(out, c->d_trace.p, (size_t)m * 64, cudaMemcpyDeviceToHost));
+  return APEX_OK;
+}
+
+// ===========================================================================
+// Ground-truth evaluation on the device (gt.cuh; evalkit.oracle_topk)
+// ===========================================================================
+
+int apex_gt_load(apex_ctx* c, const int64_t* member_ids, int64_t n_pairs, const double* latents, int64_t n_synthons,
+                 const apex_gt_task* tasks, int32_t n_tasks) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, false));
+  if (!c->lib_loaded) return set_err(APEX_ESTATE, "load the library before the ground-truth oracle");
+  if (n_pairs != c->lib_pairs || n_synthons < 1 || n_tasks < 1 || n_tasks > 4096 || !member_ids || !latents || !tasks)
+    return set_err(APEX_EINVAL, "bad ground-truth oracle arguments");
+  for (int64_t i = 0; i < n_pairs; ++i)
+    if (member_ids[i] < 0 || member_ids[i] >= n_synthons) return set_err(APEX_EINVAL, "synthon id out of range");
+  APEX_TRY(c->d_gt_members.ensure((size_t)n_pairs * sizeof(long long)));
+  APEX_TRY(c->d_gt_latent.ensure((size_t)n_tasks * n_synthons * sizeof(double)));
+  APEX_TRY(c->d_gt_tasks.ensure((size_t)n_tasks * sizeof(GtTask)));
+  APEX_CU(cudaMemcpy(c->d_gt_members.p, member_ids, (size_t)n_pairs * sizeof(long long), cudaMemcpyHostToDevice));
+  APEX_CU(cudaMemcpy(c->d_gt_latent.p, latents, (size_t)n_tasks * n_synthons * sizeof(double), cudaMemcpyHostToDevice));
+  c->gt_tasks.assign(n_tasks, GtTask{});
+  for (int t = 0; t < n_tasks; ++t) {
+    GtTask& T = c->gt_tasks[t];
+    T.latent = c->d_gt_latent.as<double>() + (size_t)t * n_synthons;
+    T.nl_scale = tasks[t].nonlinear_scale;
+    T.nl_alpha = tasks[t].nonlinear_alpha;
+    T.pair_scale = tasks[t].pair_scale;
+    T.pair_density = tasks[t].pair_density;
+    T.salt = tasks[t].salt;
+    T.flags = tasks[t].flags;
+  }
+  APEX_CU(cudaMemcpy(c->d_gt_tasks.p, c->gt_tasks.data(), (size_t)n_tasks * sizeof(GtTask), cudaMemcpyHostToDevice));
+  c->gt_synthons = n_synthons;
+  c->gt_loaded = true;
+  return APEX_OK;
+}
+
+int apex_gt_topk(apex_ctx* c, const apex_query_spec* q, apex_result* res, apex_stats* stats) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, true));
+  if (!c->gt_loaded) return set_err(APEX_ESTATE, "ground-truth oracle not loaded");
+  if (!q || !res || !res->global_index || !res->objective || !res->reaction || !res->digits ||
+      (q->n_constraints > 0 && !res->constraint_values))
+    return set_err(APEX_EINVAL, "bad ground-truth query arguments");
+  const int nt = (int)c->gt_tasks.size();
+  if (q->objective_task < 0 || q->objective_task >= nt) return set_err(APEX_ETASK, "unknown oracle task");
+  if (q->n_constraints < 0 || q->n_constraints > kMaxCons || (q->n_constraints && !q->constraints))
+    return set_err(APEX_EINVAL, "bad constraint list");
+  for (int m = 0; m < q->n_constraints; ++m)
+    if (q->constraints[m].task < 0 || q->constraints[m].task >= nt) return set_err(APEX_ETASK, "unknown oracle task");
+  if (q->k < 0) return set_err(APEX_EINVAL, "j must be >= 0");
+  if (!(q->start <= q->end && q->end <= c->total)) return set_err(APEX_ERANGE, "index range invalid");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const uint64_t span = q->end - q->start;
+  res->scanned = span;
+  res->candidates = res->admitted = 0;
+  res->full_predicate = 0;
+  res->n = 0;
+  res->discarded = 0;
+  if (q->k == 0 || span == 0) return APEX_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  int64_t max_last = 1;
+  for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
+  Plan* plan = nullptr;
+  APEX_TRY(build_plan(c, q->start, q->end, 32, 1, plan, max_last));
+  const unsigned long long cap = (unsigned long long)std::max<int64_t>(4 * q->k + 4096, 1 << 22);
+  APEX_TRY(c->d_gt_hist.ensure((65536 + 256) * sizeof(unsigned)));
+  APEX_TRY(c->d_gt_buf.ensure(cap * sizeof(Entry)));
+  APEX_TRY(c->d_gt_misc.ensure(64));
+  cudaStream_t s = c->stream;
+  GtPass P;
+  std::memset(&P, 0, sizeof(P));
+  P.rx = c->d_rx.as<DevReaction>();
+  P.tiles = plan->d_tiles.as<Tile>();
+  P.n_tiles = (unsigned)plan->tiles.size();
+  P.members = c->d_gt_members.as<long long>();
+  P.tasks = c->d_gt_tasks.as<GtTask>();
+  P.obj = q->objective_task;
+  P.maximize = q->maximize ? 1 : 0;
+  P.n_cons = q->n_constraints;
+  for (int m = 0; m < q->n_constraints; ++m) {
+    P.cons_task[m] = q->constraints[m].task;
+    P.cons_lo[m] = q->constraints[m].lower;
+    P.cons_hi[m] = q->constraints[m].upper;
+  }
+  P.hist = c->d_gt_hist.as<unsigned>();
+  P.buf = c->d_gt_buf.as<Entry>();
+  P.cap = cap;
+  unsigned long long* d_count = reinterpret_cast<unsigned long long*>(c->d_gt_misc.p);
+  long long* d_kth = reinterpret_cast<long long*>(c->d_gt_misc.as<unsigned char>() + 16);
+  unsigned* d_work = reinterpret_cast<unsigned*>(c->d_gt_misc.as<unsigned char>() + 32);
+  P.count = d_count;
+  P.work = d_work;
+  P.base = 0;
+  P.shift = 48;
+  P.glimit = q->end;
+  const int grid = c->sm_count * 8;
+  int64_t launches = 0;
+  // narrowing passes: the bin holding the j-th best key, 16 bits at a time
+  bool all = false;
+  for (int iter = 0;; ++iter) {
+    if (iter > 12) return set_err(APEX_ELIMIT, "ground-truth narrowing did not converge");
+    P.mode = 0;
+    APEX_CU(cudaMemsetAsync(P.hist, 0, (65536 + 256) * sizeof(unsigned), s));
+    APEX_CU(cudaMemsetAsync(d_work, 0, sizeof(unsigned), s));
+    gt_pass_kernel<<<grid, 256, 0, s>>>(P);
+    gt_kth_kernel<<<1, 32, 0, s>>>(P.hist, (unsigned long long)q->k, d_kth);
+    launches += 2;
+    long long kth[2];
+    APEX_CU(cudaMemcpyAsync(kth, d_kth, sizeof(kth), cudaMemcpyDeviceToHost, s));
+    APEX_CU(cudaStreamSynchronize(s));
+    const long long B = kth[0];
+    if (B < 0) {  // fewer than j admitted products: all of them are the answer (first pass: all feasible)
+      all = true;
+      break;
+    }
+    if ((unsigned long long)kth[1] <= cap) {  // bound found: collect
+      if (!P.tie) {
+        P.base = bin_edge((unsigned)B, P.base, P.shift);
+        P.shift = 63;  // collect admits key >= base (every key lands in bin 0 or 1)
+      } else {
+        const unsigned long long glo = P.gbase + ((unsigned long long)(65534 - std::min<long long>(B, 65534)) << P.gshift);
+        const unsigned long long ghi = glo + (1ull << P.gshift);
+        if (ghi > glo && ghi < P.glimit) P.glimit = ghi;
+      }
+      break;
+    }
+    if (!P.tie) {
+      const unsigned long long edge = bin_edge((unsigned)B, P.base, P.shift);
+      if (B == 65535) {
+        unsigned s2 = P.shift;
+        while (s2 < 63 && ((~0ull - edge) >> s2) >= 65535ull) ++s2;
+        P.base = edge;
+        P.shift = s2;
+      } else if (P.shift == 0) {
+        P.tie = 1;
+        P.tie_key = edge;
+        P.gbase = q->start;
+        P.glimit = q->end;
+        unsigned gs = 0;
+        while (gs < 63 && (span >> gs) >= 65535ull) ++gs;
+        P.gshift = gs;
+      } else {
+        P.base = edge;
+        P.shift = P.shift >= 16 ? P.shift - 16 : 0;
+      }
+    } else {
+      const unsigned long long glo = P.gbase + ((unsigned long long)(65534 - std::min<long long>(B, 65534)) << P.gshift);
+      const unsigned long long ghi = glo + (1ull << P.gshift);
+      if (ghi > glo && ghi < P.glimit) P.glimit = ghi;
+      P.gbase = glo;
+      P.gshift = P.gshift >= 16 ? P.gshift - 16 : 0;
+    }
+  }
+  if (all) {  // admit every feasible product at or above the current base (the first pass: base 0, everything)
+    P.shift = 63;
+  }
+  // collect
+  P.mode = 2;
+  APEX_CU(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  APEX_CU(cudaMemsetAsync(d_work, 0, sizeof(unsigned), s));
+  gt_pass_kernel<<<grid, 256, 0, s>>>(P);
+  ++launches;
+  unsigned long long count = 0;
+  APEX_CU(cudaMemcpyAsync(&count, d_count, sizeof(count), cudaMemcpyDeviceToHost, s));
+  APEX_CU(cudaStreamSynchronize(s));
+  if (count > cap) return set_err(APEX_ELIMIT, "ground-truth candidates exceed the buffer");
+  // exact select + order + decode through the merge (candidate buffer as one source)
+  apex_query_spec qm;
+  std::memset(&qm, 0, sizeof(qm));
+  qm.objective_task = 0;
+  qm.maximize = 1;
+  qm.k = q->k;
+  qm.start = q->start;
+  qm.end = q->end;
+  apex_result r = *res;
+  double* cons_keep = r.constraint_values;
+  r.constraint_values = nullptr;
+  apex_stats mst;
+  APEX_TRY(merge_impl(c, &qm, 1, c->d_gt_buf.as<Entry>(), nullptr, 1, (int64_t)count, span, &r, &mst));
+  const int n = (int)r.n;
+  // the oracle's objective / constraint values of the selected products
+  if (n > 0) {
+    DBuf dg, dv;
+    APEX_TRY(dg.ensure((size_t)n * 8));
+    APEX_TRY(dv.ensure((size_t)n * 8 * (1 + q->n_constraints)));
+    APEX_CU(cudaMemcpyAsync(dg.p, r.global_index, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    gt_values_kernel<<<(n + 127) / 128, 128, 0, s>>>(P, dg.as<unsigned long long>(), n, c->d_goff.as<unsigned long long>(),
+                                                     (int)c->rx.size(), dv.as<double>(), dv.as<double>() + n);
+    ++launches;
+    APEX_CU(cudaMemcpyAsync(r.objective, dv.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    if (q->n_constraints)
+      APEX_CU(cudaMemcpyAsync(cons_keep, dv.as<double>() + n, (size_t)n * 8 * q->n_constraints, cudaMemcpyDeviceToHost, s));
+    APEX_CU(cudaStreamSynchronize(s));
+    dg.release();
+    dv.release();
+  }
+  r.constraint_values = cons_keep;
+  r.candidates = (int64_t)count;
+  r.discarded = (int64_t)std::min<uint64_t>((uint64_t)q->k, span) - n;
+  *res = r;
+  if (stats) {
+    stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    stats->kernel_launches = launches + mst.kernel_launches;
+    stats->candidates = (int64_t)count;
+  }
   return APEX_OK;
 }
 

@@ -100,3 +100,46 @@ def test_c_oracle_matches_numpy_port(seed):
         y = fo.search_topk(values, biases, lib, q, a, b, threads=int(rng.integers(1, 6)))
         assert np.array_equal(x[0].view(np.uint64), y[0].view(np.uint64)) and np.array_equal(x[1], y[1])
         assert x[2:] == y[2:]
+
+
+def gt_cases():
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent / "golden"
+    doc = json.loads((root / "gt_golden.json").read_text())
+    arrays = dict(np.load(root / "gt_golden.npz"))
+    return doc["cases"], arrays
+
+
+def gt_oracle(case, arrays):
+    """Mirror GroundTruthOracle of a golden case (paper_2510_24380_b200.evalkit types)."""
+    from paper_2510_24380_b200 import evalkit
+
+    tasks = [evalkit.TaskDef(t["name"], t["mode"], arrays[f"{case['name']}/latent/{i}"],
+                             unhex(t["nonlinear_scale"]), unhex(t["nonlinear_alpha"]), unhex(t["pair_scale"]),
+                             unhex(t["pair_density"])) for i, t in enumerate(case["tasks"])]
+    return evalkit.GroundTruthOracle(tasks, case["seed"])
+
+
+def test_gt_oracle_matches_reference():
+    """oracle/gt_oracle.py (numpy restatement of props.oracle_block_values +
+    evalkit.oracle_topk) reproduces the reference's recorded oracle top-j."""
+    from oracle import gt_oracle as gto
+    from paper_2510_24380_b200 import csl
+
+    cases, arrays = gt_cases()
+    n = 0
+    for case in cases:
+        lib = csl.deserialize_library(case["library"])
+        oracle = gt_oracle(case, arrays)
+        names = [t["name"] for t in case["tasks"]]
+        for q in case["queries"]:
+            cons = [(names.index(t), unhex(lo), unhex(hi)) for t, lo, hi in q["constraints"]]
+            start, end = q["index_range"] if q["index_range"] else (0, None)
+            g, o = gto.topk(lib, oracle, names.index(q["objective"]), q["direction"] == "maximize", cons, q["j"],
+                            start, end)
+            assert g.tolist() == q["g"], (case["name"], q["objective"])
+            assert [x.hex() for x in o.tolist()] == q["objective_values"]
+            n += 1
+    assert n == 21
