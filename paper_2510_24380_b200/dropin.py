@@ -6,7 +6,8 @@
     python -m paper_2510_24380_b200.dropin search --library ... --table ... --query ... --out ...
 
 install() rebinds the reference's operator API for this path (the three
-search / precompute functions and load_table, memory-mapped) — the names its
+search / precompute functions, load_table (memory-mapped) and
+evalkit.oracle_topk (ground truth on the device)) — the names its
 callers resolve at call time (cli.py:166, 180-183, 199-202 via
 `engine.<name>`; evalkit.py:12-20 imports `search_topk_stream` by name, so
 that module attribute is rebound too) — and makes the drop-in raise the
@@ -36,7 +37,11 @@ def install() -> None:
                (ref_engine, "load_table", load_table)]
     try:
         import apexcsl.evalkit as ref_evalkit
+
+        from . import evalkit as _b200_eval
         targets.append((ref_evalkit, "search_topk_stream", _b200.search_topk_stream))
+        # ground truth on the device, past the 1e8 enumeration guard (evalkit.py:23)
+        targets.append((ref_evalkit, "oracle_topk", _b200_eval.oracle_topk))
     except ImportError:
         pass
     for mod, name, fn in targets:
