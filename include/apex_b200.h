@@ -276,6 +276,32 @@ int apex_gt_load(apex_ctx* ctx, const int64_t* member_ids, int64_t n_pairs, cons
  * products; objective / constraint_values are the oracle's values. */
 int apex_gt_topk(apex_ctx* ctx, const apex_query_spec* query, apex_result* result, apex_stats* stats);
 
+/* K8: the factorizer's hierarchy encoding on the device (
+ * factorizer.encode_hierarchy, factorizer.py:157-171, 218-233): synthon
+ * feature hashing (BLAKE2b-64 of "<salt>:<ngram>" for the 1/2/3-grams of each
+ * UTF-8 token, props.py:43-62), the synthon MLP, the R-group and reaction
+ * deep sets (mean pooling), the value and key MLPs, and the pair rows
+ * u[p] = v[member[p]] @ K[rgroup(p)]^T, all fp64.  nets: 7 MLP shapes in the
+ * order synthon, rgroup phi, rgroup rho, reaction phi, reaction rho, value,
+ * key (dims[0..n_layers], tanh between layers); params: every net's
+ * W0 [dims0 x dims1] (row-major), b0, W1, b1, ... concatenated in that order.
+ * The pair matrix stays resident for apex_precompute_resident; every *_out
+ * (host, optional) receives a copy. */
+typedef struct {
+  int32_t n_layers;
+  int32_t dims[7];
+} apex_mlp_shape;
+int apex_encode_hierarchy(apex_ctx* ctx, const apex_mlp_shape* nets, const double* params, int64_t n_params,
+                          const uint8_t* token_bytes, const int64_t* token_off, int64_t n_synthons,
+                          const uint8_t* salt, int32_t salt_len, int32_t p, double feature_scale,
+                          const int64_t* member_ids, int64_t n_pairs, const int64_t* rg_offsets, int32_t n_rg,
+                          const int32_t* rg_parent, const int64_t* rx_offsets, int32_t n_rx, int32_t d, int32_t d_u,
+                          double* u_out, double* h_s_out, double* h_r_out, double* h_t_out, double* features_out);
+/* K1 from the resident K8 pair matrix (engine.py:80-92): the table becomes
+ * resident (values_out, optional: host copy). */
+int apex_precompute_resident(apex_ctx* ctx, const double* head_w, const double* head_b, int32_t n_tasks,
+                             float* values_out);
+
 /* Tuning / introspection. */
 int apex_set_option(apex_ctx* ctx, const char* name, int64_t value);
 

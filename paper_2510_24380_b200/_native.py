@@ -29,6 +29,7 @@ EXPORTED = (
     "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
     "apex_query_local_async", "apex_query_local_finish", "apex_precompute_time", "apex_gt_load", "apex_gt_topk",
+    "apex_encode_hierarchy", "apex_precompute_resident",
     "apex_multi_create", "apex_multi_destroy", "apex_multi_load_library", "apex_multi_load_table",
     "apex_multi_load_cache", "apex_multi_set_option", "apex_multi_query", "apex_multi_info",
 )
@@ -122,6 +123,10 @@ class GtTaskC(C.Structure):
                 ("nonlinear_alpha", C.c_double), ("pair_scale", C.c_double), ("pair_density", C.c_double)]
 
 
+class MlpShapeC(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("dims", C.c_int32 * 7)]
+
+
 class EntryC(C.Structure):
     _fields_ = [("key", C.c_uint64), ("g", C.c_uint64)]
 
@@ -160,6 +165,10 @@ def load_library(path: Path | None = None):
                                        C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_precompute_time": ([vp, C.POINTER(C.c_double)], C.c_int),
         "apex_gt_load": ([vp, vp, C.c_int64, vp, C.c_int64, vp, C.c_int32], C.c_int),
+        "apex_encode_hierarchy": ([vp, vp, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int32, C.c_int32, C.c_double, vp,
+                                   C.c_int64, vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
+                                   vp], C.c_int),
+        "apex_precompute_resident": ([vp, vp, vp, C.c_int32, vp], C.c_int),
         "apex_gt_topk": ([vp, C.POINTER(QuerySpecC), C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_query_local_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int64, C.POINTER(Stats)], C.c_int),
         "apex_query_local_finish": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(Stats)], C.c_int),
@@ -511,6 +520,50 @@ class DeviceContext:
         _check(self.lib.apex_gt_topk(self._ctx, specs, results, C.byref(st)))
         del keep
         return self._unpack(results, bufs)[0], st.as_dict()
+
+    def encode_hierarchy(self, shapes: list[list[int]], params: np.ndarray, token_bytes: np.ndarray,
+                         token_off: np.ndarray, salt: bytes, p: int, scale: float, member_ids: np.ndarray,
+                         rg_offsets: np.ndarray, rg_parent: np.ndarray, rx_offsets: np.ndarray, d: int, d_u: int,
+                         want=("u", "h_s", "h_r", "h_t", "features")) -> dict:
+        """K8 (apex_encode_hierarchy); returns the requested host copies.  The
+        pair matrix u stays resident for precompute_resident."""
+        nets = (MlpShapeC * 7)()
+        for k, dims in enumerate(shapes):
+            nets[k].n_layers = len(dims) - 1
+            for i, x in enumerate(dims):
+                nets[k].dims[i] = int(x)
+        params = np.ascontiguousarray(params, dtype=np.float64)
+        tb = np.ascontiguousarray(token_bytes, dtype=np.uint8)
+        to = np.ascontiguousarray(token_off, dtype=np.int64)
+        mem = np.ascontiguousarray(member_ids, dtype=np.int64)
+        rgo = np.ascontiguousarray(rg_offsets, dtype=np.int64)
+        par = np.ascontiguousarray(rg_parent, dtype=np.int32)
+        rxo = np.ascontiguousarray(rx_offsets, dtype=np.int64)
+        sb = np.frombuffer(salt, dtype=np.uint8).copy()
+        n_syn, n_pairs, n_rg, n_rx = len(to) - 1, len(mem), len(rgo) - 1, len(rxo) - 1
+        d_s, d_r, d_t = shapes[0][-1], shapes[2][-1], shapes[4][-1]
+        out = {"u": np.empty((n_pairs, d)) if "u" in want else None,
+               "h_s": np.empty((n_syn, d_s)) if "h_s" in want else None,
+               "h_r": np.empty((n_rg, d_r)) if "h_r" in want else None,
+               "h_t": np.empty((n_rx, d_t)) if "h_t" in want else None,
+               "features": np.empty((n_syn, p)) if "features" in want else None}
+        ptr = lambda a: _ptr(a) if a is not None else None  # noqa: E731
+        self._u_pairs = n_pairs
+        _check(self.lib.apex_encode_hierarchy(self._ctx, nets, _ptr(params), len(params), _ptr(tb), _ptr(to), n_syn,
+                                              _ptr(sb), len(sb), int(p), float(scale), _ptr(mem), n_pairs, _ptr(rgo),
+                                              n_rg, _ptr(par), _ptr(rxo), n_rx, int(d), int(d_u), ptr(out["u"]),
+                                              ptr(out["h_s"]), ptr(out["h_r"]), ptr(out["h_t"]), ptr(out["features"])))
+        return {k: v for k, v in out.items() if v is not None}
+
+    def precompute_resident(self, head_w: np.ndarray, head_b: np.ndarray, want_values: bool = True):
+        """K1 from the resident K8 pair matrix (apex_precompute_resident); the
+        table becomes resident.  Returns the host copy of the table if asked."""
+        w = np.ascontiguousarray(head_w, dtype=np.float64)
+        b = np.ascontiguousarray(head_b, dtype=np.float64)
+        out = np.empty((w.shape[0], self._u_pairs), dtype=np.float32) if want_values else None
+        _check(self.lib.apex_precompute_resident(self._ctx, _ptr(w), _ptr(b), w.shape[0],
+                                                 _ptr(out) if out is not None else None))
+        return out
 
     def debug_thresholds(self, p: np.ndarray, b: np.ndarray, beta: np.ndarray):
         p = np.ascontiguousarray(p, dtype=np.float64)

@@ -30,6 +30,7 @@
 
 #include "kernels.cuh"
 #include "gt.cuh"
+#include "k8.cuh"
 
 using namespace apexb200;
 
@@ -271,6 +272,9 @@ struct apex_ctx {
   // ground-truth oracle (apex_gt_load): members, latents, task parameters
   DBuf d_gt_members, d_gt_latent, d_gt_tasks, d_gt_hist, d_gt_buf, d_gt_misc;
   std::vector<GtTask> gt_tasks;
+  DBuf d_u_res;                          // K8 output: the pair-row matrix u, resident for K1
+  int64_t u_res_pairs = 0;
+  int u_res_d = 0;
   int64_t gt_synthons = 0;
   bool gt_loaded = false;
   bool k1_timed = false;             // mev brackets the last K1 launch (apex_precompute_time)
@@ -1584,7 +1588,8 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->h_tau0.release();
   for (auto& ev : c->ev) cudaEventDestroy(ev);
   for (auto& ev : c->mev) cudaEventDestroy(ev);
-  for (DBuf* b : {&c->d_gt_members, &c->d_gt_latent, &c->d_gt_tasks, &c->d_gt_hist, &c->d_gt_buf, &c->d_gt_misc})
+  for (DBuf* b : {&c->d_gt_members, &c->d_gt_latent, &c->d_gt_tasks, &c->d_gt_hist, &c->d_gt_buf, &c->d_gt_misc,
+                  &c->d_u_res})
     b->release();
   {
     auto& w = c->mws;
@@ -2357,6 +2362,165 @@ int apex_gt_topk(apex_ctx* c, const apex_query_spec* q, apex_result* res, apex_s
     stats->kernel_launches = launches + mst.kernel_launches;
     stats->candidates = (int64_t)count;
   }
+  return APEX_OK;
+}
+
+// ===========================================================================
+// K8: the factorizer's hierarchy encoding on the device (k8.cuh)
+// ===========================================================================
+
+int apex_encode_hierarchy(apex_ctx* c, const apex_mlp_shape* nets, const double* params, int64_t n_params,
+                          const uint8_t* token_bytes, const int64_t* token_off, int64_t n_syn, const uint8_t* salt,
+                          int32_t salt_len, int32_t p, double feature_scale, const int64_t* member_ids, int64_t n_pairs,
+                          const int64_t* rg_offsets, int32_t n_rg, const int32_t* rg_parent, const int64_t* rx_offsets,
+                          int32_t n_rx, int32_t d, int32_t d_u, double* u_out, double* h_s_out, double* h_r_out,
+                          double* h_t_out, double* features_out) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, false));
+  if (!nets || !params || !token_bytes || !token_off || n_syn < 1 || !member_ids || n_pairs < 0 || !rg_offsets ||
+      n_rg < 1 || !rg_parent || !rx_offsets || n_rx < 1 || p < 1 || d < 1 || d_u < 1 || salt_len < 0 || salt_len > 100)
+    return set_err(APEX_EINVAL, "bad encode_hierarchy arguments");
+  // networks: synthon, rg_phi, rg_rho, rx_phi, rx_rho, value, key; flat params W0, b0, W1, b1, ... per net
+  int64_t need = 0;
+  std::vector<int64_t> net_off(8, 0);
+  for (int k = 0; k < 7; ++k) {
+    const apex_mlp_shape& S = nets[k];
+    if (S.n_layers < 1 || S.n_layers > 6) return set_err(APEX_EINVAL, "MLP layer count out of range");
+    for (int i = 0; i < S.n_layers; ++i) {
+      if (S.dims[i] < 1 || S.dims[i + 1] < 1) return set_err(APEX_EINVAL, "bad MLP dims");
+      need += (int64_t)S.dims[i] * S.dims[i + 1] + S.dims[i + 1];
+    }
+    net_off[k + 1] = need;
+  }
+  if (need != n_params) return set_err(APEX_EINVAL, "parameter count does not match the network shapes");
+  const int d_s = nets[0].dims[nets[0].n_layers], d_r = nets[2].dims[nets[2].n_layers], d_t = nets[4].dims[nets[4].n_layers];
+  if (nets[0].dims[0] != p || nets[1].dims[0] != d_s || nets[3].dims[0] != d_r || nets[5].dims[0] != d_s ||
+      nets[5].dims[nets[5].n_layers] != d_u || nets[6].dims[0] != d_r + d_t ||
+      nets[6].dims[nets[6].n_layers] != d * d_u || nets[1].dims[nets[1].n_layers] != nets[2].dims[0] ||
+      nets[3].dims[nets[3].n_layers] != nets[4].dims[0])
+    return set_err(APEX_EINVAL, "network shapes do not chain (synthon -> deep sets -> value / key -> u)");
+  if (rg_offsets[n_rg] != n_pairs || rx_offsets[n_rx] != n_rg) return set_err(APEX_EINVAL, "bad hierarchy offsets");
+  for (int64_t i = 0; i < n_pairs; ++i)
+    if (member_ids[i] < 0 || member_ids[i] >= n_syn) return set_err(APEX_EINVAL, "member id out of range");
+  cudaStream_t st = c->stream;
+  DBuf dp, dtok, dtoff, dsalt, dmem, drg, dpar, drx, feat, hs, hr, ht, v, kin, kf, t1, t2;
+  auto up = [&](DBuf& b, const void* src, size_t bytes) -> int {
+    APEX_TRY(b.ensure(std::max<size_t>(bytes, 8)));
+    if (bytes) APEX_CU(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st));
+    return APEX_OK;
+  };
+  APEX_TRY(up(dp, params, (size_t)n_params * 8));
+  APEX_TRY(up(dtok, token_bytes, (size_t)token_off[n_syn]));
+  APEX_TRY(up(dtoff, token_off, (size_t)(n_syn + 1) * 8));
+  APEX_TRY(up(dsalt, salt, (size_t)salt_len));
+  APEX_TRY(up(dmem, member_ids, (size_t)n_pairs * 8));
+  APEX_TRY(up(drg, rg_offsets, (size_t)(n_rg + 1) * 8));
+  APEX_TRY(up(dpar, rg_parent, (size_t)n_rg * 4));
+  APEX_TRY(up(drx, rx_offsets, (size_t)(n_rx + 1) * 8));
+  APEX_TRY(feat.ensure((size_t)n_syn * p * 8));
+  k8_features_kernel<<<(unsigned)((n_syn + 127) / 128), 128, 0, st>>>(dtok.as<unsigned char>(), dtoff.as<long long>(), n_syn,
+                                                                     dsalt.as<unsigned char>(), salt_len, p, feature_scale,
+                                                                     feat.as<double>());
+  APEX_CU(cudaGetLastError());
+  // one MLP (tanh between layers, none after the last) over M rows of X
+  auto mlp = [&](int k, const double* X, int ldx, const long long* gather, int64_t M, DBuf& out) -> int {
+    const apex_mlp_shape& S = nets[k];
+    const double* w = dp.as<double>() + net_off[k];
+    const double* x = X;
+    int ld = ldx;
+    const long long* gth = gather;
+    for (int i = 0; i < S.n_layers; ++i) {
+      const int K = S.dims[i], N = S.dims[i + 1];
+      const bool last = i == S.n_layers - 1;
+      DBuf& dst = last ? out : ((i & 1) ? t2 : t1);
+      APEX_TRY(dst.ensure((size_t)std::max<int64_t>(M, 1) * N * 8));
+      if (M > 0) {
+        dim3 grid((unsigned)((N + kGemmTile - 1) / kGemmTile), (unsigned)((M + kGemmTile - 1) / kGemmTile));
+        k8_gemm_kernel<<<grid, 256, 0, st>>>(x, ld, gth, M, K, w, w + (int64_t)K * N, N, last ? 0 : 1, dst.as<double>(), N);
+        APEX_CU(cudaGetLastError());
+      }
+      w += (int64_t)K * N + N;
+      x = dst.as<double>();
+      ld = N;
+      gth = nullptr;
+    }
+    return APEX_OK;
+  };
+  // h_s = synthon MLP(features)
+  APEX_TRY(mlp(0, feat.as<double>(), p, nullptr, n_syn, hs));
+  // h_r = DeepSet(h_s[member_ids], rg_offsets); h_t = DeepSet(h_r, rx_offsets)
+  DBuf phi_r, pool_r, phi_t, pool_t;
+  APEX_TRY(mlp(1, hs.as<double>(), d_s, dmem.as<long long>(), n_pairs, phi_r));
+  const int dphr = nets[1].dims[nets[1].n_layers], dpht = nets[3].dims[nets[3].n_layers];
+  APEX_TRY(pool_r.ensure((size_t)n_rg * dphr * 8));
+  k8_segment_mean_kernel<<<n_rg, 64, 0, st>>>(phi_r.as<double>(), dphr, drg.as<long long>(), pool_r.as<double>());
+  APEX_TRY(mlp(2, pool_r.as<double>(), dphr, nullptr, n_rg, hr));
+  APEX_TRY(mlp(3, hr.as<double>(), d_r, nullptr, n_rg, phi_t));
+  APEX_TRY(pool_t.ensure((size_t)n_rx * dpht * 8));
+  k8_segment_mean_kernel<<<n_rx, 64, 0, st>>>(phi_t.as<double>(), dpht, drx.as<long long>(), pool_t.as<double>());
+  APEX_TRY(mlp(4, pool_t.as<double>(), dpht, nullptr, n_rx, ht));
+  // v = value MLP(h_s); K = key MLP([h_r, h_t[parent]])
+  APEX_TRY(mlp(5, hs.as<double>(), d_s, nullptr, n_syn, v));
+  APEX_TRY(kin.ensure((size_t)n_rg * (d_r + d_t) * 8));
+  k8_key_input_kernel<<<n_rg, 128, 0, st>>>(hr.as<double>(), d_r, ht.as<double>(), d_t, dpar.as<int>(), n_rg, kin.as<double>());
+  APEX_TRY(mlp(6, kin.as<double>(), d_r + d_t, nullptr, n_rg, kf));
+  // u[p] = v[member[p]] @ K[j]^T
+  APEX_TRY(c->d_u_res.ensure((size_t)std::max<int64_t>(n_pairs, 1) * d * 8));
+  const size_t ksm = (size_t)d * d_u * 8;
+  if (ksm > 200 * 1024) return set_err(APEX_ELIMIT, "key matrix too large for shared memory");
+  APEX_CU(cudaFuncSetAttribute((const void*)k8_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm));
+  k8_pairs_kernel<<<dim3(n_rg, 8), 256, ksm, st>>>(v.as<double>(), d_u, kf.as<double>(), d, drg.as<long long>(),
+                                                   dmem.as<long long>(), c->d_u_res.as<double>());
+  APEX_CU(cudaGetLastError());
+  c->u_res_pairs = n_pairs;
+  c->u_res_d = d;
+  auto down = [&](double* dst, const DBuf& b, size_t bytes) -> int {
+    if (dst && bytes) APEX_CU(cudaMemcpyAsync(dst, b.p, bytes, cudaMemcpyDeviceToHost, st));
+    return APEX_OK;
+  };
+  APEX_TRY(down(u_out, c->d_u_res, (size_t)n_pairs * d * 8));
+  APEX_TRY(down(h_s_out, hs, (size_t)n_syn * d_s * 8));
+  APEX_TRY(down(h_r_out, hr, (size_t)n_rg * d_r * 8));
+  APEX_TRY(down(h_t_out, ht, (size_t)n_rx * d_t * 8));
+  APEX_TRY(down(features_out, feat, (size_t)n_syn * p * 8));
+  APEX_CU(cudaStreamSynchronize(st));
+  for (DBuf* b : {&dp, &dtok, &dtoff, &dsalt, &dmem, &drg, &dpar, &drx, &feat, &hs, &hr, &ht, &v, &kin, &kf, &t1, &t2,
+                  &phi_r, &pool_r, &phi_t, &pool_t})
+    b->release();
+  return APEX_OK;
+}
+
+// K1 from the resident K8 output (no host copy of u): the table becomes resident.
+int apex_precompute_resident(apex_ctx* c, const double* head_w, const double* head_b, int32_t n_tasks, float* values_out) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, false));
+  if (!c->u_res_pairs || !head_w || !head_b || n_tasks < 1) return set_err(APEX_ESTATE, "no resident pair matrix (run apex_encode_hierarchy)");
+  const int64_t n_pairs = c->u_res_pairs;
+  const int d = c->u_res_d;
+  for (int t = 0; t < n_tasks; ++t)
+    if (!std::isfinite(head_b[t])) return set_err(APEX_EINVAL, "non-finite head bias");
+  DBuf dw;
+  APEX_TRY(dw.ensure((size_t)n_tasks * d * sizeof(double)));
+  APEX_TRY(c->d_values.ensure(std::max<size_t>(1, (size_t)n_tasks * n_pairs) * sizeof(float)));
+  APEX_TRY(c->d_biases.ensure(n_tasks * sizeof(double)));
+  APEX_CU(cudaMemcpyAsync(dw.p, head_w, (size_t)n_tasks * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  APEX_CU(cudaMemcpyAsync(c->d_biases.p, head_b, n_tasks * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const bool host_heads = n_tasks == 11 && d == 64 && c->opt_pre_rows == 2;
+  int rc = apex_precompute_device(c, c->d_u_res.as<double>(), n_pairs, d, host_heads ? head_w : dw.as<double>(), n_tasks,
+                                  c->d_values.as<float>());
+  if (rc != APEX_OK) return rc;
+  c->h_values.resize((size_t)n_tasks * n_pairs);
+  if (n_pairs > 0)
+    APEX_CU(cudaMemcpyAsync(c->h_values.data(), c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float),
+                            cudaMemcpyDeviceToHost, c->stream));
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  if (values_out && n_pairs > 0) std::memcpy(values_out, c->h_values.data(), (size_t)n_tasks * n_pairs * sizeof(float));
+  dw.release();
+  c->biases.assign(head_b, head_b + n_tasks);
+  c->n_tasks = n_tasks;
+  c->n_pairs = n_pairs;
+  c->table_loaded = true;
+  c->corners_ok = false;
   return APEX_OK;
 }
 
