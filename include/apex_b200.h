@@ -276,6 +276,16 @@ int apex_gt_load(apex_ctx* ctx, const int64_t* member_ids, int64_t n_pairs, cons
  * products; objective / constraint_values are the oracle's values. */
 int apex_gt_topk(apex_ctx* ctx, const apex_query_spec* query, apex_result* result, apex_stats* stats);
 
+/* BatchTrace accounting of the chain-of-batches variant (engine.py:338-391,
+ * SURVEY §8(f) row 3): for batches [start, batch_end[0]), [batch_end[0],
+ * batch_end[1]), ... (make_batches, engine.py:316-335) the number of entries
+ * of each batch's selection — the k best of (carry ∪ batch) under the full
+ * order (violation desc, signed objective desc, global index asc), infeasible
+ * products included — that came from the batch (new_out) or the carry
+ * (carried_out).  Exact, on the device. */
+int apex_batch_trace(apex_ctx* ctx, const apex_query_spec* query, const uint64_t* batch_end, int32_t n_batches,
+                     int64_t* new_out, int64_t* carried_out);
+
 /* K8: the factorizer's hierarchy encoding on the device (
  * factorizer.encode_hierarchy, factorizer.py:157-171, 218-233): synthon
  * feature hashing (BLAKE2b-64 of "<salt>:<ngram>" for the 1/2/3-grams of each

@@ -29,7 +29,7 @@ EXPORTED = (
     "apex_set_option", "apex_get_device_info",
     "apex_debug_thresholds", "apex_debug_trace",
     "apex_query_local_async", "apex_query_local_finish", "apex_precompute_time", "apex_gt_load", "apex_gt_topk",
-    "apex_encode_hierarchy", "apex_precompute_resident",
+    "apex_encode_hierarchy", "apex_precompute_resident", "apex_batch_trace",
     "apex_multi_create", "apex_multi_destroy", "apex_multi_load_library", "apex_multi_load_table",
     "apex_multi_load_cache", "apex_multi_set_option", "apex_multi_query", "apex_multi_info",
 )
@@ -169,6 +169,7 @@ def load_library(path: Path | None = None):
                                    C.c_int64, vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp,
                                    vp], C.c_int),
         "apex_precompute_resident": ([vp, vp, vp, C.c_int32, vp], C.c_int),
+        "apex_batch_trace": ([vp, C.POINTER(QuerySpecC), vp, C.c_int32, vp, vp], C.c_int),
         "apex_gt_topk": ([vp, C.POINTER(QuerySpecC), C.POINTER(ResultC), C.POINTER(Stats)], C.c_int),
         "apex_query_local_async": ([vp, C.POINTER(QuerySpecC), C.c_int32, vp, C.c_int64, C.POINTER(Stats)], C.c_int),
         "apex_query_local_finish": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(Stats)], C.c_int),
@@ -499,6 +500,17 @@ class DeviceContext:
             "reaction": b["reaction"][:n], "digits": b["digits"][:n], "n": n, "discarded": res.discarded,
             "scanned": res.scanned,
         }, st.as_dict()
+
+    def batch_trace(self, query: dict, batch_end: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+        """BatchTrace new / carried counts of the chain of batches ending at
+        batch_end (apex_batch_trace)."""
+        specs, keep = self._specs([query])
+        ends = np.ascontiguousarray(batch_end, dtype=np.uint64)
+        new = np.zeros(len(ends), dtype=np.int64)
+        carried = np.zeros(len(ends), dtype=np.int64)
+        _check(self.lib.apex_batch_trace(self._ctx, specs, _ptr(ends), len(ends), _ptr(new), _ptr(carried)))
+        del keep
+        return new, carried
 
     def gt_load(self, member_ids: np.ndarray, latents: np.ndarray, tasks: list[dict]) -> None:
         """Ground-truth oracle tables (apex_gt_load): member_ids [n_pairs],

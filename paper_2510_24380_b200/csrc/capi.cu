@@ -31,6 +31,7 @@
 #include "kernels.cuh"
 #include "gt.cuh"
 #include "k8.cuh"
+#include "trace.cuh"
 
 using namespace apexb200;
 
@@ -2362,6 +2363,121 @@ int apex_gt_topk(apex_ctx* c, const apex_query_spec* q, apex_result* res, apex_s
     stats->kernel_launches = launches + mst.kernel_launches;
     stats->candidates = (int64_t)count;
   }
+  return APEX_OK;
+}
+
+// ===========================================================================
+// BatchTrace accounting of the chain-of-batches variant (trace.cuh)
+// ===========================================================================
+
+int apex_batch_trace(apex_ctx* c, const apex_query_spec* q, const uint64_t* batch_end, int32_t n_batches,
+                     int64_t* new_out, int64_t* carried_out) {
+  APEX_LOCK(c);
+  APEX_TRY(check_ctx(c, true));
+  APEX_TRY(validate_queries(c, q, 1));
+  if (n_batches < 0 || (n_batches > 0 && (!batch_end || !new_out || !carried_out)))
+    return set_err(APEX_EINVAL, "bad batch-trace arguments");
+  if (q->n_constraints > kMaxCons) return set_err(APEX_ELIMIT, "more than 32 constraints in a query");
+  for (int m = 0; m < q->n_constraints; ++m)
+    if (q->constraints[m].task < 0 || q->constraints[m].task >= c->n_tasks) return set_err(APEX_ETASK, "unknown task index");
+  uint64_t prev = q->start;
+  for (int i = 0; i < n_batches; ++i) {
+    if (batch_end[i] < prev || batch_end[i] > q->end) return set_err(APEX_EINVAL, "batch ends must ascend inside the range");
+    prev = batch_end[i];
+  }
+  const int64_t k = q->k;
+  if (k == 0) {
+    for (int i = 0; i < n_batches; ++i) new_out[i] = carried_out[i] = 0;
+    return APEX_OK;
+  }
+  const uint64_t kSub = 1ull << 20;  // products evaluated per launch
+  const uint64_t cap = kSub + (uint64_t)k;
+  uint64_t P_max = 1;
+  while (P_max < cap) P_max <<= 1;
+  DBuf buf, misc;
+  APEX_TRY(buf.ensure((size_t)P_max * sizeof(TEntry)));
+  APEX_TRY(misc.ensure(64));
+  unsigned long long* d_count = misc.as<unsigned long long>();
+  unsigned long long* d_orig = d_count + 1;
+  unsigned* d_work = reinterpret_cast<unsigned*>(d_count + 2);
+  cudaStream_t s = c->stream;
+  TraceEval E;
+  std::memset(&E, 0, sizeof(E));
+  E.rx = c->d_rx.as<DevReaction>();
+  E.values = c->d_values.as<float>();
+  E.n_pairs = c->n_pairs;
+  E.biases = c->d_biases.as<double>();
+  E.obj = q->objective_task;
+  E.maximize = q->maximize ? 1 : 0;
+  E.n_cons = q->n_constraints;
+  for (int m = 0; m < q->n_constraints; ++m) {
+    E.cons_task[m] = q->constraints[m].task;
+    E.cons_lo[m] = q->constraints[m].lower;
+    E.cons_hi[m] = q->constraints[m].upper;
+  }
+  E.out = buf.as<TEntry>();
+  E.count = d_count;
+  E.cap = cap;
+  E.work = d_work;
+  int64_t max_last = 1;
+  for (const auto& R : c->rx) max_last = std::max<int64_t>(max_last, R.size[R.c - 1]);
+  const size_t small_smem = 4096 * sizeof(TEntry);
+  APEX_CU(cudaFuncSetAttribute((const void*)trace_sort_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)small_smem));
+  uint64_t carry = 0;
+  prev = q->start;
+  for (int i = 0; i < n_batches; ++i) {
+    const uint64_t a = prev, b = batch_end[i];
+    prev = b;
+    if (carry) {
+      trace_origin_kernel<<<(unsigned)((carry + 255) / 256), 256, 0, s>>>(buf.as<TEntry>(), (unsigned)carry, 0, nullptr);
+    }
+    for (uint64_t a2 = a; a2 < b; a2 += kSub) {
+      const uint64_t b2 = std::min(b, a2 + kSub);
+      Plan* plan = nullptr;
+      APEX_TRY(build_plan(c, a2, b2, 32, 1, plan, max_last));
+      E.tiles = plan->d_tiles.as<Tile>();
+      E.n_tiles = (unsigned)plan->tiles.size();
+      E.a = a2;
+      E.b = b2;
+      E.worst = carry == (uint64_t)k ? buf.as<TEntry>() + (k - 1) : nullptr;
+      const unsigned long long c0 = carry;
+      APEX_CU(cudaMemcpyAsync(d_count, &c0, 8, cudaMemcpyHostToDevice, s));
+      APEX_CU(cudaMemsetAsync(d_work, 0, sizeof(unsigned), s));
+      trace_eval_kernel<<<c->sm_count * 8, 256, 0, s>>>(E);
+      APEX_CU(cudaGetLastError());
+      unsigned long long total = 0;
+      APEX_CU(cudaMemcpyAsync(&total, d_count, 8, cudaMemcpyDeviceToHost, s));
+      APEX_CU(cudaStreamSynchronize(s));
+      if (total > cap) return set_err(APEX_ELIMIT, "batch-trace candidate buffer overflow");
+      if (total > carry) {  // new candidates: order carry + candidates best-first
+        uint64_t P = 1;
+        while (P < total) P <<= 1;
+        if (P <= 4096) {
+          trace_sort_small_kernel<<<1, 1024, small_smem, s>>>(buf.as<TEntry>(), (unsigned)total, (unsigned)P);
+        } else {
+          trace_pad_kernel<<<(unsigned)((P - total + 255) / 256), 256, 0, s>>>(buf.as<TEntry>(), (unsigned)total, (unsigned)P);
+          for (uint64_t size = 2; size <= P; size <<= 1)
+            for (uint64_t stride = size >> 1; stride > 0; stride >>= 1)
+              trace_sort_step_kernel<<<(unsigned)((P / 2 + 255) / 256), 256, 0, s>>>(buf.as<TEntry>(), (unsigned)P,
+                                                                                     (unsigned)size, (unsigned)stride);
+        }
+        APEX_CU(cudaGetLastError());
+      }
+      carry = std::min<uint64_t>((uint64_t)k, total);
+    }
+    unsigned long long n_new = 0;
+    if (carry) {
+      APEX_CU(cudaMemsetAsync(d_orig, 0, 8, s));
+      trace_origin_kernel<<<(unsigned)((carry + 255) / 256), 256, 0, s>>>(buf.as<TEntry>(), (unsigned)carry, 1, d_orig);
+      APEX_CU(cudaMemcpyAsync(&n_new, d_orig, 8, cudaMemcpyDeviceToHost, s));
+      APEX_CU(cudaStreamSynchronize(s));
+    }
+    new_out[i] = (int64_t)n_new;
+    carried_out[i] = (int64_t)carry - (int64_t)n_new;
+  }
+  buf.release();
+  misc.release();
   return APEX_OK;
 }
 

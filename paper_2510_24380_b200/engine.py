@@ -183,6 +183,7 @@ class _Bound:
             g_offsets.append(g)
             g += math.prod(s)
         self.total = g
+        self.index_space = (sizes, pair_offsets, g_offsets, int(np.asarray(table.values).shape[1]))
         values = np.asarray(table.values)
         try:
             self.ctx.load_library(sizes, pair_offsets, g_offsets, values.shape[1])
@@ -393,22 +394,84 @@ def search_topk_stream(library, table, query, index_range=None, device=None):
     return _run([query], library, table, start, end, device)[0]
 
 
+@dataclass
+class BatchTrace:
+    batch_sizes: list
+    new_elements: list
+    carried_elements: list
+
+
+def batch_ends(library, chunk_size: int, start: int, end: int) -> list:
+    """Exclusive end of every batch of ``make_batches`` (engine.py:316-335):
+    whole (reaction, first-digit) slabs of ``iter_blocks`` (engine.py:169-189)
+    grouped while the running size stays <= chunk_size (a larger slab forms
+    its own batch).  Batches are contiguous ranges of the index space."""
+    ends, cur, cur_end = [], 0, None
+    off = 0
+    for rx in library.reactions:
+        sizes = [len(rg.synthon_ids) for rg in rx.rgroups]
+        size = math.prod(sizes)
+        if off + size <= start or off >= end:
+            off += size
+            continue
+        inner = size // sizes[0]
+        j0 = max(0, (start - off) // inner) if start > off else 0
+        j1 = min(sizes[0], -(-(end - off) // inner))
+        for j in range(j0, j1):
+            g0 = off + j * inner
+            lo, hi = max(start, g0), min(end, g0 + inner)
+            if lo >= hi:
+                continue
+            n = hi - lo
+            if cur and cur + n > chunk_size:
+                ends.append(cur_end)
+                cur = 0
+            cur += n
+            cur_end = hi
+        off += size
+    if cur:
+        ends.append(cur_end)
+    return ends
+
+
 def search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None, device=None):
     """Chain-of-batches variant (engine.py:345-398).  Results are identical to
     the stream variant by contract (test_engine.py:138-145), so both run the
     same device pipeline; ``chunk_size`` is validated as the reference does.
-    ``trace`` (BatchTrace accounting of the CPU chain, incl. infeasible rows)
-    has no device counterpart and is rejected."""
+    ``trace`` receives the chain's BatchTrace accounting (engine.py:387-391),
+    computed exactly on the device (apex_batch_trace: per batch, the k best of
+    carry and batch under the full order, infeasible products included)."""
     _fingerprint_ok(library, table)
     _task_index(table, query.objective)
     for con in query.constraints:
         _task_index(table, con.task)
     if chunk_size < 1:
         raise _error("chunk size must be >= 1")
-    if trace is not None:
-        raise _error("BatchTrace accounting is not supported by the B200 path (results are identical without it)")
     start, end = _validate(library, table, query, index_range)
-    return _run([query], library, table, start, end, device)[0]
+    out = _run([query], library, table, start, end, device)[0]
+    if trace is not None and query.k > 0 and end > start:
+        ends = batch_ends(library, int(chunk_size), start, end)
+        b = bind(library, table, device)
+        ctx = b.ctx if isinstance(b.ctx, _native.DeviceContext) else _native.DeviceContext(default_device_one(device))
+        if ctx is not b.ctx:
+            ctx.load_library(*b.index_space)
+            ctx.load_table(np.asarray(table.values), np.asarray(table.biases, dtype=np.float64))
+        try:
+            new, carried = ctx.batch_trace(_native_query(table, query, start, end), np.asarray(ends, dtype=np.uint64))
+        except _native.NativeError as exc:
+            raise _error(str(exc)) from None
+        prev = start
+        for e, n, c in zip(ends, new.tolist(), carried.tolist()):
+            trace.batch_sizes.append(e - prev)
+            trace.new_elements.append(int(n))
+            trace.carried_elements.append(int(c))
+            prev = e
+    return out
+
+
+def default_device_one(device) -> int:
+    dev = default_device() if device is None else device
+    return int(dev[0] if isinstance(dev, (list, tuple)) else dev)
 
 
 def search_topk_many(library, table, queries, index_range=None, device=None):
