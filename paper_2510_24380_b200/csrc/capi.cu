@@ -32,6 +32,7 @@
 #include "gt.cuh"
 #include "k8.cuh"
 #include "trace.cuh"
+#include "bind.cuh"
 
 using namespace apexb200;
 
@@ -201,7 +202,6 @@ struct apex_ctx {
   bool lib_loaded = false;
   // table
   DBuf d_values, d_biases;
-  std::vector<float> h_values;           // host copy of the table (corner lists)
   std::vector<double> biases;
   // corner seed lists (built lazily once library + table are resident)
   DBuf d_lists, d_slot_off, d_m, d_coff;
@@ -489,9 +489,13 @@ int scan_occupancy(apex_ctx* c, ScanFn fn, size_t smem, int* occ) {
   return APEX_OK;
 }
 
-// Corner seed lists: for every task, direction and (reaction, R-group) the
-// digits of the best-m synthons (largest values for maximize, smallest for
-// minimize), m chosen so a reaction's corner has ~4096 products.
+// Binding state built once per (library, table), on the device (bind.cuh):
+// every R-group column of every task sorted by (value, column); from those,
+// per task the sorted last-R-group columns with their quantile tables (the
+// sorted-column kernel) and the corner seed lists — for every task, direction
+// and (reaction, R-group) the digits of the best-m synthons (largest first for
+// maximize, smallest first for minimize), m chosen so a reaction's corner has
+// ~4096 products.  Only the list metadata is computed on the host.
 int build_corners(apex_ctx* c) {
   const int n_rx = (int)c->rx.size();
   std::vector<int32_t> slot_off((size_t)n_rx * kMaxRg, 0), m((size_t)n_rx * kMaxRg, 0);
@@ -511,68 +515,73 @@ int build_corners(apex_ctx* c) {
     coff[t + 1] = coff[t] + prod;
   }
   if (slots > INT32_MAX) return set_err(APEX_ELIMIT, "corner lists too large");
-  std::vector<int32_t> lists((size_t)c->n_tasks * 2 * slots);
-  // sorted last-R-group columns (sorted-column admission kernel): per task, at
-  // every reaction's pcol_off, values ascending with their column index
-  const size_t pc = (size_t)std::max<int64_t>(c->pcols, 4);
-  std::vector<float> sx((size_t)c->n_tasks * pc, 0.0f);
-  std::vector<uint32_t> scol((size_t)c->n_tasks * pc, 0u);
-  std::vector<float> quant((size_t)c->n_tasks * n_rx * (kQuant + 1), 0.0f);
-  auto work = [&](int task) {
-    std::vector<int32_t> idx;
+  // segments: (task, R-group) for every R-group of every reaction
+  std::vector<BindSeg> segs;
+  int64_t scratch = 0;
+  for (int task = 0; task < c->n_tasks; ++task)
     for (int t = 0; t < n_rx; ++t) {
       const DevReaction& R = c->rx[t];
-      const float* v = c->h_values.data() + (size_t)task * c->n_pairs + R.pair_off[R.c - 1];
-      const int64_t n = R.size[R.c - 1];
-      idx.resize(n);
-      std::iota(idx.begin(), idx.end(), 0);
-      std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b] || (v[a] == v[b] && a < b); });
-      float* ox = sx.data() + (size_t)task * pc + R.pcol_off;
-      uint32_t* oc = scol.data() + (size_t)task * pc + R.pcol_off;
-      for (int64_t i = 0; i < n; ++i) {
-        ox[i] = v[idx[i]];
-        oc[i] = (uint32_t)idx[i];
-      }
-      float* oq = quant.data() + ((size_t)task * n_rx + t) * (kQuant + 1);
-      for (int qq = 0; qq <= kQuant; ++qq) oq[qq] = n > 0 ? ox[std::min<int64_t>(n - 1, qq * n / kQuant)] : 0.0f;
-    }
-    for (int dir = 0; dir < 2; ++dir) {
-      int32_t* out = lists.data() + ((size_t)task * 2 + dir) * slots;
-      for (int t = 0; t < n_rx; ++t) {
-        const DevReaction& R = c->rx[t];
-        for (int j = 0; j < R.c; ++j) {
-          const float* v = c->h_values.data() + (size_t)task * c->n_pairs + R.pair_off[j];
-          const int64_t n = R.size[j];
-          const int mj = m[(size_t)t * kMaxRg + j];
-          idx.resize(n);
-          std::iota(idx.begin(), idx.end(), 0);
-          // best-first: a prefix of the list is the best-m' synthons for any m' <= m
-          if (dir == 0)
-            std::partial_sort(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] > v[b]; });
-          else
-            std::partial_sort(idx.begin(), idx.begin() + mj, idx.end(), [&](int32_t a, int32_t b) { return v[a] < v[b]; });
-          std::copy(idx.begin(), idx.begin() + mj, out + slot_off[(size_t)t * kMaxRg + j]);
+      for (int j = 0; j < R.c; ++j) {
+        BindSeg S;
+        S.pair = R.pair_off[j];
+        S.n = (int32_t)R.size[j];
+        S.task = task;
+        S.scratch = -1;
+        if (S.n > kBindSmem) {
+          int64_t P = 1;
+          while (P < S.n) P <<= 1;
+          S.scratch = scratch;
+          scratch += P;
         }
+        segs.push_back(S);
       }
     }
-  };
-  std::vector<std::thread> th;
-  for (int task = 0; task < c->n_tasks; ++task) th.emplace_back(work, task);
-  for (auto& x : th) x.join();
-  APEX_TRY(c->d_lists.ensure(std::max<size_t>(1, lists.size()) * sizeof(int32_t)));
+  cudaStream_t s = c->stream;
+  DBuf d_segs, d_keys, d_scratch;
+  APEX_TRY(d_segs.ensure(std::max<size_t>(1, segs.size()) * sizeof(BindSeg)));
+  APEX_TRY(d_keys.ensure(std::max<size_t>(1, (size_t)c->n_tasks * c->n_pairs) * sizeof(unsigned long long)));
+  APEX_TRY(d_scratch.ensure(std::max<int64_t>(1, scratch) * sizeof(unsigned long long)));
+  if (!segs.empty())
+    APEX_CU(cudaMemcpyAsync(d_segs.p, segs.data(), segs.size() * sizeof(BindSeg), cudaMemcpyHostToDevice, s));
+  const size_t pc = (size_t)std::max<int64_t>(c->pcols, 4);
+  APEX_TRY(c->d_lists.ensure(std::max<size_t>(1, (size_t)c->n_tasks * 2 * slots) * sizeof(int32_t)));
   APEX_TRY(c->d_slot_off.ensure(std::max<size_t>(1, slot_off.size()) * sizeof(int32_t)));
   APEX_TRY(c->d_m.ensure(std::max<size_t>(1, m.size()) * sizeof(int32_t)));
   APEX_TRY(c->d_coff.ensure(coff.size() * sizeof(unsigned long long)));
-  if (!lists.empty()) APEX_CU(cudaMemcpy(c->d_lists.p, lists.data(), lists.size() * 4, cudaMemcpyHostToDevice));
-  if (!slot_off.empty()) APEX_CU(cudaMemcpy(c->d_slot_off.p, slot_off.data(), slot_off.size() * 4, cudaMemcpyHostToDevice));
-  if (!m.empty()) APEX_CU(cudaMemcpy(c->d_m.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
-  APEX_CU(cudaMemcpy(c->d_coff.p, coff.data(), coff.size() * 8, cudaMemcpyHostToDevice));
-  APEX_TRY(c->d_sorted_x.ensure(sx.size() * sizeof(float)));
-  APEX_TRY(c->d_sorted_col.ensure(scol.size() * sizeof(uint32_t)));
-  APEX_CU(cudaMemcpy(c->d_sorted_x.p, sx.data(), sx.size() * sizeof(float), cudaMemcpyHostToDevice));
-  APEX_CU(cudaMemcpy(c->d_sorted_col.p, scol.data(), scol.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  APEX_TRY(c->d_quant.ensure(std::max<size_t>(1, quant.size()) * sizeof(float)));
-  if (!quant.empty()) APEX_CU(cudaMemcpy(c->d_quant.p, quant.data(), quant.size() * sizeof(float), cudaMemcpyHostToDevice));
+  APEX_TRY(c->d_sorted_x.ensure((size_t)c->n_tasks * pc * sizeof(float)));
+  APEX_TRY(c->d_sorted_col.ensure((size_t)c->n_tasks * pc * sizeof(uint32_t)));
+  APEX_TRY(c->d_quant.ensure(std::max<size_t>(1, (size_t)c->n_tasks * n_rx * (kQuant + 1)) * sizeof(float)));
+  APEX_CU(cudaMemsetAsync(c->d_sorted_x.p, 0, (size_t)c->n_tasks * pc * sizeof(float), s));
+  APEX_CU(cudaMemsetAsync(c->d_sorted_col.p, 0, (size_t)c->n_tasks * pc * sizeof(uint32_t), s));
+  if (!slot_off.empty())
+    APEX_CU(cudaMemcpyAsync(c->d_slot_off.p, slot_off.data(), slot_off.size() * 4, cudaMemcpyHostToDevice, s));
+  if (!m.empty()) APEX_CU(cudaMemcpyAsync(c->d_m.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice, s));
+  APEX_CU(cudaMemcpyAsync(c->d_coff.p, coff.data(), coff.size() * 8, cudaMemcpyHostToDevice, s));
+  if (!segs.empty()) {
+    bind_sort_kernel<<<(unsigned)segs.size(), 1024, 0, s>>>(d_segs.as<BindSeg>(), c->d_values.as<float>(), c->n_pairs,
+                                                            d_keys.as<unsigned long long>(),
+                                                            d_scratch.as<unsigned long long>());
+    APEX_CU(cudaGetLastError());
+    BindEmit E;
+    E.rx = c->d_rx.as<DevReaction>();
+    E.n_rx = n_rx;
+    E.n_pairs = c->n_pairs;
+    E.keys = d_keys.as<unsigned long long>();
+    E.sx = c->d_sorted_x.as<float>();
+    E.scol = c->d_sorted_col.as<uint32_t>();
+    E.pcols = (int64_t)pc;
+    E.quant = c->d_quant.as<float>();
+    E.lists = c->d_lists.as<int32_t>();
+    E.slot_off = c->d_slot_off.as<int32_t>();
+    E.m = c->d_m.as<int32_t>();
+    E.slots = slots;
+    bind_emit_kernel<<<dim3((unsigned)n_rx, (unsigned)c->n_tasks), 256, 0, s>>>(E);
+    APEX_CU(cudaGetLastError());
+  }
+  APEX_CU(cudaStreamSynchronize(s));
+  d_segs.release();
+  d_keys.release();
+  d_scratch.release();
   c->corner_slots = slots;
   c->corner_total = coff[n_rx];
   c->corners_ok = true;
@@ -1691,7 +1700,6 @@ int apex_load_table(apex_ctx* c, const float* values, const double* biases, int3
   if (n) APEX_CU(cudaMemcpy(c->d_values.p, values, n * sizeof(float), cudaMemcpyHostToDevice));
   APEX_CU(cudaMemcpy(c->d_biases.p, biases, n_tasks * sizeof(double), cudaMemcpyHostToDevice));
   c->biases.assign(biases, biases + n_tasks);
-  c->h_values.assign(values, values + n);
   c->n_tasks = n_tasks;
   c->n_pairs = n_pairs;
   c->table_loaded = true;
@@ -1836,9 +1844,6 @@ int apex_load_cache(apex_ctx* c, const double* u, int64_t n_pairs, int32_t d, co
   du.release();
   dw.release();
   c->biases.assign(head_b, head_b + n_tasks);
-  c->h_values.resize((size_t)n_tasks * n_pairs);
-  if (n_pairs > 0)
-    APEX_CU(cudaMemcpy(c->h_values.data(), c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float), cudaMemcpyDeviceToHost));
   c->n_tasks = n_tasks;
   c->n_pairs = n_pairs;
   c->table_loaded = true;
@@ -2625,12 +2630,10 @@ int apex_precompute_resident(apex_ctx* c, const double* head_w, const double* he
   int rc = apex_precompute_device(c, c->d_u_res.as<double>(), n_pairs, d, host_heads ? head_w : dw.as<double>(), n_tasks,
                                   c->d_values.as<float>());
   if (rc != APEX_OK) return rc;
-  c->h_values.resize((size_t)n_tasks * n_pairs);
-  if (n_pairs > 0)
-    APEX_CU(cudaMemcpyAsync(c->h_values.data(), c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float),
-                            cudaMemcpyDeviceToHost, c->stream));
+  if (values_out && n_pairs > 0)
+    APEX_CU(cudaMemcpyAsync(values_out, c->d_values.p, (size_t)n_tasks * n_pairs * sizeof(float), cudaMemcpyDeviceToHost,
+                            c->stream));
   APEX_CU(cudaStreamSynchronize(c->stream));
-  if (values_out && n_pairs > 0) std::memcpy(values_out, c->h_values.data(), (size_t)n_tasks * n_pairs * sizeof(float));
   dw.release();
   c->biases.assign(head_b, head_b + n_tasks);
   c->n_tasks = n_tasks;
