@@ -111,4 +111,16 @@ __global__ void bind_emit_kernel(const BindEmit E) {
   }
 }
 
+// pair-major copy of the table for the sorted-column kernel: packed16[p][t] =
+// values[t][p] (t < n_tasks <= 16), 0 in the padding
+__global__ void bind_pack16_kernel(const float* __restrict__ values, int64_t n_pairs, int n_tasks,
+                                   float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs * 16;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i >> 4;
+    const int t = (int)(i & 15);
+    out[i] = t < n_tasks ? __ldg(values + (int64_t)t * n_pairs + p) : 0.0f;
+  }
+}
+
 }  // namespace apexb200

@@ -210,6 +210,8 @@ struct apex_ctx {
   bool corners_ok = false;
   DBuf d_sorted_x, d_sorted_col;         // per task: each reaction's last R-group sorted ascending (value, column)
   DBuf d_quant;                          // per task, reaction: kQuant + 1 evenly spaced values of the sorted column
+  DBuf d_packed16;                       // [n_pairs][16] pair-major copy of the table (sorted-column kernel)
+  bool packed16_ok = false;
   int n_tasks = 0;
   int64_t n_pairs = 0;
   bool table_loaded = false;
@@ -256,6 +258,7 @@ struct apex_ctx {
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
+  int64_t opt_packed16 = 1;         // sorted-column kernel reads the pair-major table copy
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
   uint64_t opt_gen = 0;             // bumped by apex_set_option
@@ -577,6 +580,16 @@ int build_corners(apex_ctx* c) {
     E.slots = slots;
     bind_emit_kernel<<<dim3((unsigned)n_rx, (unsigned)c->n_tasks), 256, 0, s>>>(E);
     APEX_CU(cudaGetLastError());
+  }
+  if (c->n_tasks <= 16 && c->opt_packed16) {
+    APEX_TRY(c->d_packed16.ensure(std::max<size_t>(1, (size_t)c->n_pairs * 16) * sizeof(float)));
+    const int64_t tot = c->n_pairs * 16;
+    bind_pack16_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c->sm_count * 16)), 256,
+                         0, s>>>(c->d_values.as<float>(), c->n_pairs, c->n_tasks, c->d_packed16.as<float>());
+    APEX_CU(cudaGetLastError());
+    c->packed16_ok = true;
+  } else {
+    c->packed16_ok = false;
   }
   APEX_CU(cudaStreamSynchronize(s));
   d_segs.release();
@@ -944,10 +957,12 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
         // sorted-column admission: whole-row tiles, one launch per 64 queries
         const Plan* pr_ = B.plan_rows;
         const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
-        ScanFn fn = reinterpret_cast<ScanFn>(scan_sorted_kernel);
+        const bool p16 = c->packed16_ok && c->opt_packed16;
+        ScanFn fn = p16 ? reinterpret_cast<ScanFn>(scan_sorted_kernel<true>) : reinterpret_cast<ScanFn>(scan_sorted_kernel<false>);
         int occ = 0;
         APEX_TRY(scan_occupancy(c, fn, smem, &occ));
         SortedLaunch SL;
+        SL.packed16 = p16 ? c->d_packed16.as<float>() : nullptr;
         SL.sx = c->d_sorted_x.as<float>();
         SL.scol = c->d_sorted_col.as<uint32_t>();
         SL.pcols = std::max<int64_t>(c->pcols, 4);
@@ -966,7 +981,8 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           const int slot = wi++ % 64;
           La.work = c->d_work.as<unsigned>() + slot;
-          scan_sorted_kernel<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
+          if (p16) scan_sorted_kernel<true><<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
+          else scan_sorted_kernel<false><<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
           APEX_CU(cudaGetLastError());
           ++st.launches;
           ++st.scans;
@@ -1584,7 +1600,9 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_goff.release();
   c->d_values.release();
   c->d_biases.release();
-  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff, &c->d_sorted_x, &c->d_sorted_col, &c->d_quant}) b->release();
+  for (DBuf* b : {&c->d_lists, &c->d_slot_off, &c->d_m, &c->d_coff, &c->d_sorted_x, &c->d_sorted_col, &c->d_quant,
+                  &c->d_packed16})
+    b->release();
   c->d_queries.release();
   c->d_tau0.release();
   c->d_hists.release();
@@ -2100,6 +2118,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
     }
   }
   else if (n == "graph") c->opt_graph = v;
+  else if (n == "packed16") c->opt_packed16 = v;
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
   else if (n == "tiles_per_slot") c->opt_tiles_per_slot = std::max<int64_t>(1, v);
   else if (n == "mode") {

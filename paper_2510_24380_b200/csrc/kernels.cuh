@@ -1616,6 +1616,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_ADMIT_MINB) scan_admit_k
 // as in the streaming forms.  The candidate set is identical (feasible and
 // s >= tau, both exact), so nothing downstream changes.
 struct SortedLaunch {
+  const float* packed16;  // [n_pairs][16] pair-major copy of the table (n_tasks <= 16), or null
   const float* sx;        // [task][pcols]: each reaction's last R-group values ascending, at pcol_off
   const uint32_t* scol;   // same layout: column index of each sorted value
   int64_t pcols;
@@ -1781,6 +1782,11 @@ __device__ __forceinline__ void exact_range(const float* __restrict__ xs, int n,
 #ifndef APEX_SORTED_MINB
 #define APEX_SORTED_MINB 4
 #endif
+// P16: contributions read from the pair-major copy packed16[pair][16] (one
+// 64-byte line per pair holds every task: a row's prefix sums and a pair's
+// test values for all tests come from one line each instead of one line per
+// task), else from the task-major table values[task][pair].
+template <bool P16>
 __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
   extern __shared__ __align__(16) float sm_s[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
@@ -1789,7 +1795,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: signed-value thresholds of every test
   WorkCursor wc;
   const float* __restrict__ values = L.values;
+  const float* __restrict__ p16 = S.packed16;
   const int64_t n_pairs = L.n_pairs;
+  auto ld = [&](int task, int64_t pair) -> float {
+    return P16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
+  };
 
   unsigned qi, t;
   bool have = next_item(L, wc, live, lane, qi, t);
@@ -1829,11 +1839,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     // small are the constraint thresholds derived to find a more selective test
     double p_obj;
     {
-      const float* v = values + (int64_t)Q.test_task[0] * n_pairs;
-      double p = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+      const int task0 = Q.test_task[0];
+      double p = c > 1 ? (double)ld(task0, pr[0]) : 0.0;
 #pragma unroll
       for (int j = 1; j < kMaxRg - 1; ++j)
-        if (j < c - 1) p = __dadd_rn(p, (double)__ldg(v + pr[j]));
+        if (j < c - 1) p = __dadd_rn(p, (double)ld(task0, pr[j]));
       p_obj = p;
     }
     float th0 = __int_as_float(0x7f800000);
@@ -1871,13 +1881,12 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         for (int u = 0; u < kThrBatch; ++u) {
           const int i = min(i0 + u, nt - 1);
           task[u] = Q.test_task[i];
-          const float* v = values + (int64_t)task[u] * n_pairs;
-          double pp = c > 1 ? (double)__ldg(v + pr[0]) : 0.0;
+          double pp = c > 1 ? (double)ld(task[u], pr[0]) : 0.0;
           // fixed trip counts: pr stays in registers (a runtime-indexed pr
           // would live in local memory)
 #pragma unroll
           for (int j = 1; j < kMaxRg - 1; ++j)
-            if (j < c - 1) pp = __dadd_rn(pp, (double)__ldg(v + pr[j]));
+            if (j < c - 1) pp = __dadd_rn(pp, (double)ld(task[u], pr[j]));
           p[u] = pp;
         }
         float th[kThrBatch];
@@ -1956,7 +1965,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       bool pass = ok;
       float xo = 0.0f;
       for (int i = 0; i < nt; ++i) {
-        const float x = ok ? __ldg(values + (int64_t)Q.test_task[i] * n_pairs + last_pair + col) : 0.0f;
+        const float x = ok ? ld(Q.test_task[i], last_pair + col) : 0.0f;
         if (i == 0) xo = x;
         pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
       }

@@ -3,6 +3,7 @@
 objectives sharing a constraint set) and of the whole 20-query batch: where
 the batched pass's enumeration time goes.  Usage: python tools/c2_per_query.py"""
 import json
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -29,6 +30,10 @@ def med(ctx, qs, reps=7):
 shape = synth.make_shape(synth.SHAPES["c1"])
 u, w, b = synth.build_model(shape)
 ctx = _native.DeviceContext(0)
+# A/B knobs: APEX_OPTS="name=value,name=value" (apex_set_option)
+for kv in filter(None, os.environ.get("APEX_OPTS", "").split(",")):
+    name, val = kv.split("=")
+    ctx.set_option(name, int(val))
 ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
 ctx.load_cache(u, w, b)
 qs = synth.c2_queries()
