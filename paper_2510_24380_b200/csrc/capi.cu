@@ -876,6 +876,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       P.g_off = c->d_goff.as<unsigned long long>();
       P.n_rx = (int)c->rx.size();
       P.values = c->d_values.as<float>();
+      P.p16 = (c->packed16_ok && c->opt_packed16) ? c->d_packed16.as<float>() : nullptr;
       P.n_pairs = c->n_pairs;
       P.start = start;
       P.end = end;
@@ -891,6 +892,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       CL.queries = dq;
       CL.rx = c->d_rx.as<DevReaction>();
       CL.values = c->d_values.as<float>();
+      CL.p16 = (c->packed16_ok && c->opt_packed16) ? c->d_packed16.as<float>() : nullptr;
       CL.n_pairs = c->n_pairs;
       CL.lists = c->d_lists.as<int32_t>();
       CL.slot_off = c->d_slot_off.as<int32_t>();

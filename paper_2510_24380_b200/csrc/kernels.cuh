@@ -2005,12 +2005,20 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
 // equal cell of [start, end), jittered inside the cell).  Feasible samples are
 // counted in seed_hist by key >> 48; the k-th best sampled key bin is a valid
 // admission threshold because the samples are distinct real products.
+// contribution of task at pair row: from the pair-major copy when present
+// (one 64-byte line per pair), else the task-major table
+__device__ __forceinline__ float tval(const float* __restrict__ values, const float* __restrict__ p16, int64_t n_pairs,
+                                      int task, int64_t pair) {
+  return p16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
+}
+
 struct SampleLaunch {
   const ScanQuery* queries;
   const DevReaction* rx;
   const unsigned long long* g_off;   // [n_rx + 1]
   int n_rx;
   const float* values;
+  const float* p16;                  // pair-major copy or null
   int64_t n_pairs;
   unsigned long long start, end, samples;
 };
@@ -2073,11 +2081,11 @@ __global__ void sample_kernel(const SampleLaunch P, int nq) {
       bool feasible = true;
       double vobj = 0.0;
       for (int t = 0; t < nt; ++t) {
-        const float* v = P.values + (int64_t)Q.test_task[t] * P.n_pairs;
-        double val = (double)__ldg(v + pr[0]);
+        const int task = Q.test_task[t];
+        double val = (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]);
 #pragma unroll
         for (int j = 1; j < kMaxRg; ++j)
-          if (j < c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+          if (j < c) val = __dadd_rn(val, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
         val = __dadd_rn(val, Q.test_bias[t]);
         if (t == 0) vobj = val;
         else feasible = feasible && (Q.test_lower[t] ? (val >= Q.test_beta[t]) : (val <= Q.test_beta[t]));
@@ -2104,6 +2112,7 @@ struct CornerLaunch {
   const ScanQuery* queries;
   const DevReaction* rx;
   const float* values;
+  const float* p16;                  // pair-major copy or null
   int64_t n_pairs;
   const int32_t* lists;              // [n_tasks][2][slots] digits, best-first (dir 0 = largest, 1 = smallest)
   const int32_t* slot_off;           // [n_rx * kMaxRg] offset of (t, j)'s list within a (task, dir) block
@@ -2171,20 +2180,20 @@ __global__ void corner_kernel(const CornerLaunch P) {
       if (g >= P.start && g < P.end) {
         bool feasible = true;
         for (int tt = 1; tt < Q.nt && feasible; ++tt) {
-          const float* v = P.values + (int64_t)Q.test_task[tt] * P.n_pairs;
-          double val = (double)__ldg(v + pr[0]);
+          const int task = Q.test_task[tt];
+          double val = (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]);
 #pragma unroll
           for (int j = 1; j < kMaxRg; ++j)
-            if (j < R.c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+            if (j < R.c) val = __dadd_rn(val, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
           val = __dadd_rn(val, Q.test_bias[tt]);
           feasible = Q.test_lower[tt] ? (val >= Q.test_beta[tt]) : (val <= Q.test_beta[tt]);
         }
         if (feasible) {
-          const float* v = P.values + (int64_t)Q.test_task[0] * P.n_pairs;
-          double val = (double)__ldg(v + pr[0]);
+          const int task = Q.test_task[0];
+          double val = (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]);
 #pragma unroll
           for (int j = 1; j < kMaxRg; ++j)
-            if (j < R.c) val = __dadd_rn(val, (double)__ldg(v + pr[j]));
+            if (j < R.c) val = __dadd_rn(val, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
           val = __dadd_rn(val, Q.test_bias[0]);
           key = skey(Q.maximize ? val : -val);
         }
