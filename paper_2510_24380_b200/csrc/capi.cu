@@ -171,6 +171,8 @@ struct Batch {
   bool finalize = false;
   bool copy_out = false;       // result rows D2H inside the pass (synchronous apex_query)
   bool no_full = false;        // this signature needed no full-predicate kernel last time: skip its launches
+  bool small_only = false;     // every query of this signature's last run fit the small finalize: skip the
+                               // large-path launches (select, chunk sort, merge rank); re-run if one does not
   uint64_t key0 = 0;           // signature before no_full (history key)
   Plan* plan = nullptr;
   Plan* plan_rows = nullptr;    // whole-row tiles (sorted-column admission kernel)
@@ -223,6 +225,7 @@ struct apex_ctx {
   bool copy_next = false;                // next prepare_batch: result D2H inside the pass
   std::vector<uint64_t> seen_keys;       // recent batch signatures (graph capture on the second sighting)
   std::vector<uint64_t> nofull_keys;     // signatures whose last run sent no query to the full predicate
+  std::vector<uint64_t> small_keys;      // signatures whose last run finished every query in the small finalize
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   DBuf d_work;                           // flattened-work counters of the scan launches
@@ -771,13 +774,14 @@ cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
 // through the cooperative radix select (launched over chunks of queries that
 // fit co-resident), rank, scatter and (finalize) materialization.
 int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool finalize, RunStats& st,
-                   cudaStream_t s, bool mark, bool compute_bound = true) {
+                   cudaStream_t s, bool mark, bool compute_bound = true, bool skip_large = false) {
   MatLaunch M;
   M.queries = dq;
   M.rx = c->d_rx.as<DevReaction>();
   M.g_off = c->d_goff.as<unsigned long long>();
   M.n_rx = (int)c->rx.size();
   M.values = c->d_values.as<float>();
+  M.p16 = (c->packed16_ok && c->opt_packed16) ? c->d_packed16.as<float>() : nullptr;
   M.n_pairs = c->n_pairs;
   M.biases = c->d_biases.as<double>();
   {
@@ -791,7 +795,7 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
     finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, 0, compute_bound ? 1 : 0);
     ++st.launches;
   }
-  {
+  if (!skip_large) {
     if (!c->occ_sel)
       APEX_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->occ_sel, (const void*)select_kernel, kSelectThreads, 0));
     const int resident = std::max(1, c->occ_sel * c->sm_count);
@@ -807,11 +811,14 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
   }
   if (mark) APEX_CU(stage_mark(c, 4, s));
   if (finalize) {
-    const int ib = (int)((k_max + 255) / 256);
-    sort_chunks_kernel<<<dim3((unsigned)((k_max + kSortChunk - 1) / kSortChunk), nq), 1024, 0, s>>>(dq);
-    merge_rank_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+    if (!skip_large) {
+      const int ib = (int)((k_max + 255) / 256);
+      sort_chunks_kernel<<<dim3((unsigned)((k_max + kSortChunk - 1) / kSortChunk), nq), 1024, 0, s>>>(dq);
+      merge_rank_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
+      st.launches += 2;
+    }
     materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
-    st.launches += 3;
+    st.launches += 1;
   }
   return APEX_OK;
 }
@@ -1072,7 +1079,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   APEX_CU(stage_mark(c, 7, s));
   APEX_CU(stage_mark(c, 3, s));
   // final bound (inside the small-set finalize), exact select
-  APEX_TRY(enqueue_select(c, dq, nq, B.k_max, B.finalize, st, s, true));
+  APEX_TRY(enqueue_select(c, dq, nq, B.k_max, B.finalize, st, s, true, true, B.small_only));
   APEX_CU(cudaGetLastError());
   APEX_CU(stage_mark(c, 5, s));
   // control-block headers to host (read by check_batch): one strided copy
@@ -1104,6 +1111,19 @@ int check_batch(apex_ctx* c) {
   std::vector<RunPreset> pre(nq);
   for (int attempt = 0;; ++attempt) {
     APEX_CU(cudaStreamSynchronize(c->stream));
+    if (B.small_only) {
+      // the large path was skipped on the strength of this signature's last
+      // run: if a query did not fit the small finalize now, run it again whole
+      bool all_small = true;
+      for (int i = 0; i < nq; ++i) all_small = all_small && c->h_ctl.as<QCtl>()[i].small_done;
+      if (!all_small) {
+        B.small_only = false;
+        c->small_keys.erase(std::remove(c->small_keys.begin(), c->small_keys.end(), B.key0), c->small_keys.end());
+        ++B.st.retries;
+        APEX_TRY(enqueue_batch(c, nullptr));
+        continue;
+      }
+    }
     bool overflow = false;
     for (int i = 0; i < nq; ++i) {
       const QCtl& C = c->h_ctl.as<QCtl>()[i];
@@ -1159,6 +1179,14 @@ int check_batch(apex_ctx* c) {
     APEX_TRY(enqueue_batch(c, pre.data()));
   }
   B.pending = false;
+  if (!B.small_only) {
+    bool all_small = true;
+    for (int i = 0; i < nq; ++i) all_small = all_small && c->h_ctl.as<QCtl>()[i].small_done;
+    if (all_small && std::find(c->small_keys.begin(), c->small_keys.end(), B.key0) == c->small_keys.end()) {
+      if (c->small_keys.size() >= 64) c->small_keys.erase(c->small_keys.begin());
+      c->small_keys.push_back(B.key0);
+    }
+  }
   if (!B.no_full && c->opt_mode == 3 && B.plan_rows) {
     bool any_full = false;
     for (int i = 0; i < nq; ++i) any_full = any_full || c->h_ctl.as<QCtl>()[i].use_full;
@@ -1188,6 +1216,7 @@ uint64_t batch_key(const apex_ctx* c) {
   mix(&B.finalize, sizeof(B.finalize));
   mix(&B.copy_out, sizeof(B.copy_out));
   mix(&B.no_full, sizeof(B.no_full));
+  mix(&B.small_only, sizeof(B.small_only));
   for (int i = 0; i < B.nq; ++i) {
     const apex_query_spec& q = B.qs[i];
     mix(&q.objective_task, sizeof(q.objective_task));
@@ -1221,6 +1250,7 @@ int launch_batch(apex_ctx* c) {
   Bq.key0 = batch_key(c);
   Bq.no_full = c->opt_mode == 3 && Bq.plan_rows &&
                std::find(c->nofull_keys.begin(), c->nofull_keys.end(), Bq.key0) != c->nofull_keys.end();
+  Bq.small_only = std::find(c->small_keys.begin(), c->small_keys.end(), Bq.key0) != c->small_keys.end();
   if (!c->opt_graph || c->graph_broken) return enqueue_batch(c, nullptr);
   const uint64_t key = batch_key(c);
   if (c->gexec && key == c->gkey) {

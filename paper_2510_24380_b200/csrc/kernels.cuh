@@ -2566,6 +2566,7 @@ struct MatLaunch {
   const unsigned long long* g_off;  // [n_rx + 1]
   int n_rx;
   const float* values;
+  const float* p16;                 // pair-major copy or null
   int64_t n_pairs;
   const double* biases;
 };
@@ -2596,12 +2597,11 @@ __device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned
   // zero_start: apex_score's acc = 0.0; acc += v_r order (differs from the
   // scan's v0 + v1 + ... only in the sign of an all-zero sum)
   auto sum = [&](int task, bool zero_start) {
-    const float* __restrict__ v = M.values + (int64_t)task * M.n_pairs;
-    const double v0 = (double)__ldg(v + pr[0]);
+    const double v0 = (double)tval(M.values, M.p16, M.n_pairs, task, pr[0]);
     double acc = zero_start ? __dadd_rn(0.0, v0) : v0;
 #pragma unroll
     for (int j = 1; j < kMaxRg; ++j)
-      if (j < c) acc = __dadd_rn(acc, (double)__ldg(v + pr[j]));
+      if (j < c) acc = __dadd_rn(acc, (double)tval(M.values, M.p16, M.n_pairs, task, pr[j]));
     return __dadd_rn(acc, __ldg(M.biases + task));
   };
   Q.out_obj[i] = sum(Q.obj_task, false);
