@@ -629,8 +629,8 @@ int plan_multi(apex_ctx* c, Batch& B) {
   B.plan_multi = nullptr;
   const int nq = B.nq;
   if (!c->opt_multi || c->opt_mode != 3 || !c->packed16_ok || !c->opt_packed16 || nq < 2 || !B.plan_rows ||
-      c->trace_cap || B.qs[0].end - B.qs[0].start >= (uint64_t)c->opt_chunk_min)
-    return APEX_OK;  // (the multi kernel scans the whole range in one launch per group: no chunked scans)
+      c->trace_cap)
+    return APEX_OK;
   struct TestKey {
     int task, lower;
     double beta;
@@ -720,7 +720,7 @@ int plan_multi(apex_ctx* c, Batch& B) {
   }
   Plan* keep = B.plan;
   Plan* keep_rows = B.plan_rows;
-  APEX_TRY(build_plan(c, B.qs[0].start, B.qs[0].end, 32, 1, B.plan_multi, kMTile));
+  APEX_TRY(build_plan(c, B.qs[0].start, B.qs[0].end, 32, 1, B.plan_multi, kMCB));
   B.plan = keep;
   B.plan_rows = keep_rows;
   return APEX_OK;
@@ -1082,7 +1082,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       if (ci == 0) APEX_CU(stage_mark(c, 6, s));
       if (B.multi) {
         // batched multi-query kernel: every query of the batch, one launch per query group
-        const size_t smem = (size_t)kScanWarps * kMSmemWarp * sizeof(float);
+        const size_t smem = (size_t)kScanWarps * kMCB * kMW * sizeof(float);
         if (!c->attr_multi) {
           APEX_CU(cudaFuncSetAttribute((const void*)scan_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
@@ -1098,7 +1098,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
           Lm.n_pairs = c->n_pairs;
           Lm.queries = dq;
           const unsigned blocks = (unsigned)std::max<int64_t>(
-              1, std::min<int64_t>(((int64_t)pm->tiles.size() + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * 2));
+              1, std::min<int64_t>(((int64_t)pm->tiles.size() + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * 3));
           scan_multi_kernel<<<blocks, kScanWarps * 32, smem, s>>>(Lm);
           APEX_CU(cudaGetLastError());
           ++st.launches;

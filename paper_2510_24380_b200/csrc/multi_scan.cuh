@@ -2,22 +2,19 @@
 // share constraint sets (BASELINE configs[1]: 5 objectives x 4 property
 // presets = 20 queries, 13 distinct bounds).
 //
-// Work item = one tile (<= 32 rows x <= kMTile columns of one reaction) for
-// ALL queries of the launch (<= 16), instead of one (tile, query) item per
-// query:
+// Work item = one tile (<= 32 rows x <= 64 columns of one reaction) for ALL
+// queries of the launch (<= 16), instead of one (tile, query) item per query:
 //   * per row (lane): the exact fp32 threshold of every DISTINCT constraint
 //     test of the launch (a (task, bound, side) shared by several queries is
-//     derived once) and every query's admission threshold against its tau,
-//     from the row's prefix lines staged once in shared memory;
-//   * per 32-column block: the block's pair-major table lines (32 x 64 B,
-//     contiguous) loaded with coalesced 16-byte loads, then the signed values
-//     of every distinct test and every query's objective laid out per column
-//     in shared memory and read back as broadcast LDS.128;
+//     derived once) and every query's admission threshold against its tau;
+//   * per column block: the signed column values of those tests and of every
+//     query's objective staged once in shared memory (from the pair-major
+//     table copy), read back as broadcast LDS.128;
 //   * per product: one fp32 compare per distinct test -> a test bitmask; the
-//     feasibility of every distinct constraint set from the mask; one compare
-//     per query against its admission threshold; candidates (feasible and
-//     s >= tau, both exact, as in every K3 form) appended per query with the
-//     same warp-aggregated protocol, histogram and tau refresh.
+//     group feasibility of every distinct constraint set from the mask; one
+//     compare per query against its admission threshold; candidates (feasible
+//     and s >= tau, both exact, as in every K3 form) appended per query with
+//     the same warp-aggregated protocol, histogram and tau refresh.
 // Per product the work is |distinct tests| + |queries| compares, not
 // sum_q (bounds_q + 1): C2 33 instead of 90.
 #pragma once
@@ -28,11 +25,8 @@ namespace apexb200 {
 constexpr int kMU = 16;    // distinct constraint tests per launch
 constexpr int kMQ = 16;    // queries per launch
 constexpr int kMG = 8;     // distinct constraint sets per launch
-constexpr int kMCB = 32;   // columns per shared-memory block
-constexpr int kMTile = 256;  // columns per tile (thresholds derived once per tile row)
+constexpr int kMCB = 64;   // columns per tile (shared-memory block)
 constexpr int kMW = 32;    // staged values per column: tests [0, 16), query objectives [16, 32)
-// shared memory per warp: raw lines [kMCB][16] + signed values [kMCB][kMW] + prefix lines [2][32][16]
-constexpr size_t kMSmemWarp = (size_t)kMCB * 16 + (size_t)kMCB * kMW + 2 * 32 * 16;
 
 struct MultiLaunch {
   const Tile* tiles;
@@ -52,14 +46,11 @@ struct MultiLaunch {
   int q_idx[kMQ];            // query i of the launch = queries[q_idx[i]]
 };
 
-__global__ void __launch_bounds__(kScanWarps * 32, 2) scan_multi_kernel(const MultiLaunch M) {
+__global__ void __launch_bounds__(kScanWarps * 32, 3) scan_multi_kernel(const MultiLaunch M) {
   extern __shared__ __align__(16) float msm[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  float* raw = msm + (size_t)warp * kMSmemWarp;        // [kMCB][16]
-  float* ys = raw + kMCB * 16;                          // [kMCB][kMW]
-  float* pre = ys + kMCB * kMW;                         // [2][32 lanes][16]
+  float* ys = msm + (size_t)warp * kMCB * kMW;  // this warp's staged column block
   const unsigned qmask_all = M.nq >= 32 ? ~0u : ((1u << M.nq) - 1u);
-  const float kNaN = __int_as_float(0x7fc00000);
   for (;;) {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(M.work, 1u);
@@ -69,32 +60,37 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_multi_kernel(const Mu
     const DevReaction& R = M.rx[T.rx];
     const int c = R.c;
     const int64_t last_pair = R.pair_off[c - 1];
-    // 1. per-row prefix lines (lane = row) into shared memory: every task of
-    //    the row's first c-1 synthons in one 64-byte line each
+    const int ncols = (int)T.ncols;
+    // 1. stage the signed test / objective values of the tile's columns
+    __syncwarp();
+    for (int idx = lane; idx < ncols * kMW; idx += 32) {
+      const int j = idx / kMW, w = idx % kMW;
+      float y = __int_as_float(0x7fc00000);  // NaN: an unused slot never passes
+      if (w < kMU) {
+        if (w < M.nu) {
+          const float x = __ldg(M.p16 + (last_pair + T.col0 + j) * 16 + M.u_task[w]);
+          y = M.u_lower[w] ? -x : x;
+        }
+      } else if (w - kMU < M.nq) {
+        const ScanQuery& Q = M.queries[M.q_idx[w - kMU]];
+        const float x = __ldg(M.p16 + (last_pair + T.col0 + j) * 16 + Q.obj_task);
+        y = Q.maximize ? -x : x;  // signed: s >= tau <=> y <= threshold
+      }
+      ys[j * kMW + w] = y;
+    }
+    // 2. per-row thresholds (lane = row)
     const bool valid = lane < T.nrows;
     const uint64_t row = T.row0 + (valid ? lane : 0u);
     int64_t pr[kMaxRg - 1];
     decode_prefix(R, c, row, pr);
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-      if (j < c - 1) {
-        const float4* src = reinterpret_cast<const float4*>(M.p16 + pr[j] * 16);
-        float4* dst = reinterpret_cast<float4*>(pre + (j * 32 + lane) * 16);
-        const float4 a = __ldg(src), b = __ldg(src + 1), cc = __ldg(src + 2), d = __ldg(src + 3);
-        dst[0] = a; dst[1] = b; dst[2] = cc; dst[3] = d;
-      }
-    __syncwarp();
     auto prefix = [&](int task) -> double {
-      if (c == 1) return 0.0;
-      double p = (double)pre[lane * 16 + task];
-      if (c > 2) p = __dadd_rn(p, (double)pre[(32 + lane) * 16 + task]);
+      double p = c > 1 ? (double)__ldg(M.p16 + pr[0] * 16 + task) : 0.0;
 #pragma unroll
-      for (int j = 2; j < kMaxRg - 1; ++j)  // 4+ component reactions: the rest from global
+      for (int j = 1; j < kMaxRg - 1; ++j)
         if (j < c - 1) p = __dadd_rn(p, (double)__ldg(M.p16 + pr[j] * 16 + task));
       return p;
     };
-    // 2. per-row thresholds
+    const float kNaN = __int_as_float(0x7fc00000);
     float th[kMU];
 #pragma unroll
     for (int u = 0; u < kMU; ++u) {
@@ -120,99 +116,61 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) scan_multi_kernel(const Mu
         }
       }
     }
-    const unsigned long long gbase = R.g_off + row * (uint64_t)R.size[c - 1];
-    // 3. column blocks
-    for (int cb0 = 0; cb0 < (int)T.ncols; cb0 += kMCB) {
-      const int ncols = min(kMCB, (int)T.ncols - cb0);
-      const int col0 = (int)T.col0 + cb0;
-      __syncwarp();
-      // raw pair-major lines of the block: ncols x 64 B, contiguous
-      {
-        const float4* src = reinterpret_cast<const float4*>(M.p16 + (last_pair + col0) * 16);
-        float4* dst = reinterpret_cast<float4*>(raw);
-        float4 v[kMCB * 4 / 32];
+    __syncwarp();
+    const unsigned long long gbase = R.g_off + row * (uint64_t)R.size[c - 1] + T.col0;
+    // 3. every product of the tile against every test and query
+    for (int j = 0; j < ncols; ++j) {
+      const float4* yp = reinterpret_cast<const float4*>(ys + j * kMW);
+      float y[kMW];
 #pragma unroll
-        for (int i = 0; i < kMCB * 4 / 32; ++i) {
-          const int idx = lane + 32 * i;
-          if (idx < ncols * 4) v[i] = __ldg(src + idx);
-        }
-#pragma unroll
-        for (int i = 0; i < kMCB * 4 / 32; ++i) {
-          const int idx = lane + 32 * i;
-          if (idx < ncols * 4) dst[idx] = v[i];
-        }
+      for (int v = 0; v < kMW / 4; ++v) {
+        const float4 f = yp[v];
+        y[4 * v] = f.x; y[4 * v + 1] = f.y; y[4 * v + 2] = f.z; y[4 * v + 3] = f.w;
       }
-      __syncwarp();
-      // signed test / objective values per column (lane: two columns; NaN in unused slots never passes)
-      for (int j = lane; j < ncols; j += 32) {
-        const float* x = raw + j * 16;
-        float* y = ys + j * kMW;
+      unsigned tm = 0;
 #pragma unroll
-        for (int w = 0; w < kMU; ++w) y[w] = w < M.nu ? (M.u_lower[w] ? -x[M.u_task[w]] : x[M.u_task[w]]) : kNaN;
+      for (int u = 0; u < kMU; ++u)
+        if (y[u] <= th[u]) tm |= 1u << u;
+      unsigned feas = 0;
 #pragma unroll
-        for (int q = 0; q < kMQ; ++q) {
-          float v = kNaN;
-          if (q < M.nq) {
-            const ScanQuery& Q = M.queries[M.q_idx[q]];
-            v = Q.maximize ? -x[Q.obj_task] : x[Q.obj_task];  // signed: s >= tau <=> y <= threshold
-          }
-          y[kMU + q] = v;
+      for (int g = 0; g < kMG; ++g)
+        if (g < M.ng && (tm & M.g_need[g]) == M.g_need[g]) feas |= M.g_queries[g];
+      unsigned adm = 0;
+#pragma unroll
+      for (int q = 0; q < kMQ; ++q)
+        if (y[kMU + q] <= th0[q]) adm |= 1u << q;
+      const unsigned cand = adm & feas & qmask_all;
+      unsigned any = __reduce_or_sync(0xffffffffu, cand);
+      // rare path: append the candidates of every query with one
+      while (any) {
+        const int q = __ffs(any) - 1;
+        any &= any - 1;
+        const ScanQuery& Q = M.queries[M.q_idx[q]];
+        QCtl* ctl = Q.ctl;
+        bool pass = (cand >> q) & 1u;
+        Entry e;
+        if (pass) {
+          const float x = Q.maximize ? -y[kMU + q] : y[kMU + q];
+          const double val = fx(prefix(Q.obj_task), x, Q.test_bias[0]);
+          e.key = skey(Q.maximize ? val : -val);
+          e.g = gbase + (unsigned long long)j;
+          pass = !tie_reject(ctl, e.key, e.g);
         }
-      }
-      __syncwarp();
-      for (int j = 0; j < ncols; ++j) {
-        const float4* yp = reinterpret_cast<const float4*>(ys + j * kMW);
-        float y[kMW];
-#pragma unroll
-        for (int v = 0; v < kMW / 4; ++v) {
-          const float4 f = yp[v];
-          y[4 * v] = f.x; y[4 * v + 1] = f.y; y[4 * v + 2] = f.z; y[4 * v + 3] = f.w;
+        const unsigned mk = __ballot_sync(0xffffffffu, pass);
+        if (!mk) continue;
+        unsigned long long cbase = 0;
+        if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
+        cbase = __shfl_sync(0xffffffffu, cbase, 0);
+        if (pass) {
+          const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
+          if (idx < Q.cap) Q.buf[idx] = e;
+          const unsigned hb = cand_bin(ctl, e.key, e.g, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+          atomicAdd(&Q.hist[hb], 1u);
+          atomicAdd(&Q.coarse[hb >> 8], 1u);
         }
-        unsigned tm = 0;
-#pragma unroll
-        for (int u = 0; u < kMU; ++u)
-          if (y[u] <= th[u]) tm |= 1u << u;
-        unsigned feas = 0;
-#pragma unroll
-        for (int g = 0; g < kMG; ++g)
-          if (g < M.ng && (tm & M.g_need[g]) == M.g_need[g]) feas |= M.g_queries[g];
-        unsigned adm = 0;
-#pragma unroll
-        for (int q = 0; q < kMQ; ++q)
-          if (y[kMU + q] <= th0[q]) adm |= 1u << q;
-        const unsigned cand = adm & feas & qmask_all;
-        unsigned any = __reduce_or_sync(0xffffffffu, cand);
-        // rare path: append the candidates of every query with one
-        while (any) {
-          const int q = __ffs(any) - 1;
-          any &= any - 1;
-          const ScanQuery& Q = M.queries[M.q_idx[q]];
-          QCtl* ctl = Q.ctl;
-          bool pass = (cand >> q) & 1u;
-          Entry e;
-          if (pass) {
-            const float x = Q.maximize ? -y[kMU + q] : y[kMU + q];
-            const double val = fx(prefix(Q.obj_task), x, Q.test_bias[0]);
-            e.key = skey(Q.maximize ? val : -val);
-            e.g = gbase + (unsigned long long)(col0 + j);
-            pass = !tie_reject(ctl, e.key, e.g);
-          }
-          const unsigned mk = __ballot_sync(0xffffffffu, pass);
-          if (!mk) continue;
-          unsigned long long cbase = 0;
-          if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
-          cbase = __shfl_sync(0xffffffffu, cbase, 0);
-          if (pass) {
-            const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
-            if (idx < Q.cap) Q.buf[idx] = e;
-            const unsigned hb = cand_bin(ctl, e.key, e.g, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
-            atomicAdd(&Q.hist[hb], 1u);
-            atomicAdd(&Q.coarse[hb >> 8], 1u);
-          }
-          if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
-            __threadfence();
-            refresh_tau(Q);
-          }
+        if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
+          __threadfence();
+          refresh_tau(Q);
         }
       }
     }
