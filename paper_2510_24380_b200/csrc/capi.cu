@@ -33,7 +33,6 @@
 #include "k8.cuh"
 #include "trace.cuh"
 #include "bind.cuh"
-#include "multi_scan.cuh"
 
 using namespace apexb200;
 
@@ -177,9 +176,6 @@ struct Batch {
   uint64_t key0 = 0;           // signature before no_full (history key)
   Plan* plan = nullptr;
   Plan* plan_rows = nullptr;    // whole-row tiles (sorted-column admission kernel)
-  Plan* plan_multi = nullptr;   // 32-row x 64-column tiles (batched multi-query kernel)
-  bool multi = false;           // this batch's queries all go to scan_multi_kernel
-  std::vector<MultiLaunch> mlaunch;
   bool pending = false;
   // multi-GPU local step (apex_query_local_async): where the selected entries
   // are exported, with what per-query stride
@@ -266,9 +262,6 @@ struct apex_ctx {
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_packed16 = 1;         // sorted-column kernel reads the pair-major table copy
-  int64_t opt_multi = 1;            // batched multi-query kernel: 0 off, 1 when the cost model favours it, 2 always
-  int64_t opt_multi_sorted_rate = 14050;   // cost model: sorted kernel row-queries per us
-  int64_t opt_multi_rate = 10000000;       // cost model: multi kernel product-compares per us
   int64_t opt_chunk = 1;            // work items per atomic in the scan kernels
   int64_t opt_tiles_per_slot = 8;   // target enumeration tiles per warp slot (balance vs per-tile setup)
   uint64_t opt_gen = 0;             // bumped by apex_set_option
@@ -296,7 +289,6 @@ struct apex_ctx {
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
   std::vector<std::pair<const void*, size_t>> attr_cache;
   bool attr_small = false;
-  bool attr_multi = false;
   int occ_sel = 0;
   // a context is driven by one thread at a time: every C-ABI call on it holds
   // this lock (calls on different contexts run concurrently)
@@ -617,115 +609,6 @@ int build_corners(apex_ctx* c) {
 // enqueue (device pipeline, no host sync), check (one sync: overflow check and
 // exact re-run with the final bound if the candidate buffer overflowed).
 
-// Batched multi-query kernel: partition the batch's queries into launches of
-// <= kMQ queries whose constraint tests (deduplicated) fit kMU and whose
-// distinct constraint sets fit kMG (queries ordered by constraint set, so
-// queries sharing a preset share a launch), and take the multi kernel for the
-// whole batch when the cost model predicts it beats the sorted-column kernel:
-// sorted ~ rows x queries, multi ~ products x (distinct tests + queries).
-int plan_multi(apex_ctx* c, Batch& B) {
-  B.multi = false;
-  B.mlaunch.clear();
-  B.plan_multi = nullptr;
-  const int nq = B.nq;
-  if (!c->opt_multi || c->opt_mode != 3 || !c->packed16_ok || !c->opt_packed16 || nq < 2 || !B.plan_rows ||
-      c->trace_cap)
-    return APEX_OK;
-  struct TestKey {
-    int task, lower;
-    double beta;
-    bool operator==(const TestKey& o) const { return task == o.task && lower == o.lower && beta == o.beta; }
-  };
-  std::vector<std::vector<TestKey>> qt(nq);
-  for (int i = 0; i < nq; ++i)
-    for (int t = 1; t < B.tests[i].nt; ++t) qt[i].push_back({B.tests[i].task[t], B.tests[i].lower[t], B.tests[i].beta[t]});
-  std::vector<int> order(nq);
-  std::iota(order.begin(), order.end(), 0);
-  auto sig_less = [&](int a, int b) {
-    const auto& x = qt[a];
-    const auto& y = qt[b];
-    if (x.size() != y.size()) return x.size() < y.size();
-    for (size_t i = 0; i < x.size(); ++i) {
-      if (x[i].task != y[i].task) return x[i].task < y[i].task;
-      if (x[i].lower != y[i].lower) return x[i].lower < y[i].lower;
-      if (x[i].beta != y[i].beta) return x[i].beta < y[i].beta;
-    }
-    return a < b;
-  };
-  std::stable_sort(order.begin(), order.end(), sig_less);
-  int64_t compares = 0;
-  size_t pos = 0;
-  while (pos < order.size()) {
-    MultiLaunch L;
-    std::memset(&L, 0, sizeof(L));
-    std::vector<TestKey> tests;
-    std::vector<unsigned> gneed;
-    size_t end = pos;
-    while (end < order.size() && L.nq < kMQ) {
-      const int qi = order[end];
-      std::vector<TestKey> add;
-      unsigned need = 0;
-      for (const TestKey& k : qt[qi]) {
-        int u = -1;
-        for (size_t i = 0; i < tests.size(); ++i)
-          if (tests[i] == k) u = (int)i;
-        if (u < 0) {
-          for (size_t i = 0; i < add.size(); ++i)
-            if (add[i] == k) u = (int)(tests.size() + i);
-        }
-        if (u < 0) {
-          add.push_back(k);
-          u = (int)(tests.size() + add.size() - 1);
-        }
-        need |= 1u << u;
-      }
-      if (tests.size() + add.size() > (size_t)kMU) break;
-      int g = -1;
-      for (size_t i = 0; i < gneed.size(); ++i)
-        if (gneed[i] == need) g = (int)i;
-      if (g < 0 && gneed.size() >= (size_t)kMG) break;
-      tests.insert(tests.end(), add.begin(), add.end());
-      if (g < 0) {
-        gneed.push_back(need);
-        g = (int)gneed.size() - 1;
-      }
-      L.g_queries[g] |= 1u << L.nq;
-      L.q_idx[L.nq++] = qi;
-      ++end;
-    }
-    if (end == pos) return APEX_OK;  // a single query's tests exceed the launch limits: sorted kernel
-    L.nu = (int)tests.size();
-    L.ng = (int)gneed.size();
-    for (int u = 0; u < L.nu; ++u) {
-      L.u_task[u] = tests[u].task;
-      L.u_lower[u] = tests[u].lower;
-      L.u_beta[u] = tests[u].beta;
-      L.u_bias[u] = c->biases[tests[u].task];
-    }
-    for (int g = 0; g < L.ng; ++g) L.g_need[g] = gneed[g];
-    compares += L.nu + L.nq;
-    B.mlaunch.push_back(L);
-    pos = end;
-  }
-  // cost model (rates calibrated on C2, options): products x compares vs rows x queries
-  const uint64_t span = B.qs[0].end - B.qs[0].start;
-  uint64_t rows = 0;
-  for (const Tile& T : B.plan_rows->tiles) rows += T.nrows;
-  const double multi_us = (double)span * (double)compares / (double)c->opt_multi_rate;
-  const double sorted_us = (double)rows * (double)nq / (double)c->opt_multi_sorted_rate;
-  B.multi = c->opt_multi == 2 || multi_us < sorted_us;
-  if (!B.multi) {
-    B.mlaunch.clear();
-    return APEX_OK;
-  }
-  Plan* keep = B.plan;
-  Plan* keep_rows = B.plan_rows;
-  APEX_TRY(build_plan(c, B.qs[0].start, B.qs[0].end, 32, 1, B.plan_multi, kMCB));
-  B.plan = keep;
-  B.plan_rows = keep_rows;
-  return APEX_OK;
-}
-
 int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finalize) {
   Batch& B = c->batch;
   if (!c->corners_ok) APEX_TRY(build_corners(c));
@@ -782,7 +665,6 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32, nq, B.plan_rows, max_last));
     B.plan = keep;  // still cached: build_plan never evicts the most recently used plan
   }
-  APEX_TRY(plan_multi(c, B));
 
   if ((int)c->slots.size() < nq) c->slots.resize(nq);
   for (int i = 0; i < nq; ++i) {
@@ -964,7 +846,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   // threshold-less ones with a non-sparse feasible set, which stream the
   // full predicate; signatures that needed none of those skip its launches
   const bool sorted_all = c->opt_mode == 3 && B.plan_rows;
-  const bool full = c->opt_mode != 2 && !B.no_full && !B.multi;
+  const bool full = c->opt_mode != 2 && !B.no_full;
   const int autok = (c->opt_mode == 3 && !tau0) ? (B.no_full ? 3 : sorted_all ? 2 : 1) : 0;
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
@@ -1080,31 +962,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       L.work = c->d_work.as<unsigned>();
       L.chunk = (int)c->opt_chunk;
       if (ci == 0) APEX_CU(stage_mark(c, 6, s));
-      if (B.multi) {
-        // batched multi-query kernel: every query of the batch, one launch per query group
-        const size_t smem = (size_t)kScanWarps * kMCB * kMW * sizeof(float);
-        if (!c->attr_multi) {
-          APEX_CU(cudaFuncSetAttribute((const void*)scan_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-          c->attr_multi = true;
-        }
-        const Plan* pm = B.plan_multi;
-        for (MultiLaunch Lm : B.mlaunch) {
-          Lm.tiles = pm->d_tiles.as<Tile>();
-          Lm.n_tiles = (unsigned)pm->tiles.size();
-          Lm.work = c->d_work.as<unsigned>() + (wi++ % 64);
-          Lm.rx = c->d_rx.as<DevReaction>();
-          Lm.p16 = c->d_packed16.as<float>();
-          Lm.n_pairs = c->n_pairs;
-          Lm.queries = dq;
-          const unsigned blocks = (unsigned)std::max<int64_t>(
-              1, std::min<int64_t>(((int64_t)pm->tiles.size() + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * 3));
-          scan_multi_kernel<<<blocks, kScanWarps * 32, smem, s>>>(Lm);
-          APEX_CU(cudaGetLastError());
-          ++st.launches;
-          ++st.scans;
-        }
-      } else if (admit && B.plan_rows && bounds.size() == 1) {
+      if (admit && B.plan_rows && bounds.size() == 1) {
         // sorted-column admission: whole-row tiles, one launch per 64 queries
         const Plan* pr_ = B.plan_rows;
         const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
@@ -1177,7 +1035,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       // full-predicate launches per test class alternate between the main and
       // the side stream so consecutive classes overlap (disjoint queries)
       int n_full_launch = 0;
-      for (size_t k = 0; full && !B.multi && k + 1 < B.cls_begin.size(); ++k) {
+      for (size_t k = 0; full && k + 1 < B.cls_begin.size(); ++k) {
         ScanFn fn = pick_scan(B.cls_nt[k], B.rl, c->opt_mode == 1 ? 1 : 0);
         if (!fn) return set_err(APEX_ELIMIT, "no enumeration kernel for this test count");
         const size_t smem = scan_smem(B.cls_nt[k], cb);
@@ -1374,9 +1232,6 @@ uint64_t batch_key(const apex_ctx* c) {
   mix(&plan, sizeof(plan));
   const void* plan_rows = B.plan_rows;
   mix(&plan_rows, sizeof(plan_rows));
-  const void* plan_m = B.plan_multi;
-  mix(&plan_m, sizeof(plan_m));
-  mix(&B.multi, sizeof(B.multi));
   mix(&c->opt_gen, sizeof(c->opt_gen));
   const uint64_t gen = g_alloc_gen.load();
   mix(&gen, sizeof(gen));
@@ -2296,9 +2151,6 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   }
   else if (n == "graph") c->opt_graph = v;
   else if (n == "packed16") c->opt_packed16 = v;
-  else if (n == "multi") c->opt_multi = v;
-  else if (n == "multi_sorted_rate") c->opt_multi_sorted_rate = std::max<int64_t>(1, v);
-  else if (n == "multi_rate") c->opt_multi_rate = std::max<int64_t>(1, v);
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
   else if (n == "tiles_per_slot") c->opt_tiles_per_slot = std::max<int64_t>(1, v);
   else if (n == "mode") {

@@ -210,8 +210,7 @@ def _random_case(seed, n_rx=6, mu=3.0, sigma=0.7, n_tasks=4, c3=0.5, max_c=3):
                                   {"cap": 1024, "samples": 16}, {"refresh": 256, "samples": 64}, {"graph": 0},
                                   {"mode": 2, "dense": 1}, {"mode": 2, "dense": 5, "rl": 2}, {"mode": 2, "dense": 3}, {"mode": 2, "dense": 1, "rl": 2, "tile_products": 8192}, {"mode": 2, "dense": 2},
                                   {"sorted": 0}, {"sorted": 0, "dense": 1}, {"sorted": 0, "rl": 2, "mode": 2},
-                                  {"mode": 2, "dense": 0}, {"multi": 2}, {"multi": 2, "cap": 1024, "samples": 16},
-                                  {"multi": 2, "refresh": 256, "samples": 64}, {"multi": 0}, {"packed16": 0}])
+                                  {"mode": 2, "dense": 0}])
 def test_random_libraries_vs_oracle(native, seed, opts):
     from oracle import scan_oracle as orc
 
@@ -244,8 +243,7 @@ def test_random_libraries_vs_oracle(native, seed, opts):
 
 
 @pytest.mark.parametrize("opts", [{}, {"dense": 1}, {"dense": 3}, {"cb_admit": 64}, {"mode": 2}, {"sorted": 0},
-                                  {"sorted": 0, "mode": 2}, {"refresh": 256}, {"multi": 2}, {"multi": 2, "refresh": 256},
-                                  {"multi": 0}])
+                                  {"sorted": 0, "mode": 2}, {"refresh": 256}])
 @pytest.mark.parametrize("seed", [21, 22, 23])
 def test_shared_objective_batches_vs_oracle(native, seed, opts):
     """Batches whose queries share objective columns (same task and
