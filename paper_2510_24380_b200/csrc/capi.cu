@@ -448,11 +448,15 @@ using ScanFn = void (*)(const ScanLaunch);
 template <int NT, int RL, int MODE>
 ScanFn scan_ptr() { return scan_kernel<NT, RL, MODE>; }
 
+// (one full-predicate form is compiled: one row per lane, FSETP compare
+// chain — the FADD2 / two-rows-per-lane variants never won an A/B and only
+// cost build time)
 ScanFn pick_scan(int nt, int rl, int mode) {
+  (void)rl;
+  (void)mode;
 #define CASE(N)                                                                         \
   case N:                                                                               \
-    if (mode == 1) return rl == 1 ? scan_ptr<N, 1, 1>() : scan_ptr<N, 2, 1>();        \
-    return rl == 1 ? scan_ptr<N, 1, 0>() : scan_ptr<N, 2, 0>();
+    return scan_ptr<N, 1, 0>();
   switch (nt) {
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(14)
     CASE(16) CASE(20) CASE(24)
@@ -656,6 +660,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   B.ntp = (B.NT + 3) / 4 * 4;
   B.rl = (int)c->opt_rl;
   if (B.rl != 1 && B.rl != 2) B.rl = 1;
+  if (c->opt_mode != 2) B.rl = 1;  // two rows per lane: admission-first streaming kernel only
   APEX_TRY(build_plan(c, qs[0].start, qs[0].end, 32 * B.rl, nq, B.plan));
   B.plan_rows = nullptr;
   if (c->opt_mode >= 2 && c->opt_sorted && c->trace_cap == 0) {
@@ -2154,7 +2159,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "chunk") c->opt_chunk = std::max<int64_t>(1, v);
   else if (n == "tiles_per_slot") c->opt_tiles_per_slot = std::max<int64_t>(1, v);
   else if (n == "mode") {
-    if (v < 0 || v > 3) return set_err(APEX_EINVAL, "mode must be 0, 1, 2 or 3");
+    if (v < 0 || v > 3 || v == 1) return set_err(APEX_EINVAL, "mode must be 0, 2 or 3");
     c->opt_mode = v;
   } else if (n == "cb_admit") {
     if (v < 64 || v % 64 || v > 4096) return set_err(APEX_EINVAL, "cb_admit must be a multiple of 64 in [64, 4096]");

@@ -204,7 +204,7 @@ def _random_case(seed, n_rx=6, mu=3.0, sigma=0.7, n_tasks=4, c3=0.5, max_c=3):
 
 
 @pytest.mark.parametrize("seed", range(8))
-@pytest.mark.parametrize("opts", [{}, {"rl": 2, "mode": 2}, {"mode": 0}, {"mode": 1, "rl": 2, "cb": 8},
+@pytest.mark.parametrize("opts", [{}, {"rl": 2, "mode": 2}, {"mode": 0}, {"mode": 0, "cb": 8},
                                   {"mode": 0, "chunk_min": 1000, "tile_products": 64},
                                   {"chunk_min": 1000, "tile_products": 64, "cb_admit": 64},
                                   {"cap": 1024, "samples": 16}, {"refresh": 256, "samples": 64}, {"graph": 0},
