@@ -529,23 +529,37 @@ struct WorkCursor {
   unsigned cur = 0, lim = 0;
   unsigned nxt = 0;      // lane 0: base of the next chunk, fetched one chunk ahead
   bool primed = false;
+  unsigned sk = 0;       // static rounds taken
 };
 
 __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, unsigned long long live, unsigned lane,
                                           unsigned& q, unsigned& t) {
   const unsigned total = (L.tile_end - L.tile_begin) * (unsigned)L.nq;
-  if (!wc.primed) {
-    wc.primed = true;
-    if (lane == 0) wc.nxt = atomicAdd(L.work, (unsigned)L.chunk);
-  }
+  // the first 3/4 of the rounds are handed out statically (warp w takes items
+  // w, w + n_warps, ...: tiles are shuffled, so each warp's share is a
+  // representative sample); only the tail goes through the work counter, so
+  // the same-address atomics that balance the tail are a quarter as many
+  const unsigned nw = gridDim.x * (blockDim.x >> 5);
+  const unsigned wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned k_static = (total / nw) * 3u / 4u;
   for (;;) {
-    if (wc.cur >= wc.lim) {
-      const unsigned base = __shfl_sync(0xffffffffu, wc.nxt, 0);
-      if (lane == 0 && base < total) wc.nxt = atomicAdd(L.work, (unsigned)L.chunk);  // latency hidden by this chunk
-      wc.cur = base;
-      wc.lim = base + (unsigned)L.chunk;
+    unsigned item;
+    if (wc.sk < k_static) {
+      item = wc.sk * nw + wid;
+      ++wc.sk;
+    } else {
+      if (!wc.primed) {
+        wc.primed = true;
+        if (lane == 0) wc.nxt = k_static * nw + atomicAdd(L.work, (unsigned)L.chunk);
+      }
+      if (wc.cur >= wc.lim) {
+        const unsigned base = __shfl_sync(0xffffffffu, wc.nxt, 0);
+        if (lane == 0 && base < total) wc.nxt = k_static * nw + atomicAdd(L.work, (unsigned)L.chunk);  // one chunk ahead
+        wc.cur = base;
+        wc.lim = base + (unsigned)L.chunk;
+      }
+      item = wc.cur++;
     }
-    const unsigned item = wc.cur++;
     if (item >= total) return false;
     q = item % (unsigned)L.nq;
     t = L.tile_begin + item / (unsigned)L.nq;
@@ -1797,6 +1811,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   const float* __restrict__ values = L.values;
   const float* __restrict__ p16 = S.packed16;
   const int64_t n_pairs = L.n_pairs;
+  __shared__ unsigned s_adm[64];  // admitted products per query of the launch (statistics)
+  for (int q = threadIdx.x; q < 64; q += blockDim.x) s_adm[q] = 0;
+  __syncthreads();
   auto ld = [&](int task, int64_t pair) -> float {
     return P16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
   };
@@ -1996,8 +2013,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     }
     __syncwarp();
     const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
-    if (a && lane == 0) atomicAdd(&ctl->admitted, (unsigned long long)a);
+    if (a && lane == 0) atomicAdd(&s_adm[q_cur], a);  // per CTA; flushed once at the end
   }
+  __syncthreads();
+  for (int q = threadIdx.x; q < L.nq; q += blockDim.x)
+    if (s_adm[q]) atomicAdd(&L.queries[q].ctl->admitted, (unsigned long long)s_adm[q]);
 }
 
 // ---------------------------------------------------------------------------
