@@ -535,13 +535,12 @@ struct WorkCursor {
 __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, unsigned long long live, unsigned lane,
                                           unsigned& q, unsigned& t) {
   const unsigned total = (L.tile_end - L.tile_begin) * (unsigned)L.nq;
-  // the first 3/4 of the rounds are handed out statically (warp w takes items
-  // w, w + n_warps, ...: tiles are shuffled, so each warp's share is a
-  // representative sample); only the tail goes through the work counter, so
-  // the same-address atomics that balance the tail are a quarter as many
+  // every item through the work counter (a static share of the rounds was
+  // slower: item costs vary too much, profiles/r2_ab_static_items_rejected.log);
+  // k_static stays as the hook for a static prefix
   const unsigned nw = gridDim.x * (blockDim.x >> 5);
   const unsigned wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const unsigned k_static = (total / nw) * 3u / 4u;
+  const unsigned k_static = 0;
   for (;;) {
     unsigned item;
     if (wc.sk < k_static) {
