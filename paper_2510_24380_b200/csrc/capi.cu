@@ -171,6 +171,8 @@ struct Batch {
   bool finalize = false;
   bool copy_out = false;       // result rows D2H inside the pass (synchronous apex_query)
   bool no_full = false;        // this signature needed no full-predicate kernel last time: skip its launches
+  std::vector<int> cset_leader;  // shared constraint sets (sorted-column pre-pass): a query of each
+  int64_t cset_tests = 0;        // pre-pass threshold rows (sum of the sets' constraint tests)
   bool small_only = false;     // every query of this signature's last run fit the small finalize: skip the
                                // large-path launches (select, chunk sort, merge rank); re-run if one does not
   uint64_t key0 = 0;           // signature before no_full (history key)
@@ -191,6 +193,8 @@ struct apex_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;           // second stream: the corner seed runs beside the sample seed
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t side2 = nullptr;          // third stream: the sorted-column constraint pre-pass
+  cudaEvent_t fork2_ev = nullptr, join2_ev = nullptr;
   bool own_stream = false;
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
@@ -212,6 +216,7 @@ struct apex_ctx {
   bool corners_ok = false;
   DBuf d_sorted_x, d_sorted_col;         // per task: each reaction's last R-group sorted ascending (value, column)
   DBuf d_quant;                          // per task, reaction: kQuant + 1 evenly spaced values of the sorted column
+  DBuf d_cthr, d_cqc, d_cbest;           // sorted-column constraint pre-pass rows (shared constraint sets)
   DBuf d_packed16;                       // [n_pairs][16] pair-major copy of the table (sorted-column kernel)
   bool packed16_ok = false;
   int n_tasks = 0;
@@ -259,6 +264,8 @@ struct apex_ctx {
   int64_t opt_pre_rows = 2;         // K1 form: 2 = TMA bulk ring (11 x 64), 1 = row-parallel, 0 = smem tiles
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
+  int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
+                                    // (1: forked after the control init, 2: at the pass start, 0: off)
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_packed16 = 1;         // sorted-column kernel reads the pair-major table copy
@@ -746,6 +753,40 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
     Q.out_rx = reinterpret_cast<int32_t*>(o + (16 + 8 * (size_t)q.n_constraints) * kk);
     Q.out_dig = reinterpret_cast<int32_t*>(o + (20 + 8 * (size_t)q.n_constraints) * kk);
   }
+  // constraint sets shared by several queries: the sorted-column kernel
+  // reads their per-row thresholds and best range from a pre-pass
+  B.cset_leader.clear();
+  B.cset_tests = 0;
+  for (int i = 0; i < nq; ++i) hq[i].cset = -1;
+  if (B.plan_rows && c->opt_cpre) {
+    auto same = [&](int a, int b) {
+      const QTests &A = B.tests[a], &Bt = B.tests[b];
+      if (A.nt != Bt.nt) return false;
+      for (int t = 1; t < A.nt; ++t)
+        if (A.task[t] != Bt.task[t] || A.lower[t] != Bt.lower[t] || A.beta[t] != Bt.beta[t]) return false;
+      return true;
+    };
+    for (int i = 0; i < nq; ++i) {
+      if (hq[i].cset >= 0 || B.tests[i].nt < 2) continue;
+      int members = 0;
+      for (int j = i + 1; j < nq; ++j) members += (hq[j].cset < 0 && same(i, j)) ? 1 : 0;
+      if (!members) continue;
+      const int id = (int)B.cset_leader.size();
+      B.cset_leader.push_back(i);
+      for (int j = i; j < nq; ++j)
+        if (j == i || (hq[j].cset < 0 && same(i, j))) {
+          hq[j].cset = id;
+          hq[j].cset_off = (int32_t)B.cset_tests;
+        }
+      B.cset_tests += B.tests[i].nt - 1;
+    }
+    if (!B.cset_leader.empty()) {
+      const int64_t rows_pad = (int64_t)B.plan_rows->tiles.size() * 32;
+      APEX_TRY(c->d_cthr.ensure((size_t)std::max<int64_t>(B.cset_tests * rows_pad, 1) * sizeof(float)));
+      APEX_TRY(c->d_cqc.ensure((size_t)std::max<int64_t>(B.cset_tests * rows_pad, 1)));
+      APEX_TRY(c->d_cbest.ensure((size_t)std::max<int64_t>((int64_t)B.cset_leader.size() * rows_pad, 1) * 16));
+    }
+  }
   // upload the descriptors only when they changed (pinned staging is reused:
   // wait for the previous copy out of it first)
   const size_t bytes = nq * sizeof(ScanQuery);
@@ -853,10 +894,62 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   const bool sorted_all = c->opt_mode == 3 && B.plan_rows;
   const bool full = c->opt_mode != 2 && !B.no_full;
   const int autok = (c->opt_mode == 3 && !tau0) ? (B.no_full ? 3 : sorted_all ? 2 : 1) : 0;
+  // sorted-column constraint pre-pass (shared constraint sets), on a third
+  // stream beside the histogram clear, control init and seed kernels; joined
+  // before the enumeration
+  const bool sorted_go = admit && B.plan_rows &&
+                         !(span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && plan->tiles.size() > 1);
+  const bool cpre = sorted_go && !B.cset_leader.empty();
+  auto launch_cpre = [&]() -> int {
+    APEX_CU(cudaEventRecord(c->fork2_ev, s));
+    APEX_CU(cudaStreamWaitEvent(c->side2, c->fork2_ev, 0));
+    ConsPre P{};
+    P.queries = dq;
+    P.tiles = B.plan_rows->d_tiles.as<Tile>();
+    P.n_tiles = (unsigned)B.plan_rows->tiles.size();
+    P.rx = c->d_rx.as<DevReaction>();
+    P.values = c->d_values.as<float>();
+    P.p16 = (c->packed16_ok && c->opt_packed16) ? c->d_packed16.as<float>() : nullptr;
+    P.n_pairs = c->n_pairs;
+    P.sx = c->d_sorted_x.as<float>();
+    P.quant = c->d_quant.as<float>();
+    P.pcols = std::max<int64_t>(c->pcols, 4);
+    P.n_rx = (int)c->rx.size();
+    P.cthr = c->d_cthr.as<float>();
+    P.cbest = c->d_cbest.as<int4>();
+    P.rows_pad = (int64_t)P.n_tiles * 32;
+    P.cqc = c->d_cqc.as<unsigned char>();
+    // A: (tile, test) threshold + quantile count items
+    std::vector<std::pair<int, int>> tests;
+    for (int ld : B.cset_leader)
+      for (int i = 1; i < B.tests[ld].nt; ++i) tests.push_back({ld, i});
+    for (size_t s0 = 0; s0 < tests.size(); s0 += kConsPreItems) {
+      P.n = (int)std::min<size_t>(kConsPreItems, tests.size() - s0);
+      for (int j = 0; j < P.n; ++j) {
+        P.q[j] = tests[s0 + j].first;
+        P.ti[j] = (unsigned char)tests[s0 + j].second;
+      }
+      const int64_t items = (int64_t)P.n_tiles * P.n;
+      cons_thr_kernel<<<(unsigned)((items + 7) / 8), 256, 0, c->side2>>>(P);
+      ++st.launches;
+    }
+    // B: (tile, set) choice of the most selective test + its exact range
+    for (size_t s0 = 0; s0 < B.cset_leader.size(); s0 += kConsPreItems) {
+      P.n = (int)std::min<size_t>(kConsPreItems, B.cset_leader.size() - s0);
+      for (int j = 0; j < P.n; ++j) P.q[j] = B.cset_leader[s0 + j];
+      const int64_t items = (int64_t)P.n_tiles * P.n;
+      cons_best_kernel<<<(unsigned)((items + 7) / 8), 256, 0, c->side2>>>(P);
+      ++st.launches;
+    }
+    APEX_CU(cudaEventRecord(c->join2_ev, c->side2));
+    return APEX_OK;
+  };
+  if (cpre && c->opt_cpre == 2) APEX_TRY(launch_cpre());
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
   ++st.launches;
+  if (cpre && c->opt_cpre != 2) APEX_TRY(launch_cpre());
   // K2 pack of the streamed objective column
   if (admit && !(B.plan_rows && span < (uint64_t)c->opt_chunk_min)) {
     // (the sorted-column kernel reads the table's sorted lists, not a packed column)
@@ -936,6 +1029,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
     ++st.launches;
   }
   APEX_CU(stage_mark(c, 2, s));
+  if (cpre) APEX_CU(cudaStreamWaitEvent(s, c->join2_ev, 0));
   // K3 enumeration: chunks x test classes
   const int cb = (int)c->opt_cb;
   const size_t n_tiles = plan->tiles.size();
@@ -982,6 +1076,9 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
         SL.pcols = std::max<int64_t>(c->pcols, 4);
         SL.quant = c->d_quant.as<float>();
         SL.n_rx = (int)c->rx.size();
+        SL.cthr = c->d_cthr.as<float>();
+        SL.cbest = c->d_cbest.as<int4>();
+        SL.rows_pad = (int64_t)pr_->tiles.size() * 32;
         for (int q0 = 0; q0 < nq; q0 += 64) {
           const int nql = std::min(64, nq - q0);
           ScanLaunch La = L;
@@ -1623,6 +1720,14 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
   cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->fork2_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->join2_ev, cudaEventDisableTiming);
+  {
+    int lo = 0, hi = 0;  // the pre-pass stream at the highest priority: its rows gate the enumeration
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    (void)lo;
+    cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, hi);
+  }
   *out = c;
   return APEX_OK;
 }
@@ -1666,6 +1771,9 @@ void apex_ctx_destroy(apex_ctx* c) {
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->fork2_ev) cudaEventDestroy(c->fork2_ev);
+  if (c->join2_ev) cudaEventDestroy(c->join2_ev);
+  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -2145,6 +2253,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "vote64") c->opt_vote64 = v;
   else if (n == "dense") c->opt_dense = v;
   else if (n == "sorted") c->opt_sorted = v;
+  else if (n == "cpre") c->opt_cpre = v;
   else if (n == "trace") {
     // records of the admission scan's per-item trace (0: off); debug only
     c->trace_cap = std::max<int64_t>(0, std::min<int64_t>(v, 1ll << 26));

@@ -156,8 +156,8 @@ struct ScanQuery {
   int32_t obj_task;
   int32_t n_cons;                 // constraints (materialization order)
   int32_t slot;                   // position of the query in the caller's array
-  int32_t oc;                     // objective-column index within its multi-query group
-  int32_t _pad3;
+  int32_t cset;                   // sorted-column kernel: shared constraint set (pre-pass rows), -1: derived inline
+  int32_t cset_off;               // its first test's row block in the pre-pass threshold array
   int32_t test_task[kMaxTests];
   int32_t test_lower[kMaxTests];  // 1: lower-bound test (y = -x), 0: upper (y = x)
   double test_beta[kMaxTests];    // bound (ignored for test 0: derived from tau)

@@ -1635,6 +1635,9 @@ struct SortedLaunch {
   int64_t pcols;
   const float* quant;     // [task][n_rx][kQuant + 1]: evenly spaced values of each sorted column
   int n_rx;
+  const float* cthr;      // pre-pass: [cset_off + test - 1][rows_pad] constraint thresholds per row
+  const int4* cbest;      // pre-pass: [cset][rows_pad] (best test, its quantile count, range start, count)
+  int64_t rows_pad;       // row slots: 32 per row tile of the plan
 };
 
 // first index i in [0, n) with !(xs[i] <= t) (n if none); xs ascending
@@ -1792,6 +1795,102 @@ __device__ __forceinline__ void exact_range(const float* __restrict__ xs, int n,
   }
 }
 
+// contribution of task at pair row: from the pair-major copy when present
+// (one 64-byte line per pair), else the task-major table
+__device__ __forceinline__ float tval(const float* __restrict__ values, const float* __restrict__ p16, int64_t n_pairs,
+                                      int task, int64_t pair) {
+  return p16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
+}
+
+// Constraint pre-pass of the sorted-column kernel.  A constraint set shared
+// by several queries of the batch (the objectives of one property preset)
+// gives every row the same exact constraint thresholds, quantile counts and
+// most selective constraint range whichever query scans it: they are derived
+// once per (row tile, set) here — on a stream beside the seed kernels, whose
+// time it hides under — and the scan items of those queries read them.
+// Two short kernels, so the dependent chains stay one test long: (A) one warp
+// per (row tile, test): the exact threshold and its quantile count; (B) one
+// warp per (row tile, set): the most selective test and its exact range.
+constexpr int kConsPreItems = 384;  // (set, test) pairs per launch of A, sets per launch of B
+struct ConsPre {
+  const ScanQuery* queries;  // whole batch
+  const Tile* tiles;         // row tiles of the plan
+  unsigned n_tiles;
+  const DevReaction* rx;
+  const float* values;
+  const float* p16;
+  int64_t n_pairs;
+  const float* sx;
+  const float* quant;
+  int64_t pcols;
+  int n_rx;
+  float* cthr;               // [cset_off + i - 1][rows_pad]
+  unsigned char* cqc;        // same layout: quantile counts
+  int4* cbest;               // [cset][rows_pad]
+  int64_t rows_pad;
+  int n;                     // A: (query, test) pairs; B: sets (leader queries)
+  int q[kConsPreItems];      // A: a query of the test's set / B: a query of each set
+  unsigned char ti[kConsPreItems];  // A: test index (1..nt-1)
+};
+
+__global__ void __launch_bounds__(256) cons_thr_kernel(const __grid_constant__ ConsPre P) {
+  const unsigned lane = lane_id();
+  const unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned t = item / (unsigned)P.n, k = item % (unsigned)P.n;
+  if (t >= P.n_tiles) return;
+  const ScanQuery& Q = P.queries[P.q[k]];
+  const int i = P.ti[k];
+  const Tile T = P.tiles[t];
+  const DevReaction& R = P.rx[T.rx];
+  const int c = R.c;
+  const uint64_t row = T.row0 + (lane < T.nrows ? lane : 0u);
+  int64_t pr[kMaxRg - 1];
+  decode_prefix(R, c, row, pr);
+  const int task = Q.test_task[i];
+  double p = c > 1 ? (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]) : 0.0;
+#pragma unroll
+  for (int j = 1; j < kMaxRg - 1; ++j)
+    if (j < c - 1) p = __dadd_rn(p, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
+  const bool lower = Q.test_lower[i] != 0;
+  const float th = lower ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
+                         : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
+  const int qc = th == th ? quant_count(P.quant + ((int64_t)task * P.n_rx + T.rx) * (kQuant + 1), lower,
+                                        lower ? -th : th)
+                          : 0;
+  const int64_t o = (int64_t)(Q.cset_off + i - 1) * P.rows_pad + (int64_t)t * 32 + lane;
+  P.cthr[o] = th;
+  P.cqc[o] = (unsigned char)qc;
+}
+
+__global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ ConsPre P) {
+  const unsigned lane = lane_id();
+  const unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned t = item / (unsigned)P.n, si = item % (unsigned)P.n;
+  if (t >= P.n_tiles) return;
+  const ScanQuery& Q = P.queries[P.q[si]];
+  const Tile T = P.tiles[t];
+  const DevReaction& R = P.rx[T.rx];
+  const int nt = Q.nt;
+  const bool valid = lane < T.nrows;
+  const int64_t slot = (int64_t)t * 32 + lane;
+  int best = 0, best_q = kQuant + 2;
+  for (int i = 1; i < nt; ++i) {  // lowest test index among the smallest counts
+    const int qc = P.cqc[(int64_t)(Q.cset_off + i - 1) * P.rows_pad + slot];
+    if (qc < best_q) {
+      best_q = qc;
+      best = i;
+    }
+  }
+  int start = 0, cnt = 0;
+  if (valid && best != 0 && best_q > 0) {
+    const float th = P.cthr[(int64_t)(Q.cset_off + best - 1) * P.rows_pad + slot];
+    const bool lw = Q.test_lower[best] != 0;
+    exact_range(P.sx + (int64_t)Q.test_task[best] * P.pcols + R.pcol_off, (int)R.size[R.c - 1], lw, lw ? -th : th,
+                best_q, start, cnt);
+  }
+  P.cbest[(int64_t)Q.cset * P.rows_pad + slot] = make_int4(best, valid ? best_q : kQuant + 2, start, cnt);
+}
+
 #ifndef APEX_SORTED_MINB
 #define APEX_SORTED_MINB 4
 #endif
@@ -1826,7 +1925,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
   }
   while (have) {
-    const unsigned q_cur = qi;
+    const unsigned q_cur = qi, t_cur = t;
     const Tile T = T_n;
     const unsigned long long tau = tau_n;
     have = next_item(L, wc, live, lane, qi, t);
@@ -1880,8 +1979,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       } else {
         const float* q = qbase + Q.test_task[0] * qstride;
         best_q = quant_count(q, maximize != 0, maximize ? -th0 : th0);
-        const int64_t base0 = (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
-        exact_range(S.sx + base0, n_last, maximize != 0, maximize ? -th0 : th0, best_q, start, cnt);
       }
     }
     bool cons_ready = false;
@@ -1928,18 +2025,40 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       }
       cons_ready = true;
     };
-    if (valid && best_q > 2 && nt > 1) constraint_thresholds(true);
-    // exact passing range of a constraint that won (the objective's is known),
-    // searched only inside the quantile bracket its count identifies
-    if (valid && best != 0) {
-      start = 0;
-      cnt = 0;
-      if (best_q > 0) {
-        const float th = sthr[best * 32 + lane];
-        const bool lw = Q.test_lower[best] != 0;
-        const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
-        exact_range(S.sx + base, n_last, lw, lw ? -th : th, best_q, start, cnt);
+    if (Q.cset >= 0) {
+      // shared constraint set: the pre-pass rows (thresholds, most selective
+      // constraint and its exact range)
+      const int64_t slot = (int64_t)t_cur * 32 + lane;
+      for (int i = 1; i < nt; ++i) sthr[i * 32 + lane] = __ldg(S.cthr + (int64_t)(Q.cset_off + i - 1) * S.rows_pad + slot);
+      cons_ready = true;
+      if (valid && best_q > 2 && nt > 1) {
+        const int4 bc = __ldg(S.cbest + (int64_t)Q.cset * S.rows_pad + slot);
+        if (bc.y < best_q) {
+          best = bc.x;
+          best_q = bc.y;
+          start = bc.z;
+          cnt = bc.w;
+        }
       }
+    } else {
+      if (valid && best_q > 2 && nt > 1) constraint_thresholds(true);
+      // exact passing range of a constraint that won, searched only inside
+      // the quantile bracket its count identifies
+      if (valid && best != 0) {
+        start = 0;
+        cnt = 0;
+        if (best_q > 0) {
+          const float th = sthr[best * 32 + lane];
+          const bool lw = Q.test_lower[best] != 0;
+          const int64_t base = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off;
+          exact_range(S.sx + base, n_last, lw, lw ? -th : th, best_q, start, cnt);
+        }
+      }
+    }
+    // the objective's exact range when it is the most selective test
+    if (valid && best == 0 && th0 == th0 && th0 != __int_as_float(0x7f800000)) {
+      const int64_t base0 = (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
+      exact_range(S.sx + base0, n_last, maximize != 0, maximize ? -th0 : th0, best_q, start, cnt);
     }
     if (cnt > 0 && !cons_ready) constraint_thresholds(false);
     // flatten the warp's admitted (row, sorted position) pairs so every lane
@@ -2024,12 +2143,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
 // equal cell of [start, end), jittered inside the cell).  Feasible samples are
 // counted in seed_hist by key >> 48; the k-th best sampled key bin is a valid
 // admission threshold because the samples are distinct real products.
-// contribution of task at pair row: from the pair-major copy when present
-// (one 64-byte line per pair), else the task-major table
-__device__ __forceinline__ float tval(const float* __restrict__ values, const float* __restrict__ p16, int64_t n_pairs,
-                                      int task, int64_t pair) {
-  return p16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
-}
 
 struct SampleLaunch {
   const ScanQuery* queries;
