@@ -505,7 +505,6 @@ def run_single(args):
 
     def step_e2e():
         r, st = ctx.run_views(prepared)
-        acc["scan"].append(st["scan_kernel_ms"])
         acc["h2d"] += st["h2d_bytes"]
         acc["d2h"] += st["d2h_bytes"]
         return r
@@ -513,6 +512,20 @@ def run_single(args):
     e2e_ms, e2e_wall, res = timed_loop(stream, args.steps, step_e2e, flush)
     ctx.set_option("force_upload", 0)
     e2e_value = products / (e2e_ms * 1e-3)
+
+    # per-stage device times and the enumeration kernel's own time: a separate
+    # loop with the stage events on (option "stages": each event is a node on
+    # the pass's critical path, so the timed loops above run without them)
+    ctx.set_option("stages", 1)
+    st_stages = []
+    for _ in range(max(5, min(args.steps, 20))):
+        flush.zero_()
+        _, st_k = ctx.run_views(prepared)
+        acc["scan"].append(st_k["scan_kernel_ms"])
+        st_stages.append(st_k)
+    st_dev = {k_: statistics.median(x[k_] for x in st_stages)
+              for k_ in ("pack_ms", "seed_ms", "scan_ms", "select_ms", "finalize_ms", "d2h_ms", "total_ms",
+                         "scan_kernel_ms")} | {"candidates": st_stages[-1]["candidates"]}
 
     # Rooflines: F = algorithmic FP32 ops per product of the
     # batched pass; peak P32 = SMs x 128 FP32 lanes x the SM clock sampled
@@ -560,6 +573,8 @@ def run_single(args):
                     "kernel_ms": fm, "F_per_product": F, "products": scanned,
                     "peak_basis": f"{sm_count} SMs x 128 FP32 lanes x {clk_mhz:.0f} MHz (median SM clock under load)"}
 
+    ctx.set_option("stages", 0)
+
     # the SURVEY's roofline reference point: the C4 query over the ~5e9-product
     # library (F = 15 per product), full-predicate pass (mode 0) and the
     # default sorted-column pass, on a second context with that table resident
@@ -569,6 +584,7 @@ def run_single(args):
             c4shape, c4q = workload("c4", 1)
             u4, w4, b4 = build_model(c4shape)
             ctx4 = _native.DeviceContext(0, stream.cuda_stream)
+            ctx4.set_option("stages", 1)  # scan kernel times (stage events)
             ctx4.load_library(c4shape.sizes, c4shape.pair_off, c4shape.g_offsets(), c4shape.n_pairs)
             ctx4.load_cache(u4, w4, b4, want_values=False)
             del u4

@@ -264,6 +264,7 @@ struct apex_ctx {
   int64_t opt_pre_rows = 2;         // K1 form: 2 = TMA bulk ring (11 x 64), 1 = row-parallel, 0 = smem tiles
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
+  int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
@@ -809,6 +810,9 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
 // Stage timing event; inside a stream capture it is recorded as an external
 // event-record node so the graph replay still timestamps it.
 cudaError_t stage_mark(apex_ctx* c, int e, cudaStream_t s) {
+  // stage events are diagnostics (option "stages"): each recorded event is a
+  // node on the pass's critical path (a few microseconds per node in a graph)
+  if (!c->opt_stages) return cudaSuccess;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   if (cs == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(c->ev[e], s, cudaEventRecordExternal);
@@ -947,7 +951,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   if (cpre && c->opt_cpre == 2) APEX_TRY(launch_cpre());
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
-                                      (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u);
+                                      (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u, c->d_work.as<unsigned>());
   ++st.launches;
   if (cpre && c->opt_cpre != 2) APEX_TRY(launch_cpre());
   // K2 pack of the streamed objective column
@@ -1044,7 +1048,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   size_t tb = 0;
   st.scan_kernel_ms = 0;
   int wi = 0;  // flattened-work counter index (one per scan launch)
-  APEX_CU(cudaMemsetAsync(c->d_work.p, 0, 64 * sizeof(unsigned), s));
+  // (the flattened-work counters d_work were zeroed by init_ctl_kernel)
   for (size_t ci = 0; ci < bounds.size(); ++ci) {
     const size_t te = bounds[ci];
     if (te > tb) {
@@ -1299,8 +1303,9 @@ int check_batch(apex_ctx* c) {
   }
   // (stage times are informational: never fail the query on them)
   for (int e = 0; e < 5; ++e)
-    if (cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]) != cudaSuccess) B.st.ms[e] = 0.f;
-  if (cudaEventElapsedTime(&B.st.scan_kernel_ms, c->ev[6], c->ev[7]) != cudaSuccess) B.st.scan_kernel_ms = 0.f;
+    if (!c->opt_stages || cudaEventElapsedTime(&B.st.ms[e], c->ev[e], c->ev[e + 1]) != cudaSuccess) B.st.ms[e] = 0.f;
+  if (!c->opt_stages || cudaEventElapsedTime(&B.st.scan_kernel_ms, c->ev[6], c->ev[7]) != cudaSuccess)
+    B.st.scan_kernel_ms = 0.f;
   cudaGetLastError();
   return APEX_OK;
 }
@@ -1638,7 +1643,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u);
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u, nullptr);
   if (n_in > 0) {
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_in + 255) / 256, 4 * c->sm_count / std::max(nq, 1) + 1));
     merge_load_kernel<<<dim3(gx, nq), 256, 0, s>>>(dq, entries, n_src, nq, (unsigned long long)stride, srcs);
@@ -2254,6 +2259,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "dense") c->opt_dense = v;
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
+  else if (n == "stages") c->opt_stages = v;
   else if (n == "trace") {
     // records of the admission scan's per-item trace (0: off); debug only
     c->trace_cap = std::max<int64_t>(0, std::min<int64_t>(v, 1ll << 26));

@@ -374,9 +374,11 @@ __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n,
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
 __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPreset* __restrict__ pre,
-                                unsigned use_full) {
+                                unsigned use_full, unsigned* work) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
+  // the scan launches' flattened-work counters (replaces a memset node)
+  if (work && blockIdx.x == 0 && threadIdx.x < 64) work[threadIdx.x] = 0u;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
   // (the candidate / seed histograms are zeroed by one memset per batch)
   if (threadIdx.x == 0) {

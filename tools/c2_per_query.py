@@ -30,6 +30,7 @@ def med(ctx, qs, reps=7):
 shape = synth.make_shape(synth.SHAPES["c1"])
 u, w, b = synth.build_model(shape)
 ctx = _native.DeviceContext(0)
+ctx.set_option("stages", 1)  # per-stage events (diagnostics)
 # A/B knobs: APEX_OPTS="name=value,name=value" (apex_set_option)
 for kv in filter(None, os.environ.get("APEX_OPTS", "").split(",")):
     name, val = kv.split("=")

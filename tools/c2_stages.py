@@ -21,6 +21,7 @@ from paper_2510_24380_b200 import _native, synth  # noqa: E402
 shape = synth.make_shape(synth.SHAPES["c1"])
 u, w, b = synth.build_model(shape)
 ctx = _native.DeviceContext(0)
+ctx.set_option("stages", 1)  # per-stage events (diagnostics)
 for kv in filter(None, os.environ.get("APEX_OPTS", "").split(",")):
     name, val = kv.split("=")
     ctx.set_option(name, int(val))

@@ -32,6 +32,7 @@ def main():
     w, b = synth.random_heads(seed=1)
     w, b = synth.calibrate_heads(shape, u, w, b, n_sample=20000, seed=1)
     ctx = _native.DeviceContext(0)
+    ctx.set_option("stages", 1)  # per-stage events (diagnostics)
     ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
     ctx.load_cache(u, w, b, want_values=False)
     for k_, v in opts.items():

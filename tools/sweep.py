@@ -27,6 +27,7 @@ def main():
     w, b = synth.random_heads(seed=1)
     w, b = synth.calibrate_heads(shape, u, w, b, n_sample=20000, seed=1)
     ctx = _native.DeviceContext(0)
+    ctx.set_option("stages", 1)  # per-stage events (diagnostics)
     ctx.load_library(shape.sizes, shape.pair_off, shape.g_offsets(), shape.n_pairs)
     ctx.load_cache(u, w, b, want_values=False)
     qs = {"c1": [synth.c1_query()], "c2": synth.c2_queries(), "c3": [synth.c3_query()],
