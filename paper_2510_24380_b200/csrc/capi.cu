@@ -264,6 +264,7 @@ struct apex_ctx {
   int64_t opt_pre_rows = 2;         // K1 form: 2 = TMA bulk ring (11 x 64), 1 = row-parallel, 0 = smem tiles
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
+  int64_t opt_fin_bucket = 8;       // bucketed small finalize: max CTAs per query (0: one-CTA finalize_small_kernel)
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -297,6 +298,7 @@ struct apex_ctx {
   std::vector<std::pair<std::pair<const void*, size_t>, int>> occ_cache;
   std::vector<std::pair<const void*, size_t>> attr_cache;
   bool attr_small = false;
+  bool attr_bucket = false;
   int occ_sel = 0;
   // a context is driven by one thread at a time: every C-ABI call on it holds
   // this lock (calls on different contexts run concurrently)
@@ -841,8 +843,20 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
                                    (int)smem_small));
       c->attr_small = true;
     }
-    // (materialization runs after, for every query, in materialize_kernel)
-    finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, 0, compute_bound ? 1 : 0);
+    if (compute_bound && c->opt_fin_bucket) {
+      // bucketed: ns CTAs per query (one wave), rows materialized inside
+      const size_t smem_bucket = fin_bucket_smem();
+      if (!c->attr_bucket) {
+        APEX_CU(cudaFuncSetAttribute((const void*)finalize_bucket_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bucket));
+        c->attr_bucket = true;
+      }
+      const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_fin_bucket, c->sm_count / std::max(nq, 1)));
+      finalize_bucket_kernel<<<dim3((unsigned)ns, (unsigned)nq), kFinThreads, smem_bucket, s>>>(M, finalize ? 1 : 0);
+    } else {
+      // (materialization runs after, for every query, in materialize_kernel)
+      finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, 0, compute_bound ? 1 : 0);
+    }
     ++st.launches;
   }
   if (!skip_large) {
@@ -867,8 +881,12 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
       merge_rank_kernel<<<dim3(ib, nq), 256, 0, s>>>(dq);
       st.launches += 2;
     }
-    materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
-    st.launches += 1;
+    // (queries the bucketed finalize materialized are skipped on the device;
+    // a signature whose queries all fit it needs no launch)
+    if (!(skip_large && compute_bound && c->opt_fin_bucket)) {
+      materialize_kernel<<<dim3((unsigned)((k_max + 127) / 128), nq), 128, 0, s>>>(M);
+      st.launches += 1;
+    }
   }
   return APEX_OK;
 }
@@ -2260,6 +2278,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "fin_bucket") c->opt_fin_bucket = std::max<int64_t>(0, v);
   else if (n == "trace") {
     // records of the admission scan's per-item trace (0: off); debug only
     c->trace_cap = std::max<int64_t>(0, std::min<int64_t>(v, 1ll << 26));

@@ -69,7 +69,7 @@ struct QCtl {
   unsigned int hist_shift;
   unsigned int use_full;          // 1: full-predicate kernel, 0: admission-first kernel
   unsigned int small_done;        // 1: finalize_small_kernel produced sel/sorted (large path skipped)
-  unsigned int _pad4;
+  unsigned int mat_done;          // 1: finalize_bucket_kernel materialized the rows (materialize_kernel skips)
   unsigned int active;            // participates in the current launch
   unsigned int tile_counter;      // scan work distribution
   unsigned int barrier;           // select grid barrier

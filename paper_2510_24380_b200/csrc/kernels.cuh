@@ -396,6 +396,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPrese
     c->stale = 0;
     c->use_full = use_full;
     c->small_done = 0;
+    c->mat_done = 0;
     c->seed_max = 0;
     c->admitted = 0;
     c->count = 0;
@@ -645,6 +646,32 @@ __device__ int kth_two_level(const unsigned int* __restrict__ fine, const unsign
     return cbin << 8;
   }
   if (count_ge) *count_ge = at;
+  return (cbin << 8) | fb;
+}
+
+// kth_two_level's search over preloaded coarse counts (vc, as load_bins256),
+// returning also the count of entries in bins strictly above the returned bin
+// (*above; the total when -1 is returned).  Used on a complete histogram
+// (after the enumeration), where both levels agree.
+__device__ int kth_two_level_above(const unsigned int* __restrict__ fine, const unsigned (&vc)[8],
+                                   unsigned long long k, unsigned long long* above_out) {
+  unsigned v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = vc[i];
+  unsigned long long above = 0;
+  const int cbin = kth_bins256(v, k, above, nullptr);
+  if (cbin < 0) {
+    *above_out = above;
+    return -1;
+  }
+  load_bins256(fine + (cbin << 8), v);
+  const unsigned long long above_c = above;
+  const int fb = kth_bins256(v, k, above, nullptr);
+  if (fb < 0) {
+    *above_out = above_c;
+    return cbin << 8;
+  }
+  *above_out = above;
   return (cbin << 8) | fb;
 }
 
@@ -2705,13 +2732,26 @@ struct MatLaunch {
   const double* biases;
 };
 
-__device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned long long i, unsigned long long g) {
+constexpr int kMatBatch = 6;  // tasks whose gathers a materialized row issues together
+// goff / rxs: the reactions' g offsets and descriptors (M.g_off / M.rx, or
+// shared-memory copies: the row's reaction search and decode then make no
+// global round trip)
+__device__ __forceinline__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned long long i,
+                                                unsigned long long g, const unsigned long long* goff = nullptr,
+                                                const DevReaction* rxs = nullptr) {
   int lo = 0, hi = M.n_rx;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(M.g_off + mid) <= g) lo = mid; else hi = mid;
+  if (goff) {
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (goff[mid] <= g) lo = mid; else hi = mid;
+    }
+  } else {
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(M.g_off + mid) <= g) lo = mid; else hi = mid;
+    }
   }
-  const DevReaction& R = M.rx[lo];
+  const DevReaction& R = rxs ? rxs[lo] : M.rx[lo];
   const int c = R.c;
   uint64_t rem = g - R.g_off;
   int64_t dig[kMaxRg], pr[kMaxRg];
@@ -2727,19 +2767,39 @@ __device__ void materialize_row(const MatLaunch& M, const ScanQuery& Q, unsigned
       rem = q;
     }
   }
-  // read-only (__ldg) gathers, so stores to the outputs do not order them
-  // zero_start: apex_score's acc = 0.0; acc += v_r order (differs from the
-  // scan's v0 + v1 + ... only in the sign of an all-zero sum)
-  auto sum = [&](int task, bool zero_start) {
-    const double v0 = (double)tval(M.values, M.p16, M.n_pairs, task, pr[0]);
-    double acc = zero_start ? __dadd_rn(0.0, v0) : v0;
+  // tasks in batches of kMatBatch (t = 0: the objective in the scan's
+  // v0 + v1 + ... order, t >= 1: constraint t - 1 in apex_score's
+  // acc = 0.0; acc += v_r order, which differs only in the sign of an all-zero
+  // sum): every gather of a batch is issued before any sum or store, so a row
+  // costs one round trip per batch rather than one per task
+  const int n_cons = Q.n_cons;
+  for (int t0 = 0; t0 <= n_cons; t0 += kMatBatch) {
+    float x[kMatBatch][kMaxRg];
+    double bias[kMatBatch];
 #pragma unroll
-    for (int j = 1; j < kMaxRg; ++j)
-      if (j < c) acc = __dadd_rn(acc, (double)tval(M.values, M.p16, M.n_pairs, task, pr[j]));
-    return __dadd_rn(acc, __ldg(M.biases + task));
-  };
-  Q.out_obj[i] = sum(Q.obj_task, false);
-  for (int ci = 0; ci < Q.n_cons; ++ci) Q.out_cons[i * Q.n_cons + ci] = sum(Q.cons_task[ci], true);
+    for (int u = 0; u < kMatBatch; ++u) {
+      const int t = t0 + u;
+      const int ci = min(max(t - 1, 0), max(n_cons - 1, 0));
+      const int task = t == 0 ? Q.obj_task : Q.cons_task[ci];
+#pragma unroll
+      for (int j = 0; j < kMaxRg; ++j)
+        x[u][j] = (t <= n_cons && j < c) ? tval(M.values, M.p16, M.n_pairs, task, pr[j]) : 0.0f;
+      bias[u] = t <= n_cons ? __ldg(M.biases + task) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kMatBatch; ++u) {
+      const int t = t0 + u;
+      if (t > n_cons) break;
+      const double v0 = (double)x[u][0];
+      double acc = t > 0 ? __dadd_rn(0.0, v0) : v0;
+#pragma unroll
+      for (int j = 1; j < kMaxRg; ++j)
+        if (j < c) acc = __dadd_rn(acc, (double)x[u][j]);
+      acc = __dadd_rn(acc, bias[u]);
+      if (t == 0) Q.out_obj[i] = acc;
+      else Q.out_cons[i * n_cons + t - 1] = acc;
+    }
+  }
   Q.out_g[i] = g;
   Q.out_rx[i] = lo;
 #pragma unroll
@@ -2751,11 +2811,72 @@ __global__ void materialize_kernel(const MatLaunch M) {
   // thread per row, the whole grid in parallel (a row is a chain of dependent
   // gathers, so rows spread over many SMs rather than one CTA per query)
   const ScanQuery& Q = M.queries[blockIdx.y];
-  if (!*(volatile unsigned int*)&Q.ctl->active) return;
+  if (!*(volatile unsigned int*)&Q.ctl->active || *(volatile unsigned int*)&Q.ctl->mat_done) return;
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   materialize_row(M, Q, i, Q.sorted[i].g);
+}
+
+// Final bound of a query (one warp, converged): the k-th best candidate
+// bin's lower edge and the count at/above it (tie mode: the tied key and every
+// admitted product), written to the control block (write = true) together
+// with the parameters of the exact re-run if the candidate buffer overflowed.
+// Returns the k-th best bin (-1: fewer than k candidates).
+__device__ int final_bound(const ScanQuery& Q, bool write, unsigned long long& s_bound, unsigned long long& s_valid) {
+  QCtl* ctl = Q.ctl;
+  unsigned long long cnt_ge = 0;
+  const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, &cnt_ge);
+  if (lane_id() == 0) {
+    const bool tie = ctl->tie_on != 0;
+    const unsigned long long base = ctl->hist_base;
+    const unsigned shift = ctl->hist_shift;
+    unsigned long long bound = B >= 0 ? bin_edge((unsigned)B, base, shift) : 0ull;
+    if (tie) {  // every admitted product has key >= K; the select orders them exactly
+      bound = ctl->tie_key;
+      cnt_ge = ctl->count;
+    }
+    s_bound = bound;
+    s_valid = cnt_ge;
+    if (write) {
+      ctl->bound_key = bound;
+      ctl->comp_count = cnt_ge;
+    }
+    // overflow (count > cap): parameters of the exact re-run (capi.cu
+    // check_batch).  Every step either narrows the key bins holding the
+    // k-th best by 16 bits, or — once that bin is one exact key K — bins
+    // the tied products by g and narrows the admitted g range by 16 bits,
+    // so the admitted set shrinks to at most k + one bin.
+    if (write && ctl->count > Q.cap && B >= 0) {
+      if (!tie) {
+        if (B == 65535) {  // the absorbing top bin: re-spread [edge, 2^64) over the bins
+          unsigned s2 = shift;
+          while (s2 < 63 && ((~0ull - bound) >> s2) >= 65535ull) ++s2;
+          ctl->nx_tau = bound;
+          ctl->nx_base = bound;
+          ctl->nx_shift = s2;
+        } else if (shift == 0) {  // bin B is the single key K = bound
+          ctl->nx_tau = bound;
+          ctl->nx_tie = 1;
+          ctl->nx_tie_enter = 1;
+        } else {
+          ctl->nx_tau = bound;
+          ctl->nx_base = bound;
+          ctl->nx_shift = shift >= 16 ? shift - 16 : 0u;
+        }
+      } else {
+        const unsigned gs = ctl->tie_gshift;
+        const unsigned long long glo = ctl->tie_gbase + ((unsigned long long)(65534 - min(B, 65534)) << gs);
+        const unsigned long long ghi = glo + (1ull << gs);
+        ctl->nx_tau = ctl->tie_key;
+        ctl->nx_tie = 1;
+        ctl->nx_gbase = glo;
+        ctl->nx_glimit = (ghi > glo && ghi < ctl->tie_glimit) ? ghi : ctl->tie_glimit;
+        ctl->nx_gshift = gs >= 16 ? gs - 16 : 0u;
+      }
+    }
+  }
+  return B;
 }
 
 // Small-candidate-set finalize (one 1024-thread CTA per query): when at most
@@ -2778,55 +2899,7 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
       s_valid = *(volatile unsigned long long*)&ctl->comp_count;
     }
   } else if (threadIdx.x < 32) {
-    unsigned long long cnt_ge = 0;
-    const int B = kth_two_level(Q.hist, Q.coarse, (unsigned long long)Q.k, &cnt_ge);
-    if (threadIdx.x == 0) {
-      const bool tie = ctl->tie_on != 0;
-      const unsigned long long base = ctl->hist_base;
-      const unsigned shift = ctl->hist_shift;
-      unsigned long long bound = B >= 0 ? bin_edge((unsigned)B, base, shift) : 0ull;
-      if (tie) {  // every admitted product has key >= K; the select orders them exactly
-        bound = ctl->tie_key;
-        cnt_ge = ctl->count;
-      }
-      ctl->bound_key = bound;
-      ctl->comp_count = cnt_ge;
-      s_bound = bound;
-      s_valid = cnt_ge;
-      // overflow (count > cap): parameters of the exact re-run (capi.cu
-      // check_batch).  Every step either narrows the key bins holding the
-      // k-th best by 16 bits, or — once that bin is one exact key K — bins
-      // the tied products by g and narrows the admitted g range by 16 bits,
-      // so the admitted set shrinks to at most k + one bin.
-      if (ctl->count > Q.cap && B >= 0) {
-        if (!tie) {
-          if (B == 65535) {  // the absorbing top bin: re-spread [edge, 2^64) over the bins
-            unsigned s2 = shift;
-            while (s2 < 63 && ((~0ull - bound) >> s2) >= 65535ull) ++s2;
-            ctl->nx_tau = bound;
-            ctl->nx_base = bound;
-            ctl->nx_shift = s2;
-          } else if (shift == 0) {  // bin B is the single key K = bound
-            ctl->nx_tau = bound;
-            ctl->nx_tie = 1;
-            ctl->nx_tie_enter = 1;
-          } else {
-            ctl->nx_tau = bound;
-            ctl->nx_base = bound;
-            ctl->nx_shift = shift >= 16 ? shift - 16 : 0u;
-          }
-        } else {
-          const unsigned gs = ctl->tie_gshift;
-          const unsigned long long glo = ctl->tie_gbase + ((unsigned long long)(65534 - min(B, 65534)) << gs);
-          const unsigned long long ghi = glo + (1ull << gs);
-          ctl->nx_tau = ctl->tie_key;
-          ctl->nx_tie = 1;
-          ctl->nx_gbase = glo;
-          ctl->nx_glimit = (ghi > glo && ghi < ctl->tie_glimit) ? ghi : ctl->tie_glimit;
-          ctl->nx_gshift = gs >= 16 ? gs - 16 : 0u;
-        }
-      }
-    }
+    final_bound(Q, true, s_bound, s_valid);
   }
   __syncthreads();
   const unsigned long long n_valid = s_valid;
@@ -2871,6 +2944,149 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
     ctl->sel_count = kk;
     ctl->small_done = 1;
     if (kk == (unsigned long long)Q.k && kk > 0 && es[kk - 1].key > ctl->tau_key) ctl->tau_key = es[kk - 1].key;
+  }
+}
+
+// Bucketed small finalize (grid: ns CTAs per query).  The candidate
+// histogram orders the bins like the entries (a better entry never has a lower
+// bin, in tie mode too), so the top-kk ranks split into ns contiguous runs of
+// bins: CTA j owns the bins (b_{j+1}, b_j], b_j = the bin of rank j*kk/ns
+// (b_0 = the top bin, b_ns = below the k-th best bin B), and its entries take
+// the ranks from count(bins > b_j) on.  Each CTA sorts only its own bins'
+// entries (bitonic, shared memory) and writes and materializes their rows:
+// the one-CTA-per-query sort + separate materialization become one short
+// kernel over ns x nq CTAs.  Same outputs as finalize_small_kernel (sel,
+// sorted best-first, sel_count, small_done, final tau); CTA 0 writes the bound
+// and the overflow re-run parameters.  Every per-thread chain is kept to few
+// global round trips (~300-500 cycles each on sm_100, tools/microbench/
+// latency.cu): the bound and both rank splits are searched by three warps at
+// once, the control fields, g offsets and reaction descriptors are staged by
+// the other warps meanwhile, the buffer is read kFinBatch entries per thread
+// per round trip, and a materialized row decodes from shared memory.
+constexpr int kFinThreads = 512;
+constexpr int kFinBatch = 8;     // buffer entries per thread in flight
+constexpr int kFinRx = 256;      // reactions whose descriptors + g offsets are staged in shared memory
+__host__ __device__ constexpr size_t fin_bucket_smem() {
+  return (size_t)kSmallSel * sizeof(Entry) + (size_t)kFinRx * sizeof(DevReaction) +
+         (size_t)(kFinRx + 1) * sizeof(unsigned long long);
+}
+
+__global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatLaunch M, int materialize) {
+  const ScanQuery& Q = M.queries[blockIdx.y];
+  QCtl* ctl = Q.ctl;
+  if (!*(volatile unsigned int*)&ctl->active) return;
+  const unsigned ns = gridDim.x, j = blockIdx.x;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  extern __shared__ __align__(16) unsigned char sm_e[];
+  Entry* es = reinterpret_cast<Entry*>(sm_e);
+  DevReaction* s_rx = reinterpret_cast<DevReaction*>(sm_e + (size_t)kSmallSel * sizeof(Entry));
+  unsigned long long* s_goff = reinterpret_cast<unsigned long long*>(s_rx + kFinRx);
+  __shared__ unsigned long long s_bound, s_valid, s_above[2], s_n, s_hbase;
+  __shared__ int s_bin[3];
+  __shared__ unsigned s_hshift, s_tie, cnt;
+  const bool stage_rx = materialize && M.n_rx <= kFinRx;
+  if (warp == 0) {
+    // the final bound (CTA 0 writes it and the re-run parameters)
+    const int B = final_bound(Q, j == 0, s_bound, s_valid);
+    if (lane == 0) s_bin[2] = B;  // bins below B hold no rank < kk
+  } else if (warp <= 2) {
+    // the rank-split bins b_j (warp 1) and b_{j+1} (warp 2) and the counts above them
+    const unsigned jj = j + (warp - 1);
+    if (jj == 0 || jj >= ns) {
+      if (lane == 0) {
+        s_bin[warp - 1] = jj == 0 ? 65535 : -2;  // -2: no lower split (down to B)
+        s_above[warp - 1] = 0;
+      }
+    } else {
+      unsigned v[8];
+      load_bins256(Q.coarse, v);
+      unsigned long long tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tot += v[i];
+      tot = __reduce_add_sync(0xffffffffu, (unsigned)tot);
+      const unsigned long long kk = min((unsigned long long)Q.k, tot);  // kk = min(k, total)
+      const unsigned long long target = (unsigned long long)jj * kk / ns + 1;
+      unsigned long long above = 0;
+      const int b = kk ? kth_two_level_above(Q.hist, v, target, &above) : -1;
+      if (lane == 0) {
+        s_bin[warp - 1] = b < 0 ? -1 : b;
+        s_above[warp - 1] = above;
+      }
+    }
+  } else {
+    if (threadIdx.x == 96) {
+      s_n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
+      s_hbase = *(volatile unsigned long long*)&ctl->hist_base;
+      s_hshift = *(volatile unsigned*)&ctl->hist_shift;
+      s_tie = *(volatile unsigned*)&ctl->tie_on;
+      cnt = 0;
+    }
+    if (stage_rx) {
+      const int words = (int)(M.n_rx * (sizeof(DevReaction) / 8));
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(M.rx);
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(s_rx);
+      for (int i = threadIdx.x - 96; i < words; i += blockDim.x - 96) dst[i] = __ldg(src + i);
+      for (int i = threadIdx.x - 96; i <= M.n_rx; i += blockDim.x - 96) s_goff[i] = __ldg(M.g_off + i);
+    }
+  }
+  __syncthreads();
+  const unsigned long long n_valid = s_valid;
+  if (n_valid > (unsigned long long)kSmallSel) return;  // large path
+  // this CTA's bins: (lo_excl, hi]
+  const int hi = s_bin[0];
+  const int lo_excl = s_bin[1] == -2 ? (s_bin[2] >= 0 ? s_bin[2] - 1 : -1) : s_bin[1];
+  const unsigned long long off = s_above[0];
+  const unsigned long long kk = min((unsigned long long)Q.k, n_valid);
+  if (j == 0 && threadIdx.x == 0) {
+    ctl->sel_count = kk;
+    ctl->small_done = 1;
+    ctl->mat_done = materialize ? 1u : 0u;
+  }
+  if (hi < 0 || hi <= lo_excl || off >= kk) return;
+  const unsigned long long n = s_n, hbase = s_hbase;
+  const unsigned hshift = s_hshift;
+  const bool tie = s_tie != 0;
+  for (unsigned long long base = threadIdx.x & ~31u; base < n; base += (unsigned long long)kFinBatch * blockDim.x) {
+    Entry e[kFinBatch];
+#pragma unroll
+    for (int u = 0; u < kFinBatch; ++u) {
+      const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
+      if (i < n) e[u] = Q.buf[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kFinBatch; ++u) {
+      const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
+      bool keep = false;
+      if (i < n) {
+        const int b = (int)(tie ? cand_bin(ctl, e[u].key, e[u].g, hbase, hshift) : hist_bin(e[u].key, hbase, hshift));
+        keep = b <= hi && b > lo_excl;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (!m) continue;
+      unsigned pos = 0;
+      if (lane == 0) pos = atomicAdd(&cnt, (unsigned)__popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+      if (keep && pos < (unsigned)kSmallSel) es[pos] = e[u];
+    }
+  }
+  __syncthreads();
+  const unsigned m = min(cnt, (unsigned)kSmallSel);
+  unsigned P = 32;  // at least one warp's worth: sorted by warp shuffles
+  while (P < m) P <<= 1;
+  for (unsigned i = m + threadIdx.x; i < P; i += blockDim.x) {
+    es[i].key = 0;
+    es[i].g = ~0ull;
+  }
+  __syncthreads();
+  bitonic_best_first(es, P);
+  const unsigned n_out = (unsigned)min((unsigned long long)m, kk - off);
+  for (unsigned i = threadIdx.x; i < n_out; i += blockDim.x) {
+    const unsigned long long r = off + i;
+    const Entry e = es[i];
+    Q.sel[r] = e;
+    Q.sorted[r] = e;
+    if (materialize) materialize_row(M, Q, r, e.g, stage_rx ? s_goff : nullptr, stage_rx ? s_rx : nullptr);
+    if (r == kk - 1 && kk == (unsigned long long)Q.k && e.key > ctl->tau_key) ctl->tau_key = e.key;
   }
 }
 
