@@ -123,4 +123,27 @@ __global__ void bind_pack16_kernel(const float* __restrict__ values, int64_t n_p
   }
 }
 
+// Row-prefix table (sorted-column and pre-pass kernels): for every row of
+// every reaction (a fixed assignment of its first c-1 R-groups) and every
+// task, the fp64 prefix sum of those R-groups' contributions in the scan's
+// order (v0 + v1 + ..., engine.py:210-222 without the last R-group and the
+// bias): rowp[task][row_off + row].  grid.y = reaction, grid-stride rows.
+__global__ void bind_rowp_kernel(const DevReaction* __restrict__ rxs, const float* __restrict__ values, int64_t n_pairs,
+                                 int n_tasks, int64_t rows_total, double* __restrict__ rowp) {
+  const DevReaction R = rxs[blockIdx.y];
+  const int c = R.c;
+  for (uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; row < R.n_rows;
+       row += (uint64_t)gridDim.x * blockDim.x) {
+    int64_t pr[kMaxRg - 1];
+    decode_prefix(R, c, row, pr);
+    for (int task = 0; task < n_tasks; ++task) {
+      double p = c > 1 ? (double)__ldg(values + (int64_t)task * n_pairs + pr[0]) : 0.0;
+#pragma unroll
+      for (int j = 1; j < kMaxRg - 1; ++j)
+        if (j < c - 1) p = __dadd_rn(p, (double)__ldg(values + (int64_t)task * n_pairs + pr[j]));
+      rowp[task * rows_total + R.row_off + (int64_t)row] = p;
+    }
+  }
+}
+
 }  // namespace apexb200

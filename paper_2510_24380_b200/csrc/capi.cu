@@ -219,6 +219,9 @@ struct apex_ctx {
   DBuf d_cthr, d_cqc, d_cbest;           // sorted-column constraint pre-pass rows (shared constraint sets)
   DBuf d_packed16;                       // [n_pairs][16] pair-major copy of the table (sorted-column kernel)
   bool packed16_ok = false;
+  DBuf d_rowp;                           // [task][rows_total] fp64 row prefix sums (bind_rowp_kernel)
+  bool rowp_ok = false;
+  int64_t rows_total = 0;                // rows (first c-1 R-group assignments) of all reactions
   int n_tasks = 0;
   int64_t n_pairs = 0;
   bool table_loaded = false;
@@ -265,6 +268,8 @@ struct apex_ctx {
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
   int64_t opt_fin_bucket = 8;       // bucketed small finalize: max CTAs per query (0: one-CTA finalize_small_kernel)
+  int64_t opt_rowp = 1;             // build / use the row-prefix table
+  int64_t opt_rowp_bytes = (int64_t)4 << 30;  // its size limit
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -608,6 +613,21 @@ int build_corners(apex_ctx* c) {
   } else {
     c->packed16_ok = false;
   }
+  // row-prefix table (sorted-column scan and constraint pre-pass): every
+  // row's fp64 prefix sums for every task, when it fits the budget
+  c->rowp_ok = false;
+  if (c->opt_rowp && c->rows_total > 0 &&
+      (unsigned __int128)c->rows_total * (unsigned __int128)c->n_tasks * 8u <= (unsigned __int128)c->opt_rowp_bytes) {
+    APEX_TRY(c->d_rowp.ensure((size_t)c->rows_total * c->n_tasks * sizeof(double)));
+    int64_t max_rows = 1;
+    for (const auto& R : c->rx) max_rows = std::max<int64_t>(max_rows, (int64_t)R.n_rows);
+    const unsigned gx = (unsigned)std::min<int64_t>((max_rows + 255) / 256, 4096);
+    bind_rowp_kernel<<<dim3(gx, (unsigned)n_rx), 256, 0, s>>>(c->d_rx.as<DevReaction>(), c->d_values.as<float>(),
+                                                               c->n_pairs, c->n_tasks, c->rows_total,
+                                                               c->d_rowp.as<double>());
+    APEX_CU(cudaGetLastError());
+    c->rowp_ok = true;
+  }
   APEX_CU(cudaStreamSynchronize(s));
   d_segs.release();
   d_keys.release();
@@ -941,6 +961,8 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
     P.cbest = c->d_cbest.as<int4>();
     P.rows_pad = (int64_t)P.n_tiles * 32;
     P.cqc = c->d_cqc.as<unsigned char>();
+    P.rowp = (c->rowp_ok && c->opt_rowp) ? c->d_rowp.as<double>() : nullptr;
+    P.rows_total = c->rows_total;
     // A: (tile, test) threshold + quantile count items
     std::vector<std::pair<int, int>> tests;
     for (int ld : B.cset_leader)
@@ -1088,7 +1110,11 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
         const Plan* pr_ = B.plan_rows;
         const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
         const bool p16 = c->packed16_ok && c->opt_packed16;
-        ScanFn fn = p16 ? reinterpret_cast<ScanFn>(scan_sorted_kernel<true>) : reinterpret_cast<ScanFn>(scan_sorted_kernel<false>);
+        const bool rowp = c->rowp_ok && c->opt_rowp;
+        ScanFn fn = p16 ? (rowp ? reinterpret_cast<ScanFn>(scan_sorted_kernel<true, true>)
+                                : reinterpret_cast<ScanFn>(scan_sorted_kernel<true, false>))
+                        : (rowp ? reinterpret_cast<ScanFn>(scan_sorted_kernel<false, true>)
+                                : reinterpret_cast<ScanFn>(scan_sorted_kernel<false, false>));
         int occ = 0;
         APEX_TRY(scan_occupancy(c, fn, smem, &occ));
         SortedLaunch SL;
@@ -1101,6 +1127,8 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
         SL.cthr = c->d_cthr.as<float>();
         SL.cbest = c->d_cbest.as<int4>();
         SL.rows_pad = (int64_t)pr_->tiles.size() * 32;
+        SL.rowp = rowp ? c->d_rowp.as<double>() : nullptr;
+        SL.rows_total = c->rows_total;
         for (int q0 = 0; q0 < nq; q0 += 64) {
           const int nql = std::min(64, nq - q0);
           ScanLaunch La = L;
@@ -1114,8 +1142,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           const int slot = wi++ % 64;
           La.work = c->d_work.as<unsigned>() + slot;
-          if (p16) scan_sorted_kernel<true><<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
-          else scan_sorted_kernel<false><<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
+          reinterpret_cast<void (*)(ScanLaunch, SortedLaunch)>(fn)<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
           APEX_CU(cudaGetLastError());
           ++st.launches;
           ++st.scans;
@@ -1826,6 +1853,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   std::vector<DevReaction> rx(n_rx);
   std::vector<unsigned long long> goff(n_rx + 1, 0);
   unsigned __int128 total = 0;
+  unsigned __int128 rows_total = 0;
   int64_t pcols = 0;
   for (int t = 0; t < n_rx; ++t) {
     const apex_reaction& a = rxs[t];
@@ -1846,6 +1874,8 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
     }
     if (R.size[R.c - 1] > 0xffffffffll) return set_err(APEX_ELIMIT, "last R-group larger than 2^32");
     R.n_rows = (uint64_t)(size / (unsigned __int128)R.size[R.c - 1]);
+    R.row_off = (int64_t)rows_total;
+    rows_total += R.n_rows;
     R.pcol_off = pcols;
     pcols += (R.size[R.c - 1] + 3) / 4 * 4;
     if ((uint64_t)total != a.g_offset) return set_err(APEX_EINVAL, "reaction offsets are not the running product count");
@@ -1864,6 +1894,7 @@ int apex_load_library(apex_ctx* c, const apex_reaction* rxs, int32_t n_rx, int64
   c->total = (uint64_t)total;
   c->lib_pairs = n_pairs;
   c->pcols = pcols;
+  c->rows_total = rows_total > (unsigned __int128)INT64_MAX ? 0 : (int64_t)rows_total;  // 0: no row-prefix table
   c->lib_loaded = true;
   c->batch.plan = nullptr;
   c->batch.pending = false;
@@ -2278,6 +2309,13 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "rowp") {
+    c->opt_rowp = v;
+    c->corners_ok = false;  // rebuilt (or dropped) at the next query
+  } else if (n == "rowp_bytes") {
+    c->opt_rowp_bytes = std::max<int64_t>(0, v);
+    c->corners_ok = false;
+  }
   else if (n == "fin_bucket") c->opt_fin_bucket = std::max<int64_t>(0, v);
   else if (n == "trace") {
     // records of the admission scan's per-item trace (0: off); debug only

@@ -34,7 +34,7 @@ struct DevReaction {
   uint64_t g_off;                 // reaction_offset
   uint64_t n_rows;                // product of sizes[0..c-2]
   int64_t pcol_off;               // offset of the last R-group in the packed objective column (16-B aligned)
-  int64_t _pad2;
+  int64_t row_off;                // first row of this reaction in the row-prefix table (rows of all reactions)
 };
 
 // One enumeration tile: rows [row0, row0+nrows) x columns [col0, col0+ncols)

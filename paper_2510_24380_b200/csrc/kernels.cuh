@@ -1667,6 +1667,8 @@ struct SortedLaunch {
   const float* cthr;      // pre-pass: [cset_off + test - 1][rows_pad] constraint thresholds per row
   const int4* cbest;      // pre-pass: [cset][rows_pad] (best test, its quantile count, range start, count)
   int64_t rows_pad;       // row slots: 32 per row tile of the plan
+  const double* rowp;     // [task][rows_total] fp64 prefix sums of every row (bind), or null
+  int64_t rows_total;
 };
 
 // first index i in [0, n) with !(xs[i] <= t) (n if none); xs ascending
@@ -1857,6 +1859,8 @@ struct ConsPre {
   unsigned char* cqc;        // same layout: quantile counts
   int4* cbest;               // [cset][rows_pad]
   int64_t rows_pad;
+  const double* rowp;        // row-prefix table (bind) or null
+  int64_t rows_total;
   int n;                     // A: (query, test) pairs; B: sets (leader queries)
   int q[kConsPreItems];      // A: a query of the test's set / B: a query of each set
   unsigned char ti[kConsPreItems];  // A: test index (1..nt-1)
@@ -1873,13 +1877,18 @@ __global__ void __launch_bounds__(256) cons_thr_kernel(const __grid_constant__ C
   const DevReaction& R = P.rx[T.rx];
   const int c = R.c;
   const uint64_t row = T.row0 + (lane < T.nrows ? lane : 0u);
-  int64_t pr[kMaxRg - 1];
-  decode_prefix(R, c, row, pr);
   const int task = Q.test_task[i];
-  double p = c > 1 ? (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]) : 0.0;
+  double p;
+  if (P.rowp) {
+    p = __ldg(P.rowp + task * P.rows_total + R.row_off + (int64_t)row);
+  } else {
+    int64_t pr[kMaxRg - 1];
+    decode_prefix(R, c, row, pr);
+    p = c > 1 ? (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]) : 0.0;
 #pragma unroll
-  for (int j = 1; j < kMaxRg - 1; ++j)
-    if (j < c - 1) p = __dadd_rn(p, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
+    for (int j = 1; j < kMaxRg - 1; ++j)
+      if (j < c - 1) p = __dadd_rn(p, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
+  }
   const bool lower = Q.test_lower[i] != 0;
   const float th = lower ? -thr_lower_fast(p, Q.test_bias[i], Q.test_beta[i])
                          : thr_upper_fast(p, Q.test_bias[i], Q.test_beta[i]);
@@ -1927,7 +1936,10 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
 // 64-byte line per pair holds every task: a row's prefix sums and a pair's
 // test values for all tests come from one line each instead of one line per
 // task), else from the task-major table values[task][pair].
-template <bool P16>
+// ROWP: every row's prefix sums come from the row-prefix table built at bind
+// (one coalesced fp64 load per row and task: no mixed-radix decode of the row,
+// no gathers of the first R-groups' contributions).
+template <bool P16, bool ROWP>
 __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
   extern __shared__ __align__(16) float sm_s[];
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
@@ -1976,13 +1988,16 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     const bool valid = lane < T.nrows;
     const uint64_t row = T.row0 + (valid ? lane : 0u);
     int64_t pr[kMaxRg - 1];
-    decode_prefix(R, c, row, pr);
+    const double* rowp = ROWP ? S.rowp + R.row_off + (int64_t)row : nullptr;
+    if (!ROWP) decode_prefix(R, c, row, pr);
     const unsigned long long gbase = R.g_off + row * (uint64_t)n_last;
     // the objective's exact per-row threshold (against tau, +inf without one)
     // and its passing count in quantile steps; only when that is not already
     // small are the constraint thresholds derived to find a more selective test
     double p_obj;
-    {
+    if (ROWP) {
+      p_obj = __ldg(rowp + Q.test_task[0] * S.rows_total);
+    } else {
       const int task0 = Q.test_task[0];
       double p = c > 1 ? (double)ld(task0, pr[0]) : 0.0;
 #pragma unroll
@@ -2023,13 +2038,17 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         for (int u = 0; u < kThrBatch; ++u) {
           const int i = min(i0 + u, nt - 1);
           task[u] = Q.test_task[i];
-          double pp = c > 1 ? (double)ld(task[u], pr[0]) : 0.0;
-          // fixed trip counts: pr stays in registers (a runtime-indexed pr
-          // would live in local memory)
+          if (ROWP) {
+            p[u] = __ldg(rowp + task[u] * S.rows_total);
+          } else {
+            double pp = c > 1 ? (double)ld(task[u], pr[0]) : 0.0;
+            // fixed trip counts: pr stays in registers (a runtime-indexed pr
+            // would live in local memory)
 #pragma unroll
-          for (int j = 1; j < kMaxRg - 1; ++j)
-            if (j < c - 1) pp = __dadd_rn(pp, (double)ld(task[u], pr[j]));
-          p[u] = pp;
+            for (int j = 1; j < kMaxRg - 1; ++j)
+              if (j < c - 1) pp = __dadd_rn(pp, (double)ld(task[u], pr[j]));
+            p[u] = pp;
+          }
         }
         float th[kThrBatch];
         bool lower[kThrBatch];
