@@ -369,10 +369,21 @@ class DeviceContext:
         specs, keep = self._specs(queries)
         return PreparedBatch(queries, specs, keep, None, None)
 
-    def run_views(self, pb: "PreparedBatch") -> tuple[list[dict], dict]:
+    def run_views_raw(self, pb: "PreparedBatch"):
+        """The bare C-ABI call in view mode: apex_query with NULL result
+        arrays, so every result row lands in the context's pinned host block
+        (device pass + D2H inside the call).  Returns the apex_result array
+        and the stats; views_of() turns them into numpy views."""
         results = (ResultC * len(pb.queries))()  # all arrays NULL: view mode
         st = Stats()
         _check(self.lib.apex_query(self._ctx, pb.specs, len(pb.queries), results, C.byref(st)))
+        return results, st
+
+    def run_views(self, pb: "PreparedBatch") -> tuple[list[dict], dict]:
+        results, st = self.run_views_raw(pb)
+        return self.views_of(pb, results, st)
+
+    def views_of(self, pb: "PreparedBatch", results, st) -> tuple[list[dict], dict]:
         # one numpy view over the pinned block, sliced per query
         addr = [C.cast(results[i].global_index, C.c_void_p).value or 0 for i in range(len(pb.queries))]
         base = min(a for a in addr if a) if any(addr) else 0

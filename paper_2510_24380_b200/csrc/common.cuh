@@ -261,6 +261,14 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// single-lane atomic add whose result is consumed later: inline PTX so the
+// compiler does not turn it into a warp-aggregated atomic, whose shuffle of
+// the result waits for the atomic right away (defeating a prefetch)
+__device__ __forceinline__ unsigned atom_add_u32(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

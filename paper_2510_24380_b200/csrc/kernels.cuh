@@ -552,11 +552,11 @@ __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, u
     } else {
       if (!wc.primed) {
         wc.primed = true;
-        if (lane == 0) wc.nxt = k_static * nw + atomicAdd(L.work, (unsigned)L.chunk);
+        if (lane == 0) wc.nxt = k_static * nw + atom_add_u32(L.work, (unsigned)L.chunk);
       }
       if (wc.cur >= wc.lim) {
         const unsigned base = __shfl_sync(0xffffffffu, wc.nxt, 0);
-        if (lane == 0 && base < total) wc.nxt = k_static * nw + atomicAdd(L.work, (unsigned)L.chunk);  // one chunk ahead
+        if (lane == 0 && base < total) wc.nxt = k_static * nw + atom_add_u32(L.work, (unsigned)L.chunk);  // one chunk ahead
         wc.cur = base;
         wc.lim = base + (unsigned)L.chunk;
       }
@@ -1939,6 +1939,11 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
 // ROWP: every row's prefix sums come from the row-prefix table built at bind
 // (one coalesced fp64 load per row and task: no mixed-radix decode of the row,
 // no gathers of the first R-groups' contributions).
+#ifdef APEX_SCAN_PROF
+// per-phase cycle totals of the sorted-column scan (debug builds: -DAPEX_SCAN_PROF)
+__device__ unsigned long long g_scan_prof[10];
+__device__ unsigned g_scan_done;
+#endif
 template <bool P16, bool ROWP>
 __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted_kernel(const ScanLaunch L, const SortedLaunch S) {
   extern __shared__ __align__(16) float sm_s[];
@@ -1965,6 +1970,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     T_n = L.tiles[t];
     tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
   }
+#ifdef APEX_SCAN_PROF
+  unsigned long long prof[10] = {}, tp = clock64();
+#endif
   while (have) {
     const unsigned q_cur = qi, t_cur = t;
     const Tile T = T_n;
@@ -1974,16 +1982,28 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       T_n = L.tiles[t];
       tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
     }
+#ifdef APEX_SCAN_PROF
+    if (have && t == 0xffffffffu) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[0] += tn - tp; tp = tn; }
+#endif
     const ScanQuery& Q = L.queries[q_cur];
     QCtl* ctl = Q.ctl;
     const int maximize = Q.maximize;
     const double b_obj = Q.test_bias[0];
     const int nt = Q.nt;
     const DevReaction& R = L.rx[T.rx];
+#ifdef APEX_SCAN_PROF
+    if (nt == 12345 || maximize == 12345) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[1] += tn - tp; tp = tn; }
+#endif
     const int c = R.c;
     const int n_last = (int)R.size[c - 1];
     const int col_lo = (int)T.col0, col_hi = (int)(T.col0 + T.ncols);
     const int64_t last_pair = R.pair_off[c - 1];
+#ifdef APEX_SCAN_PROF
+    if (n_last == 12345 || last_pair == 12345) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[2] += tn - tp; tp = tn; }
+#endif
 
     const bool valid = lane < T.nrows;
     const uint64_t row = T.row0 + (valid ? lane : 0u);
@@ -2005,6 +2025,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         if (j < c - 1) p = __dadd_rn(p, (double)ld(task0, pr[j]));
       p_obj = p;
     }
+#ifdef APEX_SCAN_PROF
+    if (__double_as_longlong(p_obj) == 0x123456789ll) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[3] += tn - tp; tp = tn; }
+#endif
     float th0 = __int_as_float(0x7f800000);
     if (tau != kNoTau) {
       const double ts = key_to_score(tau);
@@ -2073,6 +2097,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       }
       cons_ready = true;
     };
+#ifdef APEX_SCAN_PROF
+    if (best_q == 123456789) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[4] += tn - tp; tp = tn; }
+#endif
     if (Q.cset >= 0) {
       // shared constraint set: the pre-pass rows (thresholds, most selective
       // constraint and its exact range)
@@ -2103,11 +2131,19 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         }
       }
     }
+#ifdef APEX_SCAN_PROF
+    if (cnt == 123456789 || best == 77) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[5] += tn - tp; tp = tn; }
+#endif
     // the objective's exact range when it is the most selective test
     if (valid && best == 0 && th0 == th0 && th0 != __int_as_float(0x7f800000)) {
       const int64_t base0 = (int64_t)Q.test_task[0] * S.pcols + R.pcol_off;
       exact_range(S.sx + base0, n_last, maximize != 0, maximize ? -th0 : th0, best_q, start, cnt);
     }
+#ifdef APEX_SCAN_PROF
+    if (cnt == 123456789) prof[9] += 1;
+    { const unsigned long long tn = clock64(); prof[6] += tn - tp; tp = tn; }
+#endif
     if (cnt > 0 && !cons_ready) constraint_thresholds(false);
     // flatten the warp's admitted (row, sorted position) pairs so every lane
     // has one per round: rows pass only a few columns each in batched passes,
@@ -2180,10 +2216,28 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     __syncwarp();
     const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
     if (a && lane == 0) atomicAdd(&s_adm[q_cur], a);  // per CTA; flushed once at the end
+#ifdef APEX_SCAN_PROF
+    prof[8] += 1;
+    { const unsigned long long tn = clock64(); prof[7] += tn - tp; tp = tn; }
+#endif
   }
   __syncthreads();
   for (int q = threadIdx.x; q < L.nq; q += blockDim.x)
     if (s_adm[q]) atomicAdd(&L.queries[q].ctl->admitted, (unsigned long long)s_adm[q]);
+#ifdef APEX_SCAN_PROF
+  if (lane == 0)
+    for (int i = 0; i < 9; ++i) atomicAdd(&g_scan_prof[i], prof[i]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&g_scan_done, 1u) == gridDim.x - 1) {
+    const unsigned long long n = g_scan_prof[8] ? g_scan_prof[8] : 1;
+    printf("SCANPROF items %llu cycles/item: next %llu Q %llu R %llu p_obj %llu thr+quant %llu cset %llu range %llu "
+           "pairs %llu\n", g_scan_prof[8], g_scan_prof[0] / n, g_scan_prof[1] / n, g_scan_prof[2] / n,
+           g_scan_prof[3] / n, g_scan_prof[4] / n, g_scan_prof[5] / n, g_scan_prof[6] / n, g_scan_prof[7] / n);
+    for (int i = 0; i < 10; ++i) g_scan_prof[i] = 0;
+    g_scan_done = 0;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -36,6 +36,19 @@ __global__ void dadd_chain(double x, int n, unsigned long long* out, double* sin
   sink[0] = a;
 }
 
+__global__ void f2f_chain(float x, int n, unsigned long long* out, double* sink) {
+  double a = 0.0;
+  float y = x;
+  const unsigned long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    a = __dadd_rn(a, (double)y);
+    y = (float)a;  // dependent: F2F.F64.F32 + DADD + F2F.F32.F64 per step
+  }
+  const unsigned long long t1 = clock64();
+  out[0] = t1 - t0;
+  sink[0] = a;
+}
+
 __global__ void div_chain(uint32_t x, uint32_t d, int n, unsigned long long* out) {
   uint32_t a = x;
   const unsigned long long t0 = clock64();
@@ -80,6 +93,9 @@ int main() {
   dadd_chain<<<1, 1>>>(1.0, 4096, d_out, d_sink);
   cudaMemcpy(h, d_out, 16, cudaMemcpyDeviceToHost);
   printf("DADD dependent chain: %.1f cyc/op\n", (double)h[0] / 4096);
+  f2f_chain<<<1, 1>>>(1.0f, 4096, d_out, d_sink);
+  cudaMemcpy(h, d_out, 16, cudaMemcpyDeviceToHost);
+  printf("F2F.F64.F32 + DADD + F2F.F32.F64 dependent chain: %.1f cyc/step\n", (double)h[0] / 4096);
   div_chain<<<1, 1>>>(123456789u, 977u, 4096, d_out);
   cudaMemcpy(h, d_out, 16, cudaMemcpyDeviceToHost);
   printf("u32 divide + add chain: %.1f cyc/op\n", (double)h[0] / 4096);
