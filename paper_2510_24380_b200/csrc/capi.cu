@@ -270,6 +270,7 @@ struct apex_ctx {
   int64_t opt_fin_bucket = 8;       // bucketed small finalize: max CTAs per query (0: one-CTA finalize_small_kernel)
   int64_t opt_rowp = 1;             // build / use the row-prefix table
   int64_t opt_rowp_bytes = (int64_t)4 << 30;  // its size limit
+  int64_t opt_heavy_first = 1;      // whole-row tile plans ordered by products, descending
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -399,6 +400,14 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan
   if (P.tiles.size() > 0xffffffffull) return set_err(APEX_ELIMIT, "too many enumeration tiles");
   std::mt19937_64 rng(0x5eed5eedull ^ start ^ (end << 1));
   std::shuffle(P.tiles.begin(), P.tiles.end(), rng);
+  if (force_cols > 0 && c->opt_heavy_first) {
+    // whole-row tiles (sorted-column kernel): the most products first, so the
+    // items whose rows can admit the most pairs start early and the tail of
+    // the dynamically distributed work is made of light items
+    std::stable_sort(P.tiles.begin(), P.tiles.end(), [](const Tile& a, const Tile& b) {
+      return (uint64_t)a.nrows * a.ncols > (uint64_t)b.nrows * b.ncols;
+    });
+  }
   P.prefix.resize(P.tiles.size() + 1);
   P.prefix[0] = 0;
   for (size_t i = 0; i < P.tiles.size(); ++i)
@@ -728,7 +737,7 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   // everything enqueue_batch touches is allocated here (no allocation may
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
-  APEX_TRY(c->d_work.ensure(64 * sizeof(unsigned)));
+  APEX_TRY(c->d_work.ensure(kWorkWords * sizeof(unsigned)));
   APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
   std::vector<ScanQuery> hq(nq);
   for (int i = 0; i < nq; ++i) {
@@ -1108,7 +1117,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       if (admit && B.plan_rows && bounds.size() == 1) {
         // sorted-column admission: whole-row tiles, one launch per 64 queries
         const Plan* pr_ = B.plan_rows;
-        const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float);
+        const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float) + (size_t)kScanWarps * 32 * sizeof(int4);
         const bool p16 = c->packed16_ok && c->opt_packed16;
         const bool rowp = c->rowp_ok && c->opt_rowp;
         ScanFn fn = p16 ? (rowp ? reinterpret_cast<ScanFn>(scan_sorted_kernel<true, true>)
@@ -1801,6 +1810,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_ctls.release();
   c->d_out.release();
   c->d_work.release();
+  for (DBuf* b : {&c->d_rowp, &c->d_cthr, &c->d_cqc, &c->d_cbest}) b->release();
   c->d_trace.release();
   c->h_queries.release();
   c->h_ctl.release();
@@ -2338,7 +2348,13 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
     c->opt_cb_admit = v;
   }
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
-  else if (n == "tile_products") {
+  else if (n == "heavy_first") {
+    c->opt_heavy_first = v;
+    c->batch.plan = nullptr;
+    c->batch.plan_rows = nullptr;
+    c->batch.pending = false;
+    c->plans.clear();
+  } else if (n == "tile_products") {
     c->opt_tile_products = v;
     c->batch.plan = nullptr;
     c->batch.pending = false;

@@ -370,6 +370,8 @@ __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n,
   }
 }
 
+constexpr int kWorkWords = 64;  // flattened-work counters of the scan launches
+
 // ---------------------------------------------------------------------------
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
@@ -378,7 +380,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPrese
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
   // the scan launches' flattened-work counters (replaces a memset node)
-  if (work && blockIdx.x == 0 && threadIdx.x < 64) work[threadIdx.x] = 0u;
+  if (work && blockIdx.x == 0 && threadIdx.x < kWorkWords) work[threadIdx.x] = 0u;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
   // (the candidate / seed histograms are zeroed by one memset per batch)
   if (threadIdx.x == 0) {
@@ -1671,6 +1673,7 @@ struct SortedLaunch {
   int64_t rows_total;
 };
 
+
 // first index i in [0, n) with !(xs[i] <= t) (n if none); xs ascending
 __device__ __forceinline__ int first_gt(const float* __restrict__ xs, int n, float t) {
   int lo = 0, p = 0, step = 1;
@@ -1740,6 +1743,13 @@ __device__ __forceinline__ int quant_count(const float* __restrict__ q, bool low
 #define APEX_THR_BATCH 1
 #endif
 constexpr int kThrBatch = APEX_THR_BATCH;  // tests whose threshold chains are interleaved
+#ifndef APEX_PAIR_BATCH
+#define APEX_PAIR_BATCH 1
+#endif
+// sorted-column pair loop: test gathers issued together (1: one at a time; 4 and
+// 8 were slower on C2 — more issue slots and registers for a loop that is not
+// latency-bound, profiles/r2_ab_pair_batch_rejected.log)
+constexpr int kPairBatch = APEX_PAIR_BATCH;
 __device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride,
                                              const int (&task)[kThrBatch], const bool (&lower)[kThrBatch],
                                              const float (&th)[kThrBatch], int (&qc)[kThrBatch]) {
@@ -1942,6 +1952,9 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
 #ifdef APEX_SCAN_PROF
 // per-phase cycle totals of the sorted-column scan (debug builds: -DAPEX_SCAN_PROF)
 __device__ unsigned long long g_scan_prof[10];
+// warp start min/max, end min/max, span sum, warps, max item cycles, max item pairs
+__device__ unsigned long long g_scan_t[8] = {~0ull, 0, ~0ull, 0, 0, 0, 0, 0};
+__device__ unsigned long long g_scan_hist[64];  // items by log2(cycles) / by log2(admitted pairs + 1)
 __device__ unsigned g_scan_done;
 #endif
 template <bool P16, bool ROWP>
@@ -1951,6 +1964,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   const unsigned long long live = live_mask(L, 0u);
   if (!live) return;
   float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: signed-value thresholds of every test
+  int4* scb = reinterpret_cast<int4*>(sm_s + (size_t)kScanWarps * kMaxTests * 32) + warp * 32;  // pre-pass best range
   WorkCursor wc;
   const float* __restrict__ values = L.values;
   const float* __restrict__ p16 = S.packed16;
@@ -1972,8 +1986,12 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   }
 #ifdef APEX_SCAN_PROF
   unsigned long long prof[10] = {}, tp = clock64();
+  const unsigned long long g_start = globaltimer_ns();
 #endif
   while (have) {
+#ifdef APEX_SCAN_PROF
+    const unsigned long long t_item = clock64();
+#endif
     const unsigned q_cur = qi, t_cur = t;
     const Tile T = T_n;
     const unsigned long long tau = tau_n;
@@ -2004,6 +2022,17 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     if (n_last == 12345 || last_pair == 12345) prof[9] += 1;
     { const unsigned long long tn = clock64(); prof[2] += tn - tp; tp = tn; }
 #endif
+    // shared constraint set: the pre-pass rows (every constraint threshold,
+    // the most selective constraint and its exact range) copied to shared
+    // memory in the background (cp.async) while the objective's chain runs
+    const int cset = Q.cset;
+    if (cset >= 0) {
+      const int64_t slot = (int64_t)t_cur * 32 + lane;
+      const float* cth = S.cthr + (int64_t)(Q.cset_off - 1) * S.rows_pad + slot;
+      for (int i = 1; i < nt; ++i) cp_async4(sthr + i * 32 + lane, cth + (int64_t)i * S.rows_pad);
+      cp_async16(scb + lane, S.cbest + (int64_t)cset * S.rows_pad + slot);
+      cp_async_commit();
+    }
 
     const bool valid = lane < T.nrows;
     const uint64_t row = T.row0 + (valid ? lane : 0u);
@@ -2101,14 +2130,13 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     if (best_q == 123456789) prof[9] += 1;
     { const unsigned long long tn = clock64(); prof[4] += tn - tp; tp = tn; }
 #endif
-    if (Q.cset >= 0) {
-      // shared constraint set: the pre-pass rows (thresholds, most selective
-      // constraint and its exact range)
-      const int64_t slot = (int64_t)t_cur * 32 + lane;
-      for (int i = 1; i < nt; ++i) sthr[i * 32 + lane] = __ldg(S.cthr + (int64_t)(Q.cset_off + i - 1) * S.rows_pad + slot);
+    if (cset >= 0) {
+      // (the pre-pass rows copied at the top of the item)
+      cp_async_wait_all();
+      __syncwarp();
       cons_ready = true;
       if (valid && best_q > 2 && nt > 1) {
-        const int4 bc = __ldg(S.cbest + (int64_t)Q.cset * S.rows_pad + slot);
+        const int4 bc = scb[lane];
         if (bc.y < best_q) {
           best = bc.x;
           best_q = bc.y;
@@ -2159,6 +2187,16 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     const int64_t sbase = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off + start - (incl - cnt);
     __syncwarp();
     unsigned admitted = 0;
+    // control fields fixed during the enumeration (set by the control init
+    // and the seed), read once per item rather than per candidate
+    bool tie_on = false;
+    unsigned long long hist_base = 0;
+    unsigned hist_shift = 0;
+    if (total > 0) {
+      tie_on = __ldcg(&ctl->tie_on) != 0;
+      hist_base = __ldcg(&ctl->hist_base);
+      hist_shift = __ldcg(&ctl->hist_shift);
+    }
     for (int j0 = 0; j0 < total; j0 += 32) {
       const int jj = j0 + (int)lane;
       const int j = jj < total ? jj : total - 1;
@@ -2179,14 +2217,20 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         col = (int)__ldg(S.scol + sb + j);
         ok = col >= col_lo && col < col_hi;
       }
-      // every test on the pair (the chosen one passes by construction);
-      // gathers issued without short-circuit
+      // every test on the pair (the chosen one passes by construction):
+      // kPairBatch gathers in flight before any compare (they hit one 64-byte
+      // line of the pair-major table), no short-circuit
       bool pass = ok;
       float xo = 0.0f;
-      for (int i = 0; i < nt; ++i) {
-        const float x = ok ? ld(Q.test_task[i], last_pair + col) : 0.0f;
-        if (i == 0) xo = x;
-        pass = pass && ((Q.test_lower[i] ? -x : x) <= sthr[i * 32 + r]);
+      for (int i0 = 0; i0 < nt; i0 += kPairBatch) {
+        float x[kPairBatch];
+#pragma unroll
+        for (int u = 0; u < kPairBatch; ++u)
+          x[u] = (ok && i0 + u < nt) ? ld(Q.test_task[i0 + u], last_pair + col) : 0.0f;
+        if (i0 == 0) xo = x[0];
+#pragma unroll
+        for (int u = 0; u < kPairBatch; ++u)
+          if (i0 + u < nt) pass = pass && ((Q.test_lower[i0 + u] ? -x[u] : x[u]) <= sthr[(i0 + u) * 32 + r]);
       }
       admitted += ok ? 1u : 0u;
       Entry e;
@@ -2194,7 +2238,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         const double val = fx(po, xo, b_obj);
         e.key = skey(maximize ? val : -val);
         e.g = gb + (unsigned long long)col;
-        pass = !tie_reject(ctl, e.key, e.g);
+        pass = !(tie_on && tie_reject(ctl, e.key, e.g));
       }
       const unsigned mk = __ballot_sync(0xffffffffu, pass);
       if (!mk) continue;
@@ -2204,7 +2248,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       if (pass) {
         const unsigned long long idx = cbase + __popc(mk & ((1u << lane) - 1u));
         if (idx < Q.cap) Q.buf[idx] = e;
-        const unsigned hb = cand_bin(ctl, e.key, e.g, __ldcg(&ctl->hist_base), __ldcg(&ctl->hist_shift));
+        const unsigned hb = tie_on ? cand_bin(ctl, e.key, e.g, hist_base, hist_shift) : hist_bin(e.key, hist_base, hist_shift);
         atomicAdd(&Q.hist[hb], 1u);
         atomicAdd(&Q.coarse[hb >> 8], 1u);
       }
@@ -2217,6 +2261,15 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
     if (a && lane == 0) atomicAdd(&s_adm[q_cur], a);  // per CTA; flushed once at the end
 #ifdef APEX_SCAN_PROF
+    if (lane == 0) {
+      const unsigned long long dur = clock64() - t_item;
+      atomicAdd(&g_scan_hist[min(31, 63 - __clzll(dur | 1))], 1ull);
+      atomicAdd(&g_scan_hist[32 + min(31, 32 - __clz(total))], 1ull);
+      atomicMax(&g_scan_t[6], dur);
+      atomicMax(&g_scan_t[7], (unsigned long long)total);
+    }
+#endif
+#ifdef APEX_SCAN_PROF
     prof[8] += 1;
     { const unsigned long long tn = clock64(); prof[7] += tn - tp; tp = tn; }
 #endif
@@ -2225,6 +2278,15 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   for (int q = threadIdx.x; q < L.nq; q += blockDim.x)
     if (s_adm[q]) atomicAdd(&L.queries[q].ctl->admitted, (unsigned long long)s_adm[q]);
 #ifdef APEX_SCAN_PROF
+  if (lane == 0) {
+    const unsigned long long g_end = globaltimer_ns();
+    atomicMin(&g_scan_t[0], g_start);
+    atomicMax(&g_scan_t[1], g_start);
+    atomicMin(&g_scan_t[2], g_end);
+    atomicMax(&g_scan_t[3], g_end);
+    atomicAdd(&g_scan_t[4], g_end - g_start);
+    atomicAdd(&g_scan_t[5], 1ull);
+  }
   if (lane == 0)
     for (int i = 0; i < 9; ++i) atomicAdd(&g_scan_prof[i], prof[i]);
   __threadfence();
@@ -2234,7 +2296,18 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     printf("SCANPROF items %llu cycles/item: next %llu Q %llu R %llu p_obj %llu thr+quant %llu cset %llu range %llu "
            "pairs %llu\n", g_scan_prof[8], g_scan_prof[0] / n, g_scan_prof[1] / n, g_scan_prof[2] / n,
            g_scan_prof[3] / n, g_scan_prof[4] / n, g_scan_prof[5] / n, g_scan_prof[6] / n, g_scan_prof[7] / n);
+    printf("SCANTIME warps %llu: first start +0, last start +%llu ns, first end +%llu, last end +%llu, mean warp span %llu ns\n",
+           g_scan_t[5], g_scan_t[1] - g_scan_t[0], g_scan_t[2] - g_scan_t[0], g_scan_t[3] - g_scan_t[0],
+           g_scan_t[4] / (g_scan_t[5] ? g_scan_t[5] : 1));
+    printf("SCANITEMS max cycles %llu max pairs %llu\n", g_scan_t[6], g_scan_t[7]);
+    for (int i = 0; i < 32; ++i)
+      if (g_scan_hist[i] || g_scan_hist[32 + i])
+        printf("SCANHIST 2^%d: items by cycles %llu | by pairs (<2^%d) %llu\n", i, g_scan_hist[i], i, g_scan_hist[32 + i]);
+    for (int i = 0; i < 64; ++i) g_scan_hist[i] = 0;
+    g_scan_t[6] = g_scan_t[7] = 0;
     for (int i = 0; i < 10; ++i) g_scan_prof[i] = 0;
+    g_scan_t[0] = g_scan_t[2] = ~0ull;
+    g_scan_t[1] = g_scan_t[3] = g_scan_t[4] = g_scan_t[5] = 0;
     g_scan_done = 0;
   }
 #endif
