@@ -271,6 +271,7 @@ struct apex_ctx {
   int64_t opt_rowp = 1;             // build / use the row-prefix table
   int64_t opt_rowp_bytes = (int64_t)4 << 30;  // its size limit
   int64_t opt_heavy_first = 1;      // whole-row tile plans ordered by products, descending
+  int64_t opt_work_ctrs = 4;        // sorted-column scan: work counters (1: one counter)
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -1151,6 +1152,10 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           const int slot = wi++ % 64;
           La.work = c->d_work.as<unsigned>() + slot;
+          if (q0 == 0 && c->opt_work_ctrs > 1) {  // the first launch: several counters (own lines)
+            La.work = c->d_work.as<unsigned>() + 64;
+            La.n_ctr = (int)std::min<int64_t>(c->opt_work_ctrs, kWorkCtrs);
+          }
           reinterpret_cast<void (*)(ScanLaunch, SortedLaunch)>(fn)<<<(unsigned)blocks, kScanWarps * 32, smem, s>>>(La, SL);
           APEX_CU(cudaGetLastError());
           ++st.launches;
@@ -2319,6 +2324,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "work_ctrs") c->opt_work_ctrs = std::max<int64_t>(1, v);
   else if (n == "rowp") {
     c->opt_rowp = v;
     c->corners_ok = false;  // rebuilt (or dropped) at the next query

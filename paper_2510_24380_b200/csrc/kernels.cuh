@@ -370,7 +370,8 @@ __device__ __forceinline__ void divmod_u64(uint64_t& q, uint64_t& r, uint64_t n,
   }
 }
 
-constexpr int kWorkWords = 64;  // flattened-work counters of the scan launches
+constexpr int kWorkCtrs = 16;  // sorted-column scan: work counters, one 128-byte line each
+constexpr int kWorkWords = 64 + 32 * kWorkCtrs;  // flattened-work counters of the scan launches
 
 // ---------------------------------------------------------------------------
 // Control-block init (one CTA per query).  tau0 = preset admission key
@@ -523,6 +524,7 @@ struct ScanLaunch {
   int dense_min;          // admission kernel: admitted products of a row in a tile that flag it dense
   unsigned long long* trace;  // per-item timing records (8 words) or null
   unsigned trace_cap;         // records
+  int n_ctr;              // > 1: that many work counters (work + 32 k), counter k hands out items k, k + n_ctr, ...
 };
 
 // Flattened persistent work distribution: item -> (tile = item / nq,
@@ -535,7 +537,40 @@ struct WorkCursor {
   unsigned nxt = 0;      // lane 0: base of the next chunk, fetched one chunk ahead
   bool primed = false;
   unsigned sk = 0;       // static rounds taken
+  unsigned k = 0, tried = 0;  // several counters: the current one, counters found exhausted
 };
+
+// Several work counters (L.n_ctr > 1, each in its own 128-byte line): one
+// counter's atomics from every warp of the grid serialise at its L2 slice and
+// come back later than a whole item takes (ncu: the warps stalled on the
+// prefetched item index); n_ctr counters over interleaved item sets keep the
+// heaviest-first order and divide that queue.  A warp starts on counter
+// (warp id mod n_ctr) and moves on when it is exhausted.
+__device__ __forceinline__ bool next_item_multi(const ScanLaunch& L, WorkCursor& wc, unsigned long long live,
+                                                unsigned lane, unsigned& q, unsigned& t) {
+  const unsigned total = (L.tile_end - L.tile_begin) * (unsigned)L.nq;
+  const unsigned n = (unsigned)L.n_ctr;
+  if (!wc.primed) {
+    wc.primed = true;
+    wc.k = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % n;
+    if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);
+  }
+  for (;;) {
+    const unsigned local = __shfl_sync(0xffffffffu, wc.nxt, 0);
+    const unsigned long long item64 = (unsigned long long)wc.k + (unsigned long long)local * n;
+    if (item64 >= total) {
+      if (++wc.tried >= n) return false;
+      wc.k = wc.k + 1 == n ? 0u : wc.k + 1;
+      if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);
+      continue;
+    }
+    if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);  // one item ahead
+    const unsigned item = (unsigned)item64;
+    q = item % (unsigned)L.nq;
+    t = L.tile_begin + item / (unsigned)L.nq;
+    if ((live >> q) & 1ull) return true;
+  }
+}
 
 __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, unsigned long long live, unsigned lane,
                                           unsigned& q, unsigned& t) {
@@ -569,6 +604,17 @@ __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, u
     t = L.tile_begin + item / (unsigned)L.nq;
     if ((live >> q) & 1ull) return true;
   }
+}
+
+// Warp-aggregated histogram increment (the whole warp calls it, converged):
+// lanes with on == true and the same bin add once, by their lowest lane.
+// Seed products of one warp mostly share bins (16-bit key prefixes of
+// near-equal top values), so this removes most same-address atomics.
+__device__ __forceinline__ void hist_add_warp(unsigned int* h, unsigned bin, bool on) {
+  const unsigned am = __ballot_sync(0xffffffffu, on);
+  if (!on) return;
+  const unsigned peers = __match_any_sync(am, bin);
+  if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
 }
 
 // queries of the launch that this kernel form scans
@@ -1939,8 +1985,11 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
   P.cbest[(int64_t)Q.cset * P.rows_pad + slot] = make_int4(best, valid ? best_q : kQuant + 2, start, cnt);
 }
 
+// CTAs per SM of the sorted-column scan (register budget 65536 / (256 x MINB)):
+// 3 (80 registers) beat 4 (64 registers, more spills) by 5-8% on C2
+// (profiles/r2_ab_sorted_minb.log); 2 (107 registers) was in between
 #ifndef APEX_SORTED_MINB
-#define APEX_SORTED_MINB 4
+#define APEX_SORTED_MINB 3
 #endif
 // P16: contributions read from the pair-major copy packed16[pair][16] (one
 // 64-byte line per pair holds every task: a row's prefix sums and a pair's
@@ -1949,6 +1998,11 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
 // ROWP: every row's prefix sums come from the row-prefix table built at bind
 // (one coalesced fp64 load per row and task: no mixed-radix decode of the row,
 // no gathers of the first R-groups' contributions).
+#ifdef APEX_SCAN_TIME
+// per-warp start / end times and item counts of the sorted-column scan (debug builds: -DAPEX_SCAN_TIME)
+__device__ unsigned long long g_wt[16384][3];
+__device__ unsigned g_wt_n, g_wt_done;
+#endif
 #ifdef APEX_SCAN_PROF
 // per-phase cycle totals of the sorted-column scan (debug builds: -DAPEX_SCAN_PROF)
 __device__ unsigned long long g_scan_prof[10];
@@ -1977,7 +2031,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   };
 
   unsigned qi, t;
-  bool have = next_item(L, wc, live, lane, qi, t);
+  bool have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
   Tile T_n;
   unsigned long long tau_n = 0;
   if (have) {
@@ -1988,14 +2042,24 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   unsigned long long prof[10] = {}, tp = clock64();
   const unsigned long long g_start = globaltimer_ns();
 #endif
+#ifdef APEX_SCAN_TIME
+  const unsigned long long w_start = globaltimer_ns();
+  unsigned long long w_items = 0, w_last = w_start;
+  unsigned w_rounds = 0, w_crounds = 0, w_refresh = 0, w_cand = 0, w_maxitem_rounds = 0;
+  unsigned long long w_maxitem = 0;
+#endif
   while (have) {
 #ifdef APEX_SCAN_PROF
     const unsigned long long t_item = clock64();
 #endif
+#ifdef APEX_SCAN_TIME
+    ++w_items;
+    w_last = globaltimer_ns();
+#endif
     const unsigned q_cur = qi, t_cur = t;
     const Tile T = T_n;
     const unsigned long long tau = tau_n;
-    have = next_item(L, wc, live, lane, qi, t);
+    have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
     if (have) {
       T_n = L.tiles[t];
       tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
@@ -2197,6 +2261,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       hist_base = __ldcg(&ctl->hist_base);
       hist_shift = __ldcg(&ctl->hist_shift);
     }
+#ifdef APEX_SCAN_TIME
+    w_rounds += (total + 31) / 32;
+#endif
     for (int j0 = 0; j0 < total; j0 += 32) {
       const int jj = j0 + (int)lane;
       const int j = jj < total ? jj : total - 1;
@@ -2242,6 +2309,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       }
       const unsigned mk = __ballot_sync(0xffffffffu, pass);
       if (!mk) continue;
+#ifdef APEX_SCAN_TIME
+      ++w_crounds;
+      w_cand += __popc(mk);
+#endif
       unsigned long long cbase = 0;
       if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
       cbase = __shfl_sync(0xffffffffu, cbase, 0);
@@ -2255,8 +2326,12 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       if ((cbase >> Q.refresh_shift) != ((cbase + __popc(mk)) >> Q.refresh_shift)) {
         __threadfence();
         refresh_tau(Q);
+#ifdef APEX_SCAN_TIME
+        ++w_refresh;
+#endif
       }
     }
+
     __syncwarp();
     const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
     if (a && lane == 0) atomicAdd(&s_adm[q_cur], a);  // per CTA; flushed once at the end
@@ -2274,9 +2349,48 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     { const unsigned long long tn = clock64(); prof[7] += tn - tp; tp = tn; }
 #endif
   }
+#ifdef APEX_SCAN_TIME
+  if (lane == 0 && globaltimer_ns() - w_start > 62000)
+    printf("SCANLATE warp %u/%u items %llu rounds %u cand_rounds %u cand %u refresh %u span %llu ns last %llu ns\n",
+           blockIdx.x, threadIdx.x >> 5, w_items, w_rounds, w_crounds, w_cand, w_refresh, globaltimer_ns() - w_start,
+           globaltimer_ns() - w_last);
+  if (lane == 0) {
+    const unsigned slot = atomicAdd(&g_wt_n, 1u);
+    if (slot < 16384) {
+      g_wt[slot][0] = w_start;
+      g_wt[slot][1] = globaltimer_ns();
+      g_wt[slot][2] = w_items | ((globaltimer_ns() - w_last) << 20);
+    }
+  }
+  __threadfence();
+#endif
   __syncthreads();
   for (int q = threadIdx.x; q < L.nq; q += blockDim.x)
     if (s_adm[q]) atomicAdd(&L.queries[q].ctl->admitted, (unsigned long long)s_adm[q]);
+#ifdef APEX_SCAN_TIME
+  if (threadIdx.x == 0 && atomicAdd(&g_wt_done, 1u) == gridDim.x - 1) {
+    const unsigned n = min(g_wt_n, 16384u);
+    unsigned long long t0 = ~0ull;
+    for (unsigned i = 0; i < n; ++i) t0 = min(t0, g_wt[i][0]);
+    // end-time histogram in 4 us buckets, items per warp, last-item duration
+    unsigned hist[64] = {};
+    unsigned long long items = 0, last_sum = 0, last_max = 0, smax = 0;
+    for (unsigned i = 0; i < n; ++i) {
+      const unsigned long long e = (g_wt[i][1] - t0) / 4000;
+      hist[min(63ull, e)]++;
+      items += g_wt[i][2] & 0xfffff;
+      last_sum += g_wt[i][2] >> 20;
+      last_max = max(last_max, g_wt[i][2] >> 20);
+      smax = max(smax, g_wt[i][0] - t0);
+    }
+    printf("SCANWARPS %u warps, items/warp %.2f, last start +%llu ns, last-item mean %llu ns max %llu ns\n", n,
+           (double)items / n, smax, last_sum / n, last_max);
+    for (int b = 0; b < 64; ++b)
+      if (hist[b]) printf("SCANEND %3d-%3d us: %u warps\n", 4 * b, 4 * b + 4, hist[b]);
+    g_wt_n = 0;
+    g_wt_done = 0;
+  }
+#endif
 #ifdef APEX_SCAN_PROF
   if (lane == 0) {
     const unsigned long long g_end = globaltimer_ns();
@@ -2333,17 +2447,6 @@ struct SampleLaunch {
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
   return x;
-}
-
-// Warp-aggregated histogram increment (the whole warp calls it, converged):
-// lanes with on == true and the same bin add once, by their lowest lane.
-// Seed products of one warp mostly share bins (16-bit key prefixes of
-// near-equal top values), so this removes most same-address atomics.
-__device__ __forceinline__ void hist_add_warp(unsigned int* h, unsigned bin, bool on) {
-  const unsigned am = __ballot_sync(0xffffffffu, on);
-  if (!on) return;
-  const unsigned peers = __match_any_sync(am, bin);
-  if ((int)lane_id() == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
 }
 
 __global__ void sample_kernel(const SampleLaunch P, int nq) {
