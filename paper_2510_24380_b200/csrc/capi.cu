@@ -272,6 +272,8 @@ struct apex_ctx {
   int64_t opt_rowp_bytes = (int64_t)4 << 30;  // its size limit
   int64_t opt_heavy_first = 1;      // whole-row tile plans ordered by products, descending
   int64_t opt_work_ctrs = 4;        // sorted-column scan: work counters (1: one counter)
+  int64_t opt_split_cols = 0;       // whole-row tiles of reactions with >= this many columns get split_rows rows (0: off)
+  int64_t opt_split_rows = 8;
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -395,7 +397,13 @@ int build_plan(apex_ctx* c, uint64_t start, uint64_t end, int rows, int nq, Plan
       emit(r_lo, 1, c_lo, n_last);
       first_full = r_lo + 1;
     }
-    for (uint64_t r = first_full; r < r_hi; r += (uint64_t)rows) emit(r, std::min<uint64_t>(rows, r_hi - r), 0, n_last);
+    // whole-row tiles of reactions with long rows (sorted-column kernel):
+    // fewer rows per tile, so a tile whose rows admit many pairs becomes
+    // several items that run on different warps instead of one long item
+    uint64_t rows_t = (uint64_t)rows;
+    if (force_cols > 0 && c->opt_split_cols > 0 && n_last >= (uint64_t)c->opt_split_cols)
+      rows_t = (uint64_t)std::max<int64_t>(1, std::min<int64_t>(rows, c->opt_split_rows));
+    for (uint64_t r = first_full; r < r_hi; r += rows_t) emit(r, std::min<uint64_t>(rows_t, r_hi - r), 0, n_last);
     if (c_hi) emit(r_hi, 1, 0, c_hi);
   }
   if (P.tiles.size() > 0xffffffffull) return set_err(APEX_ELIMIT, "too many enumeration tiles");
@@ -2354,7 +2362,13 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
     c->opt_cb_admit = v;
   }
   else if (n == "chunk_min") c->opt_chunk_min = std::max<int64_t>(v, 1);
-  else if (n == "heavy_first") {
+  else if (n == "split_cols" || n == "split_rows") {
+    (n == "split_cols" ? c->opt_split_cols : c->opt_split_rows) = std::max<int64_t>(0, v);
+    c->batch.plan = nullptr;
+    c->batch.plan_rows = nullptr;
+    c->batch.pending = false;
+    c->plans.clear();
+  } else if (n == "heavy_first") {
     c->opt_heavy_first = v;
     c->batch.plan = nullptr;
     c->batch.plan_rows = nullptr;
