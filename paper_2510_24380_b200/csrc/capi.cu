@@ -267,7 +267,7 @@ struct apex_ctx {
   int64_t opt_pre_rows = 2;         // K1 form: 2 = TMA bulk ring (11 x 64), 1 = row-parallel, 0 = smem tiles
   int64_t opt_vote64 = 1;           // admission kernel 64-column pre-vote
   int64_t opt_sorted = 1;           // sorted-column admission kernel (per-row work) instead of the streaming one
-  int64_t opt_fin_bucket = 8;       // bucketed small finalize: max CTAs per query (0: one-CTA finalize_small_kernel)
+  int64_t opt_fin_bucket = 64;      // bucketed small finalize: max CTAs per query (0: one-CTA finalize_small_kernel)
   int64_t opt_rowp = 1;             // build / use the row-prefix table
   int64_t opt_rowp_bytes = (int64_t)4 << 30;  // its size limit
   int64_t opt_heavy_first = 1;      // whole-row tile plans ordered by products, descending
@@ -889,7 +889,10 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bucket));
         c->attr_bucket = true;
       }
-      const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(c->opt_fin_bucket, c->sm_count / std::max(nq, 1)));
+      // about kFinRowsPerCta ranks per CTA, within one wave and kFinMaxSplit
+      const int64_t want = (k_max + kFinRowsPerCta - 1) / kFinRowsPerCta;
+      const int ns = (int)std::max<int64_t>(
+          1, std::min<int64_t>({want, c->opt_fin_bucket, (int64_t)kFinMaxSplit, (int64_t)c->sm_count / std::max(nq, 1)}));
       finalize_bucket_kernel<<<dim3((unsigned)ns, (unsigned)nq), kFinThreads, smem_bucket, s>>>(M, finalize ? 1 : 0);
     } else {
       // (materialization runs after, for every query, in materialize_kernel)

@@ -3213,6 +3213,9 @@ __global__ void __launch_bounds__(1024) finalize_small_kernel(const MatLaunch M,
 // the other warps meanwhile, the buffer is read kFinBatch entries per thread
 // per round trip, and a materialized row decodes from shared memory.
 constexpr int kFinThreads = 512;
+constexpr int kFinWarps = kFinThreads / 32;
+constexpr int kFinMaxSplit = 64;     // CTAs per query (rank splits)
+constexpr int kFinRowsPerCta = 128;  // target ranks per CTA
 constexpr int kFinBatch = 8;     // buffer entries per thread in flight
 constexpr int kFinRx = 256;      // reactions whose descriptors + g offsets are staged in shared memory
 __host__ __device__ constexpr size_t fin_bucket_smem() {
@@ -3230,23 +3233,19 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
   Entry* es = reinterpret_cast<Entry*>(sm_e);
   DevReaction* s_rx = reinterpret_cast<DevReaction*>(sm_e + (size_t)kSmallSel * sizeof(Entry));
   unsigned long long* s_goff = reinterpret_cast<unsigned long long*>(s_rx + kFinRx);
-  __shared__ unsigned long long s_bound, s_valid, s_above[2], s_n, s_hbase;
-  __shared__ int s_bin[3];
+  __shared__ unsigned long long s_bound, s_valid, s_above[kFinMaxSplit], s_n, s_hbase;
+  __shared__ int s_bin[kFinMaxSplit], s_B;
   __shared__ unsigned s_hshift, s_tie, cnt;
   const bool stage_rx = materialize && M.n_rx <= kFinRx;
   if (warp == 0) {
     // the final bound (CTA 0 writes it and the re-run parameters)
     const int B = final_bound(Q, j == 0, s_bound, s_valid);
-    if (lane == 0) s_bin[2] = B;  // bins below B hold no rank < kk
-  } else if (warp <= 2) {
-    // the rank-split bins b_j (warp 1) and b_{j+1} (warp 2) and the counts above them
-    const unsigned jj = j + (warp - 1);
-    if (jj == 0 || jj >= ns) {
-      if (lane == 0) {
-        s_bin[warp - 1] = jj == 0 ? 65535 : -2;  // -2: no lower split (down to B)
-        s_above[warp - 1] = 0;
-      }
-    } else {
+    if (lane == 0) s_B = B;  // bins below B hold no rank < kk
+  } else if (warp < kFinWarps - 1) {
+    // rank splits w = warp, warp + (kFinWarps - 2), ...: the bin of rank
+    // w*kk/ns and the count above it (every CTA derives all ns splits, so all
+    // agree on the path taken)
+    if (warp < ns) {
       unsigned v[8];
       load_bins256(Q.coarse, v);
       unsigned long long tot = 0;
@@ -3254,37 +3253,54 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
       for (int i = 0; i < 8; ++i) tot += v[i];
       tot = __reduce_add_sync(0xffffffffu, (unsigned)tot);
       const unsigned long long kk = min((unsigned long long)Q.k, tot);  // kk = min(k, total)
-      const unsigned long long target = (unsigned long long)jj * kk / ns + 1;
-      unsigned long long above = 0;
-      const int b = kk ? kth_two_level_above(Q.hist, v, target, &above) : -1;
-      if (lane == 0) {
-        s_bin[warp - 1] = b < 0 ? -1 : b;
-        s_above[warp - 1] = above;
+      for (unsigned w = warp; w < ns; w += kFinWarps - 2) {
+        const unsigned long long target = (unsigned long long)w * kk / ns + 1;
+        unsigned long long above = 0;
+        const int b = kk ? kth_two_level_above(Q.hist, v, target, &above) : -1;
+        if (lane == 0) {
+          s_bin[w] = b;
+          s_above[w] = above;
+        }
       }
     }
   } else {
-    if (threadIdx.x == 96) {
+    if (lane == 0) {
       s_n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
       s_hbase = *(volatile unsigned long long*)&ctl->hist_base;
       s_hshift = *(volatile unsigned*)&ctl->hist_shift;
       s_tie = *(volatile unsigned*)&ctl->tie_on;
       cnt = 0;
+      s_bin[0] = 65535;
+      s_above[0] = 0;
     }
     if (stage_rx) {
+      const int t0 = (int)lane, nt = 32;
       const int words = (int)(M.n_rx * (sizeof(DevReaction) / 8));
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(M.rx);
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(s_rx);
-      for (int i = threadIdx.x - 96; i < words; i += blockDim.x - 96) dst[i] = __ldg(src + i);
-      for (int i = threadIdx.x - 96; i <= M.n_rx; i += blockDim.x - 96) s_goff[i] = __ldg(M.g_off + i);
+      for (int i = t0; i < words; i += nt) dst[i] = __ldg(src + i);
+      for (int i = t0; i <= M.n_rx; i += nt) s_goff[i] = __ldg(M.g_off + i);
     }
   }
   __syncthreads();
   const unsigned long long n_valid = s_valid;
-  if (n_valid > (unsigned long long)kSmallSel) return;  // large path
+  // the bucketed path takes every set whose CTAs each hold at most kSmallSel
+  // entries (k above kSmallSel included, e.g. C4's k = 10,000); otherwise the
+  // large path (select / sort / rank / materialize) follows
+  if (n_valid > (unsigned long long)kSmallSel) {
+    bool ok = s_tie == 0 && s_B >= 0;
+    for (unsigned w = 1; w < ns && ok; ++w) ok = s_bin[w] >= 0;
+    for (unsigned w = 0; w < ns && ok; ++w) {
+      const unsigned long long hi_ab = s_above[w];
+      const unsigned long long lo_ab = w + 1 < ns ? s_above[w + 1] : n_valid;
+      ok = lo_ab >= hi_ab && lo_ab - hi_ab <= (unsigned long long)kSmallSel;
+    }
+    if (!ok) return;
+  }
   // this CTA's bins: (lo_excl, hi]
-  const int hi = s_bin[0];
-  const int lo_excl = s_bin[1] == -2 ? (s_bin[2] >= 0 ? s_bin[2] - 1 : -1) : s_bin[1];
-  const unsigned long long off = s_above[0];
+  const int hi = s_bin[j];
+  const int lo_excl = j + 1 < ns ? s_bin[j + 1] : (s_B >= 0 ? s_B - 1 : -1);
+  const unsigned long long off = s_above[j];
   const unsigned long long kk = min((unsigned long long)Q.k, n_valid);
   if (j == 0 && threadIdx.x == 0) {
     ctl->sel_count = kk;
