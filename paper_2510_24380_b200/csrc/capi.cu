@@ -274,6 +274,7 @@ struct apex_ctx {
   int64_t opt_work_ctrs = 4;        // sorted-column scan: work counters (1: one counter)
   int64_t opt_split_cols = 0;       // whole-row tiles of reactions with >= this many columns get split_rows rows (0: off)
   int64_t opt_split_rows = 8;
+  int64_t opt_cpre_ctas = 0;        // pre-pass grid: CTAs per SM (grid-stride; 0: one CTA per 8 items)
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -984,6 +985,11 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
     P.cqc = c->d_cqc.as<unsigned char>();
     P.rowp = (c->rowp_ok && c->opt_rowp) ? c->d_rowp.as<double>() : nullptr;
     P.rows_total = c->rows_total;
+    auto cpre_grid = [&](int64_t items) {
+      const int64_t full = (items + 7) / 8;
+      return (unsigned)std::max<int64_t>(1, c->opt_cpre_ctas > 0 ? std::min<int64_t>(full, c->sm_count * c->opt_cpre_ctas)
+                                                                  : full);
+    };
     // A: (tile, test) threshold + quantile count items
     std::vector<std::pair<int, int>> tests;
     for (int ld : B.cset_leader)
@@ -995,7 +1001,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
         P.ti[j] = (unsigned char)tests[s0 + j].second;
       }
       const int64_t items = (int64_t)P.n_tiles * P.n;
-      cons_thr_kernel<<<(unsigned)((items + 7) / 8), 256, 0, c->side2>>>(P);
+      cons_thr_kernel<<<cpre_grid(items), 256, 0, c->side2>>>(P);
       ++st.launches;
     }
     // B: (tile, set) choice of the most selective test + its exact range
@@ -1003,7 +1009,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       P.n = (int)std::min<size_t>(kConsPreItems, B.cset_leader.size() - s0);
       for (int j = 0; j < P.n; ++j) P.q[j] = B.cset_leader[s0 + j];
       const int64_t items = (int64_t)P.n_tiles * P.n;
-      cons_best_kernel<<<(unsigned)((items + 7) / 8), 256, 0, c->side2>>>(P);
+      cons_best_kernel<<<cpre_grid(items), 256, 0, c->side2>>>(P);
       ++st.launches;
     }
     APEX_CU(cudaEventRecord(c->join2_ev, c->side2));
@@ -2335,6 +2341,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "cpre_ctas") c->opt_cpre_ctas = std::max<int64_t>(0, v);
   else if (n == "work_ctrs") c->opt_work_ctrs = std::max<int64_t>(1, v);
   else if (n == "rowp") {
     c->opt_rowp = v;

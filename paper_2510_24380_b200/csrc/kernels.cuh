@@ -1922,11 +1922,13 @@ struct ConsPre {
   unsigned char ti[kConsPreItems];  // A: test index (1..nt-1)
 };
 
+// (both pre-pass kernels run a capped, grid-stride grid: a grid of every item
+// would take every SM slot first and hold back the seed kernels beside them)
 __global__ void __launch_bounds__(256) cons_thr_kernel(const __grid_constant__ ConsPre P) {
   const unsigned lane = lane_id();
-  const unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned items = P.n_tiles * (unsigned)P.n, step = gridDim.x * (blockDim.x >> 5);
+  for (unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += step) {
   const unsigned t = item / (unsigned)P.n, k = item % (unsigned)P.n;
-  if (t >= P.n_tiles) return;
   const ScanQuery& Q = P.queries[P.q[k]];
   const int i = P.ti[k];
   const Tile T = P.tiles[t];
@@ -1954,13 +1956,14 @@ __global__ void __launch_bounds__(256) cons_thr_kernel(const __grid_constant__ C
   const int64_t o = (int64_t)(Q.cset_off + i - 1) * P.rows_pad + (int64_t)t * 32 + lane;
   P.cthr[o] = th;
   P.cqc[o] = (unsigned char)qc;
+  }
 }
 
 __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ ConsPre P) {
   const unsigned lane = lane_id();
-  const unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const unsigned items = P.n_tiles * (unsigned)P.n, step = gridDim.x * (blockDim.x >> 5);
+  for (unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += step) {
   const unsigned t = item / (unsigned)P.n, si = item % (unsigned)P.n;
-  if (t >= P.n_tiles) return;
   const ScanQuery& Q = P.queries[P.q[si]];
   const Tile T = P.tiles[t];
   const DevReaction& R = P.rx[T.rx];
@@ -1983,6 +1986,7 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
                 best_q, start, cnt);
   }
   P.cbest[(int64_t)Q.cset * P.rows_pad + slot] = make_int4(best, valid ? best_q : kQuant + 2, start, cnt);
+  }
 }
 
 // CTAs per SM of the sorted-column scan (register budget 65536 / (256 x MINB)):
