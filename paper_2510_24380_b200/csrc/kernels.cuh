@@ -3220,14 +3220,26 @@ constexpr int kFinThreads = 512;
 constexpr int kFinWarps = kFinThreads / 32;
 constexpr int kFinMaxSplit = 64;     // CTAs per query (rank splits)
 constexpr int kFinRowsPerCta = 128;  // target ranks per CTA
-constexpr int kFinBatch = 8;     // buffer entries per thread in flight
+#ifndef APEX_FIN_BATCH
+#define APEX_FIN_BATCH 8
+#endif
+constexpr int kFinBatch = APEX_FIN_BATCH;  // buffer entries per thread in flight
 constexpr int kFinRx = 256;      // reactions whose descriptors + g offsets are staged in shared memory
 __host__ __device__ constexpr size_t fin_bucket_smem() {
   return (size_t)kSmallSel * sizeof(Entry) + (size_t)kFinRx * sizeof(DevReaction) +
          (size_t)(kFinRx + 1) * sizeof(unsigned long long);
 }
 
+#ifdef APEX_FIN_DEBUG
+#define FIN_T(i) if (threadIdx.x == 0) t_[i] = clock64();
+#else
+#define FIN_T(i)
+#endif
 __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatLaunch M, int materialize) {
+#ifdef APEX_FIN_DEBUG
+  unsigned long long t_[8] = {};
+#endif
+  FIN_T(0)
   const ScanQuery& Q = M.queries[blockIdx.y];
   QCtl* ctl = Q.ctl;
   if (!*(volatile unsigned int*)&ctl->active) return;
@@ -3288,6 +3300,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
   }
   __syncthreads();
   const unsigned long long n_valid = s_valid;
+  FIN_T(1)
   // the bucketed path takes every set whose CTAs each hold at most kSmallSel
   // entries (k above kSmallSel included, e.g. C4's k = 10,000); otherwise the
   // large path (select / sort / rank / materialize) follows
@@ -3339,6 +3352,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
     }
   }
   __syncthreads();
+  FIN_T(2)
   const unsigned m = min(cnt, (unsigned)kSmallSel);
   unsigned P = 32;  // at least one warp's worth: sorted by warp shuffles
   while (P < m) P <<= 1;
@@ -3348,6 +3362,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
   }
   __syncthreads();
   bitonic_best_first(es, P);
+  FIN_T(3)
   const unsigned n_out = (unsigned)min((unsigned long long)m, kk - off);
   for (unsigned i = threadIdx.x; i < n_out; i += blockDim.x) {
     const unsigned long long r = off + i;
@@ -3357,6 +3372,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
     if (materialize) materialize_row(M, Q, r, e.g, stage_rx ? s_goff : nullptr, stage_rx ? s_rx : nullptr);
     if (r == kk - 1 && kk == (unsigned long long)Q.k && e.key > ctl->tau_key) ctl->tau_key = e.key;
   }
+#ifdef APEX_FIN_DEBUG
+  __syncthreads();
+  FIN_T(4)
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x + 1 == gridDim.x || m > 1024))
+    printf("FIN q %u cta %u/%u n %llu m %u P %u off %llu cycles: prologue %llu load %llu sort %llu mat %llu\n", blockIdx.y,
+           blockIdx.x, gridDim.x, n, m, P, off, t_[1] - t_[0], t_[2] - t_[1], t_[3] - t_[2], t_[4] - t_[3]);
+#endif
 }
 
 // Multi-GPU: export the local selected set (unordered) to out + slot*stride;
