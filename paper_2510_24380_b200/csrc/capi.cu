@@ -244,6 +244,7 @@ struct apex_ctx {
   uint64_t stamp = 0;
   cudaEvent_t ev[8] = {};
   cudaEvent_t upload_ev = nullptr;
+  cudaEvent_t done_ev = nullptr;         // end of a pass (wait_stream's poll)
   std::vector<ScanQuery> uploaded;   // last ScanQuery array copied to d_queries
   Batch batch;
   // options
@@ -275,6 +276,7 @@ struct apex_ctx {
   int64_t opt_split_cols = 0;       // whole-row tiles of reactions with >= this many columns get split_rows rows (0: off)
   int64_t opt_split_rows = 8;
   int64_t opt_cpre_ctas = 0;        // pre-pass grid: CTAs per SM (grid-stride; 0: one CTA per 8 items)
+  int64_t opt_spin_us = 0;          // wait for a pass by polling its end event for up to this long (0: block; measured neutral)
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -1278,6 +1280,26 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   return APEX_OK;
 }
 
+// Wait for the pass on the context stream.  opt_spin_us > 0: poll an event
+// recorded at the end of the pass for up to that long before a blocking
+// synchronize — the waiting thread resumes within a poll of the GPU finishing
+// instead of after the driver's wake-up of a blocked or yielding thread.
+int wait_stream(apex_ctx* c) {
+  if (c->opt_spin_us > 0 && c->done_ev) {
+    APEX_CU(cudaEventRecord(c->done_ev, c->stream));
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t e = cudaEventQuery(c->done_ev);
+      if (e == cudaSuccess) return APEX_OK;
+      if (e != cudaErrorNotReady) APEX_CU(e);
+      if (std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() > c->opt_spin_us)
+        break;
+    }
+  }
+  APEX_CU(cudaStreamSynchronize(c->stream));
+  return APEX_OK;
+}
+
 // Sync, detect candidate-buffer overflow, re-run exactly if needed.  A re-run
 // is preset from the overflowed run's control block (finalize_small_kernel
 // nx_*): the admission threshold at the k-th best bin and a 16-bit narrower
@@ -1292,7 +1314,7 @@ int check_batch(apex_ctx* c) {
   const int nq = B.nq;
   std::vector<RunPreset> pre(nq);
   for (int attempt = 0;; ++attempt) {
-    APEX_CU(cudaStreamSynchronize(c->stream));
+    APEX_TRY(wait_stream(c));
     if (B.small_only) {
       // the large path was skipped on the strength of this signature's last
       // run: if a query did not fit the small finalize now, run it again whole
@@ -1798,6 +1820,7 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   for (auto& ev : c->mev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&c->upload_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
@@ -1850,6 +1873,7 @@ void apex_ctx_destroy(apex_ctx* c) {
     for (HBuf* b : {&w.h_queries, &w.h_ctl, &w.h_out}) b->release();
   }
   if (c->upload_ev) cudaEventDestroy(c->upload_ev);
+  if (c->done_ev) cudaEventDestroy(c->done_ev);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   if (c->side) cudaStreamDestroy(c->side);
@@ -2341,6 +2365,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "spin_us") c->opt_spin_us = std::max<int64_t>(0, v);
   else if (n == "cpre_ctas") c->opt_cpre_ctas = std::max<int64_t>(0, v);
   else if (n == "work_ctrs") c->opt_work_ctrs = std::max<int64_t>(1, v);
   else if (n == "rowp") {
