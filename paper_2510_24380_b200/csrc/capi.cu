@@ -1090,7 +1090,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
     }
     {
-      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used);
+      tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used, (unsigned long long)span);
       ++st.launches;
     }
   }

@@ -2631,8 +2631,9 @@ __global__ void corner_kernel(const CornerLaunch P) {
 //           seed_max] spread over ~1/4 of its bins;
 //   mode 1: raise tau from the candidate histogram;
 //   mode 2: final bound (and the count at/above it) for the select.
+constexpr double kSortedFeasibleMax = 65536.0;  // auto choice: estimated feasible products above this -> full predicate
 __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, int auto_kernel = 0,
-                           unsigned long long samples = 0) {
+                           unsigned long long samples = 0, unsigned long long span = 0) {
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const ScanQuery& Q = qs[q];
@@ -2685,8 +2686,16 @@ __global__ void tau_kernel(const ScanQuery* __restrict__ qs, int nq, int mode, i
       // feasible set is not sparse — the uniform samples found more than
       // 1/512 feasible: there the streaming full predicate beats enumerating
       // broad sorted ranges; sparse ones (e.g. Astex RO3) take the sorted kernel)
+      // ... and for threshold-less queries whose feasible set, estimated from
+      // the samples, is large in absolute terms: without a threshold the
+      // sorted-column kernel appends every feasible product it enumerates
+      // (~20 ns each), the full predicate costs ~1 ps per product
+      // (C5 over 1e9: 1.1M feasible of 1e9 took 23 ms sorted, 0.9 ms full)
       if (auto_kernel == 2)
-        ctl->use_full = (ctl->tau_key == kNoTau && (Q.nt == 1 || a0 * 512ull > samples)) ? 1u : 0u;
+        ctl->use_full = (ctl->tau_key == kNoTau &&
+                         (Q.nt == 1 || a0 * 512ull > samples ||
+                          (samples > 0 && (double)a0 * (double)span / (double)samples > kSortedFeasibleMax)))
+                            ? 1u : 0u;
       if (auto_kernel == 3) ctl->use_full = 0u;  // no full-predicate launch in this pass
     }
   } else {

@@ -43,10 +43,15 @@ def main():
     for pb in pbs[:5]:
         ctx.run(pb)
     lat, single, full, kern, cand, tot = [], [], [], [], [], []
-    for pb in pbs:
+    detail = []
+    for qi, pb in enumerate(pbs):
         t0 = time.perf_counter()
         r, st1 = ctx.run(pb)
         lat.append((time.perf_counter() - t0) * 1e3)
+        detail.append({"i": qi, "ms": round(lat[-1], 3), "k": qs[qi]["k"], "n_cons": len(qs[qi].get("cons", [])),
+                       "full": bool(r[0]["full_predicate"]), "cand": st1["candidates"], "retries": st1["retries"],
+                       "seed": round(st1["seed_ms"], 3), "scan": round(st1["scan_kernel_ms"], 3),
+                       "select": round(st1["select_ms"], 3), "total": round(st1["total_ms"], 3)})
         single.append((r[0]["g"].copy(), r[0]["objective"].copy()))
         full.append(r[0]["full_predicate"])
         kern.append(st1["scan_kernel_ms"])
@@ -77,7 +82,8 @@ def main():
         "retries_batched": st["retries"], "candidates_mean": float(np.mean(cand)),
         "scan_kernel_ms_p50": float(np.percentile(kern, 50)), "scan_kernel_ms_p99": float(np.percentile(kern, 99)),
         "device_total_ms_p50": float(np.percentile(tot, 50)) if len(tot) else None,
-        "host_ms_p50": float(np.percentile(lat - tot, 50)) if len(tot) == len(lat) else None}))
+        "host_ms_p50": float(np.percentile(lat - tot, 50)) if len(tot) == len(lat) else None,
+        "slowest": sorted(detail, key=lambda d: -d["ms"])[:8]}))
 
 
 if __name__ == "__main__":
