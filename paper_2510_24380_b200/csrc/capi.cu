@@ -277,6 +277,8 @@ struct apex_ctx {
   int64_t opt_split_rows = 8;
   int64_t opt_cpre_ctas = 0;        // pre-pass grid: CTAs per SM (grid-stride; 0: one CTA per 8 items)
   int64_t opt_spin_us = 0;          // wait for a pass by polling its end event for up to this long (0: block; measured neutral)
+  int64_t opt_bail = 128;           // sorted-column pair budget: range / this (0: no budget)
+  int64_t opt_bail_min = 4 << 20;   // ... and at least this many pairs
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -776,6 +778,14 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
       Q.refresh_shift = sh;
     }
     Q.k = q.k;
+    // pair budget of the sorted-column kernel (automatic choice only): a
+    // query that would enumerate more than 1/kBailDiv of its range gives up
+    // and re-runs with the full predicate (which exists for its test count)
+    Q.admit_budget = ~0ull;
+    if (c->opt_mode == 3 && c->opt_bail > 0 && pick_scan(kernel_nt(T.nt), 1, 0)) {
+      const uint64_t span = q.end - q.start;
+      Q.admit_budget = std::max<uint64_t>((uint64_t)c->opt_bail_min, span / (uint64_t)c->opt_bail);
+    }
     Q.nt = T.nt;
     Q.ntp = (kernel_nt(T.nt) + 3) / 4 * 4;
     Q.slot = B.perm[i];
@@ -1313,6 +1323,7 @@ int check_batch(apex_ctx* c) {
   if (!B.pending) return set_err(APEX_ESTATE, "no query batch in flight");
   const int nq = B.nq;
   std::vector<RunPreset> pre(nq);
+  std::vector<int> pre_full(nq, 0);          // queries moved to the full predicate (bail-out)
   for (int attempt = 0;; ++attempt) {
     APEX_TRY(wait_stream(c));
     if (B.small_only) {
@@ -1336,6 +1347,19 @@ int check_batch(apex_ctx* c) {
       std::memset(&P, 0, sizeof(P));
       P.tie_glimit = ~0ull;
       P.tie_gshift = 48;
+      if (C.bail) {
+        // the sorted-column kernel gave the query up (pair budget): re-run it
+        // with the full predicate from the admission key it had reached (a
+        // valid lower bound on its k-th best key)
+        overflow = true;
+        pre_full[i] = 1;
+        P.full = 1;
+        P.tau = C.bail_tau;
+        P.base = C.bail_tau;
+        P.shift = C.hist_shift;
+        continue;
+      }
+      P.full = pre_full[i] ? 1u : 0u;  // stays on the full predicate in any further re-run
       if (C.count > c->uploaded[i].cap) {
         overflow = true;
         P.tau = C.nx_tau;
@@ -1380,6 +1404,7 @@ int check_batch(apex_ctx* c) {
       return set_err(APEX_ELIMIT, "candidate buffer overflow did not converge");
     }
     ++B.st.retries;
+    if (std::find(pre_full.begin(), pre_full.end(), 1) != pre_full.end()) B.no_full = false;  // full launches needed
     APEX_TRY(enqueue_batch(c, pre.data()));
   }
   B.pending = false;
@@ -2398,6 +2423,8 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "bail") c->opt_bail = std::max<int64_t>(0, v);
+  else if (n == "bail_min") c->opt_bail_min = std::max<int64_t>(1, v);
   else if (n == "spin_us") c->opt_spin_us = std::max<int64_t>(0, v);
   else if (n == "cpre_ctas") c->opt_cpre_ctas = std::max<int64_t>(0, v);
   else if (n == "work_ctrs") c->opt_work_ctrs = std::max<int64_t>(1, v);

@@ -94,7 +94,9 @@ struct QCtl {
   unsigned int nx_gshift;
   unsigned int nx_tie_enter;      // 1: first tie run (host sets the g range from the query range)
   unsigned int stale;             // merge: some source exported an overflowed (stale) local result
-  unsigned int _pad5;
+  unsigned int bail;              // sorted-column kernel gave the query up (pair budget spent): re-run full
+  unsigned long long admit_live;  // pairs the sorted-column kernel has enumerated for the query so far
+  unsigned long long bail_tau;    // the admission key when it gave up (a valid lower bound for the re-run)
   unsigned int hist[3][256];      // select histograms (triple-buffered)
 };
 
@@ -109,7 +111,7 @@ struct RunPreset {
   unsigned int shift;
   unsigned int tie_on;
   unsigned int tie_gshift;
-  unsigned int _pad;
+  unsigned int full;              // 1: run the query with the full-predicate kernel (sorted-column bail-out)
 };
 
 constexpr int kHistBins = 65536;  // candidate histogram bins
@@ -149,6 +151,7 @@ struct ScanQuery {
   QCtl* ctl;
   unsigned long long cap;         // capacity of buf / comp (entries)
   unsigned long long refresh_shift;  // in-kernel tau refresh every 2^refresh_shift appended candidates
+  unsigned long long admit_budget;   // sorted-column kernel: pairs it may enumerate before giving the query up (~0: none)
   long long k;
   int32_t nt;                     // live tests (test 0 = objective admission)
   int32_t ntp;                    // packed row stride (floats, multiple of 4)

@@ -397,7 +397,10 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPrese
     c->nx_tie = 0;
     c->nx_tie_enter = 0;
     c->stale = 0;
-    c->use_full = use_full;
+    c->use_full = use_full || (P && P->full) ? 1u : 0u;
+    c->bail = 0;
+    c->admit_live = 0;
+    c->bail_tau = 0;
     c->small_done = 0;
     c->mat_done = 0;
     c->seed_max = 0;
@@ -1796,6 +1799,7 @@ constexpr int kThrBatch = APEX_THR_BATCH;  // tests whose threshold chains are i
 // 8 were slower on C2 — more issue slots and registers for a loop that is not
 // latency-bound, profiles/r2_ab_pair_batch_rejected.log)
 constexpr int kPairBatch = APEX_PAIR_BATCH;
+constexpr unsigned kBailFlush = 4096;  // sorted-column pair budget: per-CTA pairs between flushes
 __device__ __forceinline__ void quant_count4(const float* __restrict__ qbase, int64_t qstride,
                                              const int (&task)[kThrBatch], const bool (&lower)[kThrBatch],
                                              const float (&th)[kThrBatch], int (&qc)[kThrBatch]) {
@@ -2028,7 +2032,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   const float* __restrict__ p16 = S.packed16;
   const int64_t n_pairs = L.n_pairs;
   __shared__ unsigned s_adm[64];  // admitted products per query of the launch (statistics)
-  for (int q = threadIdx.x; q < 64; q += blockDim.x) s_adm[q] = 0;
+  __shared__ unsigned s_live[64];  // enumerated pairs per query not yet flushed to the pair budget
+  for (int q = threadIdx.x; q < 64; q += blockDim.x) s_adm[q] = s_live[q] = 0;
   __syncthreads();
   auto ld = [&](int task, int64_t pair) -> float {
     return P16 ? __ldg(p16 + pair * 16 + task) : __ldg(values + (int64_t)task * n_pairs + pair);
@@ -2251,6 +2256,25 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       if ((int)lane >= o) incl += y;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
+    // pair budget (automatic kernel choice): the pairs this query enumerates
+    // are summed per CTA and flushed to its control block every kBailFlush;
+    // past the budget the query is given up — its admission key is raised to
+    // the maximum, so its remaining items enumerate nothing — and the host
+    // re-runs it with the full predicate, which is cheaper for such queries
+    if (total > 0 && Q.admit_budget != ~0ull && lane == 0) {
+      const unsigned old = atomicAdd(&s_live[q_cur], (unsigned)total);
+      if ((unsigned long long)(old + (unsigned)total) >= min((unsigned long long)kBailFlush, Q.admit_budget)) {
+        const unsigned v = atomicExch(&s_live[q_cur], 0u);
+        if (v && atomicAdd(&ctl->admit_live, (unsigned long long)v) + v > Q.admit_budget &&
+            ld_relaxed_u64(&ctl->tau_key) != ~0ull) {
+          const unsigned long long prev = atomicExch(&ctl->tau_key, ~0ull);
+          if (prev != ~0ull) {
+            ctl->bail_tau = prev;
+            ctl->bail = 1u;
+          }
+        }
+      }
+    }
     // sorted position of flat index j of this lane's row: sbase + j
     const int64_t sbase = (int64_t)Q.test_task[best] * S.pcols + R.pcol_off + start - (incl - cnt);
     __syncwarp();
@@ -2269,6 +2293,8 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     w_rounds += (total + 31) / 32;
 #endif
     for (int j0 = 0; j0 < total; j0 += 32) {
+      // a query given up (pair budget) stops its items in flight too
+      if (((j0 >> 5) & 15) == 15 && Q.admit_budget != ~0ull && ld_relaxed_u64(&ctl->tau_key) == ~0ull) break;
       const int jj = j0 + (int)lane;
       const int j = jj < total ? jj : total - 1;
       // owning row: smallest r with incl[r] > j

@@ -49,7 +49,7 @@ def main():
         r, st1 = ctx.run(pb)
         lat.append((time.perf_counter() - t0) * 1e3)
         detail.append({"i": qi, "ms": round(lat[-1], 3), "k": qs[qi]["k"], "n_cons": len(qs[qi].get("cons", [])),
-                       "full": bool(r[0]["full_predicate"]), "cand": st1["candidates"], "retries": st1["retries"],
+                       "full": bool(r[0]["full_predicate"]), "cand": st1["candidates"], "admitted": st1.get("admitted"), "retries": st1["retries"],
                        "seed": round(st1["seed_ms"], 3), "scan": round(st1["scan_kernel_ms"], 3),
                        "select": round(st1["select_ms"], 3), "total": round(st1["total_ms"], 3)})
         single.append((r[0]["g"].copy(), r[0]["objective"].copy()))
