@@ -3422,7 +3422,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
 __global__ void export_kernel(const ScanQuery* __restrict__ qs, Entry* __restrict__ out, unsigned long long stride) {
   const ScanQuery& Q = qs[blockIdx.y];
   const unsigned long long n = *(volatile unsigned long long*)&Q.ctl->sel_count;
-  const bool stale = *(volatile unsigned long long*)&Q.ctl->count > Q.cap;  // overflowed: re-run pending
+  // overflowed or given up by the sorted-column kernel: a re-run is pending
+  const bool stale = *(volatile unsigned long long*)&Q.ctl->count > Q.cap || *(volatile unsigned*)&Q.ctl->bail;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < stride;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     Entry e;

@@ -145,7 +145,7 @@ def _rank_main(rank, world, port, seed, ties, out):
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    if ties:  # all-zero table: every local candidate set overflows the minimum capacity
+    if ties is True:  # all-zero table: every local candidate set overflows the minimum capacity
         sizes, pair_off, p = [[300, 200], [40, 30, 20]], [[0, 300], [500, 540, 570]], 590
         values, biases = np.zeros((1, p), dtype=np.float32), np.zeros(1)
     else:
@@ -154,13 +154,18 @@ def _rank_main(rank, world, port, seed, ties, out):
     ctx = _native.DeviceContext(0, stream.cuda_stream)
     ctx.load_library(sizes, pair_off, lib.offsets[:-1], p)
     ctx.load_table(values, biases)
-    if ties:
+    if ties is True:
         qs = [{"obj": 0, "maximize": True, "cons": [], "k": 700, "start": 0, "end": lib.total}]
         if rank == 1:  # only rank 1 overflows: the ranks must still agree on the re-gather
             ctx.set_option("cap", 1024)
             ctx.set_option("samples", 16)
     else:
         qs = [q for q in _queries(lib.total) if q["k"] > 0]
+        if ties == "bail" and rank == 1:
+            # only rank 1's sorted-column kernel gives its queries up (a
+            # one-pair budget): its exports are marked stale and re-gathered
+            ctx.set_option("bail", 1_000_000_000)
+            ctx.set_option("bail_min", 1)
     res, info = sharded_batch(ctx, qs)
     ref = _native.DeviceContext(0)
     ref.load_library(sizes, pair_off, lib.offsets[:-1], p)
@@ -172,7 +177,7 @@ def _rank_main(rank, world, port, seed, ties, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("ties", [False, True])
+@pytest.mark.parametrize("ties", [False, True, "bail"])
 def test_two_ranks_stream_ordered_protocol(native, ties):
     import torch.multiprocessing as mp
 
@@ -182,4 +187,4 @@ def test_two_ranks_stream_ordered_protocol(native, ties):
     assert out[0][0] and out[1][0]
     assert out[0][1] == out[1][1]  # every rank agreed on the number of gather rounds
     if ties:
-        assert out[0][1] >= 2  # the overflowed local results were marked stale and gathered again
+        assert out[0][1] >= 2  # the overflowed / given-up local results were marked stale and gathered again
