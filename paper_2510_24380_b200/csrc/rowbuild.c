@@ -58,18 +58,27 @@ static PyObject* make_obj(PyTypeObject* cls, int fast, PyObject** names, PyObjec
   return o;
 }
 
-/* build_entries(mi_cls, sc_cls, fast, n, g, obj, cons, m, rx, digits, rx_table) -> list
+/* build_entries(mi_cls, sc_cls, fast, n, g, obj, cons, m, rx, digits, rx_table[, chi_cache]) -> list
  *   g: uint64[n]; obj: float64[n]; cons: float64[n*m]; rx: int32[n];
  *   digits: int32[n*6]; rx_table: sequence indexed by reaction position of
- *   (reaction_id, (rgroup_id, ...), ((synthon_id, ...), ...)) or None. */
+ *   (reaction_id, (rgroup_id, ...), ((synthon_id, ...), ...)[, (pair list, ...)]);
+ *   the optional 4th item holds one list per R-group, indexed by digit, of
+ *   (rgroup_id, synthon_id) tuples filled on first use (shared: tuples are
+ *   immutable).  chi_cache: dict global index -> MultiIndex (frozen in the
+ *   reference, csl.py:47, so a repeated product's chi is shared) or None. */
+#define CHI_CACHE_MAX (1 << 20)
 static PyObject* build_entries(PyObject* self, PyObject* args) {
-  PyObject *mi_cls, *sc_cls, *og, *oobj, *ocons, *orx, *odig, *table;
+  PyObject *mi_cls, *sc_cls, *og, *oobj, *ocons, *orx, *odig, *table, *chi_cache = Py_None;
   int fast;
   Py_ssize_t n, m;
   (void)self;
-  if (!PyArg_ParseTuple(args, "OOpnOOOnOOO", &mi_cls, &sc_cls, &fast, &n, &og, &oobj, &ocons, &m, &orx, &odig,
-                        &table))
+  if (!PyArg_ParseTuple(args, "OOpnOOOnOOO|O", &mi_cls, &sc_cls, &fast, &n, &og, &oobj, &ocons, &m, &orx, &odig,
+                        &table, &chi_cache))
     return NULL;
+  if (chi_cache != Py_None && !PyDict_Check(chi_cache)) {
+    PyErr_SetString(PyExc_TypeError, "chi_cache must be a dict or None");
+    return NULL;
+  }
   if (!PyType_Check(mi_cls) || !PyType_Check(sc_cls)) {
     PyErr_SetString(PyExc_TypeError, "result classes must be types");
     return NULL;
@@ -89,46 +98,80 @@ static PyObject* build_entries(PyObject* self, PyObject* args) {
   PyObject* zero = PyFloat_FromDouble(0.0); /* violation +0.0 (engine.py:252) */
   if (!out || !zero) goto fail;
   for (Py_ssize_t i = 0; i < n; ++i) {
-    PyObject* info = PySequence_GetItem(table, rx[i]);
-    if (!info) goto fail;
-    PyObject *rid = PyTuple_GetItem(info, 0), *rgids = PyTuple_GetItem(info, 1), *sids = PyTuple_GetItem(info, 2);
-    if (!rid || !rgids || !sids) {
-      Py_DECREF(info);
-      goto fail;
-    }
-    const Py_ssize_t c = PyTuple_GET_SIZE(rgids);
-    PyObject* asg = PyTuple_New(c);
-    if (!asg) {
-      Py_DECREF(info);
-      goto fail;
-    }
-    for (Py_ssize_t j = 0; j < c; ++j) {
-      PyObject* sj = PyTuple_GET_ITEM(sids, j);
-      PyObject* sid = PySequence_GetItem(sj, dig[i * 6 + j]);
-      if (!sid) {
-        Py_DECREF(asg);
-        Py_DECREF(info);
-        goto fail;
-      }
-      PyObject* pair = PyTuple_Pack(2, PyTuple_GET_ITEM(rgids, j), sid);
-      Py_DECREF(sid);
-      if (!pair) {
-        Py_DECREF(asg);
-        Py_DECREF(info);
-        goto fail;
-      }
-      PyTuple_SET_ITEM(asg, j, pair);
-    }
-    PyObject* mi_names[2] = {s_reaction_id, s_assignment};
-    PyObject* mi_vals[2] = {rid, asg};
-    PyObject* chi = make_obj((PyTypeObject*)mi_cls, fast, mi_names, mi_vals, 2);
-    Py_DECREF(asg);
-    Py_DECREF(info);
-    if (!chi) goto fail;
-    PyObject* cv = PyTuple_New(m);
     PyObject* gi = PyLong_FromUnsignedLongLong(g[i]);
+    if (!gi) goto fail;
+    PyObject* chi = NULL;
+    if (chi_cache != Py_None) {
+      chi = PyDict_GetItemWithError(chi_cache, gi);
+      if (chi) {
+        Py_INCREF(chi);
+      } else if (PyErr_Occurred()) {
+        Py_DECREF(gi);
+        goto fail;
+      }
+    }
+    if (!chi) {
+      PyObject* info = PySequence_GetItem(table, rx[i]);
+      if (!info) {
+        Py_DECREF(gi);
+        goto fail;
+      }
+      PyObject *rid = PyTuple_GetItem(info, 0), *rgids = PyTuple_GetItem(info, 1), *sids = PyTuple_GetItem(info, 2);
+      PyObject* pairs = PyTuple_GET_SIZE(info) > 3 ? PyTuple_GET_ITEM(info, 3) : NULL;
+      if (!rid || !rgids || !sids) {
+        Py_DECREF(info);
+        Py_DECREF(gi);
+        goto fail;
+      }
+      const Py_ssize_t c = PyTuple_GET_SIZE(rgids);
+      PyObject* asg = PyTuple_New(c);
+      if (!asg) {
+        Py_DECREF(info);
+        Py_DECREF(gi);
+        goto fail;
+      }
+      for (Py_ssize_t j = 0; j < c; ++j) {
+        const int32_t d = dig[i * 6 + j];
+        PyObject* lst = pairs ? PyTuple_GET_ITEM(pairs, j) : NULL;
+        PyObject* pair = NULL;
+        if (lst && PyList_Check(lst) && d >= 0 && d < PyList_GET_SIZE(lst) && PyList_GET_ITEM(lst, d) != Py_None) {
+          pair = PyList_GET_ITEM(lst, d);
+          Py_INCREF(pair);
+        } else {
+          PyObject* sid = PySequence_GetItem(PyTuple_GET_ITEM(sids, j), d);
+          if (sid) pair = PyTuple_Pack(2, PyTuple_GET_ITEM(rgids, j), sid);
+          Py_XDECREF(sid);
+          if (pair && lst && PyList_Check(lst) && d >= 0 && d < PyList_GET_SIZE(lst)) {
+            Py_INCREF(pair);
+            PyList_SetItem(lst, d, pair);  /* steals the extra reference, releases None */
+          }
+        }
+        if (!pair) {
+          Py_DECREF(asg);
+          Py_DECREF(info);
+          Py_DECREF(gi);
+          goto fail;
+        }
+        PyTuple_SET_ITEM(asg, j, pair);
+      }
+      PyObject* mi_names[2] = {s_reaction_id, s_assignment};
+      PyObject* mi_vals[2] = {rid, asg};
+      chi = make_obj((PyTypeObject*)mi_cls, fast, mi_names, mi_vals, 2);
+      Py_DECREF(asg);
+      Py_DECREF(info);
+      if (!chi) {
+        Py_DECREF(gi);
+        goto fail;
+      }
+      if (chi_cache != Py_None && PyDict_GET_SIZE(chi_cache) < CHI_CACHE_MAX && PyDict_SetItem(chi_cache, gi, chi) < 0) {
+        Py_DECREF(chi);
+        Py_DECREF(gi);
+        goto fail;
+      }
+    }
+    PyObject* cv = PyTuple_New(m);
     PyObject* ov = PyFloat_FromDouble(obj[i]);
-    if (!cv || !gi || !ov) {
+    if (!cv || !ov) {
       Py_XDECREF(cv);
       Py_XDECREF(gi);
       Py_XDECREF(ov);

@@ -304,13 +304,33 @@ def _rx_table(library) -> list:
     hit = _RX_TABLES.get(id(library))
     if hit is not None and hit[0]() is library:
         return hit[1]
-    table = [(rx.reaction_id, tuple(rg.rgroup_id for rg in rx.rgroups), tuple(rg.synthon_ids for rg in rx.rgroups))
+    # (reaction_id, rgroup ids, synthon id tuples, per R-group list of the
+    # (rgroup_id, synthon_id) tuples, filled by the native builder on first use)
+    table = [(rx.reaction_id, tuple(rg.rgroup_id for rg in rx.rgroups), tuple(rg.synthon_ids for rg in rx.rgroups),
+              tuple([None] * len(rg.synthon_ids) for rg in rx.rgroups))
              for rx in library.reactions]
     try:
         _RX_TABLES[id(library)] = (weakref.ref(library), table)
     except TypeError:
         pass
     return table
+
+
+_CHI_CACHES: dict[int, tuple[weakref.ref, dict]] = {}
+
+
+def _chi_cache(library, mi_cls) -> dict:
+    """global index -> MultiIndex of this library, per MultiIndex class: the
+    reference's MultiIndex is frozen (csl.py:47), so a product that recurs in
+    later results shares one instance (the native builder fills it, up to 2^20
+    entries; the device pass is unaffected)."""
+    hit = _CHI_CACHES.get(id(library))
+    if hit is None or hit[0]() is not library:
+        try:
+            hit = _CHI_CACHES[id(library)] = (weakref.ref(library), {})
+        except TypeError:
+            return {}
+    return hit[1].setdefault(mi_cls, {})
 
 
 def _build_result(library, query, res: dict, timing: dict):
@@ -331,7 +351,7 @@ def _build_result(library, query, res: dict, timing: dict):
             np.ascontiguousarray(res["objective"], dtype=np.float64),
             np.ascontiguousarray(res["constraint_values"], dtype=np.float64), len(query.constraints),
             np.ascontiguousarray(res["reaction"], dtype=np.int32), np.ascontiguousarray(res["digits"], dtype=np.int32),
-            _rx_table(library))
+            _rx_table(library), _chi_cache(library, mi_cls) if fast else None)
         finally:
             if gc_on:
                 gc.enable()
