@@ -1094,7 +1094,9 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       // seeds across the reactions, within the precomputed list lengths
       const int64_t nrx = std::max<int64_t>(1, (int64_t)c->rx.size());
       CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, c->opt_corner_mult * B.k_max / nrx));
-      corner_kernel<<<dim3((unsigned)c->rx.size(), nq), 256, 0, c->side>>>(CL);
+      const int64_t per_rx = (int64_t)c->rx.size() * nq;
+      const unsigned split = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8, (2 * (int64_t)c->sm_count + per_rx - 1) / std::max<int64_t>(per_rx, 1)));
+      corner_kernel<<<dim3((unsigned)c->rx.size(), nq, split), 256, 0, c->side>>>(CL);
       ++st.launches;
       APEX_CU(cudaEventRecord(c->join_ev, c->side));
       APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));

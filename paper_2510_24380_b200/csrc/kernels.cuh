@@ -2594,7 +2594,9 @@ __global__ void corner_kernel(const CornerLaunch P) {
   const int dir = Q.maximize ? 0 : 1;
   const int32_t* list = P.lists + ((int64_t)Q.test_task[0] * 2 + dir) * P.slots;
   const unsigned lane = lane_id();
-  for (unsigned base_i = 0; base_i < total; base_i += blockDim.x) {
+  // grid.z CTAs share a reaction's corner (few reactions x queries: C4 has
+  // 120 reactions and one query, so one CTA per reaction left SMs idle)
+  for (unsigned base_i = blockIdx.z * blockDim.x; base_i < total; base_i += blockDim.x * gridDim.z) {
     const unsigned i = base_i + threadIdx.x;
     unsigned long long key = 0;
     if (i < total) {
