@@ -237,6 +237,7 @@ struct apex_ctx {
   DBuf d_out;                            // per-query result rows, contiguous (one D2H per batch)
   std::vector<size_t> out_off;           // byte offset of each query's rows in d_out
   DBuf d_work;                           // flattened-work counters of the scan launches
+  DBuf d_fin_scratch;                    // bucketed finalize partition regions [query][CTA][kSmallSel]
   DBuf d_trace;                          // optional per-item timing records of the admission scan
   int64_t trace_cap = 0, trace_n = 0;
   HBuf h_queries, h_ctl, h_out, h_tau0;
@@ -279,6 +280,7 @@ struct apex_ctx {
   int64_t opt_spin_us = 0;          // wait for a pass by polling its end event for up to this long (0: block; measured neutral)
   int64_t opt_bail = 128;           // sorted-column pair budget: range / this (0: no budget)
   int64_t opt_bail_min = 4 << 20;   // ... and at least this many pairs
+  int64_t opt_fin_part = 1;         // bucketed finalize partitions the buffer (cooperative) instead of full scans per CTA
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (1: forked after the control init, 2: at the pass start, 0: off)
@@ -666,6 +668,14 @@ int build_corners(apex_ctx* c) {
 // enqueue (device pipeline, no host sync), check (one sync: overflow check and
 // exact re-run with the final bound if the candidate buffer overflowed).
 
+// CTAs per query of the bucketed finalize: about kFinRowsPerCta ranks each,
+// within one wave (one CTA per SM) and kFinMaxSplit
+int fin_splits(const apex_ctx* c, int64_t k_max, int nq) {
+  const int64_t want = (k_max + kFinRowsPerCta - 1) / kFinRowsPerCta;
+  return (int)std::max<int64_t>(
+      1, std::min<int64_t>({want, c->opt_fin_bucket, (int64_t)kFinMaxSplit, (int64_t)c->sm_count / std::max(nq, 1)}));
+}
+
 int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finalize) {
   Batch& B = c->batch;
   if (!c->corners_ok) APEX_TRY(build_corners(c));
@@ -753,6 +763,9 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
   APEX_TRY(c->d_work.ensure(kWorkWords * sizeof(unsigned)));
   APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
+  if (c->opt_fin_bucket && c->opt_fin_part && fin_splits(c, B.k_max, nq) >= kFinSuffixMin)
+    // partitioned bucketed finalize: one region per (query, CTA)
+    APEX_TRY(c->d_fin_scratch.ensure((size_t)nq * fin_splits(c, B.k_max, nq) * kSmallSel * sizeof(Entry)));
   std::vector<ScanQuery> hq(nq);
   for (int i = 0; i < nq; ++i) {
     Slot& S = c->slots[i];
@@ -902,11 +915,20 @@ int enqueue_select(apex_ctx* c, const ScanQuery* dq, int nq, int64_t k_max, bool
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bucket));
         c->attr_bucket = true;
       }
-      // about kFinRowsPerCta ranks per CTA, within one wave and kFinMaxSplit
-      const int64_t want = (k_max + kFinRowsPerCta - 1) / kFinRowsPerCta;
-      const int ns = (int)std::max<int64_t>(
-          1, std::min<int64_t>({want, c->opt_fin_bucket, (int64_t)kFinMaxSplit, (int64_t)c->sm_count / std::max(nq, 1)}));
-      finalize_bucket_kernel<<<dim3((unsigned)ns, (unsigned)nq), kFinThreads, smem_bucket, s>>>(M, finalize ? 1 : 0);
+      const int ns = fin_splits(c, k_max, nq);
+      // partitioned (cooperative: the CTAs of a query meet at a barrier) when
+      // the scratch regions were allocated with the batch
+      const bool part = c->opt_fin_part && ns >= kFinSuffixMin &&
+                        c->d_fin_scratch.bytes >= (size_t)nq * ns * kSmallSel * sizeof(Entry);
+      int mat = finalize ? 1 : 0;
+      Entry* scratch = part ? c->d_fin_scratch.as<Entry>() : nullptr;
+      if (part) {
+        void* args[] = {(void*)&M, (void*)&mat, (void*)&scratch};
+        APEX_CU(cudaLaunchCooperativeKernel((const void*)finalize_bucket_kernel, dim3((unsigned)ns, (unsigned)nq),
+                                            dim3(kFinThreads), args, smem_bucket, s));
+      } else {
+        finalize_bucket_kernel<<<dim3((unsigned)ns, (unsigned)nq), kFinThreads, smem_bucket, s>>>(M, mat, scratch);
+      }
     } else {
       // (materialization runs after, for every query, in materialize_kernel)
       finalize_small_kernel<<<nq, 1024, smem_small, s>>>(M, 0, compute_bound ? 1 : 0);
@@ -1915,7 +1937,7 @@ void apex_ctx_destroy(apex_ctx* c) {
   c->d_ctls.release();
   c->d_out.release();
   c->d_work.release();
-  for (DBuf* b : {&c->d_rowp, &c->d_cthr, &c->d_cqc, &c->d_cbest}) b->release();
+  for (DBuf* b : {&c->d_rowp, &c->d_fin_scratch, &c->d_cthr, &c->d_cqc, &c->d_cbest}) b->release();
   c->d_trace.release();
   c->h_queries.release();
   c->h_ctl.release();
@@ -2425,6 +2447,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "fin_part") c->opt_fin_part = v;
   else if (n == "bail") c->opt_bail = std::max<int64_t>(0, v);
   else if (n == "bail_min") c->opt_bail_min = std::max<int64_t>(1, v);
   else if (n == "spin_us") c->opt_spin_us = std::max<int64_t>(0, v);

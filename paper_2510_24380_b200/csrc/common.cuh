@@ -95,6 +95,8 @@ struct QCtl {
   unsigned int nx_tie_enter;      // 1: first tie run (host sets the g range from the query range)
   unsigned int stale;             // merge: some source exported an overflowed (stale) local result
   unsigned int bail;              // sorted-column kernel gave the query up (pair budget spent): re-run full
+  unsigned int fin_bar;           // bucketed finalize: CTAs of the query past the partition
+  unsigned int _pad6;
   unsigned long long admit_live;  // pairs the sorted-column kernel has enumerated for the query so far
   unsigned long long bail_tau;    // the admission key when it gave up (a valid lower bound for the re-run)
   unsigned int hist[3][256];      // select histograms (triple-buffered)

@@ -399,6 +399,7 @@ __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPrese
     c->stale = 0;
     c->use_full = use_full || (P && P->full) ? 1u : 0u;
     c->bail = 0;
+    c->fin_bar = 0;
     c->admit_live = 0;
     c->bail_tau = 0;
     c->small_done = 0;
@@ -3257,6 +3258,7 @@ constexpr int kFinThreads = 512;
 constexpr int kFinWarps = kFinThreads / 32;
 constexpr int kFinMaxSplit = 64;     // CTAs per query (rank splits)
 constexpr int kFinRowsPerCta = 128;  // target ranks per CTA
+constexpr int kFinSuffixMin = 16;    // splits from which the suffix-sum search and the partitioned load pay off
 #ifndef APEX_FIN_BATCH
 #define APEX_FIN_BATCH 8
 #endif
@@ -3272,7 +3274,8 @@ __host__ __device__ constexpr size_t fin_bucket_smem() {
 #else
 #define FIN_T(i)
 #endif
-__global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatLaunch M, int materialize) {
+__global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatLaunch M, int materialize,
+                                                                      Entry* __restrict__ scratch) {
 #ifdef APEX_FIN_DEBUG
   unsigned long long t_[8] = {};
 #endif
@@ -3284,20 +3287,29 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   extern __shared__ __align__(16) unsigned char sm_e[];
   Entry* es = reinterpret_cast<Entry*>(sm_e);
+  unsigned* fsuf = reinterpret_cast<unsigned*>(sm_e);  // prologue: per distinct coarse bin, 257 suffix counts
   DevReaction* s_rx = reinterpret_cast<DevReaction*>(sm_e + (size_t)kSmallSel * sizeof(Entry));
   unsigned long long* s_goff = reinterpret_cast<unsigned long long*>(s_rx + kFinRx);
   __shared__ unsigned long long s_bound, s_valid, s_above[kFinMaxSplit], s_n, s_hbase;
   __shared__ int s_bin[kFinMaxSplit], s_B;
   __shared__ unsigned s_hshift, s_tie, cnt;
+  __shared__ unsigned s_cis[257];           // inclusive suffix sums of the coarse histogram (+ 0)
+  __shared__ short s_cw[kFinMaxSplit], s_cidx[256];
+  __shared__ unsigned char s_cflag[256];
+  __shared__ short s_clist[kFinMaxSplit];
+  __shared__ unsigned s_nd;
   const bool stage_rx = materialize && M.n_rx <= kFinRx;
+  // (A) final bound (warp 0; CTA 0 writes it and the re-run parameters), the
+  // coarse histogram (warps 1-8), control fields and staging (last warp)
+  const bool suffix = ns >= kFinSuffixMin;  // many splits: suffix-sum searches; few: one warp search each
   if (warp == 0) {
-    // the final bound (CTA 0 writes it and the re-run parameters)
     const int B = final_bound(Q, j == 0, s_bound, s_valid);
     if (lane == 0) s_B = B;  // bins below B hold no rank < kk
-  } else if (warp < kFinWarps - 1) {
-    // rank splits w = warp, warp + (kFinWarps - 2), ...: the bin of rank
-    // w*kk/ns and the count above it (every CTA derives all ns splits, so all
-    // agree on the path taken)
+  } else if (suffix && warp <= 8) {
+    const unsigned t = threadIdx.x - 32;
+    s_cis[t] = __ldcg(Q.coarse + t);
+    s_cflag[t] = 0;
+  } else if (!suffix && warp < kFinWarps - 1) {
     if (warp < ns) {
       unsigned v[8];
       load_bins256(Q.coarse, v);
@@ -3316,7 +3328,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
         }
       }
     }
-  } else {
+  } else if (warp == kFinWarps - 1) {
     if (lane == 0) {
       s_n = min(*(volatile unsigned long long*)&ctl->count, Q.cap);
       s_hbase = *(volatile unsigned long long*)&ctl->hist_base;
@@ -3325,15 +3337,123 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
       cnt = 0;
       s_bin[0] = 65535;
       s_above[0] = 0;
+      s_nd = 0;
+      s_cis[256] = 0;
     }
     if (stage_rx) {
-      const int t0 = (int)lane, nt = 32;
       const int words = (int)(M.n_rx * (sizeof(DevReaction) / 8));
       const unsigned long long* src = reinterpret_cast<const unsigned long long*>(M.rx);
       unsigned long long* dst = reinterpret_cast<unsigned long long*>(s_rx);
-      for (int i = t0; i < words; i += nt) dst[i] = __ldg(src + i);
-      for (int i = t0; i <= M.n_rx; i += nt) s_goff[i] = __ldg(M.g_off + i);
+      for (int i = (int)lane; i < words; i += 32) dst[i] = __ldg(src + i);
+      for (int i = (int)lane; i <= M.n_rx; i += 32) s_goff[i] = __ldg(M.g_off + i);
     }
+  }
+  __syncthreads();
+  if (suffix) {
+    // (B) rank splits (every CTA derives all ns, so all agree on the path):
+    // split w is the bin holding rank w*kk/ns, searched in suffix sums of the
+    // coarse level, then of the fine blocks of the distinct coarse bins hit
+    if (warp == 1) {  // coarse inclusive suffix sums, lane l: bins 8l .. 8l+7
+      unsigned v[8], sum = 0;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        v[i] = s_cis[8 * lane + i];
+        sum += v[i];
+      }
+      unsigned suf = sum;  // inclusive suffix over lanes >= this lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_down_sync(0xffffffffu, suf, o);
+        if ((int)lane + o < 32) suf += y;
+      }
+      unsigned run = suf - sum;  // bins above this lane's block
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        run += v[i];
+        s_cis[8 * lane + i] = run;
+      }
+    }
+    __syncthreads();
+    const unsigned long long tot = s_cis[0];
+    const unsigned long long kk_all = min((unsigned long long)Q.k, tot);
+    if (threadIdx.x >= 1 && threadIdx.x < ns) {
+      const unsigned long long r = (unsigned long long)threadIdx.x * kk_all / ns;  // 0-based rank
+      int lo = 0, hi = 255;  // largest c with s_cis[c] > r
+      if (kk_all == 0 || s_cis[0] <= r) {
+        s_cw[threadIdx.x] = -1;
+      } else {
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_cis[mid] > r) lo = mid; else hi = mid - 1;
+        }
+        s_cw[threadIdx.x] = (short)lo;
+        s_cflag[lo] = 1;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // distinct coarse bins hit -> list
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int cbin = 32 * i + (int)lane;
+        const bool f = s_cflag[cbin] != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) {
+          const unsigned d = s_nd + __popc(m & ((1u << lane) - 1u));
+          s_clist[d] = (short)cbin;
+          s_cidx[cbin] = (short)d;
+        }
+        __syncwarp();
+        if (lane == 0) s_nd += __popc(m);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (unsigned d = warp; d < s_nd; d += kFinWarps) {  // fine block of each: inclusive suffix sums
+      const int cbin = s_clist[d];
+      unsigned* fs = fsuf + d * 257;
+      unsigned v[8], sum = 0;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        v[i] = __ldcg(Q.hist + cbin * 256 + 8 * lane + i);
+        sum += v[i];
+      }
+      unsigned suf = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_down_sync(0xffffffffu, suf, o);
+        if ((int)lane + o < 32) suf += y;
+      }
+      unsigned run = suf - sum;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        run += v[i];
+        fs[8 * lane + i] = run;
+      }
+      if (lane == 0) fs[256] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x >= 1 && threadIdx.x < ns) {
+      const int cbin = s_cw[threadIdx.x];
+      if (cbin < 0) {
+        s_bin[threadIdx.x] = -1;
+        s_above[threadIdx.x] = 0;
+      } else {
+        const unsigned long long r = (unsigned long long)threadIdx.x * kk_all / ns - s_cis[cbin + 1];
+        const unsigned* fs = fsuf + s_cidx[cbin] * 257;
+        int lo = 0, hi = 255;  // largest f with fs[f] > r (the fine counts agree with the coarse on a complete histogram)
+        if (fs[0] <= r) {
+          lo = 0;
+        } else {
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (fs[mid] > r) lo = mid; else hi = mid - 1;
+          }
+        }
+        s_bin[threadIdx.x] = cbin * 256 + lo;
+        s_above[threadIdx.x] = (unsigned long long)s_cis[cbin + 1] + fs[lo + 1];
+      }
+    }
+
   }
   __syncthreads();
   const unsigned long long n_valid = s_valid;
@@ -3361,31 +3481,70 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
     ctl->small_done = 1;
     ctl->mat_done = materialize ? 1u : 0u;
   }
-  if (hi < 0 || hi <= lo_excl || off >= kk) return;
   const unsigned long long n = s_n, hbase = s_hbase;
   const unsigned hshift = s_hshift;
   const bool tie = s_tie != 0;
-  for (unsigned long long base = threadIdx.x & ~31u; base < n; base += (unsigned long long)kFinBatch * blockDim.x) {
-    Entry e[kFinBatch];
-#pragma unroll
-    for (int u = 0; u < kFinBatch; ++u) {
-      const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
-      if (i < n) e[u] = Q.buf[i];
-    }
-#pragma unroll
-    for (int u = 0; u < kFinBatch; ++u) {
-      const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
-      bool keep = false;
-      if (i < n) {
-        const int b = (int)(tie ? cand_bin(ctl, e[u].key, e[u].g, hbase, hshift) : hist_bin(e[u].key, hbase, hshift));
-        keep = b <= hi && b > lo_excl;
+  const int b_low = s_B >= 0 ? s_B : 0;  // bins below hold no rank < kk
+  if (scratch) {
+    // (C) partition (cooperative launch: the query's CTAs are co-resident):
+    // CTA j routes the entries of its 1/ns slice of the buffer to the CTA
+    // owning their bin (a region of kSmallSel entries each in scratch), so
+    // every entry is read once; then the query's CTAs meet at a barrier
+    Entry* reg = scratch + (size_t)(blockIdx.y * ns) * kSmallSel;
+    unsigned* rcnt = &ctl->hist[0][0];  // per destination CTA (zeroed by init_ctl; the select never ran)
+    const unsigned long long s0 = n * j / ns, s1 = n * (j + 1) / ns;
+    for (unsigned long long i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+      const Entry e = Q.buf[i];
+      const int b = (int)(tie ? cand_bin(ctl, e.key, e.g, hbase, hshift) : hist_bin(e.key, hbase, hshift));
+      if (b < b_low) continue;
+      int lo = 0, hi2 = (int)ns - 1;  // owner: largest w with s_bin[w] >= b
+      while (lo < hi2) {
+        const int mid = (lo + hi2 + 1) >> 1;
+        if (s_bin[mid] >= b) lo = mid; else hi2 = mid - 1;
       }
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (!m) continue;
-      unsigned pos = 0;
-      if (lane == 0) pos = atomicAdd(&cnt, (unsigned)__popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
-      if (keep && pos < (unsigned)kSmallSel) es[pos] = e[u];
+      const unsigned pos = atomicAdd(rcnt + lo, 1u);
+      if (pos < (unsigned)kSmallSel) reg[(size_t)lo * kSmallSel + pos] = e;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(&ctl->fin_bar, 1u);
+      while (ld_acquire_u32(&ctl->fin_bar) < ns) __nanosleep(64);
+    }
+    __syncthreads();
+    if (hi < 0 || hi <= lo_excl || off >= kk) return;
+    const unsigned m0 = min(ld_relaxed_u32(rcnt + j), (unsigned)kSmallSel);
+    const Entry* mine = reg + (size_t)j * kSmallSel;
+    for (unsigned i = threadIdx.x; i < m0; i += blockDim.x) {  // written by other CTAs: past L1
+      const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(mine + i));
+      es[i].key = v.x;
+      es[i].g = v.y;
+    }
+    if (threadIdx.x == 0) cnt = m0;
+  } else {
+    if (hi < 0 || hi <= lo_excl || off >= kk) return;
+    for (unsigned long long base = threadIdx.x & ~31u; base < n; base += (unsigned long long)kFinBatch * blockDim.x) {
+      Entry e[kFinBatch];
+#pragma unroll
+      for (int u = 0; u < kFinBatch; ++u) {
+        const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
+        if (i < n) e[u] = Q.buf[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kFinBatch; ++u) {
+        const unsigned long long i = base + (unsigned long long)u * blockDim.x + lane;
+        bool keep = false;
+        if (i < n) {
+          const int b = (int)(tie ? cand_bin(ctl, e[u].key, e[u].g, hbase, hshift) : hist_bin(e[u].key, hbase, hshift));
+          keep = b <= hi && b > lo_excl;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (!m) continue;
+        unsigned pos = 0;
+        if (lane == 0) pos = atomicAdd(&cnt, (unsigned)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+        if (keep && pos < (unsigned)kSmallSel) es[pos] = e[u];
+      }
     }
   }
   __syncthreads();
