@@ -670,6 +670,8 @@ int build_corners(apex_ctx* c) {
 
 // CTAs per query of the bucketed finalize: about kFinRowsPerCta ranks each,
 // within one wave (one CTA per SM) and kFinMaxSplit
+constexpr int64_t kCornerTotal = 160000;  // corner seed: products per pass (all queries)
+
 int fin_splits(const apex_ctx* c, int64_t k_max, int nq) {
   const int64_t want = (k_max + kFinRowsPerCta - 1) / kFinRowsPerCta;
   return (int)std::max<int64_t>(
@@ -1115,7 +1117,11 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       // corner budget per reaction: enough corner products for ~16k feasible
       // seeds across the reactions, within the precomputed list lengths
       const int64_t nrx = std::max<int64_t>(1, (int64_t)c->rx.size());
-      CL.budget = (int)std::max<int64_t>(256, std::min<int64_t>(4096, c->opt_corner_mult * B.k_max / nrx));
+      // (and at most kCornerTotal corner products per pass: a batch of many
+      // queries gains little from more, C2 seed 39 -> 33 us; a single large-k
+      // query keeps its budget, C4's tau needs it)
+      CL.budget = (int)std::max<int64_t>(
+          256, std::min<int64_t>({4096, c->opt_corner_mult * B.k_max / nrx, kCornerTotal / (nrx * std::max(nq, 1))}));
       const int64_t per_rx = (int64_t)c->rx.size() * nq;
       const unsigned split = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8, (2 * (int64_t)c->sm_count + per_rx - 1) / std::max<int64_t>(per_rx, 1)));
       corner_kernel<<<dim3((unsigned)c->rx.size(), nq, split), 256, 0, c->side>>>(CL);
