@@ -282,8 +282,8 @@ struct apex_ctx {
   int64_t opt_bail_min = 4 << 20;   // ... and at least this many pairs
   int64_t opt_fin_part = 1;         // bucketed finalize partitions the buffer (cooperative) instead of full scans per CTA
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
-  int64_t opt_cpre = 1;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
-                                    // (1: forked after the control init, 2: at the pass start, 0: off)
+  int64_t opt_cpre = 3;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
+                                    // (3: after the control init, enqueued after the seeds; 1: right after the init; 2: at the pass start; 0: off)
   int64_t opt_dense = 16;           // admission kernel dense-row trigger (admitted products of a row in a tile; 0 = off)
   int64_t opt_graph = 1;            // replay the device pipeline of a repeated batch as a CUDA graph
   int64_t opt_packed16 = 1;         // sorted-column kernel reads the pair-major table copy
@@ -1000,8 +1000,9 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   const bool sorted_go = admit && B.plan_rows &&
                          !(span >= (uint64_t)c->opt_chunk_min && c->opt_chunk_div > 1 && plan->tiles.size() > 1);
   const bool cpre = sorted_go && !B.cset_leader.empty();
+  bool cpre_forked = false;
   auto launch_cpre = [&]() -> int {
-    APEX_CU(cudaEventRecord(c->fork2_ev, s));
+    if (!cpre_forked) APEX_CU(cudaEventRecord(c->fork2_ev, s));
     APEX_CU(cudaStreamWaitEvent(c->side2, c->fork2_ev, 0));
     ConsPre P{};
     P.queries = dq;
@@ -1056,7 +1057,16 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
                                       (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u, c->d_work.as<unsigned>());
   ++st.launches;
-  if (cpre && c->opt_cpre != 2) APEX_TRY(launch_cpre());
+  // (3: the pre-pass depends on the control init only, but is enqueued after
+  // the seed kernels, so their CTAs are dispatched first: they lead to the
+  // threshold, the longer chain)
+  const bool cpre_late = cpre && c->opt_cpre == 3 && !tau0;
+  if (cpre_late) {
+    APEX_CU(cudaEventRecord(c->fork2_ev, s));
+    cpre_forked = true;
+  } else if (cpre && c->opt_cpre != 2) {
+    APEX_TRY(launch_cpre());
+  }
   // K2 pack of the streamed objective column
   if (admit && !(B.plan_rows && span < (uint64_t)c->opt_chunk_min)) {
     // (the sorted-column kernel reads the table's sorted lists, not a packed column)
@@ -1127,7 +1137,10 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       corner_kernel<<<dim3((unsigned)c->rx.size(), nq, split), 256, 0, c->side>>>(CL);
       ++st.launches;
       APEX_CU(cudaEventRecord(c->join_ev, c->side));
+      if (cpre_late) APEX_TRY(launch_cpre());
       APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
+    } else if (cpre_late) {
+      APEX_TRY(launch_cpre());
     }
     {
       tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used, (unsigned long long)span);
