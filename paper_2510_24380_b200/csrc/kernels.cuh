@@ -638,38 +638,55 @@ __device__ __forceinline__ unsigned long long live_mask(const ScanLaunch& L, uns
   return m;
 }
 
+// 256 histogram bins, 8 per lane in blocks from the top: lane l, slot i holds
+// bin 255 - 8 l - i (lane 0 the highest block).
 __device__ __forceinline__ void load_bins256(const unsigned int* __restrict__ h, unsigned (&v)[8]) {
   const unsigned lane = lane_id();
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __ldcg(h + (255 - 32 * i - (int)lane));
+  for (int i = 0; i < 8; ++i) v[i] = __ldcg(h + (255 - 8 * (int)lane - i));
 }
 
-// Highest bin B (as 255 - 32 i - lane order, i.e. scanning from the top) with
-// above + sum_{b >= B} v[b] >= k over 256 bins held 8 per lane (lane l, slot i
-// = bin 255 - 32 i - l).  Returns B or -1; *above_io += bins above B (or all).
+// Highest bin B (scanning from the top) with above + sum_{b >= B} v[b] >= k
+// over 256 bins held as load_bins256 does.  Returns B or -1; above += the
+// count of the bins above B (or of all); *incl_at = the count at/above B.
+// One warp prefix sum over the lanes' block sums finds the block, the lane
+// holding it walks its 8 bins (round 1's form scanned 8 slot groups with a
+// prefix sum each: ~10x the instructions on this latency-bound chain).
 __device__ __forceinline__ int kth_bins256(const unsigned (&v)[8], unsigned long long k, unsigned long long& above,
                                            unsigned long long* incl_at) {
   const unsigned lane = lane_id();
+  unsigned long long blk = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) blk += v[i];
+  unsigned long long incl = blk;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if ((int)lane >= off) incl += o;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
+  if (!m) {
+    above += __shfl_sync(0xffffffffu, incl, 31);
+    return -1;
+  }
+  const int l = __ffs(m) - 1;
+  int b = 0;
+  unsigned long long run = above + incl - blk, at = 0;  // (meaningful in lane l)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    unsigned long long incl = v[i];
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += o;
+    if (b == 0 && run + v[i] >= k) {
+      b = 256 - 8 * (int)lane - i;  // bin + 1 (0: not found yet)
+      at = run + v[i];
+    } else if (b == 0) {
+      run += v[i];
     }
-    const unsigned m = __ballot_sync(0xffffffffu, above + incl >= k);
-    if (m) {
-      const int l = __ffs(m) - 1;
-      const unsigned long long il = __shfl_sync(0xffffffffu, incl, l);
-      const unsigned long long vl = __shfl_sync(0xffffffffu, (unsigned long long)v[i], l);
-      if (incl_at) *incl_at = above + il;
-      above += il - vl;
-      return 255 - 32 * i - l;
-    }
-    above += __shfl_sync(0xffffffffu, incl, 31);
   }
-  return -1;
+  b = __shfl_sync(0xffffffffu, b, l) - 1;
+  const unsigned long long run_l = __shfl_sync(0xffffffffu, run, l);
+  const unsigned long long at_l = __shfl_sync(0xffffffffu, at, l);
+  if (incl_at) *incl_at = at_l;
+  above = run_l;
+  return b;
 }
 
 // Two-level (256 coarse x 256 fine) search by ONE warp of the highest fine
