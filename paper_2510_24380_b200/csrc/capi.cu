@@ -281,6 +281,9 @@ struct apex_ctx {
   int64_t opt_bail = 128;           // sorted-column pair budget: range / this (0: no budget)
   int64_t opt_bail_min = 4 << 20;   // ... and at least this many pairs
   int64_t opt_fin_part = 1;         // bucketed finalize partitions the buffer (cooperative) instead of full scans per CTA
+  int64_t opt_graph_prio = 1;       // graphs honour the streams' priorities (cudaGraphInstantiateFlagUseNodePriority)
+  int64_t opt_cpre_prio = -1;       // pre-pass stream priority: 1 highest, -1 lowest
+  int64_t opt_tau_side = 1;         // threshold kernel on the high-priority side stream
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 3;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (3: after the control init, enqueued after the seeds; 1: right after the init; 2: at the pass start; 0: off)
@@ -1136,13 +1139,25 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       const unsigned split = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8, (2 * (int64_t)c->sm_count + per_rx - 1) / std::max<int64_t>(per_rx, 1)));
       corner_kernel<<<dim3((unsigned)c->rx.size(), nq, split), 256, 0, c->side>>>(CL);
       ++st.launches;
-      APEX_CU(cudaEventRecord(c->join_ev, c->side));
       if (cpre_late) APEX_TRY(launch_cpre());
-      APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
-    } else if (cpre_late) {
-      APEX_TRY(launch_cpre());
-    }
-    {
+      if (c->opt_tau_side) {
+        // the threshold kernel on the (high-priority) side stream after both
+        // seeds: its few CTAs are dispatched ahead of the pre-pass's
+        APEX_CU(cudaEventRecord(c->fork_ev, s));
+        APEX_CU(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+        tau_kernel<<<(nq + 7) / 8, 256, 0, c->side>>>(dq, nq, 0, autok, (unsigned long long)S_used,
+                                                       (unsigned long long)span);
+        ++st.launches;
+        APEX_CU(cudaEventRecord(c->join_ev, c->side));
+        APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
+      } else {
+        APEX_CU(cudaEventRecord(c->join_ev, c->side));
+        APEX_CU(cudaStreamWaitEvent(s, c->join_ev, 0));
+        tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used, (unsigned long long)span);
+        ++st.launches;
+      }
+    } else {
+      if (cpre_late) APEX_TRY(launch_cpre());
       tau_kernel<<<(nq + 7) / 8, 256, 0, s>>>(dq, nq, 0, autok, (unsigned long long)S_used, (unsigned long long)span);
       ++st.launches;
     }
@@ -1553,7 +1568,11 @@ int launch_batch(apex_ctx* c) {
   const int rc = enqueue_batch(c, nullptr);
   const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
   cudaGraphExec_t exec = nullptr;
-  const cudaError_t ei = (rc == APEX_OK && ec == cudaSuccess) ? cudaGraphInstantiate(&exec, graph, 0) : ec;
+  // node priorities (the streams' priorities, recorded at capture) are honoured
+  // only with UseNodePriority: the constraint pre-pass runs at the lowest, so
+  // the short seed / threshold kernels get SM slots as soon as any frees
+  const unsigned long long gflags = c->opt_graph_prio ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
+  const cudaError_t ei = (rc == APEX_OK && ec == cudaSuccess) ? cudaGraphInstantiateWithFlags(&exec, graph, gflags) : ec;
   if (graph) cudaGraphDestroy(graph);
   if (rc != APEX_OK || ec != cudaSuccess || ei != cudaSuccess) {
     cudaGetLastError();
@@ -1924,14 +1943,20 @@ int apex_ctx_create(int32_t device, void* stream, apex_ctx** out) {
   cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming);
-  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  {
+    int lo = 0, hi = 0;  // the seed side stream at the highest priority (see the pre-pass stream below)
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+  }
   cudaEventCreateWithFlags(&c->fork2_ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->join2_ev, cudaEventDisableTiming);
   {
-    int lo = 0, hi = 0;  // the pre-pass stream at the highest priority: its rows gate the enumeration
+    // the pre-pass stream at the lowest priority (its thousands of CTAs would
+    // otherwise hold every SM slot while the threshold kernel waits), the
+    // context's own streams at the highest
+    int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    (void)lo;
-    cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, c->opt_cpre_prio > 0 ? hi : lo);
   }
   *out = c;
   return APEX_OK;
@@ -2466,6 +2491,16 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "tau_side") c->opt_tau_side = v;
+  else if (n == "graph_prio") c->opt_graph_prio = v;
+  else if (n == "cpre_prio") {
+    c->opt_cpre_prio = v;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    APEX_CU(cudaStreamSynchronize(c->side2));
+    cudaStreamDestroy(c->side2);
+    APEX_CU(cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, v > 0 ? hi : lo));
+  }
   else if (n == "fin_part") c->opt_fin_part = v;
   else if (n == "bail") c->opt_bail = std::max<int64_t>(0, v);
   else if (n == "bail_min") c->opt_bail_min = std::max<int64_t>(1, v);
