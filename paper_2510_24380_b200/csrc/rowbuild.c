@@ -58,22 +58,23 @@ static PyObject* make_obj(PyTypeObject* cls, int fast, PyObject** names, PyObjec
   return o;
 }
 
-/* build_entries(mi_cls, sc_cls, fast, n, g, obj, cons, m, rx, digits, rx_table[, chi_cache]) -> list
+/* build_entries(mi_cls, sc_cls, fast, n, g, obj, cons, m, rx, digits, rx_table[, chi_cache[, chi_insert]]) -> list
  *   g: uint64[n]; obj: float64[n]; cons: float64[n*m]; rx: int32[n];
  *   digits: int32[n*6]; rx_table: sequence indexed by reaction position of
  *   (reaction_id, (rgroup_id, ...), ((synthon_id, ...), ...)[, (pair list, ...)]);
  *   the optional 4th item holds one list per R-group, indexed by digit, of
  *   (rgroup_id, synthon_id) tuples filled on first use (shared: tuples are
  *   immutable).  chi_cache: dict global index -> MultiIndex (frozen in the
- *   reference, csl.py:47, so a repeated product's chi is shared) or None. */
-#define CHI_CACHE_MAX (1 << 20)
+ *   reference, csl.py:47, so a repeated product's chi is shared) or None;
+ *   chi_insert: whether new MultiIndex instances are added to it. */
+#define CHI_CACHE_MAX (1 << 16) /* cleared when full: bounded memory, no large-dict resize pauses */
 static PyObject* build_entries(PyObject* self, PyObject* args) {
   PyObject *mi_cls, *sc_cls, *og, *oobj, *ocons, *orx, *odig, *table, *chi_cache = Py_None;
-  int fast;
+  int fast, chi_insert = 1;
   Py_ssize_t n, m;
   (void)self;
-  if (!PyArg_ParseTuple(args, "OOpnOOOnOOO|O", &mi_cls, &sc_cls, &fast, &n, &og, &oobj, &ocons, &m, &orx, &odig,
-                        &table, &chi_cache))
+  if (!PyArg_ParseTuple(args, "OOpnOOOnOOO|Op", &mi_cls, &sc_cls, &fast, &n, &og, &oobj, &ocons, &m, &orx, &odig,
+                        &table, &chi_cache, &chi_insert))
     return NULL;
   if (chi_cache != Py_None && !PyDict_Check(chi_cache)) {
     PyErr_SetString(PyExc_TypeError, "chi_cache must be a dict or None");
@@ -163,7 +164,8 @@ static PyObject* build_entries(PyObject* self, PyObject* args) {
         Py_DECREF(gi);
         goto fail;
       }
-      if (chi_cache != Py_None && PyDict_GET_SIZE(chi_cache) < CHI_CACHE_MAX && PyDict_SetItem(chi_cache, gi, chi) < 0) {
+      if (chi_cache != Py_None && chi_insert && PyDict_GET_SIZE(chi_cache) >= CHI_CACHE_MAX) PyDict_Clear(chi_cache);
+      if (chi_cache != Py_None && chi_insert && PyDict_SetItem(chi_cache, gi, chi) < 0) {
         Py_DECREF(chi);
         Py_DECREF(gi);
         goto fail;

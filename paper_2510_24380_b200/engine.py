@@ -22,6 +22,7 @@ fallback — without the library or a B200 the call raises.
 
 from __future__ import annotations
 
+import collections
 import gc
 import math
 import operator
@@ -317,13 +318,14 @@ def _rx_table(library) -> list:
 
 
 _CHI_CACHES: dict[int, tuple[weakref.ref, dict]] = {}
+_CHI_CACHE_ON = os.environ.get("APEX_B200_CHI_CACHE", "1") != "0"
 
 
 def _chi_cache(library, mi_cls) -> dict:
     """global index -> MultiIndex of this library, per MultiIndex class: the
     reference's MultiIndex is frozen (csl.py:47), so a product that recurs in
-    later results shares one instance (the native builder fills it, up to 2^20
-    entries; the device pass is unaffected)."""
+    later results shares one instance (the native builder fills it and clears
+    it at 2^16 entries; the device pass is unaffected)."""
     hit = _CHI_CACHES.get(id(library))
     if hit is None or hit[0]() is not library:
         try:
@@ -331,6 +333,23 @@ def _chi_cache(library, mi_cls) -> dict:
         except TypeError:
             return {}
     return hit[1].setdefault(mi_cls, {})
+
+
+_RECENT: dict[int, collections.deque] = {}
+
+
+def _repeated(library, query, res) -> bool:
+    """Whether this query (spec and range) was among the library's last 64:
+    only a repeated query adds its products to the MultiIndex cache (a stream
+    of distinct queries would pay the inserts and gain nothing)."""
+    sig = (query.objective, query.direction, int(query.k),
+           tuple((c.task, float(c.lower), float(c.upper)) for c in query.constraints), int(res["scanned"]),
+           int(res["g"][0]) if len(res["g"]) else -1)
+    recent = _RECENT.setdefault(id(library), collections.deque(maxlen=64))
+    hit = sig in recent
+    if not hit:
+        recent.append(sig)
+    return hit
 
 
 def _build_result(library, query, res: dict, timing: dict):
@@ -351,7 +370,8 @@ def _build_result(library, query, res: dict, timing: dict):
             np.ascontiguousarray(res["objective"], dtype=np.float64),
             np.ascontiguousarray(res["constraint_values"], dtype=np.float64), len(query.constraints),
             np.ascontiguousarray(res["reaction"], dtype=np.int32), np.ascontiguousarray(res["digits"], dtype=np.int32),
-            _rx_table(library), _chi_cache(library, mi_cls) if fast else None)
+            _rx_table(library), _chi_cache(library, mi_cls) if fast and _CHI_CACHE_ON else None,
+            _repeated(library, query, res))
         finally:
             if gc_on:
                 gc.enable()
