@@ -284,6 +284,7 @@ struct apex_ctx {
   int64_t opt_graph_prio = 1;       // graphs honour the streams' priorities (cudaGraphInstantiateFlagUseNodePriority)
   int64_t opt_cpre_prio = -1;       // pre-pass stream priority: 1 highest, -1 lowest
   int64_t opt_tau_side = 1;         // threshold kernel on the high-priority side stream
+  int64_t opt_lazy_hist = 1;        // histograms zeroed by the control init where the last pass left counts
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 3;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (3: after the control init, enqueued after the seeds; 1: right after the init; 2: at the pass start; 0: off)
@@ -767,7 +768,11 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
   APEX_TRY(c->d_work.ensure(kWorkWords * sizeof(unsigned)));
-  APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
+  {
+    const void* before = c->d_hists.p;
+    APEX_TRY(c->d_hists.ensure((size_t)nq * kHistWords * sizeof(unsigned)));
+    if (c->d_hists.p != before) APEX_CU(cudaMemset(c->d_hists.p, 0, c->d_hists.bytes));  // lazy zeroing starts clean
+  }
   if (c->opt_fin_bucket && c->opt_fin_part && fin_splits(c, B.k_max, nq) >= kFinSuffixMin)
     // partitioned bucketed finalize: one region per (query, CTA)
     APEX_TRY(c->d_fin_scratch.ensure((size_t)nq * fin_splits(c, B.k_max, nq) * kSmallSel * sizeof(Entry)));
@@ -1056,9 +1061,10 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
     return APEX_OK;
   };
   if (cpre && c->opt_cpre == 2) APEX_TRY(launch_cpre());
-  APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
-                                      (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u, c->d_work.as<unsigned>());
+  if (!c->opt_lazy_hist) APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
+  init_ctl_kernel<<<dim3(nq, c->opt_lazy_hist ? 8 : 1), 1024, 0, s>>>(dq, tau0 ? c->d_tau0.as<RunPreset>() : nullptr,
+                                      (c->opt_mode == 0 || c->opt_mode == 1) ? 1u : 0u, c->d_work.as<unsigned>(),
+                                      c->opt_lazy_hist ? 1u : 0u);
   ++st.launches;
   // (3: the pre-pass depends on the control init only, but is enqueued after
   // the seed kernels, so their CTAs are dispatched first: they lead to the
@@ -1828,7 +1834,7 @@ int merge_impl(apex_ctx* c, const apex_query_spec* qs, int nq, const Entry* entr
   APEX_CU(cudaMemcpyAsync(c->d_queries.p, c->h_queries.p, qbytes, cudaMemcpyHostToDevice, s));
   APEX_CU(cudaEventRecord(c->upload_ev, s));
   APEX_CU(cudaMemsetAsync(c->d_hists.p, 0, (size_t)nq * kHistWords * sizeof(unsigned), s));
-  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u, nullptr);
+  init_ctl_kernel<<<nq, 1024, 0, s>>>(dq, nullptr, 0u, nullptr, 0u);
   if (n_in > 0) {
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_in + 255) / 256, 4 * c->sm_count / std::max(nq, 1) + 1));
     merge_load_kernel<<<dim3(gx, nq), 256, 0, s>>>(dq, entries, n_src, nq, (unsigned long long)stride, srcs);
@@ -2491,6 +2497,10 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "lazy_hist") {
+    if (v && !c->opt_lazy_hist && c->d_hists.p) APEX_CU(cudaMemset(c->d_hists.p, 0, c->d_hists.bytes));
+    c->opt_lazy_hist = v;
+  }
   else if (n == "tau_side") c->opt_tau_side = v;
   else if (n == "graph_prio") c->opt_graph_prio = v;
   else if (n == "cpre_prio") {

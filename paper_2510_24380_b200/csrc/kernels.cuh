@@ -377,9 +377,29 @@ constexpr int kWorkWords = 64 + 32 * kWorkCtrs;  // flattened-work counters of t
 // Control-block init (one CTA per query).  tau0 = preset admission key
 // (kNoTau normally; the final threshold of an overflowed run on re-run).
 __global__ void init_ctl_kernel(const ScanQuery* __restrict__ qs, const RunPreset* __restrict__ pre,
-                                unsigned use_full, unsigned* work) {
+                                unsigned use_full, unsigned* work, unsigned lazy_zero) {
   const ScanQuery& Q = qs[blockIdx.x];
   QCtl* c = Q.ctl;
+  if (lazy_zero) {
+    // Histograms zeroed where the last pass left counts (replaces a memset of
+    // every bin of every query: 15.8 MB on C2): every fine increment comes
+    // with its coarse one, so the fine blocks of the nonzero coarse bins are
+    // exactly the dirty ones (the buffer is zeroed once when allocated).
+    // gridDim.y CTAs per query share the 768 coarse bins (3 histograms).
+    unsigned* const coarse[3] = {Q.coarse, Q.seed_hist + 2 * kHistBins, Q.seed_hist + 2 * kHistBins + 256};
+    unsigned* const fine[3] = {Q.hist, Q.seed_hist, Q.seed_hist + kHistBins};
+    const unsigned per = (768 + gridDim.y - 1) / gridDim.y, b0 = blockIdx.y * per, b1 = min(768u, b0 + per);
+    const unsigned warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = lane_id();
+    for (unsigned blk = b0 + warp; blk < b1; blk += nw) {
+      const unsigned cv = __ldcg(coarse[blk >> 8] + (blk & 255));
+      if (cv) {
+        uint4* f = reinterpret_cast<uint4*>(fine[blk >> 8] + (blk & 255) * 256);
+        for (unsigned i = lane; i < 64; i += 32) f[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (lane == 0) coarse[blk >> 8][blk & 255] = 0u;
+      }
+    }
+    if (blockIdx.y != 0) return;
+  }
   // the scan launches' flattened-work counters (replaces a memset node)
   if (work && blockIdx.x == 0 && threadIdx.x < kWorkWords) work[threadIdx.x] = 0u;
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&c->hist[0][0])[i] = 0u;
