@@ -285,6 +285,7 @@ struct apex_ctx {
   int64_t opt_cpre_prio = -1;       // pre-pass stream priority: 1 highest, -1 lowest
   int64_t opt_tau_side = 1;         // threshold kernel on the high-priority side stream
   int64_t opt_lazy_hist = 1;        // histograms zeroed by the control init where the last pass left counts
+  int64_t opt_cpre_fused = 0;       // constraint pre-pass as one fused kernel (measured slower: 27 us vs 16 + 5)
   int64_t opt_stages = 0;           // record the per-stage events (stats pack/seed/scan/select/finalize ms)
   int64_t opt_cpre = 3;             // sorted-column kernel: constraint pre-pass for sets shared by several queries
                                     // (3: after the control init, enqueued after the seeds; 1: right after the init; 2: at the pass start; 0: off)
@@ -1035,6 +1036,18 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       return (unsigned)std::max<int64_t>(1, c->opt_cpre_ctas > 0 ? std::min<int64_t>(full, c->sm_count * c->opt_cpre_ctas)
                                                                   : full);
     };
+    if (c->opt_cpre_fused) {
+      // one kernel: (tile, set) items
+      for (size_t s0 = 0; s0 < B.cset_leader.size(); s0 += kConsPreItems) {
+        P.n = (int)std::min<size_t>(kConsPreItems, B.cset_leader.size() - s0);
+        for (int j = 0; j < P.n; ++j) P.q[j] = B.cset_leader[s0 + j];
+        const int64_t items = (int64_t)P.n_tiles * P.n;
+        cons_fused_kernel<<<cpre_grid(items), 256, 0, c->side2>>>(P);
+        ++st.launches;
+      }
+      APEX_CU(cudaEventRecord(c->join2_ev, c->side2));
+      return APEX_OK;
+    }
     // A: (tile, test) threshold + quantile count items
     std::vector<std::pair<int, int>> tests;
     for (int ld : B.cset_leader)
@@ -1886,7 +1899,8 @@ const char* apex_version(void) { return "apex_b200 0.1 (sm_100a)"; }
 void preload_kernels() {
   const void* fns[] = {
       (const void*)init_ctl_kernel, (const void*)pack_kernel, (const void*)pack_obj_kernel,
-      (const void*)cons_thr_kernel, (const void*)cons_best_kernel, (const void*)sample_kernel,
+      (const void*)cons_thr_kernel, (const void*)cons_best_kernel, (const void*)cons_fused_kernel,
+      (const void*)sample_kernel,
       (const void*)corner_kernel, (const void*)tau_kernel, (const void*)scan_sorted_kernel<true, true>,
       (const void*)scan_sorted_kernel<true, false>, (const void*)scan_sorted_kernel<false, true>,
       (const void*)scan_sorted_kernel<false, false>, (const void*)scan_admit_kernel<1, false>,
@@ -2497,6 +2511,7 @@ int apex_set_option(apex_ctx* c, const char* name, int64_t v) {
   else if (n == "sorted") c->opt_sorted = v;
   else if (n == "cpre") c->opt_cpre = v;
   else if (n == "stages") c->opt_stages = v;
+  else if (n == "cpre_fused") c->opt_cpre_fused = v;
   else if (n == "lazy_hist") {
     if (v && !c->opt_lazy_hist && c->d_hists.p) APEX_CU(cudaMemset(c->d_hists.p, 0, c->d_hists.bytes));
     c->opt_lazy_hist = v;

@@ -2031,6 +2031,72 @@ __global__ void __launch_bounds__(256) cons_best_kernel(const __grid_constant__ 
   }
 }
 
+// The two pre-pass kernels fused: one warp per (row tile, set) derives every
+// constraint threshold of the set (all the set's prefix loads issued before
+// any threshold, the tests' quantile searches interleaved), keeps the most
+// selective test and searches its exact range — one launch and no round trip
+// of the quantile counts through memory.
+constexpr int kConsFuseBatch = 8;
+__global__ void __launch_bounds__(256) cons_fused_kernel(const __grid_constant__ ConsPre P) {
+  const unsigned lane = lane_id();
+  const unsigned items = P.n_tiles * (unsigned)P.n, step = gridDim.x * (blockDim.x >> 5);
+  for (unsigned item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += step) {
+    const unsigned t = item / (unsigned)P.n, si = item % (unsigned)P.n;
+    const ScanQuery& Q = P.queries[P.q[si]];
+    const Tile T = P.tiles[t];
+    const DevReaction& R = P.rx[T.rx];
+    const int c = R.c, nt = Q.nt;
+    const bool valid = lane < T.nrows;
+    const uint64_t row = T.row0 + (valid ? lane : 0u);
+    const int64_t slot = (int64_t)t * 32 + lane;
+    int64_t pr[kMaxRg - 1];
+    if (!P.rowp) decode_prefix(R, c, row, pr);
+    const float* qbase = P.quant + (int64_t)T.rx * (kQuant + 1);
+    const int64_t qstride = (int64_t)P.n_rx * (kQuant + 1);
+    int best = 0, best_q = kQuant + 2;
+    float best_th = 0.0f;
+    for (int i0 = 1; i0 < nt; i0 += kConsFuseBatch) {
+      double p[kConsFuseBatch];
+#pragma unroll
+      for (int u = 0; u < kConsFuseBatch; ++u) {
+        const int i = min(i0 + u, nt - 1);
+        const int task = Q.test_task[i];
+        if (P.rowp) {
+          p[u] = __ldg(P.rowp + task * P.rows_total + R.row_off + (int64_t)row);
+        } else {
+          double pp = c > 1 ? (double)tval(P.values, P.p16, P.n_pairs, task, pr[0]) : 0.0;
+#pragma unroll
+          for (int j = 1; j < kMaxRg - 1; ++j)
+            if (j < c - 1) pp = __dadd_rn(pp, (double)tval(P.values, P.p16, P.n_pairs, task, pr[j]));
+          p[u] = pp;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kConsFuseBatch; ++u) {
+        const int i = i0 + u;
+        if (i >= nt) break;
+        const bool lower = Q.test_lower[i] != 0;
+        const float th = lower ? -thr_lower_fast(p[u], Q.test_bias[i], Q.test_beta[i])
+                               : thr_upper_fast(p[u], Q.test_bias[i], Q.test_beta[i]);
+        P.cthr[(int64_t)(Q.cset_off + i - 1) * P.rows_pad + slot] = th;
+        const int qc = th == th ? quant_count(qbase + Q.test_task[i] * qstride, lower, lower ? -th : th) : 0;
+        if (qc < best_q) {  // lowest test index among the smallest counts
+          best_q = qc;
+          best = i;
+          best_th = th;
+        }
+      }
+    }
+    int start = 0, cnt = 0;
+    if (valid && best != 0 && best_q > 0) {
+      const bool lw = Q.test_lower[best] != 0;
+      exact_range(P.sx + (int64_t)Q.test_task[best] * P.pcols + R.pcol_off, (int)R.size[R.c - 1], lw,
+                  lw ? -best_th : best_th, best_q, start, cnt);
+    }
+    P.cbest[(int64_t)Q.cset * P.rows_pad + slot] = make_int4(best, valid ? best_q : kQuant + 2, start, cnt);
+  }
+}
+
 // CTAs per SM of the sorted-column scan (register budget 65536 / (256 x MINB)):
 // 3 (80 registers) beat 4 (64 registers, more spills) by 5-8% on C2
 // (profiles/r2_ab_sorted_minb.log); 2 (107 registers) was in between

@@ -213,7 +213,7 @@ def _random_case(seed, n_rx=6, mu=3.0, sigma=0.7, n_tasks=4, c3=0.5, max_c=3):
                                   {"mode": 2, "dense": 0}, {"packed16": 0}, {"rowp": 0}, {"packed16": 0, "rowp": 0},
                                   {"fin_bucket": 0}, {"fin_bucket": 2}, {"cpre": 0}, {"stages": 1},
                                   {"bail": 1000000000, "bail_min": 1}, {"bail": 1000000000, "bail_min": 64},
-                                  {"bail": 0}, {"cpre": 1}, {"cpre": 2}, {"lazy_hist": 0}])
+                                  {"bail": 0}, {"cpre": 1}, {"cpre": 2}, {"lazy_hist": 0}, {"cpre_fused": 0}])
 def test_random_libraries_vs_oracle(native, seed, opts):
     from oracle import scan_oracle as orc
 
