@@ -184,6 +184,39 @@ def test_native_row_builder_equals_python(use_reference, monkeypatch):
                                                                            slow.discarded_for_violation)
 
 
+def test_native_row_builder_caches():
+    """The builder's shared objects: a repeated query (same spec, range and
+    first row) reuses the MultiIndex instances of its first result, a distinct
+    one does not fill the cache; (rgroup_id, synthon_id) tuples are shared per
+    library and digit; every result still equals the Python builder's."""
+    import __graft_entry__ as gr
+
+    gr._build_rowbuild()
+    from conftest import golden_cases
+    from paper_2510_24380_b200 import engine
+
+    case = golden_cases()[0]
+    library = case.library()
+    query = engine.QuerySpec(case.task_names[0], "maximize", tuple(engine.Constraint(t) for t in case.task_names[:2]),
+                             10)
+    rows = _fake_rows(library, 40, len(query.constraints))
+    first = engine._build_result(library, query, rows, {})
+    second = engine._build_result(library, query, rows, {})   # repeated: fills the cache
+    third = engine._build_result(library, query, rows, {})    # served from it
+    assert first.entries == second.entries == third.entries
+    assert all(a.chi is b.chi for a, b in zip(second.entries, third.entries))
+    # pair tuples shared between rows with the same (R-group, synthon)
+    pairs = {}
+    for e in third.entries:
+        for pr in e.chi.assignment:
+            assert pairs.setdefault(pr, pr) is pr
+    other = engine.QuerySpec(case.task_names[0], "minimize", (), 10)
+    rows2 = _fake_rows(library, 40, 0)
+    before = len(engine._chi_cache(library, type(first.entries[0].chi)))
+    engine._build_result(library, other, rows2, {})
+    assert len(engine._chi_cache(library, type(first.entries[0].chi))) == before  # a first-time query adds nothing
+
+
 @pytest.mark.parametrize("mmap", [True, False])
 def test_table_file_roundtrip_and_reference_bytes(tmp_path, mmap):
     """save_table writes the reference's apexblob1 bytes; load_table (memory
