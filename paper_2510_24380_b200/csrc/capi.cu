@@ -676,6 +676,7 @@ int build_corners(apex_ctx* c) {
 // CTAs per query of the bucketed finalize: about kFinRowsPerCta ranks each,
 // within one wave (one CTA per SM) and kFinMaxSplit
 constexpr int64_t kCornerTotal = 160000;  // corner seed: products per pass (all queries)
+constexpr size_t kCtlHdr = (offsetof(QCtl, hist) + 15) / 16 * 16;  // control header bytes per query in the result block
 
 int fin_splits(const apex_ctx* c, int64_t k_max, int nq) {
   const int64_t want = (k_max + kFinRowsPerCta - 1) / kFinRowsPerCta;
@@ -763,8 +764,9 @@ int prepare_batch(apex_ctx* c, const apex_query_spec* qs_in, int nq, bool finali
   c->out_off.assign(nq + 1, 0);
   for (int i = 0; i < nq; ++i)
     c->out_off[i + 1] = c->out_off[i] + (out_bytes(std::max<int64_t>(qs[i].k, 1), qs[i].n_constraints) + 15) / 16 * 16;
-  APEX_TRY(c->d_out.ensure(c->out_off[nq]));
-  if (finalize) APEX_TRY(c->h_out.ensure(c->out_off[nq]));
+  // the control headers ride at the tail of the result block (one D2H)
+  APEX_TRY(c->d_out.ensure(c->out_off[nq] + (size_t)nq * kCtlHdr));
+  APEX_TRY(c->h_out.ensure(c->out_off[nq] + (size_t)nq * kCtlHdr));
   // everything enqueue_batch touches is allocated here (no allocation may
   // happen while the pipeline is being captured into a CUDA graph)
   APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
@@ -1353,16 +1355,20 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
   APEX_TRY(enqueue_select(c, dq, nq, B.k_max, B.finalize, st, s, true, true, B.small_only));
   APEX_CU(cudaGetLastError());
   APEX_CU(stage_mark(c, 5, s));
-  // control-block headers to host (read by check_batch): one strided copy
-  APEX_TRY(c->h_ctl.ensure(nq * sizeof(QCtl)));
-  APEX_CU(cudaMemcpy2DAsync(c->h_ctl.p, sizeof(QCtl), c->d_ctls.p, sizeof(QCtl), offsetof(QCtl, hist), nq,
-                            cudaMemcpyDeviceToHost, s));
-  st.d2h_bytes += nq * (int64_t)offsetof(QCtl, hist);
+  // control-block headers (read by check_batch) gathered at the tail of the
+  // result block by a kernel, then ONE copy: rows + headers when the rows go
+  // to the host in this pass (synchronous call; an overflow re-run copies
+  // again), else the headers alone
+  ctl_export_kernel<<<nq, 64, 0, s>>>(dq, c->d_out.as<unsigned char>() + c->out_off[nq]);
+  ++st.launches;
+  const size_t hdr = (size_t)nq * kCtlHdr;
   if (B.copy_out) {
-    // result rows to pinned host memory in the same pass (one host sync per
-    // call; an overflow re-run copies again)
-    APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, c->out_off[nq], cudaMemcpyDeviceToHost, s));
+    APEX_CU(cudaMemcpyAsync(c->h_out.p, c->d_out.p, c->out_off[nq] + hdr, cudaMemcpyDeviceToHost, s));
+  } else {
+    APEX_CU(cudaMemcpyAsync(c->h_out.as<unsigned char>() + c->out_off[nq], c->d_out.as<unsigned char>() + c->out_off[nq],
+                            hdr, cudaMemcpyDeviceToHost, s));
   }
+  st.d2h_bytes += (int64_t)hdr;
   B.pending = true;
   return APEX_OK;
 }
@@ -1403,6 +1409,12 @@ int check_batch(apex_ctx* c) {
   std::vector<int> pre_full(nq, 0);          // queries moved to the full predicate (bail-out)
   for (int attempt = 0;; ++attempt) {
     APEX_TRY(wait_stream(c));
+    {  // the control headers from the tail of the result block
+      const unsigned char* src = c->h_out.as<unsigned char>() + c->out_off[nq];
+      for (int i = 0; i < nq; ++i)
+        std::memcpy(c->h_ctl.as<unsigned char>() + (size_t)i * sizeof(QCtl), src + (size_t)i * kCtlHdr,
+                    offsetof(QCtl, hist));
+    }
     if (B.small_only) {
       // the large path was skipped on the strength of this signature's last
       // run: if a query did not fit the small finalize now, run it again whole

@@ -3680,6 +3680,15 @@ __global__ void __launch_bounds__(kFinThreads) finalize_bucket_kernel(const MatL
 #endif
 }
 
+// Control-block headers of every query (the fields before the select
+// histograms) gathered into one contiguous block for a single D2H.
+__global__ void ctl_export_kernel(const ScanQuery* __restrict__ qs, unsigned char* __restrict__ dst) {
+  const QCtl* ctl = qs[blockIdx.x].ctl;
+  const unsigned* src = reinterpret_cast<const unsigned*>(ctl);
+  unsigned* d = reinterpret_cast<unsigned*>(dst + (size_t)blockIdx.x * ((offsetof(QCtl, hist) + 15) / 16 * 16));
+  for (unsigned i = threadIdx.x; i < offsetof(QCtl, hist) / 4; i += blockDim.x) d[i] = __ldcg(src + i);
+}
+
 // Multi-GPU: export the local selected set (unordered) to out + slot*stride;
 // the slots past the selected count are written as padding (g == ~0), so the
 // exported block is complete without a separate memset.
