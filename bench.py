@@ -551,11 +551,12 @@ def run_single(args):
     peak_tops = sm_count * 128 * clk_mhz * 1e6 / 1e12
     scanned = shape.total
     F = f_ops(queries_named)
-    traffic = None
+    traffic = traffic_sorted = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(args.config)
+            tj = json.loads(prof.read_text())
+            traffic, traffic_sorted = tj.get(args.config), tj.get(args.config + "_sorted")
         except Exception:
             traffic = None
     kern_ms = statistics.mean(acc["scan"]) if acc["scan"] else None
@@ -679,7 +680,7 @@ def run_single(args):
     roofline_dominant = None
     if effective is not None:
         roofline_dominant = {"bound": "fp32", "achieved": effective["F_equivalent_tops"], "peak": peak_tops,
-                             "unit": "TFLOP/s", "frac": effective["frac_equivalent"], "traffic": traffic,
+                             "unit": "TFLOP/s", "frac": effective["frac_equivalent"], "traffic": traffic_sorted,
                              "kernel": "scan_sorted_kernel (default; per-row exact thresholds, most selective test's "
                                        "sorted range)", "kernel_ms": kern_ms, "F_per_product": F, "products": scanned,
                              "note": "F-equivalent: products the kernel proves cannot pass are never evaluated",
