@@ -676,6 +676,14 @@ int build_corners(apex_ctx* c) {
 // CTAs per query of the bucketed finalize: about kFinRowsPerCta ranks each,
 // within one wave (one CTA per SM) and kFinMaxSplit
 constexpr int64_t kCornerTotal = 160000;  // corner seed: products per pass (all queries)
+
+// Reciprocal for the scan kernels' item -> (tile, query) split (item_div):
+// ceil(2^32 / nq) is exact for every item index below 2^26 when nq <= 64
+// (error below item / 2^32 < 1/64 <= 1/nq); 0 = divide.
+unsigned nq_magic(unsigned tiles, int nq) {
+  if (nq < 2 || nq > 64 || (uint64_t)tiles * (uint64_t)nq >= (1ull << 26)) return 0u;
+  return (unsigned)(((1ull << 32) + (uint64_t)nq - 1) / (uint64_t)nq);
+}
 constexpr size_t kCtlHdr = (offsetof(QCtl, hist) + 15) / 16 * 16;  // control header bytes per query in the result block
 
 int fin_splits(const apex_ctx* c, int64_t k_max, int nq) {
@@ -1254,7 +1262,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
           La.tile_begin = 0;
           La.tile_end = (unsigned)pr_->tiles.size();
           La.queries = dq + q0;
-          La.nq = nql;
+          La.nq = nql; La.nq_magic = nq_magic((La.tile_end - La.tile_begin), nql);
           const int64_t items = (int64_t)pr_->tiles.size() * nql;
           const int64_t blocks = std::max<int64_t>(
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
@@ -1321,7 +1329,7 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
               1, std::min<int64_t>((items + kScanWarps - 1) / kScanWarps, (int64_t)c->sm_count * occ));
           ScanLaunch Lc = L;
           Lc.queries = dq + q0;
-          Lc.nq = nql;
+          Lc.nq = nql; Lc.nq_magic = nq_magic((Lc.tile_end - Lc.tile_begin), nql);
           Lc.work = c->d_work.as<unsigned>() + (wi++ % 64);
           cudaStream_t ls = s;
           if (n_full_launch % 2 == 1) {

@@ -549,6 +549,7 @@ struct ScanLaunch {
   unsigned long long* trace;  // per-item timing records (8 words) or null
   unsigned trace_cap;         // records
   int n_ctr;              // > 1: that many work counters (work + 32 k), counter k hands out items k, k + n_ctr, ...
+  unsigned nq_magic;      // ceil(2^32 / nq) when every item index < 2^26 (item_div), else 0
 };
 
 // Flattened persistent work distribution: item -> (tile = item / nq,
@@ -556,6 +557,12 @@ struct ScanLaunch {
 // same tiles (shared column data stays hot in L1/L2) and one launch keeps
 // every SM busy however many queries there are.  Warps take `chunk` items per
 // atomic; items of queries this kernel does not scan (mask) are skipped.
+// item / nq by a multiply-high with the launch's reciprocal (nq <= 64; exact
+// for item < 2^26, checked on the host, else a division)
+__device__ __forceinline__ unsigned item_div(const ScanLaunch& L, unsigned item) {
+  return L.nq_magic ? (unsigned)(((unsigned long long)item * L.nq_magic) >> 32) : item / (unsigned)L.nq;
+}
+
 struct WorkCursor {
   unsigned cur = 0, lim = 0;
   unsigned nxt = 0;      // lane 0: base of the next chunk, fetched one chunk ahead
@@ -590,8 +597,9 @@ __device__ __forceinline__ bool next_item_multi(const ScanLaunch& L, WorkCursor&
     }
     if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);  // one item ahead
     const unsigned item = (unsigned)item64;
-    q = item % (unsigned)L.nq;
-    t = L.tile_begin + item / (unsigned)L.nq;
+    const unsigned tq = item_div(L, item);
+    q = item - tq * (unsigned)L.nq;
+    t = L.tile_begin + tq;
     if ((live >> q) & 1ull) return true;
   }
 }
@@ -624,8 +632,9 @@ __device__ __forceinline__ bool next_item(const ScanLaunch& L, WorkCursor& wc, u
       item = wc.cur++;
     }
     if (item >= total) return false;
-    q = item % (unsigned)L.nq;
-    t = L.tile_begin + item / (unsigned)L.nq;
+    const unsigned tq = item_div(L, item);
+    q = item - tq * (unsigned)L.nq;
+    t = L.tile_begin + tq;
     if ((live >> q) & 1ull) return true;
   }
 }
