@@ -453,16 +453,35 @@ def c5_latencies(local, stream, n=60):
         extra = next((synth.query_spec(q) for q in allq[n:] if synth.query_spec(q).k == kk), None)
         if extra is not None:
             engine.search_topk_stream(library, table, extra)
-    lat, by_k = [], {}
-    for q in qs:
-        t0 = time.perf_counter()
-        engine.search_topk_stream(library, table, q)
-        dt = (time.perf_counter() - t0) * 1e3
-        lat.append(dt)
-        by_k.setdefault(q.k, []).append(dt)
+    # the interpreter's cyclic-GC pauses that land inside a call (a gen-2
+    # sweep walks every live object of the process) are part of its latency;
+    # record them so an outlier can be attributed
+    import gc
+    gc_t = {"t0": 0.0, "ms": 0.0}
+
+    def gc_cb(phase, info):
+        if phase == "start":
+            gc_t["t0"] = time.perf_counter()
+        else:
+            gc_t["ms"] += (time.perf_counter() - gc_t["t0"]) * 1e3
+
+    lat, by_k, rows = [], {}, []
+    gc.callbacks.append(gc_cb)
+    try:
+        for i, q in enumerate(qs):
+            gc_t["ms"] = 0.0
+            t0 = time.perf_counter()
+            engine.search_topk_stream(library, table, q)
+            dt = (time.perf_counter() - t0) * 1e3
+            lat.append(dt)
+            by_k.setdefault(q.k, []).append(dt)
+            rows.append({"i": i, "ms": round(dt, 3), "k": q.k, "gc_ms": round(gc_t["ms"], 3)})
+    finally:
+        gc.callbacks.remove(gc_cb)
     return {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)), "mean": float(np.mean(lat)),
             "n": len(lat), "first_call_ms": first,
             "p50_by_k": {str(k): float(np.median(v)) for k, v in sorted(by_k.items())},
+            "slowest": sorted(rows, key=lambda r: -r["ms"])[:3],
             "call": "engine.search_topk_stream, first n synth.c5_queries() (config 5) over the c3 library, after one "
                     "untimed query per k class"}
 

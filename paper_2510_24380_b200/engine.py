@@ -23,6 +23,7 @@ fallback — without the library or a B200 the call raises.
 from __future__ import annotations
 
 import collections
+import functools
 import gc
 import math
 import operator
@@ -427,6 +428,30 @@ def _timing(t0: float, start: int, end: int, stats: dict) -> dict:
 # operator API
 # ---------------------------------------------------------------------------
 
+def _gc_paused(fn):
+    """Run an operator call with the cyclic GC paused.  A call allocates k
+    result rows (none in reference cycles); with the GC live, the sweeps they
+    trigger run while the rows are still referenced, promote them, and every
+    few calls escalate to a full sweep of every live object in the process —
+    tens of ms with a 1e9-product library's ~3e5 synthon records resident.
+    Paused, the allocation count falls back as soon as the caller drops a
+    result, so a stream of queries never pays a sweep it did not cause; a
+    caller that keeps its results pays it at its own next allocation, as it
+    would for any other objects.  Nothing is allocated between the re-enable
+    and the return."""
+    @functools.wraps(fn)
+    def call(*args, **kwargs):
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            if gc_on:
+                gc.enable()
+    return call
+
+
+@_gc_paused
 def search_topk_stream(library, table, query, index_range=None, device=None):
     """Exact constrained top-k (engine.py:265-313), on the B200 — on several
     B200s when ``device`` is a sequence of ids (or APEX_B200_DEVICES is set)."""
@@ -474,6 +499,7 @@ def batch_ends(library, chunk_size: int, start: int, end: int) -> list:
     return ends
 
 
+@_gc_paused
 def search_topk_batched(library, table, query, chunk_size, index_range=None, trace=None, device=None):
     """Chain-of-batches variant (engine.py:345-398).  Results are identical to
     the stream variant by contract (test_engine.py:138-145), so both run the
@@ -514,6 +540,7 @@ def default_device_one(device) -> int:
     return int(dev[0] if isinstance(dev, (list, tuple)) else dev)
 
 
+@_gc_paused
 def search_topk_many(library, table, queries, index_range=None, device=None):
     """Several queries in one batched device pass; same results as one
     ``search_topk_stream`` call per query."""

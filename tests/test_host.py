@@ -241,3 +241,35 @@ def test_table_file_roundtrip_and_reference_bytes(tmp_path, mmap):
     assert q.read_bytes() == p.read_bytes()
     ref_back = rengine.load_table(p)
     assert ref_back.values.tobytes() == np.asarray(back.values).tobytes()
+
+
+def test_operator_calls_pause_gc_and_restore_it():
+    """engine._gc_paused: the cyclic GC is off inside an operator call and
+    restored after it, on return and on error; a caller that had it off
+    keeps it off."""
+    import gc
+
+    from paper_2510_24380_b200 import engine
+
+    seen = []
+
+    @engine._gc_paused
+    def op(fail=False):
+        seen.append(gc.isenabled())
+        if fail:
+            raise ValueError("x")
+        return 7
+
+    assert gc.isenabled()
+    assert op() == 7 and seen == [False] and gc.isenabled()
+    with pytest.raises(ValueError):
+        op(fail=True)
+    assert gc.isenabled()
+    gc.disable()
+    try:
+        op()
+        assert not gc.isenabled()
+    finally:
+        gc.enable()
+    for f in (engine.search_topk_stream, engine.search_topk_many, engine.search_topk_batched):
+        assert f.__wrapped__ is not None
