@@ -2214,8 +2214,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     const int cset = Q.cset;
     if (cset >= 0) {
       const int64_t slot = (int64_t)t_cur * 32 + lane;
-      const float* cth = S.cthr + (int64_t)(Q.cset_off - 1) * S.rows_pad + slot;
-      for (int i = 1; i < nt; ++i) cp_async4(sthr + i * 32 + lane, cth + (int64_t)i * S.rows_pad);
+      // a test's 32 row thresholds are 128 contiguous bytes: 8 lanes copy
+      // one test with 16-byte copies (rows_pad is a multiple of 32)
+      const float* cth = S.cthr + (int64_t)(Q.cset_off - 1) * S.rows_pad + (int64_t)t_cur * 32;
+      for (int ch = lane + 8; ch < nt * 8; ch += 32)
+        cp_async16(sthr + (ch >> 3) * 32 + (ch & 7) * 4, cth + (int64_t)(ch >> 3) * S.rows_pad + (ch & 7) * 4);
       cp_async16(scb + lane, S.cbest + (int64_t)cset * S.rows_pad + slot);
       cp_async_commit();
     }
