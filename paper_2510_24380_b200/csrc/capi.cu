@@ -1234,7 +1234,8 @@ int enqueue_batch(apex_ctx* c, const RunPreset* tau0) {
       if (admit && B.plan_rows && bounds.size() == 1) {
         // sorted-column admission: whole-row tiles, one launch per 64 queries
         const Plan* pr_ = B.plan_rows;
-        const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float) + (size_t)kScanWarps * 32 * sizeof(int4);
+        const size_t smem = (size_t)kScanWarps * kMaxTests * 32 * sizeof(float) + (size_t)kScanWarps * 32 * sizeof(int4) +
+                            (APEX_CAND_STAGE ? (size_t)kScanWarps * kCandStage * sizeof(Entry) : 0);
         const bool p16 = c->packed16_ok && c->opt_packed16;
         const bool rowp = c->rowp_ok && c->opt_rowp;
         ScanFn fn = p16 ? (rowp ? reinterpret_cast<ScanFn>(scan_sorted_kernel<true, true>)

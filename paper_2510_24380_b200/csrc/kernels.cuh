@@ -2112,6 +2112,12 @@ __global__ void __launch_bounds__(256) cons_fused_kernel(const __grid_constant__
 #ifndef APEX_SORTED_MINB
 #define APEX_SORTED_MINB 3
 #endif
+// candidates staged per warp in shared memory before the buffer append
+// (0: one append per round with candidates)
+#ifndef APEX_CAND_STAGE
+#define APEX_CAND_STAGE 1
+#endif
+constexpr int kCandStage = 64;
 // P16: contributions read from the pair-major copy packed16[pair][16] (one
 // 64-byte line per pair holds every task: a row's prefix sums and a pair's
 // test values for all tests come from one line each instead of one line per
@@ -2140,6 +2146,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   if (!live) return;
   float* sthr = sm_s + (size_t)warp * kMaxTests * 32;  // [test][lane]: signed-value thresholds of every test
   int4* scb = reinterpret_cast<int4*>(sm_s + (size_t)kScanWarps * kMaxTests * 32) + warp * 32;  // pre-pass best range
+#if APEX_CAND_STAGE
+  Entry* stg = reinterpret_cast<Entry*>(reinterpret_cast<int4*>(sm_s + (size_t)kScanWarps * kMaxTests * 32) +
+                                        kScanWarps * 32) + warp * kCandStage;  // staged candidates
+#endif
   WorkCursor wc;
   const float* __restrict__ values = L.values;
   const float* __restrict__ p16 = S.packed16;
@@ -2408,6 +2418,23 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
 #ifdef APEX_SCAN_TIME
     w_rounds += (total + 31) / 32;
 #endif
+#if APEX_CAND_STAGE
+    unsigned n_stg = 0;  // warp-uniform
+    auto flush_stage = [&]() {
+      __syncwarp();
+      unsigned long long cb = 0;
+      if (lane == 0) cb = atomicAdd(&ctl->count, (unsigned long long)n_stg);
+      cb = __shfl_sync(0xffffffffu, cb, 0);
+      for (unsigned i = lane; i < n_stg; i += 32)
+        if (cb + i < Q.cap) Q.buf[cb + i] = stg[i];
+      if ((cb >> Q.refresh_shift) != ((cb + n_stg) >> Q.refresh_shift)) {
+        __threadfence();
+        refresh_tau(Q);
+      }
+      n_stg = 0;
+      __syncwarp();
+    };
+#endif
     for (int j0 = 0; j0 < total; j0 += 32) {
       // a query given up (pair budget) stops its items in flight too
       if (((j0 >> 5) & 15) == 15 && Q.admit_budget != ~0ull && ld_relaxed_u64(&ctl->tau_key) == ~0ull) break;
@@ -2459,6 +2486,21 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       ++w_crounds;
       w_cand += __popc(mk);
 #endif
+#if APEX_CAND_STAGE
+      // staged in the warp's shared-memory slots; the buffer append (one
+      // atomic round trip) happens once per kCandStage - 31 candidates or at
+      // the item's end instead of once per round (the histogram counts them
+      // now, so the tau refresh sees them; every staged entry is flushed
+      // before the item ends)
+      if (pass) {
+        stg[n_stg + __popc(mk & ((1u << lane) - 1u))] = e;
+        const unsigned hb = tie_on ? cand_bin(ctl, e.key, e.g, hist_base, hist_shift) : hist_bin(e.key, hist_base, hist_shift);
+        atomicAdd(&Q.hist[hb], 1u);
+        atomicAdd(&Q.coarse[hb >> 8], 1u);
+      }
+      n_stg += __popc(mk);
+      if (n_stg > (unsigned)(kCandStage - 32)) flush_stage();
+#else
       unsigned long long cbase = 0;
       if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
       cbase = __shfl_sync(0xffffffffu, cbase, 0);
@@ -2476,7 +2518,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         ++w_refresh;
 #endif
       }
+#endif
     }
+#if APEX_CAND_STAGE
+    if (n_stg) flush_stage();
+#endif
 
     __syncwarp();
     const unsigned a = __reduce_add_sync(0xffffffffu, admitted);
