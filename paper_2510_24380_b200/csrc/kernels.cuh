@@ -2117,7 +2117,10 @@ __global__ void __launch_bounds__(256) cons_fused_kernel(const __grid_constant__
 #ifndef APEX_CAND_STAGE
 #define APEX_CAND_STAGE 1
 #endif
-constexpr int kCandStage = 64;
+#ifndef APEX_CAND_SLOTS
+#define APEX_CAND_SLOTS 64
+#endif
+constexpr int kCandStage = APEX_CAND_SLOTS;
 // P16: contributions read from the pair-major copy packed16[pair][16] (one
 // 64-byte line per pair holds every task: a row's prefix sums and a pair's
 // test values for all tests come from one line each instead of one line per
