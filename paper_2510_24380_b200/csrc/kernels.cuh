@@ -569,6 +569,7 @@ struct WorkCursor {
   bool primed = false;
   unsigned sk = 0;       // static rounds taken
   unsigned k = 0, tried = 0;  // several counters: the current one, counters found exhausted
+  bool tail = false;     // the item just returned is in the last window: nothing claimed ahead
 };
 
 // Several work counters (L.n_ctr > 1, each in its own 128-byte line): one
@@ -586,8 +587,16 @@ __device__ __forceinline__ bool next_item_multi(const ScanLaunch& L, WorkCursor&
     wc.k = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % n;
     if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);
   }
+  // the last window of items (one per warp of the grid) is claimed just in
+  // time: an item claimed ahead by a warp still busy with a heavy item would
+  // wait behind it while other warps find the counters empty
+  const unsigned long long window = (unsigned long long)gridDim.x * (blockDim.x >> 5);
   for (;;) {
-    const unsigned local = __shfl_sync(0xffffffffu, wc.nxt, 0);
+    unsigned local = __shfl_sync(0xffffffffu, wc.nxt, 0);
+    if (local == ~0u) {  // not claimed ahead
+      if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);
+      local = __shfl_sync(0xffffffffu, wc.nxt, 0);
+    }
     const unsigned long long item64 = (unsigned long long)wc.k + (unsigned long long)local * n;
     if (item64 >= total) {
       if (++wc.tried >= n) return false;
@@ -595,7 +604,8 @@ __device__ __forceinline__ bool next_item_multi(const ScanLaunch& L, WorkCursor&
       if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);
       continue;
     }
-    if (lane == 0) wc.nxt = atom_add_u32(L.work + 32 * wc.k, 1u);  // one item ahead
+    wc.tail = item64 + window >= total;
+    if (lane == 0) wc.nxt = wc.tail ? ~0u : atom_add_u32(L.work + 32 * wc.k, 1u);  // one item ahead
     const unsigned item = (unsigned)item64;
     const unsigned tq = item_div(L, item);
     q = item - tq * (unsigned)L.nq;
@@ -2183,7 +2193,17 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   unsigned w_rounds = 0, w_crounds = 0, w_refresh = 0, w_cand = 0, w_maxitem_rounds = 0;
   unsigned long long w_maxitem = 0;
 #endif
-  while (have) {
+  bool pending = false;  // the next item is fetched after this one (tail window)
+  for (;;) {
+    if (pending) {
+      pending = false;
+      have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
+      if (have) {
+        T_n = L.tiles[t];
+        tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
+      }
+    }
+    if (!have) break;
 #ifdef APEX_SCAN_PROF
     const unsigned long long t_item = clock64();
 #endif
@@ -2194,10 +2214,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     const unsigned q_cur = qi, t_cur = t;
     const Tile T = T_n;
     const unsigned long long tau = tau_n;
-    have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
-    if (have) {
-      T_n = L.tiles[t];
-      tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
+    if (wc.tail) {
+      pending = true;
+    } else {
+      have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
+      if (have) {
+        T_n = L.tiles[t];
+        tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
+      }
     }
 #ifdef APEX_SCAN_PROF
     if (have && t == 0xffffffffu) prof[9] += 1;
