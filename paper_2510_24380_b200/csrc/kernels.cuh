@@ -2131,6 +2131,9 @@ __global__ void __launch_bounds__(256) cons_fused_kernel(const __grid_constant__
 #define APEX_CAND_SLOTS 64
 #endif
 constexpr int kCandStage = APEX_CAND_SLOTS;
+#ifndef APEX_TILE_SMEM
+#define APEX_TILE_SMEM 0  // 1: measured neutral (profiles/r2_ab_tile_smem_rejected.log)
+#endif
 // P16: contributions read from the pair-major copy packed16[pair][16] (one
 // 64-byte line per pair holds every task: a row's prefix sums and a pair's
 // test values for all tests come from one line each instead of one line per
@@ -2145,7 +2148,7 @@ __device__ unsigned g_wt_n, g_wt_done;
 #endif
 #ifdef APEX_SCAN_PROF
 // per-phase cycle totals of the sorted-column scan (debug builds: -DAPEX_SCAN_PROF)
-__device__ unsigned long long g_scan_prof[10];
+__device__ unsigned long long g_scan_prof[16];
 // warp start min/max, end min/max, span sum, warps, max item cycles, max item pairs
 __device__ unsigned long long g_scan_t[8] = {~0ull, 0, ~0ull, 0, 0, 0, 0, 0};
 __device__ unsigned long long g_scan_hist[64];  // items by log2(cycles) / by log2(admitted pairs + 1)
@@ -2169,6 +2172,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   const int64_t n_pairs = L.n_pairs;
   __shared__ unsigned s_adm[64];  // admitted products per query of the launch (statistics)
   __shared__ unsigned s_live[64];  // enumerated pairs per query not yet flushed to the pair budget
+#if APEX_TILE_SMEM
+  // the launch's control-block pointers, and each warp's next tile copied in
+  // the background (cp.async) while the current item runs: neither is a
+  // dependent global load at the top of an item
+  __shared__ QCtl* s_ctl[64];
+  __shared__ __align__(16) Tile s_tile[kScanWarps];
+  for (int q = threadIdx.x; q < L.nq; q += blockDim.x) s_ctl[q] = L.queries[q].ctl;
+#endif
   for (int q = threadIdx.x; q < 64; q += blockDim.x) s_adm[q] = s_live[q] = 0;
   __syncthreads();
   auto ld = [&](int task, int64_t pair) -> float {
@@ -2179,12 +2190,22 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
   bool have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
   Tile T_n;
   unsigned long long tau_n = 0;
+#if APEX_TILE_SMEM
+  auto fetch_next = [&]() {
+    if (lane < sizeof(Tile) / 8)
+      cp_async8(reinterpret_cast<uint64_t*>(&s_tile[warp]) + lane, reinterpret_cast<const uint64_t*>(L.tiles + t) + lane);
+    cp_async_commit();
+    tau_n = ld_relaxed_u64(&s_ctl[qi]->tau_key);
+  };
+  if (have) fetch_next();
+#else
   if (have) {
     T_n = L.tiles[t];
     tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
   }
+#endif
 #ifdef APEX_SCAN_PROF
-  unsigned long long prof[10] = {}, tp = clock64();
+  unsigned long long prof[16] = {}, tp = clock64();
   const unsigned long long g_start = globaltimer_ns();
 #endif
 #ifdef APEX_SCAN_TIME
@@ -2198,10 +2219,14 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     if (pending) {
       pending = false;
       have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
+#if APEX_TILE_SMEM
+      if (have) fetch_next();
+#else
       if (have) {
         T_n = L.tiles[t];
         tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
       }
+#endif
     }
     if (!have) break;
 #ifdef APEX_SCAN_PROF
@@ -2212,23 +2237,44 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     w_last = globaltimer_ns();
 #endif
     const unsigned q_cur = qi, t_cur = t;
+#if APEX_TILE_SMEM
+    cp_async_wait_all();
+    __syncwarp();
+    T_n = s_tile[warp];
+    __syncwarp();  // every lane has the tile before the next copy lands
+#endif
     const Tile T = T_n;
     const unsigned long long tau = tau_n;
+#ifdef APEX_SCAN_PROF
+    { const unsigned long long tn = clock64(); prof[14] += tn - tp; tp = tn; }
+#endif
     if (wc.tail) {
       pending = true;
     } else {
       have = (L.n_ctr > 1 ? next_item_multi(L, wc, live, lane, qi, t) : next_item(L, wc, live, lane, qi, t));
+#ifdef APEX_SCAN_PROF
+      if (have && t == 0xffffffffu) prof[9] += 1;
+      { const unsigned long long tn = clock64(); prof[15] += tn - tp; tp = tn; }
+#endif
+#if APEX_TILE_SMEM
+      if (have) fetch_next();
+#else
       if (have) {
         T_n = L.tiles[t];
         tau_n = ld_relaxed_u64(&L.queries[qi].ctl->tau_key);
       }
+#endif
     }
 #ifdef APEX_SCAN_PROF
     if (have && t == 0xffffffffu) prof[9] += 1;
     { const unsigned long long tn = clock64(); prof[0] += tn - tp; tp = tn; }
 #endif
     const ScanQuery& Q = L.queries[q_cur];
+#if APEX_TILE_SMEM
+    QCtl* ctl = s_ctl[q_cur];
+#else
     QCtl* ctl = Q.ctl;
+#endif
     const int maximize = Q.maximize;
     const double b_obj = Q.test_bias[0];
     const int nt = Q.nt;
@@ -2465,6 +2511,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     for (int j0 = 0; j0 < total; j0 += 32) {
       // a query given up (pair budget) stops its items in flight too
       if (((j0 >> 5) & 15) == 15 && Q.admit_budget != ~0ull && ld_relaxed_u64(&ctl->tau_key) == ~0ull) break;
+#ifdef APEX_SCAN_PROF
+      const unsigned long long r_t0 = clock64();
+#endif
       const int jj = j0 + (int)lane;
       const int j = jj < total ? jj : total - 1;
       // owning row: smallest r with incl[r] > j
@@ -2508,6 +2557,12 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         pass = !(tie_on && tie_reject(ctl, e.key, e.g));
       }
       const unsigned mk = __ballot_sync(0xffffffffu, pass);
+#ifdef APEX_SCAN_PROF
+      if (mk == 0x12345u) prof[9] += 1;
+      const unsigned long long r_t1 = clock64();
+      prof[11] += r_t1 - r_t0;
+      prof[10] += 1;
+#endif
       if (!mk) continue;
 #ifdef APEX_SCAN_TIME
       ++w_crounds;
@@ -2527,6 +2582,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
       }
       n_stg += __popc(mk);
       if (n_stg > (unsigned)(kCandStage - 32)) flush_stage();
+#ifdef APEX_SCAN_PROF
+      if (n_stg == 0x12345u) prof[9] += 1;
+      prof[12] += clock64() - r_t1;
+      prof[13] += 1;
+#endif
 #else
       unsigned long long cbase = 0;
       if (lane == 0) cbase = atomicAdd(&ctl->count, (unsigned long long)__popc(mk));
@@ -2621,7 +2681,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     atomicAdd(&g_scan_t[5], 1ull);
   }
   if (lane == 0)
-    for (int i = 0; i < 9; ++i) atomicAdd(&g_scan_prof[i], prof[i]);
+    for (int i = 0; i < 16; ++i) if (i != 9) atomicAdd(&g_scan_prof[i], prof[i]);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(&g_scan_done, 1u) == gridDim.x - 1) {
@@ -2629,6 +2689,11 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
     printf("SCANPROF items %llu cycles/item: next %llu Q %llu R %llu p_obj %llu thr+quant %llu cset %llu range %llu "
            "pairs %llu\n", g_scan_prof[8], g_scan_prof[0] / n, g_scan_prof[1] / n, g_scan_prof[2] / n,
            g_scan_prof[3] / n, g_scan_prof[4] / n, g_scan_prof[5] / n, g_scan_prof[6] / n, g_scan_prof[7] / n);
+    printf("SCANNEXT cycles/item: loop top %llu, next_item %llu, loads %llu\n", g_scan_prof[14] / n, g_scan_prof[15] / n,
+           g_scan_prof[0] / n);
+    printf("SCANROUNDS %llu rounds, cycles/round: to ballot %llu, append %llu (rounds with candidates %llu)\n",
+           g_scan_prof[10], g_scan_prof[11] / (g_scan_prof[10] ? g_scan_prof[10] : 1),
+           g_scan_prof[12] / (g_scan_prof[13] ? g_scan_prof[13] : 1), g_scan_prof[13]);
     printf("SCANTIME warps %llu: first start +0, last start +%llu ns, first end +%llu, last end +%llu, mean warp span %llu ns\n",
            g_scan_t[5], g_scan_t[1] - g_scan_t[0], g_scan_t[2] - g_scan_t[0], g_scan_t[3] - g_scan_t[0],
            g_scan_t[4] / (g_scan_t[5] ? g_scan_t[5] : 1));
@@ -2638,7 +2703,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, APEX_SORTED_MINB) scan_sorted
         printf("SCANHIST 2^%d: items by cycles %llu | by pairs (<2^%d) %llu\n", i, g_scan_hist[i], i, g_scan_hist[32 + i]);
     for (int i = 0; i < 64; ++i) g_scan_hist[i] = 0;
     g_scan_t[6] = g_scan_t[7] = 0;
-    for (int i = 0; i < 10; ++i) g_scan_prof[i] = 0;
+    for (int i = 0; i < 16; ++i) g_scan_prof[i] = 0;
     g_scan_t[0] = g_scan_t[2] = ~0ull;
     g_scan_t[1] = g_scan_t[3] = g_scan_t[4] = g_scan_t[5] = 0;
     g_scan_done = 0;
